@@ -1,0 +1,228 @@
+"""Generate golden vectors from the REAL reference (voxsplat) for parity tests.
+
+Run in the container that has the read-only reference mounted:
+
+    PYTHONPATH=/root/reference/pkg/src:/root/reference/pkg/tests \
+        python tests/golden/make_golden.py
+
+Writes small ``*.npz`` fixtures next to this script.  Nothing at test or bench
+time reads /root/reference; the fixtures are the pin.  Every case below calls
+the reference's own public functions (rasterize_forward / backward,
+shade_gaussians / shade_backward, render_composed, inverse._step, vq.kmeans /
+assign_nearest, losses.photometric_loss).
+"""
+
+import os
+import sys
+
+import numpy as np
+
+HERE = os.path.dirname(os.path.abspath(__file__))
+REPO = os.path.dirname(os.path.dirname(HERE))
+sys.path.insert(0, REPO)
+for p in ("/root/reference/pkg/src", "/root/reference/pkg/tests"):
+    if p not in sys.path:
+        sys.path.insert(0, p)
+
+from voxsplat import inverse as ref_inverse  # noqa: E402
+from voxsplat.gaussians import GaussianGeometry, orbit_camera  # noqa: E402
+from voxsplat.losses import photometric_loss  # noqa: E402
+from voxsplat.rasterizer import rasterize_backward, rasterize_forward  # noqa: E402
+from voxsplat.scene import ComposedScene, EditState, apply_edits, render_composed  # noqa: E402
+from voxsplat.shading import LightConfig, Palette, ShadingAttributes, shade_backward, shade_gaussians  # noqa: E402
+from voxsplat.vq import assign_nearest, kmeans  # noqa: E402
+from voxsplat.scene import STAGE_EDITABLE, BasicSceneModel  # noqa: E402
+from oracles import random_editable_model  # noqa: E402
+
+from paper_2504_17954_b200.synthetic import editable_arrays, GEOM_KEYS, SHADE_KEYS  # noqa: E402
+
+
+def model_from(a):
+    geom = GaussianGeometry(*(a[k] for k in GEOM_KEYS))
+    attrs = ShadingAttributes(*(a[k] for k in SHADE_KEYS))
+    return BasicSceneModel(STAGE_EDITABLE, geom, shading=attrs, palette=Palette(a["palette"]))
+
+
+def cam_dict(cam, prefix="cam_"):
+    return {prefix + "position": cam.position, prefix + "rotation": cam.rotation,
+            prefix + "fov_y": np.float64(cam.fov_y), prefix + "width": np.int64(cam.width),
+            prefix + "height": np.int64(cam.height), prefix + "focal": np.float64(cam.focal)}
+
+
+def check_generator():
+    """Our seeded generator reproduces the reference fixture bit-for-bit."""
+    for seed, n in ((0, 50), (3, 7)):
+        ref = random_editable_model(np.random.default_rng(seed), n)
+        ours = editable_arrays(seed, n)
+        for k in GEOM_KEYS:
+            assert np.array_equal(getattr(ref.geometry, k), ours[k]), k
+        for k in SHADE_KEYS:
+            assert np.array_equal(getattr(ref.shading, k), ours[k]), k
+        assert np.array_equal(ref.palette.c_p, ours["palette"])
+
+
+def render_case(name, seed, n, W, H, density=None, light=None, azimuth=0.8, dtype=np.float32):
+    a = editable_arrays(seed, n, density=density)
+    m = model_from(a)
+    cam = orbit_camera(np.zeros(3), 3.0, 0.3, azimuth, np.pi / 3, W, H)
+    light = light or LightConfig()
+    scene = ComposedScene.compose([m], light)
+    rgb, _, _ = shade_gaussians(m.geometry, m.shading, m.palette, light, cam)
+    out, st = rasterize_forward(m.geometry, rgb, cam, dtype=dtype)
+    comp = render_composed(scene, cam, dtype=dtype)
+    assert np.array_equal(comp.color, out.color)
+    proj = st["proj"]
+    d = dict(a)
+    d.update(cam_dict(cam))
+    d.update(light_mode=np.array(light.mode), light_polar=np.float64(light.polar),
+             light_azimuth=np.float64(light.azimuth), light_ts=light.term_scales,
+             rgb=rgb, depth=proj["depth"], mean2d=proj["mean2d"], conic=proj["conic"],
+             cov2d=proj["cov2d"], valid=proj["valid"],
+             pair_splat=st["pair_splat"].astype(np.int32),
+             tile_ranges=st["tile_ranges"].astype(np.int32),
+             kmean2d=st["kmean2d"], kconic=st["kconic"], kopacity=st["kopacity"],
+             values=st["values"], color=out.color, alpha=out.alpha,
+             contrib=out.per_pixel_contrib_count,
+             last_pos=st["last_pos"].astype(np.int32), t_final=st["t_final"])
+    np.savez_compressed(os.path.join(HERE, name + ".npz"), **d)
+    print(name, "N", n, "P", st["pair_splat"].size, "img", (H, W))
+
+
+def composed_case():
+    parts = [editable_arrays(s, 1500) for s in (1, 2, 3)]
+    models = [model_from(a) for a in parts]
+    light = LightConfig("orbital", 0.45, 0.9, np.array([1.2, 0.8, 1.0, 1.0]))
+    scene = ComposedScene.compose(models, light)
+    scene.edits[1] = EditState(palette_override=np.array([0.2, 0.6, 0.9]))
+    scene.edits[2] = EditState(opacity_scale=0.5)
+    cam = orbit_camera(np.zeros(3), 3.0, 0.3, 0.8, np.pi / 3, 96, 80)
+    eff = apply_edits(scene)
+    rgb, _, _ = shade_gaussians(eff.geometry, eff.shading, eff.palette_rgb, eff.light, cam)
+    o32 = render_composed(scene, cam, dtype=np.float32)
+    o64 = render_composed(scene, cam, dtype=np.float64)
+    d = {}
+    for i, a in enumerate(parts):
+        for k, v in a.items():
+            d[f"m{i}_{k}"] = v
+    d.update(cam_dict(cam))
+    d.update(eff_o_logit=eff.geometry.o_logit, rgb=rgb, color32=o32.color, alpha32=o32.alpha,
+             contrib32=o32.per_pixel_contrib_count, color64=o64.color, alpha64=o64.alpha,
+             contrib64=o64.per_pixel_contrib_count)
+    np.savez_compressed(os.path.join(HERE, "composed_edit.npz"), **d)
+    print("composed_edit", eff.geometry.mu.shape[0])
+
+
+def backward_case():
+    a = editable_arrays(11, 40, spread=0.5)
+    geom = GaussianGeometry(*(a[k] for k in GEOM_KEYS))
+    rng = np.random.default_rng(5)
+    colors = rng.uniform(0.1, 0.9, (40, 3))
+    attrs = {"ka": rng.uniform(0.1, 0.9, 40)}
+    cam = orbit_camera(np.zeros(3), 2.5, 0.3, 0.8, 0.9, 24, 24)
+    w = {"color": rng.normal(size=(24, 24, 3)), "alpha": rng.normal(size=(24, 24)),
+         "depth": rng.normal(size=(24, 24)) * 0.1, "normal": rng.normal(size=(24, 24, 3)),
+         "ka": rng.normal(size=(24, 24))}
+    out, st = rasterize_forward(geom, colors, cam, channels=("color", "alpha", "depth", "normal"),
+                                attrs=attrs, dtype=np.float64)
+    g = rasterize_backward(st, w)
+    d = dict(a)
+    d.update(cam_dict(cam))
+    d.update(colors=colors, attr_ka=attrs["ka"], **{"w_" + k: v for k, v in w.items()})
+    for k in ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_mean2d"):
+        d[k] = g[k]
+    d["d_attr_ka"] = g["d_attrs"]["ka"]
+    d["color"], d["alpha"], d["depth_map"], d["normal_map"] = out.color, out.alpha, out.depth, out.normal
+    d["attr_map"] = out.attr["ka"]
+    np.savez_compressed(os.path.join(HERE, "backward_small.npz"), **d)
+    print("backward_small")
+
+
+def shade_case():
+    a = editable_arrays(21, 500)
+    geom = GaussianGeometry(*(a[k] for k in GEOM_KEYS))
+    attrs = ShadingAttributes(*(a[k] for k in SHADE_KEYS))
+    cam = orbit_camera(np.zeros(3), 3.0, 0.3, 0.8, np.pi / 3, 64, 64)
+    rng = np.random.default_rng(7)
+    d_rgb = rng.normal(size=(500, 3))
+    pal = rng.uniform(0.1, 0.9, (500, 3))
+    d = dict(a)
+    d.update(cam_dict(cam), d_rgb=d_rgb, palette_ps=pal)
+    lam, b = np.array([1.2, 0.8, 1.1, 0.9]), np.array([0.01, -0.02, 0.03, 0.2])
+    for tag, light, ct, palette in (
+            ("head", LightConfig(), None, Palette(a["palette"])),
+            ("orb", LightConfig("orbital", 0.45, 0.9, np.array([1.2, 0.8, 1.0, 1.1])), (lam, b), pal)):
+        rgb, terms, cache = shade_gaussians(geom, attrs, palette, light, cam, coeff_transform=ct)
+        g = shade_backward(cache, d_rgb)
+        d[tag + "_rgb"] = rgb
+        for k, v in g.items():
+            d[tag + "_" + k] = np.asarray(v)
+    np.savez_compressed(os.path.join(HERE, "shade.npz"), **d)
+    print("shade")
+
+
+def vq_case():
+    rng = np.random.default_rng(3)
+    samples = np.concatenate([rng.normal(size=1500), rng.normal(3.0, 0.2, 500)])
+    cents = kmeans(samples, 16, seed=1)
+    c4096 = np.sort(rng.normal(size=4096) * 2.0)
+    vals = rng.normal(size=50000) * 2.5
+    mids = 0.5 * (c4096[1:] + c4096[:-1])
+    vals[:64] = mids[rng.integers(0, mids.size, 64)]  # exact ties -> lower index
+    vals[64] = np.nan
+    vals[65], vals[66] = -1e300, 1e300
+    idx = assign_nearest(vals, c4096)
+    np.savez_compressed(os.path.join(HERE, "vq.npz"), samples=samples, kmeans16=cents,
+                        centroids=c4096, values=vals, indices=idx.astype(np.int32))
+    print("vq")
+
+
+def loss_case():
+    rng = np.random.default_rng(4)
+    pred = rng.uniform(0, 1, (32, 40, 4))
+    gt = rng.uniform(0, 1, (32, 40, 4))
+    loss, d = photometric_loss(pred, gt)
+    np.savez_compressed(os.path.join(HERE, "loss.npz"), pred=pred, gt=gt, loss=np.float64(loss), d=d)
+    print("loss")
+
+
+def inverse_case():
+    parts = [editable_arrays(s, 60, spread=0.5) for s in (31, 32)]
+    scene = ComposedScene.compose([model_from(a) for a in parts], LightConfig())
+    cam = orbit_camera(np.zeros(3), 2.5, 0.3, 0.8, 0.9, 40, 40)
+    gt = scene.copy()
+    gt.edits[0] = EditState(palette_override=np.array([0.2, 0.6, 0.9]))
+    gt.edits[1] = EditState(opacity_scale=0.5)
+    gp = ref_inverse.init_transform(gt)
+    gp.lam = np.array([1.2, 0.8, 1.0, 1.0])
+    ref = ref_inverse.render_with_transform(gt, gp, cam, dtype=np.float64)
+    p0 = ref_inverse.init_transform(scene)
+    loss, grads = ref_inverse._step(ref_inverse._frozen_parts(scene), scene.light, p0, cam, ref)
+    fitted, losses = ref_inverse.optimize_to_reference(scene, p0, ref, cam, iters=5, lr=0.01)
+    d = {}
+    for i, a in enumerate(parts):
+        for k, v in a.items():
+            d[f"m{i}_{k}"] = v
+    d.update(cam_dict(cam), reference=ref, loss0=np.float64(loss),
+             fit_losses=np.array(losses), fit_c_p=fitted.c_p, fit_opacity_raw=fitted.opacity_raw,
+             fit_lam=fitted.lam, fit_b=fitted.b)
+    for k, v in grads.items():
+        d["g_" + k] = v
+    np.savez_compressed(os.path.join(HERE, "inverse.npz"), **d)
+    print("inverse")
+
+
+if __name__ == "__main__":
+    check_generator()
+    # C1 (bench config 0): 10k density-scaled, 128^2
+    render_case("render_c1", 0, 10_000, 128, 128, density=10_000)
+    # unmodified fixture scales: large overlapping splats, early termination
+    render_case("render_fixture", 1, 2000, 64, 64)
+    # non-multiple-of-16 frame, orbital light with term scales
+    render_case("render_ragged", 2, 3000, 72, 50, density=3000,
+                light=LightConfig("orbital", -0.3, 2.0, np.array([0.9, 1.3, 1.0, 0.7])), azimuth=-2.1)
+    composed_case()
+    backward_case()
+    shade_case()
+    vq_case()
+    loss_case()
+    inverse_case()
