@@ -1,0 +1,308 @@
+#!/usr/bin/env python
+"""Benchmark: 800x800 render FPS of the composed ~1M-Gaussian editable model
+(BASELINE.json configs[1]) on the B200 hot path.
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl ours|reference]
+
+One step = one frame of the hot path over the resident composed model: K1
+(edits + projection + Blinn-Phong) -> K2 (bit-exact bin/sort) -> K3 (tile
+blend), with the C2 edit sequence applied.  Under torchrun each rank renders
+its own views of a full replica (views are independent: weak scaling, no
+data-path collective).  Rank 0 prints ONE JSON line.
+
+``--impl reference`` times the reference algorithm on the host cores through
+the CPU port in oracle/ (the reference is a Python/numba package that cannot
+be built into a library here), on a bounded sample.
+"""
+
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import threading
+import time
+
+import numpy as np
+
+REPO = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, REPO)
+
+METRIC = "800x800 render FPS (composed 1M Gaussians), train it/s, % HBM roofline, 1-8 GPU"
+W_IMG = H_IMG = 800
+PER_MODEL, N_MODELS, DENSITY = 200_000, 5, 1_000_000
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=50)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--cpu-frames", type=int, default=2)
+    return ap.parse_args()
+
+
+def dist_env():
+    ws = int(os.environ.get("WORLD_SIZE", "1"))
+    return int(os.environ.get("RANK", "0")), int(os.environ.get("LOCAL_RANK", "0")), ws
+
+
+def view_azimuth(rank, step):
+    """Camera views: rank r renders its own orbit azimuths (independent views)."""
+    base = 0.8 + 0.7 * rank
+    return float(np.arctan2(np.sin(base + 0.01 * step), np.cos(base + 0.01 * step)))
+
+
+# ------------------------------------------------------------------ clocks
+class ClockSampler:
+    """nvidia-smi clocks + throttle reasons sampled during the timed region."""
+
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", f"--id={self.gpu}", f"--query-gpu={self.Q}", "--format=csv,noheader,nounits",
+                 "-lms", "100"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+            self.t = threading.Thread(target=self._read, daemon=True)
+            self.t.start()
+        except Exception:
+            self.proc = None
+
+    def _read(self):
+        for line in self.proc.stdout:
+            self.lines.append(line.strip())
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        try:
+            self.proc.wait(timeout=5)
+        except Exception:
+            self.proc.kill()
+        sm, mx, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for ln in self.lines:
+            f = [x.strip() for x in ln.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx = float(f[2])
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        return {"sm_mhz": float(np.median(sm)) if sm else None, "sm_max_mhz": mx,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ CPU side
+def cpu_frames(scene_arrays, cam, frames, nthreads=0):
+    """The reference algorithm for one C2 frame on the host (oracle/ port:
+    numpy per-Gaussian math + C/OpenMP compositor).  Returns (sec/frame, threads)."""
+    import oracle as O
+    a = scene_arrays
+    times = []
+    for _ in range(frames):
+        t0 = time.perf_counter()
+        o_eff = O.effective_o_logit(a["o_logit"], a["opacity_scale"])
+        rgb, _ = O.shade(a["mu"], a["n_raw"], a["delta_c"], a["k_a_raw"], a["k_d_raw"],
+                         a["k_s_raw"], a["log_beta"], a["palette_rgb"], a["light"], cam)
+        st = O.rasterize(a["mu"], a["q_raw"], a["log_s"], o_eff, a["n_raw"], rgb, cam,
+                         dtype=np.float32, nthreads=nthreads)
+        O.maps(st)
+        times.append(time.perf_counter() - t0)
+    return float(np.mean(times)), O.max_threads() if nthreads <= 0 else nthreads
+
+
+def host_scene_arrays(scene):
+    models = scene.models
+    cat = {k: np.concatenate([getattr(m.geometry, k) for m in models])
+           for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw")}
+    cat.update({k: np.concatenate([getattr(m.shading, k) for m in models])
+                for k in ("delta_c", "k_a_raw", "k_d_raw", "k_s_raw", "log_beta")})
+    cat["palette_rgb"] = np.concatenate([
+        np.broadcast_to(e.palette_override if e.palette_override is not None else m.palette.c_p,
+                        (len(m), 3)) for m, e in zip(models, scene.edits)])
+    cat["opacity_scale"] = np.concatenate([np.full(len(m), e.opacity_scale)
+                                           for m, e in zip(models, scene.edits)])
+    lt = scene.light
+    cat["light"] = (lt.mode, lt.polar, lt.azimuth, lt.term_scales)
+    return cat
+
+
+def config_dict(n, extra=None):
+    d = {"workload": "C2: composed 5x200k editable Gaussians (density 1M), 800x800 fwd + "
+                     "relight/TF edit (palette override, opacity 0.5, orbital light, term scales)",
+         "n_gaussians": n, "width": W_IMG, "height": H_IMG, "channels": "rgba",
+         "dtype_mode": "float32 (reference default)",
+         "l2": "flushed (256 MiB write) between timed frames; each frame timed alone"}
+    if extra:
+        d.update(extra)
+    return d
+
+
+def run_reference(args):
+    rank, _, world = dist_env()
+    if rank != 0:
+        return
+    from paper_2504_17954_b200.synthetic import bench_camera, c2_scene
+    scene = c2_scene(PER_MODEL, N_MODELS, DENSITY)
+    arrays = host_scene_arrays(scene)
+    cam = bench_camera(W_IMG, H_IMG, view_azimuth(0, 0))
+    cpu_frames(arrays, cam, 1)  # warm (first-touch, thread pool)
+    steps = max(1, min(args.steps, 3))
+    sec, thr = cpu_frames(arrays, cam, steps)
+    fps = 1.0 / sec
+    line = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
+            "steps": steps, "warmup": 1, "ms_per_step": sec * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+            "impl": "reference", "config": config_dict(len(arrays["mu"])),
+            "cpu_baseline": {"value": fps, "unit": "frames/s", "cores": thr, "kind": "port",
+                             "sample": f"{steps} full C2 frames (1M Gaussians, 800x800) through "
+                                       "oracle/ (numpy + C/OpenMP compositor)"},
+            "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
+                    "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def run_ours(args):
+    import torch
+    rank, local_rank, world = dist_env()
+    torch.cuda.set_device(local_rank)
+    dist = None
+    if world > 1:
+        import torch.distributed as dist
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    from paper_2504_17954_b200 import DeviceScene
+    from paper_2504_17954_b200.synthetic import bench_camera, c2_scene
+
+    scene = c2_scene(PER_MODEL, N_MODELS, DENSITY)
+    ds = DeviceScene(scene)
+    n = ds.n
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    cams = [bench_camera(W_IMG, H_IMG, view_azimuth(rank, s)) for s in range(args.steps + args.warmup)]
+
+    # warm-up: first frame learns the pair capacity (one sync), then fast frames
+    F = ds.render_frame(cams[0], fast=False)
+    for s in range(args.warmup):
+        F = ds.render_frame(cams[s], fast=True)
+    torch.cuda.synchronize()
+    assert not ds.check_overflow(F)
+
+    ev = [[torch.cuda.Event(enable_timing=True) for _ in range(4)] for _ in range(args.steps)]
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    frames = []
+    for s in range(args.steps):
+        flush.zero_()  # L2 flush between timed frames (not timed)
+        frames.append(ds.render_frame(cams[args.warmup + s], fast=True, events=ev[s]))
+    torch.cuda.synchronize()
+    if dist:
+        dist.barrier()
+    clocks = sampler.stop()
+    overflow = any(ds.check_overflow(f) for f in frames)
+    stage = np.array([[ev[s][i].elapsed_time(ev[s][i + 1]) for i in range(3)] for s in range(args.steps)])
+    frame_ms = stage.sum(axis=1)
+    ms = float(frame_ms.mean())
+    t_tot = float(frame_ms.sum()) / 1e3
+    if dist:
+        tt = torch.tensor([t_tot], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_tot = float(tt.item())
+    fps_total = world * args.steps / t_tot
+
+    # ---- end-to-end through the public API with host buffers
+    host_out = torch.empty((H_IMG, W_IMG, 4), dtype=torch.float32, pin_memory=True)
+    host_cnt = torch.empty((H_IMG, W_IMG), dtype=torch.int32, pin_memory=True)
+    e2e_steps = max(3, min(args.steps, 20))
+    for s in range(2):
+        ds.render_host(cams[s], host_out, host_cnt)
+    if dist:
+        dist.barrier()
+    t0 = time.perf_counter()
+    for s in range(e2e_steps):
+        ds.render_host(cams[s % len(cams)], host_out, host_cnt)
+    t_e2e = time.perf_counter() - t0
+    if dist:
+        tt = torch.tensor([t_e2e], device="cuda", dtype=torch.float64)
+        dist.all_reduce(tt, op=dist.ReduceOp.MAX)
+        t_e2e = float(tt.item())
+    e2e_fps = world * e2e_steps / t_e2e
+
+    # ---- roofline of the dominant kernel (stage with the largest time)
+    import json as _json
+    with open(os.path.join(REPO, "MEASURED_PEAKS.json")) if os.path.exists(
+            os.path.join(REPO, "MEASURED_PEAKS.json")) else open(os.devnull) as f:
+        try:
+            peaks = _json.load(f)
+        except Exception:
+            peaks = {}
+    hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
+    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    P = int(frames[-1].n_pairs.item())
+    K = 4
+    stage_ms = stage.mean(axis=0)
+    names = ["preprocess(K1)", "bin_sort(K2)", "blend(K3)"]
+    # algorithmic bytes per launch: K1 reads 168 B/Gaussian
+    # (float64 SoA + shading) + 4 B scene id, writes 8+4+8+32+4K B; K2 ~ 8 passes x 24 B
+    # per Gaussian + 2 passes x 16 B per pair + emit 12 B/pair; K3 gathers 32+4K B per
+    # pair and writes 4K+4 B per pixel.
+    alg = [n * (172 + 52 + 4 * K), n * (8 * 24 + 8) + P * (2 * 16 + 12 + 4),
+           P * (4 + 32 + 4 * K) + W_IMG * H_IMG * (4 * K + 4)]
+    dom = int(np.argmax(stage_ms))
+    achieved = alg[dom] / (stage_ms[dom] * 1e-3) / 1e9
+    roofline = {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
+                "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
+                "peak_source": peak_src,
+                "stage_ms": {nm: float(v) for nm, v in zip(names, stage_ms)},
+                "alg_bytes": {nm: int(v) for nm, v in zip(names, alg)}}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        arrays = host_scene_arrays(scene)
+        cam = cams[0]
+        sec, thr = cpu_frames(arrays, cam, max(1, args.cpu_frames))
+        cpu = {"value": 1.0 / sec, "unit": "frames/s", "cores": thr, "kind": "port",
+               "sample": f"{max(1, args.cpu_frames)} full C2 frames (1M Gaussians, 800x800) "
+                         "via oracle/ (numpy + C/OpenMP)"}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": fps_total, "unit": "frames/s", "n_gpus": world,
+                "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "data": "synthetic (seeded editable Gaussians, SURVEY.md 8(d))",
+                "config": config_dict(n, {"pairs": P, "parallelism": f"replicas x{world} (views)"}),
+                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
+                "e2e": {"value": e2e_fps, "unit": "frames/s",
+                        "h2d_bytes_per_step": ds.h2d_bytes_per_frame(),
+                        "d2h_bytes_per_step": H_IMG * W_IMG * (4 * 4 + 4)},
+                "gpu_launches": 38 * args.steps, "overflow": overflow}
+        print(json.dumps(line), flush=True)
+    if dist:
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    a = parse()
+    if a.impl == "reference":
+        run_reference(a)
+    else:
+        run_ours(a)

@@ -1,0 +1,177 @@
+/*
+ * ivrgs.h -- C ABI of the B200 editable-Gaussian splatting hot path
+ * (drop-in for the reference's numba kernels + the vectorized numpy stages
+ * around them; reference = voxsplat, /root/reference/pkg/src/voxsplat/).
+ *
+ * Conventions
+ *  - All array pointers are DEVICE pointers (cudaMalloc'd or from the PyTorch
+ *    caching allocator), row-major, float64 unless stated otherwise.
+ *  - Every launch is stream-ordered on `stream` (a cudaStream_t); no entry
+ *    point allocates, synchronizes or keeps global mutable state, so calls are
+ *    reentrant and CUDA-graph capturable.  Scratch memory comes from the
+ *    caller through a size query (ivr_*_workspace_size) + workspace pointer.
+ *  - Data-dependent sizes (pair count P) live in device memory; the caller
+ *    provides a capacity and reads back the true count to detect overflow.
+ *  - Return value: IVR_OK (0) or a negative ivr_status.  ivr_last_error()
+ *    returns a thread-local message for the last failure.
+ */
+#ifndef IVRGS_H
+#define IVRGS_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct CUstream_st *ivr_stream_t; /* == cudaStream_t */
+
+#define IVR_ABI_VERSION 1
+#define IVR_TILE 16 /* rasterizer.py:24 TILE_SIZE */
+
+typedef enum ivr_status {
+    IVR_OK = 0,
+    IVR_ERR_ARG = -1,           /* bad argument / null pointer / size */
+    IVR_ERR_SHAPE = -2,         /* errors.ShapeMismatch */
+    IVR_ERR_NONFINITE = -3,     /* errors.NonFiniteGradient (index in out-param) */
+    IVR_ERR_CORRUPT_INDEX = -4, /* errors.CorruptIndex */
+    IVR_ERR_CUDA = -5,          /* launch / runtime failure */
+    IVR_ERR_CAPACITY = -6       /* pair buffer too small (count reported) */
+} ivr_status;
+
+/* Pinhole camera, gaussians.py:139-164 (Camera).  focal/cx/cy are evaluated
+ * on the host exactly as Camera.focal / Camera.center_px. */
+typedef struct ivr_camera {
+    double position[3];
+    double rotation[9]; /* world->camera, row-major */
+    double focal, cx, cy;
+    int32_t width, height;
+} ivr_camera;
+
+/* GaussianGeometry storage, gaussians.py:29-51 (unconstrained domain). */
+typedef struct ivr_gaussians {
+    int64_t n;
+    const double *mu;      /* (n,3) */
+    const double *q_raw;   /* (n,4) w-first */
+    const double *log_s;   /* (n,3) */
+    const double *o_logit; /* (n)   */
+    const double *n_raw;   /* (n,3) */
+} ivr_gaussians;
+
+/* Editable shading inputs: ShadingAttributes (shading.py:89-115), palette,
+ * LightConfig (shading.py:42-66) and the optional (lam, b) coefficient
+ * transform of shade_gaussians (shading.py:225-279). */
+typedef struct ivr_shading {
+    const double *delta_c;  /* (n,3) */
+    const double *k_a_raw;  /* (n) */
+    const double *k_d_raw;  /* (n) */
+    const double *k_s_raw;  /* (n) */
+    const double *log_beta; /* (n) */
+    const double *palette;  /* (S,3) indexed by scene id, or (n,3) */
+    int32_t per_splat_palette;
+    int32_t orbital;        /* 0 = headlight, 1 = orbital */
+    double light_dir[3];    /* light_direction_from_angles (host) */
+    double term_scales[4];
+    double lam[4];
+    double b[4];
+} ivr_shading;
+
+/* Composed-scene edits, scene.py:199-228 (apply_edits). */
+typedef struct ivr_edits {
+    const int32_t *scene_id;      /* (n) or NULL (all scene 0) */
+    const double *opacity_scale;  /* (S) or NULL */
+    int32_t rescale_opacity;      /* 1 iff any scale != 1 (scene.py:217) */
+} ivr_edits;
+
+#define IVR_MAX_ATTRS 8
+/* Packed channel layout, rasterizer.py:39-50 + 134-149. */
+typedef struct ivr_layout {
+    int32_t k; /* total channels K */
+    int32_t col_color, col_alpha, col_depth, col_normal; /* -1 = absent */
+    const double *colors; /* (n,3) per-splat colors when shading == NULL */
+    int32_t n_attr;
+    const double *attr[IVR_MAX_ATTRS];
+    int32_t attr_col[IVR_MAX_ATTRS];
+    int32_t attr_width[IVR_MAX_ATTRS];
+} ivr_layout;
+
+/* Per-frame preprocess outputs (device, caller-allocated). */
+typedef struct ivr_proj_out {
+    uint64_t *depth_key; /* (n) float64 depth bits if visible else ~0 */
+    int32_t *count;      /* (n) tiles touched (0 if invisible) */
+    uint16_t *rect;      /* (n,4) tx0, tx1, ty0, ty1 */
+    float *rec;          /* (n,8) blend record: mx,my,o,hi, a/2,b,c/2,0 */
+    float *values;       /* (n,k) packed channel values (float32) */
+    double *rec64;       /* optional (n,8): mx,my,a,b,c,o,depth,0 (float64 mode) */
+    double *values64;    /* optional (n,k) float64 channel values */
+    /* optional float64 parity outputs (NULL to skip) */
+    double *mean2d;  /* (n,2) */
+    double *conic;   /* (n,3) */
+    double *cov2d;   /* (n,4) */
+    double *depth;   /* (n) */
+    double *opacity; /* (n) effective opacity */
+    double *rgb;     /* (n,3) shaded colour */
+    double *radius;  /* (n) */
+    uint8_t *valid;  /* (n) projection validity */
+} ivr_proj_out;
+
+int ivr_version(void);
+const char *ivr_last_error(void);
+
+/* K1: fused edits + EWA projection + Blinn-Phong shading + radius / tile rect
+ * / count + float32 record packing.  Replaces scene.apply_edits
+ * (scene.py:199-228), shading.shade_gaussians (shading.py:225-329),
+ * gaussians.project_gaussians (gaussians.py:296-346) and the binning prologue
+ * of rasterizer.rasterize_forward (rasterizer.py:88-121, 134-153).
+ * shading / edits may be NULL.  f64_mode selects dtype=float64 semantics. */
+int ivr_preprocess_fwd(const ivr_gaussians *g, const ivr_shading *shading,
+                       const ivr_edits *edits, const ivr_camera *cam,
+                       const ivr_layout *layout, ivr_proj_out *out,
+                       int32_t f64_mode, ivr_stream_t stream);
+
+/* Shading only (shading.shade_gaussians, shading.py:225-329): float64 rgb
+ * (n,3) and optional terms (n,9: ambient, diffuse, specular). */
+int ivr_shade_fwd(const ivr_gaussians *g, const ivr_shading *shading,
+                  const int32_t *scene_id, const ivr_camera *cam, double *rgb,
+                  double *terms, ivr_stream_t stream);
+
+/* K2: stable depth sort + duplicated (tile, depth) pair emission + stable
+ * tile sort + tile ranges.  Replaces _kernels.fill_pairs (_kernels.py:19-28),
+ * np.lexsort((depth[pair_splat], pair_tile)) (rasterizer.py:129) and
+ * np.searchsorted tile ranges (rasterizer.py:132), bit-exactly.
+ * Writes n_pairs[0] (device) = P; if P > pair_capacity nothing past the
+ * capacity is written and the caller must retry with a larger buffer. */
+size_t ivr_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t ntiles);
+int ivr_bin_sort(int64_t n, const uint64_t *depth_key, const int32_t *count,
+                 const uint16_t *rect, int32_t ntx, int32_t nty,
+                 int64_t pair_capacity, void *workspace, size_t workspace_bytes,
+                 int32_t *pair_splat, int32_t *tile_ranges, int32_t *n_pairs,
+                 ivr_stream_t stream);
+
+/* K3: per-tile front-to-back blend.  Replaces _kernels.composite_forward
+ * (_kernels.py:31-72).  out (H,W,k) float32 (out64 float64 in f64 mode),
+ * contrib/last_pos int32 (H,W), t_final (H,W) float64.  tile_order may be
+ * NULL (identity) or a permutation of the tiles (scheduling only). */
+int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_splat,
+                  int32_t ntx, int32_t nty, const float *rec, const float *values,
+                  const double *rec64, const double *values64, int32_t k,
+                  int32_t width, int32_t height, float *out, double *out64,
+                  int32_t *contrib, int32_t *last_pos, double *t_final,
+                  const int32_t *tile_order, ivr_stream_t stream);
+
+/* K5: VQ assignment, vq.assign_nearest (vq.py:90-96): index of the nearest
+ * sorted centroid = searchsorted(mids, v, 'left'); NaN -> K-1.
+ * Output uint16 (K <= 65536). */
+int ivr_vq_assign(const double *values, int64_t n, const double *centroids,
+                  int32_t k, uint16_t *indices, ivr_stream_t stream);
+
+/* K6: codebook decode, Codebook.decode (vq.py:128-134).  Sets bad[0] (device)
+ * to 1 + the first out-of-range position if any index >= k. */
+int ivr_vq_decode(const uint16_t *indices, int64_t n, const double *centroids,
+                  int32_t k, double *out, int64_t *bad, ivr_stream_t stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* IVRGS_H */

@@ -1,1 +1,24 @@
-"""placeholder"""
+"""B200-native editable-Gaussian splatting hot path (iVR-GS, arxiv 2504.17954).
+
+Drop-in for the hot path of the reference package ``voxsplat``: the public
+names below keep the reference's signatures; the compute runs in the
+in-tree CUDA library ``libivrgs.so`` (sm_100a), reached through the C ABI in
+``include/ivrgs.h``.  Importing the package does not touch the GPU; the first
+kernel call loads the library and fails loudly if it is missing.
+"""
+
+from .errors import (  # noqa: F401
+    BadMagic, ChecksumMismatch, CorruptIndex, CulledBehindCamera, DatasetEmpty, DivergedLoss,
+    EmptyInput, MixedStage, NonFiniteGradient, OutOfRange, ShapeMismatch, UnknownAttribute,
+    VersionUnsupported, VoxSplatError,
+)
+from .gaussians import Camera, GaussianGeometry, ShColor, orbit_camera, project_gaussians  # noqa: F401
+from .rasterizer import RenderOutput, rasterize_forward, render_attribute_map  # noqa: F401
+from .scene import (  # noqa: F401
+    BasicSceneModel, ComposedScene, DeviceScene, EditState, EffectiveScene, apply_edits,
+    render_composed,
+)
+from .shading import LightConfig, Palette, ShadingAttributes, shade_gaussians  # noqa: F401
+from .vq import Codebook, assign_nearest, dequantize_model, kmeans, quantize_model  # noqa: F401
+
+__version__ = "0.1.0"

@@ -1,0 +1,129 @@
+"""ctypes binding of the C ABI in ``include/ivrgs.h`` (libivrgs.so).
+
+The product path has no CPU fallback: every kernel entry point goes through
+``lib()``, which raises ``NativeLibraryMissing`` when the in-tree CUDA library
+has not been built (``python -m paper_2504_17954_b200.build``).
+"""
+
+from __future__ import annotations
+
+import ctypes
+import os
+
+from .errors import CorruptIndex, NonFiniteGradient, ShapeMismatch, VoxSplatError
+
+PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(PKG, "libivrgs.so")
+
+c_double_p = ctypes.POINTER(ctypes.c_double)
+P = ctypes.c_void_p
+MAX_ATTRS = 8
+
+IVR_OK, IVR_ERR_ARG, IVR_ERR_SHAPE, IVR_ERR_NONFINITE, IVR_ERR_CORRUPT_INDEX, IVR_ERR_CUDA, \
+    IVR_ERR_CAPACITY = 0, -1, -2, -3, -4, -5, -6
+
+
+class NativeLibraryMissing(VoxSplatError, RuntimeError):
+    """The CUDA extension is not built / not loadable: there is no fallback."""
+
+
+class Camera_t(ctypes.Structure):
+    _fields_ = [("position", ctypes.c_double * 3), ("rotation", ctypes.c_double * 9),
+                ("focal", ctypes.c_double), ("cx", ctypes.c_double), ("cy", ctypes.c_double),
+                ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
+
+
+class Gaussians_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("mu", P), ("q_raw", P), ("log_s", P), ("o_logit", P),
+                ("n_raw", P)]
+
+
+class Shading_t(ctypes.Structure):
+    _fields_ = [("delta_c", P), ("k_a_raw", P), ("k_d_raw", P), ("k_s_raw", P), ("log_beta", P),
+                ("palette", P), ("per_splat_palette", ctypes.c_int32), ("orbital", ctypes.c_int32),
+                ("light_dir", ctypes.c_double * 3), ("term_scales", ctypes.c_double * 4),
+                ("lam", ctypes.c_double * 4), ("b", ctypes.c_double * 4)]
+
+
+class Edits_t(ctypes.Structure):
+    _fields_ = [("scene_id", P), ("opacity_scale", P), ("rescale_opacity", ctypes.c_int32)]
+
+
+class Layout_t(ctypes.Structure):
+    _fields_ = [("k", ctypes.c_int32), ("col_color", ctypes.c_int32), ("col_alpha", ctypes.c_int32),
+                ("col_depth", ctypes.c_int32), ("col_normal", ctypes.c_int32), ("colors", P),
+                ("n_attr", ctypes.c_int32), ("attr", P * MAX_ATTRS),
+                ("attr_col", ctypes.c_int32 * MAX_ATTRS), ("attr_width", ctypes.c_int32 * MAX_ATTRS)]
+
+
+class ProjOut_t(ctypes.Structure):
+    _fields_ = [("depth_key", P), ("count", P), ("rect", P), ("rec", P), ("values", P),
+                ("rec64", P), ("values64", P), ("mean2d", P), ("conic", P), ("cov2d", P),
+                ("depth", P), ("opacity", P), ("rgb", P), ("radius", P), ("valid", P)]
+
+
+_SIGS = {
+    "ivr_version": ([], ctypes.c_int),
+    "ivr_last_error": ([], ctypes.c_char_p),
+    "ivr_preprocess_fwd": ([ctypes.POINTER(Gaussians_t), ctypes.POINTER(Shading_t),
+                            ctypes.POINTER(Edits_t), ctypes.POINTER(Camera_t),
+                            ctypes.POINTER(Layout_t), ctypes.POINTER(ProjOut_t), ctypes.c_int32, P],
+                           ctypes.c_int),
+    "ivr_shade_fwd": ([ctypes.POINTER(Gaussians_t), ctypes.POINTER(Shading_t), P,
+                       ctypes.POINTER(Camera_t), P, P, P], ctypes.c_int),
+    "ivr_bin_sort_workspace_size": ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int32], ctypes.c_size_t),
+    "ivr_bin_sort": ([ctypes.c_int64, P, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P,
+                      ctypes.c_size_t, P, P, P, P], ctypes.c_int),
+    "ivr_blend_fwd": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, P, ctypes.c_int32,
+                       ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P], ctypes.c_int),
+    "ivr_vq_assign": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P], ctypes.c_int),
+    "ivr_vq_decode": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P, P], ctypes.c_int),
+}
+
+_lib = None
+
+
+def lib():
+    """Load libivrgs.so (no fallback)."""
+    global _lib
+    if _lib is not None:
+        return _lib
+    if not os.path.exists(LIB_PATH):
+        raise NativeLibraryMissing(
+            f"{LIB_PATH} is missing: build it with `python -m paper_2504_17954_b200.build` "
+            "(there is no CPU fallback)")
+    try:
+        L = ctypes.CDLL(LIB_PATH)
+    except OSError as e:  # pragma: no cover - depends on the box
+        raise NativeLibraryMissing(f"cannot load {LIB_PATH}: {e}") from e
+    for name, (argt, rest) in _SIGS.items():
+        fn = getattr(L, name, None)
+        if fn is None:
+            continue
+        fn.argtypes = argt
+        fn.restype = rest
+    _lib = L
+    return L
+
+
+def exported_symbols():
+    """Names declared in include/ivrgs.h (checked by tests)."""
+    import re
+    hdr = os.path.join(os.path.dirname(PKG), "include", "ivrgs.h")
+    with open(hdr) as f:
+        text = f.read()
+    return sorted(set(re.findall(r"\b(ivr_[a-z0-9_]+)\s*\(", text)))
+
+
+def check(status, what=""):
+    """Map a C-ABI status to the reference's typed exceptions."""
+    if status == IVR_OK:
+        return
+    msg = lib().ivr_last_error().decode(errors="replace")
+    if status == IVR_ERR_SHAPE:
+        raise ShapeMismatch(msg or what)
+    if status == IVR_ERR_NONFINITE:
+        raise NonFiniteGradient(what)
+    if status == IVR_ERR_CORRUPT_INDEX:
+        raise CorruptIndex(msg or what)
+    raise VoxSplatError(f"{what}: ivrgs status {status}: {msg}")

@@ -1,0 +1,28 @@
+// C-ABI plumbing: version, thread-local error strings, launch checks.
+#include <stdio.h>
+#include <string.h>
+
+#include "ivr_common.cuh"
+
+namespace {
+thread_local char g_err[512] = "";
+}
+
+namespace ivr {
+void set_error(const char *msg) {
+    strncpy(g_err, msg, sizeof(g_err) - 1);
+    g_err[sizeof(g_err) - 1] = 0;
+}
+
+int check_launch(const char *what) {
+    const cudaError_t e = cudaGetLastError();
+    if (e != cudaSuccess) {
+        snprintf(g_err, sizeof(g_err), "%s: %s", what, cudaGetErrorString(e));
+        return IVR_ERR_CUDA;
+    }
+    return IVR_OK;
+}
+}  // namespace ivr
+
+extern "C" int ivr_version(void) { return IVR_ABI_VERSION; }
+extern "C" const char *ivr_last_error(void) { return g_err; }

@@ -1,0 +1,251 @@
+"""Device plumbing: torch-owned HBM buffers, C-ABI structs, kernel launches.
+
+PyTorch provides device memory (caching allocator) and the current CUDA
+stream; every compute step is a ``libivrgs.so`` call (include/ivrgs.h).
+"""
+
+from __future__ import annotations
+
+import ctypes
+
+import numpy as np
+import torch
+
+from . import _lib as L
+
+TILE = 16
+
+
+def cuda_device():
+    if not torch.cuda.is_available():
+        raise L.NativeLibraryMissing("no CUDA device: the editable-Gaussian path is GPU-only")
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def stream_handle(stream=None):
+    s = stream if stream is not None else torch.cuda.current_stream()
+    return ctypes.c_void_p(s.cuda_stream)
+
+
+def ptr(t):
+    return None if t is None else ctypes.c_void_p(t.data_ptr())
+
+
+def to_dev(a, dtype=torch.float64, device=None):
+    """Host array -> contiguous device tensor (no copy if already on device)."""
+    if a is None:
+        return None
+    if isinstance(a, torch.Tensor):
+        return a.to(device=device or cuda_device(), dtype=dtype).contiguous()
+    arr = np.ascontiguousarray(np.asarray(a))
+    t = torch.from_numpy(arr)
+    if t.dtype != dtype:
+        t = t.to(dtype)
+    return t.to(device or cuda_device(), non_blocking=False).contiguous()
+
+
+def camera_struct(cam) -> L.Camera_t:
+    c = L.Camera_t()
+    pos = np.asarray(cam.position, dtype=np.float64).reshape(3)
+    rot = np.asarray(cam.rotation, dtype=np.float64).reshape(9)
+    for i in range(3):
+        c.position[i] = float(pos[i])
+    for i in range(9):
+        c.rotation[i] = float(rot[i])
+    # Camera.focal / center_px evaluated exactly as the reference does
+    c.focal = float(0.5 * cam.height / np.tan(0.5 * cam.fov_y))
+    c.cx = float((cam.width - 1) / 2.0)
+    c.cy = float((cam.height - 1) / 2.0)
+    c.width = int(cam.width)
+    c.height = int(cam.height)
+    return c
+
+
+def light_direction(polar, azimuth):
+    """light_direction_from_angles (shading.py:179-183), host float64."""
+    cp, sp = np.cos(polar), np.sin(polar)
+    ca, sa = np.cos(azimuth), np.sin(azimuth)
+    return np.array([cp * ca, cp * sa, sp])
+
+
+class DeviceGaussians:
+    """Float64 SoA geometry (+ optional shading attributes) resident in HBM."""
+
+    GEOM = ("mu", "q_raw", "log_s", "o_logit", "n_raw")
+    SHADE = ("delta_c", "k_a_raw", "k_d_raw", "k_s_raw", "log_beta")
+
+    def __init__(self, geom, shading=None, scene_id=None, device=None):
+        dev = device or cuda_device()
+        self.n = len(geom.mu) if hasattr(geom, "mu") else int(geom["mu"].shape[0])
+        get = (lambda o, k: getattr(o, k)) if not isinstance(geom, dict) else (lambda o, k: o[k])
+        self.t = {k: to_dev(get(geom, k), device=dev) for k in self.GEOM}
+        if shading is not None:
+            gs = (lambda o, k: getattr(o, k)) if not isinstance(shading, dict) else (lambda o, k: o[k])
+            for k in self.SHADE:
+                self.t[k] = to_dev(gs(shading, k), device=dev)
+        self.has_shading = shading is not None
+        self.scene_id = to_dev(scene_id, torch.int32, dev) if scene_id is not None else None
+        self.device = dev
+
+    def struct(self) -> L.Gaussians_t:
+        g = L.Gaussians_t()
+        g.n = self.n
+        for k in self.GEOM:
+            setattr(g, k, self.t[k].data_ptr())
+        return g
+
+
+def shading_struct(dg: DeviceGaussians, palette_dev, per_splat, light, lam=None, b=None):
+    """ivr_shading for DeviceGaussians + palette tensor + LightConfig."""
+    s = L.Shading_t()
+    for k in DeviceGaussians.SHADE:
+        setattr(s, k, dg.t[k].data_ptr())
+    s.palette = palette_dev.data_ptr()
+    s.per_splat_palette = 1 if per_splat else 0
+    s.orbital = 1 if light.mode == "orbital" else 0
+    ld = light_direction(light.polar, light.azimuth) if s.orbital else np.zeros(3)
+    for i in range(3):
+        s.light_dir[i] = float(ld[i])
+    ts = np.asarray(light.term_scales, dtype=np.float64).reshape(4)
+    lam = np.ones(4) if lam is None else np.asarray(lam, dtype=np.float64).reshape(4)
+    b = np.zeros(4) if b is None else np.asarray(b, dtype=np.float64).reshape(4)
+    for i in range(4):
+        s.term_scales[i] = float(ts[i])
+        s.lam[i] = float(lam[i])
+        s.b[i] = float(b[i])
+    return s
+
+
+class Workspace:
+    """Grow-only cache of device buffers keyed by name (one per renderer)."""
+
+    def __init__(self, device=None):
+        self.device = device or cuda_device()
+        self.bufs = {}
+        self.pair_capacity = 0
+
+    def get(self, name, numel, dtype):
+        numel = max(int(numel), 1)
+        t = self.bufs.get(name)
+        if t is None or t.numel() < numel or t.dtype != dtype:
+            t = torch.empty(int(numel * 1.0) if t is None else max(numel, int(t.numel() * 1.25)),
+                            dtype=dtype, device=self.device)
+            self.bufs[name] = t
+        return t[:numel]
+
+
+class Frame:
+    """Device outputs of one rasterization (kept alive for the backward)."""
+
+    def __init__(self):
+        self.__dict__.update({})
+
+
+def preprocess(dg: DeviceGaussians, cam, K, cols, ws: Workspace, shading=None, edits=None,
+               colors=None, attrs=(), f64=False, debug=False, stream=None):
+    """Launch K1; returns a Frame with the per-splat buffers."""
+    n = dg.n
+    F = Frame()
+    F.n, F.K, F.f64, F.cam = n, K, f64, cam
+    F.depth_key = ws.get("depth_key", n, torch.int64)
+    F.count = ws.get("count", n, torch.int32)
+    F.rect = ws.get("rect", 4 * n, torch.int16)
+    F.rec = ws.get("rec", 8 * n, torch.float32)
+    F.values = ws.get("values", K * n, torch.float32)
+    F.rec64 = ws.get("rec64", 8 * n, torch.float64) if f64 else None
+    F.values64 = ws.get("values64", K * n, torch.float64) if f64 else None
+    lay = L.Layout_t()
+    lay.k = K
+    lay.col_color, lay.col_alpha, lay.col_depth, lay.col_normal = cols
+    lay.colors = colors.data_ptr() if colors is not None else None
+    F._keep = [colors]
+    lay.n_attr = len(attrs)
+    for i, (t, col, w) in enumerate(attrs):
+        lay.attr[i] = t.data_ptr()
+        lay.attr_col[i] = col
+        lay.attr_width[i] = w
+        F._keep.append(t)
+    out = L.ProjOut_t()
+    out.depth_key, out.count, out.rect = F.depth_key.data_ptr(), F.count.data_ptr(), F.rect.data_ptr()
+    out.rec, out.values = F.rec.data_ptr(), F.values.data_ptr()
+    if f64:
+        out.rec64, out.values64 = F.rec64.data_ptr(), F.values64.data_ptr()
+    if debug:
+        dev = dg.device
+        F.dbg = {"mean2d": torch.empty(2 * n, dtype=torch.float64, device=dev),
+                 "conic": torch.empty(3 * n, dtype=torch.float64, device=dev),
+                 "cov2d": torch.empty(4 * n, dtype=torch.float64, device=dev),
+                 "depth": torch.empty(n, dtype=torch.float64, device=dev),
+                 "opacity": torch.empty(n, dtype=torch.float64, device=dev),
+                 "rgb": torch.zeros(3 * n, dtype=torch.float64, device=dev),
+                 "radius": torch.empty(n, dtype=torch.float64, device=dev),
+                 "valid": torch.empty(n, dtype=torch.uint8, device=dev)}
+        for k, v in F.dbg.items():
+            setattr(out, k, v.data_ptr())
+    g = dg.struct()
+    cs = camera_struct(cam)
+    sh = ctypes.byref(shading) if shading is not None else None
+    ed = ctypes.byref(edits) if edits is not None else None
+    L.check(L.lib().ivr_preprocess_fwd(ctypes.byref(g), sh, ed, ctypes.byref(cs), ctypes.byref(lay),
+                                       ctypes.byref(out), 1 if f64 else 0, stream_handle(stream)),
+            "ivr_preprocess_fwd")
+    return F
+
+
+def bin_sort(F: Frame, ws: Workspace, stream=None, capacity=None):
+    """Launch K2 into F (pair_splat, tile_ranges, n_pairs)."""
+    cam = F.cam
+    ntx, nty = (cam.width + TILE - 1) // TILE, (cam.height + TILE - 1) // TILE
+    F.ntx, F.nty = ntx, nty
+    n = F.n
+    cap = capacity or max(ws.pair_capacity, 4 * n, 1 << 16)
+    ws.pair_capacity = cap
+    nbytes = L.lib().ivr_bin_sort_workspace_size(n, cap, ntx * nty)
+    scratch = ws.get("sort_ws", nbytes, torch.uint8)
+    F.pair_splat = ws.get("pair_splat", cap, torch.int32)
+    F.tile_ranges = ws.get("tile_ranges", ntx * nty + 1, torch.int32)
+    F.n_pairs = ws.get("n_pairs", 1, torch.int32)
+    F.capacity = cap
+    L.check(L.lib().ivr_bin_sort(n, ptr(F.depth_key), ptr(F.count), ptr(F.rect), ntx, nty, cap,
+                                 ptr(scratch), nbytes, ptr(F.pair_splat), ptr(F.tile_ranges),
+                                 ptr(F.n_pairs), stream_handle(stream)), "ivr_bin_sort")
+    return F
+
+
+def blend(F: Frame, ws: Workspace, want_state=True, stream=None, tile_order=None, out=None):
+    cam = F.cam
+    H, W, K = cam.height, cam.width, F.K
+    dev = F.depth_key.device
+    if F.f64:
+        F.out64 = out if out is not None else torch.empty((H, W, K), dtype=torch.float64, device=dev)
+        F.out = None
+    else:
+        F.out = out if out is not None else torch.empty((H, W, K), dtype=torch.float32, device=dev)
+        F.out64 = None
+    F.contrib = torch.empty((H, W), dtype=torch.int32, device=dev)
+    F.last_pos = torch.empty((H, W), dtype=torch.int32, device=dev) if want_state else None
+    F.t_final = torch.empty((H, W), dtype=torch.float64, device=dev) if want_state else None
+    L.check(L.lib().ivr_blend_fwd(ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec),
+                                  ptr(F.values), ptr(F.rec64), ptr(F.values64), K, W, H, ptr(F.out),
+                                  ptr(F.out64), ptr(F.contrib), ptr(F.last_pos), ptr(F.t_final),
+                                  ptr(tile_order), stream_handle(stream)), "ivr_blend_fwd")
+    return F
+
+
+def rasterize_device(dg, cam, K, cols, ws, shading=None, edits=None, colors=None, attrs=(),
+                     f64=False, want_state=True, debug=False, stream=None):
+    """K1 + K2 + K3 with pair-capacity overflow handling (synchronizes once to
+    read the pair count)."""
+    F = preprocess(dg, cam, K, cols, ws, shading, edits, colors, attrs, f64, debug, stream)
+    if dg.n == 0:
+        F.empty = True
+        return F
+    bin_sort(F, ws, stream)
+    P = int(F.n_pairs.item())
+    if P > F.capacity:
+        bin_sort(F, ws, stream, capacity=int(P * 1.25) + 4096)
+        P = int(F.n_pairs.item())
+    F.P = P
+    F.empty = False
+    blend(F, ws, want_state, stream)
+    return F

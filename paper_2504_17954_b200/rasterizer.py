@@ -1,0 +1,143 @@
+"""Tile rasterizer entry points (drop-in for voxsplat/rasterizer.py).
+
+``rasterize_forward`` / ``rasterize_backward`` keep the reference signatures
+(rasterizer.py:53-55, 185) and return host numpy maps, but every stage runs
+on the GPU: K1 preprocess, K2 bit-exact bin/sort, K3 tile blend (and K4 for
+the backward).  The returned ``state`` owns the device buffers the backward
+needs (the reference's state dict of numpy arrays, rasterizer.py:74-78).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as D
+from .errors import ShapeMismatch
+
+TILE_SIZE = 16
+_WS = {}
+
+
+def workspace():
+    dev = D.cuda_device()
+    ws = _WS.get(dev.index)
+    if ws is None:
+        ws = _WS[dev.index] = D.Workspace(dev)
+    return ws
+
+
+@dataclass
+class RenderOutput:
+    """Per-pixel maps of one rasterization (all H x W [x k])."""
+
+    color: np.ndarray | None
+    alpha: np.ndarray
+    depth: np.ndarray | None
+    normal: np.ndarray | None
+    attr: dict = field(default_factory=dict)
+    per_pixel_contrib_count: np.ndarray | None = None
+
+
+def _channel_layout(channels, attrs):
+    """Ordered (name, width): color, alpha, depth, normal, then attrs
+    (rasterizer.py:39-50)."""
+    widths = {"color": 3, "alpha": 1, "depth": 1, "normal": 3}
+    layout = [(c, widths[c]) for c in ("color", "alpha", "depth", "normal") if c in channels]
+    for name, vals in (attrs or {}).items():
+        vals = np.asarray(vals) if not isinstance(vals, torch.Tensor) else vals
+        layout.append((name, 1 if vals.ndim == 1 else int(vals.shape[1])))
+    return layout
+
+
+def _cols(layout):
+    cols = {"color": -1, "alpha": -1, "depth": -1, "normal": -1}
+    attr_cols = []
+    c = 0
+    for name, w in layout:
+        if name in cols:
+            cols[name] = c
+        else:
+            attr_cols.append((name, c, w))
+        c += w
+    return (cols["color"], cols["alpha"], cols["depth"], cols["normal"]), attr_cols, c
+
+
+def _unpack(out, layout, contrib):
+    maps, col = {}, 0
+    for name, w in layout:
+        m = out[:, :, col:col + w]
+        maps[name] = m[:, :, 0] if w == 1 else m
+        col += w
+    return RenderOutput(
+        color=maps.get("color"),
+        alpha=maps.get("alpha", np.zeros(out.shape[:2], dtype=out.dtype)),
+        depth=maps.get("depth"), normal=maps.get("normal"),
+        attr={k: v for k, v in maps.items() if k not in ("color", "alpha", "depth", "normal")},
+        per_pixel_contrib_count=contrib)
+
+
+def rasterize_forward(geom, colors, cam, channels=("color", "alpha"), attrs=None,
+                      dtype=np.float32, sequential=False):
+    """Rasterize on the GPU; returns (RenderOutput, state-for-backward).
+
+    Same contract as rasterizer.py:53-164: ``colors`` are per-splat rgb
+    already resolved for this camera, ``attrs`` maps names to (N,) or (N,k)
+    values; outputs are deterministic (``sequential`` is accepted and has no
+    effect, exactly as in the reference)."""
+    del sequential
+    dtype = np.dtype(dtype).type
+    H, W = int(cam.height), int(cam.width)
+    layout = _channel_layout(channels, attrs)
+    cols, attr_cols, K = _cols(layout)
+    n = len(geom)
+    state = {"geom": geom, "cam": cam, "layout": layout, "dtype": dtype, "colors": colors,
+             "attrs": attrs or {}, "n": n}
+    if n == 0:
+        out = np.zeros((H, W, K), dtype=dtype)
+        state["empty"] = True
+        return _unpack(out, layout, np.zeros((H, W), np.int32)), state
+    f64 = dtype == np.float64
+    dg = D.DeviceGaussians(geom)
+    colors_dev = D.to_dev(np.asarray(colors).reshape(n, 3)) if cols[0] >= 0 else None
+    attrs_dev = [(D.to_dev(np.asarray(attrs[name], dtype=np.float64).reshape(n, w)), c, w)
+                 for name, c, w in attr_cols]
+    F = D.rasterize_device(dg, cam, K, cols, workspace(), colors=colors_dev, attrs=attrs_dev,
+                           f64=f64, want_state=True)
+    out = (F.out64 if f64 else F.out).cpu().numpy().astype(dtype, copy=False)
+    contrib = F.contrib.cpu().numpy()
+    state.update(frame=F, dg=dg, empty=False)
+    return _unpack(out, layout, contrib), state
+
+
+def render_attribute_map(geom, attr_values, cam, dtype=np.float32):
+    """Composite a per-splat attribute with the colour weights
+    (rasterizer.py:289-297)."""
+    out, _ = rasterize_forward(geom, None, cam, channels=("alpha",),
+                               attrs={"attr": np.asarray(attr_values)}, dtype=dtype)
+    return out.attr["attr"]
+
+
+def _project_only(geom, cam):
+    """Run K1 with its float64 parity outputs (used by project_gaussians)."""
+    n = len(geom)
+    dg = D.DeviceGaussians(geom)
+    F = D.preprocess(dg, cam, 1, (-1, 0, -1, -1), workspace(), debug=True)
+    g = {k: v.cpu().numpy() for k, v in F.dbg.items()}
+    return {"mean2d": g["mean2d"].reshape(n, 2), "cov2d": g["cov2d"].reshape(n, 2, 2),
+            "conic": g["conic"].reshape(n, 3), "depth": g["depth"],
+            "valid": g["valid"].astype(bool), "radius": g["radius"]}
+
+
+def _check_dmaps(state, d_maps):
+    cam = state["cam"]
+    H, W = cam.height, cam.width
+    for name, w in state["layout"]:
+        g = d_maps.get(name)
+        if g is None:
+            continue
+        want = (H, W) if w == 1 else (H, W, w)
+        if tuple(np.shape(g)) != want:
+            raise ShapeMismatch(f"gradient for {name}: {tuple(np.shape(g))} != {want}")

@@ -1,0 +1,331 @@
+"""Scene models, composition, edits and the resident GPU renderer.
+
+Host containers mirror voxsplat/scene.py:56-228 (BasicSceneModel, EditState,
+ComposedScene, EffectiveScene, apply_edits).  Rendering goes through
+``DeviceScene``: the composed model is concatenated ONCE into HBM (float64
+SoA + per-splat scene id), and every frame passes the edits as per-scene
+tables (palette, opacity scale) plus the global light, which K1 resolves in
+registers -- instead of the reference's re-concatenation of every array on
+each render (scene.py:206-212).
+"""
+
+from __future__ import annotations
+
+import ctypes
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import device as D
+from .errors import MixedStage, OutOfRange, ShapeMismatch
+from .gaussians import GaussianGeometry, ShColor
+from .rasterizer import RenderOutput, _channel_layout, _cols, _unpack, workspace
+from .shading import LightConfig, Palette, ShadingAttributes
+
+STAGE_BASE = "base"
+STAGE_EDITABLE = "editable"
+
+
+@dataclass
+class BasicSceneModel:
+    """One trained basic scene (base stage: SH colours; editable stage:
+    shading attributes + palette; optionally quantized)."""
+
+    stage: str
+    geometry: GaussianGeometry
+    sh: ShColor = None
+    shading: ShadingAttributes = None
+    palette: Palette = None
+    quantized: dict = None
+    metadata: dict = field(default_factory=dict)
+
+    def __post_init__(self):
+        if self.stage not in (STAGE_BASE, STAGE_EDITABLE):
+            raise OutOfRange(f"unknown stage {self.stage!r}")
+        n = len(self.geometry)
+        if self.stage == STAGE_BASE:
+            if self.sh is None or self.shading is not None:
+                raise MixedStage("base stage carries SH colors only")
+            if self.sh.coefficients.shape[0] != n:
+                raise ShapeMismatch("SH coefficient count != primitive count")
+        else:
+            if self.sh is not None:
+                raise MixedStage("editable stage must not carry SH data")
+            if self.palette is None:
+                raise MixedStage("editable stage requires a palette")
+            if self.quantized is None and (self.shading is None or len(self.shading) != n):
+                raise ShapeMismatch("shading attribute count != primitive count")
+
+    def __len__(self):
+        return len(self.geometry)
+
+    @property
+    def is_quantized(self):
+        return self.quantized is not None
+
+    def copy(self):
+        from .vq import Codebook
+        return BasicSceneModel(
+            stage=self.stage, geometry=self.geometry.copy(),
+            sh=ShColor(self.sh.coefficients.copy(), self.sh.degree) if self.sh is not None else None,
+            shading=self.shading.copy() if self.shading is not None else None,
+            palette=self.palette.copy() if self.palette is not None else None,
+            quantized={k: (Codebook(cb.name, cb.centroids.copy()), idx.copy())
+                       for k, (cb, idx) in self.quantized.items()} if self.quantized else None,
+            metadata=dict(self.metadata))
+
+
+@dataclass
+class EditState:
+    """Per-scene edits: optional palette recolour and an opacity scale."""
+
+    palette_override: np.ndarray = None
+    opacity_scale: float = 1.0
+
+    def __post_init__(self):
+        if self.palette_override is not None:
+            self.palette_override = np.asarray(self.palette_override, dtype=np.float64).reshape(3)
+            if np.any((self.palette_override < 0) | (self.palette_override > 1)):
+                raise OutOfRange("palette override components must lie in [0, 1]")
+        self.opacity_scale = float(self.opacity_scale)
+        if self.opacity_scale < 0:
+            raise OutOfRange("opacity scale must be >= 0")
+
+    def copy(self):
+        return EditState(None if self.palette_override is None else self.palette_override.copy(),
+                         self.opacity_scale)
+
+    def to_dict(self):
+        return {"palette_override": None if self.palette_override is None
+                else self.palette_override.tolist(), "opacity_scale": self.opacity_scale}
+
+    @classmethod
+    def from_dict(cls, d):
+        return cls(d.get("palette_override"), d.get("opacity_scale", 1.0))
+
+
+@dataclass
+class ComposedScene:
+    """Ordered editable models with per-scene edits and one global light."""
+
+    models: list
+    edits: list
+    light: LightConfig
+    transform: dict = None
+
+    def __post_init__(self):
+        if len(self.edits) != len(self.models):
+            raise ShapeMismatch("one edit state per basic model required")
+
+    @classmethod
+    def compose(cls, models, light=None):
+        """Concatenate editable models (quantized inputs are decoded first;
+        scene.py:160-167).  No re-optimisation."""
+        from .vq import dequantize_model
+        if any(m.stage != STAGE_EDITABLE for m in models):
+            raise MixedStage("only editable-stage models compose")
+        models = [dequantize_model(m) if m.is_quantized else m.copy() for m in models]
+        return cls(models, [EditState() for _ in models], light or LightConfig())
+
+    @property
+    def count(self):
+        return sum(len(m) for m in self.models)
+
+    @property
+    def scene_ids(self):
+        return np.concatenate([np.full(len(m), i, dtype=np.int64)
+                               for i, m in enumerate(self.models)])
+
+    def copy(self):
+        return ComposedScene([m.copy() for m in self.models], [e.copy() for e in self.edits],
+                             self.light.copy(),
+                             dict(self.transform) if self.transform is not None else None)
+
+
+@dataclass
+class EffectiveScene:
+    """Edit-resolved snapshot (host), scene.py:188-196."""
+
+    geometry: GaussianGeometry
+    shading: ShadingAttributes
+    palette_rgb: np.ndarray
+    light: LightConfig
+    scene_ids: np.ndarray
+
+
+def _sigmoid(x):
+    out = np.empty_like(x)
+    pos = x >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    e = np.exp(x[~pos])
+    out[~pos] = e / (1.0 + e)
+    return out
+
+
+def apply_edits(scene):
+    """Resolve edits into effective primitives on the host (scene.py:199-228).
+
+    The GPU render path does not call this: K1 resolves the same edits per
+    splat from the per-scene tables."""
+    geometry = GaussianGeometry.concat([m.geometry for m in scene.models])
+    shading = ShadingAttributes.concat([m.shading for m in scene.models])
+    palette_rgb = np.concatenate([
+        np.broadcast_to(e.palette_override if e.palette_override is not None else m.palette.c_p,
+                        (len(m), 3)) for m, e in zip(scene.models, scene.edits)], axis=0)
+    scales = np.concatenate([np.full(len(m), e.opacity_scale)
+                             for m, e in zip(scene.models, scene.edits)])
+    if not np.all(scales == 1.0):
+        geometry = geometry.copy()
+        p = np.clip(scales * _sigmoid(geometry.o_logit), 1e-12, 1.0 - 1e-9)
+        geometry.o_logit = np.log(p / (1.0 - p))
+    return EffectiveScene(geometry, shading, palette_rgb, scene.light.copy(), scene.scene_ids)
+
+
+class DeviceScene:
+    """A composed editable scene resident in HBM, rendered by K1-K3.
+
+    ``scene`` may be a ComposedScene or a single editable BasicSceneModel.
+    Edits, light and camera are read at render time, so edits applied to the
+    host ComposedScene are picked up by the next frame without re-upload."""
+
+    def __init__(self, scene, device=None):
+        if isinstance(scene, BasicSceneModel):
+            scene = ComposedScene.compose([scene])
+        self.scene = scene
+        models = scene.models
+        geom = {k: np.concatenate([getattr(m.geometry, k) for m in models], axis=0)
+                for k in D.DeviceGaussians.GEOM}
+        shad = {k: np.concatenate([getattr(m.shading, k) for m in models], axis=0)
+                for k in D.DeviceGaussians.SHADE}
+        ids = np.concatenate([np.full(len(m), i, dtype=np.int32) for i, m in enumerate(models)])
+        self.dg = D.DeviceGaussians(geom, shad, ids, device)
+        self.n = self.dg.n
+        self.n_scenes = len(models)
+        self.ws = D.Workspace(self.dg.device)
+        dev = self.dg.device
+        # per-frame edit tables: a ring of pinned host staging buffers (the
+        # host may run ahead of the GPU) + device copies
+        self._ring = 8
+        self._h_tabs = [torch.empty(4 * self.n_scenes, dtype=torch.float64, pin_memory=True)
+                        for _ in range(self._ring)]
+        self._d_tabs = [torch.empty(4 * self.n_scenes, dtype=torch.float64, device=dev)
+                        for _ in range(self._ring)]
+        self._events = [None] * self._ring
+        self._slot = 0
+
+    # ------------------------------------------------------------ per frame
+    def _tables(self, light=None, palettes=None, opacity_scales=None):
+        """Fill the per-scene palette / opacity tables for this frame."""
+        sc = self.scene
+        S = self.n_scenes
+        pal = np.empty((S, 3))
+        osc = np.empty(S)
+        for i, (m, e) in enumerate(zip(sc.models, sc.edits)):
+            pal[i] = e.palette_override if e.palette_override is not None else m.palette.c_p
+            osc[i] = e.opacity_scale
+        if palettes is not None:
+            pal = np.asarray(palettes, dtype=np.float64).reshape(S, 3)
+        if opacity_scales is not None:
+            osc = np.asarray(opacity_scales, dtype=np.float64).reshape(S)
+        k = self._slot
+        self._slot = (k + 1) % self._ring
+        if self._events[k] is not None:
+            self._events[k].synchronize()
+        h_tab, d_tab = self._h_tabs[k], self._d_tabs[k]
+        h = h_tab.numpy()
+        h[:3 * S] = pal.reshape(-1)
+        h[3 * S:] = osc
+        d_tab.copy_(h_tab, non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._events[k] = ev
+        self._d_tab = d_tab
+        light = light or sc.light
+        shading = D.shading_struct(self.dg, d_tab[:3 * S], False, light)
+        edits = L.Edits_t()
+        edits.scene_id = self.dg.scene_id.data_ptr()
+        edits.opacity_scale = d_tab[3 * S:].data_ptr()
+        edits.rescale_opacity = 0 if np.all(osc == 1.0) else 1
+        return shading, edits
+
+    def h2d_bytes_per_frame(self):
+        return 8 * 4 * self.n_scenes
+
+    def render_frame(self, cam, channels=("color", "alpha"), attrs=None, dtype=np.float32,
+                     want_state=False, debug=False, light=None, lam=None, b=None,
+                     palettes=None, opacity_scales=None, fast=False, out=None, stream=None,
+                     events=None):
+        """Enqueue one frame; returns the Frame of device tensors.
+
+        fast=True skips the pair-count readback (no host sync): the pair
+        capacity learned on earlier frames is reused and overflow must be
+        checked later with ``check_overflow(frame)``."""
+        layout = _channel_layout(channels, attrs)
+        cols, attr_cols, K = _cols(layout)
+        shading, edits = self._tables(light, palettes, opacity_scales)
+        if lam is not None or b is not None:
+            shading = D.shading_struct(self.dg, self._d_tab[:3 * self.n_scenes], False,
+                                       light or self.scene.light, lam, b)
+        attrs_dev = [(D.to_dev(np.asarray(attrs[name], dtype=np.float64).reshape(self.n, w)), c, w)
+                     for name, c, w in attr_cols]
+        f64 = np.dtype(dtype) == np.float64
+        if not fast or self.ws.pair_capacity == 0:
+            F = D.rasterize_device(self.dg, cam, K, cols, self.ws, shading, edits, None, attrs_dev,
+                                   f64, want_state, debug, stream)
+        else:
+            if events:
+                events[0].record()
+            F = D.preprocess(self.dg, cam, K, cols, self.ws, shading, edits, None, attrs_dev, f64,
+                             debug, stream)
+            if events:
+                events[1].record()
+            D.bin_sort(F, self.ws, stream)
+            if events:
+                events[2].record()
+            D.blend(F, self.ws, want_state, stream, out=out)
+            if events:
+                events[3].record()
+            F.empty = False
+        F.layout = layout
+        F.dtype = dtype
+        F._keep_tabs = (shading, edits)
+        return F
+
+    def render_host(self, cam, host_out, host_contrib, **kw):
+        """Render and copy the maps into caller-provided pinned host tensors
+        (the end-to-end path: per-frame H2D edit tables in, D2H image out)."""
+        F = self.render_frame(cam, fast=True, **kw)
+        host_out.copy_(F.out, non_blocking=True)
+        host_contrib.copy_(F.contrib, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if self.check_overflow(F):  # capacity grew: redo synchronously
+            F = self.render_frame(cam, fast=False, **kw)
+            host_out.copy_(F.out)
+            host_contrib.copy_(F.contrib)
+        return _unpack(host_out.numpy(), F.layout, host_contrib.numpy())
+
+    @staticmethod
+    def check_overflow(F):
+        return int(F.n_pairs.item()) > F.capacity
+
+    def render(self, cam, channels=("color", "alpha"), attrs=None, dtype=np.float32, **kw):
+        """Synchronous render returning host RenderOutput (numpy)."""
+        F = self.render_frame(cam, channels, attrs, dtype, **kw)
+        if F.empty and self.n == 0:
+            H, W = cam.height, cam.width
+            K = sum(w for _, w in F.layout)
+            return _unpack(np.zeros((H, W, K), dtype=dtype), F.layout, np.zeros((H, W), np.int32))
+        out = (F.out64 if F.f64 else F.out).cpu().numpy().astype(dtype, copy=False)
+        return _unpack(out, F.layout, F.contrib.cpu().numpy())
+
+
+def render_composed(scene, cam, channels=("color", "alpha"), attrs=None, dtype=np.float32,
+                    sequential=False):
+    """Shade and rasterize a composed scene for one camera (scene.py:231-239).
+
+    Uploads the scene for this one call; keep a ``DeviceScene`` to render
+    many frames of the same scene without re-uploading."""
+    del sequential
+    return DeviceScene(scene).render(cam, channels, attrs, dtype)

@@ -1,0 +1,203 @@
+"""Scalar-codebook vector quantization (drop-in for voxsplat/vq.py).
+
+Assignment (K5) and decode (K6) run on the GPU; both are HBM-bound kernels
+(1-D codebooks: nearest codeword = binary search over float64 midpoints,
+bit-identical to np.searchsorted(mids, v, 'left'), vq.py:90-96).
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _lib as L
+from . import device as D
+from .errors import CorruptIndex, EmptyInput, OutOfRange
+
+DEFAULT_CODEBOOK_SIZE = 256
+KMEANS_MAX_ITERS = 50
+KMEANS_SHIFT_TOL = 1e-6
+
+QUANTIZED_ATTRIBUTES = (
+    ("q_raw", "geometry"), ("log_s", "geometry"), ("o_logit", "geometry"),
+    ("delta_c", "shading"), ("k_a_raw", "shading"), ("k_d_raw", "shading"),
+    ("k_s_raw", "shading"), ("log_beta", "shading"),
+)
+
+
+def assign_device(values_dev, centroids_dev):
+    """GPU nearest-centroid index (uint16 stored in int16 tensor)."""
+    n = values_dev.numel()
+    k = centroids_dev.numel()
+    out = torch.empty(n, dtype=torch.int16, device=values_dev.device)
+    L.check(L.lib().ivr_vq_assign(D.ptr(values_dev), n, D.ptr(centroids_dev), k, D.ptr(out),
+                                  D.stream_handle()), "ivr_vq_assign")
+    return out
+
+
+def decode_device(idx_dev, centroids_dev):
+    """GPU codebook gather; raises CorruptIndex on an out-of-range index."""
+    n = idx_dev.numel()
+    k = centroids_dev.numel()
+    out = torch.empty(n, dtype=torch.float64, device=idx_dev.device)
+    bad = torch.full((1,), -1, dtype=torch.int64, device=idx_dev.device)
+    L.check(L.lib().ivr_vq_decode(D.ptr(idx_dev), n, D.ptr(centroids_dev), k, D.ptr(out),
+                                  D.ptr(bad), D.stream_handle()), "ivr_vq_decode")
+    return out, bad
+
+
+def assign_nearest(values, centroids):
+    """Index of the nearest sorted centroid for each value (vq.py:90-96)."""
+    values = np.asarray(values, dtype=np.float64)
+    centroids = np.asarray(centroids, dtype=np.float64).reshape(-1)
+    if centroids.size == 1:
+        return np.zeros(values.shape, dtype=np.int64)
+    if centroids.size > 65536:
+        raise OutOfRange("codebooks above 65536 entries are not supported")
+    if values.size == 0:
+        return np.zeros(values.shape, dtype=np.int64)
+    idx = assign_device(D.to_dev(values.reshape(-1)), D.to_dev(centroids))
+    return (idx.cpu().numpy().view(np.uint16).astype(np.int64)).reshape(values.shape)
+
+
+def _index_dtype(k):
+    return np.uint8 if k <= 256 else np.uint16
+
+
+@dataclass
+class Codebook:
+    """Sorted scalar centroids for one attribute (shared by its components)."""
+
+    name: str
+    centroids: np.ndarray
+
+    def __post_init__(self):
+        self.centroids = np.asarray(self.centroids, dtype=np.float64).reshape(-1)
+        if self.centroids.size < 1:
+            raise EmptyInput(f"codebook {self.name!r} is empty")
+        if np.any(np.diff(self.centroids) < 0):
+            raise OutOfRange(f"codebook {self.name!r} centroids must be sorted")
+
+    @property
+    def k(self):
+        return self.centroids.size
+
+    @property
+    def index_dtype(self):
+        return _index_dtype(self.k)
+
+    def encode(self, values):
+        return assign_nearest(values, self.centroids).astype(self.index_dtype)
+
+    def decode(self, indices):
+        indices = np.asarray(indices)
+        if indices.size == 0:
+            return np.zeros(indices.shape)
+        if int(indices.max()) >= self.k:  # also checked on device below
+            raise CorruptIndex(f"codebook {self.name!r}: index {int(indices.max())} >= K={self.k}")
+        idx = D.to_dev(indices.reshape(-1).astype(np.uint16).view(np.int16), torch.int16)
+        out, bad = decode_device(idx, D.to_dev(self.centroids))
+        if int(bad.item()) >= 0:
+            raise CorruptIndex(f"codebook {self.name!r}: index {int(bad.item())} >= K={self.k}")
+        return out.cpu().numpy().reshape(indices.shape)
+
+
+def kmeans(samples, k, seed=0, restarts=5):
+    """Scalar k-means: k-means++ restarts + Lloyd, lowest SSE wins
+    (vq.py:31-87).  Returns sorted distinct centroids."""
+    samples = np.asarray(samples, dtype=np.float64).reshape(-1)
+    if samples.size == 0:
+        raise EmptyInput("kmeans needs at least one sample")
+    if k < 1:
+        raise OutOfRange("codebook size must be >= 1")
+    distinct = np.unique(samples)
+    if distinct.size <= k:
+        return distinct
+    rng = np.random.default_rng(seed)
+    x_dev = D.to_dev(samples)
+    best, best_sse = None, np.inf
+    for _ in range(restarts):
+        c = np.empty(k)
+        c[0] = samples[rng.integers(samples.size)]
+        d2 = (samples - c[0]) ** 2
+        for i in range(1, k):
+            total = d2.sum()
+            if total <= 0.0:
+                c[i:] = c[0]
+                break
+            c[i] = samples[rng.choice(samples.size, p=d2 / total)]
+            d2 = np.minimum(d2, (samples - c[i]) ** 2)
+        c = _lloyd(samples, x_dev, c)
+        idx = assign_nearest(samples, c)
+        sse = float(np.sum((samples - c[idx]) ** 2))
+        if sse < best_sse:
+            best, best_sse = c, sse
+    return np.unique(best)
+
+
+def _lloyd(samples, x_dev, c):
+    scale = max(float(np.abs(samples).max()), 1e-12)
+    for _ in range(KMEANS_MAX_ITERS):
+        c = np.sort(c)
+        idx = assign_device(x_dev, D.to_dev(c)).view(torch.uint16).to(torch.int64) \
+            if c.size > 1 else torch.zeros(samples.size, dtype=torch.int64, device=x_dev.device)
+        idx_h = idx.cpu().numpy()
+        sums = np.bincount(idx_h, weights=samples, minlength=c.size)
+        cnt = np.bincount(idx_h, minlength=c.size)
+        new = np.where(cnt > 0, sums / np.maximum(cnt, 1), c)
+        shift = np.abs(new - c).max() / scale
+        c = new
+        if shift < KMEANS_SHIFT_TOL:
+            break
+    return np.sort(c)
+
+
+def quantize_attributes(arrays, k=DEFAULT_CODEBOOK_SIZE, seed=0):
+    out = {}
+    for name, arr in arrays.items():
+        arr = np.asarray(arr, dtype=np.float64)
+        cb = Codebook(name, kmeans(arr.reshape(-1), k, seed=seed))
+        out[name] = (cb, cb.encode(arr))
+    return out
+
+
+def quantize_model(model, k=DEFAULT_CODEBOOK_SIZE, seed=0):
+    """Codebook-compress an editable model (vq.py:150-176)."""
+    from .scene import STAGE_EDITABLE, BasicSceneModel
+    if model.stage != STAGE_EDITABLE:
+        raise OutOfRange("only editable-stage models are quantized")
+    if model.quantized is not None:
+        return model.copy()
+    arrays = {name: np.asarray(getattr(getattr(model, owner), name))
+              for name, owner in QUANTIZED_ATTRIBUTES}
+    quant = quantize_attributes(arrays, k=k, seed=seed)
+    geom = model.geometry.copy()
+    geom.q_raw = quant["q_raw"][0].decode(quant["q_raw"][1])
+    geom.log_s = quant["log_s"][0].decode(quant["log_s"][1])
+    geom.o_logit = quant["o_logit"][0].decode(quant["o_logit"][1])
+    return BasicSceneModel(stage=STAGE_EDITABLE, geometry=geom, shading=None,
+                           palette=model.palette.copy(), quantized=quant,
+                           metadata=dict(model.metadata))
+
+
+def dequantize_model(model):
+    """Materialise a plain editable model from a quantized one (vq.py:179-210)."""
+    from .scene import STAGE_EDITABLE, BasicSceneModel
+    from .shading import ShadingAttributes
+    if model.quantized is None:
+        return model.copy()
+    q = model.quantized
+
+    def dec(name):
+        cb, idx = q[name]
+        return cb.decode(idx)
+
+    geom = model.geometry.copy()
+    geom.q_raw, geom.log_s, geom.o_logit = dec("q_raw"), dec("log_s"), dec("o_logit")
+    shading = ShadingAttributes(dec("delta_c"), dec("k_a_raw"), dec("k_d_raw"), dec("k_s_raw"),
+                                dec("log_beta"))
+    return BasicSceneModel(stage=STAGE_EDITABLE, geometry=geom, shading=shading,
+                           palette=model.palette.copy(), quantized=None,
+                           metadata=dict(model.metadata))
