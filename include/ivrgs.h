@@ -101,7 +101,7 @@ typedef struct ivr_proj_out {
     uint64_t *depth_key; /* (n) float64 depth bits if visible else ~0 */
     int32_t *count;      /* (n) tiles touched (0 if invisible) */
     uint16_t *rect;      /* (n,4) tx0, tx1, ty0, ty1 */
-    float *rec;          /* (n,8) blend record: mx,my,o,hi, a/2,b,c/2,0 */
+    float *rec;          /* (n,8) blend record: mx,my,o,hi, a/2,b,c/2,thr */
     float *values;       /* (n,k) packed channel values (float32) */
     double *rec64;       /* optional (n,8): mx,my,a,b,c,o,depth,0 (float64 mode) */
     double *values64;    /* optional (n,k) float64 channel values */
@@ -149,16 +149,37 @@ int ivr_bin_sort(int64_t n, const uint64_t *depth_key, const int32_t *count,
                  int32_t *pair_splat, int32_t *tile_ranges, int32_t *n_pairs,
                  ivr_stream_t stream);
 
+/* K2 with the per-pair tile cull: pairs whose splat provably stays below
+ * alpha 1/255 over their whole tile (float64 minimum of the exponent over the
+ * tile rectangle vs the record's bound) get bit 31 set in pair_splat;
+ * (pair_splat & 0x7fffffff) is still the reference list.  rec is K1's float32
+ * record; width/height the frame size.  ntiles <= 8192. */
+int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int32_t *count,
+                      const uint16_t *rect, const float *rec, int32_t ntx, int32_t nty,
+                      int32_t width, int32_t height, int64_t pair_capacity,
+                      void *workspace, size_t workspace_bytes, int32_t *pair_splat,
+                      int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream);
+
 /* K3: per-tile front-to-back blend.  Replaces _kernels.composite_forward
  * (_kernels.py:31-72).  out (H,W,k) float32 (out64 float64 in f64 mode),
- * contrib/last_pos int32 (H,W), t_final (H,W) float64.  tile_order may be
- * NULL (identity) or a permutation of the tiles (scheduling only). */
+ * contrib/last_pos int32 (H,W), t_final (H,W) float64 (last_pos / t_final /
+ * contrib may be NULL).  tile_order may be NULL (identity) or a permutation
+ * of the tiles (scheduling only).  flags & IVR_BLEND_EXACT: bit-faithful
+ * float64 evaluation of every candidate pair; otherwise float32 with
+ * certified decisions (same contributors, values within ~1e-6). */
+#define IVR_BLEND_EXACT 1     /* flags: every non-skipped pair in reference float64 */
+#define IVR_BLEND_PRECULLED 2 /* flags: pair_splat carries ivr_bin_sort_cull's bit 31 */
 int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_splat,
                   int32_t ntx, int32_t nty, const float *rec, const float *values,
                   const double *rec64, const double *values64, int32_t k,
                   int32_t width, int32_t height, float *out, double *out64,
                   int32_t *contrib, int32_t *last_pos, double *t_final,
-                  const int32_t *tile_order, ivr_stream_t stream);
+                  const int32_t *tile_order, int32_t flags, ivr_stream_t stream);
+
+/* Heaviest-first tile launch order (descending pair count, ties by tile id)
+ * for ivr_blend_fwd; ntiles <= 4096. */
+int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_t *order,
+                   ivr_stream_t stream);
 
 /* K5: VQ assignment, vq.assign_nearest (vq.py:90-96): index of the nearest
  * sorted centroid = searchsorted(mids, v, 'left'); NaN -> K-1.

@@ -18,6 +18,8 @@ LIB_PATH = os.path.join(PKG, "libivrgs.so")
 c_double_p = ctypes.POINTER(ctypes.c_double)
 P = ctypes.c_void_p
 MAX_ATTRS = 8
+BLEND_EXACT = 1
+BLEND_PRECULLED = 2
 
 IVR_OK, IVR_ERR_ARG, IVR_ERR_SHAPE, IVR_ERR_NONFINITE, IVR_ERR_CORRUPT_INDEX, IVR_ERR_CUDA, \
     IVR_ERR_CAPACITY = 0, -1, -2, -3, -4, -5, -6
@@ -75,7 +77,12 @@ _SIGS = {
     "ivr_bin_sort": ([ctypes.c_int64, P, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P,
                       ctypes.c_size_t, P, P, P, P], ctypes.c_int),
     "ivr_blend_fwd": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, P, ctypes.c_int32,
-                       ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P], ctypes.c_int),
+                       ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_int32, P],
+                      ctypes.c_int),
+    "ivr_tile_order": ([P, ctypes.c_int32, P, P], ctypes.c_int),
+    "ivr_bin_sort_cull": ([ctypes.c_int64, P, P, P, P, ctypes.c_int32, ctypes.c_int32,
+                           ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P, ctypes.c_size_t, P,
+                           P, P, P], ctypes.c_int),
     "ivr_vq_assign": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_vq_decode": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P, P], ctypes.c_int),
 }

@@ -191,10 +191,12 @@ preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E,
     const float mx32 = (float)mx, my32 = (float)my;
     const float a32 = (float)q0, b32 = (float)q1, c32 = (float)q2, o32 = (float)opacity;
     float hi32 = __int_as_float(0x7f800000);  // +inf: always take the exact path
+    float thr32 = 0.0f;                         // ln(o / (1/255)): alpha-skip exponent
     {
         const double a = a32, b = b32, c = c32;
         const double oo = f64_mode ? opacity : (double)o32;
         const double thr = log(oo / kAlphaSkip);
+        if (thr == thr && fabs(thr) < 1e30) thr32 = (float)thr;
         const double hm = 0.5 * (a + c), dd = sqrt(0.25 * (a - c) * (a - c) + b * b);
         const double lmin = hm - dd, lmaxq = hm + dd;
         if (lmin > 0.0 && a > 0.0 && c > 0.0 && thr == thr) {
@@ -210,7 +212,7 @@ preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E,
     }
     float4 *rec = reinterpret_cast<float4 *>(O.rec) + 2 * i;
     rec[0] = make_float4(mx32, my32, o32, hi32);
-    rec[1] = make_float4(0.5f * a32, b32, 0.5f * c32, 0.0f);
+    rec[1] = make_float4(0.5f * a32, b32, 0.5f * c32, thr32);
     if (O.rec64) {
         double *r = O.rec64 + 8 * i;
         r[0] = mx; r[1] = my; r[2] = q0; r[3] = q1; r[4] = q2; r[5] = opacity; r[6] = tz; r[7] = 0.0;

@@ -1,18 +1,31 @@
 // K2 -- bit-exact (tile, depth) pair ordering on device.
 //
 // Reproduces np.lexsort((depth[pair_splat], pair_tile)) (rasterizer.py:129)
-// over the pairs emitted by fill_pairs (_kernels.py:19-28) without ever
-// materialising an 80-bit composite key:
-//   1. stable LSD radix sort of the N float64 depth keys (positive doubles
-//      compare like their bit patterns; invisible splats carry ~0 and sort
-//      last; ties keep index order = lexsort's tie break on pair order);
-//   2. exclusive scan of the per-splat tile counts in depth-rank order and
-//      emission of the (tile, splat) pairs in rank order;
-//   3. stable LSD radix sort of the pairs by 16-bit tile id (2 passes);
-//   4. tile ranges (np.searchsorted(pair_tile, arange(T+1))) from the run
-//      boundaries of the sorted tile ids.
-// All sizes that depend on the data live in device memory, so the whole
-// sequence is stream-ordered and CUDA-graph capturable.
+// over the pairs of fill_pairs (_kernels.py:19-28) and the tile ranges of
+// np.searchsorted (rasterizer.py:132), without materialising a composite key:
+//
+//  1. depth ranks.  Positive float64 depths order like their bit patterns.
+//     The bits are shifted into a 31-bit "coarse" key (bits - min) >> s, the
+//     coarse keys are radix-sorted stably (4 x 8-bit LSD passes; invisible
+//     splats carry 0xffffffff and sort last), and runs of equal coarse keys
+//     are re-ordered by the full 64-bit key (insertion sort, stable).  If a
+//     run is longer than kMaxRun the whole order is recomputed with a full
+//     64-bit LSD sort (8 passes) -- correctness never depends on the data.
+//     Ties keep index order = lexsort's tie break on fill_pairs' order.
+//  2. rank offsets: exclusive scan of the per-splat tile counts in rank order
+//     (total = P).
+//  3. counting placement: pairs are enumerated in rank order (pair p belongs
+//     to the rank r with roff[r] <= p < roff[r+1]); per 8192-pair block a
+//     per-tile histogram is built, scanned per tile across blocks, and each
+//     pair is written once to tile_start[t] + block offset + its stable rank
+//     inside the block (warp match_any ranking).  Tile ranges are the
+//     exclusive scan of the tile totals.
+//  4. optional tile cull: while placing, each pair is tested in float64 for
+//     whether its splat can reach alpha >= 1/255 anywhere in the tile; pairs
+//     that cannot are marked with bit 31 (pair_splat & 0x7fffffff is the
+//     reference list), letting the blend skip them without loading records.
+// All data-dependent sizes live in device memory: the sequence is
+// stream-ordered and CUDA-graph capturable.
 #include "ivr_common.cuh"
 
 namespace ivr {
@@ -20,16 +33,27 @@ namespace sortk {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 8;                       // per thread
-constexpr int kChunk = kThreads * kItems;       // 2048 items per block
+constexpr int kItems = 8;                  // per thread in radix passes
+constexpr int kChunk = kThreads * kItems;  // 2048 keys per radix block
 constexpr int kRadix = 256;
+constexpr int kPairBlock = 8192;           // pairs per placement block
+constexpr int kPairPerWarp = kPairBlock / kWarps;
+constexpr int kMaxRun = 64;
+constexpr uint32_t kInvisible = 0xffffffffu;
+constexpr int kMaxTiles = 8192;  // placement keeps 8 x ntiles uint16 counters in smem
+
+__global__ void init_minmax_kernel(unsigned long long *mm, int32_t *flag) {
+    mm[0] = ~0ull;
+    mm[1] = 0ull;
+    *flag = 0;
+}
 
 __device__ __forceinline__ int64_t load_n(const int32_t *n_dev, int64_t n_host, int64_t cap) {
     int64_t n = n_dev ? (int64_t)(*n_dev) : n_host;
     return n < cap ? n : cap;
 }
 
-// Inclusive block scan of one uint32 per thread (256 threads).
+// Inclusive block scan of one uint32 per thread (kThreads threads).
 __device__ __forceinline__ uint32_t block_incl_scan(uint32_t x, uint32_t *s_warp, uint32_t &total) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
 #pragma unroll
@@ -55,92 +79,83 @@ __device__ __forceinline__ uint32_t block_incl_scan(uint32_t x, uint32_t *s_warp
     return x;
 }
 
-// ----------------------------------------------------------------- digit histograms
-// All eight byte-histograms of the depth keys in one read; used to skip
-// passes whose digit is constant over all keys.
+// ----------------------------------------------------------------- coarse keys
 __global__ void __launch_bounds__(kThreads)
-key64_hist_kernel(const uint64_t *keys, int64_t n, uint32_t *hist /* [8][256] */) {
-    __shared__ uint32_t s[8 * kRadix];
-    for (int i = threadIdx.x; i < 8 * kRadix; i += kThreads) s[i] = 0;
-    __syncthreads();
+minmax_kernel(const uint64_t *keys, int64_t n, unsigned long long *mm /* [min, max] */) {
+    unsigned long long lo = ~0ull, hi = 0ull;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * kThreads) {
-        const uint64_t k = keys[i];
+        const unsigned long long k = keys[i];
+        if (k != ~0ull) {
+            lo = k < lo ? k : lo;
+            hi = k > hi ? k : hi;
+        }
+    }
 #pragma unroll
-        for (int p = 0; p < 8; ++p) atomicAdd(&s[p * kRadix + ((k >> (8 * p)) & 255)], 1u);
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
     }
-    __syncthreads();
-    for (int i = threadIdx.x; i < 8 * kRadix; i += kThreads)
-        if (s[i]) atomicAdd(&hist[i], s[i]);
-}
-
-// cur[p] in {0: caller input (values = identity), 1: buffer A, 2: buffer B}
-__global__ void pass_plan_kernel(const uint32_t *hist, int64_t n, int npass, int32_t *skip,
-                                 int32_t *cur) {
-    if (threadIdx.x != 0 || blockIdx.x != 0) return;
-    int c = 0;
-    cur[0] = 0;
-    for (int p = 0; p < npass; ++p) {
-        bool trivial = false;
-        for (int d = 0; d < kRadix; ++d)
-            if ((int64_t)hist[p * kRadix + d] == n) trivial = true;
-        skip[p] = trivial || n == 0;
-        if (!skip[p]) c = (c == 1) ? 2 : 1;
-        cur[p + 1] = c;
+    if ((threadIdx.x & 31) == 0) {
+        atomicMin(mm, lo);
+        atomicMax(mm + 1, hi);
     }
 }
 
-template <typename KeyT>
-struct Bufs {
-    const KeyT *in_keys;      // cur == 0
-    const uint32_t *in_vals;  // cur == 0 (nullptr = identity)
-    KeyT *keys[2];            // cur == 1, 2
-    uint32_t *vals[2];
-};
-
-template <typename KeyT>
-__device__ __forceinline__ void src_of(const Bufs<KeyT> &B, int c, const KeyT *&k, const uint32_t *&v) {
-    if (c == 0) { k = B.in_keys; v = B.in_vals; }
-    else { k = B.keys[c - 1]; v = B.vals[c - 1]; }
+__global__ void __launch_bounds__(kThreads)
+coarse_key_kernel(const uint64_t *keys, int64_t n, const unsigned long long *mm, uint32_t *ck) {
+    const unsigned long long lo = mm[0], hi = mm[1];
+    const unsigned long long range = hi >= lo ? hi - lo : 0ull;
+    const int bits = range ? 64 - __clzll((long long)range) : 0;
+    const int s = bits > 31 ? bits - 31 : 0;
+    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kThreads) {
+        const unsigned long long k = keys[i];
+        ck[i] = k == ~0ull ? kInvisible : (uint32_t)((k - lo) >> s);
+    }
 }
 
-// ----------------------------------------------------------------- upsweep
+// ----------------------------------------------------------------- radix passes
+// Stable LSD pass (8-bit digit at `shift`) of (key, value) pairs.  vals_in ==
+// nullptr means identity values.  `gate` (device int, may be null): the pass
+// runs only when *gate != 0.
 template <typename KeyT>
 __global__ void __launch_bounds__(kThreads)
-upsweep_kernel(Bufs<KeyT> B, const int32_t *cur, const int32_t *skip, int pass, int shift,
-               const int32_t *n_dev, int64_t n_host, int64_t cap, uint32_t *blockhist,
-               int nblocks) {
-    if (skip && skip[pass]) return;
-    const int64_t n = load_n(n_dev, n_host, cap);
+upsweep_kernel(const KeyT *keys, int64_t n, int shift, uint32_t *blockhist, int nblocks,
+               const int32_t *gate) {
+    if (gate && *gate == 0) return;
     __shared__ uint32_t s[kRadix];
     s[threadIdx.x] = 0;
     __syncthreads();
-    const KeyT *keys;
-    const uint32_t *vals;
-    src_of(B, cur ? cur[pass] : pass == 0 ? 0 : 1, keys, vals);
     const int64_t base = (int64_t)blockIdx.x * kChunk;
+    KeyT k[kItems];
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const int64_t idx = base + r * kThreads + threadIdx.x;
-        if (idx < n) atomicAdd(&s[(uint32_t)(keys[idx] >> shift) & 255u], 1u);
+        k[r] = idx < n ? keys[idx] : (KeyT)0;
+    }
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int64_t idx = base + r * kThreads + threadIdx.x;
+        if (idx < n) atomicAdd(&s[(uint32_t)(k[r] >> shift) & 255u], 1u);
     }
     __syncthreads();
     blockhist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = s[threadIdx.x];
 }
 
-// ----------------------------------------------------------------- per-digit row scan
-// grid = 256 (one block per digit): exclusive scan of blockhist[d][0..nblocks)
+// grid = #rows: exclusive scan of row[0..ncols) in place, row total -> rowtotal.
 __global__ void __launch_bounds__(1024)
-rowscan_kernel(const int32_t *skip, int pass, uint32_t *blockhist, int nblocks,
-               uint32_t *rowtotal) {
-    if (skip && skip[pass]) return;
+rowscan_kernel(uint32_t *rows, int ncols, uint32_t *rowtotal, const int32_t *gate) {
+    if (gate && *gate == 0) return;
     __shared__ uint32_t s_warp[32];
-    uint32_t *row = blockhist + (int64_t)blockIdx.x * nblocks;
+    uint32_t *row = rows + (int64_t)blockIdx.x * ncols;
     uint32_t carry = 0;
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int base = 0; base < nblocks; base += 1024) {
+    for (int base = 0; base < ncols; base += 1024) {
         const int i = base + threadIdx.x;
-        const uint32_t v = i < nblocks ? row[i] : 0;
+        const uint32_t v = i < ncols ? row[i] : 0;
         uint32_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -160,56 +175,52 @@ rowscan_kernel(const int32_t *skip, int pass, uint32_t *blockhist, int nblocks,
         }
         __syncthreads();
         const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0);
-        if (i < nblocks) row[i] = carry + incl - v;
+        if (i < ncols) row[i] = carry + incl - v;
         carry += s_warp[31];
         __syncthreads();
     }
     if (threadIdx.x == 0) rowtotal[blockIdx.x] = carry;
 }
 
-// ----------------------------------------------------------------- downsweep
 template <typename KeyT>
 __global__ void __launch_bounds__(kThreads)
-downsweep_kernel(Bufs<KeyT> B, const int32_t *cur, const int32_t *skip, int pass, int shift,
-                 const int32_t *n_dev, int64_t n_host, int64_t cap,
-                 const uint32_t *blockhist, const uint32_t *rowtotal, int nblocks,
-                 KeyT *fixed_dst_keys, uint32_t *fixed_dst_vals) {
-    if (skip && skip[pass]) return;
-    const int64_t n = load_n(n_dev, n_host, cap);
+downsweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
+                 const uint32_t *blockhist, const uint32_t *rowtotal, int nblocks, KeyT *dkeys,
+                 uint32_t *dvals, const int32_t *gate) {
+    if (gate && *gate == 0) return;
     const int64_t base = (int64_t)blockIdx.x * kChunk;
     if (base >= n) return;
     __shared__ uint32_t s_wcnt[kWarps][kRadix];
-    __shared__ uint32_t s_gbase[kRadix];    // global base of digit d for this block
-    __shared__ uint32_t s_lstart[kRadix];   // block-local start of digit d
+    __shared__ uint32_t s_gbase[kRadix];
+    __shared__ uint32_t s_lstart[kRadix];
     __shared__ uint32_t s_warp[kWarps];
     __shared__ KeyT s_keys[kChunk];
     __shared__ uint32_t s_vals[kChunk];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    KeyT k[kItems];
+    uint32_t v[kItems];
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {  // all loads first (memory-level parallelism)
+        const int64_t idx = base + warp * (32 * kItems) + r * 32 + lane;
+        const bool ok = idx < n;
+        k[r] = ok ? keys[idx] : (KeyT)0;
+        v[r] = ok ? (vals ? vals[idx] : (uint32_t)idx) : 0u;
+    }
+#pragma unroll
     for (int w = 0; w < kWarps; ++w) s_wcnt[w][tid] = 0;
-    // digit base = exclusive scan of the digit totals + this block's row offset
     uint32_t tot;
     const uint32_t rt = rowtotal[tid];
     const uint32_t incl = block_incl_scan(rt, s_warp, tot);
     s_gbase[tid] = incl - rt + blockhist[(int64_t)tid * nblocks + blockIdx.x];
-
-    const int c_src = cur ? cur[pass] : (pass == 0 ? 0 : 1);
-    const KeyT *keys;
-    const uint32_t *vals;
-    src_of(B, c_src, keys, vals);
-    KeyT *dkeys = fixed_dst_keys ? fixed_dst_keys : B.keys[cur ? cur[pass + 1] - 1 : (pass & 1) ? 0 : 1];
-    uint32_t *dvals = fixed_dst_vals ? fixed_dst_vals : B.vals[cur ? cur[pass + 1] - 1 : (pass & 1) ? 0 : 1];
     __syncthreads();
 
-    KeyT k[kItems];
-    uint32_t v[kItems], dig[kItems], rank[kItems];
+    uint32_t dig[kItems], rank[kItems];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const int64_t idx = base + warp * (32 * kItems) + r * 32 + lane;
         const bool ok = idx < n;
-        k[r] = ok ? keys[idx] : (KeyT)0;
-        v[r] = ok ? (vals ? vals[idx] : (uint32_t)idx) : 0u;
         dig[r] = ok ? ((uint32_t)(k[r] >> shift) & 255u) : 256u;
         const uint32_t peers = __match_any_sync(0xffffffffu, dig[r]);
         uint32_t before = 0;
@@ -220,9 +231,9 @@ downsweep_kernel(Bufs<KeyT> B, const int32_t *cur, const int32_t *skip, int pass
         rank[r] = before + __popc(peers & lt);
     }
     __syncthreads();
-    // per digit: exclusive scan across warps; block count per digit
     {
         uint32_t run = 0;
+#pragma unroll
         for (int w = 0; w < kWarps; ++w) {
             const uint32_t c = s_wcnt[w][tid];
             s_wcnt[w][tid] = run;
@@ -251,29 +262,131 @@ downsweep_kernel(Bufs<KeyT> B, const int32_t *cur, const int32_t *skip, int pass
     }
 }
 
-// ----------------------------------------------------------------- rank-order scan
-__device__ __forceinline__ const uint32_t *sorted_vals(const Bufs<uint64_t> &B, const int32_t *cur, int npass) {
-    const int c = cur[npass];
-    return c == 0 ? nullptr : B.vals[c - 1];
-}
-
-__device__ __forceinline__ uint32_t count_at(const Bufs<uint64_t> &B, const int32_t *cur,
-                                             int npass, const int32_t *count, int64_t r) {
-    const uint32_t *sv = sorted_vals(B, cur, npass);
-    const int64_t i = sv ? (int64_t)sv[r] : r;
-    return (uint32_t)count[i];
-}
-
+// ----------------------------------------------------------------- run fix-up
+// Re-order runs of equal coarse keys by the full 64-bit key (stable).  Runs
+// longer than kMaxRun set *need_full (the 64-bit fallback sort then runs).
 __global__ void __launch_bounds__(kThreads)
-scan_reduce_kernel(Bufs<uint64_t> B, const int32_t *cur, int npass, const int32_t *count,
-                   int64_t n, uint32_t *partial) {
+fixup_kernel(const uint32_t *ck, uint32_t *idx, int64_t n, const uint64_t *full,
+             int32_t *need_full) {
+    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    if (i >= n) return;
+    const uint32_t k = ck[i];
+    if (k == kInvisible) return;
+    if (i > 0 && ck[i - 1] == k) return;        // not a run head
+    if (i + 1 >= n || ck[i + 1] != k) return;   // run of one
+    int64_t e = i + 1;
+    while (e < n && ck[e] == k && e - i <= kMaxRun) ++e;
+    if (e - i > kMaxRun) {
+        *need_full = 1;
+        return;
+    }
+    const int len = (int)(e - i);
+    uint32_t v[kMaxRun];
+    uint64_t key[kMaxRun];
+    for (int a = 0; a < len; ++a) {
+        v[a] = idx[i + a];
+        key[a] = full[v[a]];
+    }
+    for (int a = 1; a < len; ++a) {  // stable insertion sort (indices ascending on ties)
+        const uint32_t tv = v[a];
+        const uint64_t tk = key[a];
+        int b = a - 1;
+        while (b >= 0 && key[b] > tk) {
+            key[b + 1] = key[b];
+            v[b + 1] = v[b];
+            --b;
+        }
+        key[b + 1] = tk;
+        v[b + 1] = tv;
+    }
+    for (int a = 0; a < len; ++a) idx[i + a] = v[a];
+}
+
+// ----------------------------------------------------------------- fallback
+// Rare path (a coarse-key run longer than kMaxRun, i.e. many depths packed
+// into one 31-bit bucket by an extreme depth range): one CTA recomputes the
+// whole order with a stable 8 x 8-bit LSD sort of the full 64-bit keys.
+// Launched every frame; returns immediately unless *need_full.
+constexpr int kFbThreads = 1024;
+constexpr int kFbWarps = kFbThreads / 32;
+
+__global__ void __launch_bounds__(kFbThreads, 1)
+fallback_sort_kernel(const uint64_t *depth_key, int64_t n, const int32_t *need_full,
+                     uint64_t *kA, uint64_t *kB, uint32_t *vA, uint32_t *vB) {
+    if (*need_full == 0) return;
+    __shared__ uint32_t s_off[kRadix];
+    __shared__ uint32_t s_wc[kFbWarps][kRadix];
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const uint32_t lt = lanemask_lt();
+    for (int p = 0; p < 8; ++p) {
+        const uint64_t *ki = p == 0 ? depth_key : ((p & 1) ? kB : kA);
+        const uint32_t *vi = p == 0 ? nullptr : ((p & 1) ? vB : vA);
+        uint64_t *ko = (p & 1) ? kA : kB;
+        uint32_t *vo = (p & 1) ? vA : vB;
+        const int sh = 8 * p;
+        // digit histogram -> exclusive offsets
+        if (tid < kRadix) s_off[tid] = 0;
+        __syncthreads();
+        for (int64_t i = tid; i < n; i += kFbThreads) atomicAdd(&s_off[(ki[i] >> sh) & 255], 1u);
+        __syncthreads();
+        if (tid == 0) {
+            uint32_t run = 0;
+            for (int d = 0; d < kRadix; ++d) {
+                const uint32_t c = s_off[d];
+                s_off[d] = run;
+                run += c;
+            }
+        }
+        __syncthreads();
+        // stable scatter, one 1024-element tile at a time
+        for (int64_t base = 0; base < n; base += kFbThreads) {
+            for (int i = tid; i < kFbWarps * kRadix; i += kFbThreads) (&s_wc[0][0])[i] = 0;
+            __syncthreads();
+            const int64_t i = base + tid;
+            const bool ok = i < n;
+            const uint64_t k = ok ? ki[i] : 0ull;
+            const uint32_t v = ok ? (vi ? vi[i] : (uint32_t)i) : 0u;
+            const uint32_t d = ok ? (uint32_t)((k >> sh) & 255) : 256u;
+            const uint32_t peers = __match_any_sync(0xffffffffu, d);
+            if (ok && (peers & lt) == 0) s_wc[warp][d] = __popc(peers);
+            __syncthreads();
+            if (tid < kRadix) {  // exclusive scan across warps for digit tid
+                uint32_t run = 0;
+                for (int w = 0; w < kFbWarps; ++w) {
+                    const uint32_t c = s_wc[w][tid];
+                    s_wc[w][tid] = run;
+                    run += c;
+                }
+            }
+            __syncthreads();
+            if (ok) {
+                const uint32_t pos = s_off[d] + s_wc[warp][d] + __popc(peers & lt);
+                ko[pos] = k;
+                vo[pos] = v;
+            }
+            __syncthreads();
+            // advance the digit offsets by this tile's per-digit totals
+            if (tid < kRadix) s_wc[1][tid] = 0;
+            __syncthreads();
+            if (ok) atomicAdd(&s_wc[1][d], 1u);
+            __syncthreads();
+            if (tid < kRadix) s_off[tid] += s_wc[1][tid];
+            __syncthreads();
+        }
+    }
+    // result in kA/vA after 8 passes (pass 7 writes A)
+}
+
+// ----------------------------------------------------------------- rank offsets
+__global__ void __launch_bounds__(kThreads)
+scan_reduce_kernel(const uint32_t *order, const int32_t *count, int64_t n, uint32_t *partial) {
     __shared__ uint32_t s_warp[kWarps];
     const int64_t base = (int64_t)blockIdx.x * kChunk;
     uint32_t sum = 0;
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const int64_t idx = base + r * kThreads + threadIdx.x;
-        if (idx < n) sum += count_at(B, cur, npass, count, idx);
+        if (idx < n) sum += (uint32_t)count[order[idx]];
     }
     uint32_t tot;
     block_incl_scan(sum, s_warp, tot);
@@ -312,58 +425,233 @@ scan_partials_kernel(uint32_t *partial, int nb, int32_t *n_pairs) {
     if (threadIdx.x == 0) *n_pairs = carry > 0x7fffffffull ? 0x7fffffff : (int32_t)carry;
 }
 
-// exclusive scan of counts in rank order, then emit this rank's pairs
+// roff[r] = exclusive prefix of count[order[r]] (blocked: thread t owns 8 ranks)
 __global__ void __launch_bounds__(kThreads)
-emit_kernel(Bufs<uint64_t> B, const int32_t *cur, int npass, const int32_t *count,
-            const ushort4 *rect, int64_t n, const uint32_t *partial, int ntx, int64_t cap,
-            uint32_t *tile_key, uint32_t *pair_val) {
+scan_apply_kernel(const uint32_t *order, const int32_t *count, int64_t n,
+                  const uint32_t *partial, const int32_t *n_pairs, uint32_t *roff) {
     __shared__ uint32_t s_warp[kWarps];
     const int64_t base = (int64_t)blockIdx.x * kChunk;
-    const uint32_t *sv = sorted_vals(B, cur, npass);
-    // blocked arrangement: thread t owns items base + t*kItems .. +kItems-1
     uint32_t c[kItems];
     uint32_t sum = 0;
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const int64_t idx = base + (int64_t)threadIdx.x * kItems + r;
-        c[r] = idx < n ? (uint32_t)count[sv ? (int64_t)sv[idx] : idx] : 0u;
+        c[r] = idx < n ? (uint32_t)count[order[idx]] : 0u;
         sum += c[r];
     }
     uint32_t tot;
     const uint32_t incl = block_incl_scan(sum, s_warp, tot);
-    uint64_t off = (uint64_t)partial[blockIdx.x] + incl - sum;
+    uint32_t off = partial[blockIdx.x] + incl - sum;
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
         const int64_t idx = base + (int64_t)threadIdx.x * kItems + r;
-        if (c[r]) {
-            const uint32_t i = sv ? sv[idx] : (uint32_t)idx;
-            const ushort4 rc = rect[i];
-            const int w = rc.y - rc.x + 1;
-            for (uint32_t q = 0; q < c[r]; ++q) {
-                const uint64_t pos = off + q;
-                if (pos >= (uint64_t)cap) break;
-                const int ty = rc.z + (int)q / w, tx = rc.x + (int)q % w;
-                tile_key[pos] = (uint32_t)(ty * ntx + tx);
-                pair_val[pos] = i;
-            }
-        }
+        if (idx < n) roff[idx] = off;
         off += c[r];
     }
+    if (blockIdx.x == 0 && threadIdx.x == 0) roff[n] = (uint32_t)*n_pairs;
 }
 
-__global__ void __launch_bounds__(kThreads)
-ranges_kernel(const uint32_t *tile_key, const int32_t *n_pairs, int64_t cap, int ntiles,
-              int32_t *ranges) {
-    const int64_t n = load_n(n_pairs, 0, cap);
-    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (i > n) return;
-    if (n == 0) {
-        for (int t = 0; t <= ntiles; ++t) ranges[t] = 0;
-        return;
+// ----------------------------------------------------------------- placement
+struct PairCtx {
+    const uint32_t *order;  // rank -> splat
+    const uint32_t *roff;   // rank -> first pair (n+1 entries)
+    const ushort4 *rect;
+    const float4 *rec;      // blend records (for the tile cull), may be null
+    int64_t n;
+    int ntx, ntiles;
+    int64_t cap;
+    const int32_t *n_pairs;
+};
+
+// last rank r with roff[r] <= p (zero-count ranks share offsets with the next)
+__device__ __forceinline__ int64_t rank_of(const uint32_t *roff, int64_t lo, int64_t hi, uint32_t p) {
+    // invariant: roff[lo] <= p < roff[hi] (hi may be n with roff[n] = P)
+    while (hi - lo > 1) {
+        const int64_t m = (lo + hi) >> 1;
+        if (roff[m] <= p) lo = m; else hi = m;
     }
-    const int prev = i == 0 ? -1 : (int)tile_key[i - 1];
-    const int here = i == n ? ntiles : (int)tile_key[i];
-    for (int t = prev + 1; t <= here; ++t) ranges[t] = (int32_t)i;
+    return lo;
+}
+
+__device__ __forceinline__ bool tile_cull64(const float4 r0, const float4 r1, int px0, int px1,
+                                            int py0, int py1) {
+    // true when the splat's float64 exponent exceeds hi everywhere in the tile
+    const double hi = r0.w;
+    if (!(hi < 1e30)) return false;
+    const double a = 2.0 * (double)r1.x, b = r1.y, c = 2.0 * (double)r1.z;
+    if (!(a > 0.0 && c > 0.0 && a * c - b * b > 0.0)) return false;
+    const double mx = r0.x, my = r0.y;
+    const double ex0 = px0 - mx, ex1 = px1 - mx, ey0 = py0 - my, ey1 = py1 - my;
+    if (ex0 <= 0.0 && ex1 >= 0.0 && ey0 <= 0.0 && ey1 >= 0.0) return false;
+    const double ia = 1.0 / a, ic = 1.0 / c;
+    double best = 1e300;
+#pragma unroll
+    for (int k = 0; k < 2; ++k) {
+        const double e = k ? ex1 : ex0;
+        double dy = -b * e * ic;
+        dy = dy < ey0 ? ey0 : (dy > ey1 ? ey1 : dy);
+        const double s = 0.5 * (a * e * e + c * dy * dy) + b * e * dy;
+        best = s < best ? s : best;
+        const double f = k ? ey1 : ey0;
+        double dx = -b * f * ia;
+        dx = dx < ex0 ? ex0 : (dx > ex1 ? ex1 : dx);
+        const double t = 0.5 * (a * dx * dx + c * f * f) + b * dx * f;
+        best = t < best ? t : best;
+    }
+    return best > hi;
+}
+
+// Pair p -> (splat, tile); returns false past the end.
+__device__ __forceinline__ bool pair_at(const PairCtx &C, const uint32_t *s_roff, int64_t r0,
+                                        int64_t r1, int64_t P, int64_t p, uint32_t &splat,
+                                        int &tile, int &tx, int &ty) {
+    if (p >= P) return false;
+    const int64_t r = r0 + rank_of(s_roff, 0, r1 - r0, (uint32_t)p);
+    const uint32_t q = (uint32_t)p - s_roff[r - r0];
+    splat = C.order[r];
+    const ushort4 rc = C.rect[splat];
+    const uint32_t w = (uint32_t)(rc.y - rc.x + 1);
+    ty = rc.z + (int)(q / w);
+    tx = rc.x + (int)(q % w);
+    tile = ty * C.ntx + tx;
+    return true;
+}
+
+// Loads the rank offsets covering this block's pairs into shared memory.
+__device__ __forceinline__ void block_ranks(const PairCtx &C, int64_t p0, int64_t P,
+                                            uint32_t *s_roff, int64_t &r0, int64_t &r1) {
+    __shared__ int64_t s_r[2];
+    if (threadIdx.x == 0) {
+        const int64_t pl = (p0 + kPairBlock < P ? p0 + kPairBlock : P) - 1;
+        s_r[0] = rank_of(C.roff, 0, C.n, (uint32_t)p0);
+        s_r[1] = rank_of(C.roff, 0, C.n, (uint32_t)pl) + 1;
+    }
+    __syncthreads();
+    r0 = s_r[0];
+    r1 = s_r[1];
+    for (int64_t i = threadIdx.x; i <= r1 - r0; i += blockDim.x) s_roff[i] = C.roff[r0 + i];
+    __syncthreads();
+}
+
+// per-block tile histogram -> hist[tile * nblocks + block]
+__global__ void __launch_bounds__(kThreads)
+pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
+    extern __shared__ uint32_t smem_u32[];
+    uint32_t *s_cnt = smem_u32;                 // ntiles
+    uint32_t *s_roff = smem_u32 + C.ntiles;     // <= kPairBlock + 1
+    const int64_t P = load_n(C.n_pairs, 0, C.cap);
+    const int64_t p0 = (int64_t)blockIdx.x * kPairBlock;
+    for (int t = threadIdx.x; t < C.ntiles; t += kThreads) s_cnt[t] = 0;
+    __syncthreads();
+    if (p0 < P) {
+        int64_t r0, r1;
+        block_ranks(C, p0, P, s_roff, r0, r1);
+        for (int k = threadIdx.x; k < kPairBlock; k += kThreads) {
+            uint32_t sp;
+            int tile, tx, ty;
+            if (pair_at(C, s_roff, r0, r1, P, p0 + k, sp, tile, tx, ty)) atomicAdd(&s_cnt[tile], 1u);
+        }
+        __syncthreads();
+    }
+    for (int t = threadIdx.x; t < C.ntiles; t += kThreads)
+        hist[(int64_t)t * nblocks + blockIdx.x] = s_cnt[t];
+}
+
+// tile_ranges = exclusive scan of tile totals (single block)
+__global__ void __launch_bounds__(1024)
+tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges) {
+    __shared__ uint32_t s_warp[32];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    uint32_t carry = 0;
+    for (int base = 0; base < ntiles; base += 1024) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < ntiles ? totals[i] : 0;
+        uint32_t x = v;
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = s_warp[lane];
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            s_warp[lane] = w;
+        }
+        __syncthreads();
+        const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0);
+        if (i < ntiles) ranges[i] = (int32_t)(carry + incl - v);
+        carry += s_warp[31];
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) ranges[ntiles] = (int32_t)carry;
+}
+
+// stable placement: each warp owns a contiguous 1024-pair sub-range
+__global__ void __launch_bounds__(kThreads)
+pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *ranges,
+                  int32_t *pair_splat, int W, int H) {
+    extern __shared__ uint32_t smem_u32[];
+    uint32_t *s_roff = smem_u32;                                     // kPairBlock + 1
+    uint16_t *s_wc = reinterpret_cast<uint16_t *>(smem_u32 + kPairBlock + 1);  // [warp][ntiles]
+    const int64_t P = load_n(C.n_pairs, 0, C.cap);
+    const int64_t p0 = (int64_t)blockIdx.x * kPairBlock;
+    if (p0 >= P) return;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < kWarps * C.ntiles; i += kThreads) s_wc[i] = 0;
+    int64_t r0, r1;
+    block_ranks(C, p0, P, s_roff, r0, r1);
+    uint16_t *wc = s_wc + warp * C.ntiles;
+    const uint32_t lt = lanemask_lt();
+    const int64_t wbase = p0 + (int64_t)warp * kPairPerWarp;
+    // phase 1: per-warp tile counts
+    for (int k = 0; k < kPairPerWarp; k += 32) {
+        uint32_t sp;
+        int tile = -1, tx, ty;
+        const bool ok = pair_at(C, s_roff, r0, r1, P, wbase + k + lane, sp, tile, tx, ty);
+        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? tile : -1);
+        if (ok && (peers & lt) == 0) wc[tile] = (uint16_t)(wc[tile] + __popc(peers));
+        __syncwarp();
+    }
+    __syncthreads();
+    // phase 2: exclusive scan across warps, per tile
+    for (int t = tid; t < C.ntiles; t += kThreads) {
+        uint32_t run = 0;
+#pragma unroll
+        for (int w = 0; w < kWarps; ++w) {
+            const uint32_t c = s_wc[w * C.ntiles + t];
+            s_wc[w * C.ntiles + t] = (uint16_t)run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    // phase 3: place (and cull-flag) every pair
+    for (int k = 0; k < kPairPerWarp; k += 32) {
+        uint32_t sp = 0;
+        int tile = -1, tx = 0, ty = 0;
+        const bool ok = pair_at(C, s_roff, r0, r1, P, wbase + k + lane, sp, tile, tx, ty);
+        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? tile : -1);
+        uint32_t before = 0;
+        if (ok) before = wc[tile];
+        __syncwarp();
+        if (ok && (peers & lt) == 0) wc[tile] = (uint16_t)(before + __popc(peers));
+        __syncwarp();
+        if (ok) {
+            const uint32_t pos = (uint32_t)ranges[tile] + hist[(int64_t)tile * nblocks + blockIdx.x] +
+                                 before + __popc(peers & lt);
+            uint32_t v = sp;
+            if (C.rec) {
+                const int px0 = tx * kTile, py0 = ty * kTile;
+                const int px1 = min(px0 + kTile - 1, W - 1), py1 = min(py0 + kTile - 1, H - 1);
+                const float4 a0 = __ldg(C.rec + 2 * sp), a1 = __ldg(C.rec + 2 * sp + 1);
+                if (tile_cull64(a0, a1, px0, px1, py0, py1)) v |= 0x80000000u;
+            }
+            pair_splat[pos] = (int32_t)v;
+        }
+    }
 }
 
 }  // namespace sortk
@@ -372,30 +660,31 @@ ranges_kernel(const uint32_t *tile_key, const int32_t *n_pairs, int64_t cap, int
 using namespace ivr::sortk;
 
 namespace {
-struct Layout {
-    size_t off[16];
-    size_t total;
-};
-
 inline size_t al(size_t x) { return (x + 255) & ~(size_t)255; }
 
-Layout plan(int64_t n, int64_t cap, int32_t ntiles) {
-    Layout L{};
-    const int64_t nb_keys = (n + kChunk - 1) / kChunk;
-    const int64_t nb_pairs = (cap + kChunk - 1) / kChunk;
-    const int64_t nbmax = nb_keys > nb_pairs ? nb_keys : nb_pairs;
+struct Plan {
+    size_t off[16];
+    size_t total;
+    int nbk, nbp;
+};
+
+Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
+    Plan L{};
+    L.nbk = (int)((n + kChunk - 1) / kChunk);
+    L.nbp = (int)((cap + kPairBlock - 1) / kPairBlock);
     size_t sz[16] = {
-        al(8 * (size_t)n), al(8 * (size_t)n),       // keyA keyB
-        al(4 * (size_t)n), al(4 * (size_t)n),       // valA valB
-        al(4 * (size_t)cap), al(4 * (size_t)cap),   // tile keys A/B
-        al(4 * (size_t)cap), al(4 * (size_t)cap),   // pair vals A/B
-        al(4 * (size_t)(256 * (nbmax + 1))),        // blockhist
-        al(4 * 256),                                // rowtotal
-        al(4 * 8 * 256),                            // key64 hist
-        al(4 * 16), al(4 * 16),                     // skip, cur
-        al(4 * (size_t)(nb_keys + 1)),              // scan partials
+        al(4 * (size_t)n), al(4 * (size_t)n),                    // 0,1 coarse keys A/B
+        al(4 * (size_t)n), al(4 * (size_t)n),                    // 2,3 vals A/B
+        al(8 * (size_t)n), al(8 * (size_t)n),                    // 4,5 full keys (fallback) A/B
+        al(4 * (size_t)(n + 1)),                                 // 6 rank offsets
+        al(4 * (size_t)(L.nbk + 1)),                             // 7 scan partials
+        al(4 * (size_t)256 * (L.nbk + 1)),                       // 8 radix blockhist
+        al(4 * 256),                                             // 9 radix rowtotal
+        al(4 * (size_t)ntiles * (L.nbp + 1)),                    // 10 pair tile hist
+        al(4 * (size_t)(ntiles + 1)),                            // 11 tile totals
+        al(16),                                                  // 12 minmax
+        al(16),                                                  // 13 flags
         0, 0};
-    (void)ntiles;
     size_t o = 0;
     for (int i = 0; i < 16; ++i) {
         L.off[i] = o;
@@ -404,20 +693,39 @@ Layout plan(int64_t n, int64_t cap, int32_t ntiles) {
     L.total = o;
     return L;
 }
+
+template <typename KeyT>
+void radix_pass(cudaStream_t st, const KeyT *k_in, const uint32_t *v_in, KeyT *k_out,
+                uint32_t *v_out, int64_t n, int shift, int nbk, uint32_t *bh, uint32_t *rt,
+                const int32_t *gate) {
+    upsweep_kernel<KeyT><<<nbk, kThreads, 0, st>>>(k_in, n, shift, bh, nbk, gate);
+    rowscan_kernel<<<256, 1024, 0, st>>>(bh, nbk, rt, gate);
+    downsweep_kernel<KeyT><<<nbk, kThreads, 0, st>>>(k_in, v_in, n, shift, bh, rt, nbk, k_out, v_out,
+                                                     gate);
+}
 }  // namespace
 
 extern "C" size_t ivr_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t ntiles) {
-    return plan(n < 1 ? 1 : n, pair_capacity < 1 ? 1 : pair_capacity, ntiles).total;
+    return plan(n < 1 ? 1 : n, pair_capacity < 1 ? 1 : pair_capacity, ntiles < 1 ? 1 : ntiles).total;
 }
 
 extern "C" int ivr_bin_sort(int64_t n, const uint64_t *depth_key, const int32_t *count,
                             const uint16_t *rect, int32_t ntx, int32_t nty, int64_t pair_capacity,
                             void *workspace, size_t workspace_bytes, int32_t *pair_splat,
                             int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream) {
+    return ivr_bin_sort_cull(n, depth_key, count, rect, nullptr, ntx, nty, 0, 0, pair_capacity,
+                             workspace, workspace_bytes, pair_splat, tile_ranges, n_pairs, stream);
+}
+
+extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int32_t *count,
+                                 const uint16_t *rect, const float *rec, int32_t ntx, int32_t nty,
+                                 int32_t width, int32_t height, int64_t pair_capacity,
+                                 void *workspace, size_t workspace_bytes, int32_t *pair_splat,
+                                 int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int32_t ntiles = ntx * nty;
-    if (n < 0 || pair_capacity < 1 || ntx < 1 || nty < 1 || ntiles > 65535 || !tile_ranges ||
-        !n_pairs || !pair_splat || !workspace) {
+    if (n < 0 || pair_capacity < 1 || ntx < 1 || nty < 1 || ntiles > kMaxTiles || !tile_ranges ||
+        !n_pairs || !pair_splat || !workspace || (rec && (width < 1 || height < 1))) {
         ivr::set_error("ivr_bin_sort: bad argument");
         return IVR_ERR_ARG;
     }
@@ -425,7 +733,7 @@ extern "C" int ivr_bin_sort(int64_t n, const uint64_t *depth_key, const int32_t 
         ivr::set_error("ivr_bin_sort: sizes must fit int32");
         return IVR_ERR_ARG;
     }
-    const Layout L = plan(n < 1 ? 1 : n, pair_capacity, ntiles);
+    const Plan L = plan(n < 1 ? 1 : n, pair_capacity, ntiles);
     if (workspace_bytes < L.total) {
         ivr::set_error("ivr_bin_sort: workspace too small");
         return IVR_ERR_ARG;
@@ -436,68 +744,56 @@ extern "C" int ivr_bin_sort(int64_t n, const uint64_t *depth_key, const int32_t 
         return ivr::check_launch("ivr_bin_sort(empty)");
     }
     char *ws = (char *)workspace;
-    Bufs<uint64_t> DB{};
-    DB.in_keys = depth_key;
-    DB.in_vals = nullptr;
-    DB.keys[0] = (uint64_t *)(ws + L.off[0]);
-    DB.keys[1] = (uint64_t *)(ws + L.off[1]);
-    DB.vals[0] = (uint32_t *)(ws + L.off[2]);
-    DB.vals[1] = (uint32_t *)(ws + L.off[3]);
-    uint32_t *tkA = (uint32_t *)(ws + L.off[4]);
-    uint32_t *tkB = (uint32_t *)(ws + L.off[5]);
-    uint32_t *pvA = (uint32_t *)(ws + L.off[6]);
-    uint32_t *pvB = (uint32_t *)(ws + L.off[7]);
-    uint32_t *blockhist = (uint32_t *)(ws + L.off[8]);
-    uint32_t *rowtotal = (uint32_t *)(ws + L.off[9]);
-    uint32_t *hist64 = (uint32_t *)(ws + L.off[10]);
-    int32_t *skip = (int32_t *)(ws + L.off[11]);
-    int32_t *cur = (int32_t *)(ws + L.off[12]);
-    uint32_t *partial = (uint32_t *)(ws + L.off[13]);
+    uint32_t *ckA = (uint32_t *)(ws + L.off[0]), *ckB = (uint32_t *)(ws + L.off[1]);
+    uint32_t *vA = (uint32_t *)(ws + L.off[2]), *vB = (uint32_t *)(ws + L.off[3]);
+    uint64_t *fkA = (uint64_t *)(ws + L.off[4]), *fkB = (uint64_t *)(ws + L.off[5]);
+    uint32_t *roff = (uint32_t *)(ws + L.off[6]);
+    uint32_t *partial = (uint32_t *)(ws + L.off[7]);
+    uint32_t *bh = (uint32_t *)(ws + L.off[8]);
+    uint32_t *rt = (uint32_t *)(ws + L.off[9]);
+    uint32_t *phist = (uint32_t *)(ws + L.off[10]);
+    uint32_t *ttot = (uint32_t *)(ws + L.off[11]);
+    unsigned long long *mm = (unsigned long long *)(ws + L.off[12]);
+    int32_t *need_full = (int32_t *)(ws + L.off[13]);
+    const int nbk = L.nbk, nbp = L.nbp;
 
-    // ---- 1. stable depth sort (8 byte-passes, constant digits skipped)
-    const int nbk = (int)((n + kChunk - 1) / kChunk);
-    cudaMemsetAsync(hist64, 0, 4 * 8 * 256, st);
-    int hb = (int)((n + kThreads * 16 - 1) / (kThreads * 16));
-    hb = hb < 1 ? 1 : (hb > 1184 ? 1184 : hb);
-    key64_hist_kernel<<<hb, kThreads, 0, st>>>(depth_key, n, hist64);
-    pass_plan_kernel<<<1, 32, 0, st>>>(hist64, n, 8, skip, cur);
-    for (int p = 0; p < 8; ++p) {
-        upsweep_kernel<uint64_t><<<nbk, kThreads, 0, st>>>(DB, cur, skip, p, 8 * p, nullptr, n, n,
-                                                            blockhist, nbk);
-        rowscan_kernel<<<256, 1024, 0, st>>>(skip, p, blockhist, nbk, rowtotal);
-        downsweep_kernel<uint64_t><<<nbk, kThreads, 0, st>>>(DB, cur, skip, p, 8 * p, nullptr, n, n,
-                                                              blockhist, rowtotal, nbk, nullptr,
-                                                              nullptr);
-    }
-    // ---- 2. counts in rank order -> offsets -> emit pairs
-    scan_reduce_kernel<<<nbk, kThreads, 0, st>>>(DB, cur, 8, count, n, partial);
+    // ---- 1. depth ranks: 31-bit coarse keys, 4 stable passes, run fix-up
+    init_minmax_kernel<<<1, 1, 0, st>>>(mm, need_full);
+    int gb = (int)((n + kThreads * 8 - 1) / (kThreads * 8));
+    gb = gb < 1 ? 1 : (gb > 1184 ? 1184 : gb);
+    minmax_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm);
+    coarse_key_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm, ckA);
+    radix_pass<uint32_t>(st, ckA, nullptr, ckB, vB, n, 0, nbk, bh, rt, nullptr);
+    radix_pass<uint32_t>(st, ckB, vB, ckA, vA, n, 8, nbk, bh, rt, nullptr);
+    radix_pass<uint32_t>(st, ckA, vA, ckB, vB, n, 16, nbk, bh, rt, nullptr);
+    radix_pass<uint32_t>(st, ckB, vB, ckA, vA, n, 24, nbk, bh, rt, nullptr);
+    fixup_kernel<<<(int)((n + kThreads - 1) / kThreads), kThreads, 0, st>>>(ckA, vA, n, depth_key,
+                                                                           need_full);
+    // fallback (device-gated, normally an immediate return): full 64-bit sort into vA
+    fallback_sort_kernel<<<1, kFbThreads, 0, st>>>(depth_key, n, need_full, fkA, fkB, vA, vB);
+    // ---- 2. rank offsets
+    scan_reduce_kernel<<<nbk, kThreads, 0, st>>>(vA, count, n, partial);
     scan_partials_kernel<<<1, 1024, 0, st>>>(partial, nbk, n_pairs);
-    emit_kernel<<<nbk, kThreads, 0, st>>>(DB, cur, 8, count, (const ushort4 *)rect, n, partial, ntx,
-                                          pair_capacity, tkA, pvA);
-    // ---- 3. stable tile sort: (tkA, pvA) -> (tkB, pvB) -> (tkA, pair_splat)
-    const int nbp = (int)((pair_capacity + kChunk - 1) / kChunk);
-    {
-        Bufs<uint32_t> P0{};
-        P0.in_keys = tkA;
-        P0.in_vals = pvA;
-        upsweep_kernel<uint32_t><<<nbp, kThreads, 0, st>>>(P0, nullptr, nullptr, 0, 0, n_pairs, 0,
-                                                            pair_capacity, blockhist, nbp);
-        rowscan_kernel<<<256, 1024, 0, st>>>(nullptr, 0, blockhist, nbp, rowtotal);
-        downsweep_kernel<uint32_t><<<nbp, kThreads, 0, st>>>(P0, nullptr, nullptr, 0, 0, n_pairs, 0,
-                                                              pair_capacity, blockhist, rowtotal, nbp,
-                                                              tkB, pvB);
-        Bufs<uint32_t> P1{};
-        P1.in_keys = tkB;
-        P1.in_vals = pvB;
-        upsweep_kernel<uint32_t><<<nbp, kThreads, 0, st>>>(P1, nullptr, nullptr, 0, 8, n_pairs, 0,
-                                                            pair_capacity, blockhist, nbp);
-        rowscan_kernel<<<256, 1024, 0, st>>>(nullptr, 0, blockhist, nbp, rowtotal);
-        downsweep_kernel<uint32_t><<<nbp, kThreads, 0, st>>>(P1, nullptr, nullptr, 0, 8, n_pairs, 0,
-                                                              pair_capacity, blockhist, rowtotal, nbp,
-                                                              tkA, (uint32_t *)pair_splat);
-    }
-    // ---- 4. tile ranges
-    const int rb = (int)((pair_capacity + 1 + kThreads - 1) / kThreads);
-    ranges_kernel<<<rb, kThreads, 0, st>>>(tkA, n_pairs, pair_capacity, ntiles, tile_ranges);
+    scan_apply_kernel<<<nbk, kThreads, 0, st>>>(vA, count, n, partial, n_pairs, roff);
+    // ---- 3. counting placement by tile (+ optional tile cull flag)
+    PairCtx C{};
+    C.order = vA;
+    C.roff = roff;
+    C.rect = (const ushort4 *)rect;
+    C.rec = (const float4 *)rec;
+    C.n = n;
+    C.ntx = ntx;
+    C.ntiles = ntiles;
+    C.cap = pair_capacity;
+    C.n_pairs = n_pairs;
+    const size_t sm_hist = 4 * ((size_t)ntiles + kPairBlock + 1);
+    const size_t sm_place = 4 * ((size_t)kPairBlock + 1) + 2 * (size_t)kWarps * ntiles + 16;
+    cudaFuncSetAttribute(pair_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_hist);
+    cudaFuncSetAttribute(pair_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_place);
+    pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
+    rowscan_kernel<<<ntiles, 1024, 0, st>>>(phist, nbp, ttot, nullptr);
+    tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges);
+    pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, nbp, tile_ranges, pair_splat,
+                                                       width, height);
     return ivr::check_launch("ivr_bin_sort");
 }

@@ -137,8 +137,10 @@ class Workspace:
 class Frame:
     """Device outputs of one rasterization (kept alive for the backward)."""
 
-    def __init__(self):
-        self.__dict__.update({})
+    def pairs(self):
+        """The reference's per-tile pair list (pair_splat without the cull bit)."""
+        P = int(self.n_pairs.item())
+        return (self.pair_splat[:P] & 0x7fffffff).cpu().numpy()
 
 
 def preprocess(dg: DeviceGaussians, cam, K, cols, ws: Workspace, shading=None, edits=None,
@@ -206,13 +208,23 @@ def bin_sort(F: Frame, ws: Workspace, stream=None, capacity=None):
     F.tile_ranges = ws.get("tile_ranges", ntx * nty + 1, torch.int32)
     F.n_pairs = ws.get("n_pairs", 1, torch.int32)
     F.capacity = cap
-    L.check(L.lib().ivr_bin_sort(n, ptr(F.depth_key), ptr(F.count), ptr(F.rect), ntx, nty, cap,
-                                 ptr(scratch), nbytes, ptr(F.pair_splat), ptr(F.tile_ranges),
-                                 ptr(F.n_pairs), stream_handle(stream)), "ivr_bin_sort")
+    # K2 with the per-pair tile cull (bit 31 of pair_splat; masked in .pairs())
+    L.check(L.lib().ivr_bin_sort_cull(n, ptr(F.depth_key), ptr(F.count), ptr(F.rect), ptr(F.rec),
+                                      ntx, nty, cam.width, cam.height, cap, ptr(scratch), nbytes,
+                                      ptr(F.pair_splat), ptr(F.tile_ranges), ptr(F.n_pairs),
+                                      stream_handle(stream)), "ivr_bin_sort_cull")
+    F.preculled = True
+    F.tile_order = None
+    if ntx * nty <= 4096:
+        F.tile_order = ws.get("tile_order", ntx * nty, torch.int32)
+        L.check(L.lib().ivr_tile_order(ptr(F.tile_ranges), ntx * nty, ptr(F.tile_order),
+                                       stream_handle(stream)), "ivr_tile_order")
     return F
 
 
-def blend(F: Frame, ws: Workspace, want_state=True, stream=None, tile_order=None, out=None):
+def blend(F: Frame, ws: Workspace, want_state=True, stream=None, out=None, exact=False):
+    """Launch K3.  exact=True: bit-faithful float64 evaluation of every
+    candidate pair (IVR_BLEND_EXACT); otherwise certified float32 (FAST)."""
     cam = F.cam
     H, W, K = cam.height, cam.width, F.K
     dev = F.depth_key.device
@@ -228,12 +240,17 @@ def blend(F: Frame, ws: Workspace, want_state=True, stream=None, tile_order=None
     L.check(L.lib().ivr_blend_fwd(ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec),
                                   ptr(F.values), ptr(F.rec64), ptr(F.values64), K, W, H, ptr(F.out),
                                   ptr(F.out64), ptr(F.contrib), ptr(F.last_pos), ptr(F.t_final),
-                                  ptr(tile_order), stream_handle(stream)), "ivr_blend_fwd")
+                                  ptr(getattr(F, "tile_order", None)),
+                                  (L.BLEND_EXACT if exact else 0) |
+                                  (L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0),
+                                  stream_handle(stream)),
+            "ivr_blend_fwd")
+    F.exact = exact
     return F
 
 
 def rasterize_device(dg, cam, K, cols, ws, shading=None, edits=None, colors=None, attrs=(),
-                     f64=False, want_state=True, debug=False, stream=None):
+                     f64=False, want_state=True, debug=False, stream=None, exact=True):
     """K1 + K2 + K3 with pair-capacity overflow handling (synchronizes once to
     read the pair count)."""
     F = preprocess(dg, cam, K, cols, ws, shading, edits, colors, attrs, f64, debug, stream)
@@ -247,5 +264,5 @@ def rasterize_device(dg, cam, K, cols, ws, shading=None, edits=None, colors=None
         P = int(F.n_pairs.item())
     F.P = P
     F.empty = False
-    blend(F, ws, want_state, stream)
+    blend(F, ws, want_state, stream, exact=exact)
     return F

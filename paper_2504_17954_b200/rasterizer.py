@@ -80,13 +80,14 @@ def _unpack(out, layout, contrib):
 
 
 def rasterize_forward(geom, colors, cam, channels=("color", "alpha"), attrs=None,
-                      dtype=np.float32, sequential=False):
+                      dtype=np.float32, sequential=False, *, exact=True):
     """Rasterize on the GPU; returns (RenderOutput, state-for-backward).
 
     Same contract as rasterizer.py:53-164: ``colors`` are per-splat rgb
     already resolved for this camera, ``attrs`` maps names to (N,) or (N,k)
     values; outputs are deterministic (``sequential`` is accepted and has no
-    effect, exactly as in the reference)."""
+    effect, exactly as in the reference).  ``exact`` (extension) selects the
+    bit-faithful float64 blend (default) or the certified float32 blend."""
     del sequential
     dtype = np.dtype(dtype).type
     H, W = int(cam.height), int(cam.width)
@@ -105,7 +106,7 @@ def rasterize_forward(geom, colors, cam, channels=("color", "alpha"), attrs=None
     attrs_dev = [(D.to_dev(np.asarray(attrs[name], dtype=np.float64).reshape(n, w)), c, w)
                  for name, c, w in attr_cols]
     F = D.rasterize_device(dg, cam, K, cols, workspace(), colors=colors_dev, attrs=attrs_dev,
-                           f64=f64, want_state=True)
+                           f64=f64, want_state=True, exact=exact)
     out = (F.out64 if f64 else F.out).cpu().numpy().astype(dtype, copy=False)
     contrib = F.contrib.cpu().numpy()
     state.update(frame=F, dg=dg, empty=False)

@@ -256,12 +256,16 @@ class DeviceScene:
     def render_frame(self, cam, channels=("color", "alpha"), attrs=None, dtype=np.float32,
                      want_state=False, debug=False, light=None, lam=None, b=None,
                      palettes=None, opacity_scales=None, fast=False, out=None, stream=None,
-                     events=None):
+                     events=None, exact=None):
         """Enqueue one frame; returns the Frame of device tensors.
 
         fast=True skips the pair-count readback (no host sync): the pair
         capacity learned on earlier frames is reused and overflow must be
-        checked later with ``check_overflow(frame)``."""
+        checked later with ``check_overflow(frame)``.  exact=None picks the
+        certified float32 blend for fast frames and the bit-faithful float64
+        blend otherwise."""
+        if exact is None:
+            exact = not fast
         layout = _channel_layout(channels, attrs)
         cols, attr_cols, K = _cols(layout)
         shading, edits = self._tables(light, palettes, opacity_scales)
@@ -273,7 +277,7 @@ class DeviceScene:
         f64 = np.dtype(dtype) == np.float64
         if not fast or self.ws.pair_capacity == 0:
             F = D.rasterize_device(self.dg, cam, K, cols, self.ws, shading, edits, None, attrs_dev,
-                                   f64, want_state, debug, stream)
+                                   f64, want_state, debug, stream, exact=exact)
         else:
             if events:
                 events[0].record()
@@ -284,7 +288,7 @@ class DeviceScene:
             D.bin_sort(F, self.ws, stream)
             if events:
                 events[2].record()
-            D.blend(F, self.ws, want_state, stream, out=out)
+            D.blend(F, self.ws, want_state, stream, out=out, exact=exact)
             if events:
                 events[3].record()
             F.empty = False

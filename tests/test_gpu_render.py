@@ -62,15 +62,16 @@ def test_preprocess_matches_reference(case):
         assert np.nanmax(rel[d["valid"]]) < 1e-12, k
 
 
+@pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("case", CASES)
-def test_sort_and_image_match_reference(case):
+def test_sort_and_image_match_reference(case, exact):
     from paper_2504_17954_b200 import rasterize_forward
     d = golden(case)
-    out, st = rasterize_forward(_geom(d), d["rgb"], _cam(d), dtype=np.float32)
+    out, st = rasterize_forward(_geom(d), d["rgb"], _cam(d), dtype=np.float32, exact=exact)
     F = st["frame"]
     P = int(F.n_pairs.item())
     assert P == d["pair_splat"].size
-    assert np.array_equal(F.pair_splat[:P].cpu().numpy(), d["pair_splat"])
+    assert np.array_equal(F.pairs(), d["pair_splat"])
     assert np.array_equal(F.tile_ranges.cpu().numpy(), d["tile_ranges"])
     rec = F.rec.cpu().numpy().reshape(-1, 8)
     vis = np.zeros(len(d["depth"]), bool)
@@ -83,12 +84,15 @@ def test_sort_and_image_match_reference(case):
     assert np.abs(out.alpha - d["alpha"]).max() <= IMG_TOL
     assert np.array_equal(out.per_pixel_contrib_count, d["contrib"])
     assert np.array_equal(F.last_pos.cpu().numpy(), d["last_pos"])
-    exact = np.mean(out.color == d["color"])
-    assert exact > 0.999, exact
+    if exact:  # bit-faithful mode: every pixel identical to the reference
+        same = np.mean(out.color == d["color"])
+        assert same > 0.999, same
+    assert np.abs(F.t_final.cpu().numpy() - d["t_final"]).max() <= 1e-5
 
 
+@pytest.mark.parametrize("fast", [False, True])
 @pytest.mark.parametrize("case", CASES)
-def test_fused_shading_render(case):
+def test_fused_shading_render(case, fast):
     """K1 with fused Blinn-Phong shading vs reference render_composed."""
     from paper_2504_17954_b200 import (BasicSceneModel, ComposedScene, DeviceScene, Palette,
                                        ShadingAttributes)
@@ -100,9 +104,11 @@ def test_fused_shading_render(case):
     rgb = F.dbg["rgb"].cpu().numpy().reshape(-1, 3)
     rel = np.abs(rgb - d["rgb"]) / np.maximum(np.abs(d["rgb"]), 1e-300)
     assert rel.max() < 1e-12
-    out = ds.render(_cam(d))
-    assert np.abs(out.color - d["color"]).max() <= IMG_TOL
-    assert np.array_equal(out.per_pixel_contrib_count, d["contrib"])
+    for _ in range(2):  # second fast frame reuses the learned pair capacity
+        out = ds.render(_cam(d), fast=fast)
+        assert np.abs(out.color - d["color"]).max() <= IMG_TOL
+        assert np.abs(out.alpha - d["alpha"]).max() <= IMG_TOL
+        assert np.array_equal(out.per_pixel_contrib_count, d["contrib"])
 
 
 def _composed_scene(d):
@@ -159,14 +165,34 @@ def test_random_scenes_vs_oracle():
         rng = np.random.default_rng(seed)
         colors = rng.uniform(0, 1, (n, 3))
         geom = GaussianGeometry(a["mu"], a["q_raw"], a["log_s"], a["o_logit"], a["n_raw"])
-        for dtype in (np.float32, np.float64):
-            out, st = rasterize_forward(geom, colors, cam, dtype=dtype)
+        for dtype, exact in ((np.float32, True), (np.float64, True), (np.float32, False),
+                             (np.float64, False)):
+            out, st = rasterize_forward(geom, colors, cam, dtype=dtype, exact=exact)
             ref = O.rasterize(a["mu"], a["q_raw"], a["log_s"], a["o_logit"], a["n_raw"], colors,
                               cam, dtype=dtype)
             F = st["frame"]
-            P = int(F.n_pairs.item())
-            assert np.array_equal(F.pair_splat[:P].cpu().numpy(), ref["pair_splat"])
+            assert np.array_equal(F.pairs(), ref["pair_splat"])
             assert np.array_equal(F.tile_ranges.cpu().numpy(), ref["tile_ranges"])
             m = O.maps(ref)
             assert np.abs(out.color - m["color"]).max() <= IMG_TOL
             assert np.array_equal(out.per_pixel_contrib_count, ref["contrib"])
+
+
+def test_depth_sort_fallback_long_runs():
+    """Thousands of depths within ~100 ulps plus one far outlier collapse into
+    one 31-bit coarse bucket: the 64-bit fallback sort must keep lexsort order."""
+    import oracle as O
+    from paper_2504_17954_b200 import Camera, GaussianGeometry, rasterize_forward
+    rng = np.random.default_rng(3)
+    n = 3000
+    mu = np.column_stack([rng.uniform(-1, 1, n), rng.uniform(-1, 1, n), 1e-13 * rng.normal(size=n)])
+    mu[0] = (0.0, 0.0, 1e4)
+    geom = GaussianGeometry(mu, rng.normal(size=(n, 4)), np.full((n, 3), np.log(0.05)),
+                            rng.normal(size=n), rng.normal(size=(n, 3)))
+    cam = Camera.look_at((0.0, 0.0, -4.0), (0.0, 0.0, 0.0), np.pi / 3, 96, 64)
+    colors = rng.uniform(0, 1, (n, 3))
+    out, st = rasterize_forward(geom, colors, cam)
+    ref = O.rasterize(geom.mu, geom.q_raw, geom.log_s, geom.o_logit, geom.n_raw, colors, cam)
+    assert np.array_equal(st["frame"].pairs(), ref["pair_splat"])
+    assert np.array_equal(st["frame"].tile_ranges.cpu().numpy(), ref["tile_ranges"])
+    assert np.array_equal(out.per_pixel_contrib_count, ref["contrib"])
