@@ -33,6 +33,10 @@ sys.path.insert(0, REPO)
 METRIC = "800x800 render FPS (composed 1M Gaussians), train it/s, % HBM roofline, 1-8 GPU"
 W_IMG = H_IMG = 800
 PER_MODEL, N_MODELS, DENSITY = 200_000, 5, 1_000_000
+# our kernels per frame: K1 (1) + K2 (init, minmax, coarse key, 4x3 radix, fix-up,
+# fallback gate, 3 scan, tile hist, tile rowscan, tile ranges, placement, tile order
+# = 25) + K3 (1)
+LAUNCHES_PER_FRAME = 27
 
 
 def parse():
@@ -294,7 +298,7 @@ def run_ours(args):
                 "e2e": {"value": e2e_fps, "unit": "frames/s",
                         "h2d_bytes_per_step": ds.h2d_bytes_per_frame(),
                         "d2h_bytes_per_step": H_IMG * W_IMG * (4 * 4 + 4)},
-                "gpu_launches": 38 * args.steps, "overflow": overflow}
+                "gpu_launches": LAUNCHES_PER_FRAME * args.steps, "overflow": overflow}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
