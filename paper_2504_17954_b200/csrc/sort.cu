@@ -12,14 +12,14 @@
 //     run is longer than kMaxRun the whole order is recomputed with a full
 //     64-bit LSD sort (8 passes) -- correctness never depends on the data.
 //     Ties keep index order = lexsort's tie break on fill_pairs' order.
-//  2. rank offsets: exclusive scan of the per-splat tile counts in rank order
-//     (total = P).
-//  3. counting placement: pairs are enumerated in rank order (pair p belongs
-//     to the rank r with roff[r] <= p < roff[r+1]); per 8192-pair block a
-//     per-tile histogram is built, scanned per tile across blocks, and each
-//     pair is written once to tile_start[t] + block offset + its stable rank
-//     inside the block (warp match_any ranking).  Tile ranges are the
-//     exclusive scan of the tile totals.
+//  2. P = sum of the per-splat tile counts.
+//  3. counting placement: each block owns 2048 consecutive depth ranks; its
+//     warps expand their ranks' pairs in fill_pairs order (load-balanced
+//     warp expansion, no per-pair global searches), build a per-tile
+//     histogram that is scanned per tile across blocks, and write each pair
+//     once to tile_start[t] + block offset + its stable rank inside the block
+//     (warp match_any ranking).  Tile ranges are the exclusive scan of the
+//     tile totals.
 //  4. optional tile cull: while placing, each pair is tested in float64 for
 //     whether its splat can reach alpha >= 1/255 anywhere in the tile; pairs
 //     that cannot are marked with bit 31 (pair_splat & 0x7fffffff is the
@@ -36,8 +36,6 @@ constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 8;                  // per thread in radix passes
 constexpr int kChunk = kThreads * kItems;  // 2048 keys per radix block
 constexpr int kRadix = 256;
-constexpr int kPairBlock = 8192;           // pairs per placement block
-constexpr int kPairPerWarp = kPairBlock / kWarps;
 constexpr int kMaxRun = 64;
 constexpr uint32_t kInvisible = 0xffffffffu;
 constexpr int kMaxTiles = 8192;  // placement keeps 8 x ntiles uint16 counters in smem
@@ -425,53 +423,19 @@ scan_partials_kernel(uint32_t *partial, int nb, int32_t *n_pairs) {
     if (threadIdx.x == 0) *n_pairs = carry > 0x7fffffffull ? 0x7fffffff : (int32_t)carry;
 }
 
-// roff[r] = exclusive prefix of count[order[r]] (blocked: thread t owns 8 ranks)
-__global__ void __launch_bounds__(kThreads)
-scan_apply_kernel(const uint32_t *order, const int32_t *count, int64_t n,
-                  const uint32_t *partial, const int32_t *n_pairs, uint32_t *roff) {
-    __shared__ uint32_t s_warp[kWarps];
-    const int64_t base = (int64_t)blockIdx.x * kChunk;
-    uint32_t c[kItems];
-    uint32_t sum = 0;
-#pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const int64_t idx = base + (int64_t)threadIdx.x * kItems + r;
-        c[r] = idx < n ? (uint32_t)count[order[idx]] : 0u;
-        sum += c[r];
-    }
-    uint32_t tot;
-    const uint32_t incl = block_incl_scan(sum, s_warp, tot);
-    uint32_t off = partial[blockIdx.x] + incl - sum;
-#pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const int64_t idx = base + (int64_t)threadIdx.x * kItems + r;
-        if (idx < n) roff[idx] = off;
-        off += c[r];
-    }
-    if (blockIdx.x == 0 && threadIdx.x == 0) roff[n] = (uint32_t)*n_pairs;
-}
-
 // ----------------------------------------------------------------- placement
+constexpr int kRanksPerWarp = 256;
+constexpr int kRanksPerBlock = kRanksPerWarp * kWarps;  // 2048 ranks per block
+
 struct PairCtx {
     const uint32_t *order;  // rank -> splat
-    const uint32_t *roff;   // rank -> first pair (n+1 entries)
-    const ushort4 *rect;
-    const float4 *rec;      // blend records (for the tile cull), may be null
+    const int32_t *count;   // splat -> tiles touched
+    const ushort4 *rect;    // splat -> tile rect
+    const float4 *rec;      // blend records (tile cull), may be null
     int64_t n;
     int ntx, ntiles;
     int64_t cap;
-    const int32_t *n_pairs;
 };
-
-// last rank r with roff[r] <= p (zero-count ranks share offsets with the next)
-__device__ __forceinline__ int64_t rank_of(const uint32_t *roff, int64_t lo, int64_t hi, uint32_t p) {
-    // invariant: roff[lo] <= p < roff[hi] (hi may be n with roff[n] = P)
-    while (hi - lo > 1) {
-        const int64_t m = (lo + hi) >> 1;
-        if (roff[m] <= p) lo = m; else hi = m;
-    }
-    return lo;
-}
 
 __device__ __forceinline__ bool tile_cull64(const float4 r0, const float4 r1, int px0, int px1,
                                             int py0, int py1) {
@@ -501,58 +465,75 @@ __device__ __forceinline__ bool tile_cull64(const float4 r0, const float4 r1, in
     return best > hi;
 }
 
-// Pair p -> (splat, tile); returns false past the end.
-__device__ __forceinline__ bool pair_at(const PairCtx &C, const uint32_t *s_roff, int64_t r0,
-                                        int64_t r1, int64_t P, int64_t p, uint32_t &splat,
-                                        int &tile, int &tx, int &ty) {
-    if (p >= P) return false;
-    const int64_t r = r0 + rank_of(s_roff, 0, r1 - r0, (uint32_t)p);
-    const uint32_t q = (uint32_t)p - s_roff[r - r0];
-    splat = C.order[r];
-    const ushort4 rc = C.rect[splat];
-    const uint32_t w = (uint32_t)(rc.y - rc.x + 1);
-    ty = rc.z + (int)(q / w);
-    tx = rc.x + (int)(q % w);
-    tile = ty * C.ntx + tx;
-    return true;
-}
-
-// Loads the rank offsets covering this block's pairs into shared memory.
-__device__ __forceinline__ void block_ranks(const PairCtx &C, int64_t p0, int64_t P,
-                                            uint32_t *s_roff, int64_t &r0, int64_t &r1) {
-    __shared__ int64_t s_r[2];
-    if (threadIdx.x == 0) {
-        const int64_t pl = (p0 + kPairBlock < P ? p0 + kPairBlock : P) - 1;
-        s_r[0] = rank_of(C.roff, 0, C.n, (uint32_t)p0);
-        s_r[1] = rank_of(C.roff, 0, C.n, (uint32_t)pl) + 1;
+// Warp-cooperative, load-balanced expansion of the pairs of ranks
+// [rbase, rend) in fill_pairs order (rank-major, then ty, then tx): each lane
+// owns one rank of a 32-rank group; the group's pairs are visited 32 at a
+// time, every lane finding its owner rank with a 5-step shuffle search over
+// the group's inclusive count prefix.  f(ok, splat, tile, tx, ty) is called
+// by all 32 lanes for each 32-pair chunk (convergent; ok marks real pairs).
+template <typename Fn>
+__device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, int64_t rend, Fn &&f) {
+    const int lane = threadIdx.x & 31;
+    for (int64_t g = rbase; g < rend; g += 32) {
+        const int64_t r = g + lane;
+        uint32_t sp = 0, cnt = 0, rx = 0, rz = 0;
+        if (r < rend) {
+            sp = C.order[r];
+            cnt = (uint32_t)C.count[sp];
+            if (cnt) {
+                const ushort4 rc = C.rect[sp];
+                rx = (uint32_t)rc.x | ((uint32_t)rc.y << 16);
+                rz = (uint32_t)rc.z | ((uint32_t)rc.w << 16);
+            }
+        }
+        uint32_t incl = cnt;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, incl, o);
+            if (lane >= o) incl += y;
+        }
+        const uint32_t G = __shfl_sync(0xffffffffu, incl, 31);
+        if (G == 0) break;  // invisible ranks (count 0) sort last: nothing further
+        const uint32_t excl = incl - cnt;
+        for (uint32_t k0 = 0; k0 < G; k0 += 32) {
+            const uint32_t k = k0 + lane;
+            int owner = 0;
+#pragma unroll
+            for (int step = 16; step >= 1; step >>= 1) {
+                const uint32_t v = __shfl_sync(0xffffffffu, incl, owner + step - 1);
+                if (v <= k) owner += step;
+            }
+            const uint32_t o_excl = __shfl_sync(0xffffffffu, excl, owner);
+            const uint32_t o_sp = __shfl_sync(0xffffffffu, sp, owner);
+            const uint32_t o_rx = __shfl_sync(0xffffffffu, rx, owner);
+            const uint32_t o_rz = __shfl_sync(0xffffffffu, rz, owner);
+            const bool ok = k < G;
+            const uint32_t q = k - o_excl;
+            const uint32_t tx0 = o_rx & 0xffffu, tx1 = o_rx >> 16, ty0 = o_rz & 0xffffu;
+            const uint32_t w = tx1 - tx0 + 1;
+            const int ty = ok ? (int)(ty0 + q / w) : 0;
+            const int tx = ok ? (int)(tx0 + q % w) : 0;
+            f(ok, o_sp, ok ? ty * C.ntx + tx : -1, tx, ty);
+        }
     }
-    __syncthreads();
-    r0 = s_r[0];
-    r1 = s_r[1];
-    for (int64_t i = threadIdx.x; i <= r1 - r0; i += blockDim.x) s_roff[i] = C.roff[r0 + i];
-    __syncthreads();
 }
 
 // per-block tile histogram -> hist[tile * nblocks + block]
 __global__ void __launch_bounds__(kThreads)
 pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
     extern __shared__ uint32_t smem_u32[];
-    uint32_t *s_cnt = smem_u32;                 // ntiles
-    uint32_t *s_roff = smem_u32 + C.ntiles;     // <= kPairBlock + 1
-    const int64_t P = load_n(C.n_pairs, 0, C.cap);
-    const int64_t p0 = (int64_t)blockIdx.x * kPairBlock;
+    uint32_t *s_cnt = smem_u32;  // ntiles
     for (int t = threadIdx.x; t < C.ntiles; t += kThreads) s_cnt[t] = 0;
     __syncthreads();
-    if (p0 < P) {
-        int64_t r0, r1;
-        block_ranks(C, p0, P, s_roff, r0, r1);
-        for (int k = threadIdx.x; k < kPairBlock; k += kThreads) {
-            uint32_t sp;
-            int tile, tx, ty;
-            if (pair_at(C, s_roff, r0, r1, P, p0 + k, sp, tile, tx, ty)) atomicAdd(&s_cnt[tile], 1u);
-        }
-        __syncthreads();
-    }
+    const int warp = threadIdx.x >> 5;
+    const uint32_t lt = lanemask_lt();
+    const int64_t rb = (int64_t)blockIdx.x * kRanksPerBlock + (int64_t)warp * kRanksPerWarp;
+    const int64_t re = rb + kRanksPerWarp < C.n ? rb + kRanksPerWarp : C.n;
+    expand_pairs(C, rb, re, [&](bool ok, uint32_t, int tile, int, int) {
+        const uint32_t peers = __match_any_sync(0xffffffffu, tile);
+        if (ok && (peers & lt) == 0) atomicAdd(&s_cnt[tile], (uint32_t)__popc(peers));
+    });
+    __syncthreads();
     for (int t = threadIdx.x; t < C.ntiles; t += kThreads)
         hist[(int64_t)t * nblocks + blockIdx.x] = s_cnt[t];
 }
@@ -590,34 +571,27 @@ tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges) {
     if (threadIdx.x == 0) ranges[ntiles] = (int32_t)carry;
 }
 
-// stable placement: each warp owns a contiguous 1024-pair sub-range
+// stable placement: warp w of block b owns ranks [b*2048 + w*256, +256)
 __global__ void __launch_bounds__(kThreads)
 pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *ranges,
                   int32_t *pair_splat, int W, int H) {
     extern __shared__ uint32_t smem_u32[];
-    uint32_t *s_roff = smem_u32;                                     // kPairBlock + 1
-    uint16_t *s_wc = reinterpret_cast<uint16_t *>(smem_u32 + kPairBlock + 1);  // [warp][ntiles]
-    const int64_t P = load_n(C.n_pairs, 0, C.cap);
-    const int64_t p0 = (int64_t)blockIdx.x * kPairBlock;
-    if (p0 >= P) return;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    uint16_t *s_wc = reinterpret_cast<uint16_t *>(smem_u32);  // [warp][ntiles]
+    const int tid = threadIdx.x, warp = tid >> 5;
     for (int i = tid; i < kWarps * C.ntiles; i += kThreads) s_wc[i] = 0;
-    int64_t r0, r1;
-    block_ranks(C, p0, P, s_roff, r0, r1);
+    __syncthreads();
     uint16_t *wc = s_wc + warp * C.ntiles;
     const uint32_t lt = lanemask_lt();
-    const int64_t wbase = p0 + (int64_t)warp * kPairPerWarp;
-    // phase 1: per-warp tile counts
-    for (int k = 0; k < kPairPerWarp; k += 32) {
-        uint32_t sp;
-        int tile = -1, tx, ty;
-        const bool ok = pair_at(C, s_roff, r0, r1, P, wbase + k + lane, sp, tile, tx, ty);
-        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? tile : -1);
+    const int64_t rb = (int64_t)blockIdx.x * kRanksPerBlock + (int64_t)warp * kRanksPerWarp;
+    const int64_t re = rb + kRanksPerWarp < C.n ? rb + kRanksPerWarp : C.n;
+    // phase 1: per-warp tile counts (<= 256 per tile per warp)
+    expand_pairs(C, rb, re, [&](bool ok, uint32_t, int tile, int, int) {
+        const uint32_t peers = __match_any_sync(0xffffffffu, tile);
         if (ok && (peers & lt) == 0) wc[tile] = (uint16_t)(wc[tile] + __popc(peers));
         __syncwarp();
-    }
+    });
     __syncthreads();
-    // phase 2: exclusive scan across warps, per tile
+    // phase 2: exclusive scan across warps, per tile (block total <= 2048)
     for (int t = tid; t < C.ntiles; t += kThreads) {
         uint32_t run = 0;
 #pragma unroll
@@ -629,29 +603,29 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
     }
     __syncthreads();
     // phase 3: place (and cull-flag) every pair
-    for (int k = 0; k < kPairPerWarp; k += 32) {
-        uint32_t sp = 0;
-        int tile = -1, tx = 0, ty = 0;
-        const bool ok = pair_at(C, s_roff, r0, r1, P, wbase + k + lane, sp, tile, tx, ty);
-        const uint32_t peers = __match_any_sync(0xffffffffu, ok ? tile : -1);
+    expand_pairs(C, rb, re, [&](bool ok, uint32_t sp, int tile, int tx, int ty) {
+        const uint32_t peers = __match_any_sync(0xffffffffu, tile);
         uint32_t before = 0;
         if (ok) before = wc[tile];
         __syncwarp();
         if (ok && (peers & lt) == 0) wc[tile] = (uint16_t)(before + __popc(peers));
         __syncwarp();
         if (ok) {
-            const uint32_t pos = (uint32_t)ranges[tile] + hist[(int64_t)tile * nblocks + blockIdx.x] +
-                                 before + __popc(peers & lt);
-            uint32_t v = sp;
-            if (C.rec) {
-                const int px0 = tx * kTile, py0 = ty * kTile;
-                const int px1 = min(px0 + kTile - 1, W - 1), py1 = min(py0 + kTile - 1, H - 1);
-                const float4 a0 = __ldg(C.rec + 2 * sp), a1 = __ldg(C.rec + 2 * sp + 1);
-                if (tile_cull64(a0, a1, px0, px1, py0, py1)) v |= 0x80000000u;
+            const uint32_t pos = (uint32_t)ranges[tile] +
+                                 hist[(int64_t)tile * nblocks + blockIdx.x] + before +
+                                 __popc(peers & lt);
+            if ((int64_t)pos < C.cap) {
+                uint32_t v = sp;
+                if (C.rec) {
+                    const int px0 = tx * kTile, py0 = ty * kTile;
+                    const int px1 = min(px0 + kTile - 1, W - 1), py1 = min(py0 + kTile - 1, H - 1);
+                    const float4 a0 = __ldg(C.rec + 2 * sp), a1 = __ldg(C.rec + 2 * sp + 1);
+                    if (tile_cull64(a0, a1, px0, px1, py0, py1)) v |= 0x80000000u;
+                }
+                pair_splat[pos] = (int32_t)v;
             }
-            pair_splat[pos] = (int32_t)v;
         }
-    }
+    });
 }
 
 }  // namespace sortk
@@ -671,12 +645,12 @@ struct Plan {
 Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
     Plan L{};
     L.nbk = (int)((n + kChunk - 1) / kChunk);
-    L.nbp = (int)((cap + kPairBlock - 1) / kPairBlock);
+    L.nbp = (int)((n + kRanksPerBlock - 1) / kRanksPerBlock);
     size_t sz[16] = {
         al(4 * (size_t)n), al(4 * (size_t)n),                    // 0,1 coarse keys A/B
         al(4 * (size_t)n), al(4 * (size_t)n),                    // 2,3 vals A/B
         al(8 * (size_t)n), al(8 * (size_t)n),                    // 4,5 full keys (fallback) A/B
-        al(4 * (size_t)(n + 1)),                                 // 6 rank offsets
+        al(4),                                                   // 6 (unused)
         al(4 * (size_t)(L.nbk + 1)),                             // 7 scan partials
         al(4 * (size_t)256 * (L.nbk + 1)),                       // 8 radix blockhist
         al(4 * 256),                                             // 9 radix rowtotal
@@ -747,7 +721,6 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     uint32_t *ckA = (uint32_t *)(ws + L.off[0]), *ckB = (uint32_t *)(ws + L.off[1]);
     uint32_t *vA = (uint32_t *)(ws + L.off[2]), *vB = (uint32_t *)(ws + L.off[3]);
     uint64_t *fkA = (uint64_t *)(ws + L.off[4]), *fkB = (uint64_t *)(ws + L.off[5]);
-    uint32_t *roff = (uint32_t *)(ws + L.off[6]);
     uint32_t *partial = (uint32_t *)(ws + L.off[7]);
     uint32_t *bh = (uint32_t *)(ws + L.off[8]);
     uint32_t *rt = (uint32_t *)(ws + L.off[9]);
@@ -771,25 +744,25 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
                                                                            need_full);
     // fallback (device-gated, normally an immediate return): full 64-bit sort into vA
     fallback_sort_kernel<<<1, kFbThreads, 0, st>>>(depth_key, n, need_full, fkA, fkB, vA, vB);
-    // ---- 2. rank offsets
+    // ---- 2. pair count P (sum of tile counts) -> n_pairs
     scan_reduce_kernel<<<nbk, kThreads, 0, st>>>(vA, count, n, partial);
     scan_partials_kernel<<<1, 1024, 0, st>>>(partial, nbk, n_pairs);
-    scan_apply_kernel<<<nbk, kThreads, 0, st>>>(vA, count, n, partial, n_pairs, roff);
     // ---- 3. counting placement by tile (+ optional tile cull flag)
     PairCtx C{};
     C.order = vA;
-    C.roff = roff;
+    C.count = count;
     C.rect = (const ushort4 *)rect;
     C.rec = (const float4 *)rec;
     C.n = n;
     C.ntx = ntx;
     C.ntiles = ntiles;
     C.cap = pair_capacity;
-    C.n_pairs = n_pairs;
-    const size_t sm_hist = 4 * ((size_t)ntiles + kPairBlock + 1);
-    const size_t sm_place = 4 * ((size_t)kPairBlock + 1) + 2 * (size_t)kWarps * ntiles + 16;
-    cudaFuncSetAttribute(pair_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_hist);
-    cudaFuncSetAttribute(pair_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_place);
+    const size_t sm_hist = 4 * (size_t)ntiles;
+    const size_t sm_place = 2 * (size_t)kWarps * ntiles;
+    if (sm_hist > 48 * 1024)
+        cudaFuncSetAttribute(pair_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_hist);
+    if (sm_place > 48 * 1024)
+        cudaFuncSetAttribute(pair_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_place);
     pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
     rowscan_kernel<<<ntiles, 1024, 0, st>>>(phist, nbp, ttot, nullptr);
     tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges);

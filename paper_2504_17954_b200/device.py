@@ -7,6 +7,7 @@ stream; every compute step is a ``libivrgs.so`` call (include/ivrgs.h).
 from __future__ import annotations
 
 import ctypes
+import os
 
 import numpy as np
 import torch
@@ -215,7 +216,7 @@ def bin_sort(F: Frame, ws: Workspace, stream=None, capacity=None):
                                       stream_handle(stream)), "ivr_bin_sort_cull")
     F.preculled = True
     F.tile_order = None
-    if ntx * nty <= 4096:
+    if ntx * nty <= 4096 and os.environ.get("IVR_TILE_ORDER", "1") != "0":
         F.tile_order = ws.get("tile_order", ntx * nty, torch.int32)
         L.check(L.lib().ivr_tile_order(ptr(F.tile_ranges), ntx * nty, ptr(F.tile_order),
                                        stream_handle(stream)), "ivr_tile_order")
