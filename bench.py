@@ -277,6 +277,8 @@ def run_ours(args):
                 "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
                 "peak_source": peak_src,
                 "stage_ms": {nm: float(v) for nm, v in zip(names, stage_ms)},
+                "frame_ms_min_med_max": [float(frame_ms.min()), float(np.median(frame_ms)),
+                                         float(frame_ms.max())],
                 "alg_bytes": {nm: int(v) for nm, v in zip(names, alg)}}
 
     cpu = None

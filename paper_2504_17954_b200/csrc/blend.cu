@@ -3,27 +3,28 @@
 // Replaces _kernels.composite_forward (_kernels.py:31-72).  One CTA per 16x16
 // tile (tiles launched heaviest-first when a tile order is given), one thread
 // per pixel.  The tile's depth-sorted pair list is streamed through shared
-// memory in batches of 256 pairs; while a batch is staged each thread tests
-// one pair against the whole tile in float64 (minimum of the Gaussian exponent
-// over the tile rectangle) and culls pairs the reference's alpha test rejects
-// at every pixel of the tile.  Survivors are compacted in list order (warp
-// ballots), so each pixel walks exactly the reference list minus provably
-// skipped pairs, and the CTA retires once every pixel has passed T < 1e-4.
+// memory in batches of 256 pairs.  Pairs that provably stay below alpha 1/255
+// over the whole tile are skipped without loading their records (bit 31 set
+// by ivr_bin_sort_cull, or -- without that flag -- a float64 minimum of the
+// exponent over the tile rectangle evaluated while staging).  Survivors are
+// compacted in list order (warp ballots), so each pixel walks exactly the
+// reference list minus provably skipped pairs; the CTA retires as soon as
+// every pixel has passed T < 1e-4.
 //
 // Decisions (sigma < 0, alpha < 1/255, T < 1e-4) must match the reference's
-// float64 arithmetic exactly -- a flipped alpha-skip moves a pixel by
+// float64 arithmetic exactly: a flipped alpha-skip moves a pixel by
 // ~T/255 >> 1e-4 (SURVEY.md finding 4).  Two modes:
 //  * EXACT: every non-skipped pair is re-evaluated with the reference's
 //    float64 arithmetic (separately rounded, exp, cap, skip, T *= 1-alpha,
 //    float32 accumulation rounding) -> bit-faithful images.
-//  * FAST: the exponent is evaluated in float32 together with a rigorous
+//  * FAST: the exponent is evaluated in float32 with a rigorous
 //    per-evaluation error bound E.  Pairs certainly on one side of the
-//    alpha-skip threshold use float32 alpha; only pairs inside the +-E band
-//    take the exact float64 path.  T is tracked in float32 with a running
-//    relative error bound; if T lands inside its band around 1e-4 the pixel
-//    is replayed in EXACT mode.  Decisions therefore still match the
-//    reference; only the accumulated values carry float32 rounding
-//    (~1e-6, tolerance 1e-4).
+//    alpha-skip threshold take float32 alpha; only pairs inside the band take
+//    the exact float64 path.  T is tracked in float32 with a running relative
+//    error bound; a pixel whose T lands inside its band around 1e-4 is
+//    flagged, and the CTA re-walks its list once in EXACT mode for the
+//    flagged pixels only.  Decisions therefore match the reference; values
+//    carry float32 rounding (~1e-6 against the 1e-4 tolerance).
 #include <math.h>
 
 #include "ivr_common.cuh"
@@ -33,6 +34,10 @@ namespace ivr {
 constexpr int kBlendThreads = 256;
 constexpr int kModeExact = 0;
 constexpr int kModeFast = 1;
+// |sigma32 - sigma_ref| <= kSigmaErr * (|a/2 dx^2| + |b dx dy| + |c/2 dy^2|):
+// 5 roundings per term + dx/dy rounding (5.1 ulp) + float32 conic rounding in
+// dtype=float64 mode (1 ulp), with slack: 6.7 ulp of 2^-24.
+constexpr float kSigmaErr = 4.0e-7f;
 
 // Can splat (record r0, r1) reach alpha >= 1/255 anywhere in the pixel
 // rectangle [px0, px1] x [py0, py1]?  Conservative: true unless the float64
@@ -78,219 +83,190 @@ __device__ __forceinline__ double exact_alpha(double dpx, double dpy, double mx,
     return al;
 }
 
-// EXACT replay of one pixel over its whole tile list (global memory).  Used
-// by FAST mode when T lands in its ambiguity band around T_STOP.
+struct BlendArgs {
+    const int32_t *ranges;
+    const int32_t *pair_splat;
+    int ntx;
+    const float4 *rec;
+    const float *values;
+    const double *rec64;
+    const double *values64;
+    int K, W, H;
+    float *out;
+    double *out64;
+    int32_t *contrib, *last_pos;
+    double *t_final;
+    const int32_t *tile_order;
+    int preculled;
+};
+
 template <int KMAX, bool F64>
-__device__ void replay_pixel(int s0, int s1, const int32_t *__restrict__ pair_splat,
-                             const float4 *__restrict__ rec, const float *__restrict__ values,
-                             const double *__restrict__ rec64, const double *__restrict__ values64,
-                             int K, int px, int py, float *acc, double *acc64, double &T, int &nc,
-                             int &last) {
-    const double dpx = px, dpy = py;
-    const float fpx = px, fpy = py;
-    T = 1.0;
-    nc = 0;
-    last = s0;
-#pragma unroll
-    for (int c = 0; c < KMAX; ++c) acc[c] = 0.0f;
-#pragma unroll
-    for (int c = 0; c < (F64 ? KMAX : 1); ++c) acc64[c] = 0.0;
-    for (int j = s0; j < s1; ++j) {
-        const int sp = pair_splat[j];
-        if (sp < 0) continue;  // culled for the whole tile (never contributes)
-        const float4 a0 = __ldg(rec + 2 * sp), a1 = __ldg(rec + 2 * sp + 1);
-        const float dx = fpx - a0.x, dy = fpy - a0.y;
-        const float sig = fmaf(fmaf(a1.x, dx, a1.y * dy), dx, (a1.z * dy) * dy);
-        if (sig > a0.w) continue;
-        double al;
-        if (F64) {
-            const double *r = rec64 + 8 * (int64_t)sp;
-            al = exact_alpha(dpx, dpy, r[0], r[1], r[2], r[3], r[4], r[5]);
-        } else {
-            al = exact_alpha(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y, 2.0 * (double)a1.z, a0.z);
-        }
-        if (al < 0.0) continue;
-        const double w = dmul(T, al);
-        if (F64) {
-            for (int c = 0; c < K; ++c) acc64[c] = dadd(acc64[c], dmul(w, values64[(int64_t)K * sp + c]));
-        } else {
-#pragma unroll
-            for (int c = 0; c < KMAX; ++c)
-                if (c < K) acc[c] = (float)dadd((double)acc[c], dmul(w, (double)__ldg(values + (int64_t)K * sp + c)));
-        }
-        T = dmul(T, dsub(1.0, al));
-        ++nc;
-        last = j + 1;
-        if (T < kTStop) break;
-    }
-}
-
-template <int KMAX, bool F64, int MODE>
-__global__ void __launch_bounds__(kBlendThreads, 3)
-blend_fwd_kernel(const int32_t *__restrict__ ranges, const int32_t *__restrict__ pair_splat,
-                 int ntx, const float4 *__restrict__ rec, const float *__restrict__ values,
-                 const double *__restrict__ rec64, const double *__restrict__ values64, int K,
-                 int W, int H, float *__restrict__ out, double *__restrict__ out64,
-                 int32_t *__restrict__ contrib, int32_t *__restrict__ last_pos,
-                 double *__restrict__ t_final, const int32_t *__restrict__ tile_order,
-                 int preculled) {
-    extern __shared__ __align__(16) unsigned char smem[];
-    constexpr bool kStage64 = F64 && MODE == kModeExact;
-    constexpr bool kStageMean64 = F64 && MODE == kModeFast;
-    float4 *s_r0 = reinterpret_cast<float4 *>(smem);
-    float4 *s_r1 = s_r0 + kBlendThreads;
-    int *s_j = reinterpret_cast<int *>(s_r1 + kBlendThreads);
-    int *s_sp = s_j + kBlendThreads;
-    float *s_v = reinterpret_cast<float *>(s_sp + kBlendThreads);
-    double *s_r64 = reinterpret_cast<double *>(s_v + kBlendThreads * KMAX);  // 6/pair
-    double *s_v64 = s_r64 + (kStage64 ? 6 * kBlendThreads : (kStageMean64 ? 2 * kBlendThreads : 0));
-    __shared__ int s_wsum[kBlendThreads / 32];
-
-    const int tile = tile_order ? tile_order[blockIdx.x] : (int)blockIdx.x;
-    const int tx = tile % ntx, ty = tile / ntx;
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int px = tx * kTile + (tid & 15), py = ty * kTile + (tid >> 4);
-    const bool inside = px < W && py < H;
-    const int s0 = ranges[tile], s1 = ranges[tile + 1];
-    const int px0 = tx * kTile, py0 = ty * kTile;
-    const int px1 = min(px0 + kTile - 1, W - 1), py1 = min(py0 + kTile - 1, H - 1);
-    const float fpx = (float)px, fpy = (float)py;
-    const double dpx = (double)px, dpy = (double)py;
-
-    double T = 1.0;     // EXACT mode transmittance (float64, reference arithmetic)
-    float Tf = 1.0f;    // FAST mode transmittance
-    float errT = 0.0f;  // FAST: bound on |Tf - T_ref| / T_ref
+struct PixelState {
+    double T;     // EXACT: float64 transmittance (reference arithmetic)
+    float Tf;     // FAST: float32 transmittance
+    float errT;   // FAST: bound on |Tf / T_ref - 1|
     float acc[KMAX];
     double acc64[F64 ? KMAX : 1];
-#pragma unroll
-    for (int c = 0; c < KMAX; ++c) acc[c] = 0.0f;
-#pragma unroll
-    for (int c = 0; c < (F64 ? KMAX : 1); ++c) acc64[c] = 0.0;
-    int nc = 0, last = s0;
-    bool done = !inside, replay = false;
+    int nc, last;
+    bool done, replay;
 
+    __device__ __forceinline__ void reset(int s0, bool done0) {
+        T = 1.0;
+        Tf = 1.0f;
+        errT = 0.0f;
+#pragma unroll
+        for (int c = 0; c < KMAX; ++c) acc[c] = 0.0f;
+#pragma unroll
+        for (int c = 0; c < (F64 ? KMAX : 1); ++c) acc64[c] = 0.0;
+        nc = 0;
+        last = s0;
+        done = done0;
+        replay = false;
+    }
+};
+
+struct Smem {
+    float4 *r0, *r1;
+    int *j, *sp;
+    float *v;
+    double *r64;  // F64: 6 per pair (mx, my, a, b, c, o)
+    double *v64;  // F64: KMAX per pair
+    int *wsum;
+};
+
+// One pass over the tile's pair list for every pixel with !st.done.
+template <int KMAX, bool F64, int MODE>
+__device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int s0, int s1,
+                                          int px, int py, int px0, int px1, int py0, int py1,
+                                          PixelState<KMAX, F64> &st) {
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int K = A.K;
+    const float fpx = (float)px, fpy = (float)py;
+    const double dpx = (double)px, dpy = (double)py;
     for (int base = s0; base < s1; base += kBlendThreads) {
-        if (__syncthreads_count(!done) == 0) break;
-        // ---- stage + cull one batch (each thread one pair)
+        if (__syncthreads_count(!st.done) == 0) break;
+        // ---- stage one batch (each thread one pair), compact survivors in order
         const int j = base + tid;
         bool keep = false;
         float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
         int sp = 0;
         if (j < s1) {
-            sp = pair_splat[j];
-            if (preculled) {
-                keep = sp >= 0;  // bit 31 = culled by ivr_bin_sort_cull
+            sp = A.pair_splat[j];
+            if (A.preculled) {
+                keep = sp >= 0;  // bit 31 = culled for this tile by ivr_bin_sort_cull
                 if (keep) {
-                    r0 = __ldg(rec + 2 * sp);
-                    r1 = __ldg(rec + 2 * sp + 1);
+                    r0 = __ldg(A.rec + 2 * sp);
+                    r1 = __ldg(A.rec + 2 * sp + 1);
                 }
             } else {
-                r0 = __ldg(rec + 2 * sp);
-                r1 = __ldg(rec + 2 * sp + 1);
+                r0 = __ldg(A.rec + 2 * sp);
+                r1 = __ldg(A.rec + 2 * sp + 1);
                 keep = tile_touch(r0, r1, px0, px1, py0, py1);
             }
         }
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) s_wsum[warp] = __popc(m);
+        if (lane == 0) S.wsum[warp] = __popc(m);
         __syncthreads();
         int off = 0, total = 0;
 #pragma unroll
         for (int w = 0; w < kBlendThreads / 32; ++w) {
-            const int c = s_wsum[w];
+            const int c = S.wsum[w];
             off += (w < warp) ? c : 0;
             total += c;
         }
         if (keep) {
             const int q = off + __popc(m & lanemask_lt());
-            s_r0[q] = r0;
-            s_r1[q] = r1;
-            s_j[q] = j;
-            s_sp[q] = sp;
-            const float *v = values + (int64_t)K * sp;
+            S.r0[q] = r0;
+            S.r1[q] = r1;
+            S.j[q] = j;
+            S.sp[q] = sp;
+            const float *v = A.values + (int64_t)K * sp;
 #pragma unroll
             for (int c = 0; c < KMAX; ++c)
-                if (c < K) s_v[q * KMAX + c] = __ldg(v + c);
-            if (kStageMean64) {
-                s_r64[2 * q] = __ldg(rec64 + 8 * (int64_t)sp);
-                s_r64[2 * q + 1] = __ldg(rec64 + 8 * (int64_t)sp + 1);
-            }
-            if (kStage64) {
-                const double *r = rec64 + 8 * (int64_t)sp;
+                if (c < K) S.v[q * KMAX + c] = __ldg(v + c);
+            if (F64) {
+                const double *r = A.rec64 + 8 * (int64_t)sp;
 #pragma unroll
-                for (int c = 0; c < 6; ++c) s_r64[q * 6 + c] = __ldg(r + c);
-                const double *v64 = values64 + (int64_t)K * sp;
+                for (int c = 0; c < 6; ++c) S.r64[q * 6 + c] = __ldg(r + c);
+                if (MODE == kModeExact) {
+                    const double *v64 = A.values64 + (int64_t)K * sp;
 #pragma unroll
-                for (int c = 0; c < KMAX; ++c)
-                    if (c < K) s_v64[q * KMAX + c] = __ldg(v64 + c);
+                    for (int c = 0; c < KMAX; ++c)
+                        if (c < K) S.v64[q * KMAX + c] = __ldg(v64 + c);
+                }
             }
         }
         __syncthreads();
-        if (done) continue;
+        if (st.done) continue;
         // ---- per-pixel walk over the survivors, in list order
         for (int q = 0; q < total; ++q) {
-            const float4 a0 = s_r0[q];
-            const float4 a1 = s_r1[q];
+            const float4 a0 = S.r0[q];
+            const float4 a1 = S.r1[q];
             const float dx = fpx - a0.x, dy = fpy - a0.y;
             const float bdy = a1.y * dy, hcdy = a1.z * dy;
             const float sig = fmaf(fmaf(a1.x, dx, bdy), dx, hcdy * dy);
             if (sig > a0.w) continue;  // reference alpha < 1/255 for certain
             if (MODE == kModeExact) {
                 double al;
-                if (kStage64) {
-                    const double *r = s_r64 + q * 6;
+                if (F64) {
+                    const double *r = S.r64 + q * 6;
                     al = exact_alpha(dpx, dpy, r[0], r[1], r[2], r[3], r[4], r[5]);
                 } else {
                     al = exact_alpha(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
                                      2.0 * (double)a1.z, a0.z);
                 }
                 if (al < 0.0) continue;
-                const double w = dmul(T, al);
+                const double w = dmul(st.T, al);
                 if (F64) {
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c)
-                        if (c < K) acc64[c] = dadd(acc64[c], dmul(w, s_v64[q * KMAX + c]));
+                        if (c < K) st.acc64[c] = dadd(st.acc64[c], dmul(w, S.v64[q * KMAX + c]));
                 } else {
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c)
                         if (c < K)
-                            acc[c] = (float)dadd((double)acc[c], dmul(w, (double)s_v[q * KMAX + c]));
+                            st.acc[c] =
+                                (float)dadd((double)st.acc[c], dmul(w, (double)S.v[q * KMAX + c]));
                 }
-                T = dmul(T, dsub(1.0, al));
-                ++nc;
-                last = s_j[q] + 1;
-                if (T < kTStop) {
-                    done = true;
+                st.T = dmul(st.T, dsub(1.0, al));
+                ++st.nc;
+                st.last = S.j[q] + 1;
+                if (st.T < kTStop) {
+                    st.done = true;
                     break;
                 }
             } else {
-                // candidate: recompute with the float64 mean in dtype=float64 mode
+                // candidate: in dtype=float64 mode recompute dx, dy from the float64 mean
                 float cdx = dx, cdy = dy, cbdy = bdy, chcdy = hcdy, csig = sig;
-                if (kStageMean64) {
-                    cdx = (float)dsub(dpx, s_r64[2 * q]);
-                    cdy = (float)dsub(dpy, s_r64[2 * q + 1]);
+                if (F64) {
+                    cdx = (float)dsub(dpx, S.r64[q * 6]);
+                    cdy = (float)dsub(dpy, S.r64[q * 6 + 1]);
                     cbdy = a1.y * cdy;
                     chcdy = a1.z * cdy;
                     csig = fmaf(fmaf(a1.x, cdx, cbdy), cdx, chcdy * cdy);
                 }
-                // rigorous bound on |csig - sigma_ref|: ~17 ulp of the term
-                // magnitudes (dx/dy rounding, 5 ops, float32 conic rounding)
                 const float terms = fmaf(a1.x * cdx, cdx, fmaf(chcdy, cdy, fabsf(cbdy * cdx)));
-                const float E = 1.0e-6f * terms + 1e-30f;
-                const float sig_c = csig;
+                const float E = kSigmaErr * terms + 1e-30f;
                 const float thr = a1.w;
-                const float tm = 2.4e-7f * fabsf(thr) + 1e-7f;  // thr rounding + exp/1/255 margin
-                float al;
-                float dal;  // relative error bound of al
-                if (sig_c - E > 0.0f && sig_c + E < thr - tm) {
-                    al = a0.z * exp2f(-1.4426950408889634f * sig_c);
-                    al = fminf(al, 0.99f);
-                    dal = E + 6e-7f * (1.0f + sig_c);
-                } else if (sig_c - E > thr + tm) {
+                const float tm = 2.4e-7f * fabsf(thr) + 1e-7f;  // thr rounding + margins
+                float al, dal;  // alpha and a bound on |dAlpha| (absolute)
+                if (csig - E > 0.0f && csig + E < thr - tm) {
+                    const float au = a0.z * exp2f(-1.4426950408889634f * csig);
+                    // relative error: sigma bound, argument rounding, ex2.approx, * o
+                    const float rel = E + 1.2e-7f * csig + 3.6e-7f;
+                    if (au > 0.99f * (1.0f + rel)) {  // reference capped too: alpha = 0.99
+                        al = 0.99f;
+                        dal = 1.1e-8f;  // |0.99f - 0.99|
+                    } else {
+                        al = fminf(au, 0.99f);
+                        dal = au * rel;
+                    }
+                } else if (csig - E > thr + tm) {
                     continue;  // certainly skipped by the reference
                 } else {
                     double ad;
                     if (F64) {
-                        const double *r = rec64 + 8 * (int64_t)s_sp[q];
+                        const double *r = S.r64 + q * 6;
                         ad = exact_alpha(dpx, dpy, r[0], r[1], r[2], r[3], r[4], r[5]);
                     } else {
                         ad = exact_alpha(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
@@ -298,84 +274,100 @@ blend_fwd_kernel(const int32_t *__restrict__ ranges, const int32_t *__restrict__
                     }
                     if (ad < 0.0) continue;
                     al = (float)ad;
-                    dal = 1.2e-7f;
+                    dal = 6e-8f * al;
                 }
-                const float w = Tf * al;
+                const float w = st.Tf * al;
 #pragma unroll
                 for (int c = 0; c < KMAX; ++c)
-                    if (c < K) acc[c] = fmaf(w, s_v[q * KMAX + c], acc[c]);
-                Tf = Tf * (1.0f - al);
-                errT += al * dal * __frcp_rn(1.0f - al) * 1.01f + 1.2e-7f;
-                ++nc;
-                last = s_j[q] + 1;
-                if (Tf < 1e-4f * (1.0f + errT + 1e-6f)) {
-                    if (Tf < 1e-4f * (1.0f - errT - 1e-6f)) {
-                        done = true;  // reference also stopped here
-                    } else {
-                        done = true;  // ambiguous: replay this pixel exactly
-                        replay = true;
-                    }
+                    if (c < K) st.acc[c] = fmaf(w, S.v[q * KMAX + c], st.acc[c]);
+                const float om = 1.0f - al;
+                st.Tf = st.Tf * om;
+                st.errT += dal * __frcp_rn(om) * 1.01f + 1.3e-7f;
+                ++st.nc;
+                st.last = S.j[q] + 1;
+                if (st.Tf < 1e-4f * (1.0f + st.errT + 1e-6f)) {
+                    st.done = true;  // certain stop, or ambiguous -> EXACT re-walk
+                    st.replay = !(st.Tf < 1e-4f * (1.0f - st.errT - 1e-6f));
                     break;
                 }
             }
         }
     }
-    if (!inside) return;
+}
+
+template <int KMAX, bool F64, int MODE>
+__global__ void __launch_bounds__(kBlendThreads, 3)
+blend_fwd_kernel(BlendArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    __shared__ int s_wsum[kBlendThreads / 32];
+    Smem S;
+    S.r0 = reinterpret_cast<float4 *>(smem);
+    S.r1 = S.r0 + kBlendThreads;
+    S.j = reinterpret_cast<int *>(S.r1 + kBlendThreads);
+    S.sp = S.j + kBlendThreads;
+    S.v = reinterpret_cast<float *>(S.sp + kBlendThreads);
+    S.r64 = reinterpret_cast<double *>(S.v + kBlendThreads * KMAX);
+    S.v64 = S.r64 + (F64 ? 6 * kBlendThreads : 0);
+    S.wsum = s_wsum;
+
+    const int tile = A.tile_order ? A.tile_order[blockIdx.x] : (int)blockIdx.x;
+    const int tx = tile % A.ntx, ty = tile / A.ntx;
+    const int tid = threadIdx.x;
+    const int px = tx * kTile + (tid & 15), py = ty * kTile + (tid >> 4);
+    const bool inside = px < A.W && py < A.H;
+    const int s0 = A.ranges[tile], s1 = A.ranges[tile + 1];
+    const int px0 = tx * kTile, py0 = ty * kTile;
+    const int px1 = min(px0 + kTile - 1, A.W - 1), py1 = min(py0 + kTile - 1, A.H - 1);
+
+    PixelState<KMAX, F64> st;
+    st.reset(s0, !inside);
+    tile_walk<KMAX, F64, MODE>(A, S, s0, s1, px, py, px0, px1, py0, py1, st);
+    bool exact_out = MODE == kModeExact;
     if (MODE == kModeFast) {
-        if (replay) {
-            replay_pixel<KMAX, F64>(s0, s1, pair_splat, rec, values, rec64, values64, K, px, py,
-                                    acc, acc64, T, nc, last);
-            if (F64) {
-#pragma unroll
-                for (int c = 0; c < KMAX; ++c) acc[c] = (float)acc64[c];
+        // pixels whose T landed in the ambiguity band: one EXACT re-walk
+        const bool need = st.replay;
+        if (__syncthreads_or(need)) {
+            PixelState<KMAX, F64> ex;
+            ex.reset(s0, !need);
+            tile_walk<KMAX, F64, kModeExact>(A, S, s0, s1, px, py, px0, px1, py0, py1, ex);
+            if (need) {
+                st = ex;
+                exact_out = true;
             }
-        } else {
-            T = (double)Tf;
         }
+        if (!exact_out) st.T = (double)st.Tf;
     }
-    const int64_t pix = (int64_t)py * W + px;
+    if (!inside) return;
+    const int64_t pix = (int64_t)py * A.W + px;
+    const int K = A.K;
     if (F64) {
-        double *o = out64 + pix * K;
-        if (MODE == kModeExact) {
-#pragma unroll
-            for (int c = 0; c < KMAX; ++c)
-                if (c < K) o[c] = acc64[c];
-        } else {
-#pragma unroll
-            for (int c = 0; c < KMAX; ++c)
-                if (c < K) o[c] = replay ? acc64[c] : (double)acc[c];
-        }
-    } else {
-        float *o = out + pix * K;
+        double *o = A.out64 + pix * K;
 #pragma unroll
         for (int c = 0; c < KMAX; ++c)
-            if (c < K) o[c] = acc[c];
+            if (c < K) o[c] = exact_out ? st.acc64[c] : (double)st.acc[c];
+    } else {
+        float *o = A.out + pix * K;
+#pragma unroll
+        for (int c = 0; c < KMAX; ++c)
+            if (c < K) o[c] = st.acc[c];
     }
-    if (contrib) contrib[pix] = nc;
-    if (last_pos) last_pos[pix] = last;
-    if (t_final) t_final[pix] = T;
+    if (A.contrib) A.contrib[pix] = st.nc;
+    if (A.last_pos) A.last_pos[pix] = st.last;
+    if (A.t_final) A.t_final[pix] = st.T;
 }
 
-template <int KMAX, bool F64, int MODE>
+template <int KMAX, bool F64>
 size_t blend_smem_bytes() {
     return (size_t)kBlendThreads * (16 + 16 + 4 + 4 + 4 * KMAX) +
-           ((F64 && MODE == kModeExact) ? (size_t)kBlendThreads * 8 * (6 + KMAX) : 0) +
-           ((F64 && MODE == kModeFast) ? (size_t)kBlendThreads * 16 : 0);
+           (F64 ? (size_t)kBlendThreads * 8 * (6 + KMAX) : 0);
 }
 
 template <int KMAX, bool F64, int MODE>
-int launch_blend(const int32_t *ranges, const int32_t *pair_splat, int ntx, int nty,
-                 const float *rec, const float *values, const double *rec64,
-                 const double *values64, int K, int W, int H, float *out, double *out64,
-                 int32_t *contrib, int32_t *last_pos, double *t_final, const int32_t *tile_order,
-                 int preculled, cudaStream_t st) {
-    const size_t sm = blend_smem_bytes<KMAX, F64, MODE>();
+int launch_blend(const BlendArgs &A, int ntiles, cudaStream_t st) {
+    const size_t sm = blend_smem_bytes<KMAX, F64>();
     auto fn = blend_fwd_kernel<KMAX, F64, MODE>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
-    fn<<<ntx * nty, kBlendThreads, sm, st>>>(ranges, pair_splat, ntx,
-                                            reinterpret_cast<const float4 *>(rec), values, rec64,
-                                            values64, K, W, H, out, out64, contrib, last_pos,
-                                            t_final, tile_order, preculled);
+    fn<<<ntiles, kBlendThreads, sm, st>>>(A);
     return check_launch("blend_fwd_kernel");
 }
 
@@ -423,7 +415,7 @@ extern "C" int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_
         set_error("ivr_tile_order: bad argument");
         return IVR_ERR_ARG;
     }
-    if (ntiles > 4096) {  // identity order for very large frames
+    if (ntiles > 4096) {
         set_error("ivr_tile_order: more than 4096 tiles");
         return IVR_ERR_ARG;
     }
@@ -449,23 +441,36 @@ extern "C" int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_spl
         set_error("ivr_blend_fwd: float64 mode needs rec64/values64/out64; float32 needs out");
         return IVR_ERR_ARG;
     }
+    BlendArgs A;
+    A.ranges = tile_ranges;
+    A.pair_splat = pair_splat;
+    A.ntx = ntx;
+    A.rec = reinterpret_cast<const float4 *>(rec);
+    A.values = values;
+    A.rec64 = rec64;
+    A.values64 = values64;
+    A.K = k;
+    A.W = width;
+    A.H = height;
+    A.out = out;
+    A.out64 = out64;
+    A.contrib = contrib;
+    A.last_pos = last_pos;
+    A.t_final = t_final;
+    A.tile_order = tile_order;
+    A.preculled = (flags & IVR_BLEND_PRECULLED) != 0 ? 1 : 0;
     const bool exact = (flags & IVR_BLEND_EXACT) != 0;
-    const int preculled = (flags & IVR_BLEND_PRECULLED) != 0 ? 1 : 0;
-#define IVR_BLEND_M(KM, F, M)                                                                    \
-    return launch_blend<KM, F, M>(tile_ranges, pair_splat, ntx, nty, rec, values, rec64, values64, \
-                                  k, width, height, out, out64, contrib, last_pos, t_final,       \
-                                  tile_order, preculled, st)
-#define IVR_BLEND(KM)                                                                             \
-    if (f64) {                                                                                    \
-        if (exact) { IVR_BLEND_M(KM, true, kModeExact); }                                         \
-        IVR_BLEND_M(KM, true, kModeFast);                                                         \
-    }                                                                                             \
-    if (exact) { IVR_BLEND_M(KM, false, kModeExact); }                                            \
-    IVR_BLEND_M(KM, false, kModeFast)
+    const int nt = ntx * nty;
+#define IVR_BLEND(KM)                                                                   \
+    if (f64) {                                                                          \
+        return exact ? launch_blend<KM, true, kModeExact>(A, nt, st)                    \
+                     : launch_blend<KM, true, kModeFast>(A, nt, st);                    \
+    }                                                                                   \
+    return exact ? launch_blend<KM, false, kModeExact>(A, nt, st)                       \
+                 : launch_blend<KM, false, kModeFast>(A, nt, st)
     if (k <= 4) { IVR_BLEND(4); }
     if (k <= 8) { IVR_BLEND(8); }
     if (k <= 16) { IVR_BLEND(16); }
     IVR_BLEND(32);
 #undef IVR_BLEND
-#undef IVR_BLEND_M
 }

@@ -314,7 +314,7 @@ fallback_sort_kernel(const uint64_t *depth_key, int64_t n, const int32_t *need_f
     if (*need_full == 0) return;
     __shared__ uint32_t s_off[kRadix];
     __shared__ uint32_t s_wc[kFbWarps][kRadix];
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
     for (int p = 0; p < 8; ++p) {
         const uint64_t *ki = p == 0 ? depth_key : ((p & 1) ? kB : kA);
