@@ -130,6 +130,28 @@ int ivr_preprocess_fwd(const ivr_gaussians *g, const ivr_shading *shading,
                        const ivr_layout *layout, ivr_proj_out *out,
                        int32_t f64_mode, ivr_stream_t stream);
 
+/* Per-frame view/light/edit state that may live in DEVICE memory, so that a
+ * captured CUDA graph of a whole frame can be replayed with new cameras and
+ * edits (the host refreshes this struct with one small H2D copy). */
+typedef struct ivr_frame_params {
+    ivr_camera cam;
+    double light_dir[3];
+    double term_scales[4];
+    double lam[4];
+    double b[4];
+    int32_t orbital;
+    int32_t rescale_opacity;
+} ivr_frame_params;
+
+/* ivr_preprocess_fwd with the camera, light, coefficient transform and the
+ * opacity-rescale flag read from `params` (a DEVICE pointer) instead of the
+ * host structs; shading/edits still supply the array pointers.  width/height
+ * must equal params->cam.width/height (they size the tile grid). */
+int ivr_preprocess_fwd_params(const ivr_gaussians *g, const ivr_shading *shading,
+                              const ivr_edits *edits, const ivr_frame_params *params,
+                              int32_t width, int32_t height, const ivr_layout *layout,
+                              ivr_proj_out *out, int32_t f64_mode, ivr_stream_t stream);
+
 /* Shading only (shading.shade_gaussians, shading.py:225-329): float64 rgb
  * (n,3) and optional terms (n,9: ambient, diffuse, specular). */
 int ivr_shade_fwd(const ivr_gaussians *g, const ivr_shading *shading,

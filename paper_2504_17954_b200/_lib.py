@@ -35,6 +35,13 @@ class Camera_t(ctypes.Structure):
                 ("width", ctypes.c_int32), ("height", ctypes.c_int32)]
 
 
+class FrameParams_t(ctypes.Structure):
+    _fields_ = [("cam", Camera_t), ("light_dir", ctypes.c_double * 3),
+                ("term_scales", ctypes.c_double * 4), ("lam", ctypes.c_double * 4),
+                ("b", ctypes.c_double * 4), ("orbital", ctypes.c_int32),
+                ("rescale_opacity", ctypes.c_int32)]
+
+
 class Gaussians_t(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("mu", P), ("q_raw", P), ("log_s", P), ("o_logit", P),
                 ("n_raw", P)]
@@ -71,6 +78,10 @@ _SIGS = {
                             ctypes.POINTER(Edits_t), ctypes.POINTER(Camera_t),
                             ctypes.POINTER(Layout_t), ctypes.POINTER(ProjOut_t), ctypes.c_int32, P],
                            ctypes.c_int),
+    "ivr_preprocess_fwd_params": ([ctypes.POINTER(Gaussians_t), ctypes.POINTER(Shading_t),
+                                   ctypes.POINTER(Edits_t), P, ctypes.c_int32, ctypes.c_int32,
+                                   ctypes.POINTER(Layout_t), ctypes.POINTER(ProjOut_t),
+                                   ctypes.c_int32, P], ctypes.c_int),
     "ivr_shade_fwd": ([ctypes.POINTER(Gaussians_t), ctypes.POINTER(Shading_t), P,
                        ctypes.POINTER(Camera_t), P, P, P], ctypes.c_int),
     "ivr_bin_sort_workspace_size": ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int32], ctypes.c_size_t),

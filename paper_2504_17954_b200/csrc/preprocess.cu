@@ -21,20 +21,21 @@ struct ShadeOut {
 };
 
 // shading.py:236-297 for one splat.  `nrm` is the unit normal (eps 1e-12).
-__device__ __forceinline__ void shade_one(const ivr_shading &S, int64_t i, int32_t sid,
-                                          const double mu[3], const double nrm[3],
-                                          const ivr_camera &cam, ShadeOut &o) {
+__device__ __forceinline__ void shade_one(const ivr_shading &S, const ivr_frame_params &P,
+                                          int64_t i, int32_t sid, const double mu[3],
+                                          const double nrm[3], ShadeOut &o) {
+    const ivr_camera &cam = P.cam;
     double w[3] = {dsub(cam.position[0], mu[0]), dsub(cam.position[1], mu[1]),
                    dsub(cam.position[2], mu[2])};
     const double wn = dmax(norm3(w[0], w[1], w[2]), 1e-12);
     const double v[3] = {ddiv(w[0], wn), ddiv(w[1], wn), ddiv(w[2], wn)};
     double l[3], h[3];
-    if (!S.orbital) {
+    if (!P.orbital) {
         for (int k = 0; k < 3; ++k) l[k] = h[k] = v[k];
     } else {
         double u[3];
         for (int k = 0; k < 3; ++k) {
-            l[k] = S.light_dir[k];
+            l[k] = P.light_dir[k];
             u[k] = dadd(v[k], l[k]);
         }
         const double un = dmax(norm3(u[0], u[1], u[2]), 1e-12);
@@ -44,14 +45,14 @@ __device__ __forceinline__ void shade_one(const ivr_shading &S, int64_t i, int32
     const double sd = sigmoid_ref(S.k_d_raw[i]);
     const double ss = sigmoid_ref(S.k_s_raw[i]);
     const double beta1 = dadd(exp(S.log_beta[i]), 1.0);
-    const double ta = dadd(dmul(S.lam[0], sa), S.b[0]);
-    const double td = dadd(dmul(S.lam[1], sd), S.b[1]);
-    const double tsp = dadd(dmul(S.lam[2], ss), S.b[2]);
-    const double tb = dadd(dmul(S.lam[3], beta1), S.b[3]);
-    const double k_a = dmul(S.term_scales[0], clip01(ta));
-    const double k_d = dmul(S.term_scales[1], clip01(td));
-    const double k_s = dmul(S.term_scales[2], clip01(tsp));
-    const double beta = dmul(S.term_scales[3], dmax(tb, 1.0));
+    const double ta = dadd(dmul(P.lam[0], sa), P.b[0]);
+    const double td = dadd(dmul(P.lam[1], sd), P.b[1]);
+    const double tsp = dadd(dmul(P.lam[2], ss), P.b[2]);
+    const double tb = dadd(dmul(P.lam[3], beta1), P.b[3]);
+    const double k_a = dmul(P.term_scales[0], clip01(ta));
+    const double k_d = dmul(P.term_scales[1], clip01(td));
+    const double k_s = dmul(P.term_scales[2], clip01(tsp));
+    const double beta = dmul(P.term_scales[3], dmax(tb, 1.0));
     const double *cp = S.per_splat_palette ? S.palette + 3 * i : S.palette + 3 * (int64_t)sid;
     double cv[3];
     for (int k = 0; k < 3; ++k) cv[k] = clip01(dadd(cp[k], S.delta_c[3 * i + k]));
@@ -69,17 +70,16 @@ __device__ __forceinline__ void shade_one(const ivr_shading &S, int64_t i, int32
     }
 }
 
-__global__ void __launch_bounds__(256)
-preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E,
-                  int has_edits, ivr_camera cam, ivr_layout L, ivr_proj_out O,
-                  int f64_mode) {
-    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= G.n) return;
+__device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr_shading &S,
+                                               int has_shading, const ivr_edits &E, int has_edits,
+                                               const ivr_frame_params &P, const ivr_layout &L,
+                                               const ivr_proj_out &O, int f64_mode, int64_t i) {
+    const ivr_camera &cam = P.cam;
     const int32_t sid = (has_edits && E.scene_id) ? E.scene_id[i] : 0;
 
     // ---- effective opacity (scene.py:214-220; every splat when any scale != 1)
     double o_logit = G.o_logit[i];
-    if (has_edits && E.rescale_opacity && E.opacity_scale) {
+    if (has_edits && P.rescale_opacity && E.opacity_scale) {
         double p = dmul(E.opacity_scale[sid], sigmoid_ref(o_logit));
         p = p < 1e-12 ? 1e-12 : (p > 1.0 - 1e-9 ? 1.0 - 1e-9 : p);
         o_logit = log(ddiv(p, dsub(1.0, p)));
@@ -185,7 +185,7 @@ preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E,
     const double nrm[3] = {ddiv(nr[0], nn), ddiv(nr[1], nn), ddiv(nr[2], nn)};
 
     ShadeOut sh;
-    if (has_shading) shade_one(S, i, sid, mu, nrm, cam, sh);
+    if (has_shading) shade_one(S, P, i, sid, mu, nrm, sh);
 
     // ---- float32 blend record (rasterizer.py:151-153 casts) + skip threshold
     const float mx32 = (float)mx, my32 = (float)my;
@@ -250,9 +250,32 @@ preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E,
     if (O.rgb && has_shading) for (int k = 0; k < 3; ++k) O.rgb[3 * i + k] = sh.rgb[k];
 }
 
+// Per-frame parameters (camera, light, transform, rescale flag) are staged in
+// shared memory once per block, from kernel parameters or from device memory.
+__device__ __forceinline__ void stage_params(const ivr_frame_params *src, ivr_frame_params &dst) {
+    static_assert(sizeof(ivr_frame_params) % 4 == 0, "params must be word-sized");
+    constexpr int kWords = (int)(sizeof(ivr_frame_params) / 4);
+    for (int w = threadIdx.x; w < kWords; w += blockDim.x)
+        reinterpret_cast<int *>(&dst)[w] = reinterpret_cast<const int *>(src)[w];
+    __syncthreads();
+}
+
 __global__ void __launch_bounds__(256)
-shade_kernel(ivr_gaussians G, ivr_shading S, const int32_t *scene_id, ivr_camera cam,
+preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E, int has_edits,
+                  ivr_frame_params Pv, const ivr_frame_params *__restrict__ Pd, ivr_layout L,
+                  ivr_proj_out O, int f64_mode) {
+    __shared__ ivr_frame_params sp;
+    stage_params(Pd ? Pd : &Pv, sp);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= G.n) return;
+    preprocess_one(G, S, has_shading, E, has_edits, sp, L, O, f64_mode, i);
+}
+
+__global__ void __launch_bounds__(256)
+shade_kernel(ivr_gaussians G, ivr_shading S, const int32_t *scene_id, ivr_frame_params Pv,
              double *rgb, double *terms) {
+    __shared__ ivr_frame_params sp;
+    stage_params(&Pv, sp);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G.n) return;
     const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
@@ -260,7 +283,7 @@ shade_kernel(ivr_gaussians G, ivr_shading S, const int32_t *scene_id, ivr_camera
     const double nn = dmax(norm3(nr[0], nr[1], nr[2]), 1e-12);
     const double nrm[3] = {ddiv(nr[0], nn), ddiv(nr[1], nn), ddiv(nr[2], nn)};
     ShadeOut sh;
-    shade_one(S, i, scene_id ? scene_id[i] : 0, mu, nrm, cam, sh);
+    shade_one(S, sp, i, scene_id ? scene_id[i] : 0, mu, nrm, sh);
     for (int k = 0; k < 3; ++k) rgb[3 * i + k] = sh.rgb[k];
     if (terms) {
         for (int k = 0; k < 3; ++k) {
@@ -269,6 +292,22 @@ shade_kernel(ivr_gaussians G, ivr_shading S, const int32_t *scene_id, ivr_camera
             terms[9 * i + 6 + k] = sh.spec;
         }
     }
+}
+
+ivr_frame_params params_from(const ivr_camera &cam, const ivr_shading *S, const ivr_edits *E) {
+    ivr_frame_params P{};
+    P.cam = cam;
+    if (S) {
+        P.orbital = S->orbital;
+        for (int k = 0; k < 3; ++k) P.light_dir[k] = S->light_dir[k];
+        for (int k = 0; k < 4; ++k) {
+            P.term_scales[k] = S->term_scales[k];
+            P.lam[k] = S->lam[k];
+            P.b[k] = S->b[k];
+        }
+    }
+    P.rescale_opacity = E ? E->rescale_opacity : 0;
+    return P;
 }
 
 }  // namespace ivr
@@ -297,9 +336,40 @@ extern "C" int ivr_preprocess_fwd(const ivr_gaussians *g, const ivr_shading *sha
     if (edits) E = *edits;
     const int threads = 256;
     const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
+    ivr_frame_params P = ivr::params_from(*cam, shading, edits);
     ivr::preprocess_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
-        *g, S, shading != nullptr, E, edits != nullptr, *cam, *layout, *out, f64_mode);
+        *g, S, shading != nullptr, E, edits != nullptr, P, nullptr, *layout, *out, f64_mode);
     return ivr::check_launch("preprocess_kernel");
+}
+
+extern "C" int ivr_preprocess_fwd_params(const ivr_gaussians *g, const ivr_shading *shading,
+                                         const ivr_edits *edits, const ivr_frame_params *params,
+                                         int32_t width, int32_t height, const ivr_layout *layout,
+                                         ivr_proj_out *out, int32_t f64_mode,
+                                         ivr_stream_t stream) {
+    if (!g || !params || !layout || !out || g->n < 0 || width < 1 || height < 1) {
+        ivr::set_error("ivr_preprocess_fwd_params: null argument");
+        return IVR_ERR_ARG;
+    }
+    if (!out->depth_key || !out->count || !out->rect || !out->rec || !out->values || layout->k < 1 ||
+        layout->n_attr < 0 || layout->n_attr > IVR_MAX_ATTRS ||
+        (f64_mode && (!out->rec64 || !out->values64))) {
+        ivr::set_error("ivr_preprocess_fwd_params: missing output buffer or bad layout");
+        return IVR_ERR_ARG;
+    }
+    if (g->n == 0) return IVR_OK;
+    ivr_shading S{};
+    ivr_edits E{};
+    if (shading) S = *shading;
+    if (edits) E = *edits;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
+    ivr_frame_params Pv{};
+    Pv.cam.width = width;
+    Pv.cam.height = height;
+    ivr::preprocess_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
+        *g, S, shading != nullptr, E, edits != nullptr, Pv, params, *layout, *out, f64_mode);
+    return ivr::check_launch("preprocess_kernel(params)");
 }
 
 extern "C" int ivr_shade_fwd(const ivr_gaussians *g, const ivr_shading *shading,
@@ -312,7 +382,8 @@ extern "C" int ivr_shade_fwd(const ivr_gaussians *g, const ivr_shading *shading,
     if (g->n == 0) return IVR_OK;
     const int threads = 256;
     const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
-    ivr::shade_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(*g, *shading, scene_id, *cam,
-                                                                   rgb, terms);
+    ivr_frame_params P = ivr::params_from(*cam, shading, nullptr);
+    ivr::shade_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(*g, *shading, scene_id, P, rgb,
+                                                                   terms);
     return ivr::check_launch("shade_kernel");
 }

@@ -145,8 +145,11 @@ class Frame:
 
 
 def preprocess(dg: DeviceGaussians, cam, K, cols, ws: Workspace, shading=None, edits=None,
-               colors=None, attrs=(), f64=False, debug=False, stream=None):
-    """Launch K1; returns a Frame with the per-splat buffers."""
+               colors=None, attrs=(), f64=False, debug=False, stream=None, params_dev=None):
+    """Launch K1; returns a Frame with the per-splat buffers.  With
+    ``params_dev`` (a device tensor holding an ivr_frame_params) the camera
+    and light come from device memory (CUDA-graph replay); ``cam`` then only
+    supplies width/height."""
     n = dg.n
     F = Frame()
     F.n, F.K, F.f64, F.cam = n, K, f64, cam
@@ -186,13 +189,39 @@ def preprocess(dg: DeviceGaussians, cam, K, cols, ws: Workspace, shading=None, e
         for k, v in F.dbg.items():
             setattr(out, k, v.data_ptr())
     g = dg.struct()
-    cs = camera_struct(cam)
     sh = ctypes.byref(shading) if shading is not None else None
     ed = ctypes.byref(edits) if edits is not None else None
-    L.check(L.lib().ivr_preprocess_fwd(ctypes.byref(g), sh, ed, ctypes.byref(cs), ctypes.byref(lay),
-                                       ctypes.byref(out), 1 if f64 else 0, stream_handle(stream)),
-            "ivr_preprocess_fwd")
+    if params_dev is not None:
+        L.check(L.lib().ivr_preprocess_fwd_params(
+            ctypes.byref(g), sh, ed, ptr(params_dev), int(cam.width), int(cam.height),
+            ctypes.byref(lay), ctypes.byref(out), 1 if f64 else 0, stream_handle(stream)),
+            "ivr_preprocess_fwd_params")
+    else:
+        cs = camera_struct(cam)
+        L.check(L.lib().ivr_preprocess_fwd(ctypes.byref(g), sh, ed, ctypes.byref(cs),
+                                           ctypes.byref(lay), ctypes.byref(out), 1 if f64 else 0,
+                                           stream_handle(stream)), "ivr_preprocess_fwd")
     return F
+
+
+def frame_params(cam, light=None, lam=None, b=None, rescale_opacity=False) -> L.FrameParams_t:
+    """Host ivr_frame_params for one frame (camera + light + transform)."""
+    P = L.FrameParams_t()
+    P.cam = camera_struct(cam)
+    if light is not None:
+        P.orbital = 1 if light.mode == "orbital" else 0
+        ld = light_direction(light.polar, light.azimuth) if P.orbital else np.zeros(3)
+        ts = np.asarray(light.term_scales, dtype=np.float64).reshape(4)
+    else:
+        P.orbital, ld, ts = 0, np.zeros(3), np.ones(4)
+    lam = np.ones(4) if lam is None else np.asarray(lam, dtype=np.float64).reshape(4)
+    b = np.zeros(4) if b is None else np.asarray(b, dtype=np.float64).reshape(4)
+    for i in range(3):
+        P.light_dir[i] = float(ld[i])
+    for i in range(4):
+        P.term_scales[i], P.lam[i], P.b[i] = float(ts[i]), float(lam[i]), float(b[i])
+    P.rescale_opacity = 1 if rescale_opacity else 0
+    return P
 
 
 def bin_sort(F: Frame, ws: Workspace, stream=None, capacity=None):

@@ -325,6 +325,130 @@ class DeviceScene:
         return _unpack(out, F.layout, F.contrib.cpu().numpy())
 
 
+class FrameGraph:
+    """A whole frame (K1 -> K2 -> K3) captured once as a CUDA graph.
+
+    Per frame the host writes the camera / light / edit tables into pinned
+    staging (a ring, so the host can run ahead), one small H2D copy lands
+    them in fixed device buffers, and the graph replays: one launch instead of
+    ~27, and no host gaps inside the frame.  Resolution, channel layout and
+    mode are fixed per graph.  The pair capacity learned on the warm-up frame
+    is reused (with 30% headroom); ``overflowed()`` reports whether a replay
+    needed more, in which case ``recapture()`` grows it.
+    """
+
+    RING = 8
+
+    def __init__(self, ds, width, height, exact=False, headroom=1.3, warm_cam=None):
+        self.ds, self.W, self.H, self.exact = ds, int(width), int(height), exact
+        dev = ds.dg.device
+        S = ds.n_scenes
+        nb = ctypes.sizeof(L.FrameParams_t)
+        self._h = [torch.empty(nb + 8 * 4 * S, dtype=torch.uint8, pin_memory=True)
+                   for _ in range(self.RING)]
+        self._ev = [None] * self.RING
+        self._slot = 0
+        self.d_params = torch.empty(nb, dtype=torch.uint8, device=dev)
+        self.d_tab = torch.empty(4 * S, dtype=torch.float64, device=dev)
+        self.nb = nb
+        from .synthetic import bench_camera
+        cam = warm_cam or bench_camera(self.W, self.H)
+        F = ds.render_frame(cam, fast=False, exact=exact)  # learns the pair capacity
+        self.capacity = max(int(int(F.n_pairs.item()) * headroom) + 4096, 1 << 16)
+        self._capture(cam)
+
+    def _stage(self, cam, light=None, palettes=None, opacity_scales=None):
+        sc = self.ds.scene
+        S = self.ds.n_scenes
+        pal = np.empty((S, 3))
+        osc = np.empty(S)
+        for i, (m, e) in enumerate(zip(sc.models, sc.edits)):
+            pal[i] = e.palette_override if e.palette_override is not None else m.palette.c_p
+            osc[i] = e.opacity_scale
+        if palettes is not None:
+            pal = np.asarray(palettes, dtype=np.float64).reshape(S, 3)
+        if opacity_scales is not None:
+            osc = np.asarray(opacity_scales, dtype=np.float64).reshape(S)
+        if int(cam.width) != self.W or int(cam.height) != self.H:
+            raise ValueError("FrameGraph resolution is fixed at capture time")
+        k = self._slot
+        self._slot = (k + 1) % self.RING
+        if self._ev[k] is not None:
+            self._ev[k].synchronize()
+        h = self._h[k]
+        P = D.frame_params(cam, light or sc.light, rescale_opacity=not np.all(osc == 1.0))
+        ctypes.memmove(h.data_ptr(), ctypes.addressof(P), self.nb)
+        tab = np.frombuffer(h.numpy(), dtype=np.float64, count=4 * S, offset=self.nb)
+        tab[:3 * S] = pal.reshape(-1)
+        tab[3 * S:] = osc
+        self.d_params.copy_(h[:self.nb], non_blocking=True)
+        self.d_tab.copy_(h[self.nb:].view(torch.float64), non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._ev[k] = ev
+
+    def _capture(self, cam):
+        ds = self.ds
+        S = ds.n_scenes
+        self._stage(cam)
+        torch.cuda.synchronize()
+        shading = D.shading_struct(ds.dg, self.d_tab[:3 * S], False, ds.scene.light)
+        edits = L.Edits_t()
+        edits.scene_id = ds.dg.scene_id.data_ptr()
+        edits.opacity_scale = self.d_tab[3 * S:].data_ptr()
+        edits.rescale_opacity = 0  # taken from d_params
+        layout = _channel_layout(("color", "alpha"), None)
+        cols, _, K = _cols(layout)
+        # allocate every workspace buffer at its final size before capture
+        ws = ds.ws
+        F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=self.d_params)
+        D.bin_sort(F, ws, capacity=self.capacity)
+        D.blend(F, ws, want_state=False, exact=self.exact)
+        torch.cuda.synchronize()
+        g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(g):
+            F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=self.d_params)
+            D.bin_sort(F, ws, capacity=self.capacity)
+            D.blend(F, ws, want_state=False, exact=self.exact)
+        F.layout = layout
+        self.F, self.g = F, g
+        self._keep = (shading, edits)
+
+    def stage(self, cam, **edits):
+        """Enqueue this frame's camera / light / edit upload (async)."""
+        self._stage(cam, **edits)
+
+    def launch(self):
+        """Enqueue the captured frame; returns the Frame whose .out holds RGBA."""
+        self.g.replay()
+        return self.F
+
+    def replay(self, cam, **edits):
+        """stage() + launch()."""
+        self._stage(cam, **edits)
+        self.g.replay()
+        return self.F
+
+    def render_host(self, cam, host_out, host_contrib=None, **edits):
+        """End-to-end frame: H2D inputs, replay, D2H image (synchronous)."""
+        F = self.replay(cam, **edits)
+        host_out.copy_(F.out, non_blocking=True)
+        if host_contrib is not None:
+            host_contrib.copy_(F.contrib, non_blocking=True)
+        torch.cuda.current_stream().synchronize()
+        if self.overflowed():  # pair capacity too small for this view: grow and redo
+            self.recapture(cam)
+            return self.render_host(cam, host_out, host_contrib, **edits)
+        return host_out
+
+    def overflowed(self):
+        return int(self.F.n_pairs.item()) > self.capacity
+
+    def recapture(self, cam):
+        self.capacity = int(int(self.F.n_pairs.item()) * 1.3) + 4096
+        self._capture(cam)
+
+
 def render_composed(scene, cam, channels=("color", "alpha"), attrs=None, dtype=np.float32,
                     sequential=False):
     """Shade and rasterize a composed scene for one camera (scene.py:231-239).
