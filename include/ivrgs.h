@@ -203,6 +203,56 @@ int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_splat,
 int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_t *order,
                    ivr_stream_t stream);
 
+/* K4a: blend backward.  Replaces _kernels.composite_backward
+ * (_kernels.py:75-135) and the np.add.at per-Gaussian reductions
+ * (rasterizer.py:240-243).  Walks each pixel's contributors front to back up
+ * to last_pos with the same certified decisions as K3 (the remaining colour
+ * is out - accumulated, so no division by 1 - alpha), and accumulates with
+ * warp-reduced float32 atomics into caller-zeroed per-Gaussian buffers:
+ * g_values (n,k), g_mean2d (n,2), g_conic (n,3), g_opacity (n).
+ * out = K3's float32 output (H,W,k); d_out (H,W,k) float32 upstream gradient.
+ * rec64 selects dtype=float64 decisions.  flags: IVR_BLEND_PRECULLED. */
+int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
+                  int32_t nty, const float *rec, const float *values, const double *rec64,
+                  int32_t k, int32_t width, int32_t height, const float *out,
+                  const int32_t *last_pos, const float *d_out, float *g_values,
+                  float *g_mean2d, float *g_conic, float *g_opacity, int32_t flags,
+                  ivr_stream_t stream);
+
+/* Per-Gaussian backward outputs (float64, NULL = not wanted). */
+typedef struct ivr_grads {
+    /* inputs: K4a accumulators (float32, NULL if none) and an optional extra
+     * upstream gradient on the shaded rgb (n,3) (shade_backward API) */
+    const float *g_values, *g_mean2d, *g_conic, *g_opacity;
+    const double *d_rgb_extra;
+    /* rasterize_backward outputs (rasterizer.py:273-286) */
+    double *d_mu, *d_q_raw, *d_log_s, *d_o_logit, *d_n_raw, *d_colors, *d_mean2d;
+    double *d_values; /* (n,k) raw per-channel gradients (attribute columns) */
+    /* shade_backward outputs (shading.py:426-439) */
+    double *d_delta_c, *d_k_a_raw, *d_k_d_raw, *d_k_s_raw, *d_log_beta;
+    double *d_c_p;     /* (n,3) per splat, or (S,3) summed per scene if per_scene */
+    double *d_scale;   /* (S) opacity-scale chain of inverse._step (inverse.py:174-180) */
+    double *d_globals; /* [10] d_lam[4], d_b[4], d_polar, d_azimuth (summed) */
+    int32_t per_scene;
+    double dl_dp[3], dl_da[3]; /* orbital light direction derivatives (host) */
+    /* [16] first non-finite row per output (init ~0): 0 d_mu, 1 d_q_raw,
+     * 2 d_log_s, 3 d_o_logit, 4 d_n_raw, 5 d_colors, 6 d_k_a_raw, 7 d_k_d_raw,
+     * 8 d_k_s_raw, 9 d_log_beta, 10 d_delta_c / d_c_p */
+    unsigned long long *bad;
+} ivr_grads;
+
+/* K4b: per-Gaussian backward in float64: conic -> cov2d chain
+ * (rasterizer.py:245-255), channel unpack (rasterizer.py:257-270),
+ * gaussians.project_backward (gaussians.py:349-400, when geometry != 0),
+ * opacity-logit chain (rasterizer.py:278-279) and, when shading != NULL,
+ * shading.shade_backward (shading.py:332-445) plus the composed-scene /
+ * inverse reductions (inverse.py:170-181).  Camera/light from `params`
+ * (device pointer) if non-NULL else from cam + shading. */
+int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *shading,
+                       const ivr_edits *edits, const ivr_frame_params *params,
+                       const ivr_camera *cam, const ivr_layout *layout, ivr_grads *grads,
+                       int32_t geometry, ivr_stream_t stream);
+
 /* K5: VQ assignment, vq.assign_nearest (vq.py:90-96): index of the nearest
  * sorted centroid = searchsorted(mids, v, 'left'); NaN -> K-1.
  * Output uint16 (K <= 65536). */

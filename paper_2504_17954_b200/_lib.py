@@ -71,6 +71,20 @@ class ProjOut_t(ctypes.Structure):
                 ("depth", P), ("opacity", P), ("rgb", P), ("radius", P), ("valid", P)]
 
 
+class Grads_t(ctypes.Structure):
+    _fields_ = [("g_values", P), ("g_mean2d", P), ("g_conic", P), ("g_opacity", P),
+                ("d_rgb_extra", P), ("d_mu", P), ("d_q_raw", P), ("d_log_s", P), ("d_o_logit", P),
+                ("d_n_raw", P), ("d_colors", P), ("d_mean2d", P), ("d_values", P),
+                ("d_delta_c", P), ("d_k_a_raw", P), ("d_k_d_raw", P), ("d_k_s_raw", P),
+                ("d_log_beta", P), ("d_c_p", P), ("d_scale", P), ("d_globals", P),
+                ("per_scene", ctypes.c_int32), ("dl_dp", ctypes.c_double * 3),
+                ("dl_da", ctypes.c_double * 3), ("bad", P)]
+
+
+BAD_IDS = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_k_a_raw",
+           "d_k_d_raw", "d_k_s_raw", "d_log_beta", "d_delta_c")
+
+
 _SIGS = {
     "ivr_version": ([], ctypes.c_int),
     "ivr_last_error": ([], ctypes.c_char_p),
@@ -91,6 +105,13 @@ _SIGS = {
                        ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_int32, P],
                       ctypes.c_int),
     "ivr_tile_order": ([P, ctypes.c_int32, P, P], ctypes.c_int),
+    "ivr_blend_bwd": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
+                       ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, ctypes.c_int32, P],
+                      ctypes.c_int),
+    "ivr_preprocess_bwd": ([ctypes.POINTER(Gaussians_t), ctypes.POINTER(Shading_t),
+                            ctypes.POINTER(Edits_t), P, ctypes.POINTER(Camera_t),
+                            ctypes.POINTER(Layout_t), ctypes.POINTER(Grads_t), ctypes.c_int32, P],
+                           ctypes.c_int),
     "ivr_bin_sort_cull": ([ctypes.c_int64, P, P, P, P, ctypes.c_int32, ctypes.c_int32,
                            ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P, ctypes.c_size_t, P,
                            P, P, P], ctypes.c_int),

@@ -1,0 +1,625 @@
+// K4 -- backward pass.
+//
+// K4a blend_bwd_kernel replaces _kernels.composite_backward
+// (_kernels.py:75-135) + the per-Gaussian np.add.at reductions
+// (rasterizer.py:240-243).  One CTA per tile, one thread per pixel; pairs are
+// staged through shared memory exactly as in K3 and each pixel walks its
+// contributors FRONT to back up to last_pos (known from the forward).  With
+// C = forward output and A_i = colour accumulated through contributor i, the
+// colour behind i is C - A_i, so
+//   dL/dalpha_i = sum_k dout_k (T_i v_ik - (C_k - A_ik) / (1 - alpha_i)),
+// the same quantity the reference obtains by walking back to front and
+// recovering T by division.  Decisions (skip / contribute) use the certified
+// float32-with-bound test of K3, so the contributor set is the reference's.
+// Per (splat, warp) the 32 pixel contributions are warp-reduced and added
+// with one float32 atomic per component.
+//
+// K4b preprocess_bwd_kernel (one thread per Gaussian, float64) chains the
+// per-Gaussian accumulators through conic -> cov2d, the channel unpack,
+// project_backward, the opacity logit, and optionally shade_backward with
+// the inverse-fitting per-scene reductions.
+#include <math.h>
+
+#include "project.cuh"
+
+namespace ivr {
+
+constexpr int kBwdThreads = 256;
+constexpr float kSigmaErrB = 4.0e-7f;
+
+struct BwdArgs {
+    const int32_t *ranges, *pair_splat;
+    int ntx;
+    const float4 *rec;
+    const float *values;
+    const double *rec64;
+    int K, W, H;
+    const float *out;
+    const int32_t *last_pos;
+    const float *d_out;
+    float *g_values, *g_mean, *g_conic, *g_opac;
+    int preculled;
+};
+
+__device__ __forceinline__ double exact_alpha_b(double dpx, double dpy, double mx, double my,
+                                                double ca, double cb, double cc, double o,
+                                                double &alpha_u, double &g) {
+    const double ddx = dsub(dpx, mx), ddy = dsub(dpy, my);
+    const double sg = dadd(dmul(0.5, dadd(dmul(dmul(ca, ddx), ddx), dmul(dmul(cc, ddy), ddy))),
+                           dmul(dmul(cb, ddx), ddy));
+    if (sg < 0.0) return -1.0;
+    g = exp(-sg);
+    alpha_u = dmul(o, g);
+    double al = alpha_u;
+    if (al > kAlphaCap) al = kAlphaCap;
+    if (al < kAlphaSkip) return -1.0;
+    return al;
+}
+
+__device__ __forceinline__ float warp_sum(float x) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) x += __shfl_xor_sync(0xffffffffu, x, o);
+    return x;
+}
+
+template <int KMAX, bool F64>
+__global__ void __launch_bounds__(kBwdThreads)
+blend_bwd_kernel(BwdArgs A) {
+    extern __shared__ __align__(16) unsigned char smem[];
+    float4 *s_r0 = reinterpret_cast<float4 *>(smem);
+    float4 *s_r1 = s_r0 + kBwdThreads;
+    int *s_j = reinterpret_cast<int *>(s_r1 + kBwdThreads);
+    int *s_sp = s_j + kBwdThreads;
+    float *s_v = reinterpret_cast<float *>(s_sp + kBwdThreads);
+    double *s_r64 = reinterpret_cast<double *>(s_v + kBwdThreads * KMAX);
+    __shared__ int s_wsum[kBwdThreads / 32];
+    __shared__ int s_end;
+
+    const int tile = blockIdx.x;
+    const int tx = tile % A.ntx, ty = tile / A.ntx;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    const int px = tx * kTile + (tid & 15), py = ty * kTile + (tid >> 4);
+    const bool inside = px < A.W && py < A.H;
+    const int s0 = A.ranges[tile];
+    const int K = A.K;
+    const int64_t pix = (int64_t)py * A.W + px;
+    const int last = inside ? A.last_pos[pix] : s0;
+    if (tid == 0) s_end = s0;
+    __syncthreads();
+    atomicMax(&s_end, last);
+    __syncthreads();
+    const int s_stop = s_end;  // no pixel of this tile contributes past here
+
+    float C[KMAX], acc[KMAX], dout[KMAX];
+#pragma unroll
+    for (int c = 0; c < KMAX; ++c) {
+        C[c] = (inside && c < K) ? A.out[pix * K + c] : 0.0f;
+        dout[c] = (inside && c < K) ? A.d_out[pix * K + c] : 0.0f;
+        acc[c] = 0.0f;
+    }
+    float T = 1.0f;
+    const float fpx = (float)px, fpy = (float)py;
+    const double dpx = (double)px, dpy = (double)py;
+
+    for (int base = s0; base < s_stop; base += kBwdThreads) {
+        __syncthreads();
+        const int j = base + tid;
+        bool keep = false;
+        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+        int sp = 0;
+        if (j < s_stop) {
+            sp = A.pair_splat[j];
+            keep = !A.preculled || sp >= 0;
+            if (keep) {
+                r0 = __ldg(A.rec + 2 * sp);
+                r1 = __ldg(A.rec + 2 * sp + 1);
+            }
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        if (lane == 0) s_wsum[warp] = __popc(m);
+        __syncthreads();
+        int off = 0, total = 0;
+#pragma unroll
+        for (int w = 0; w < kBwdThreads / 32; ++w) {
+            const int c = s_wsum[w];
+            off += (w < warp) ? c : 0;
+            total += c;
+        }
+        if (keep) {
+            const int q = off + __popc(m & lanemask_lt());
+            s_r0[q] = r0;
+            s_r1[q] = r1;
+            s_j[q] = j;
+            s_sp[q] = sp;
+            const float *v = A.values + (int64_t)K * sp;
+#pragma unroll
+            for (int c = 0; c < KMAX; ++c)
+                if (c < K) s_v[q * KMAX + c] = __ldg(v + c);
+            if (F64) {
+                const double *r = A.rec64 + 8 * (int64_t)sp;
+#pragma unroll
+                for (int c = 0; c < 6; ++c) s_r64[q * 6 + c] = __ldg(r + c);
+            }
+        }
+        __syncthreads();
+        for (int q = 0; q < total; ++q) {
+            const float4 a0 = s_r0[q];
+            const float4 a1 = s_r1[q];
+            bool contrib = false;
+            float al = 0.f, alu = 0.f, g = 0.f;
+            float dx = 0.f, dy = 0.f;
+            if (inside && s_j[q] < last) {
+                dx = fpx - a0.x;
+                dy = fpy - a0.y;
+                const float bdy = a1.y * dy, hcdy = a1.z * dy;
+                const float sig = fmaf(fmaf(a1.x, dx, bdy), dx, hcdy * dy);
+                if (!(sig > a0.w)) {
+                    float cdx = dx, cdy = dy, cbdy = bdy, chcdy = hcdy, csig = sig;
+                    if (F64) {
+                        cdx = (float)dsub(dpx, s_r64[q * 6]);
+                        cdy = (float)dsub(dpy, s_r64[q * 6 + 1]);
+                        cbdy = a1.y * cdy;
+                        chcdy = a1.z * cdy;
+                        csig = fmaf(fmaf(a1.x, cdx, cbdy), cdx, chcdy * cdy);
+                    }
+                    const float terms = fmaf(a1.x * cdx, cdx, fmaf(chcdy, cdy, fabsf(cbdy * cdx)));
+                    const float E = kSigmaErrB * terms + 1e-30f;
+                    const float thr = a1.w;
+                    const float tm = 2.4e-7f * fabsf(thr) + 1e-7f;
+                    if (csig - E > 0.0f && csig + E < thr - tm) {
+                        g = exp2f(-1.4426950408889634f * csig);
+                        alu = a0.z * g;
+                        al = fminf(alu, 0.99f);
+                        contrib = true;
+                    } else if (!(csig - E > thr + tm)) {
+                        double au, gd, ad;
+                        if (F64) {
+                            const double *r = s_r64 + q * 6;
+                            ad = exact_alpha_b(dpx, dpy, r[0], r[1], r[2], r[3], r[4], r[5], au, gd);
+                        } else {
+                            ad = exact_alpha_b(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
+                                               2.0 * (double)a1.z, a0.z, au, gd);
+                        }
+                        if (ad >= 0.0) {
+                            al = (float)ad;
+                            alu = (float)au;
+                            g = (float)gd;
+                            contrib = true;
+                        }
+                    }
+                    dx = cdx;
+                    dy = cdy;
+                }
+            }
+            // per-pixel contributions (zero when not contributing)
+            float gv[KMAX], gm0 = 0.f, gm1 = 0.f, gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, go = 0.f;
+#pragma unroll
+            for (int c = 0; c < KMAX; ++c) gv[c] = 0.f;
+            if (contrib) {
+                const float w = T * al;
+                const float inv = __frcp_rn(1.0f - al);
+                float d_alpha = 0.f;
+#pragma unroll
+                for (int c = 0; c < KMAX; ++c) {
+                    if (c < K) {
+                        const float vk = s_v[q * KMAX + c];
+                        acc[c] = fmaf(w, vk, acc[c]);
+                        const float after = C[c] - acc[c];
+                        d_alpha = fmaf(dout[c], T * vk - after * inv, d_alpha);
+                        gv[c] = dout[c] * w;
+                    }
+                }
+                if (alu < 0.99f) {
+                    go = g * d_alpha;
+                    const float d_sigma = -alu * d_alpha;
+                    gc0 = 0.5f * dx * dx * d_sigma;
+                    gc1 = dx * dy * d_sigma;
+                    gc2 = 0.5f * dy * dy * d_sigma;
+                    const float ca = 2.0f * a1.x, cb = a1.y, cc = 2.0f * a1.z;
+                    gm0 = -d_sigma * (ca * dx + cb * dy);
+                    gm1 = -d_sigma * (cb * dx + cc * dy);
+                }
+                T = T * (1.0f - al);
+            }
+            if (__any_sync(0xffffffffu, contrib)) {
+                const int s = s_sp[q];
+#pragma unroll
+                for (int c = 0; c < KMAX; ++c) {
+                    if (c < K) {
+                        const float r = warp_sum(gv[c]);
+                        if (lane == 0 && r != 0.f) atomicAdd(A.g_values + (int64_t)K * s + c, r);
+                    }
+                }
+                const float r0s = warp_sum(gm0), r1s = warp_sum(gm1);
+                const float c0s = warp_sum(gc0), c1s = warp_sum(gc1), c2s = warp_sum(gc2);
+                const float os = warp_sum(go);
+                if (lane == 0) {
+                    if (r0s != 0.f) atomicAdd(A.g_mean + 2 * (int64_t)s, r0s);
+                    if (r1s != 0.f) atomicAdd(A.g_mean + 2 * (int64_t)s + 1, r1s);
+                    if (c0s != 0.f) atomicAdd(A.g_conic + 3 * (int64_t)s, c0s);
+                    if (c1s != 0.f) atomicAdd(A.g_conic + 3 * (int64_t)s + 1, c1s);
+                    if (c2s != 0.f) atomicAdd(A.g_conic + 3 * (int64_t)s + 2, c2s);
+                    if (os != 0.f) atomicAdd(A.g_opac + s, os);
+                }
+            }
+        }
+    }
+}
+
+template <int KMAX, bool F64>
+int launch_bwd(const BwdArgs &A, int ntiles, cudaStream_t st) {
+    const size_t sm = (size_t)kBwdThreads * (16 + 16 + 4 + 4 + 4 * KMAX) +
+                      (F64 ? (size_t)kBwdThreads * 48 : 0);
+    auto fn = blend_bwd_kernel<KMAX, F64>;
+    if (sm > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+    fn<<<ntiles, kBwdThreads, sm, st>>>(A);
+    return check_launch("blend_bwd_kernel");
+}
+
+// ----------------------------------------------------------------- K4b helpers
+__device__ __forceinline__ void normalize_bwd(const double v[3], const double d[3], double out[3]) {
+    // _mathutil.normalize_rows_backward: (d - (d.u) u) / |v|
+    const double n = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    const double u[3] = {v[0] / n, v[1] / n, v[2] / n};
+    const double pr = d[0] * u[0] + d[1] * u[1] + d[2] * u[2];
+    for (int k = 0; k < 3; ++k) out[k] = (d[k] - pr * u[k]) / n;
+}
+
+__device__ __forceinline__ double sgn(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
+
+// bad[id] = first row with a non-finite value in output tensor `id`
+__device__ __forceinline__ void flag_bad(unsigned long long *bad, int64_t i, int id, double x) {
+    if (bad && !isfinite(x)) atomicMin(bad + id, (unsigned long long)i);
+}
+
+struct BwdConst {
+    ivr_gaussians G;
+    ivr_shading S;
+    int has_shading;
+    ivr_edits E;
+    int has_edits;
+    ivr_layout L;
+    ivr_grads R;
+    int geometry;
+};
+
+__global__ void __launch_bounds__(128)
+preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *__restrict__ Pd) {
+    __shared__ ivr_frame_params P;
+    __shared__ double s_glob[10];
+    extern __shared__ double s_scene[];  // [S][4] per-scene d_c_p (3) + d_scale
+    {
+        const ivr_frame_params *src = Pd ? Pd : &Pv;
+        constexpr int kWords = (int)(sizeof(ivr_frame_params) / 4);
+        for (int w = threadIdx.x; w < kWords; w += blockDim.x)
+            reinterpret_cast<int *>(&P)[w] = reinterpret_cast<const int *>(src)[w];
+        if (threadIdx.x < 10) s_glob[threadIdx.x] = 0.0;
+    }
+    const int nsc = B.R.per_scene;  // number of per-scene slots in s_scene (0 = none)
+    for (int k = threadIdx.x; k < 4 * nsc; k += blockDim.x) s_scene[k] = 0.0;
+    __syncthreads();
+    const ivr_gaussians &G = B.G;
+    const ivr_grads &R = B.R;
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i < G.n) {
+        const ivr_camera &cam = P.cam;
+        const int K = B.L.k;
+        const int32_t sid = (B.has_edits && B.E.scene_id) ? B.E.scene_id[i] : 0;
+        // ---- per-Gaussian upstream from K4a
+        double gv_color[3] = {0, 0, 0}, gv_depth = 0.0, gv_norm[3] = {0, 0, 0};
+        double gmean[2] = {0, 0}, gcon[3] = {0, 0, 0}, gop = 0.0;
+        if (R.g_values) {
+            const float *gv = R.g_values + (int64_t)K * i;
+            if (B.L.col_color >= 0) for (int k = 0; k < 3; ++k) gv_color[k] = gv[B.L.col_color + k];
+            if (B.L.col_depth >= 0) gv_depth = gv[B.L.col_depth];
+            if (B.L.col_normal >= 0) for (int k = 0; k < 3; ++k) gv_norm[k] = gv[B.L.col_normal + k];
+            if (R.d_values) for (int c = 0; c < K; ++c) R.d_values[(int64_t)K * i + c] = gv[c];
+        }
+        if (R.g_mean2d) { gmean[0] = R.g_mean2d[2 * i]; gmean[1] = R.g_mean2d[2 * i + 1]; }
+        if (R.g_conic) for (int k = 0; k < 3; ++k) gcon[k] = R.g_conic[3 * i + k];
+        if (R.g_opacity) gop = R.g_opacity[i];
+        if (R.d_colors) for (int k = 0; k < 3; ++k) R.d_colors[3 * i + k] = gv_color[k];
+        if (R.d_mean2d) { R.d_mean2d[2 * i] = gmean[0]; R.d_mean2d[2 * i + 1] = gmean[1]; }
+        for (int k = 0; k < 3; ++k) flag_bad(R.bad, i, 5, gv_color[k]);
+
+        double d_mu[3] = {0, 0, 0}, d_n_raw[3] = {0, 0, 0};
+        const double nraw[3] = {G.n_raw[3 * i], G.n_raw[3 * i + 1], G.n_raw[3 * i + 2]};
+        if (B.L.col_normal >= 0 && R.g_values) normalize_bwd(nraw, gv_norm, d_n_raw);
+
+        // ---- opacity: effective logit chain (rasterizer.py:278-279) + inverse scale
+        const bool rescale = B.has_edits && P.rescale_opacity && B.E.opacity_scale;
+        const double scale = rescale ? B.E.opacity_scale[sid] : 1.0;
+        const double o_base = sigmoid_ref(G.o_logit[i]);
+        double pcl = o_base, o_eff = o_base;
+        bool open_gate = true;
+        if (rescale) {
+            const double praw = scale * o_base;
+            pcl = praw < 1e-12 ? 1e-12 : (praw > 1.0 - 1e-9 ? 1.0 - 1e-9 : praw);
+            open_gate = (praw > 1e-12) && (praw < 1.0 - 1e-9);
+            o_eff = sigmoid_ref(log(pcl / (1.0 - pcl)));
+        }
+        const double d_o_logit = gop * o_eff * (1.0 - o_eff);
+        if (R.d_o_logit) R.d_o_logit[i] = d_o_logit;
+        flag_bad(R.bad, i, 3, d_o_logit);
+        if (R.d_scale && nsc > 0) {
+            const double d_p = d_o_logit / (pcl * (1.0 - pcl));
+            const double ds = open_gate ? d_p * o_base : 0.0;
+            atomicAdd(&s_scene[4 * sid + 3], ds);
+        }
+
+        // ---- geometry (gaussians.project_backward)
+        if (B.geometry) {
+            Proj p;
+            project_one(G, i, cam, p);
+            double dq[4] = {0, 0, 0, 0}, dls[3] = {0, 0, 0};
+            if (p.valid) {
+                // conic -> cov2d: dC = -Q dQ Q (symmetric split of the b term)
+                const double Q[4] = {p.conic[0], p.conic[1], p.conic[1], p.conic[2]};
+                const double dQ[4] = {gcon[0], 0.5 * gcon[1], 0.5 * gcon[1], gcon[2]};
+                double T1[4], dC[4];
+                for (int r = 0; r < 2; ++r)
+                    for (int c = 0; c < 2; ++c)
+                        T1[2 * r + c] = Q[2 * r] * dQ[c] + Q[2 * r + 1] * dQ[2 + c];
+                for (int r = 0; r < 2; ++r)
+                    for (int c = 0; c < 2; ++c)
+                        dC[2 * r + c] = -(T1[2 * r] * Q[c] + T1[2 * r + 1] * Q[2 + c]);
+                const double *W = cam.rotation;
+                const double f = cam.focal, tz = p.tzs;
+                // d_cov3d = M^T dC M ; dM = dC M C3^T + dC^T M C3
+                double MtdC[6];  // (3x2) = M^T dC
+                for (int a = 0; a < 3; ++a)
+                    for (int c = 0; c < 2; ++c)
+                        MtdC[2 * a + c] = p.M[a] * dC[c] + p.M[3 + a] * dC[2 + c];
+                double dC3[9];
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b)
+                        dC3[3 * a + b] = MtdC[2 * a] * p.M[b] + MtdC[2 * a + 1] * p.M[3 + b];
+                double dM[6];
+                for (int r = 0; r < 2; ++r)
+                    for (int c = 0; c < 3; ++c) {
+                        double acc = 0.0;
+                        for (int m = 0; m < 2; ++m)
+                            for (int k = 0; k < 3; ++k) {
+                                acc += dC[2 * r + m] * p.M[3 * m + k] * p.C3[3 * c + k];
+                                acc += dC[2 * m + r] * p.M[3 * m + k] * p.C3[3 * k + c];
+                            }
+                        dM[3 * r + c] = acc;
+                    }
+                double dJ[6];
+                for (int r = 0; r < 2; ++r)
+                    for (int k = 0; k < 3; ++k)
+                        dJ[3 * r + k] = dM[3 * r] * W[3 * k] + dM[3 * r + 1] * W[3 * k + 1] +
+                                        dM[3 * r + 2] * W[3 * k + 2];
+                const double tz2 = tz * tz, tz3 = tz2 * tz;
+                double dt[3];
+                dt[0] = dJ[2] * (-f / tz2) + gmean[0] * f / tz;
+                dt[1] = dJ[5] * (-f / tz2) + gmean[1] * f / tz;
+                dt[2] = dJ[0] * (-f / tz2) + dJ[4] * (-f / tz2) + dJ[2] * (2 * f * p.t[0] / tz3) +
+                        dJ[5] * (2 * f * p.t[1] / tz3) - gmean[0] * f * p.t[0] / tz2 -
+                        gmean[1] * f * p.t[1] / tz2 + gv_depth;
+                for (int j = 0; j < 3; ++j)
+                    d_mu[j] += dt[0] * W[j] + dt[1] * W[3 + j] + dt[2] * W[6 + j];
+                // covariance_backward (gaussians.py:278-289)
+                double Gs[9], dM3[9];
+                for (int a = 0; a < 3; ++a)
+                    for (int b = 0; b < 3; ++b) Gs[3 * a + b] = dC3[3 * a + b] + dC3[3 * b + a];
+                for (int a = 0; a < 3; ++a)
+                    for (int k = 0; k < 3; ++k) {
+                        double acc = 0.0;
+                        for (int b = 0; b < 3; ++b) acc += Gs[3 * a + b] * p.R[3 * b + k] * p.s[k];
+                        dM3[3 * a + k] = acc;
+                    }
+                double ds[3] = {0, 0, 0}, dR[9];
+                for (int k = 0; k < 3; ++k)
+                    for (int a = 0; a < 3; ++a) {
+                        ds[k] += dM3[3 * a + k] * p.R[3 * a + k];
+                        dR[3 * a + k] = dM3[3 * a + k] * p.s[k];
+                    }
+                // quat_to_rot_backward (gaussians.py:239-264)
+                const double w = p.q[0], x = p.q[1], y = p.q[2], z = p.q[3];
+                const double *g = dR;
+                const double qw = 2 * (-z * g[1] + y * g[2] + z * g[3] - x * g[5] - y * g[6] + x * g[7]);
+                const double qx = 2 * (y * g[1] + z * g[2] + y * g[3] - 2 * x * g[4] - w * g[5] +
+                                       z * g[6] + w * g[7] - 2 * x * g[8]);
+                const double qy = 2 * (-2 * y * g[0] + x * g[1] + w * g[2] + x * g[3] + z * g[5] -
+                                       w * g[6] + z * g[7] - 2 * y * g[8]);
+                const double qz = 2 * (-2 * z * g[0] - w * g[1] + x * g[2] + w * g[3] - 2 * z * g[4] +
+                                       y * g[5] + x * g[6] + y * g[7]);
+                const double qraw[4] = {G.q_raw[4 * i], G.q_raw[4 * i + 1], G.q_raw[4 * i + 2],
+                                        G.q_raw[4 * i + 3]};
+                const double qn = sqrt(qraw[0] * qraw[0] + qraw[1] * qraw[1] + qraw[2] * qraw[2] +
+                                       qraw[3] * qraw[3]);
+                const double dqv[4] = {qw, qx, qy, qz};
+                double pr = 0.0;
+                for (int k = 0; k < 4; ++k) pr += dqv[k] * (qraw[k] / qn);
+                for (int k = 0; k < 4; ++k) dq[k] = (dqv[k] - pr * (qraw[k] / qn)) / qn;
+                for (int k = 0; k < 3; ++k) dls[k] = ds[k] * p.s[k];
+            }
+            if (R.d_q_raw) for (int k = 0; k < 4; ++k) R.d_q_raw[4 * i + k] = dq[k];
+            if (R.d_log_s) for (int k = 0; k < 3; ++k) R.d_log_s[3 * i + k] = dls[k];
+            for (int k = 0; k < 4; ++k) flag_bad(R.bad, i, 1, dq[k]);
+            for (int k = 0; k < 3; ++k) flag_bad(R.bad, i, 2, dls[k]);
+        }
+
+        // ---- shading (shading.shade_backward)
+        if (B.has_shading) {
+            const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
+            double nrm[3];
+            unit_normal(G, i, nrm);
+            ShadeState st;
+            shade_state(B.S, P, i, sid, mu, nrm, st);
+            double d_rgb[3];
+            for (int k = 0; k < 3; ++k)
+                d_rgb[k] = gv_color[k] + (R.d_rgb_extra ? R.d_rgb_extra[3 * i + k] : 0.0);
+            const double s3 = d_rgb[0] + d_rgb[1] + d_rgb[2];
+            const double dot_cv = d_rgb[0] * st.c_v[0] + d_rgb[1] * st.c_v[1] + d_rgb[2] * st.c_v[2];
+            const double k_a = st.k[0], k_d = st.k[1], k_s = st.k[2], beta = st.k[3];
+            double d_c_v[3];
+            for (int k = 0; k < 3; ++k) d_c_v[k] = (k_a + k_d * st.a_ndl) * d_rgb[k];
+            const double d_k_a = dot_cv, d_k_d = st.a_ndl * dot_cv, d_k_s = st.spow * s3;
+            const double d_spow = k_s * s3;
+            const bool safe = st.a_ndh > 0.0;
+            const double log_andh = log(safe ? st.a_ndh : 1.0);
+            const double d_a_ndh = (st.gate && safe) ? d_spow * beta * exp((beta - 1.0) * log_andh) : 0.0;
+            const double d_beta = (st.gate && safe) ? d_spow * st.spow * log_andh : 0.0;
+            const double d_a_ndl = k_d * dot_cv;
+            const double d_ndl = sgn(st.ndl) * d_a_ndl, d_ndh = sgn(st.ndh) * d_a_ndh;
+            double d_n_unit[3], d_l[3], d_h[3], d_v[3];
+            for (int k = 0; k < 3; ++k) {
+                d_n_unit[k] = d_ndl * st.l[k] + d_ndh * st.h[k];
+                d_l[k] = d_ndl * nrm[k];
+                d_h[k] = d_ndh * nrm[k];
+            }
+            if (!P.orbital) {
+                for (int k = 0; k < 3; ++k) d_v[k] = d_h[k] + d_l[k];
+            } else {
+                double d_u[3];
+                normalize_bwd(st.u, d_h, d_u);
+                for (int k = 0; k < 3; ++k) {
+                    d_v[k] = d_u[k];
+                    d_l[k] += d_u[k];
+                }
+                double dp = 0.0, da = 0.0;
+                for (int k = 0; k < 3; ++k) {
+                    dp += d_l[k] * R.dl_dp[k];
+                    da += d_l[k] * R.dl_da[k];
+                }
+                atomicAdd(&s_glob[8], dp);
+                atomicAdd(&s_glob[9], da);
+            }
+            double d_w[3];
+            normalize_bwd(st.w_cam, d_v, d_w);
+            for (int k = 0; k < 3; ++k) d_mu[k] -= d_w[k];
+            double d_nr2[3];
+            normalize_bwd(nraw, d_n_unit, d_nr2);
+            for (int k = 0; k < 3; ++k) d_n_raw[k] += d_nr2[k];
+            const double e_a = d_k_a * P.term_scales[0] * (st.gates[0] ? 1.0 : 0.0);
+            const double e_d = d_k_d * P.term_scales[1] * (st.gates[1] ? 1.0 : 0.0);
+            const double e_s = d_k_s * P.term_scales[2] * (st.gates[2] ? 1.0 : 0.0);
+            const double e_b = d_beta * P.term_scales[3] * (st.gates[3] ? 1.0 : 0.0);
+            atomicAdd(&s_glob[0], e_a * st.sig[0]);
+            atomicAdd(&s_glob[1], e_d * st.sig[1]);
+            atomicAdd(&s_glob[2], e_s * st.sig[2]);
+            atomicAdd(&s_glob[3], e_b * st.beta1);
+            atomicAdd(&s_glob[4], e_a);
+            atomicAdd(&s_glob[5], e_d);
+            atomicAdd(&s_glob[6], e_s);
+            atomicAdd(&s_glob[7], e_b);
+            const double dka = e_a * P.lam[0] * st.sig[0] * (1.0 - st.sig[0]);
+            const double dkd = e_d * P.lam[1] * st.sig[1] * (1.0 - st.sig[1]);
+            const double dks = e_s * P.lam[2] * st.sig[2] * (1.0 - st.sig[2]);
+            const double dlb = e_b * P.lam[3] * (st.beta1 - 1.0);
+            if (R.d_k_a_raw) R.d_k_a_raw[i] = dka;
+            if (R.d_k_d_raw) R.d_k_d_raw[i] = dkd;
+            if (R.d_k_s_raw) R.d_k_s_raw[i] = dks;
+            if (R.d_log_beta) R.d_log_beta[i] = dlb;
+            double dco[3];
+            for (int k = 0; k < 3; ++k) dco[k] = st.open[k] ? d_c_v[k] : 0.0;
+            if (R.d_delta_c) for (int k = 0; k < 3; ++k) R.d_delta_c[3 * i + k] = dco[k];
+            if (R.d_c_p) {
+                if (nsc > 0) {
+                    for (int k = 0; k < 3; ++k) atomicAdd(&s_scene[4 * sid + k], dco[k]);
+                } else {
+                    for (int k = 0; k < 3; ++k) R.d_c_p[3 * i + k] = dco[k];
+                }
+            }
+            flag_bad(R.bad, i, 6, dka);
+            flag_bad(R.bad, i, 7, dkd);
+            flag_bad(R.bad, i, 8, dks);
+            flag_bad(R.bad, i, 9, dlb);
+            for (int k = 0; k < 3; ++k) flag_bad(R.bad, i, 10, dco[k]);
+        }
+        if (R.d_mu) for (int k = 0; k < 3; ++k) R.d_mu[3 * i + k] = d_mu[k];
+        if (R.d_n_raw) for (int k = 0; k < 3; ++k) R.d_n_raw[3 * i + k] = d_n_raw[k];
+        for (int k = 0; k < 3; ++k) {
+            flag_bad(R.bad, i, 0, d_mu[k]);
+            flag_bad(R.bad, i, 4, d_n_raw[k]);
+        }
+    }
+    __syncthreads();
+    if (R.d_globals && B.has_shading && threadIdx.x < 10) atomicAdd(&R.d_globals[threadIdx.x], s_glob[threadIdx.x]);
+    for (int k = threadIdx.x; k < 4 * nsc; k += blockDim.x) {
+        const double v = s_scene[k];
+        if (v == 0.0) continue;
+        if ((k & 3) == 3) {
+            if (R.d_scale) atomicAdd(&R.d_scale[k >> 2], v);
+        } else if (R.d_c_p) {
+            atomicAdd(&R.d_c_p[3 * (k >> 2) + (k & 3)], v);
+        }
+    }
+}
+
+ivr_frame_params params_from(const ivr_camera &cam, const ivr_shading *S, const ivr_edits *E);
+
+}  // namespace ivr
+
+extern "C" int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
+                             int32_t nty, const float *rec, const float *values,
+                             const double *rec64, int32_t k, int32_t width, int32_t height,
+                             const float *out, const int32_t *last_pos, const float *d_out,
+                             float *g_values, float *g_mean2d, float *g_conic, float *g_opacity,
+                             int32_t flags, ivr_stream_t stream) {
+    using namespace ivr;
+    if (!tile_ranges || !pair_splat || !rec || !values || !out || !last_pos || !d_out ||
+        !g_values || !g_mean2d || !g_conic || !g_opacity || k < 1 || k > 32 ||
+        ntx != (width + kTile - 1) / kTile || nty != (height + kTile - 1) / kTile) {
+        set_error("ivr_blend_bwd: bad argument");
+        return IVR_ERR_ARG;
+    }
+    BwdArgs A;
+    A.ranges = tile_ranges;
+    A.pair_splat = pair_splat;
+    A.ntx = ntx;
+    A.rec = reinterpret_cast<const float4 *>(rec);
+    A.values = values;
+    A.rec64 = rec64;
+    A.K = k;
+    A.W = width;
+    A.H = height;
+    A.out = out;
+    A.last_pos = last_pos;
+    A.d_out = d_out;
+    A.g_values = g_values;
+    A.g_mean = g_mean2d;
+    A.g_conic = g_conic;
+    A.g_opac = g_opacity;
+    A.preculled = (flags & IVR_BLEND_PRECULLED) ? 1 : 0;
+    cudaStream_t st = (cudaStream_t)stream;
+    const int nt = ntx * nty;
+    const bool f64 = rec64 != nullptr;
+#define IVR_BWD(KM) return f64 ? launch_bwd<KM, true>(A, nt, st) : launch_bwd<KM, false>(A, nt, st)
+    if (k <= 4) { IVR_BWD(4); }
+    if (k <= 8) { IVR_BWD(8); }
+    if (k <= 16) { IVR_BWD(16); }
+    IVR_BWD(32);
+#undef IVR_BWD
+}
+
+extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *shading,
+                                  const ivr_edits *edits, const ivr_frame_params *params,
+                                  const ivr_camera *cam, const ivr_layout *layout, ivr_grads *grads,
+                                  int32_t geometry, ivr_stream_t stream) {
+    using namespace ivr;
+    if (!g || !layout || !grads || (!params && !cam) || g->n < 0 || grads->per_scene < 0 ||
+        grads->per_scene > 1024) {
+        set_error("ivr_preprocess_bwd: bad argument");
+        return IVR_ERR_ARG;
+    }
+    if (g->n == 0) return IVR_OK;
+    BwdConst B{};
+    B.G = *g;
+    if (shading) B.S = *shading;
+    B.has_shading = shading != nullptr;
+    if (edits) B.E = *edits;
+    B.has_edits = edits != nullptr;
+    B.L = *layout;
+    B.R = *grads;
+    B.geometry = geometry;
+    ivr_frame_params Pv{};
+    if (!params) Pv = params_from(*cam, shading, edits);
+    const int threads = 128;
+    const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
+    const size_t sm = (size_t)grads->per_scene * 4 * sizeof(double);
+    preprocess_bwd_kernel<<<blocks, threads, sm, (cudaStream_t)stream>>>(B, Pv, params);
+    return check_launch("preprocess_bwd_kernel");
+}

@@ -6,69 +6,14 @@
 //   gaussians.project_gaussians  gaussians.py:296-346 (EWA, dgemm FMA chains)
 //   rasterizer.rasterize_forward rasterizer.py:88-121 (radius/rect/count),
 //                                rasterizer.py:134-153 (f32 packing)
-// and emits the float32 blend record plus the conservative sigma threshold
-// `hi` that lets the blend skip a pair in float32 only when the reference's
-// float64 alpha test certainly skips it.
+// and emits the float32 blend record plus the conservative exponent bound
+// `hi` (sigma32 > hi implies the reference's float64 alpha < 1/255) and the
+// alpha-skip exponent thr = ln(255 o) used by K3.
 #include <math.h>
 
-#include "ivr_common.cuh"
+#include "project.cuh"
 
 namespace ivr {
-
-struct ShadeOut {
-    double rgb[3];
-    double amb[3], dif[3], spec;
-};
-
-// shading.py:236-297 for one splat.  `nrm` is the unit normal (eps 1e-12).
-__device__ __forceinline__ void shade_one(const ivr_shading &S, const ivr_frame_params &P,
-                                          int64_t i, int32_t sid, const double mu[3],
-                                          const double nrm[3], ShadeOut &o) {
-    const ivr_camera &cam = P.cam;
-    double w[3] = {dsub(cam.position[0], mu[0]), dsub(cam.position[1], mu[1]),
-                   dsub(cam.position[2], mu[2])};
-    const double wn = dmax(norm3(w[0], w[1], w[2]), 1e-12);
-    const double v[3] = {ddiv(w[0], wn), ddiv(w[1], wn), ddiv(w[2], wn)};
-    double l[3], h[3];
-    if (!P.orbital) {
-        for (int k = 0; k < 3; ++k) l[k] = h[k] = v[k];
-    } else {
-        double u[3];
-        for (int k = 0; k < 3; ++k) {
-            l[k] = P.light_dir[k];
-            u[k] = dadd(v[k], l[k]);
-        }
-        const double un = dmax(norm3(u[0], u[1], u[2]), 1e-12);
-        for (int k = 0; k < 3; ++k) h[k] = ddiv(u[k], un);
-    }
-    const double sa = sigmoid_ref(S.k_a_raw[i]);
-    const double sd = sigmoid_ref(S.k_d_raw[i]);
-    const double ss = sigmoid_ref(S.k_s_raw[i]);
-    const double beta1 = dadd(exp(S.log_beta[i]), 1.0);
-    const double ta = dadd(dmul(P.lam[0], sa), P.b[0]);
-    const double td = dadd(dmul(P.lam[1], sd), P.b[1]);
-    const double tsp = dadd(dmul(P.lam[2], ss), P.b[2]);
-    const double tb = dadd(dmul(P.lam[3], beta1), P.b[3]);
-    const double k_a = dmul(P.term_scales[0], clip01(ta));
-    const double k_d = dmul(P.term_scales[1], clip01(td));
-    const double k_s = dmul(P.term_scales[2], clip01(tsp));
-    const double beta = dmul(P.term_scales[3], dmax(tb, 1.0));
-    const double *cp = S.per_splat_palette ? S.palette + 3 * i : S.palette + 3 * (int64_t)sid;
-    double cv[3];
-    for (int k = 0; k < 3; ++k) cv[k] = clip01(dadd(cp[k], S.delta_c[3 * i + k]));
-    const double a_ndl = fabs(dot3(nrm, l));
-    const double a_ndh = fabs(dot3(nrm, h));
-    double spow = 0.0;
-    if (a_ndh > 0.0) spow = pow(dmax(a_ndh, 1e-300), beta);
-    if (!(a_ndl > 0.0)) spow = 0.0;
-    const double kdl = dmul(k_d, a_ndl);
-    o.spec = dmul(dmul(k_s, spow), 1.0);
-    for (int k = 0; k < 3; ++k) {
-        o.amb[k] = dmul(k_a, cv[k]);
-        o.dif[k] = dmul(kdl, cv[k]);
-        o.rgb[k] = dadd(dadd(o.amb[k], o.dif[k]), o.spec);
-    }
-}
 
 __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr_shading &S,
                                                int has_shading, const ivr_edits &E, int has_edits,
@@ -76,77 +21,15 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
                                                const ivr_proj_out &O, int f64_mode, int64_t i) {
     const ivr_camera &cam = P.cam;
     const int32_t sid = (has_edits && E.scene_id) ? E.scene_id[i] : 0;
+    const bool rescale = has_edits && P.rescale_opacity && E.opacity_scale;
+    const double opacity =
+        effective_opacity(G.o_logit[i], rescale, rescale ? E.opacity_scale[sid] : 1.0);
 
-    // ---- effective opacity (scene.py:214-220; every splat when any scale != 1)
-    double o_logit = G.o_logit[i];
-    if (has_edits && P.rescale_opacity && E.opacity_scale) {
-        double p = dmul(E.opacity_scale[sid], sigmoid_ref(o_logit));
-        p = p < 1e-12 ? 1e-12 : (p > 1.0 - 1e-9 ? 1.0 - 1e-9 : p);
-        o_logit = log(ddiv(p, dsub(1.0, p)));
-    }
-    const double opacity = sigmoid_ref(o_logit);
-
-    // ---- projection (gaussians.py:302-339)
-    const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
-    const double qr[4] = {G.q_raw[4 * i], G.q_raw[4 * i + 1], G.q_raw[4 * i + 2],
-                          G.q_raw[4 * i + 3]};
-    const double qn = norm4(qr[0], qr[1], qr[2], qr[3]);
-    const double qw = ddiv(qr[0], qn), qx = ddiv(qr[1], qn), qy = ddiv(qr[2], qn),
-                 qz = ddiv(qr[3], qn);
-    const double s[3] = {exp(G.log_s[3 * i]), exp(G.log_s[3 * i + 1]), exp(G.log_s[3 * i + 2])};
-    const double *W = cam.rotation;
-    const double d[3] = {dsub(mu[0], cam.position[0]), dsub(mu[1], cam.position[1]),
-                         dsub(mu[2], cam.position[2])};
-    double t[3];
-    for (int j = 0; j < 3; ++j) t[j] = chain3(d[0], W[3 * j], d[1], W[3 * j + 1], d[2], W[3 * j + 2]);
-    const double tz = t[2];
-    bool valid = tz > kNearPlane;
-    const double tzs = valid ? tz : 1.0;
-    const double f = cam.focal;
-    const double mx = dadd(ddiv(dmul(f, t[0]), tzs), cam.cx);
-    const double my = dadd(ddiv(dmul(f, t[1]), tzs), cam.cy);
-
-    // quat_to_rot (gaussians.py:222-236)
-    double R[9];
-    R[0] = dsub(1.0, dmul(2.0, dadd(dmul(qy, qy), dmul(qz, qz))));
-    R[1] = dmul(2.0, dsub(dmul(qx, qy), dmul(qw, qz)));
-    R[2] = dmul(2.0, dadd(dmul(qx, qz), dmul(qw, qy)));
-    R[3] = dmul(2.0, dadd(dmul(qx, qy), dmul(qw, qz)));
-    R[4] = dsub(1.0, dmul(2.0, dadd(dmul(qx, qx), dmul(qz, qz))));
-    R[5] = dmul(2.0, dsub(dmul(qy, qz), dmul(qw, qx)));
-    R[6] = dmul(2.0, dsub(dmul(qx, qz), dmul(qw, qy)));
-    R[7] = dmul(2.0, dadd(dmul(qy, qz), dmul(qw, qx)));
-    R[8] = dsub(1.0, dmul(2.0, dadd(dmul(qx, qx), dmul(qy, qy))));
-    double M3[9];
-    for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) M3[3 * r + c] = dmul(R[3 * r + c], s[c]);
-    double C3[9];  // M3 @ M3^T
-    for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c)
-            C3[3 * r + c] = chain3(M3[3 * r], M3[3 * c], M3[3 * r + 1], M3[3 * c + 1],
-                                   M3[3 * r + 2], M3[3 * c + 2]);
-    double J[6] = {ddiv(f, tzs), 0.0, ddiv(dmul(-f, t[0]), dmul(tzs, tzs)),
-                   0.0, ddiv(f, tzs), ddiv(dmul(-f, t[1]), dmul(tzs, tzs))};
-    double M[6];  // J @ W
-    for (int r = 0; r < 2; ++r)
-        for (int c = 0; c < 3; ++c)
-            M[3 * r + c] = chain3(J[3 * r], W[c], J[3 * r + 1], W[3 + c], J[3 * r + 2], W[6 + c]);
-    double A[6];  // M @ cov3d
-    for (int r = 0; r < 2; ++r)
-        for (int c = 0; c < 3; ++c)
-            A[3 * r + c] = chain3(M[3 * r], C3[c], M[3 * r + 1], C3[3 + c], M[3 * r + 2], C3[6 + c]);
-    double C2[4];  // A @ M^T
-    for (int r = 0; r < 2; ++r)
-        for (int c = 0; c < 2; ++c)
-            C2[2 * r + c] = chain3(A[3 * r], M[3 * c], A[3 * r + 1], M[3 * c + 1], A[3 * r + 2],
-                                   M[3 * c + 2]);
-    C2[0] = dadd(C2[0], kCov2dDilation);
-    C2[3] = dadd(C2[3], kCov2dDilation);
-    const double ca = C2[0], cb = C2[1], cc = C2[3];
-    const double det = dsub(dmul(ca, cc), dmul(cb, cb));
-    const double dets = det > 0.0 ? det : 1.0;
-    const double q0 = ddiv(cc, dets), q1 = ddiv(-cb, dets), q2 = ddiv(ca, dets);
-    valid = valid && (det > 0.0);
+    Proj p;
+    project_one(G, i, cam, p);
+    const double tz = p.t[2];
+    const double mx = p.mx, my = p.my;
+    const double ca = p.C2[0], cb = p.C2[1], cc = p.C2[3];
 
     // ---- radius / visibility / tile rect (rasterizer.py:88-118)
     const double half_tr = dmul(0.5, dadd(ca, cc));
@@ -156,7 +39,7 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
     const double cut = sqrt(dmul(2.0, log(dmax(ddiv(opacity, kAlphaSkip), 1.0))));
     const double radius = dadd(ceil(dmul(sqrt(dmax(lam_max, 0.0)), cut)), 1.0);
     const int ntx = (cam.width + kTile - 1) / kTile, nty = (cam.height + kTile - 1) / kTile;
-    bool visible = valid && (opacity >= kAlphaSkip) && (radius > 0.0);
+    bool visible = p.valid && (opacity >= kAlphaSkip) && (radius > 0.0);
     visible = visible && (dadd(mx, radius) >= 0.0) && (dsub(mx, radius) < (double)cam.width) &&
               (dadd(my, radius) >= 0.0) && (dsub(my, radius) < (double)cam.height);
     auto tclip = [](double x, int hi) -> int {
@@ -179,19 +62,20 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
     rc.z = (unsigned short)ty0; rc.w = (unsigned short)(ty1 < 0 ? 0 : ty1);
     reinterpret_cast<ushort4 *>(O.rect)[i] = rc;
 
-    // ---- normals (GaussianGeometry.normals, eps 1e-12)
-    const double nr[3] = {G.n_raw[3 * i], G.n_raw[3 * i + 1], G.n_raw[3 * i + 2]};
-    const double nn = dmax(norm3(nr[0], nr[1], nr[2]), 1e-12);
-    const double nrm[3] = {ddiv(nr[0], nn), ddiv(nr[1], nn), ddiv(nr[2], nn)};
+    double nrm[3];
+    unit_normal(G, i, nrm);
+    ShadeState sh;
+    if (has_shading) {
+        const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
+        shade_state(S, P, i, sid, mu, nrm, sh);
+    }
 
-    ShadeOut sh;
-    if (has_shading) shade_one(S, P, i, sid, mu, nrm, sh);
-
-    // ---- float32 blend record (rasterizer.py:151-153 casts) + skip threshold
+    // ---- float32 blend record (rasterizer.py:151-153 casts) + skip bounds
     const float mx32 = (float)mx, my32 = (float)my;
-    const float a32 = (float)q0, b32 = (float)q1, c32 = (float)q2, o32 = (float)opacity;
+    const float a32 = (float)p.conic[0], b32 = (float)p.conic[1], c32 = (float)p.conic[2];
+    const float o32 = (float)opacity;
     float hi32 = __int_as_float(0x7f800000);  // +inf: always take the exact path
-    float thr32 = 0.0f;                         // ln(o / (1/255)): alpha-skip exponent
+    float thr32 = 0.0f;                         // ln(o / (1/255))
     {
         const double a = a32, b = b32, c = c32;
         const double oo = f64_mode ? opacity : (double)o32;
@@ -215,7 +99,8 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
     rec[1] = make_float4(0.5f * a32, b32, 0.5f * c32, thr32);
     if (O.rec64) {
         double *r = O.rec64 + 8 * i;
-        r[0] = mx; r[1] = my; r[2] = q0; r[3] = q1; r[4] = q2; r[5] = opacity; r[6] = tz; r[7] = 0.0;
+        r[0] = mx; r[1] = my; r[2] = p.conic[0]; r[3] = p.conic[1]; r[4] = p.conic[2];
+        r[5] = opacity; r[6] = tz; r[7] = 0.0;
     }
 
     // ---- packed values (rasterizer.py:134-149)
@@ -241,12 +126,12 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
 
     // ---- optional float64 parity outputs
     if (O.mean2d) { O.mean2d[2 * i] = mx; O.mean2d[2 * i + 1] = my; }
-    if (O.conic) { O.conic[3 * i] = q0; O.conic[3 * i + 1] = q1; O.conic[3 * i + 2] = q2; }
-    if (O.cov2d) for (int k = 0; k < 4; ++k) O.cov2d[4 * i + k] = C2[k];
+    if (O.conic) for (int k = 0; k < 3; ++k) O.conic[3 * i + k] = p.conic[k];
+    if (O.cov2d) for (int k = 0; k < 4; ++k) O.cov2d[4 * i + k] = p.C2[k];
     if (O.depth) O.depth[i] = tz;
     if (O.opacity) O.opacity[i] = opacity;
     if (O.radius) O.radius[i] = radius;
-    if (O.valid) O.valid[i] = valid ? 1 : 0;
+    if (O.valid) O.valid[i] = p.valid ? 1 : 0;
     if (O.rgb && has_shading) for (int k = 0; k < 3; ++k) O.rgb[3 * i + k] = sh.rgb[k];
 }
 
@@ -279,11 +164,10 @@ shade_kernel(ivr_gaussians G, ivr_shading S, const int32_t *scene_id, ivr_frame_
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
     if (i >= G.n) return;
     const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
-    const double nr[3] = {G.n_raw[3 * i], G.n_raw[3 * i + 1], G.n_raw[3 * i + 2]};
-    const double nn = dmax(norm3(nr[0], nr[1], nr[2]), 1e-12);
-    const double nrm[3] = {ddiv(nr[0], nn), ddiv(nr[1], nn), ddiv(nr[2], nn)};
-    ShadeOut sh;
-    shade_one(S, sp, i, scene_id ? scene_id[i] : 0, mu, nrm, sh);
+    double nrm[3];
+    unit_normal(G, i, nrm);
+    ShadeState sh;
+    shade_state(S, sp, i, scene_id ? scene_id[i] : 0, mu, nrm, sh);
     for (int k = 0; k < 3; ++k) rgb[3 * i + k] = sh.rgb[k];
     if (terms) {
         for (int k = 0; k < 3; ++k) {
@@ -304,6 +188,11 @@ ivr_frame_params params_from(const ivr_camera &cam, const ivr_shading *S, const 
             P.term_scales[k] = S->term_scales[k];
             P.lam[k] = S->lam[k];
             P.b[k] = S->b[k];
+        }
+    } else {
+        for (int k = 0; k < 4; ++k) {
+            P.term_scales[k] = 1.0;
+            P.lam[k] = 1.0;
         }
     }
     P.rescale_opacity = E ? E->rescale_opacity : 0;

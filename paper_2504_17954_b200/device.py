@@ -279,6 +279,96 @@ def blend(F: Frame, ws: Workspace, want_state=True, stream=None, out=None, exact
     return F
 
 
+def blend_backward(F: Frame, d_out, stream=None):
+    """K4a: per-Gaussian float32 accumulators from the upstream image gradient
+    d_out (H,W,K float32 device tensor)."""
+    n, K = F.n, F.K
+    dev = F.depth_key.device
+    g = {"values": torch.zeros(n * K, dtype=torch.float32, device=dev),
+         "mean2d": torch.zeros(2 * n, dtype=torch.float32, device=dev),
+         "conic": torch.zeros(3 * n, dtype=torch.float32, device=dev),
+         "opacity": torch.zeros(n, dtype=torch.float32, device=dev)}
+    out = F.out if not F.f64 else F.out64.float()
+    d_out = d_out.to(torch.float32).contiguous()
+    cam = F.cam
+    L.check(L.lib().ivr_blend_bwd(ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec),
+                                  ptr(F.values), ptr(F.rec64), K, cam.width, cam.height, ptr(out),
+                                  ptr(F.last_pos), ptr(d_out), ptr(g["values"]), ptr(g["mean2d"]),
+                                  ptr(g["conic"]), ptr(g["opacity"]),
+                                  L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0,
+                                  stream_handle(stream)), "ivr_blend_bwd")
+    return g
+
+
+GRAD_SHAPES = {"d_mu": 3, "d_q_raw": 4, "d_log_s": 3, "d_o_logit": 1, "d_n_raw": 3, "d_colors": 3,
+               "d_mean2d": 2, "d_delta_c": 3, "d_k_a_raw": 1, "d_k_d_raw": 1, "d_k_s_raw": 1,
+               "d_log_beta": 1}
+
+
+def preprocess_backward(dg: DeviceGaussians, cam, K, cols, g=None, shading=None, edits=None,
+                        params_dev=None, d_rgb=None, geometry=True, want=(), per_scene=0,
+                        per_splat_c_p=False, light=None, stream=None):
+    """K4b: float64 per-Gaussian gradients.  Returns (dict of device tensors,
+    bad-row tensor)."""
+    n = dg.n
+    dev = dg.device
+    out = {}
+    R = L.Grads_t()
+    if g is not None:
+        R.g_values, R.g_mean2d = g["values"].data_ptr(), g["mean2d"].data_ptr()
+        R.g_conic, R.g_opacity = g["conic"].data_ptr(), g["opacity"].data_ptr()
+    if d_rgb is not None:
+        R.d_rgb_extra = d_rgb.data_ptr()
+    for name in want:
+        if name in GRAD_SHAPES:
+            out[name] = torch.zeros(n * GRAD_SHAPES[name], dtype=torch.float64, device=dev)
+            setattr(R, name, out[name].data_ptr())
+    if "d_values" in want:
+        out["d_values"] = torch.zeros(n * K, dtype=torch.float64, device=dev)
+        R.d_values = out["d_values"].data_ptr()
+    if "d_c_p" in want:
+        out["d_c_p"] = torch.zeros((n if per_splat_c_p else max(per_scene, 1)) * 3,
+                                   dtype=torch.float64, device=dev)
+        R.d_c_p = out["d_c_p"].data_ptr()
+    if "d_scale" in want:
+        out["d_scale"] = torch.zeros(max(per_scene, 1), dtype=torch.float64, device=dev)
+        R.d_scale = out["d_scale"].data_ptr()
+    if shading is not None:
+        out["d_globals"] = torch.zeros(10, dtype=torch.float64, device=dev)
+        R.d_globals = out["d_globals"].data_ptr()
+    R.per_scene = 0 if per_splat_c_p else int(per_scene)
+    if light is not None and light.mode == "orbital":
+        p, a = light.polar, light.azimuth
+        dp = (-np.sin(p) * np.cos(a), -np.sin(p) * np.sin(a), np.cos(p))
+        da = (-np.cos(p) * np.sin(a), np.cos(p) * np.cos(a), 0.0)
+        for i in range(3):
+            R.dl_dp[i], R.dl_da[i] = float(dp[i]), float(da[i])
+    bad = torch.full((16,), -1, dtype=torch.int64, device=dev)  # ~0 as uint64
+    R.bad = bad.data_ptr()
+    lay = L.Layout_t()
+    lay.k = K
+    lay.col_color, lay.col_alpha, lay.col_depth, lay.col_normal = cols
+    gs = dg.struct()
+    cs = camera_struct(cam)
+    L.check(L.lib().ivr_preprocess_bwd(
+        ctypes.byref(gs), ctypes.byref(shading) if shading is not None else None,
+        ctypes.byref(edits) if edits is not None else None, ptr(params_dev), ctypes.byref(cs),
+        ctypes.byref(lay), ctypes.byref(R), 1 if geometry else 0, stream_handle(stream)),
+        "ivr_preprocess_bwd")
+    return out, bad
+
+
+def raise_if_bad(bad, n, order):
+    """NonFiniteGradient(first tensor in `order` with a bad row, that row)."""
+    b = bad.cpu().numpy().view(np.uint64)
+    for name in order:
+        if name in L.BAD_IDS:
+            v = int(b[L.BAD_IDS.index(name)])
+            if v != 0xFFFFFFFFFFFFFFFF and v < n:
+                from .errors import NonFiniteGradient
+                raise NonFiniteGradient(name, v)
+
+
 def rasterize_device(dg, cam, K, cols, ws, shading=None, edits=None, colors=None, attrs=(),
                      f64=False, want_state=True, debug=False, stream=None, exact=True):
     """K1 + K2 + K3 with pair-capacity overflow handling (synchronizes once to

@@ -105,8 +105,9 @@ def rasterize_forward(geom, colors, cam, channels=("color", "alpha"), attrs=None
     colors_dev = D.to_dev(np.asarray(colors).reshape(n, 3)) if cols[0] >= 0 else None
     attrs_dev = [(D.to_dev(np.asarray(attrs[name], dtype=np.float64).reshape(n, w)), c, w)
                  for name, c, w in attr_cols]
-    F = D.rasterize_device(dg, cam, K, cols, workspace(), colors=colors_dev, attrs=attrs_dev,
-                           f64=f64, want_state=True, exact=exact)
+    # the returned state owns its buffers (a later call must not overwrite them)
+    F = D.rasterize_device(dg, cam, K, cols, D.Workspace(dg.device), colors=colors_dev,
+                           attrs=attrs_dev, f64=f64, want_state=True, exact=exact)
     out = (F.out64 if f64 else F.out).cpu().numpy().astype(dtype, copy=False)
     contrib = F.contrib.cpu().numpy()
     state.update(frame=F, dg=dg, empty=False)
@@ -130,6 +131,57 @@ def _project_only(geom, cam):
     return {"mean2d": g["mean2d"].reshape(n, 2), "cov2d": g["cov2d"].reshape(n, 2, 2),
             "conic": g["conic"].reshape(n, 3), "depth": g["depth"],
             "valid": g["valid"].astype(bool), "radius": g["radius"]}
+
+
+def d_out_tensor(state, d_maps, device):
+    """Pack the named upstream map gradients into one (H, W, K) float32 tensor
+    (rasterizer.py:209-219)."""
+    _check_dmaps(state, d_maps)
+    cam = state["cam"]
+    H, W = cam.height, cam.width
+    K = sum(w for _, w in state["layout"])
+    d_out = torch.zeros((H, W, K), dtype=torch.float32, device=device)
+    col = 0
+    for name, w in state["layout"]:
+        g = d_maps.get(name)
+        if g is not None:
+            t = g if isinstance(g, torch.Tensor) else torch.from_numpy(np.asarray(g, np.float64))
+            d_out[:, :, col:col + w] = t.to(device=device, dtype=torch.float32).reshape(H, W, w)
+        col += w
+    return d_out
+
+
+def rasterize_backward(state, d_maps):
+    """Exact-decision gradients of the forward pass on the GPU (K4a + K4b).
+
+    Same contract as rasterizer.py:185-286: returns d_mu, d_q_raw, d_log_s,
+    d_o_logit, d_n_raw, d_colors, d_attrs, d_mean2d (host float64) and raises
+    NonFiniteGradient(key, row) for the first non-finite key."""
+    geom, n = state["geom"], state["n"]
+    grads = {"d_mean2d": np.zeros((n, 2)), "d_mu": np.zeros((n, 3)), "d_q_raw": np.zeros((n, 4)),
+             "d_log_s": np.zeros((n, 3)), "d_o_logit": np.zeros(n), "d_n_raw": np.zeros((n, 3)),
+             "d_colors": np.zeros((n, 3)),
+             "d_attrs": {k: np.zeros(np.asarray(v).shape) for k, v in state["attrs"].items()}}
+    if state.get("empty"):
+        _check_dmaps(state, d_maps)
+        return grads
+    F, dg = state["frame"], state["dg"]
+    layout = state["layout"]
+    cols, attr_cols, K = _cols(layout)
+    d_out = d_out_tensor(state, d_maps, dg.device)
+    g = D.blend_backward(F, d_out)
+    want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_mean2d",
+            "d_values")
+    out, bad = D.preprocess_backward(dg, state["cam"], K, cols, g=g, geometry=True, want=want)
+    D.raise_if_bad(bad, n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors"))
+    for key, w in (("d_mu", 3), ("d_q_raw", 4), ("d_log_s", 3), ("d_n_raw", 3), ("d_colors", 3),
+                   ("d_mean2d", 2)):
+        grads[key] = out[key].cpu().numpy().reshape(n, w)
+    grads["d_o_logit"] = out["d_o_logit"].cpu().numpy()
+    dv = out["d_values"].cpu().numpy().reshape(n, K)
+    for name, c, w in attr_cols:
+        grads["d_attrs"][name] = dv[:, c:c + w].reshape(np.asarray(state["attrs"][name]).shape).copy()
+    return grads
 
 
 def _check_dmaps(state, d_maps):

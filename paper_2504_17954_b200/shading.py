@@ -193,3 +193,44 @@ def shade_gaussians(geom, attrs, palette, light, cam, coeff_transform=None):
              "b": np.zeros(4) if b is None else np.asarray(b, dtype=np.float64).reshape(4),
              "dg": dg, "pal_dev": pal, "n": n}
     return rgb_h, terms_h, cache
+
+
+def shade_backward(cache, d_rgb):
+    """Gradients of the shaded colour w.r.t. every learnable input on the GPU
+    (float64; shading.py:332-445): d_delta_c, d_k_a_raw, d_k_d_raw, d_k_s_raw,
+    d_log_beta, d_n_raw, d_c_p (per splat for per-splat palettes, else summed),
+    d_mu, d_lam, d_b, d_polar, d_azimuth.  Raises NonFiniteGradient."""
+    import torch
+    n = cache["n"]
+    if n == 0:
+        z = np.zeros((0, 3))
+        return {"d_delta_c": z, "d_k_a_raw": np.zeros(0), "d_k_d_raw": np.zeros(0),
+                "d_k_s_raw": np.zeros(0), "d_log_beta": np.zeros(0), "d_n_raw": z,
+                "d_c_p": z if cache["per_splat_palette"] else np.zeros(3), "d_mu": z,
+                "d_lam": np.zeros(4), "d_b": np.zeros(4), "d_polar": 0.0, "d_azimuth": 0.0}
+    dg = cache["dg"]
+    light = cache["light"]
+    S = D.shading_struct(dg, cache["pal_dev"], cache["per_splat_palette"], light, cache["lam"],
+                         cache["b"])
+    d_rgb_dev = D.to_dev(np.asarray(d_rgb, dtype=np.float64).reshape(n, 3))
+    want = ("d_mu", "d_n_raw", "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta",
+            "d_c_p")
+    out, bad = D.preprocess_backward(dg, cache["cam"], 1, (-1, -1, -1, -1), shading=S,
+                                     d_rgb=d_rgb_dev, geometry=False, want=want, per_scene=1,
+                                     per_splat_c_p=cache["per_splat_palette"], light=light)
+    D.raise_if_bad(bad, n, ("d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta",
+                            "d_n_raw", "d_mu"))
+    h = {k: v.cpu().numpy() for k, v in out.items()}
+    gl = h["d_globals"]
+    res = {"d_delta_c": h["d_delta_c"].reshape(n, 3), "d_k_a_raw": h["d_k_a_raw"],
+           "d_k_d_raw": h["d_k_d_raw"], "d_k_s_raw": h["d_k_s_raw"], "d_log_beta": h["d_log_beta"],
+           "d_n_raw": h["d_n_raw"].reshape(n, 3),
+           "d_c_p": h["d_c_p"].reshape(n, 3) if cache["per_splat_palette"] else h["d_c_p"][:3],
+           "d_mu": h["d_mu"].reshape(n, 3), "d_lam": gl[0:4].copy(), "d_b": gl[4:8].copy(),
+           "d_polar": float(gl[8]) if light.mode == ORBITAL else 0.0,
+           "d_azimuth": float(gl[9]) if light.mode == ORBITAL else 0.0}
+    for name in ("d_lam", "d_b"):
+        if not np.all(np.isfinite(res[name])):
+            from .errors import NonFiniteGradient
+            raise NonFiniteGradient(name, int(np.flatnonzero(~np.isfinite(res[name]))[0]))
+    return res

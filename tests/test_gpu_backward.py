@@ -1,0 +1,160 @@
+"""GPU backward parity (K4): rasterize_backward / shade_backward vs the
+reference's gradients (golden fixtures) and the CPU oracle.
+
+Tolerance (BASELINE.json north_star): relative gradient error <= 1e-3, per
+tensor as ||g - g_ref|| / ||g_ref||, plus an element-wise check with a floor.
+"""
+
+import numpy as np
+import pytest
+
+from conftest import golden
+
+pytestmark = pytest.mark.gpu
+
+REL = 1e-3
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2504_17954_b200 import _lib
+    _lib.lib()
+
+
+def _close(got, ref, rel=REL, name=""):
+    got, ref = np.asarray(got, np.float64), np.asarray(ref, np.float64)
+    assert got.shape == ref.shape, (name, got.shape, ref.shape)
+    nr = np.linalg.norm(ref)
+    err = np.linalg.norm(got - ref)
+    assert err <= rel * max(nr, 1e-12), (name, err, nr)
+    floor = 1e-3 * max(np.abs(ref).max(), 1e-12)
+    assert np.all(np.abs(got - ref) <= rel * np.maximum(np.abs(ref), floor) + 1e-12 + rel * floor * 10), name
+
+
+def _cam(d):
+    from paper_2504_17954_b200 import Camera
+    return Camera(d["cam_position"], d["cam_rotation"], float(d["cam_fov_y"]),
+                  int(d["cam_width"]), int(d["cam_height"]))
+
+
+def test_rasterize_backward_matches_reference():
+    from paper_2504_17954_b200 import GaussianGeometry, rasterize_backward, rasterize_forward
+    d = golden("backward_small")
+    geom = GaussianGeometry(d["mu"], d["q_raw"], d["log_s"], d["o_logit"], d["n_raw"])
+    out, st = rasterize_forward(geom, d["colors"], _cam(d),
+                                channels=("color", "alpha", "depth", "normal"),
+                                attrs={"ka": d["attr_ka"]}, dtype=np.float64)
+    assert np.abs(out.color - d["color"]).max() <= 1e-4
+    assert np.abs(out.depth - d["depth_map"]).max() <= 1e-4
+    w = {k: d["w_" + k] for k in ("color", "alpha", "depth", "normal", "ka")}
+    g = rasterize_backward(st, w)
+    for k in ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_mean2d"):
+        _close(g[k], d[k], name=k)
+    _close(g["d_attrs"]["ka"], d["d_attr_ka"], name="d_attr_ka")
+
+
+@pytest.mark.parametrize("tag", ["head", "orb"])
+def test_shade_backward_matches_reference(tag):
+    from paper_2504_17954_b200 import (GaussianGeometry, LightConfig, Palette, ShadingAttributes,
+                                       shade_gaussians)
+    from paper_2504_17954_b200.shading import shade_backward
+    d = golden("shade")
+    geom = GaussianGeometry(d["mu"], d["q_raw"], d["log_s"], d["o_logit"], d["n_raw"])
+    attrs = ShadingAttributes(d["delta_c"], d["k_a_raw"], d["k_d_raw"], d["k_s_raw"], d["log_beta"])
+    if tag == "head":
+        light, ct, pal = LightConfig(), None, Palette(d["palette"])
+    else:
+        light = LightConfig("orbital", 0.45, 0.9, np.array([1.2, 0.8, 1.0, 1.1]))
+        ct = (np.array([1.2, 0.8, 1.1, 0.9]), np.array([0.01, -0.02, 0.03, 0.2]))
+        pal = d["palette_ps"]
+    rgb, _, cache = shade_gaussians(geom, attrs, pal, light, _cam(d), coeff_transform=ct)
+    rel = np.abs(rgb - d[tag + "_rgb"]) / np.maximum(np.abs(d[tag + "_rgb"]), 1e-300)
+    assert rel.max() < 1e-12
+    g = shade_backward(cache, d["d_rgb"])
+    for k in ("d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta", "d_n_raw", "d_c_p",
+              "d_mu", "d_lam", "d_b"):
+        _close(g[k], d[f"{tag}_{k}"], rel=1e-9, name=k)
+    for k in ("d_polar", "d_azimuth"):
+        assert abs(g[k] - float(d[f"{tag}_{k}"])) <= 1e-9 * max(1.0, abs(float(d[f"{tag}_{k}"]))), k
+
+
+@pytest.mark.parametrize("dtype", [np.float32, np.float64])
+def test_backward_vs_oracle_random_scene(dtype):
+    import oracle as O
+    from paper_2504_17954_b200 import GaussianGeometry, rasterize_backward, rasterize_forward
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
+    a = editable_arrays(7, 4000, density=4000)
+    cam = bench_camera(96, 64, azimuth=0.4)
+    rng = np.random.default_rng(1)
+    colors = rng.uniform(0, 1, (4000, 3))
+    geom = GaussianGeometry(a["mu"], a["q_raw"], a["log_s"], a["o_logit"], a["n_raw"])
+    ch = ("color", "alpha", "depth", "normal")
+    out, st = rasterize_forward(geom, colors, cam, channels=ch, dtype=dtype)
+    ref = O.rasterize(a["mu"], a["q_raw"], a["log_s"], a["o_logit"], a["n_raw"], colors, cam,
+                      channels=ch, dtype=dtype)
+    w = {"color": rng.normal(size=(64, 96, 3)), "alpha": rng.normal(size=(64, 96)),
+         "depth": 0.1 * rng.normal(size=(64, 96)), "normal": rng.normal(size=(64, 96, 3))}
+    g = rasterize_backward(st, w)
+    gr = O.rasterize_backward(ref, w)
+    for k in ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_mean2d"):
+        _close(g[k], gr[k], name=k)
+
+
+def test_zero_upstream_gives_zero_grads():
+    from paper_2504_17954_b200 import GaussianGeometry, rasterize_backward, rasterize_forward
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
+    a = editable_arrays(2, 300)
+    geom = GaussianGeometry(a["mu"], a["q_raw"], a["log_s"], a["o_logit"], a["n_raw"])
+    cam = bench_camera(32, 32)
+    _, st = rasterize_forward(geom, np.ones((300, 3)), cam, dtype=np.float64)
+    g = rasterize_backward(st, {"color": np.zeros((32, 32, 3)), "alpha": np.zeros((32, 32))})
+    for k in ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors"):
+        assert float(np.abs(g[k]).max()) == 0.0
+
+
+def test_bad_gradient_shape_raises():
+    from paper_2504_17954_b200 import (GaussianGeometry, ShapeMismatch, rasterize_backward,
+                                       rasterize_forward)
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
+    a = editable_arrays(2, 50)
+    geom = GaussianGeometry(a["mu"], a["q_raw"], a["log_s"], a["o_logit"], a["n_raw"])
+    _, st = rasterize_forward(geom, np.ones((50, 3)), bench_camera(16, 16))
+    with pytest.raises(ShapeMismatch):
+        rasterize_backward(st, {"color": np.zeros((8, 8, 3))})
+
+
+def test_finite_differences_small_scene():
+    """Central differences on a 10-splat scene (the reference's FD protocol,
+    tests/test_rasterizer.py:165-207), through the GPU forward/backward."""
+    from paper_2504_17954_b200 import Camera, GaussianGeometry, rasterize_backward, rasterize_forward
+    from paper_2504_17954_b200.synthetic import editable_arrays
+    a = editable_arrays(0, 10, spread=0.5)
+    rng = np.random.default_rng(0)
+    geom = GaussianGeometry(a["mu"], a["q_raw"], np.log(rng.uniform(0.12, 0.35, (10, 3))),
+                            a["o_logit"], a["n_raw"])
+    cam = Camera.look_at((0, 0, -4.0), (0, 0, 0), np.pi / 3, 16, 16)
+    colors = rng.uniform(0.1, 0.9, size=(10, 3))
+    w = {"color": rng.normal(size=(16, 16, 3)), "alpha": rng.normal(size=(16, 16))}
+
+    def loss():
+        out, st = rasterize_forward(geom, colors, cam, dtype=np.float64)
+        return float(np.sum(out.color * w["color"]) + np.sum(out.alpha * w["alpha"])), st
+
+    _, st = loss()
+    g = rasterize_backward(st, w)
+    eps = 1e-4
+    for key, arr in (("d_mu", geom.mu), ("d_o_logit", geom.o_logit), ("d_colors", colors)):
+        flat = arr.reshape(-1)
+        gf = np.asarray(g[key]).reshape(-1)
+        for i in range(flat.size):
+            o = flat[i]
+            flat[i] = o + eps
+            lp, _ = loss()
+            flat[i] = o - eps
+            lm, _ = loss()
+            flat[i] = o
+            fd = (lp - lm) / (2 * eps)
+            assert abs(fd - gf[i]) <= 1e-3 * max(abs(fd), abs(gf[i]), 1e-2), (key, i, fd, gf[i])
