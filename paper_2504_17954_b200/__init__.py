@@ -13,12 +13,16 @@ from .errors import (  # noqa: F401
     VersionUnsupported, VoxSplatError,
 )
 from .gaussians import Camera, GaussianGeometry, ShColor, orbit_camera, project_gaussians  # noqa: F401
-from .rasterizer import RenderOutput, rasterize_forward, render_attribute_map  # noqa: F401
-from .scene import (  # noqa: F401
-    BasicSceneModel, ComposedScene, DeviceScene, EditState, EffectiveScene, apply_edits,
-    render_composed,
+from .rasterizer import (  # noqa: F401
+    RenderOutput, rasterize_backward, rasterize_forward, render_attribute_map,
 )
-from .shading import LightConfig, Palette, ShadingAttributes, shade_gaussians  # noqa: F401
+from .scene import (  # noqa: F401
+    BasicSceneModel, ComposedScene, DeviceScene, EditState, EffectiveScene, FrameGraph,
+    apply_edits, render_composed,
+)
+from .shading import (  # noqa: F401
+    LightConfig, Palette, ShadingAttributes, shade_backward, shade_gaussians,
+)
 from .vq import Codebook, assign_nearest, dequantize_model, kmeans, quantize_model  # noqa: F401
 
 __version__ = "0.1.0"
