@@ -1,0 +1,262 @@
+"""Inverse appearance fitting on the GPU (drop-in for voxsplat/inverse.py).
+
+The scene's primitives stay frozen and resident in HBM (a DeviceScene); each
+iteration renders with the transform (K1-K3, float64 semantics), evaluates
+the L1+SSIM loss on the device, runs K4 with only the transform gradients
+requested (per-scene palette and opacity scale, global (lam, b), light
+angles -- inverse.py:161-190), and applies the reference's Adam on the
+(4S+10)-float parameter vector.
+
+Multi-view extension: ``optimize_to_reference``
+accepts lists of references/cameras and minimises the MEAN per-view loss;
+under torch.distributed each rank owns a slice of the views and the packed
+gradient vector (4S+10 floats + loss) is summed with ONE NCCL all-reduce per
+iteration, so every rank applies the identical Adam step.  One view reproduces
+the reference exactly.
+"""
+
+from __future__ import annotations
+
+import hashlib
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import device as D
+from .errors import DivergedLoss, OutOfRange, ShapeMismatch
+from .losses import photometric_loss_t
+from .scene import ComposedScene, DeviceScene
+from .shading import ORBITAL, LightConfig
+
+
+def softplus(x):
+    return np.logaddexp(0.0, np.asarray(x, dtype=np.float64))
+
+
+def inv_softplus(y):
+    y = np.asarray(y, dtype=np.float64)
+    if np.any(y <= 0.0):
+        raise OutOfRange("softplus output must be positive")
+    return y + np.log1p(-np.exp(-y))
+
+
+def _sigmoid(x):
+    """_mathutil.sigmoid (branch on sign)."""
+    x = np.atleast_1d(np.asarray(x, dtype=np.float64))
+    out = np.empty_like(x)
+    pos = x >= 0
+    out[pos] = 1.0 / (1.0 + np.exp(-x[pos]))
+    e = np.exp(x[~pos])
+    out[~pos] = e / (1.0 + e)
+    return out
+
+
+@dataclass
+class TransformParams:
+    """Per-scene palette (S,3) and opacity softplus pre-image (S,), global
+    (lam, b) on (k_a, k_d, k_s, beta), orbital light angles (inverse.py:35-88)."""
+
+    c_p: np.ndarray
+    opacity_raw: np.ndarray
+    lam: np.ndarray
+    b: np.ndarray
+    polar: float = 0.0
+    azimuth: float = 0.0
+    light_mode: str = "headlight"
+
+    def __post_init__(self):
+        self.c_p = np.atleast_2d(np.asarray(self.c_p, dtype=np.float64))
+        s = self.c_p.shape[0]
+        if self.c_p.shape != (s, 3):
+            raise ShapeMismatch(f"c_p must be (S, 3), got {self.c_p.shape}")
+        self.opacity_raw = np.asarray(self.opacity_raw, dtype=np.float64).reshape(s)
+        self.lam = np.asarray(self.lam, dtype=np.float64).reshape(4)
+        self.b = np.asarray(self.b, dtype=np.float64).reshape(4)
+        self.polar = float(self.polar)
+        self.azimuth = float(self.azimuth)
+
+    @property
+    def opacity_scale(self):
+        return softplus(self.opacity_raw)
+
+    def copy(self):
+        return TransformParams(self.c_p.copy(), self.opacity_raw.copy(), self.lam.copy(),
+                               self.b.copy(), self.polar, self.azimuth, self.light_mode)
+
+    def to_dict(self):
+        return {"c_p": self.c_p.tolist(), "opacity_scale": self.opacity_scale.tolist(),
+                "lam": self.lam.tolist(), "b": self.b.tolist(), "polar": self.polar,
+                "azimuth": self.azimuth, "light_mode": self.light_mode}
+
+    @classmethod
+    def from_dict(cls, d):
+        return cls(np.asarray(d["c_p"]), inv_softplus(np.asarray(d["opacity_scale"])),
+                   np.asarray(d["lam"]), np.asarray(d["b"]), d["polar"], d["azimuth"],
+                   d["light_mode"])
+
+
+def init_transform(scene: ComposedScene) -> TransformParams:
+    """Identity transform for the scene's current edits (inverse.py:91-101)."""
+    c_p = np.stack([e.palette_override if e.palette_override is not None else m.palette.c_p
+                    for m, e in zip(scene.models, scene.edits)])
+    scales = np.array([max(e.opacity_scale, 1e-6) for e in scene.edits])
+    return TransformParams(c_p, inv_softplus(scales), np.ones(4), np.zeros(4),
+                           scene.light.polar, scene.light.azimuth, scene.light.mode)
+
+
+class Adam:
+    """trainer.Adam (trainer.py:100-128) on host float64 arrays."""
+
+    def __init__(self, eps=1e-15, betas=(0.9, 0.999)):
+        self.eps = eps
+        self.b1, self.b2 = betas
+        self.state = {}
+
+    def step(self, name, param, grad, lr):
+        st = self.state.setdefault(name, {"m": np.zeros_like(param), "v": np.zeros_like(param),
+                                          "t": 0})
+        st["t"] += 1
+        st["m"] = self.b1 * st["m"] + (1.0 - self.b1) * grad
+        st["v"] = self.b2 * st["v"] + (1.0 - self.b2) * grad * grad
+        mhat = st["m"] / (1.0 - self.b1 ** st["t"])
+        vhat = st["v"] / (1.0 - self.b2 ** st["t"])
+        param -= lr * mhat / (np.sqrt(vhat) + self.eps)
+        return param
+
+
+def _light(scene, params):
+    return LightConfig(scene.light.mode, params.polar, params.azimuth,
+                       term_scales=scene.light.term_scales.copy())
+
+
+class InverseFitter:
+    """Frozen scene resident on the device + per-view references."""
+
+    def __init__(self, scene, references, cams, exact=False, ds=None):
+        self.scene = scene
+        self.ds = ds or DeviceScene(scene)
+        self.cams = list(cams)
+        self.refs = [D.to_dev(np.asarray(r, dtype=np.float64)) if not isinstance(r, torch.Tensor)
+                     else r.to(self.ds.dg.device, torch.float64) for r in references]
+        self.exact = exact
+        self.S = self.ds.n_scenes
+
+    def render(self, params, cam, dtype=np.float64, want_state=False):
+        return self.ds.render_frame(cam, ("color", "alpha"), None, dtype, want_state=want_state,
+                                    light=_light(self.scene, params), lam=params.lam, b=params.b,
+                                    palettes=params.c_p, opacity_scales=params.opacity_scale,
+                                    exact=self.exact)
+
+    def view_grads(self, params, v):
+        """(loss, packed gradient (4S+10,) float64 device tensor) for view v."""
+        cam, ref = self.cams[v], self.refs[v]
+        F = self.render(params, cam, want_state=True)
+        rgba = F.out64 if F.f64 else F.out.double()
+        loss, d = photometric_loss_t(rgba, ref)
+        g = D.blend_backward(F, d)
+        shading, edits = F._keep_tabs
+        light = _light(self.scene, params)
+        out, _ = D.preprocess_backward(self.ds.dg, cam, 4, (0, 3, -1, -1), g=g, shading=shading,
+                                       edits=edits, geometry=False, want=("d_c_p", "d_scale"),
+                                       per_scene=self.S, light=light)
+        S = self.S
+        sig = torch.from_numpy(_sigmoid(params.opacity_raw)).to(out["d_scale"].device)
+        gl = out["d_globals"]
+        packed = torch.cat([out["d_c_p"][:3 * S], out["d_scale"][:S] * sig, gl[0:4], gl[4:8],
+                            gl[8:10] if light.mode == ORBITAL else torch.zeros_like(gl[8:10])])
+        return loss, packed
+
+    def unpack(self, packed):
+        S = self.S
+        p = packed.cpu().numpy() if isinstance(packed, torch.Tensor) else packed
+        return {"c_p": p[:3 * S].reshape(S, 3), "opacity_raw": p[3 * S:4 * S],
+                "lam": p[4 * S:4 * S + 4], "b": p[4 * S + 4:4 * S + 8],
+                "angles": p[4 * S + 8:4 * S + 10]}
+
+
+def _frozen_fingerprint(scene):
+    h = hashlib.sha256()
+    for m in scene.models:
+        for arr in (m.geometry.mu, m.geometry.q_raw, m.geometry.log_s, m.geometry.o_logit,
+                    m.geometry.n_raw, m.shading.delta_c, m.shading.k_a_raw, m.shading.k_d_raw,
+                    m.shading.k_s_raw, m.shading.log_beta, m.palette.c_p):
+            h.update(np.ascontiguousarray(arr).tobytes())
+    return h.hexdigest()
+
+
+def render_with_transform(scene, params, cam, dtype=np.float32):
+    """RGBA render of a composed scene under an appearance transform
+    (inverse.py:154-158)."""
+    fit = InverseFitter(scene, [], [], exact=True)
+    F = fit.render(params, cam, dtype=dtype)
+    return (F.out64 if F.f64 else F.out).cpu().numpy().astype(dtype, copy=False)
+
+
+def optimize_to_reference(scene, params, reference_rgba, reference_cam, iters=1000, lr=0.01,
+                          callback=None, learnable=None, group=None, exact=False):
+    """Fit the transform to reference image(s) with Adam on L1 + SSIM
+    (inverse.py:205-244).  Returns (fitted params, per-iteration losses).
+
+    ``reference_rgba`` / ``reference_cam`` may be lists (multi-view mean loss).
+    With torch.distributed initialised (or ``group`` given) and more than one
+    rank, each rank passes ITS views; gradients are all-reduced (sum) once per
+    iteration and divided by the global view count."""
+    refs = reference_rgba if isinstance(reference_rgba, (list, tuple)) else [reference_rgba]
+    cams = reference_cam if isinstance(reference_cam, (list, tuple)) else [reference_cam]
+    if len(refs) != len(cams):
+        raise ShapeMismatch("one camera per reference image required")
+    params = params.copy()
+    before = _frozen_fingerprint(scene)
+    learnable = learnable or ("c_p", "opacity_raw", "lam", "b", "angles")
+    fit = InverseFitter(scene, refs, cams, exact=exact)
+    dist = None
+    if torch.distributed.is_available() and torch.distributed.is_initialized():
+        if torch.distributed.get_world_size(group) > 1:
+            dist = torch.distributed
+    n_views = torch.tensor([float(len(refs))], dtype=torch.float64, device=fit.ds.dg.device)
+    if dist:
+        dist.all_reduce(n_views, group=group)
+    n_views = float(n_views.item())
+    adam = Adam(eps=1e-15)
+    angles = np.array([params.polar, params.azimuth])
+    fit_light = params.light_mode == ORBITAL and "angles" in learnable
+    losses = []
+    for it in range(1, iters + 1):
+        total = None
+        loss_sum = torch.zeros(1, dtype=torch.float64, device=fit.ds.dg.device)
+        for v in range(len(refs)):
+            loss, packed = fit.view_grads(params, v)
+            total = packed if total is None else total + packed
+            loss_sum = loss_sum + loss
+        if total is None:
+            total = torch.zeros(4 * fit.S + 10, dtype=torch.float64, device=fit.ds.dg.device)
+        buf = torch.cat([total, loss_sum])
+        if dist:
+            dist.all_reduce(buf, group=group)  # the only NCCL traffic: (4S+10)+1 floats
+        buf = buf / n_views
+        host = buf.cpu().numpy()
+        loss = float(host[-1])
+        if not np.isfinite(loss):
+            raise DivergedLoss(f"loss became {loss}")
+        grads = fit.unpack(host[:-1])
+        losses.append(loss)
+        floor = 1e-12
+        for name in ("c_p", "opacity_raw", "lam", "b"):
+            if name in learnable and np.abs(grads[name]).max() > floor:
+                adam.step(name, getattr(params, name), grads[name], lr)
+        if fit_light and np.abs(grads["angles"]).max() > floor:
+            adam.step("angles", angles, grads["angles"], lr)
+            params.polar, params.azimuth = float(angles[0]), float(angles[1])
+        if callback is not None:
+            callback(it, loss, params)
+    after = _frozen_fingerprint(scene)
+    assert before == after, "primitive attributes changed during inverse fitting"
+    return params, losses
+
+
+def inverse_step(scene, params, cam, reference, exact=False):
+    """One inverse._step (inverse.py:161-190): (loss, grads dict)."""
+    fit = InverseFitter(scene, [reference], [cam], exact=exact)
+    loss, packed = fit.view_grads(params, 0)
+    return float(loss), fit.unpack(packed)

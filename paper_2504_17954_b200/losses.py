@@ -1,0 +1,246 @@
+"""Training / fitting objectives on the GPU (drop-in for voxsplat/losses.py).
+
+Every function takes numpy arrays or CUDA tensors, computes in float64 on the
+device with torch ops (separable Gaussian SSIM windows as conv2d; these are
+library ops -- the hot path's own kernels are K1-K4), and returns the
+reference's (loss, gradient) pairs with the analytic gradients of
+losses.py:45-268.  Inputs given as numpy come back as numpy.
+"""
+
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from .errors import ShapeMismatch
+
+SSIM_SIGMA = 1.5
+SSIM_RADIUS = 5
+SSIM_C1 = 0.01 ** 2
+SSIM_C2 = 0.03 ** 2
+
+_offs = np.arange(-SSIM_RADIUS, SSIM_RADIUS + 1, dtype=np.float64)
+_K1D = np.exp(-(_offs ** 2) / (2.0 * SSIM_SIGMA ** 2))
+_K1D /= _K1D.sum()
+
+
+@dataclass
+class LossWeights:
+    """Default weighting of the total objective (losses.py:28-42)."""
+
+    l1_weight: float = 0.8
+    ssim_weight: float = 0.2
+    normal_consistency: float = 0.01
+    opacity_l1: float = 0.1
+    offset_sparsity: float = 0.01
+    bilateral_smoothness: float = 0.01
+
+    def __post_init__(self):
+        for f in self.__dataclass_fields__:
+            if getattr(self, f) < 0:
+                raise ValueError(f"loss weight {f} must be >= 0")
+
+
+def _dev():
+    return torch.device("cuda", torch.cuda.current_device())
+
+
+def _t(x):
+    if isinstance(x, torch.Tensor):
+        return x.to(device=_dev(), dtype=torch.float64)
+    return torch.from_numpy(np.ascontiguousarray(np.asarray(x, dtype=np.float64))).to(_dev())
+
+
+def _out(ref, t):
+    return t if isinstance(ref, torch.Tensor) else t.cpu().numpy()
+
+
+_KCACHE = {}
+
+
+def _kern(device):
+    k = _KCACHE.get(device)
+    if k is None:
+        k1 = torch.from_numpy(_K1D).to(device)
+        k = (k1.view(1, 1, -1, 1), k1.view(1, 1, 1, -1))
+        _KCACHE[device] = k
+    return k
+
+
+def _filt(img, full):
+    """Separable 11x11 Gaussian window; img (C,H,W); 'valid' or its adjoint
+    'full' (losses.py:45-54)."""
+    kv, kh = _kern(img.device)
+    x = img.unsqueeze(1)
+    r = SSIM_RADIUS * 2
+    if full:
+        x = torch.nn.functional.conv2d(x, kv, padding=(r, 0))
+        x = torch.nn.functional.conv2d(x, kh, padding=(0, r))
+    else:
+        x = torch.nn.functional.conv2d(x, kv)
+        x = torch.nn.functional.conv2d(x, kh)
+    return x.squeeze(1)
+
+
+def ssim_t(x, y):
+    """Mean SSIM over channels and its gradient w.r.t. x (torch float64;
+    x, y (H, W, C))."""
+    if x.shape != y.shape:
+        raise ShapeMismatch(f"ssim inputs differ: {tuple(x.shape)} vs {tuple(y.shape)}")
+    h, w, nc = x.shape
+    win = 2 * SSIM_RADIUS + 1
+    if h < win or w < win:
+        raise ShapeMismatch(f"image {h}x{w} smaller than the {win}x{win} ssim window")
+    X, Y = x.permute(2, 0, 1), y.permute(2, 0, 1)
+    ux, uy = _filt(X, False), _filt(Y, False)
+    uxx, uyy, uxy = _filt(X * X, False), _filt(Y * Y, False), _filt(X * Y, False)
+    vx, vy, vxy = uxx - ux * ux, uyy - uy * uy, uxy - ux * uy
+    a1, a2 = 2.0 * ux * uy + SSIM_C1, 2.0 * vxy + SSIM_C2
+    b1, b2 = ux * ux + uy * uy + SSIM_C1, vx + vy + SSIM_C2
+    s = (a1 * a2) / (b1 * b2)
+    value = s.mean(dim=(1, 2)).sum() / nc
+    n_valid = (h - win + 1) * (w - win + 1)
+    up = 1.0 / (n_valid * nc)
+    da1, da2 = a2 / (b1 * b2) * up, a1 / (b1 * b2) * up
+    db1, db2 = -s / b1 * up, -s / b2 * up
+    d_uxy = 2.0 * da2
+    d_uxx = db2
+    d_ux = 2.0 * uy * da1 + 2.0 * ux * db1 - 2.0 * ux * db2 - uy * d_uxy
+    dX = _filt(d_ux, True) + 2.0 * X * _filt(d_uxx, True) + Y * _filt(d_uxy, True)
+    return value, dX.permute(1, 2, 0)
+
+
+def ssim(x, y):
+    """losses.ssim (losses.py:57-115): (value, d_value/d_x); (H,W) or (H,W,C)."""
+    xt, yt = _t(x), _t(y)
+    sq = xt.dim() == 2
+    if sq:
+        xt, yt = xt[..., None], yt[..., None]
+    v, d = ssim_t(xt, yt)
+    if sq:
+        d = d[..., 0]
+    return float(v), _out(x, d)
+
+
+def photometric_loss_t(pred, gt, weights=None):
+    """0.8 L1 + 0.2 (1 - SSIM) on device tensors; returns (loss tensor, d_pred)."""
+    weights = weights or LossWeights()
+    if pred.shape != gt.shape:
+        raise ShapeMismatch(f"prediction {tuple(pred.shape)} vs ground truth {tuple(gt.shape)}")
+    diff = pred - gt
+    loss = weights.l1_weight * diff.abs().mean()
+    d = weights.l1_weight * torch.sign(diff) / diff.numel()
+    if weights.ssim_weight > 0.0:
+        s, ds = ssim_t(pred if pred.dim() == 3 else pred[..., None],
+                       gt if gt.dim() == 3 else gt[..., None])
+        if pred.dim() == 2:
+            ds = ds[..., 0]
+        loss = loss + weights.ssim_weight * (1.0 - s)
+        d = d - weights.ssim_weight * ds
+    return loss, d
+
+
+def photometric_loss(pred_rgba, gt_rgba, weights=None):
+    """losses.photometric_loss (losses.py:118-138): (loss, d_pred)."""
+    loss, d = photometric_loss_t(_t(pred_rgba), _t(gt_rgba), weights)
+    return float(loss), _out(pred_rgba, d)
+
+
+def pseudo_normal_from_depth(depth, alpha, cam, alpha_threshold=1e-3):
+    """losses.py:141-181: camera-oriented pseudo-normals from a depth map."""
+    d, a = _t(depth), _t(alpha)
+    if d.shape != a.shape:
+        raise ShapeMismatch(f"depth {tuple(d.shape)} vs alpha {tuple(a.shape)}")
+    h, w = d.shape
+    py, px = torch.meshgrid(torch.arange(h, dtype=torch.float64, device=d.device),
+                            torch.arange(w, dtype=torch.float64, device=d.device), indexing="ij")
+    cx, cy = (cam.width - 1) / 2.0, (cam.height - 1) / 2.0
+    f = 0.5 * cam.height / np.tan(0.5 * cam.fov_y)
+    pts = torch.stack([(px - cx) * d / f, (py - cy) * d / f, d], dim=-1)
+    dx = torch.empty_like(pts)
+    dx[:, :-1] = pts[:, 1:] - pts[:, :-1]
+    dx[:, -1] = pts[:, -1] - pts[:, -2]
+    dy = torch.empty_like(pts)
+    dy[:-1] = pts[1:] - pts[:-1]
+    dy[-1] = pts[-1] - pts[-2]
+    n = torch.linalg.cross(dx, dy, dim=-1)
+    norms = torch.linalg.norm(n, dim=-1, keepdim=True)
+    good = norms[..., 0] > 1e-12
+    n = torch.where(good[..., None], n / torch.clamp(norms, min=1e-12), torch.zeros_like(n))
+    away = (n * pts).sum(-1) > 0.0
+    n = torch.where(away[..., None], -n, n)
+    rot = torch.from_numpy(np.asarray(cam.rotation, dtype=np.float64)).to(d.device)
+    nw = n @ rot
+    mask = (a > alpha_threshold) & good
+    nw = torch.where(mask[..., None], nw, torch.zeros_like(nw))
+    return _out(depth, nw), _out(depth, mask)
+
+
+def normal_consistency_loss(normal_map, target, mask):
+    """losses.py:184-206: mean L2 distance over masked pixels, gradient to the map."""
+    n, t = _t(normal_map), _t(target)
+    m = mask.to(_dev()).bool() if isinstance(mask, torch.Tensor) else \
+        torch.from_numpy(np.asarray(mask, bool)).to(_dev())
+    if n.shape != t.shape:
+        raise ShapeMismatch(f"normal maps differ: {tuple(n.shape)} vs {tuple(t.shape)}")
+    cnt = int(m.sum())
+    d_n = torch.zeros_like(n)
+    if cnt == 0:
+        return 0.0, _out(normal_map, d_n)
+    diff = (n - t)[m]
+    norms = torch.linalg.norm(diff, dim=-1)
+    loss = float(norms.sum()) / cnt
+    safe = norms > 1e-12
+    g = torch.zeros_like(diff)
+    g[safe] = diff[safe] / norms[safe, None] / cnt
+    d_n[m] = g
+    return loss, _out(normal_map, d_n)
+
+
+def _fdiff_abs(img):
+    img = img if img.dim() == 3 else img[..., None]
+    gx = torch.zeros(img.shape[:2], dtype=img.dtype, device=img.device)
+    gy = torch.zeros_like(gx)
+    gx[:, :-1] = (img[:, 1:] - img[:, :-1]).abs().sum(-1)
+    gy[:-1] = (img[1:] - img[:-1]).abs().sum(-1)
+    return gx + gy
+
+
+def bilateral_smoothness(attr_map, gt_color, mask=None):
+    """losses.py:219-253: edge-aware smoothness and its gradient."""
+    k, c = _t(attr_map), _t(gt_color)
+    if k.shape[:2] != c.shape[:2]:
+        raise ShapeMismatch(f"attribute {tuple(k.shape)} vs color {tuple(c.shape)}")
+    m = torch.ones(k.shape[:2], dtype=torch.bool, device=k.device) if mask is None else _t(mask).bool()
+    cnt = int(m.sum())
+    d_k = torch.zeros_like(k)
+    if cnt == 0:
+        return 0.0, _out(attr_map, d_k)
+    weight = torch.exp(-_fdiff_abs(c)) * m / cnt
+    k3 = k if k.dim() == 3 else k[..., None]
+    d3 = d_k if d_k.dim() == 3 else d_k[..., None]
+    gx = k3[:, 1:] - k3[:, :-1]
+    gy = k3[1:] - k3[:-1]
+    loss = float((gx.abs().sum(-1) * weight[:, :-1]).sum() + (gy.abs().sum(-1) * weight[:-1]).sum())
+    sx = torch.sign(gx) * weight[:, :-1, None]
+    sy = torch.sign(gy) * weight[:-1, :, None]
+    d3[:, 1:] += sx
+    d3[:, :-1] -= sx
+    d3[1:] += sy
+    d3[:-1] -= sy
+    return loss, _out(attr_map, d_k)
+
+
+def offset_sparsity_loss(offset_map):
+    """losses.py:256-260."""
+    m = _t(offset_map)
+    return float(m.abs().mean()), _out(offset_map, torch.sign(m) / m.numel())
+
+
+def opacity_l1_loss(o_logit):
+    """losses.py:263-268: mean mapped opacity, gradient w.r.t. the logits."""
+    x = _t(o_logit)
+    o = torch.sigmoid(x)
+    return float(o.mean()), _out(o_logit, o * (1.0 - o) / o.numel())
