@@ -1,0 +1,394 @@
+"""Editable-stage (stage-2) training on the GPU (trainer.py:375-626 semantics).
+
+All parameters, Adam moments and the per-step work stay on the device:
+K1 (shading + projection, K=15 channels: colour, alpha, depth, normal, Δc,
+k_a, k_d, k_s, β) -> K2 -> K3 -> L1+SSIM and the four regularizers in torch
+(losses.py) -> K4a -> K4b (projection + shading backward fused) -> the
+attribute chain rules of _stage2_step (trainer.py:433-442) -> Adam with the
+reference's learning-rate schedules -> periodic densify / prune (torch).
+
+One training view per iteration (reference semantics, trainer.py:485).  Runs
+for independent basic transfer functions shard one per GPU with no
+communication.
+"""
+
+from __future__ import annotations
+
+import json
+import math
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import device as D
+from .errors import DatasetEmpty, DivergedLoss, OutOfRange
+from .gaussians import GaussianGeometry
+from .losses import (LossWeights, bilateral_smoothness, normal_consistency_loss,
+                     photometric_loss_t, pseudo_normal_from_depth)
+from .rasterizer import _channel_layout, _cols
+from .scene import STAGE_BASE, STAGE_EDITABLE, BasicSceneModel, DeviceScene
+from .shading import LightConfig, Palette, ShadingAttributes
+
+PSNR_CAP = 99.0
+
+
+@dataclass
+class TrainConfig:
+    """Hyper-parameters (trainer.py:46-94)."""
+
+    stage1_iters: int = 30000
+    stage2_iters: int = 10000
+    adam_eps: float = 1e-15
+    adam_betas: tuple = (0.9, 0.999)
+    lr_mu: float = 1.6e-4
+    lr_mu_final: float = 1.6e-6
+    lr_q: float = 1e-3
+    lr_log_s: float = 5e-3
+    lr_o: float = 0.05
+    lr_sh: float = 2.5e-3
+    lr_normal: float = 0.01
+    lr_shading: float = 0.01
+    lr_decay_floor: float = 0.1
+    densify_interval: int = 100
+    densify_start_iter: int = 500
+    densify_until_iter: int = None
+    densify_grad_threshold: float = 2e-4
+    prune_opacity_threshold: float = 0.005
+    max_primitives: int = 120000
+    init_count: int = 5000
+    init_opacity: float = 0.1
+    sh_degree: int = 2
+    silhouette_carve: bool = False
+    seed: int = 0
+    log_interval: int = 50
+    weights: LossWeights = field(default_factory=LossWeights)
+
+    def __post_init__(self):
+        if self.stage1_iters < 0 or self.stage2_iters < 0:
+            raise OutOfRange("iteration counts must be >= 0")
+        for name in ("densify_grad_threshold", "prune_opacity_threshold", "densify_interval",
+                     "init_count", "max_primitives"):
+            if getattr(self, name) <= 0:
+                raise OutOfRange(f"{name} must be > 0")
+
+    def until_iter(self, stage_iters):
+        return self.densify_until_iter if self.densify_until_iter is not None else stage_iters // 2
+
+
+class DeviceAdam:
+    """trainer.Adam on device tensors; moments survive densification (remap)."""
+
+    def __init__(self, eps=1e-15, betas=(0.9, 0.999)):
+        self.eps, (self.b1, self.b2), self.state = eps, betas, {}
+
+    @torch.no_grad()
+    def step(self, name, param, grad, lr):
+        st = self.state.get(name)
+        if st is None:
+            st = self.state[name] = {"m": torch.zeros_like(param), "v": torch.zeros_like(param), "t": 0}
+        st["t"] += 1
+        t = st["t"]
+        st["m"].mul_(self.b1).add_(grad, alpha=1.0 - self.b1)
+        st["v"].mul_(self.b2).addcmul_(grad, grad, value=1.0 - self.b2)
+        mhat = st["m"] / (1.0 - self.b1 ** t)
+        vhat = st["v"] / (1.0 - self.b2 ** t)
+        param.sub_(lr * mhat / (vhat.sqrt() + self.eps))
+
+    def remap(self, parents, is_new):
+        for st in self.state.values():
+            for key in ("m", "v"):
+                arr = st[key][parents].clone()
+                arr[is_new] = 0.0
+                st[key] = arr
+
+
+_LR = {"mu": "lr_mu", "q_raw": "lr_q", "log_s": "lr_log_s", "o_logit": "lr_o", "n_raw": "lr_normal",
+       "delta_c": "lr_shading", "k_a_raw": "lr_shading", "k_d_raw": "lr_shading",
+       "k_s_raw": "lr_shading", "log_beta": "lr_shading"}
+GEOM = ("mu", "q_raw", "log_s", "o_logit", "n_raw")
+SHADE = ("delta_c", "k_a_raw", "k_d_raw", "k_s_raw", "log_beta")
+ATTR_NAMES = ("delta_c", "k_a", "k_d", "k_s", "beta")
+
+
+def _psnr_t(a, b):
+    mse = float(((a[..., :3] - b[..., :3]) ** 2).mean())
+    return PSNR_CAP if mse <= 0.0 else min(10.0 * math.log10(1.0 / mse), PSNR_CAP)
+
+
+class EditableTrainer:
+    """Stage-2 state on the device: params (float64 tensors), palette, light."""
+
+    def __init__(self, params, palette, light, cfg=None, device=None):
+        self.dev = device or D.cuda_device()
+        self.p = {k: D.to_dev(params[k], device=self.dev) for k in GEOM + SHADE}
+        self.palette = D.to_dev(np.asarray(palette, np.float64).reshape(1, 3), device=self.dev)
+        self.light = light
+        self.cfg = cfg or TrainConfig()
+        self.adam = DeviceAdam(self.cfg.adam_eps, self.cfg.adam_betas)
+        self.ws = D.Workspace(self.dev)
+        self.layout = _channel_layout(("color", "alpha", "depth", "normal"),
+                                      {"delta_c": np.zeros((1, 3)), "k_a": np.zeros(1),
+                                       "k_d": np.zeros(1), "k_s": np.zeros(1), "beta": np.zeros(1)})
+        self.cols, self.attr_cols, self.K = _cols(self.layout)
+        self.colmap = {name: (c, w) for name, c, w in self.attr_cols}
+
+    @property
+    def n(self):
+        return int(self.p["mu"].shape[0])
+
+    def _dg(self):
+        return D.DeviceGaussians({k: self.p[k] for k in GEOM}, {k: self.p[k] for k in SHADE},
+                                 None, self.dev)
+
+    def forward(self, cam, want_state=True, dg=None):
+        dg = dg or self._dg()
+        S = D.shading_struct(dg, self.palette, False, self.light)
+        p = self.p
+        attrs = {"delta_c": p["delta_c"], "k_a": torch.sigmoid(p["k_a_raw"]),
+                 "k_d": torch.sigmoid(p["k_d_raw"]), "k_s": torch.sigmoid(p["k_s_raw"]),
+                 "beta": torch.exp(p["log_beta"]) + 1.0}
+        attrs_dev = [(attrs[name].reshape(self.n, w).contiguous(), c, w)
+                     for name, c, w in self.attr_cols]
+        F = D.rasterize_device(dg, cam, self.K, self.cols, self.ws, shading=S, attrs=attrs_dev,
+                               f64=False, want_state=want_state, exact=False)
+        return F, S, attrs, dg
+
+    def step(self, cam, gt, weights=None):
+        """One _stage2_step (trainer.py:397-444): (loss, grads, densify stat),
+        all device tensors."""
+        weights = weights or self.cfg.weights
+        F, S, attrs, dg = self.forward(cam)
+        H, W = cam.height, cam.width
+        out = F.out.double()
+        c = {name: c for name, c, w in _cols_named(self.layout)}
+        rgba = torch.cat([out[..., c["color"]:c["color"] + 3], out[..., c["alpha"]:c["alpha"] + 1]],
+                         dim=-1)
+        loss, d_rgba = photometric_loss_t(rgba, gt, weights)
+        if not torch.isfinite(loss):
+            raise DivergedLoss(f"loss became {float(loss)}")
+        d_out = torch.zeros((H, W, self.K), dtype=torch.float64, device=self.dev)
+        d_out[..., c["color"]:c["color"] + 3] = d_rgba[..., :3]
+        d_out[..., c["alpha"]] = d_rgba[..., 3]
+        if weights.normal_consistency > 0.0:
+            target, mask = pseudo_normal_from_depth(out[..., c["depth"]], out[..., c["alpha"]], cam)
+            nl, d_n = normal_consistency_loss(out[..., c["normal"]:c["normal"] + 3], target, mask)
+            loss = loss + weights.normal_consistency * nl
+            d_out[..., c["normal"]:c["normal"] + 3] = weights.normal_consistency * d_n
+        if weights.offset_sparsity > 0.0:
+            m = out[..., c["delta_c"]:c["delta_c"] + 3]
+            loss = loss + weights.offset_sparsity * m.abs().mean()
+            d_out[..., c["delta_c"]:c["delta_c"] + 3] = weights.offset_sparsity * torch.sign(m) / m.numel()
+        if weights.bilateral_smoothness > 0.0:
+            for name in ("k_a", "k_d", "k_s", "beta"):
+                bl, d_map = bilateral_smoothness(out[..., c[name]], gt[..., :3])
+                loss = loss + weights.bilateral_smoothness * bl
+                d_out[..., c[name]] = weights.bilateral_smoothness * d_map
+        g = D.blend_backward(F, d_out.float())
+        want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_mean2d", "d_values",
+                "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta")
+        gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, shading=S, geometry=True,
+                                        want=want, light=self.light)
+        n, K = self.n, self.K
+        dv = gr["d_values"].view(n, K)
+        o = torch.sigmoid(self.p["o_logit"])
+        d_o = gr["d_o_logit"]
+        if weights.opacity_l1 > 0.0:
+            loss = loss + weights.opacity_l1 * o.mean()
+            d_o = d_o + weights.opacity_l1 * o * (1.0 - o) / n
+        ka, kd, ks, beta = attrs["k_a"], attrs["k_d"], attrs["k_s"], attrs["beta"]
+        grads = {"mu": gr["d_mu"].view(n, 3), "q_raw": gr["d_q_raw"].view(n, 4),
+                 "log_s": gr["d_log_s"].view(n, 3), "o_logit": d_o,
+                 "n_raw": gr["d_n_raw"].view(n, 3),
+                 "delta_c": gr["d_delta_c"].view(n, 3) + dv[:, c["delta_c"]:c["delta_c"] + 3],
+                 "k_a_raw": gr["d_k_a_raw"] + dv[:, c["k_a"]] * ka * (1.0 - ka),
+                 "k_d_raw": gr["d_k_d_raw"] + dv[:, c["k_d"]] * kd * (1.0 - kd),
+                 "k_s_raw": gr["d_k_s_raw"] + dv[:, c["k_s"]] * ks * (1.0 - ks),
+                 "log_beta": gr["d_log_beta"] + dv[:, c["beta"]] * (beta - 1.0)}
+        stat = torch.linalg.norm(gr["d_mean2d"].view(n, 2), dim=1) + \
+            torch.linalg.norm(grads["n_raw"], dim=1)
+        self._bad = bad
+        return loss, grads, stat
+
+    def apply(self, grads, it, iters, decay_extra=("o_logit",)):
+        """Adam on every group with the reference schedules (trainer.py:491-499)."""
+        cfg = self.cfg
+        frac = it / max(iters, 1)
+        for name, grad in grads.items():
+            lr = getattr(cfg, _LR[name])
+            if name == "mu" and cfg.lr_mu > 0.0:
+                lr = cfg.lr_mu * (cfg.lr_mu_final / cfg.lr_mu) ** frac
+            elif _LR[name] in ("lr_shading", "lr_normal") or name in decay_extra:
+                lr = lr * cfg.lr_decay_floor ** frac
+            self.adam.step(name, self.p[name], grad, lr)
+
+    @torch.no_grad()
+    def densify(self, mean_stat, extent, gen):
+        """_densify_params (trainer.py:135-193) on the device."""
+        cfg, p = self.cfg, self.p
+        n = self.n
+        over = mean_stat >= cfg.densify_grad_threshold
+        budget = cfg.max_primitives - n
+        if budget <= 0:
+            over[:] = False
+        else:
+            cand = torch.nonzero(over).flatten()
+            if cand.numel() > budget:
+                order = torch.argsort(-mean_stat[cand], stable=True)
+                over = torch.zeros_like(over)
+                over[cand[order[:budget]]] = True
+        scales = torch.exp(p["log_s"])
+        big = scales.max(dim=1).values >= 0.01 * extent
+        clone, split = over & ~big, over & big
+        keep = torch.nonzero(~split).flatten()
+        c_idx = torch.nonzero(clone).flatten()
+        s_idx = torch.nonzero(split).flatten()
+        parents = torch.cat([keep, c_idx, s_idx, s_idx])
+        out = {k: v[parents].clone() for k, v in p.items()}
+        ns = s_idx.numel()
+        if ns:
+            sp = torch.cat([s_idx, s_idx])
+            q = p["q_raw"][sp]
+            q = q / torch.clamp(torch.linalg.norm(q, dim=1, keepdim=True), min=1e-12)
+            R = _quat_rot_t(q)
+            offs = torch.randn((2 * ns, 3), generator=gen, dtype=torch.float64,
+                               device=self.dev) * scales[sp]
+            out["mu"][-2 * ns:] = p["mu"][sp] + torch.einsum("nij,nj->ni", R, offs)
+            out["log_s"][-2 * ns:] = p["log_s"][sp] - math.log(1.6)
+        alive = torch.sigmoid(out["o_logit"]) >= cfg.prune_opacity_threshold
+        is_new = torch.arange(parents.numel(), device=self.dev) >= keep.numel()
+        if int(alive.sum()) == 0:
+            return {"cloned": 0, "split": 0, "pruned": 0, "count": n}
+        self.p = {k: v[alive].contiguous() for k, v in out.items()}
+        self.adam.remap(parents[alive], is_new[alive])
+        return {"cloned": int(c_idx.numel()), "split": int(ns),
+                "pruned": int((~alive).sum()), "count": self.n}
+
+    def render_rgba(self, cam):
+        F, _, _, _ = self.forward(cam, want_state=False)
+        c = {name: c for name, c, w in _cols_named(self.layout)}
+        out = F.out.double()
+        return torch.cat([out[..., c["color"]:c["color"] + 3], out[..., c["alpha"]:c["alpha"] + 1]], -1)
+
+    def model(self, palette, metadata=None):
+        h = {k: v.cpu().numpy() for k, v in self.p.items()}
+        geom = GaussianGeometry(*(h[k] for k in GEOM))
+        attrs = ShadingAttributes(*(h[k] for k in SHADE))
+        return BasicSceneModel(STAGE_EDITABLE, geom, shading=attrs, palette=Palette(palette),
+                               metadata=metadata or {})
+
+
+def _cols_named(layout):
+    c = 0
+    for name, w in layout:
+        yield name, c, w
+        c += w
+
+
+def _quat_rot_t(q):
+    w, x, y, z = q[:, 0], q[:, 1], q[:, 2], q[:, 3]
+    R = torch.empty((q.shape[0], 3, 3), dtype=q.dtype, device=q.device)
+    R[:, 0, 0] = 1 - 2 * (y * y + z * z)
+    R[:, 0, 1] = 2 * (x * y - w * z)
+    R[:, 0, 2] = 2 * (x * z + w * y)
+    R[:, 1, 0] = 2 * (x * y + w * z)
+    R[:, 1, 1] = 1 - 2 * (x * x + z * z)
+    R[:, 1, 2] = 2 * (y * z - w * x)
+    R[:, 2, 0] = 2 * (x * z - w * y)
+    R[:, 2, 1] = 2 * (y * z + w * x)
+    R[:, 2, 2] = 1 - 2 * (x * x + y * y)
+    return R
+
+
+def scene_extent(mu):
+    """Half the bounding-box diagonal (trainer.py:233-238)."""
+    mu = np.asarray(mu)
+    if mu.size == 0:
+        return 1.0
+    return max(0.5 * float(np.linalg.norm(mu.max(axis=0) - mu.min(axis=0))), 1e-6)
+
+
+def foreground_mean_color(dataset):
+    """Alpha-weighted mean rgb over the training images (trainer.py:331-341)."""
+    num, den = np.zeros(3), 0.0
+    for img in dataset.images:
+        img = np.asarray(img, np.float64)
+        a = img[..., 3]
+        num += (img[..., :3] * a[..., None]).sum(axis=(0, 1))
+        den += a.sum()
+    return np.full(3, 0.5) if den <= 0.0 else num / den
+
+
+def _stage2_init(n):
+    """trainer.py:562-577: neutral start."""
+    return {"delta_c": np.zeros((n, 3)), "k_a_raw": np.zeros(n), "k_d_raw": np.zeros(n),
+            "k_s_raw": np.zeros(n), "log_beta": np.full(n, np.log(9.0))}
+
+
+def train_editable(base, dataset, cfg=None):
+    """Stage 2 on the GPU (trainer.py:580-626): returns (editable model, log)."""
+    cfg = cfg or TrainConfig()
+    if base.stage != STAGE_BASE and base.stage != STAGE_EDITABLE:
+        raise OutOfRange("stage-2 training expects a base-stage model")
+    if len(dataset) < 2:
+        raise DatasetEmpty("training needs at least two views")
+    rng = np.random.default_rng(cfg.seed + 1)
+    gen = torch.Generator(device=D.cuda_device()).manual_seed(cfg.seed + 1)
+    palette = foreground_mean_color(dataset)
+    light = dataset.light
+    g = base.geometry
+    params = {k: getattr(g, k) for k in GEOM}
+    params.update(_stage2_init(len(g)))
+    tr = EditableTrainer(params, palette, light, cfg)
+    iters = cfg.stage2_iters
+    extent = scene_extent(np.stack(dataset.bbox()))
+    until = cfg.until_iter(iters)
+    start = cfg.densify_interval
+    holdout = len(dataset) - 1
+    gts = [D.to_dev(np.asarray(im, np.float64)) for im in dataset.images]
+    stats_sum = torch.zeros(tr.n, dtype=torch.float64, device=tr.dev)
+    stats_iters = 0
+    log = []
+    for it in range(1, iters + 1):
+        view = int(rng.integers(len(dataset)))
+        loss, grads, stat = tr.step(dataset.cameras[view], gts[view])
+        D.raise_if_bad(tr._bad, tr.n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw",
+                                       "d_colors")) if it % cfg.log_interval == 0 else None
+        tr.apply(grads, it, iters)
+        stats_sum += stat
+        stats_iters += 1
+        if it % cfg.densify_interval == 0:
+            if start <= it <= until:
+                tr.densify(stats_sum / max(stats_iters, 1), extent, gen)
+            stats_sum = torch.zeros(tr.n, dtype=torch.float64, device=tr.dev)
+            stats_iters = 0
+        if it % cfg.log_interval == 0 or it == iters:
+            lv = float(loss)
+            if not np.isfinite(lv):
+                raise DivergedLoss(f"loss became {lv} at iteration {it}")
+            img = tr.render_rgba(dataset.cameras[holdout])
+            log.append({"iteration": it, "loss": lv, "count": tr.n,
+                        "psnr": _psnr_t(img, gts[holdout])})
+    model = tr.model(palette, {"stage2_iters": cfg.stage2_iters, "seed": cfg.seed,
+                               "light": light.to_dict()})
+    return model, log
+
+
+def render_model(model, cam, light=None, dtype=np.float32):
+    """RGBA image of one editable basic model (trainer.py:633-647)."""
+    from .vq import dequantize_model
+    if model.is_quantized:
+        model = dequantize_model(model)
+    if model.stage != STAGE_EDITABLE:
+        raise OutOfRange("the GPU path renders editable-stage models")
+    from .scene import ComposedScene
+    sc = ComposedScene.compose([model], light or LightConfig())
+    out = DeviceScene(sc).render(cam, dtype=dtype)
+    return np.concatenate([np.asarray(out.color, np.float64), np.asarray(out.alpha, np.float64)[..., None]],
+                          axis=-1)
+
+
+def write_training_log(path, records):
+    with open(path, "w") as f:
+        for rec in records:
+            f.write(json.dumps(rec, sort_keys=True) + "\n")

@@ -211,7 +211,33 @@ def inverse_case():
     print("inverse")
 
 
+def stage2_case():
+    """One trainer._stage2_step (trainer.py:397-444) with all regularizers."""
+    from voxsplat import trainer as ref_trainer
+    from voxsplat.losses import LossWeights
+    a = editable_arrays(41, 300, spread=0.5)
+    geom = GaussianGeometry(*(a[k] for k in GEOM_KEYS))
+    attrs = ShadingAttributes(*(a[k] for k in SHADE_KEYS))
+    cam = orbit_camera(np.zeros(3), 2.5, 0.3, 0.8, 0.9, 40, 32)
+    rng = np.random.default_rng(8)
+    gt = rng.uniform(0, 1, (32, 40, 4))
+    light = LightConfig("orbital", 0.3, -0.7, np.array([1.0, 1.1, 0.9, 1.0]))
+    loss, grads, stat = ref_trainer._stage2_step(geom, attrs, Palette(a["palette"]), light, cam, gt,
+                                                 LossWeights())
+    d = dict(a)
+    d.update(cam_dict(cam), gt=gt, loss=np.float64(loss), stat=stat)
+    for k, v in grads.items():
+        d["g_" + k] = v
+    np.savez_compressed(os.path.join(HERE, "stage2.npz"), **d)
+    print("stage2", loss)
+
+
 if __name__ == "__main__":
+    import sys as _sys
+    if len(_sys.argv) > 1:  # regenerate selected cases only
+        for name in _sys.argv[1:]:
+            globals()[name]()
+        _sys.exit(0)
     check_generator()
     # C1 (bench config 0): 10k density-scaled, 128^2
     render_case("render_c1", 0, 10_000, 128, 128, density=10_000)
@@ -226,3 +252,4 @@ if __name__ == "__main__":
     vq_case()
     loss_case()
     inverse_case()
+    stage2_case()
