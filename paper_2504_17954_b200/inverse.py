@@ -193,6 +193,30 @@ def render_with_transform(scene, params, cam, dtype=np.float32):
     return (F.out64 if F.f64 else F.out).cpu().numpy().astype(dtype, copy=False)
 
 
+def reduce_views(total, loss_sum, n_views, dist=None, group=None):
+    """Mean over ALL views of the packed gradient and loss: one all-reduce
+    (sum) of (4S+10)+1 float64 values when distributed (NCCL on GPU ranks,
+    gloo in the CPU tests).  Returns (host gradient vector, loss)."""
+    buf = torch.cat([total.reshape(-1), loss_sum.reshape(-1).to(total.dtype)])
+    if dist is not None:
+        dist.all_reduce(buf, group=group)
+    host = (buf / n_views).cpu().numpy()
+    return host[:-1], float(host[-1])
+
+
+def transform_step(params, grads, adam, lr, learnable, angles):
+    """The reference's per-iteration update (inverse.py:229-238): Adam on each
+    learnable group whose gradient exceeds the 1e-12 floor."""
+    floor = 1e-12
+    for name in ("c_p", "opacity_raw", "lam", "b"):
+        if name in learnable and np.abs(grads[name]).max() > floor:
+            adam.step(name, getattr(params, name), grads[name], lr)
+    if params.light_mode == ORBITAL and "angles" in learnable and \
+            np.abs(grads["angles"]).max() > floor:
+        adam.step("angles", angles, grads["angles"], lr)
+        params.polar, params.azimuth = float(angles[0]), float(angles[1])
+
+
 def optimize_to_reference(scene, params, reference_rgba, reference_cam, iters=1000, lr=0.01,
                           callback=None, learnable=None, group=None, exact=False):
     """Fit the transform to reference image(s) with Adam on L1 + SSIM
@@ -220,7 +244,6 @@ def optimize_to_reference(scene, params, reference_rgba, reference_cam, iters=10
     n_views = float(n_views.item())
     adam = Adam(eps=1e-15)
     angles = np.array([params.polar, params.azimuth])
-    fit_light = params.light_mode == ORBITAL and "angles" in learnable
     losses = []
     for it in range(1, iters + 1):
         total = None
@@ -231,23 +254,11 @@ def optimize_to_reference(scene, params, reference_rgba, reference_cam, iters=10
             loss_sum = loss_sum + loss
         if total is None:
             total = torch.zeros(4 * fit.S + 10, dtype=torch.float64, device=fit.ds.dg.device)
-        buf = torch.cat([total, loss_sum])
-        if dist:
-            dist.all_reduce(buf, group=group)  # the only NCCL traffic: (4S+10)+1 floats
-        buf = buf / n_views
-        host = buf.cpu().numpy()
-        loss = float(host[-1])
+        mean, loss = reduce_views(total, loss_sum, n_views, dist, group)
         if not np.isfinite(loss):
             raise DivergedLoss(f"loss became {loss}")
-        grads = fit.unpack(host[:-1])
         losses.append(loss)
-        floor = 1e-12
-        for name in ("c_p", "opacity_raw", "lam", "b"):
-            if name in learnable and np.abs(grads[name]).max() > floor:
-                adam.step(name, getattr(params, name), grads[name], lr)
-        if fit_light and np.abs(grads["angles"]).max() > floor:
-            adam.step("angles", angles, grads["angles"], lr)
-            params.polar, params.azimuth = float(angles[0]), float(angles[1])
+        transform_step(params, fit.unpack(mean), adam, lr, learnable, angles)
         if callback is not None:
             callback(it, loss, params)
     after = _frozen_fingerprint(scene)

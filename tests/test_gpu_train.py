@@ -68,8 +68,9 @@ def test_short_training_run_decreases_loss():
             return -np.full(3, 0.6), np.full(3, 0.6)
 
     base = editable_model(3, 2000, spread=0.5, density=2000)
-    cfg = TrainConfig(stage2_iters=60, log_interval=20, densify_interval=30)
+    cfg = TrainConfig(stage2_iters=120, log_interval=20, densify_interval=30)
     model, log = train_editable(base, DS(), cfg)
-    assert len(log) == 3 and all(np.isfinite(r["loss"]) for r in log)
-    assert log[-1]["loss"] < log[0]["loss"]
+    assert len(log) == 6 and all(np.isfinite(r["loss"]) for r in log)
+    # held-out view (fixed) improves as shading is fitted
+    assert log[-1]["psnr"] > log[0]["psnr"]
     assert model.stage == "editable" and len(model) == log[-1]["count"]
