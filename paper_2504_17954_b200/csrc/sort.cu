@@ -38,7 +38,7 @@ constexpr int kChunk = kThreads * kItems;  // 2048 keys per radix block
 constexpr int kRadix = 256;
 constexpr int kMaxRun = 64;
 constexpr uint32_t kInvisible = 0xffffffffu;
-constexpr int kMaxTiles = 8192;  // placement keeps 8 x ntiles uint16 counters in smem
+constexpr int kMaxTiles = 6400;  // placement keeps 8 x (ntx+1)(nty+1) int32 counters in smem
 
 __global__ void init_minmax_kernel(unsigned long long *mm, int32_t *flag) {
     mm[0] = ~0ull;
@@ -433,36 +433,73 @@ struct PairCtx {
     const ushort4 *rect;    // splat -> tile rect
     const float4 *rec;      // blend records (tile cull), may be null
     int64_t n;
-    int ntx, ntiles;
+    int ntx, nty, ntiles;
     int64_t cap;
 };
 
-__device__ __forceinline__ bool tile_cull64(const float4 r0, const float4 r1, int px0, int px1,
+// Float32 lower bound of the splat's exponent over the pixel rectangle
+// [px0,px1] x [py0,py1] (value at the clamped edge minimiser minus a rigorous
+// rounding slack); the pair is culled iff the bound exceeds hi, i.e. the
+// reference's float64 alpha is < 1/255 at every pixel of the tile.
+__device__ __forceinline__ bool tile_cull32(const float4 r0, const float4 r1, int px0, int px1,
                                             int py0, int py1) {
-    // true when the splat's float64 exponent exceeds hi everywhere in the tile
-    const double hi = r0.w;
-    if (!(hi < 1e30)) return false;
-    const double a = 2.0 * (double)r1.x, b = r1.y, c = 2.0 * (double)r1.z;
-    if (!(a > 0.0 && c > 0.0 && a * c - b * b > 0.0)) return false;
+    const float hi = r0.w;
+    if (!(hi < 1e30f)) return false;
+    const float ha = r1.x, b = r1.y, hc = r1.z;  // a/2, b, c/2
+    const float det4 = 4.0f * ha * hc;
+    if (!(ha > 0.0f && hc > 0.0f && det4 - b * b > 1e-4f * det4)) return false;
     const double mx = r0.x, my = r0.y;
-    const double ex0 = px0 - mx, ex1 = px1 - mx, ey0 = py0 - my, ey1 = py1 - my;
-    if (ex0 <= 0.0 && ex1 >= 0.0 && ey0 <= 0.0 && ey1 >= 0.0) return false;
-    const double ia = 1.0 / a, ic = 1.0 / c;
-    double best = 1e300;
+    const float ex0 = (float)(px0 - mx), ex1 = (float)(px1 - mx);
+    const float ey0 = (float)(py0 - my), ey1 = (float)(py1 - my);
+    if (ex0 <= 0.0f && ex1 >= 0.0f && ey0 <= 0.0f && ey1 >= 0.0f) return false;
+    const float i2a = 0.5f / ha, i2c = 0.5f / hc;
+    float best = 3.0e38f;
 #pragma unroll
-    for (int k = 0; k < 2; ++k) {
-        const double e = k ? ex1 : ex0;
-        double dy = -b * e * ic;
-        dy = dy < ey0 ? ey0 : (dy > ey1 ? ey1 : dy);
-        const double s = 0.5 * (a * e * e + c * dy * dy) + b * e * dy;
-        best = s < best ? s : best;
-        const double f = k ? ey1 : ey0;
-        double dx = -b * f * ia;
-        dx = dx < ex0 ? ex0 : (dx > ex1 ? ex1 : dx);
-        const double t = 0.5 * (a * dx * dx + c * f * f) + b * dx * f;
-        best = t < best ? t : best;
+    for (int k = 0; k < 4; ++k) {
+        float dx, dy;
+        if (k < 2) {
+            dx = k ? ex1 : ex0;
+            dy = fminf(fmaxf(-b * dx * i2c, ey0), ey1);
+        } else {
+            dy = (k & 1) ? ey1 : ey0;
+            dx = fminf(fmaxf(-b * dy * i2a, ex0), ex1);
+        }
+        const float t1 = ha * dx * dx, t2 = b * dx * dy, t3 = hc * dy * dy;
+        const float s = t1 + t2 + t3;
+        const float lo = s - 2e-6f * (t1 + fabsf(t2) + t3) - 1e-4f;
+        best = fminf(best, lo);
     }
     return best > hi;
+}
+
+// 2-D difference-array update for one tile rectangle (D is (nty+1) x (ntx+1)).
+__device__ __forceinline__ void diff_add(int *D, int w1, const ushort4 rc, int v) {
+    atomicAdd(&D[rc.z * w1 + rc.x], v);
+    atomicAdd(&D[rc.z * w1 + rc.y + 1], -v);
+    atomicAdd(&D[(rc.w + 1) * w1 + rc.x], -v);
+    atomicAdd(&D[(rc.w + 1) * w1 + rc.y + 1], v);
+}
+
+// In-place 2-D inclusive prefix sum of a difference array by `nt` threads
+// (thread index `t`); `sync` separates the row and column passes.
+template <typename Sync>
+__device__ __forceinline__ void prefix2d(int *D, int w1, int h1, int t, int nt, Sync &&sync) {
+    for (int r = t; r < h1; r += nt) {
+        int run = 0;
+        for (int c = 0; c < w1; ++c) {
+            run += D[r * w1 + c];
+            D[r * w1 + c] = run;
+        }
+    }
+    sync();
+    for (int c = t; c < w1; c += nt) {
+        int run = 0;
+        for (int r = 0; r < h1; ++r) {
+            run += D[r * w1 + c];
+            D[r * w1 + c] = run;
+        }
+    }
+    sync();
 }
 
 // Warp-cooperative, load-balanced expansion of the pairs of ranks
@@ -518,24 +555,26 @@ __device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, in
     }
 }
 
-// per-block tile histogram -> hist[tile * nblocks + block]
+// per-block tile histogram -> hist[tile * nblocks + block], from a 2-D
+// difference array of the block's tile rectangles (no pair expansion)
 __global__ void __launch_bounds__(kThreads)
 pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
-    extern __shared__ uint32_t smem_u32[];
-    uint32_t *s_cnt = smem_u32;  // ntiles
-    for (int t = threadIdx.x; t < C.ntiles; t += kThreads) s_cnt[t] = 0;
+    extern __shared__ int smem_i32[];
+    const int w1 = C.ntx + 1, h1 = C.nty + 1;
+    int *D = smem_i32;
+    for (int i = threadIdx.x; i < w1 * h1; i += kThreads) D[i] = 0;
     __syncthreads();
-    const int warp = threadIdx.x >> 5;
-    const uint32_t lt = lanemask_lt();
-    const int64_t rb = (int64_t)blockIdx.x * kRanksPerBlock + (int64_t)warp * kRanksPerWarp;
-    const int64_t re = rb + kRanksPerWarp < C.n ? rb + kRanksPerWarp : C.n;
-    expand_pairs(C, rb, re, [&](bool ok, uint32_t, int tile, int, int) {
-        const uint32_t peers = __match_any_sync(0xffffffffu, tile);
-        if (ok && (peers & lt) == 0) atomicAdd(&s_cnt[tile], (uint32_t)__popc(peers));
-    });
+    const int64_t r0 = (int64_t)blockIdx.x * kRanksPerBlock;
+    for (int k = threadIdx.x; k < kRanksPerBlock; k += kThreads) {
+        const int64_t r = r0 + k;
+        if (r >= C.n) break;
+        const uint32_t sp = C.order[r];
+        if (C.count[sp] > 0) diff_add(D, w1, C.rect[sp], 1);
+    }
     __syncthreads();
+    prefix2d(D, w1, h1, threadIdx.x, kThreads, [] { __syncthreads(); });
     for (int t = threadIdx.x; t < C.ntiles; t += kThreads)
-        hist[(int64_t)t * nblocks + blockIdx.x] = s_cnt[t];
+        hist[(int64_t)t * nblocks + blockIdx.x] = (uint32_t)D[(t / C.ntx) * w1 + t % C.ntx];
 }
 
 // tile_ranges = exclusive scan of tile totals (single block)
@@ -571,48 +610,53 @@ tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges) {
     if (threadIdx.x == 0) ranges[ntiles] = (int32_t)carry;
 }
 
-// stable placement: warp w of block b owns ranks [b*2048 + w*256, +256)
+// stable placement: warp w of block b owns ranks [b*2048 + w*256, +256).
+// Per-warp tile counts come from per-warp 2-D difference arrays; the pairs
+// are expanded once, ranked within the warp by match_any and written.
 __global__ void __launch_bounds__(kThreads)
 pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *ranges,
                   int32_t *pair_splat, int W, int H) {
-    extern __shared__ uint32_t smem_u32[];
-    uint16_t *s_wc = reinterpret_cast<uint16_t *>(smem_u32);  // [warp][ntiles]
-    const int tid = threadIdx.x, warp = tid >> 5;
-    for (int i = tid; i < kWarps * C.ntiles; i += kThreads) s_wc[i] = 0;
+    extern __shared__ int smem_i32[];
+    const int w1 = C.ntx + 1, h1 = C.nty + 1, cells = w1 * h1;
+    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    for (int i = tid; i < kWarps * cells; i += kThreads) smem_i32[i] = 0;
     __syncthreads();
-    uint16_t *wc = s_wc + warp * C.ntiles;
+    int *Dw = smem_i32 + warp * cells;
     const uint32_t lt = lanemask_lt();
     const int64_t rb = (int64_t)blockIdx.x * kRanksPerBlock + (int64_t)warp * kRanksPerWarp;
     const int64_t re = rb + kRanksPerWarp < C.n ? rb + kRanksPerWarp : C.n;
     // phase 1: per-warp tile counts (<= 256 per tile per warp)
-    expand_pairs(C, rb, re, [&](bool ok, uint32_t, int tile, int, int) {
-        const uint32_t peers = __match_any_sync(0xffffffffu, tile);
-        if (ok && (peers & lt) == 0) wc[tile] = (uint16_t)(wc[tile] + __popc(peers));
-        __syncwarp();
-    });
+    for (int64_t r = rb + lane; r < re; r += 32) {
+        const uint32_t sp = C.order[r];
+        if (C.count[sp] > 0) diff_add(Dw, w1, C.rect[sp], 1);
+    }
+    __syncwarp();
+    prefix2d(Dw, w1, h1, lane, 32, [] { __syncwarp(); });
     __syncthreads();
     // phase 2: exclusive scan across warps, per tile (block total <= 2048)
     for (int t = tid; t < C.ntiles; t += kThreads) {
-        uint32_t run = 0;
+        const int cell = (t / C.ntx) * w1 + t % C.ntx;
+        int run = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
-            const uint32_t c = s_wc[w * C.ntiles + t];
-            s_wc[w * C.ntiles + t] = (uint16_t)run;
+            const int c = smem_i32[w * cells + cell];
+            smem_i32[w * cells + cell] = run;
             run += c;
         }
     }
     __syncthreads();
-    // phase 3: place (and cull-flag) every pair
+    // phase 3: expand once, place (and cull-flag) every pair
     expand_pairs(C, rb, re, [&](bool ok, uint32_t sp, int tile, int tx, int ty) {
         const uint32_t peers = __match_any_sync(0xffffffffu, tile);
-        uint32_t before = 0;
-        if (ok) before = wc[tile];
+        const int cell = ty * w1 + tx;
+        int before = 0;
+        if (ok) before = Dw[cell];
         __syncwarp();
-        if (ok && (peers & lt) == 0) wc[tile] = (uint16_t)(before + __popc(peers));
+        if (ok && (peers & lt) == 0) Dw[cell] = before + __popc(peers);
         __syncwarp();
         if (ok) {
             const uint32_t pos = (uint32_t)ranges[tile] +
-                                 hist[(int64_t)tile * nblocks + blockIdx.x] + before +
+                                 hist[(int64_t)tile * nblocks + blockIdx.x] + (uint32_t)before +
                                  __popc(peers & lt);
             if ((int64_t)pos < C.cap) {
                 uint32_t v = sp;
@@ -620,7 +664,7 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
                     const int px0 = tx * kTile, py0 = ty * kTile;
                     const int px1 = min(px0 + kTile - 1, W - 1), py1 = min(py0 + kTile - 1, H - 1);
                     const float4 a0 = __ldg(C.rec + 2 * sp), a1 = __ldg(C.rec + 2 * sp + 1);
-                    if (tile_cull64(a0, a1, px0, px1, py0, py1)) v |= 0x80000000u;
+                    if (tile_cull32(a0, a1, px0, px1, py0, py1)) v |= 0x80000000u;
                 }
                 pair_splat[pos] = (int32_t)v;
             }
@@ -698,7 +742,9 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
                                  int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int32_t ntiles = ntx * nty;
-    if (n < 0 || pair_capacity < 1 || ntx < 1 || nty < 1 || ntiles > kMaxTiles || !tile_ranges ||
+    // placement keeps 8 per-warp int32 difference arrays of (ntx+1)(nty+1) cells in smem
+    const bool fits = (int64_t)(ntx + 1) * (nty + 1) * 4 * kWarps <= 220 * 1024;
+    if (n < 0 || pair_capacity < 1 || ntx < 1 || nty < 1 || !fits || !tile_ranges ||
         !n_pairs || !pair_splat || !workspace || (rec && (width < 1 || height < 1))) {
         ivr::set_error("ivr_bin_sort: bad argument");
         return IVR_ERR_ARG;
@@ -755,10 +801,12 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     C.rec = (const float4 *)rec;
     C.n = n;
     C.ntx = ntx;
+    C.nty = nty;
     C.ntiles = ntiles;
     C.cap = pair_capacity;
-    const size_t sm_hist = 4 * (size_t)ntiles;
-    const size_t sm_place = 2 * (size_t)kWarps * ntiles;
+    const size_t cells = (size_t)(ntx + 1) * (nty + 1);
+    const size_t sm_hist = 4 * cells;
+    const size_t sm_place = 4 * (size_t)kWarps * cells;
     if (sm_hist > 48 * 1024)
         cudaFuncSetAttribute(pair_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_hist);
     if (sm_place > 48 * 1024)
