@@ -199,7 +199,8 @@ def run_ours(args):
     ds = DeviceScene(scene)
     n = ds.n
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
-    cams = [bench_camera(W_IMG, H_IMG, view_azimuth(rank, s)) for s in range(args.steps + args.warmup)]
+    cams = [bench_camera(W_IMG, H_IMG, view_azimuth(rank, s))
+            for s in range(max(args.steps, 10) + args.warmup)]
 
     # warm-up: first frame learns the pair capacity (one sync), then fast frames
     F = ds.render_frame(cams[0], fast=False)
