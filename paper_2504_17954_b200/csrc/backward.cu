@@ -21,6 +21,7 @@
 #include <math.h>
 
 #include "project.cuh"
+#include "cull.cuh"
 
 namespace ivr {
 
@@ -89,6 +90,8 @@ blend_bwd_kernel(BwdArgs A) {
     atomicMax(&s_end, last);
     __syncthreads();
     const int s_stop = s_end;  // no pixel of this tile contributes past here
+    const int cx0 = tx * kTile, cy0 = ty * kTile;
+    const int cx1 = min(cx0 + kTile - 1, A.W - 1), cy1 = min(cy0 + kTile - 1, A.H - 1);
 
     float C[KMAX], acc[KMAX], dout[KMAX];
 #pragma unroll
@@ -113,6 +116,7 @@ blend_bwd_kernel(BwdArgs A) {
             if (keep) {
                 r0 = __ldg(A.rec + 2 * sp);
                 r1 = __ldg(A.rec + 2 * sp + 1);
+                if (!A.preculled) keep = !tile_cull32(r0, r1, cx0, cx1, cy0, cy1);
             }
         }
         const uint32_t m = __ballot_sync(0xffffffffu, keep);

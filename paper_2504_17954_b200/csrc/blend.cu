@@ -27,7 +27,7 @@
 //    carry float32 rounding (~1e-6 against the 1e-4 tolerance).
 #include <math.h>
 
-#include "ivr_common.cuh"
+#include "cull.cuh"
 
 namespace ivr {
 
@@ -161,7 +161,7 @@ __device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int
             } else {
                 r0 = __ldg(A.rec + 2 * sp);
                 r1 = __ldg(A.rec + 2 * sp + 1);
-                keep = tile_touch(r0, r1, px0, px1, py0, py1);
+                keep = !tile_cull32(r0, r1, px0, px1, py0, py1);
             }
         }
         const uint32_t m = __ballot_sync(0xffffffffu, keep);

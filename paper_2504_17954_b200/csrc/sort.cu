@@ -26,7 +26,7 @@
 //     reference list), letting the blend skip them without loading records.
 // All data-dependent sizes live in device memory: the sequence is
 // stream-ordered and CUDA-graph capturable.
-#include "ivr_common.cuh"
+#include "cull.cuh"
 
 namespace ivr {
 namespace sortk {
@@ -436,41 +436,6 @@ struct PairCtx {
     int ntx, nty, ntiles;
     int64_t cap;
 };
-
-// Float32 lower bound of the splat's exponent over the pixel rectangle
-// [px0,px1] x [py0,py1] (value at the clamped edge minimiser minus a rigorous
-// rounding slack); the pair is culled iff the bound exceeds hi, i.e. the
-// reference's float64 alpha is < 1/255 at every pixel of the tile.
-__device__ __forceinline__ bool tile_cull32(const float4 r0, const float4 r1, int px0, int px1,
-                                            int py0, int py1) {
-    const float hi = r0.w;
-    if (!(hi < 1e30f)) return false;
-    const float ha = r1.x, b = r1.y, hc = r1.z;  // a/2, b, c/2
-    const float det4 = 4.0f * ha * hc;
-    if (!(ha > 0.0f && hc > 0.0f && det4 - b * b > 1e-4f * det4)) return false;
-    const double mx = r0.x, my = r0.y;
-    const float ex0 = (float)(px0 - mx), ex1 = (float)(px1 - mx);
-    const float ey0 = (float)(py0 - my), ey1 = (float)(py1 - my);
-    if (ex0 <= 0.0f && ex1 >= 0.0f && ey0 <= 0.0f && ey1 >= 0.0f) return false;
-    const float i2a = 0.5f / ha, i2c = 0.5f / hc;
-    float best = 3.0e38f;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-        float dx, dy;
-        if (k < 2) {
-            dx = k ? ex1 : ex0;
-            dy = fminf(fmaxf(-b * dx * i2c, ey0), ey1);
-        } else {
-            dy = (k & 1) ? ey1 : ey0;
-            dx = fminf(fmaxf(-b * dy * i2a, ex0), ex1);
-        }
-        const float t1 = ha * dx * dx, t2 = b * dx * dy, t3 = hc * dy * dy;
-        const float s = t1 + t2 + t3;
-        const float lo = s - 2e-6f * (t1 + fabsf(t2) + t3) - 1e-4f;
-        best = fminf(best, lo);
-    }
-    return best > hi;
-}
 
 // 2-D difference-array update for one tile rectangle (D is (nty+1) x (ntx+1)).
 __device__ __forceinline__ void diff_add(int *D, int w1, const ushort4 rc, int v) {

@@ -238,12 +238,15 @@ def bin_sort(F: Frame, ws: Workspace, stream=None, capacity=None):
     F.tile_ranges = ws.get("tile_ranges", ntx * nty + 1, torch.int32)
     F.n_pairs = ws.get("n_pairs", 1, torch.int32)
     F.capacity = cap
-    # K2 with the per-pair tile cull (bit 31 of pair_splat; masked in .pairs())
-    L.check(L.lib().ivr_bin_sort_cull(n, ptr(F.depth_key), ptr(F.count), ptr(F.rect), ptr(F.rec),
-                                      ntx, nty, cam.width, cam.height, cap, ptr(scratch), nbytes,
-                                      ptr(F.pair_splat), ptr(F.tile_ranges), ptr(F.n_pairs),
-                                      stream_handle(stream)), "ivr_bin_sort_cull")
-    F.preculled = True
+    # K2; the per-(splat, tile) cull runs in K3/K4 staging (precull=False) or
+    # here as bit 31 of pair_splat (precull=True; masked in .pairs())
+    precull = os.environ.get("IVR_PRECULL", "0") == "1"
+    L.check(L.lib().ivr_bin_sort_cull(n, ptr(F.depth_key), ptr(F.count), ptr(F.rect),
+                                      ptr(F.rec) if precull else None, ntx, nty, cam.width,
+                                      cam.height, cap, ptr(scratch), nbytes, ptr(F.pair_splat),
+                                      ptr(F.tile_ranges), ptr(F.n_pairs), stream_handle(stream)),
+            "ivr_bin_sort_cull")
+    F.preculled = precull
     F.tile_order = None
     if ntx * nty <= 4096 and os.environ.get("IVR_TILE_ORDER", "1") != "0":
         F.tile_order = ws.get("tile_order", ntx * nty, torch.int32)
