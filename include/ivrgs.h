@@ -198,8 +198,9 @@ int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_splat,
                   int32_t *contrib, int32_t *last_pos, double *t_final,
                   const int32_t *tile_order, int32_t flags, ivr_stream_t stream);
 
-/* Heaviest-first tile launch order (descending pair count, ties by tile id)
- * for ivr_blend_fwd; ntiles <= 4096. */
+/* Heaviest-first tile launch order for ivr_blend_fwd (counting sort on
+ * half-octave buckets of the per-tile pair count, descending).  Scheduling
+ * only: any permutation yields identical images. */
 int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_t *order,
                    ivr_stream_t stream);
 

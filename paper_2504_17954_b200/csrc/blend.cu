@@ -132,6 +132,7 @@ struct Smem {
     double *r64;  // F64: 6 per pair (mx, my, a, b, c, o)
     double *v64;  // F64: KMAX per pair
     int *wsum;
+    uint32_t *wmask;  // [warp][kBlendThreads/32] strip-filter bitmasks
 };
 
 // One pass over the tile's pair list for every pixel with !st.done.
@@ -197,9 +198,28 @@ __device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int
             }
         }
         __syncthreads();
+        // ---- per-warp strip filter: keep survivors that can reach alpha 1/255
+        // in this warp's 16x2 pixel strip (same rigorous test as the tile cull)
+        if (!__any_sync(0xffffffffu, !st.done)) continue;
+        const int nwords = (total + 31) >> 5;
+        {
+            const int wy0 = min(py0 + 2 * warp, A.H - 1), wy1 = min(py0 + 2 * warp + 1, A.H - 1);
+            for (int w = 0; w < nwords; ++w) {
+                const int q = (w << 5) + lane;
+                bool t = false;
+                if (q < total) t = !tile_cull32(S.r0[q], S.r1[q], px0, px1, wy0, wy1);
+                const uint32_t b = __ballot_sync(0xffffffffu, t);
+                if (lane == 0) S.wmask[warp * (kBlendThreads / 32) + w] = b;
+            }
+            __syncwarp();
+        }
         if (st.done) continue;
-        // ---- per-pixel walk over the survivors, in list order
-        for (int q = 0; q < total; ++q) {
+        // ---- per-pixel walk over the strip's survivors, in list order
+        for (int w = 0; w < nwords; ++w) {
+          uint32_t mbits = S.wmask[warp * (kBlendThreads / 32) + w];
+          while (mbits) {
+            const int q = (w << 5) + __ffs(mbits) - 1;
+            mbits &= mbits - 1;
             const float4 a0 = S.r0[q];
             const float4 a1 = S.r1[q];
             const float dx = fpx - a0.x, dy = fpy - a0.y;
@@ -233,7 +253,7 @@ __device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int
                 st.last = S.j[q] + 1;
                 if (st.T < kTStop) {
                     st.done = true;
-                    break;
+                    goto batch_done;
                 }
             } else {
                 // candidate: in dtype=float64 mode recompute dx, dy from the float64 mean
@@ -288,10 +308,12 @@ __device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int
                 if (st.Tf < 1e-4f * (1.0f + st.errT + 1e-6f)) {
                     st.done = true;  // certain stop, or ambiguous -> EXACT re-walk
                     st.replay = !(st.Tf < 1e-4f * (1.0f - st.errT - 1e-6f));
-                    break;
+                    goto batch_done;
                 }
             }
+          }
         }
+    batch_done:;
     }
 }
 
@@ -300,6 +322,7 @@ __global__ void __launch_bounds__(kBlendThreads, 3)
 blend_fwd_kernel(BlendArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     __shared__ int s_wsum[kBlendThreads / 32];
+    __shared__ uint32_t s_wmask[(kBlendThreads / 32) * (kBlendThreads / 32)];
     Smem S;
     S.r0 = reinterpret_cast<float4 *>(smem);
     S.r1 = S.r0 + kBlendThreads;
@@ -309,6 +332,7 @@ blend_fwd_kernel(BlendArgs A) {
     S.r64 = reinterpret_cast<double *>(S.v + kBlendThreads * KMAX);
     S.v64 = S.r64 + (F64 ? 6 * kBlendThreads : 0);
     S.wsum = s_wsum;
+    S.wmask = s_wmask;
 
     const int tile = A.tile_order ? A.tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % A.ntx, ty = tile / A.ntx;
@@ -374,36 +398,33 @@ int launch_blend(const BlendArgs &A, int ntiles, cudaStream_t st) {
 // ----------------------------------------------------------------- tile order
 // Heaviest tiles first: a tile's CTA runtime grows with its pair count, and the
 // longest tiles otherwise start in the last wave and set the frame's tail.
-// Single CTA bitonic sort of (count desc, tile asc) for up to 4096 tiles.
+// The order is only a schedule (any permutation gives identical results), so
+// a single-CTA counting sort on half-octave buckets of the pair count
+// (descending) is enough: histogram, scan, scatter.
+constexpr int kOrderBuckets = 64;
+
 __global__ void __launch_bounds__(1024)
 tile_order_kernel(const int32_t *ranges, int ntiles, int32_t *order) {
-    __shared__ unsigned long long key[4096];
-    const int n2 = 4096;
-    for (int i = threadIdx.x; i < n2; i += 1024) {
-        unsigned long long k = ~0ull;
-        if (i < ntiles) {
-            const uint32_t cnt = (uint32_t)(ranges[i + 1] - ranges[i]);
-            k = ((unsigned long long)(0xffffffffu - cnt) << 32) | (uint32_t)i;
+    __shared__ int s_hist[kOrderBuckets];
+    if (threadIdx.x < kOrderBuckets) s_hist[threadIdx.x] = 0;
+    __syncthreads();
+    auto bucket = [](int cnt) {
+        const int b = (int)(2.0f * __log2f((float)cnt + 1.0f));
+        return kOrderBuckets - 1 - (b < kOrderBuckets - 1 ? b : kOrderBuckets - 1);
+    };
+    for (int t = threadIdx.x; t < ntiles; t += 1024) atomicAdd(&s_hist[bucket(ranges[t + 1] - ranges[t])], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int b = 0; b < kOrderBuckets; ++b) {
+            const int c = s_hist[b];
+            s_hist[b] = run;
+            run += c;
         }
-        key[i] = k;
     }
     __syncthreads();
-    for (int size = 2; size <= n2; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int i = threadIdx.x; i < n2 / 2; i += 1024) {
-                const int lo = 2 * i - (i & (stride - 1));
-                const int hi = lo + stride;
-                const bool up = ((lo & size) == 0);
-                const unsigned long long a = key[lo], b = key[hi];
-                if ((a > b) == up) {
-                    key[lo] = b;
-                    key[hi] = a;
-                }
-            }
-            __syncthreads();
-        }
-    }
-    for (int i = threadIdx.x; i < ntiles; i += 1024) order[i] = (int32_t)(key[i] & 0xffffffffu);
+    for (int t = threadIdx.x; t < ntiles; t += 1024)
+        order[atomicAdd(&s_hist[bucket(ranges[t + 1] - ranges[t])], 1)] = t;
 }
 
 }  // namespace ivr
@@ -413,10 +434,6 @@ extern "C" int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_
     using namespace ivr;
     if (!tile_ranges || !order || ntiles < 1) {
         set_error("ivr_tile_order: bad argument");
-        return IVR_ERR_ARG;
-    }
-    if (ntiles > 4096) {
-        set_error("ivr_tile_order: more than 4096 tiles");
         return IVR_ERR_ARG;
     }
     tile_order_kernel<<<1, 1024, 0, (cudaStream_t)stream>>>(tile_ranges, ntiles, order);

@@ -38,7 +38,6 @@ constexpr int kChunk = kThreads * kItems;  // 2048 keys per radix block
 constexpr int kRadix = 256;
 constexpr int kMaxRun = 64;
 constexpr uint32_t kInvisible = 0xffffffffu;
-constexpr int kMaxTiles = 6400;  // placement keeps 8 x (ntx+1)(nty+1) int32 counters in smem
 
 __global__ void init_minmax_kernel(unsigned long long *mm, int32_t *flag) {
     mm[0] = ~0ull;

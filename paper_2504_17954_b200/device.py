@@ -248,7 +248,7 @@ def bin_sort(F: Frame, ws: Workspace, stream=None, capacity=None):
             "ivr_bin_sort_cull")
     F.preculled = precull
     F.tile_order = None
-    if ntx * nty <= 4096 and os.environ.get("IVR_TILE_ORDER", "1") != "0":
+    if os.environ.get("IVR_TILE_ORDER", "1") != "0":
         F.tile_order = ws.get("tile_order", ntx * nty, torch.int32)
         L.check(L.lib().ivr_tile_order(ptr(F.tile_ranges), ntx * nty, ptr(F.tile_order),
                                        stream_handle(stream)), "ivr_tile_order")
