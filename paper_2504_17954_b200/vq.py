@@ -112,46 +112,66 @@ def kmeans(samples, k, seed=0, restarts=5):
         raise EmptyInput("kmeans needs at least one sample")
     if k < 1:
         raise OutOfRange("codebook size must be >= 1")
-    distinct = np.unique(samples)
-    if distinct.size <= k:
-        return distinct
+    x = D.to_dev(samples)
+    distinct = torch.unique(x)  # sorted
+    if distinct.numel() <= k:
+        return distinct.cpu().numpy()
     rng = np.random.default_rng(seed)
-    x_dev = D.to_dev(samples)
+    n = samples.size
     best, best_sse = None, np.inf
     for _ in range(restarts):
-        c = np.empty(k)
-        c[0] = samples[rng.integers(samples.size)]
-        d2 = (samples - c[0]) ** 2
-        for i in range(1, k):
-            total = d2.sum()
-            if total <= 0.0:
-                c[i:] = c[0]
-                break
-            c[i] = samples[rng.choice(samples.size, p=d2 / total)]
-            d2 = np.minimum(d2, (samples - c[i]) ** 2)
-        c = _lloyd(samples, x_dev, c)
-        idx = assign_nearest(samples, c)
-        sse = float(np.sum((samples - c[idx]) ** 2))
+        c = _seed_plusplus(x, k, rng)
+        c = _lloyd(x, c)
+        idx = _assign_idx(x, c)
+        sse = float(((x - c[idx]) ** 2).sum())
         if sse < best_sse:
             best, best_sse = c, sse
-    return np.unique(best)
+    del n
+    return torch.unique(best).cpu().numpy()
 
 
-def _lloyd(samples, x_dev, c):
-    scale = max(float(np.abs(samples).max()), 1e-12)
+def _seed_plusplus(x, k, rng):
+    """k-means++ seeding on the device (vq.py:60-72) with the reference's
+    random stream: rng.integers for the first centre, then one rng.random()
+    per rng.choice(p = d2 / sum d2) (inverse CDF, side='right')."""
+    n = x.numel()
+    first = int(rng.integers(n))
+    u = torch.from_numpy(rng.random(k - 1)).to(x.device)
+    c = torch.empty(k, dtype=torch.float64, device=x.device)
+    c[0] = x[first]
+    d2 = (x - c[0]) ** 2
+    for i in range(1, k):
+        cdf = torch.cumsum(d2, 0)
+        tot = cdf[-1]
+        j = torch.searchsorted(cdf, (u[i - 1] * tot).reshape(1), right=True).clamp_(max=n - 1)
+        ci = torch.where(tot > 0, x[j], c[0])  # all mass on existing centres: repeat c[0]
+        c[i] = ci[0]
+        d2 = torch.minimum(d2, (x - ci) ** 2)
+    return c
+
+
+def _assign_idx(x, c):
+    if c.numel() == 1:
+        return torch.zeros(x.numel(), dtype=torch.int64, device=x.device)
+    return assign_device(x, c.contiguous()).view(torch.uint16).to(torch.int64)
+
+
+def _lloyd(x, c):
+    """Lloyd iterations on the device (vq.py:75-87): assign with K5, centroid
+    update with bincount sums (float64)."""
+    scale = max(float(x.abs().max()), 1e-12)
+    k = c.numel()
     for _ in range(KMEANS_MAX_ITERS):
-        c = np.sort(c)
-        idx = assign_device(x_dev, D.to_dev(c)).view(torch.uint16).to(torch.int64) \
-            if c.size > 1 else torch.zeros(samples.size, dtype=torch.int64, device=x_dev.device)
-        idx_h = idx.cpu().numpy()
-        sums = np.bincount(idx_h, weights=samples, minlength=c.size)
-        cnt = np.bincount(idx_h, minlength=c.size)
-        new = np.where(cnt > 0, sums / np.maximum(cnt, 1), c)
-        shift = np.abs(new - c).max() / scale
+        c = torch.sort(c).values
+        idx = _assign_idx(x, c)
+        sums = torch.bincount(idx, weights=x, minlength=k)
+        cnt = torch.bincount(idx, minlength=k)
+        new = torch.where(cnt > 0, sums / torch.clamp(cnt, min=1).to(torch.float64), c)
+        shift = float((new - c).abs().max()) / scale
         c = new
         if shift < KMEANS_SHIFT_TOL:
             break
-    return np.sort(c)
+    return torch.sort(c).values
 
 
 def quantize_attributes(arrays, k=DEFAULT_CODEBOOK_SIZE, seed=0):
