@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--cpu-frames", type=int, default=2)
+    ap.add_argument("--no-extra", action="store_true",
+                    help="skip the C3 train / C4 inverse / C5 VQ secondary measurements")
     return ap.parse_args()
 
 
@@ -184,6 +186,105 @@ def run_reference(args):
     print(json.dumps(line), flush=True)
 
 
+def _device_time(fn, steps, warmup=2):
+    """Mean device ms of fn() over `steps` calls (CUDA events, L2 flushed)."""
+    import torch
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(warmup):
+        fn()
+    torch.cuda.synchronize()
+    ts = []
+    for _ in range(steps):
+        flush.zero_()
+        e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        e0.record()
+        fn()
+        e1.record()
+        torch.cuda.synchronize()
+        ts.append(e0.elapsed_time(e1))
+    return float(np.mean(ts)), float(np.median(ts))
+
+
+def bench_train(scene):
+    """C3: stage-2 training step (K=15 channels, fwd + all losses + bwd +
+    Adam) on one 300k-Gaussian basic model at 800x800, one view / iteration."""
+    from paper_2504_17954_b200 import LightConfig
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
+    from paper_2504_17954_b200.trainer import EditableTrainer, _stage2_init
+    a = editable_arrays(0, 300_000, density=300_000)
+    light = LightConfig("orbital", 0.45, 0.9)
+    cams = [bench_camera(W_IMG, H_IMG, az) for az in np.linspace(-3.0, 3.0, 8)]
+    gt_tr = EditableTrainer(a, a["palette"], light)
+    gts = [gt_tr.render_rgba(c).clone() for c in cams]
+    p = {k: a[k] for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw")}
+    p.update(_stage2_init(300_000))
+    tr = EditableTrainer(p, a["palette"], light)
+    it = [0]
+
+    def step():
+        v = it[0] % len(cams)
+        it[0] += 1
+        loss, grads, _ = tr.step(cams[v], gts[v])
+        tr.apply(grads, it[0], 10000)
+    mean_ms, med_ms = _device_time(step, 10)
+    return {"metric": "stage-2 train it/s (300k Gaussians, 800x800, K=15, 1 view/it)",
+            "value": 1000.0 / mean_ms, "unit": "it/s", "ms_per_it": mean_ms,
+            "ms_per_it_median": med_ms, "n_gaussians": 300_000,
+            "note": "includes fwd (K1-K3), L1+SSIM + normal/offset/bilateral/opacity terms, "
+                    "K4a+K4b, Adam; densify excluded"}
+
+
+def bench_inverse(scene):
+    """C4: one inverse-exploration iteration on the composed 1M scene (render
+    f64-semantics + loss + transform-only backward + Adam), 1 view."""
+    from paper_2504_17954_b200.inverse import (Adam, InverseFitter, init_transform, reduce_views,
+                                               transform_step)
+    from paper_2504_17954_b200.synthetic import bench_camera
+    cam = bench_camera(W_IMG, H_IMG, 0.8)
+    p_true = init_transform(scene)
+    p_true.lam = np.array([1.2, 0.8, 1.0, 1.0])
+    fit0 = InverseFitter(scene, [], [])
+    ref = fit0.render(p_true, cam).out64.clone()
+    fit = InverseFitter(scene, [ref], [cam], ds=fit0.ds)
+    params = init_transform(scene)
+    adam = Adam(eps=1e-15)
+    angles = np.array([params.polar, params.azimuth])
+
+    def step():
+        loss, packed = fit.view_grads(params, 0)
+        mean, lv = reduce_views(packed, loss.reshape(1), 1.0)
+        transform_step(params, fit.unpack(mean), adam, 0.01,
+                       ("c_p", "opacity_raw", "lam", "b", "angles"), angles)
+    mean_ms, med_ms = _device_time(step, 10)
+    return {"metric": "inverse exploration it/s (composed 1M, 800x800, 1 view)",
+            "value": 1000.0 / mean_ms, "unit": "it/s", "ms_per_it": mean_ms,
+            "ms_per_it_median": med_ms,
+            "note": "includes the per-iteration pair-count sync and host Adam on 30 floats"}
+
+
+def bench_vq(scene):
+    """C5: K5 assign + K6 decode over the 60M scalar attribute values of a 4M
+    editable model with a 4096-entry codebook (HBM-bound)."""
+    import torch
+    from paper_2504_17954_b200.vq import assign_device, decode_device
+    n_vals = 4_000_000 * 15
+    g = torch.Generator(device="cuda").manual_seed(0)
+    vals = torch.randn(n_vals, dtype=torch.float64, device="cuda", generator=g)
+    cents = torch.sort(torch.randn(4096, dtype=torch.float64, device="cuda", generator=g)).values
+    out = {}
+    a_ms, _ = _device_time(lambda: out.__setitem__("idx", assign_device(vals, cents)), 5)
+    d_ms, _ = _device_time(lambda: decode_device(out["idx"], cents), 5)
+    hbm = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)) \
+        if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
+    a_gbs = n_vals * 10 / (a_ms * 1e-3) / 1e9
+    d_gbs = n_vals * 10 / (d_ms * 1e-3) / 1e9
+    return {"metric": "VQ assign/decode over 60M values, K=4096", "assign_ms": a_ms,
+            "decode_ms": d_ms, "assign_gbs": a_gbs, "decode_gbs": d_gbs,
+            "assign_hbm_frac": a_gbs / hbm, "decode_hbm_frac": d_gbs / hbm,
+            "alg_bytes_per_value": 10}
+
+
 def run_ours(args):
     import torch
     rank, local_rank, world = dist_env()
@@ -312,6 +413,17 @@ def run_ours(args):
                "sample": f"{max(1, args.cpu_frames)} full C2 frames (1M Gaussians, 800x800) "
                          "via oracle/ (numpy + C/OpenMP)"}
 
+    extra = None
+    if world == 1 and not args.no_extra:
+        extra = {}
+        for name, fn in (("train_c3", bench_train), ("inverse_c4", bench_inverse),
+                         ("vq_c5", bench_vq)):
+            try:
+                extra[name] = fn(scene)
+            except Exception as e:  # report, never hide the headline line
+                extra[name] = {"error": f"{type(e).__name__}: {e}"}
+            torch.cuda.empty_cache()
+
     if rank == 0:
         line = {"metric": METRIC, "value": fps_total, "unit": "frames/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
@@ -322,7 +434,8 @@ def run_ours(args):
                 "e2e": {"value": e2e_fps, "unit": "frames/s",
                         "h2d_bytes_per_step": fg.nb + 32 * ds.n_scenes,
                         "d2h_bytes_per_step": H_IMG * W_IMG * (4 * 4 + 4)},
-                "gpu_launches": LAUNCHES_PER_FRAME * args.steps, "overflow": overflow}
+                "gpu_launches": LAUNCHES_PER_FRAME * args.steps, "overflow": overflow,
+                "extra": extra}
         print(json.dumps(line), flush=True)
     if dist:
         dist.destroy_process_group()
