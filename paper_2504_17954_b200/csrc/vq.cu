@@ -24,20 +24,40 @@ vq_assign_kernel(const double *__restrict__ values, int64_t n, const double *__r
             s_mid[i] = 0.5 * (cents[i + 1] + cents[i]);
         __syncthreads();
     }
-    for (int64_t i = (int64_t)blockIdx.x * kVqThreads + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * kVqThreads) {
-        const double v = values[i];
-        int lo = 0, hi = k - 1;  // first mid index with mid >= v (searchsorted 'left')
-        if (v != v) {
-            lo = k - 1;
-        } else {
-            while (lo < hi) {
-                const int m = (lo + hi) >> 1;
-                const double mid = SMEM ? s_mid[m] : 0.5 * (__ldg(cents + m + 1) + __ldg(cents + m));
-                if (mid < v) lo = m + 1; else hi = m;
+    // searchsorted(mids, v, 'left') = number of mids < v.  Fixed-trip-count
+    // binary search over kVqIlp independent values per thread, interleaved so
+    // the shared-memory loads of different values overlap (the search is
+    // latency-bound, not bandwidth-bound).
+    const int nm = k - 1;
+    int top = 1;
+    while ((top << 1) <= nm) top <<= 1;
+    constexpr int kVqIlp = 8;
+    const int64_t chunk = (int64_t)kVqThreads * kVqIlp;
+    for (int64_t base = (int64_t)blockIdx.x * chunk; base < n; base += (int64_t)gridDim.x * chunk) {
+        double v[kVqIlp];
+        int pos[kVqIlp];
+#pragma unroll
+        for (int r = 0; r < kVqIlp; ++r) {
+            const int64_t i = base + r * kVqThreads + threadIdx.x;
+            v[r] = i < n ? values[i] : 0.0;
+            pos[r] = 0;
+        }
+        for (int step = top; step > 0; step >>= 1) {
+#pragma unroll
+            for (int r = 0; r < kVqIlp; ++r) {
+                const int m = pos[r] + step;
+                if (m <= nm) {
+                    const double mid = SMEM ? s_mid[m - 1]
+                                            : 0.5 * (__ldg(cents + m) + __ldg(cents + m - 1));
+                    if (mid < v[r]) pos[r] = m;
+                }
             }
         }
-        out[i] = (uint16_t)lo;
+#pragma unroll
+        for (int r = 0; r < kVqIlp; ++r) {
+            const int64_t i = base + r * kVqThreads + threadIdx.x;
+            if (i < n) out[i] = (uint16_t)(v[r] != v[r] ? nm : pos[r]);  // NaN sorts last
+        }
     }
 }
 
