@@ -63,6 +63,29 @@ __device__ __forceinline__ float warp_sum(float x) {
     return x;
 }
 
+// Transpose reduction of NS per-lane values: each step a lane keeps one half
+// of its array and trades the other half with its partner at xor offset h, so
+// after log2(NS) steps lane l holds slot (l & (NS-1)) summed over its NS-lane
+// group; a final xor over the remaining lane bits completes the warp total.
+// NS-1 (+1 for NS=16) shuffles in place of 5 per slot.
+template <int NS>
+__device__ __forceinline__ float warp_transpose_sum(float *x, int lane) {
+#pragma unroll
+    for (int h = NS / 2; h >= 1; h >>= 1) {
+        const bool up = (lane & h) != 0;
+#pragma unroll
+        for (int i = 0; i < h; ++i) {
+            const float send = up ? x[i] : x[i + h];
+            const float keep = up ? x[i + h] : x[i];
+            x[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
+        }
+    }
+    float r = x[0];
+#pragma unroll
+    for (int o = NS; o < 32; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
+    return r;
+}
+
 template <int KMAX, bool F64>
 __global__ void __launch_bounds__(kBwdThreads)
 blend_bwd_kernel(BwdArgs A) {
@@ -74,6 +97,7 @@ blend_bwd_kernel(BwdArgs A) {
     float *s_v = reinterpret_cast<float *>(s_sp + kBwdThreads);
     double *s_r64 = reinterpret_cast<double *>(s_v + kBwdThreads * KMAX);
     __shared__ int s_wsum[kBwdThreads / 32];
+    __shared__ uint32_t s_wmask[(kBwdThreads / 32) * (kBwdThreads / 32)];
     __shared__ int s_end;
 
     const int tile = blockIdx.x;
@@ -146,7 +170,24 @@ blend_bwd_kernel(BwdArgs A) {
             }
         }
         __syncthreads();
-        for (int q = 0; q < total; ++q) {
+        // per-warp strip filter (as in K3): survivors that can touch this warp's 16x2 pixels
+        const int nwords = (total + 31) >> 5;
+        {
+            const int wy0 = min(cy0 + 2 * warp, A.H - 1), wy1 = min(cy0 + 2 * warp + 1, A.H - 1);
+            for (int w = 0; w < nwords; ++w) {
+                const int q = (w << 5) + lane;
+                bool t = false;
+                if (q < total) t = !tile_cull32(s_r0[q], s_r1[q], cx0, cx1, wy0, wy1);
+                const uint32_t b = __ballot_sync(0xffffffffu, t);
+                if (lane == 0) s_wmask[warp * (kBwdThreads / 32) + w] = b;
+            }
+            __syncwarp();
+        }
+        for (int w = 0; w < nwords; ++w) {
+          uint32_t mbits = s_wmask[warp * (kBwdThreads / 32) + w];
+          while (mbits) {
+            const int q = (w << 5) + __ffs(mbits) - 1;
+            mbits &= mbits - 1;
             const float4 a0 = s_r0[q];
             const float4 a1 = s_r1[q];
             bool contrib = false;
@@ -195,10 +236,14 @@ blend_bwd_kernel(BwdArgs A) {
                     dy = cdy;
                 }
             }
-            // per-pixel contributions (zero when not contributing)
-            float gv[KMAX], gm0 = 0.f, gm1 = 0.f, gc0 = 0.f, gc1 = 0.f, gc2 = 0.f, go = 0.f;
+            // per-pixel contributions in fixed slots: [0,K) d_values, KMAX/KMAX+1
+            // d_mean2d, KMAX+2..KMAX+4 d_conic, KMAX+5 d_opacity (zero when not
+            // contributing); reduced in chunks of CH lanes
+            constexpr int CH = KMAX + 6 <= 16 ? 16 : 32;
+            constexpr int NX = (KMAX + 6 + CH - 1) / CH * CH;
+            float x[NX];
 #pragma unroll
-            for (int c = 0; c < KMAX; ++c) gv[c] = 0.f;
+            for (int c = 0; c < NX; ++c) x[c] = 0.f;
             if (contrib) {
                 const float w = T * al;
                 const float inv = __frcp_rn(1.0f - al);
@@ -210,42 +255,40 @@ blend_bwd_kernel(BwdArgs A) {
                         acc[c] = fmaf(w, vk, acc[c]);
                         const float after = C[c] - acc[c];
                         d_alpha = fmaf(dout[c], T * vk - after * inv, d_alpha);
-                        gv[c] = dout[c] * w;
+                        x[c] = dout[c] * w;
                     }
                 }
                 if (alu < 0.99f) {
-                    go = g * d_alpha;
                     const float d_sigma = -alu * d_alpha;
-                    gc0 = 0.5f * dx * dx * d_sigma;
-                    gc1 = dx * dy * d_sigma;
-                    gc2 = 0.5f * dy * dy * d_sigma;
                     const float ca = 2.0f * a1.x, cb = a1.y, cc = 2.0f * a1.z;
-                    gm0 = -d_sigma * (ca * dx + cb * dy);
-                    gm1 = -d_sigma * (cb * dx + cc * dy);
+                    x[KMAX] = -d_sigma * (ca * dx + cb * dy);
+                    x[KMAX + 1] = -d_sigma * (cb * dx + cc * dy);
+                    x[KMAX + 2] = 0.5f * dx * dx * d_sigma;
+                    x[KMAX + 3] = dx * dy * d_sigma;
+                    x[KMAX + 4] = 0.5f * dy * dy * d_sigma;
+                    x[KMAX + 5] = g * d_alpha;
                 }
                 T = T * (1.0f - al);
             }
             if (__any_sync(0xffffffffu, contrib)) {
+                // transpose reduction: lane i ends with the warp total of slot i
+                // (CH-1 shuffles per chunk instead of 5 per slot), then parallel atomics
                 const int s = s_sp[q];
 #pragma unroll
-                for (int c = 0; c < KMAX; ++c) {
-                    if (c < K) {
-                        const float r = warp_sum(gv[c]);
-                        if (lane == 0 && r != 0.f) atomicAdd(A.g_values + (int64_t)K * s + c, r);
+                for (int ch = 0; ch < NX / CH; ++ch) {
+                    const float tot = warp_transpose_sum<CH>(x + ch * CH, lane);
+                    const int slot = ch * CH + (lane & (CH - 1));
+                    if (lane < CH && tot != 0.f) {
+                        float *dst = nullptr;
+                        if (slot < K) dst = A.g_values + (int64_t)K * s + slot;
+                        else if (slot >= KMAX && slot < KMAX + 2) dst = A.g_mean + 2 * (int64_t)s + (slot - KMAX);
+                        else if (slot >= KMAX + 2 && slot < KMAX + 5) dst = A.g_conic + 3 * (int64_t)s + (slot - KMAX - 2);
+                        else if (slot == KMAX + 5) dst = A.g_opac + s;
+                        if (dst) atomicAdd(dst, tot);
                     }
                 }
-                const float r0s = warp_sum(gm0), r1s = warp_sum(gm1);
-                const float c0s = warp_sum(gc0), c1s = warp_sum(gc1), c2s = warp_sum(gc2);
-                const float os = warp_sum(go);
-                if (lane == 0) {
-                    if (r0s != 0.f) atomicAdd(A.g_mean + 2 * (int64_t)s, r0s);
-                    if (r1s != 0.f) atomicAdd(A.g_mean + 2 * (int64_t)s + 1, r1s);
-                    if (c0s != 0.f) atomicAdd(A.g_conic + 3 * (int64_t)s, c0s);
-                    if (c1s != 0.f) atomicAdd(A.g_conic + 3 * (int64_t)s + 1, c1s);
-                    if (c2s != 0.f) atomicAdd(A.g_conic + 3 * (int64_t)s + 2, c2s);
-                    if (os != 0.f) atomicAdd(A.g_opac + s, os);
-                }
             }
+          }
         }
     }
 }
