@@ -260,10 +260,25 @@ int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *shading,
 int ivr_vq_assign(const double *values, int64_t n, const double *centroids,
                   int32_t k, uint16_t *indices, ivr_stream_t stream);
 
-/* K6: codebook decode, Codebook.decode (vq.py:128-134).  Sets bad[0] (device)
- * to 1 + the first out-of-range position if any index >= k. */
+/* K6: codebook decode, Codebook.decode (vq.py:128-134).  bad[0] (device,
+ * caller-initialised to -1) receives the largest index >= k, if any; those
+ * positions decode to 0. */
 int ivr_vq_decode(const uint16_t *indices, int64_t n, const double *centroids,
                   int32_t k, double *out, int64_t *bad, ivr_stream_t stream);
+
+/* Stage-1 colour: eval_sh(ShColor, view_dirs(mu, cam_pos))
+ * (gaussians.py:497-508, 521-524).  coeffs (n, (degree+1)^2, 3) float64,
+ * degree 0..3; rgb (n,3) = max(sum_b basis_b * coeffs_b + 0.5, 0). */
+int ivr_sh_eval(int64_t n, int32_t degree, const double *mu, const double *coeffs,
+                const double cam_pos[3], double *rgb, ivr_stream_t stream);
+
+/* eval_sh_backward + view_dirs_backward (gaussians.py:511-518, 527-529):
+ * d_coeffs (n, nb, 3) is overwritten; d_mu (n,3), when non-NULL, is
+ * incremented by the view-direction gradient (the caller passes the
+ * projection gradient there, as _stage1_step sums them, trainer.py:386-388). */
+int ivr_sh_bwd(int64_t n, int32_t degree, const double *mu, const double *coeffs,
+               const double cam_pos[3], const double *d_rgb, double *d_coeffs, double *d_mu,
+               ivr_stream_t stream);
 
 #ifdef __cplusplus
 }

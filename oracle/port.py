@@ -26,7 +26,7 @@ __all__ = [
     "inv_softplus", "normalize", "normalize_backward", "quat_rot", "project",
     "shade", "effective_o_logit", "channel_layout", "rasterize",
     "maps", "light_dir", "rasterize_backward", "project_backward", "shade_backward", "vq_assign",
-    "vq_decode", "kmeans", "ssim", "photometric_loss", "inverse_step", "Adam",
+    "vq_decode", "kmeans", "sh_basis", "sh_colors", "sh_colors_backward", "ssim", "photometric_loss", "inverse_step", "Adam",
     "lib", "max_threads",
 ]
 
@@ -556,6 +556,77 @@ def rasterize_backward(st, d_maps, nthreads=0):
     o = st["opacity"]
     g["d_o_logit"] += d_op * o * (1.0 - o)
     return g
+
+
+# --------------------------------------------------------------- SH colour
+SH_C0 = 0.28209479177387814
+SH_C1 = 0.4886025119029199
+SH_C2 = (1.0925484305920792, -1.0925484305920792, 0.31539156525252005,
+         -1.0925484305920792, 0.5462742152960396)
+SH_C3 = (-0.5900435899266435, 2.890611442640554, -0.4570457994644658,
+         0.3731763325901154, -0.4570457994644658, 1.445305721320277,
+         -0.5900435899266435)
+
+
+def sh_basis(d, degree):
+    """Real SH basis (N,B) and d basis / d dir (N,B,3), gaussians.py:427-494."""
+    x, y, z = d[:, 0], d[:, 1], d[:, 2]
+    n, nb = d.shape[0], (degree + 1) ** 2
+    B, D = np.zeros((n, nb)), np.zeros((n, nb, 3))
+    B[:, 0] = SH_C0
+    if degree >= 1:
+        B[:, 1], B[:, 2], B[:, 3] = -SH_C1 * y, SH_C1 * z, -SH_C1 * x
+        D[:, 1, 1], D[:, 2, 2], D[:, 3, 0] = -SH_C1, SH_C1, -SH_C1
+    if degree >= 2:
+        xx, yy, zz = x * x, y * y, z * z
+        c = SH_C2
+        B[:, 4], B[:, 5] = c[0] * x * y, c[1] * y * z
+        B[:, 6], B[:, 7], B[:, 8] = c[2] * (2 * zz - xx - yy), c[3] * x * z, c[4] * (xx - yy)
+        D[:, 4, 0], D[:, 4, 1], D[:, 5, 1], D[:, 5, 2] = c[0] * y, c[0] * x, c[1] * z, c[1] * y
+        D[:, 6, 0], D[:, 6, 1], D[:, 6, 2] = c[2] * (-2 * x), c[2] * (-2 * y), c[2] * (4 * z)
+        D[:, 7, 0], D[:, 7, 2] = c[3] * z, c[3] * x
+        D[:, 8, 0], D[:, 8, 1] = c[4] * (2 * x), c[4] * (-2 * y)
+    if degree >= 3:
+        xx, yy, zz = x * x, y * y, z * z
+        c = SH_C3
+        B[:, 9] = c[0] * y * (3 * xx - yy)
+        B[:, 10] = c[1] * x * y * z
+        B[:, 11] = c[2] * y * (4 * zz - xx - yy)
+        B[:, 12] = c[3] * z * (2 * zz - 3 * xx - 3 * yy)
+        B[:, 13] = c[4] * x * (4 * zz - xx - yy)
+        B[:, 14] = c[5] * z * (xx - yy)
+        B[:, 15] = c[6] * x * (xx - 3 * yy)
+        D[:, 9, 0], D[:, 9, 1] = c[0] * 6 * x * y, c[0] * (3 * xx - 3 * yy)
+        D[:, 10, 0], D[:, 10, 1], D[:, 10, 2] = c[1] * y * z, c[1] * x * z, c[1] * x * y
+        D[:, 11, 0] = c[2] * (-2 * x * y)
+        D[:, 11, 1] = c[2] * (4 * zz - xx - 3 * yy)
+        D[:, 11, 2] = c[2] * (8 * y * z)
+        D[:, 12, 0], D[:, 12, 1] = c[3] * (-6 * x * z), c[3] * (-6 * y * z)
+        D[:, 12, 2] = c[3] * (6 * zz - 3 * xx - 3 * yy)
+        D[:, 13, 0] = c[4] * (4 * zz - 3 * xx - yy)
+        D[:, 13, 1], D[:, 13, 2] = c[4] * (-2 * x * y), c[4] * (8 * x * z)
+        D[:, 14, 0], D[:, 14, 1], D[:, 14, 2] = c[5] * (2 * x * z), c[5] * (-2 * y * z), c[5] * (xx - yy)
+        D[:, 15, 0], D[:, 15, 1] = c[6] * (3 * xx - 3 * yy), c[6] * (-6 * x * y)
+    return B, D
+
+
+def sh_colors(mu, coeffs, degree, cam_pos):
+    """view_dirs + eval_sh (gaussians.py:497-508, 521-524): (rgb, cache)."""
+    v = mu - np.asarray(cam_pos)[None, :]
+    d = normalize(v, eps=1e-12)
+    B, D = sh_basis(d, degree)
+    raw = np.einsum("nb,nbc->nc", B, coeffs) + 0.5
+    return np.maximum(raw, 0.0), {"B": B, "D": D, "raw": raw, "coeffs": coeffs, "v": v}
+
+
+def sh_colors_backward(cache, d_rgb):
+    """eval_sh_backward + view_dirs_backward (gaussians.py:511-518, 527-529):
+    (d_coeffs, d_mu)."""
+    g = d_rgb * (cache["raw"] > 0)
+    d_coeffs = cache["B"][:, :, None] * g[:, None, :]
+    inner = np.einsum("nbc,nc->nb", cache["coeffs"], g)
+    d_dir = np.einsum("nb,nbk->nk", inner, cache["D"])
+    return d_coeffs, normalize_backward(cache["v"], d_dir)
 
 
 # --------------------------------------------------------------- VQ

@@ -23,6 +23,9 @@ from .scene import (  # noqa: F401
 from .shading import (  # noqa: F401
     LightConfig, Palette, ShadingAttributes, shade_backward, shade_gaussians,
 )
+from .trainer import (  # noqa: F401
+    TrainConfig, ViewDataset, render_model, train_base, train_editable,
+)
 from .vq import Codebook, assign_nearest, dequantize_model, kmeans, quantize_model  # noqa: F401
 
 __version__ = "0.1.0"

@@ -117,6 +117,10 @@ _SIGS = {
                            P, P, P], ctypes.c_int),
     "ivr_vq_assign": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_vq_decode": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P, P], ctypes.c_int),
+    "ivr_sh_eval": ([ctypes.c_int64, ctypes.c_int32, P, P, ctypes.POINTER(ctypes.c_double), P, P],
+                    ctypes.c_int),
+    "ivr_sh_bwd": ([ctypes.c_int64, ctypes.c_int32, P, P, ctypes.POINTER(ctypes.c_double), P, P, P,
+                    P], ctypes.c_int),
 }
 
 _lib = None

@@ -1,11 +1,19 @@
-"""Editable-stage (stage-2) training on the GPU (trainer.py:375-626 semantics).
+"""Two-stage training on the GPU (trainer.py:375-626 semantics).
 
-All parameters, Adam moments and the per-step work stay on the device:
-K1 (shading + projection, K=15 channels: colour, alpha, depth, normal, Δc,
-k_a, k_d, k_s, β) -> K2 -> K3 -> L1+SSIM and the four regularizers in torch
-(losses.py) -> K4a -> K4b (projection + shading backward fused) -> the
-attribute chain rules of _stage2_step (trainer.py:433-442) -> Adam with the
-reference's learning-rate schedules -> periodic densify / prune (torch).
+Stage 1 (base, ``train_base``): SH colour (csrc/sh.cu) -> K1 (K=8 channels:
+colour, alpha, depth, normal) -> K2 -> K3 -> L1+SSIM + normal consistency ->
+K4a -> K4b -> SH / view-direction backward (_stage1_step, trainer.py:375-394).
+
+Stage 2 (editable, ``train_editable``): K1 with fused shading (K=15 channels:
+colour, alpha, depth, normal, Δc, k_a, k_d, k_s, β) -> K2 -> K3 -> L1+SSIM and
+the four regularizers in torch (losses.py) -> K4a -> K4b (projection +
+shading backward fused) -> the attribute chain rules of _stage2_step
+(trainer.py:433-442).
+
+Both stages: all parameters, Adam moments and the per-step work stay on the
+device; Adam with the reference's learning-rate schedules and periodic
+densify / prune (torch) run in the shared loop ``_run_stage``
+(trainer.py:463-526).
 
 One training view per iteration (reference semantics, trainer.py:485).  Runs
 for independent basic transfer functions shard one per GPU with no
@@ -23,7 +31,7 @@ import torch
 
 from . import device as D
 from .errors import DatasetEmpty, DivergedLoss, OutOfRange
-from .gaussians import GaussianGeometry
+from .gaussians import GaussianGeometry, ShColor
 from .losses import (LossWeights, bilateral_smoothness, normal_consistency_loss,
                      photometric_loss_t, pseudo_normal_from_depth)
 from .rasterizer import _channel_layout, _cols
@@ -104,6 +112,7 @@ class DeviceAdam:
 
 
 _LR = {"mu": "lr_mu", "q_raw": "lr_q", "log_s": "lr_log_s", "o_logit": "lr_o", "n_raw": "lr_normal",
+       "sh": "lr_sh",
        "delta_c": "lr_shading", "k_a_raw": "lr_shading", "k_d_raw": "lr_shading",
        "k_s_raw": "lr_shading", "log_beta": "lr_shading"}
 GEOM = ("mu", "q_raw", "log_s", "o_logit", "n_raw")
@@ -116,101 +125,26 @@ def _psnr_t(a, b):
     return PSNR_CAP if mse <= 0.0 else min(10.0 * math.log10(1.0 / mse), PSNR_CAP)
 
 
-class EditableTrainer:
-    """Stage-2 state on the device: params (float64 tensors), palette, light."""
+class _StageTrainer:
+    """Device state of one training stage: row-aligned float64 parameter
+    tensors, Adam moments, the render workspace (the reference's ``params``
+    dict + Adam of _run_stage, trainer.py:463-474)."""
 
-    def __init__(self, params, palette, light, cfg=None, device=None):
+    KEYS = GEOM
+
+    def __init__(self, params, cfg=None, device=None):
         self.dev = device or D.cuda_device()
-        self.p = {k: D.to_dev(params[k], device=self.dev) for k in GEOM + SHADE}
-        self.palette = D.to_dev(np.asarray(palette, np.float64).reshape(1, 3), device=self.dev)
-        self.light = light
+        self.p = {k: D.to_dev(params[k], device=self.dev) for k in self.KEYS}
         self.cfg = cfg or TrainConfig()
         self.adam = DeviceAdam(self.cfg.adam_eps, self.cfg.adam_betas)
         self.ws = D.Workspace(self.dev)
-        self.layout = _channel_layout(("color", "alpha", "depth", "normal"),
-                                      {"delta_c": np.zeros((1, 3)), "k_a": np.zeros(1),
-                                       "k_d": np.zeros(1), "k_s": np.zeros(1), "beta": np.zeros(1)})
-        self.cols, self.attr_cols, self.K = _cols(self.layout)
-        self.colmap = {name: (c, w) for name, c, w in self.attr_cols}
+        self._bad = None
 
     @property
     def n(self):
         return int(self.p["mu"].shape[0])
 
-    def _dg(self):
-        return D.DeviceGaussians({k: self.p[k] for k in GEOM}, {k: self.p[k] for k in SHADE},
-                                 None, self.dev)
-
-    def forward(self, cam, want_state=True, dg=None):
-        dg = dg or self._dg()
-        S = D.shading_struct(dg, self.palette, False, self.light)
-        p = self.p
-        attrs = {"delta_c": p["delta_c"], "k_a": torch.sigmoid(p["k_a_raw"]),
-                 "k_d": torch.sigmoid(p["k_d_raw"]), "k_s": torch.sigmoid(p["k_s_raw"]),
-                 "beta": torch.exp(p["log_beta"]) + 1.0}
-        attrs_dev = [(attrs[name].reshape(self.n, w).contiguous(), c, w)
-                     for name, c, w in self.attr_cols]
-        F = D.rasterize_device(dg, cam, self.K, self.cols, self.ws, shading=S, attrs=attrs_dev,
-                               f64=False, want_state=want_state, exact=False)
-        return F, S, attrs, dg
-
-    def step(self, cam, gt, weights=None):
-        """One _stage2_step (trainer.py:397-444): (loss, grads, densify stat),
-        all device tensors."""
-        weights = weights or self.cfg.weights
-        F, S, attrs, dg = self.forward(cam)
-        H, W = cam.height, cam.width
-        out = F.out.double()
-        c = {name: c for name, c, w in _cols_named(self.layout)}
-        rgba = torch.cat([out[..., c["color"]:c["color"] + 3], out[..., c["alpha"]:c["alpha"] + 1]],
-                         dim=-1)
-        loss, d_rgba = photometric_loss_t(rgba, gt, weights)
-        if not torch.isfinite(loss):
-            raise DivergedLoss(f"loss became {float(loss)}")
-        d_out = torch.zeros((H, W, self.K), dtype=torch.float64, device=self.dev)
-        d_out[..., c["color"]:c["color"] + 3] = d_rgba[..., :3]
-        d_out[..., c["alpha"]] = d_rgba[..., 3]
-        if weights.normal_consistency > 0.0:
-            target, mask = pseudo_normal_from_depth(out[..., c["depth"]], out[..., c["alpha"]], cam)
-            nl, d_n = normal_consistency_loss(out[..., c["normal"]:c["normal"] + 3], target, mask)
-            loss = loss + weights.normal_consistency * nl
-            d_out[..., c["normal"]:c["normal"] + 3] = weights.normal_consistency * d_n
-        if weights.offset_sparsity > 0.0:
-            m = out[..., c["delta_c"]:c["delta_c"] + 3]
-            loss = loss + weights.offset_sparsity * m.abs().mean()
-            d_out[..., c["delta_c"]:c["delta_c"] + 3] = weights.offset_sparsity * torch.sign(m) / m.numel()
-        if weights.bilateral_smoothness > 0.0:
-            for name in ("k_a", "k_d", "k_s", "beta"):
-                bl, d_map = bilateral_smoothness(out[..., c[name]], gt[..., :3])
-                loss = loss + weights.bilateral_smoothness * bl
-                d_out[..., c[name]] = weights.bilateral_smoothness * d_map
-        g = D.blend_backward(F, d_out.float())
-        want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_mean2d", "d_values",
-                "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta")
-        gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, shading=S, geometry=True,
-                                        want=want, light=self.light)
-        n, K = self.n, self.K
-        dv = gr["d_values"].view(n, K)
-        o = torch.sigmoid(self.p["o_logit"])
-        d_o = gr["d_o_logit"]
-        if weights.opacity_l1 > 0.0:
-            loss = loss + weights.opacity_l1 * o.mean()
-            d_o = d_o + weights.opacity_l1 * o * (1.0 - o) / n
-        ka, kd, ks, beta = attrs["k_a"], attrs["k_d"], attrs["k_s"], attrs["beta"]
-        grads = {"mu": gr["d_mu"].view(n, 3), "q_raw": gr["d_q_raw"].view(n, 4),
-                 "log_s": gr["d_log_s"].view(n, 3), "o_logit": d_o,
-                 "n_raw": gr["d_n_raw"].view(n, 3),
-                 "delta_c": gr["d_delta_c"].view(n, 3) + dv[:, c["delta_c"]:c["delta_c"] + 3],
-                 "k_a_raw": gr["d_k_a_raw"] + dv[:, c["k_a"]] * ka * (1.0 - ka),
-                 "k_d_raw": gr["d_k_d_raw"] + dv[:, c["k_d"]] * kd * (1.0 - kd),
-                 "k_s_raw": gr["d_k_s_raw"] + dv[:, c["k_s"]] * ks * (1.0 - ks),
-                 "log_beta": gr["d_log_beta"] + dv[:, c["beta"]] * (beta - 1.0)}
-        stat = torch.linalg.norm(gr["d_mean2d"].view(n, 2), dim=1) + \
-            torch.linalg.norm(grads["n_raw"], dim=1)
-        self._bad = bad
-        return loss, grads, stat
-
-    def apply(self, grads, it, iters, decay_extra=("o_logit",)):
+    def apply(self, grads, it, iters, decay_extra=()):
         """Adam on every group with the reference schedules (trainer.py:491-499)."""
         cfg = self.cfg
         frac = it / max(iters, 1)
@@ -264,11 +198,160 @@ class EditableTrainer:
         return {"cloned": int(c_idx.numel()), "split": int(ns),
                 "pruned": int((~alive).sum()), "count": self.n}
 
+    def _rgba(self, out):
+        c = {name: c for name, c, w in _cols_named(self.layout)}
+        return torch.cat([out[..., c["color"]:c["color"] + 3], out[..., c["alpha"]:c["alpha"] + 1]],
+                         dim=-1)
+
+    def _photometric(self, out, cam, gt, weights):
+        """L1+SSIM on RGBA plus the normal-consistency term; returns
+        (loss, d_out (H,W,K) float64, column map)."""
+        H, W = cam.height, cam.width
+        c = {name: c for name, c, w in _cols_named(self.layout)}
+        loss, d_rgba = photometric_loss_t(self._rgba(out), gt, weights)
+        if not torch.isfinite(loss):
+            raise DivergedLoss(f"loss became {float(loss)}")
+        d_out = torch.zeros((H, W, self.K), dtype=torch.float64, device=self.dev)
+        d_out[..., c["color"]:c["color"] + 3] = d_rgba[..., :3]
+        d_out[..., c["alpha"]] = d_rgba[..., 3]
+        if weights.normal_consistency > 0.0:
+            target, mask = pseudo_normal_from_depth(out[..., c["depth"]], out[..., c["alpha"]], cam)
+            nl, d_n = normal_consistency_loss(out[..., c["normal"]:c["normal"] + 3], target, mask)
+            loss = loss + weights.normal_consistency * nl
+            d_out[..., c["normal"]:c["normal"] + 3] = weights.normal_consistency * d_n
+        return loss, d_out, c
+
+
+class BaseTrainer(_StageTrainer):
+    """Stage-1 state: geometry + SH coefficients (trainer.py:375-394, 532-560)."""
+
+    KEYS = GEOM + ("sh",)
+
+    def __init__(self, params, degree, cfg=None, device=None):
+        super().__init__(params, cfg, device)
+        self.degree = int(degree)
+        self.layout = _channel_layout(("color", "alpha", "depth", "normal"), None)
+        self.cols, self.attr_cols, self.K = _cols(self.layout)
+
+    def _dg(self):
+        return D.DeviceGaussians({k: self.p[k] for k in GEOM}, None, None, self.dev)
+
+    def forward(self, cam, want_state=True):
+        from .sh import sh_eval_device
+        dg = self._dg()
+        rgb = sh_eval_device(self.p["mu"], self.p["sh"], self.degree, cam.position)
+        F = D.rasterize_device(dg, cam, self.K, self.cols, self.ws, colors=rgb, f64=False,
+                               want_state=want_state, exact=False)
+        return F, dg
+
+    def step(self, cam, gt, weights=None):
+        """One _stage1_step (trainer.py:375-394): (loss, grads, densify stat)."""
+        from .sh import sh_backward_device
+        weights = weights or self.cfg.weights
+        F, dg = self.forward(cam)
+        loss, d_out, _ = self._photometric(F.out.double(), cam, gt, weights)
+        g = D.blend_backward(F, d_out.float())
+        want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_mean2d")
+        gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, geometry=True, want=want)
+        n = self.n
+        d_mu = gr["d_mu"].view(n, 3)
+        d_sh = sh_backward_device(self.p["mu"], self.p["sh"], self.degree, cam.position,
+                                  gr["d_colors"].view(n, 3), d_mu=d_mu)
+        grads = {"mu": d_mu, "q_raw": gr["d_q_raw"].view(n, 4), "log_s": gr["d_log_s"].view(n, 3),
+                 "o_logit": gr["d_o_logit"], "n_raw": gr["d_n_raw"].view(n, 3), "sh": d_sh}
+        stat = torch.linalg.norm(gr["d_mean2d"].view(n, 2), dim=1) + \
+            torch.linalg.norm(grads["n_raw"], dim=1)
+        self._bad = bad
+        return loss, grads, stat
+
+    def render_rgba(self, cam):
+        F, _ = self.forward(cam, want_state=False)
+        return self._rgba(F.out.double())
+
+    def model(self, metadata=None):
+        h = {k: v.cpu().numpy() for k, v in self.p.items()}
+        geom = GaussianGeometry(*(h[k] for k in GEOM))
+        return BasicSceneModel(STAGE_BASE, geom, sh=ShColor(h["sh"], self.degree),
+                               metadata=metadata or {})
+
+
+class EditableTrainer(_StageTrainer):
+    """Stage-2 state on the device: params (float64 tensors), palette, light."""
+
+    KEYS = GEOM + SHADE
+
+    def __init__(self, params, palette, light, cfg=None, device=None):
+        super().__init__(params, cfg, device)
+        self.palette = D.to_dev(np.asarray(palette, np.float64).reshape(1, 3), device=self.dev)
+        self.light = light
+        self.layout = _channel_layout(("color", "alpha", "depth", "normal"),
+                                      {"delta_c": np.zeros((1, 3)), "k_a": np.zeros(1),
+                                       "k_d": np.zeros(1), "k_s": np.zeros(1), "beta": np.zeros(1)})
+        self.cols, self.attr_cols, self.K = _cols(self.layout)
+        self.colmap = {name: (c, w) for name, c, w in self.attr_cols}
+
+    def _dg(self):
+        return D.DeviceGaussians({k: self.p[k] for k in GEOM}, {k: self.p[k] for k in SHADE},
+                                 None, self.dev)
+
+    def forward(self, cam, want_state=True, dg=None):
+        dg = dg or self._dg()
+        S = D.shading_struct(dg, self.palette, False, self.light)
+        p = self.p
+        attrs = {"delta_c": p["delta_c"], "k_a": torch.sigmoid(p["k_a_raw"]),
+                 "k_d": torch.sigmoid(p["k_d_raw"]), "k_s": torch.sigmoid(p["k_s_raw"]),
+                 "beta": torch.exp(p["log_beta"]) + 1.0}
+        attrs_dev = [(attrs[name].reshape(self.n, w).contiguous(), c, w)
+                     for name, c, w in self.attr_cols]
+        F = D.rasterize_device(dg, cam, self.K, self.cols, self.ws, shading=S, attrs=attrs_dev,
+                               f64=False, want_state=want_state, exact=False)
+        return F, S, attrs, dg
+
+    def step(self, cam, gt, weights=None):
+        """One _stage2_step (trainer.py:397-444): (loss, grads, densify stat),
+        all device tensors."""
+        weights = weights or self.cfg.weights
+        F, S, attrs, dg = self.forward(cam)
+        out = F.out.double()
+        loss, d_out, c = self._photometric(out, cam, gt, weights)
+        if weights.offset_sparsity > 0.0:
+            m = out[..., c["delta_c"]:c["delta_c"] + 3]
+            loss = loss + weights.offset_sparsity * m.abs().mean()
+            d_out[..., c["delta_c"]:c["delta_c"] + 3] = weights.offset_sparsity * torch.sign(m) / m.numel()
+        if weights.bilateral_smoothness > 0.0:
+            for name in ("k_a", "k_d", "k_s", "beta"):
+                bl, d_map = bilateral_smoothness(out[..., c[name]], gt[..., :3])
+                loss = loss + weights.bilateral_smoothness * bl
+                d_out[..., c[name]] = weights.bilateral_smoothness * d_map
+        g = D.blend_backward(F, d_out.float())
+        want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_mean2d", "d_values",
+                "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta")
+        gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, shading=S, geometry=True,
+                                        want=want, light=self.light)
+        n, K = self.n, self.K
+        dv = gr["d_values"].view(n, K)
+        o = torch.sigmoid(self.p["o_logit"])
+        d_o = gr["d_o_logit"]
+        if weights.opacity_l1 > 0.0:
+            loss = loss + weights.opacity_l1 * o.mean()
+            d_o = d_o + weights.opacity_l1 * o * (1.0 - o) / n
+        ka, kd, ks, beta = attrs["k_a"], attrs["k_d"], attrs["k_s"], attrs["beta"]
+        grads = {"mu": gr["d_mu"].view(n, 3), "q_raw": gr["d_q_raw"].view(n, 4),
+                 "log_s": gr["d_log_s"].view(n, 3), "o_logit": d_o,
+                 "n_raw": gr["d_n_raw"].view(n, 3),
+                 "delta_c": gr["d_delta_c"].view(n, 3) + dv[:, c["delta_c"]:c["delta_c"] + 3],
+                 "k_a_raw": gr["d_k_a_raw"] + dv[:, c["k_a"]] * ka * (1.0 - ka),
+                 "k_d_raw": gr["d_k_d_raw"] + dv[:, c["k_d"]] * kd * (1.0 - kd),
+                 "k_s_raw": gr["d_k_s_raw"] + dv[:, c["k_s"]] * ks * (1.0 - ks),
+                 "log_beta": gr["d_log_beta"] + dv[:, c["beta"]] * (beta - 1.0)}
+        stat = torch.linalg.norm(gr["d_mean2d"].view(n, 2), dim=1) + \
+            torch.linalg.norm(grads["n_raw"], dim=1)
+        self._bad = bad
+        return loss, grads, stat
+
     def render_rgba(self, cam):
         F, _, _, _ = self.forward(cam, want_state=False)
-        c = {name: c for name, c, w in _cols_named(self.layout)}
-        out = F.out.double()
-        return torch.cat([out[..., c["color"]:c["color"] + 3], out[..., c["alpha"]:c["alpha"] + 1]], -1)
+        return self._rgba(F.out.double())
 
     def model(self, palette, metadata=None):
         h = {k: v.cpu().numpy() for k, v in self.p.items()}
@@ -319,31 +402,104 @@ def foreground_mean_color(dataset):
     return np.full(3, 0.5) if den <= 0.0 else num / den
 
 
-def _stage2_init(n):
-    """trainer.py:562-577: neutral start."""
-    return {"delta_c": np.zeros((n, 3)), "k_a_raw": np.zeros(n), "k_d_raw": np.zeros(n),
-            "k_s_raw": np.zeros(n), "log_beta": np.full(n, np.log(9.0))}
+@dataclass
+class ViewDataset:
+    """Multi-view RGBA images with their cameras and light (the fields of
+    dvr.VolumeDataset the trainer reads, dvr.py:459-482)."""
+
+    cameras: list
+    images: list
+    light: LightConfig = field(default_factory=LightConfig)
+    manifest: dict = field(default_factory=dict)
+
+    def __len__(self):
+        return len(self.cameras)
+
+    def bbox(self):
+        """Volume bounds from the manifest, else a cube inside the camera
+        orbit (dvr.py:471-482)."""
+        vol = self.manifest.get("volume")
+        if vol is not None:
+            half = (np.asarray(vol["dims"], dtype=np.float64) - 1.0) \
+                * np.asarray(vol["spacing"], dtype=np.float64) / 2.0
+            return -half, half
+        pos = np.array([c.position for c in self.cameras])
+        r = 0.5 * float(np.min(np.linalg.norm(pos, axis=1)))
+        half = np.full(3, max(r, 1e-6))
+        return -half, half
 
 
-def train_editable(base, dataset, cfg=None):
-    """Stage 2 on the GPU (trainer.py:580-626): returns (editable model, log)."""
-    cfg = cfg or TrainConfig()
-    if base.stage != STAGE_BASE and base.stage != STAGE_EDITABLE:
-        raise OutOfRange("stage-2 training expects a base-stage model")
+def _project_px(points, cam):
+    rel = (points - cam.position[None, :]) @ cam.rotation.T
+    z = rel[:, 2]
+    ok = z > 1e-6
+    zs = np.where(ok, z, 1.0)
+    px = (cam.focal * rel[:, 0] / zs + cam.center_px[0]).astype(np.int64)
+    py = (cam.focal * rel[:, 1] / zs + cam.center_px[1]).astype(np.int64)
+    ok &= (px >= 0) & (px < cam.width) & (py >= 0) & (py < cam.height)
+    return np.nonzero(ok)[0], px, py
+
+
+def _dc_colors_from_view(points, cam, image):
+    """rgb of the training pixel each point projects to, else mid grey
+    (trainer.py:264-279)."""
+    rgb = np.full((points.shape[0], 3), 0.5)
+    idx, px, py = _project_px(points, cam)
+    rgb[idx] = np.asarray(image)[py[idx], px[idx], :3]
+    return rgb
+
+
+def _inside_any_silhouette(points, dataset):
+    """trainer.py:282-294."""
+    keep = np.zeros(points.shape[0], dtype=bool)
+    for cam, img in zip(dataset.cameras, dataset.images):
+        idx, px, py = _project_px(points, cam)
+        keep[idx] |= np.asarray(img)[py[idx], px[idx], 3] > 0.0
+    return keep
+
+
+def initialize_base(dataset, cfg, rng):
+    """Uniform in-box seeding, 3-NN scales, DC colours from the first view
+    (trainer.py:297-328).  Host-side, once per run."""
+    from scipy.spatial import cKDTree
+    lo, hi = dataset.bbox()
+    pts = rng.uniform(lo, hi, (cfg.init_count, 3))
+    if cfg.silhouette_carve:
+        for _ in range(20):
+            keep = _inside_any_silhouette(pts, dataset)
+            if keep.all():
+                break
+            fresh = rng.uniform(lo, hi, (int(np.count_nonzero(~keep)), 3))
+            pts = np.concatenate([pts[keep], fresh])
+        pts = pts[:cfg.init_count]
+    n = pts.shape[0]
+    if n > 1:
+        dists, _ = cKDTree(pts).query(pts, k=min(4, n))
+        nn = np.maximum(dists[:, 1:].mean(axis=1), 1e-6)
+    else:
+        nn = np.full(n, 0.1 * scene_extent(np.stack([lo, hi])))
+    log_s = np.log(nn)[:, None].repeat(3, axis=1)
+    q_raw = np.zeros((n, 4))
+    q_raw[:, 0] = 1.0
+    o_logit = np.full(n, np.log(cfg.init_opacity / (1.0 - cfg.init_opacity)))
+    first = dataset.cameras[0]
+    v = first.position[None, :] - pts
+    n_raw = v / np.maximum(np.linalg.norm(v, axis=-1, keepdims=True), 1e-12)
+    geom = GaussianGeometry(pts, q_raw, log_s, o_logit, n_raw)
+    sh = ShColor.from_dc(_dc_colors_from_view(pts, first, dataset.images[0]), degree=cfg.sh_degree)
+    return geom, sh
+
+
+def _run_stage(tr, dataset, cfg, iters, rng, gen, densify_start=None, decay_extra=()):
+    """The shared optimisation loop (trainer.py:463-526) over a device
+    trainer: one random view per iteration, Adam with the schedules,
+    densify/prune on the trailing interval's mean statistic, holdout PSNR
+    logged every ``log_interval``."""
     if len(dataset) < 2:
         raise DatasetEmpty("training needs at least two views")
-    rng = np.random.default_rng(cfg.seed + 1)
-    gen = torch.Generator(device=D.cuda_device()).manual_seed(cfg.seed + 1)
-    palette = foreground_mean_color(dataset)
-    light = dataset.light
-    g = base.geometry
-    params = {k: getattr(g, k) for k in GEOM}
-    params.update(_stage2_init(len(g)))
-    tr = EditableTrainer(params, palette, light, cfg)
-    iters = cfg.stage2_iters
     extent = scene_extent(np.stack(dataset.bbox()))
     until = cfg.until_iter(iters)
-    start = cfg.densify_interval
+    start = cfg.densify_start_iter if densify_start is None else densify_start
     holdout = len(dataset) - 1
     gts = [D.to_dev(np.asarray(im, np.float64)) for im in dataset.images]
     stats_sum = torch.zeros(tr.n, dtype=torch.float64, device=tr.dev)
@@ -352,9 +508,10 @@ def train_editable(base, dataset, cfg=None):
     for it in range(1, iters + 1):
         view = int(rng.integers(len(dataset)))
         loss, grads, stat = tr.step(dataset.cameras[view], gts[view])
-        D.raise_if_bad(tr._bad, tr.n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw",
-                                       "d_colors")) if it % cfg.log_interval == 0 else None
-        tr.apply(grads, it, iters)
+        if it % cfg.log_interval == 0:
+            D.raise_if_bad(tr._bad, tr.n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw",
+                                           "d_colors"))
+        tr.apply(grads, it, iters, decay_extra)
         stats_sum += stat
         stats_iters += 1
         if it % cfg.densify_interval == 0:
@@ -369,21 +526,70 @@ def train_editable(base, dataset, cfg=None):
             img = tr.render_rgba(dataset.cameras[holdout])
             log.append({"iteration": it, "loss": lv, "count": tr.n,
                         "psnr": _psnr_t(img, gts[holdout])})
+    return log
+
+
+def train_base(dataset, cfg=None, init=None):
+    """Stage 1 on the GPU (trainer.py:532-560): returns (base model, log).
+    ``init`` optionally supplies a (geometry, ShColor) starting point."""
+    cfg = cfg or TrainConfig()
+    if len(dataset) < 2:
+        raise DatasetEmpty("training needs at least two views")
+    rng = np.random.default_rng(cfg.seed)
+    geom, sh = init if init is not None else initialize_base(dataset, cfg, rng)
+    gen = torch.Generator(device=D.cuda_device()).manual_seed(cfg.seed)
+    params = {k: getattr(geom, k) for k in GEOM}
+    params["sh"] = np.asarray(sh.coefficients, np.float64)
+    tr = BaseTrainer(params, sh.degree, cfg)
+    log = _run_stage(tr, dataset, cfg, cfg.stage1_iters, rng, gen)
+    return tr.model({"stage1_iters": cfg.stage1_iters, "seed": cfg.seed}), log
+
+
+def _stage2_init(n):
+    """trainer.py:562-577: neutral start."""
+    return {"delta_c": np.zeros((n, 3)), "k_a_raw": np.zeros(n), "k_d_raw": np.zeros(n),
+            "k_s_raw": np.zeros(n), "log_beta": np.full(n, np.log(9.0))}
+
+
+def train_editable(base, dataset, cfg=None):
+    """Stage 2 on the GPU (trainer.py:580-626): returns (editable model, log)."""
+    cfg = cfg or TrainConfig()
+    if base.stage != STAGE_BASE:
+        raise OutOfRange("stage-2 training expects a base-stage model")
+    rng = np.random.default_rng(cfg.seed + 1)
+    gen = torch.Generator(device=D.cuda_device()).manual_seed(cfg.seed + 1)
+    if len(dataset) < 2:
+        raise DatasetEmpty("training needs at least two views")
+    palette = foreground_mean_color(dataset)
+    light = dataset.light
+    g = base.geometry
+    params = {k: getattr(g, k) for k in GEOM}
+    params.update(_stage2_init(len(g)))
+    tr = EditableTrainer(params, palette, light, cfg)
+    log = _run_stage(tr, dataset, cfg, cfg.stage2_iters, rng, gen,
+                     densify_start=cfg.densify_interval, decay_extra=("o_logit",))
     model = tr.model(palette, {"stage2_iters": cfg.stage2_iters, "seed": cfg.seed,
-                               "light": light.to_dict()})
+                               "light": light.to_dict(),
+                               "transfer_function": getattr(dataset, "manifest", {}).get(
+                                   "transfer_function")})
     return model, log
 
 
 def render_model(model, cam, light=None, dtype=np.float32):
-    """RGBA image of one editable basic model (trainer.py:633-647)."""
+    """RGBA image of one basic model of either stage (trainer.py:633-647)."""
     from .vq import dequantize_model
     if model.is_quantized:
         model = dequantize_model(model)
-    if model.stage != STAGE_EDITABLE:
-        raise OutOfRange("the GPU path renders editable-stage models")
-    from .scene import ComposedScene
-    sc = ComposedScene.compose([model], light or LightConfig())
-    out = DeviceScene(sc).render(cam, dtype=dtype)
+    if model.stage == STAGE_BASE:
+        from .rasterizer import rasterize_forward
+        from .sh import sh_colors
+        rgb = sh_colors(model.geometry, model.sh, cam)
+        out, _ = rasterize_forward(model.geometry, rgb, cam, channels=("color", "alpha"),
+                                   dtype=dtype)
+    else:
+        from .scene import ComposedScene
+        sc = ComposedScene.compose([model], light or LightConfig())
+        out = DeviceScene(sc).render(cam, dtype=dtype)
     return np.concatenate([np.asarray(out.color, np.float64), np.asarray(out.alpha, np.float64)[..., None]],
                           axis=-1)
 

@@ -232,6 +232,50 @@ def stage2_case():
     print("stage2", loss)
 
 
+def sh_case():
+    """view_dirs + eval_sh / eval_sh_backward + view_dirs_backward
+    (gaussians.py:497-529) for degrees 0..3, including clamped channels."""
+    from voxsplat.gaussians import ShColor, eval_sh, eval_sh_backward, view_dirs, view_dirs_backward
+    rng = np.random.default_rng(12)
+    d = {}
+    n = 400
+    mu = rng.uniform(-1, 1, (n, 3))
+    pos = np.array([0.3, -2.2, 1.1])
+    d["mu"], d["pos"] = mu, pos
+    for deg in range(4):
+        coeffs = rng.normal(0, 0.6, (n, (deg + 1) ** 2, 3))
+        dirs = view_dirs(mu, pos)
+        rgb, cache = eval_sh(ShColor(coeffs, deg), dirs)
+        d_rgb = rng.normal(size=(n, 3))
+        d_c, d_dir = eval_sh_backward(cache, d_rgb)
+        d_mu = view_dirs_backward(mu, pos, d_dir)
+        d.update({f"coeffs{deg}": coeffs, f"rgb{deg}": rgb, f"drgb{deg}": d_rgb,
+                  f"dcoeffs{deg}": d_c, f"dmu{deg}": d_mu})
+    np.savez_compressed(os.path.join(HERE, "sh.npz"), **d)
+    print("sh")
+
+
+def stage1_case():
+    """One trainer._stage1_step (trainer.py:375-394): SH colour, colour/alpha/
+    depth/normal channels, L1+SSIM + normal consistency."""
+    from voxsplat import trainer as ref_trainer
+    from voxsplat.gaussians import ShColor
+    from voxsplat.losses import LossWeights
+    a = editable_arrays(43, 300, spread=0.5)
+    geom = GaussianGeometry(*(a[k] for k in GEOM_KEYS))
+    rng = np.random.default_rng(9)
+    sh = ShColor(rng.normal(0, 0.5, (300, 9, 3)), 2)
+    cam = orbit_camera(np.zeros(3), 2.5, 0.35, -0.6, 0.9, 40, 32)
+    gt = rng.uniform(0, 1, (32, 40, 4))
+    loss, grads, stat = ref_trainer._stage1_step(geom, sh, cam, gt, LossWeights())
+    d = {k: a[k] for k in GEOM_KEYS}
+    d.update(cam_dict(cam), sh=sh.coefficients, gt=gt, loss=np.float64(loss), stat=stat)
+    for k, v in grads.items():
+        d["g_" + k] = v
+    np.savez_compressed(os.path.join(HERE, "stage1.npz"), **d)
+    print("stage1", loss)
+
+
 if __name__ == "__main__":
     import sys as _sys
     if len(_sys.argv) > 1:  # regenerate selected cases only
@@ -253,3 +297,5 @@ if __name__ == "__main__":
     loss_case()
     inverse_case()
     stage2_case()
+    sh_case()
+    stage1_case()

@@ -67,7 +67,9 @@ def test_short_training_run_decreases_loss():
         def bbox(self):
             return -np.full(3, 0.6), np.full(3, 0.6)
 
-    base = editable_model(3, 2000, spread=0.5, density=2000)
+    from paper_2504_17954_b200 import BasicSceneModel, ShColor
+    ed = editable_model(3, 2000, spread=0.5, density=2000)
+    base = BasicSceneModel("base", ed.geometry, sh=ShColor.from_dc(np.full((2000, 3), 0.5)))
     cfg = TrainConfig(stage2_iters=120, log_interval=20, densify_interval=30)
     model, log = train_editable(base, DS(), cfg)
     assert len(log) == 6 and all(np.isfinite(r["loss"]) for r in log)

@@ -113,6 +113,16 @@ def test_shade_forward_backward(tag):
         np.testing.assert_array_equal(np.asarray(v), d[f"{tag}_{k}"], err_msg=k)
 
 
+@pytest.mark.parametrize("deg", [0, 1, 2, 3])
+def test_sh_colour_forward_backward(deg):
+    d = golden("sh")
+    rgb, cache = O.sh_colors(d["mu"], d[f"coeffs{deg}"], deg, d["pos"])
+    assert np.array_equal(rgb, d[f"rgb{deg}"])
+    d_c, d_mu = O.sh_colors_backward(cache, d[f"drgb{deg}"])
+    assert np.array_equal(d_c, d[f"dcoeffs{deg}"])
+    assert np.array_equal(d_mu, d[f"dmu{deg}"])
+
+
 def test_vq_assign_and_kmeans():
     d = golden("vq")
     idx = O.vq_assign(d["values"], d["centroids"])
