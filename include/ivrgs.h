@@ -280,6 +280,19 @@ int ivr_sh_bwd(int64_t n, int32_t degree, const double *mu, const double *coeffs
                const double cam_pos[3], const double *d_rgb, double *d_coeffs, double *d_mu,
                ivr_stream_t stream);
 
+/* IVRG files (scene.py:242-436) resident in HBM.
+ * ivr_crc32: zlib CRC-32 of n device bytes into *out (device uint32); the
+ * check load_model does with zlib.crc32 on the host (scene.py:359-361). */
+int ivr_crc32(const uint8_t *data, int64_t n, uint32_t *out, ivr_stream_t stream);
+
+/* Widen `count` packed little-endian elements at any byte alignment:
+ * kind 0 f32 -> double (_Reader.f32, scene.py:343-347), kind 1 u8 -> u16,
+ * kind 2 u16 -> u16 (QATT codebook indices, scene.py:388-394). */
+int ivr_unpack(const uint8_t *src, int64_t count, int32_t kind, void *dst, ivr_stream_t stream);
+
+/* double -> little-endian f32 bytes (_f32_bytes, scene.py:243-244). */
+int ivr_pack_f32(const double *src, int64_t count, uint8_t *dst, ivr_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

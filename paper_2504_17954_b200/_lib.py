@@ -121,6 +121,9 @@ _SIGS = {
                     ctypes.c_int),
     "ivr_sh_bwd": ([ctypes.c_int64, ctypes.c_int32, P, P, ctypes.POINTER(ctypes.c_double), P, P, P,
                     P], ctypes.c_int),
+    "ivr_crc32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
+    "ivr_unpack": ([P, ctypes.c_int64, ctypes.c_int32, P, P], ctypes.c_int),
+    "ivr_pack_f32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
 }
 
 _lib = None

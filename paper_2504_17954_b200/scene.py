@@ -190,17 +190,19 @@ class DeviceScene:
     Edits, light and camera are read at render time, so edits applied to the
     host ComposedScene are picked up by the next frame without re-upload."""
 
-    def __init__(self, scene, device=None):
+    def __init__(self, scene, device=None, dg=None):
         if isinstance(scene, BasicSceneModel):
             scene = ComposedScene.compose([scene])
         self.scene = scene
         models = scene.models
-        geom = {k: np.concatenate([getattr(m.geometry, k) for m in models], axis=0)
-                for k in D.DeviceGaussians.GEOM}
-        shad = {k: np.concatenate([getattr(m.shading, k) for m in models], axis=0)
-                for k in D.DeviceGaussians.SHADE}
-        ids = np.concatenate([np.full(len(m), i, dtype=np.int32) for i, m in enumerate(models)])
-        self.dg = D.DeviceGaussians(geom, shad, ids, device)
+        if dg is None:
+            geom = {k: np.concatenate([getattr(m.geometry, k) for m in models], axis=0)
+                    for k in D.DeviceGaussians.GEOM}
+            shad = {k: np.concatenate([getattr(m.shading, k) for m in models], axis=0)
+                    for k in D.DeviceGaussians.SHADE}
+            ids = np.concatenate([np.full(len(m), i, dtype=np.int32) for i, m in enumerate(models)])
+            dg = D.DeviceGaussians(geom, shad, ids, device)
+        self.dg = dg  # or arrays already resident (ivrg.load_device)
         self.n = self.dg.n
         self.n_scenes = len(models)
         self.ws = D.Workspace(self.dg.device)

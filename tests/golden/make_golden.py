@@ -276,6 +276,52 @@ def stage1_case():
     print("stage1", loss)
 
 
+def ivrg_case():
+    """IVRG files written by the reference save_model (scene.py:286-329) plus
+    the arrays its load_model returns (scene.py:349-436)."""
+    from voxsplat.gaussians import ShColor
+    from voxsplat.scene import STAGE_BASE, load_model, save_model
+    from voxsplat.vq import quantize_model
+    out_dir = os.path.join(HERE, "ivrg")
+    os.makedirs(out_dir, exist_ok=True)
+    ed = model_from(editable_arrays(50, 300))
+    ed.metadata = {"name": "editable", "seed": 50}
+    a = editable_arrays(51, 200)
+    sh = ShColor(np.random.default_rng(51).normal(0, 0.5, (200, 9, 3)), 2)
+    base = BasicSceneModel(STAGE_BASE, GaussianGeometry(*(a[k] for k in GEOM_KEYS)), sh=sh,
+                           metadata={"stage1_iters": 7})
+    quant = quantize_model(model_from(editable_arrays(52, 400)), k=16, seed=3)
+    quant_wide = quantize_model(model_from(editable_arrays(53, 600)), k=300, seed=4)
+    comp = ComposedScene.compose([model_from(editable_arrays(54 + i, 150 + 50 * i)) for i in range(3)],
+                                 LightConfig("orbital", 0.4, -1.1, np.array([1.1, 0.9, 1.0, 1.2])))
+    comp.edits[1] = EditState(np.array([0.1, 0.7, 0.3]), 0.5)
+    comp.edits[2] = EditState(None, 1.5)
+    comp.transform = {"c_p": [[0.2, 0.6, 0.9]], "note": "fit"}
+    for name, obj in (("editable", ed), ("base", base), ("quantized", quant),
+                      ("quantized_wide", quant_wide), ("composed", comp)):
+        path = os.path.join(out_dir, name + ".ivrg")
+        save_model(obj, path)
+        back = load_model(path)
+        models = back.models if isinstance(back, ComposedScene) else [back]
+        d = {}
+        for i, m in enumerate(models):
+            for k in GEOM_KEYS:
+                d[f"m{i}_{k}"] = getattr(m.geometry, k)
+            if m.sh is not None:
+                d[f"m{i}_sh"] = m.sh.coefficients
+            if m.shading is not None:
+                for k in SHADE_KEYS:
+                    d[f"m{i}_{k}"] = getattr(m.shading, k)
+            if m.palette is not None:
+                d[f"m{i}_palette"] = m.palette.c_p
+            if m.quantized is not None:
+                for k, (cb, idx) in m.quantized.items():
+                    d[f"m{i}_cb_{k}"] = cb.centroids
+                    d[f"m{i}_idx_{k}"] = idx
+        np.savez_compressed(os.path.join(out_dir, name + ".npz"), **d)
+    print("ivrg")
+
+
 if __name__ == "__main__":
     import sys as _sys
     if len(_sys.argv) > 1:  # regenerate selected cases only
@@ -299,3 +345,4 @@ if __name__ == "__main__":
     stage2_case()
     sh_case()
     stage1_case()
+    ivrg_case()
