@@ -2,14 +2,14 @@
 //
 // Replaces _kernels.composite_forward (_kernels.py:31-72).  One CTA per 16x16
 // tile (tiles launched heaviest-first when a tile order is given), one thread
-// per pixel.  The tile's depth-sorted pair list is streamed through shared
-// memory in batches of 256 pairs.  Pairs that provably stay below alpha 1/255
-// over the whole tile are skipped without loading their records (bit 31 set
-// by ivr_bin_sort_cull, or -- without that flag -- a float64 minimum of the
-// exponent over the tile rectangle evaluated while staging).  Survivors are
-// compacted in list order (warp ballots), so each pixel walks exactly the
-// reference list minus provably skipped pairs; the CTA retires as soon as
-// every pixel has passed T < 1e-4.
+// per pixel, and each warp an independent 16x2 strip: the warp streams the
+// tile's depth-sorted pair list in chunks of 32, culls every pair against its
+// own strip (a rigorous float32 lower bound of the exponent over the strip vs
+// the record's skip bound; bit 31 of a pair id = already culled for the tile
+// by ivr_bin_sort_cull), stashes survivors in per-warp shared slots and walks
+// them in list order.  Each pixel therefore visits exactly the reference list
+// minus provably skipped pairs, and a warp retires as soon as its 32 pixels
+// have passed T < 1e-4 -- there is no CTA-wide barrier.
 //
 // Decisions (sigma < 0, alpha < 1/255, T < 1e-4) must match the reference's
 // float64 arithmetic exactly: a flipped alpha-skip moves a pixel by
@@ -22,7 +22,7 @@
 //    alpha-skip threshold take float32 alpha; only pairs inside the band take
 //    the exact float64 path.  T is tracked in float32 with a running relative
 //    error bound; a pixel whose T lands inside its band around 1e-4 is
-//    flagged, and the CTA re-walks its list once in EXACT mode for the
+//    flagged, and its warp re-walks the list once in EXACT mode for the
 //    flagged pixels only.  Decisions therefore match the reference; values
 //    carry float32 rounding (~1e-6 against the 1e-4 tolerance).
 #include <math.h>
@@ -125,103 +125,78 @@ struct PixelState {
     }
 };
 
-struct Smem {
-    float4 *r0, *r1;
-    int *j, *sp;
-    float *v;
-    double *r64;  // F64: 6 per pair (mx, my, a, b, c, o)
-    double *v64;  // F64: KMAX per pair
-    int *wsum;
-    uint32_t *wmask;  // [warp][kBlendThreads/32] strip-filter bitmasks
+// Per-warp staging slots: one 32-pair chunk of the tile list at a time.
+template <int KMAX, bool F64, int MODE>
+struct WarpSlots {
+    float4 r0[32], r1[32];
+    float v[32 * KMAX];
+    double r64[F64 ? 32 * 6 : 1];                           // mx, my, a, b, c, o
+    double v64[(F64 && MODE == kModeExact) ? 32 * KMAX : 1];
 };
 
-// One pass over the tile's pair list for every pixel with !st.done.
-template <int KMAX, bool F64, int MODE>
-__device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int s0, int s1,
-                                          int px, int py, int px0, int px1, int py0, int py1,
-                                          PixelState<KMAX, F64> &st) {
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+// One warp = one 16x2 strip of the tile.  The warp streams the tile's pair
+// list in chunks of 32 (one pair per lane): load id + record, cull against the
+// strip rectangle (rigorous float32 bound), stash survivors in its own shared
+// slots, then every lane walks the survivors in list order for its pixel.
+// No CTA barrier anywhere: each warp retires as soon as its 32 pixels have
+// passed T < 1e-4, and the next chunk's ids and records are prefetched into
+// registers while the current chunk is walked.
+template <int KMAX, bool F64, int MODE, int WMODE>
+__device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F64, WMODE> &W,
+                                          int s0, int s1, int px, int py, int sx0, int sx1,
+                                          int sy0, int sy1, PixelState<KMAX, F64> &st) {
+    const int lane = threadIdx.x & 31;
     const int K = A.K;
     const float fpx = (float)px, fpy = (float)py;
     const double dpx = (double)px, dpy = (double)py;
-    for (int base = s0; base < s1; base += kBlendThreads) {
-        if (__syncthreads_count(!st.done) == 0) break;
-        // ---- stage one batch (each thread one pair), compact survivors in order
-        const int j = base + tid;
-        bool keep = false;
-        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-        int sp = 0;
+    int sp = 0;
+    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+    auto fetch = [&](int base) {
+        const int j = base + lane;
         if (j < s1) {
-            sp = A.pair_splat[j];
-            if (A.preculled) {
-                keep = sp >= 0;  // bit 31 = culled for this tile by ivr_bin_sort_cull
-                if (keep) {
-                    r0 = __ldg(A.rec + 2 * sp);
-                    r1 = __ldg(A.rec + 2 * sp + 1);
-                }
-            } else {
+            sp = __ldg(A.pair_splat + j);  // bit 31: culled for this tile by ivr_bin_sort_cull
+            if (sp >= 0) {
                 r0 = __ldg(A.rec + 2 * sp);
                 r1 = __ldg(A.rec + 2 * sp + 1);
-                keep = !tile_cull32(r0, r1, px0, px1, py0, py1);
             }
         }
-        const uint32_t m = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) S.wsum[warp] = __popc(m);
-        __syncthreads();
-        int off = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < kBlendThreads / 32; ++w) {
-            const int c = S.wsum[w];
-            off += (w < warp) ? c : 0;
-            total += c;
+    };
+    if (s0 < s1) fetch(s0);
+    for (int base = s0; base < s1; base += 32) {
+        if (__all_sync(0xffffffffu, st.done)) break;
+        const int j = base + lane;
+        bool keep = false;
+        if (j < s1) {
+            keep = sp >= 0 && !tile_cull32(r0, r1, sx0, sx1, sy0, sy1);
         }
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (keep) {
-            const int q = off + __popc(m & lanemask_lt());
-            S.r0[q] = r0;
-            S.r1[q] = r1;
-            S.j[q] = j;
-            S.sp[q] = sp;
+            W.r0[lane] = r0;
+            W.r1[lane] = r1;
             const float *v = A.values + (int64_t)K * sp;
 #pragma unroll
             for (int c = 0; c < KMAX; ++c)
-                if (c < K) S.v[q * KMAX + c] = __ldg(v + c);
+                if (c < K) W.v[lane * KMAX + c] = __ldg(v + c);
             if (F64) {
                 const double *r = A.rec64 + 8 * (int64_t)sp;
 #pragma unroll
-                for (int c = 0; c < 6; ++c) S.r64[q * 6 + c] = __ldg(r + c);
-                if (MODE == kModeExact) {
+                for (int c = 0; c < 6; ++c) W.r64[lane * 6 + c] = __ldg(r + c);
+                if (WMODE == kModeExact) {
                     const double *v64 = A.values64 + (int64_t)K * sp;
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c)
-                        if (c < K) S.v64[q * KMAX + c] = __ldg(v64 + c);
+                        if (c < K) W.v64[lane * KMAX + c] = __ldg(v64 + c);
                 }
             }
         }
-        __syncthreads();
-        // ---- per-warp strip filter: keep survivors that can reach alpha 1/255
-        // in this warp's 16x2 pixel strip (same rigorous test as the tile cull)
-        if (!__any_sync(0xffffffffu, !st.done)) continue;
-        const int nwords = (total + 31) >> 5;
-        {
-            const int wy0 = min(py0 + 2 * warp, A.H - 1), wy1 = min(py0 + 2 * warp + 1, A.H - 1);
-            for (int w = 0; w < nwords; ++w) {
-                const int q = (w << 5) + lane;
-                bool t = false;
-                if (q < total) t = !tile_cull32(S.r0[q], S.r1[q], px0, px1, wy0, wy1);
-                const uint32_t b = __ballot_sync(0xffffffffu, t);
-                if (lane == 0) S.wmask[warp * (kBlendThreads / 32) + w] = b;
-            }
-            __syncwarp();
-        }
-        if (st.done) continue;
-        // ---- per-pixel walk over the strip's survivors, in list order
-        for (int w = 0; w < nwords; ++w) {
-          uint32_t mbits = S.wmask[warp * (kBlendThreads / 32) + w];
-          while (mbits) {
-            const int q = (w << 5) + __ffs(mbits) - 1;
+        __syncwarp();
+        if (base + 32 < s1) fetch(base + 32);  // prefetch the next chunk during the walk
+        uint32_t mbits = st.done ? 0u : m;
+        while (mbits) {
+            const int q = __ffs(mbits) - 1;
             mbits &= mbits - 1;
-            const float4 a0 = S.r0[q];
-            const float4 a1 = S.r1[q];
+            const float4 a0 = W.r0[q];
+            const float4 a1 = W.r1[q];
             const float dx = fpx - a0.x, dy = fpy - a0.y;
             const float bdy = a1.y * dy, hcdy = a1.z * dy;
             const float sig = fmaf(fmaf(a1.x, dx, bdy), dx, hcdy * dy);
@@ -229,7 +204,7 @@ __device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int
             if (MODE == kModeExact) {
                 double al;
                 if (F64) {
-                    const double *r = S.r64 + q * 6;
+                    const double *r = W.r64 + q * 6;
                     al = exact_alpha(dpx, dpy, r[0], r[1], r[2], r[3], r[4], r[5]);
                 } else {
                     al = exact_alpha(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
@@ -240,27 +215,27 @@ __device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int
                 if (F64) {
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c)
-                        if (c < K) st.acc64[c] = dadd(st.acc64[c], dmul(w, S.v64[q * KMAX + c]));
+                        if (c < K) st.acc64[c] = dadd(st.acc64[c], dmul(w, W.v64[q * KMAX + c]));
                 } else {
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c)
                         if (c < K)
                             st.acc[c] =
-                                (float)dadd((double)st.acc[c], dmul(w, (double)S.v[q * KMAX + c]));
+                                (float)dadd((double)st.acc[c], dmul(w, (double)W.v[q * KMAX + c]));
                 }
                 st.T = dmul(st.T, dsub(1.0, al));
                 ++st.nc;
-                st.last = S.j[q] + 1;
+                st.last = base + q + 1;
                 if (st.T < kTStop) {
                     st.done = true;
-                    goto batch_done;
+                    break;
                 }
             } else {
                 // candidate: in dtype=float64 mode recompute dx, dy from the float64 mean
                 float cdx = dx, cdy = dy, cbdy = bdy, chcdy = hcdy, csig = sig;
                 if (F64) {
-                    cdx = (float)dsub(dpx, S.r64[q * 6]);
-                    cdy = (float)dsub(dpy, S.r64[q * 6 + 1]);
+                    cdx = (float)dsub(dpx, W.r64[q * 6]);
+                    cdy = (float)dsub(dpy, W.r64[q * 6 + 1]);
                     cbdy = a1.y * cdy;
                     chcdy = a1.z * cdy;
                     csig = fmaf(fmaf(a1.x, cdx, cbdy), cdx, chcdy * cdy);
@@ -286,7 +261,7 @@ __device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int
                 } else {
                     double ad;
                     if (F64) {
-                        const double *r = S.r64 + q * 6;
+                        const double *r = W.r64 + q * 6;
                         ad = exact_alpha(dpx, dpy, r[0], r[1], r[2], r[3], r[4], r[5]);
                     } else {
                         ad = exact_alpha(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
@@ -299,21 +274,21 @@ __device__ __forceinline__ void tile_walk(const BlendArgs &A, const Smem &S, int
                 const float w = st.Tf * al;
 #pragma unroll
                 for (int c = 0; c < KMAX; ++c)
-                    if (c < K) st.acc[c] = fmaf(w, S.v[q * KMAX + c], st.acc[c]);
+                    if (c < K) st.acc[c] = fmaf(w, W.v[q * KMAX + c], st.acc[c]);
                 const float om = 1.0f - al;
                 st.Tf = st.Tf * om;
-                st.errT += dal * __frcp_rn(om) * 1.01f + 1.3e-7f;
+                // 1/om by MUFU.RCP (rel. error < 2^-22, covered by the 1.01 factor)
+                st.errT += dal * __fdividef(1.0f, om) * 1.01f + 1.3e-7f;
                 ++st.nc;
-                st.last = S.j[q] + 1;
+                st.last = base + q + 1;
                 if (st.Tf < 1e-4f * (1.0f + st.errT + 1e-6f)) {
                     st.done = true;  // certain stop, or ambiguous -> EXACT re-walk
                     st.replay = !(st.Tf < 1e-4f * (1.0f - st.errT - 1e-6f));
-                    goto batch_done;
+                    break;
                 }
             }
-          }
         }
-    batch_done:;
+        __syncwarp();  // slots are rewritten by the next chunk
     }
 }
 
@@ -321,39 +296,31 @@ template <int KMAX, bool F64, int MODE>
 __global__ void __launch_bounds__(kBlendThreads, 3)
 blend_fwd_kernel(BlendArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
-    __shared__ int s_wsum[kBlendThreads / 32];
-    __shared__ uint32_t s_wmask[(kBlendThreads / 32) * (kBlendThreads / 32)];
-    Smem S;
-    S.r0 = reinterpret_cast<float4 *>(smem);
-    S.r1 = S.r0 + kBlendThreads;
-    S.j = reinterpret_cast<int *>(S.r1 + kBlendThreads);
-    S.sp = S.j + kBlendThreads;
-    S.v = reinterpret_cast<float *>(S.sp + kBlendThreads);
-    S.r64 = reinterpret_cast<double *>(S.v + kBlendThreads * KMAX);
-    S.v64 = S.r64 + (F64 ? 6 * kBlendThreads : 0);
-    S.wsum = s_wsum;
-    S.wmask = s_wmask;
+    using Slots = WarpSlots<KMAX, F64, kModeExact>;  // EXACT layout also serves FAST
+    Slots &W = reinterpret_cast<Slots *>(smem)[threadIdx.x >> 5];
 
     const int tile = A.tile_order ? A.tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % A.ntx, ty = tile / A.ntx;
-    const int tid = threadIdx.x;
-    const int px = tx * kTile + (tid & 15), py = ty * kTile + (tid >> 4);
+    const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
+    // warp w owns rows 2w, 2w+1 of the tile; lane -> (x = lane & 15, y = lane >> 4)
+    const int px = tx * kTile + (lane & 15), py = ty * kTile + 2 * warp + (lane >> 4);
     const bool inside = px < A.W && py < A.H;
     const int s0 = A.ranges[tile], s1 = A.ranges[tile + 1];
-    const int px0 = tx * kTile, py0 = ty * kTile;
-    const int px1 = min(px0 + kTile - 1, A.W - 1), py1 = min(py0 + kTile - 1, A.H - 1);
+    const int sx0 = tx * kTile, sx1 = min(sx0 + kTile - 1, A.W - 1);
+    const int sy0 = min(ty * kTile + 2 * warp, A.H - 1), sy1 = min(sy0 + 1, A.H - 1);
 
     PixelState<KMAX, F64> st;
     st.reset(s0, !inside);
-    tile_walk<KMAX, F64, MODE>(A, S, s0, s1, px, py, px0, px1, py0, py1, st);
+    warp_walk<KMAX, F64, MODE, kModeExact>(A, W, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
     bool exact_out = MODE == kModeExact;
     if (MODE == kModeFast) {
-        // pixels whose T landed in the ambiguity band: one EXACT re-walk
+        // pixels whose T landed in the ambiguity band: one EXACT re-walk (per warp)
         const bool need = st.replay;
-        if (__syncthreads_or(need)) {
+        if (__any_sync(0xffffffffu, need)) {
             PixelState<KMAX, F64> ex;
             ex.reset(s0, !need);
-            tile_walk<KMAX, F64, kModeExact>(A, S, s0, s1, px, py, px0, px1, py0, py1, ex);
+            warp_walk<KMAX, F64, kModeExact, kModeExact>(A, W, s0, s1, px, py, sx0, sx1, sy0, sy1,
+                                                         ex);
             if (need) {
                 st = ex;
                 exact_out = true;
@@ -382,8 +349,7 @@ blend_fwd_kernel(BlendArgs A) {
 
 template <int KMAX, bool F64>
 size_t blend_smem_bytes() {
-    return (size_t)kBlendThreads * (16 + 16 + 4 + 4 + 4 * KMAX) +
-           (F64 ? (size_t)kBlendThreads * 8 * (6 + KMAX) : 0);
+    return (kBlendThreads / 32) * sizeof(WarpSlots<KMAX, F64, kModeExact>);
 }
 
 template <int KMAX, bool F64, int MODE>
