@@ -32,6 +32,9 @@
 namespace ivr {
 
 constexpr int kBlendThreads = 256;
+// Warp footprint width: 8 -> 8x4 pixel blocks (less perimeter per pixel than
+// 16x2, so more lanes fall inside a footprint that touches the warp).
+constexpr int kWarpW = 8;
 constexpr int kModeExact = 0;
 constexpr int kModeFast = 1;
 // |sigma32 - sigma_ref| <= kSigmaErr * (|a/2 dx^2| + |b dx dy| + |c/2 dy^2|):
@@ -83,6 +86,20 @@ __device__ __forceinline__ double exact_alpha(double dpx, double dpy, double mx,
     return al;
 }
 
+// MUFU.EX2 / MUFU.RCP without the denormal-range fix-ups of exp2f/__fdividef
+// (arguments here are far from the denormal range; error bounds below assume
+// the approx instructions' ~2 ulp)
+__device__ __forceinline__ float ex2_approx(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
 struct BlendArgs {
     const int32_t *ranges;
     const int32_t *pair_splat;
@@ -104,7 +121,7 @@ template <int KMAX, bool F64>
 struct PixelState {
     double T;     // EXACT: float64 transmittance (reference arithmetic)
     float Tf;     // FAST: float32 transmittance
-    float errT;   // FAST: bound on |Tf / T_ref - 1|
+    float errT;   // FAST: 1e-4 x bound on |Tf / T_ref - 1|
     float acc[KMAX];
     double acc64[F64 ? KMAX : 1];
     int nc, last;
@@ -151,6 +168,8 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
     const double dpx = (double)px, dpy = (double)py;
     int sp = 0;
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+    constexpr int KPF = KMAX <= 4 ? KMAX : 0;  // values prefetched with the record (K <= 4)
+    float pv[KPF > 0 ? KPF : 1];
     auto fetch = [&](int base) {
         const int j = base + lane;
         if (j < s1) {
@@ -158,6 +177,8 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
             if (sp >= 0) {
                 r0 = __ldg(A.rec + 2 * sp);
                 r1 = __ldg(A.rec + 2 * sp + 1);
+#pragma unroll
+                for (int c = 0; c < KPF; ++c) pv[c] = c < K ? __ldg(A.values + (int64_t)K * sp + c) : 0.0f;
             }
         }
     };
@@ -172,11 +193,19 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
         if (keep) {
             W.r0[lane] = r0;
-            W.r1[lane] = r1;
-            const float *v = A.values + (int64_t)K * sp;
+            // FAST mode reads thr_lo = thr - (thr rounding + margins) in place of thr
+            W.r1[lane] = MODE == kModeFast
+                             ? make_float4(r1.x, r1.y, r1.z, r1.w - (2.4e-7f * fabsf(r1.w) + 1e-7f))
+                             : r1;
+            if (KPF > 0) {
 #pragma unroll
-            for (int c = 0; c < KMAX; ++c)
-                if (c < K) W.v[lane * KMAX + c] = __ldg(v + c);
+                for (int c = 0; c < KPF; ++c) W.v[lane * KMAX + c] = pv[c];
+            } else {
+                const float *v = A.values + (int64_t)K * sp;
+#pragma unroll
+                for (int c = 0; c < KMAX; ++c)  // zero-padded to KMAX: no channel predicates below
+                    W.v[lane * KMAX + c] = c < K ? __ldg(v + c) : 0.0f;
+            }
             if (F64) {
                 const double *r = A.rec64 + 8 * (int64_t)sp;
 #pragma unroll
@@ -184,8 +213,7 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                 if (WMODE == kModeExact) {
                     const double *v64 = A.values64 + (int64_t)K * sp;
 #pragma unroll
-                    for (int c = 0; c < KMAX; ++c)
-                        if (c < K) W.v64[lane * KMAX + c] = __ldg(v64 + c);
+                    for (int c = 0; c < KMAX; ++c) W.v64[lane * KMAX + c] = c < K ? __ldg(v64 + c) : 0.0;
                 }
             }
         }
@@ -215,13 +243,11 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                 if (F64) {
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c)
-                        if (c < K) st.acc64[c] = dadd(st.acc64[c], dmul(w, W.v64[q * KMAX + c]));
+                        st.acc64[c] = dadd(st.acc64[c], dmul(w, W.v64[q * KMAX + c]));
                 } else {
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c)
-                        if (c < K)
-                            st.acc[c] =
-                                (float)dadd((double)st.acc[c], dmul(w, (double)W.v[q * KMAX + c]));
+                        st.acc[c] = (float)dadd((double)st.acc[c], dmul(w, (double)W.v[q * KMAX + c]));
                 }
                 st.T = dmul(st.T, dsub(1.0, al));
                 ++st.nc;
@@ -242,11 +268,9 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                 }
                 const float terms = fmaf(a1.x * cdx, cdx, fmaf(chcdy, cdy, fabsf(cbdy * cdx)));
                 const float E = kSigmaErr * terms + 1e-30f;
-                const float thr = a1.w;
-                const float tm = 2.4e-7f * fabsf(thr) + 1e-7f;  // thr rounding + margins
                 float al, dal;  // alpha and a bound on |dAlpha| (absolute)
-                if (csig - E > 0.0f && csig + E < thr - tm) {
-                    const float au = a0.z * exp2f(-1.4426950408889634f * csig);
+                if (csig - E > 0.0f && csig + E < a1.w) {  // a1.w = thr_lo (staged)
+                    const float au = a0.z * ex2_approx(-1.4426950408889634f * csig);
                     // relative error: sigma bound, argument rounding, ex2.approx, * o
                     const float rel = E + 1.2e-7f * csig + 3.6e-7f;
                     if (au > 0.99f * (1.0f + rel)) {  // reference capped too: alpha = 0.99
@@ -256,8 +280,8 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                         al = fminf(au, 0.99f);
                         dal = au * rel;
                     }
-                } else if (csig - E > thr + tm) {
-                    continue;  // certainly skipped by the reference
+                } else if (csig - E > a0.w) {
+                    continue;  // certainly skipped: sigma_ref >= csig - E > hi >= thr_ref
                 } else {
                     double ad;
                     if (F64) {
@@ -273,17 +297,18 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                 }
                 const float w = st.Tf * al;
 #pragma unroll
-                for (int c = 0; c < KMAX; ++c)
-                    if (c < K) st.acc[c] = fmaf(w, W.v[q * KMAX + c], st.acc[c]);
+                for (int c = 0; c < KMAX; ++c) st.acc[c] = fmaf(w, W.v[q * KMAX + c], st.acc[c]);
                 const float om = 1.0f - al;
                 st.Tf = st.Tf * om;
-                // 1/om by MUFU.RCP (rel. error < 2^-22, covered by the 1.01 factor)
-                st.errT += dal * __fdividef(1.0f, om) * 1.01f + 1.3e-7f;
+                // errT carried pre-scaled by 1e-4 (the stop threshold):
+                // += 1e-4 * (dal / om * 1.01 + 1.3e-7); 1/om by MUFU.RCP, whose
+                // error is covered by the 1.01 factor
+                st.errT = fmaf(dal * rcp_approx(om), 1.01e-4f, st.errT + 1.3e-11f);
                 ++st.nc;
                 st.last = base + q + 1;
-                if (st.Tf < 1e-4f * (1.0f + st.errT + 1e-6f)) {
+                if (st.Tf < 1.0000001e-4f + st.errT) {
                     st.done = true;  // certain stop, or ambiguous -> EXACT re-walk
-                    st.replay = !(st.Tf < 1e-4f * (1.0f - st.errT - 1e-6f));
+                    st.replay = !(st.Tf < 0.9999999e-4f - st.errT);
                     break;
                 }
             }
@@ -302,12 +327,15 @@ blend_fwd_kernel(BlendArgs A) {
     const int tile = A.tile_order ? A.tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % A.ntx, ty = tile / A.ntx;
     const int tid = threadIdx.x, warp = tid >> 5, lane = tid & 31;
-    // warp w owns rows 2w, 2w+1 of the tile; lane -> (x = lane & 15, y = lane >> 4)
-    const int px = tx * kTile + (lane & 15), py = ty * kTile + 2 * warp + (lane >> 4);
+    // warp footprint kWarpW x (32 / kWarpW) pixels; lane -> (lane % kWarpW, lane / kWarpW)
+    constexpr int kWarpH = 32 / kWarpW, kPerRow = kTile / kWarpW;
+    const int sx0 = tx * kTile + kWarpW * (warp % kPerRow);
+    const int sy_raw = ty * kTile + kWarpH * (warp / kPerRow);
+    const int px = sx0 + (lane % kWarpW), py = sy_raw + lane / kWarpW;
     const bool inside = px < A.W && py < A.H;
     const int s0 = A.ranges[tile], s1 = A.ranges[tile + 1];
-    const int sx0 = tx * kTile, sx1 = min(sx0 + kTile - 1, A.W - 1);
-    const int sy0 = min(ty * kTile + 2 * warp, A.H - 1), sy1 = min(sy0 + 1, A.H - 1);
+    const int sx1 = min(sx0 + kWarpW - 1, A.W - 1);
+    const int sy0 = min(sy_raw, A.H - 1), sy1 = min(sy_raw + kWarpH - 1, A.H - 1);
 
     PixelState<KMAX, F64> st;
     st.reset(s0, !inside);
