@@ -5,9 +5,10 @@
 // np.searchsorted (rasterizer.py:132), without materialising a composite key:
 //
 //  1. depth ranks.  Positive float64 depths order like their bit patterns.
-//     The bits are shifted into a 31-bit "coarse" key (bits - min) >> s, the
-//     coarse keys are radix-sorted stably (4 x 8-bit LSD passes; invisible
-//     splats carry 0xffffffff and sort last), and runs of equal coarse keys
+//     The bits are shifted into a "coarse" key (bits - min) >> s of about
+//     log2(n) + 3 bits (~8 buckets per splat), the coarse keys are
+//     radix-sorted stably (8-bit LSD passes, 3 for 1M splats; invisible
+//     splats carry all ones and sort last), and runs of equal coarse keys
 //     are re-ordered by the full 64-bit key (insertion sort, stable).  If a
 //     run is longer than kMaxRun the whole order is recomputed with a full
 //     64-bit LSD sort (8 passes) -- correctness never depends on the data.
@@ -101,12 +102,15 @@ minmax_kernel(const uint64_t *keys, int64_t n, unsigned long long *mm /* [min, m
     }
 }
 
+// Visible keys get `vbits` bits ((bits - min) >> s < 2^vbits); invisible
+// splats carry all ones, above every visible key in the sorted digits.
 __global__ void __launch_bounds__(kThreads)
-coarse_key_kernel(const uint64_t *keys, int64_t n, const unsigned long long *mm, uint32_t *ck) {
+coarse_key_kernel(const uint64_t *keys, int64_t n, const unsigned long long *mm, int vbits,
+                  uint32_t *ck) {
     const unsigned long long lo = mm[0], hi = mm[1];
     const unsigned long long range = hi >= lo ? hi - lo : 0ull;
     const int bits = range ? 64 - __clzll((long long)range) : 0;
-    const int s = bits > 31 ? bits - 31 : 0;
+    const int s = bits > vbits ? bits - vbits : 0;
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * kThreads) {
         const unsigned long long k = keys[i];
@@ -597,7 +601,9 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
     __syncwarp();
     prefix2d(Dw, w1, h1, lane, 32, [] { __syncwarp(); });
     __syncthreads();
-    // phase 2: exclusive scan across warps, per tile (block total <= 2048)
+    // phase 2: exclusive scan across warps, per tile (block total <= 2048), and
+    // the block's global base per tile (tile start + earlier blocks) in smem
+    uint32_t *s_base = reinterpret_cast<uint32_t *>(smem_i32 + kWarps * cells);
     for (int t = tid; t < C.ntiles; t += kThreads) {
         const int cell = (t / C.ntx) * w1 + t % C.ntx;
         int run = 0;
@@ -607,6 +613,7 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
             smem_i32[w * cells + cell] = run;
             run += c;
         }
+        s_base[cell] = run ? (uint32_t)ranges[t] + hist[(int64_t)t * nblocks + blockIdx.x] : 0u;
     }
     __syncthreads();
     // phase 3: expand once, place (and cull-flag) every pair
@@ -619,9 +626,7 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
         if (ok && (peers & lt) == 0) Dw[cell] = before + __popc(peers);
         __syncwarp();
         if (ok) {
-            const uint32_t pos = (uint32_t)ranges[tile] +
-                                 hist[(int64_t)tile * nblocks + blockIdx.x] + (uint32_t)before +
-                                 __popc(peers & lt);
+            const uint32_t pos = s_base[cell] + (uint32_t)before + __popc(peers & lt);
             if ((int64_t)pos < C.cap) {
                 uint32_t v = sp;
                 if (C.rec) {
@@ -706,8 +711,9 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
                                  int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int32_t ntiles = ntx * nty;
-    // placement keeps 8 per-warp int32 difference arrays of (ntx+1)(nty+1) cells in smem
-    const bool fits = (int64_t)(ntx + 1) * (nty + 1) * 4 * kWarps <= 220 * 1024;
+    // placement keeps 8 per-warp int32 difference arrays of (ntx+1)(nty+1) cells
+    // plus one table of per-tile block bases in smem
+    const bool fits = (int64_t)(ntx + 1) * (nty + 1) * 4 * (kWarps + 1) <= 220 * 1024;
     if (n < 0 || pair_capacity < 1 || ntx < 1 || nty < 1 || !fits || !tile_ranges ||
         !n_pairs || !pair_splat || !workspace || (rec && (width < 1 || height < 1))) {
         ivr::set_error("ivr_bin_sort: bad argument");
@@ -740,26 +746,39 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     int32_t *need_full = (int32_t *)(ws + L.off[13]);
     const int nbk = L.nbk, nbp = L.nbp;
 
-    // ---- 1. depth ranks: 31-bit coarse keys, 4 stable passes, run fix-up
+    // ---- 1. depth ranks: coarse keys with ~8 buckets per splat (at least
+    //      log2(n) + 3 bits; 8-bit digits), stable LSD passes, run fix-up
+    int lg = 1;
+    while (lg < 62 && (1ll << lg) < n) ++lg;
+    int passes = (lg + 4 + 7) / 8;
+    passes = passes < 2 ? 2 : (passes > 4 ? 4 : passes);
+    const int vbits = 8 * passes - 1;
     init_minmax_kernel<<<1, 1, 0, st>>>(mm, need_full);
     int gb = (int)((n + kThreads * 8 - 1) / (kThreads * 8));
     gb = gb < 1 ? 1 : (gb > 1184 ? 1184 : gb);
     minmax_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm);
-    coarse_key_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm, ckA);
-    radix_pass<uint32_t>(st, ckA, nullptr, ckB, vB, n, 0, nbk, bh, rt, nullptr);
-    radix_pass<uint32_t>(st, ckB, vB, ckA, vA, n, 8, nbk, bh, rt, nullptr);
-    radix_pass<uint32_t>(st, ckA, vA, ckB, vB, n, 16, nbk, bh, rt, nullptr);
-    radix_pass<uint32_t>(st, ckB, vB, ckA, vA, n, 24, nbk, bh, rt, nullptr);
-    fixup_kernel<<<(int)((n + kThreads - 1) / kThreads), kThreads, 0, st>>>(ckA, vA, n, depth_key,
+    coarse_key_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm, vbits, ckA);
+    uint32_t *kin = ckA, *kout = ckB, *vin = nullptr, *vout = vB;
+    for (int p = 0; p < passes; ++p) {
+        radix_pass<uint32_t>(st, kin, vin, kout, vout, n, 8 * p, nbk, bh, rt, nullptr);
+        uint32_t *t = kin;
+        kin = kout;
+        kout = t;
+        vin = vout;
+        vout = (vout == vB) ? vA : vB;
+    }
+    // sorted (key, order) now in (kin, vin)
+    uint32_t *ord = vin, *vscratch = (vin == vA) ? vB : vA;
+    fixup_kernel<<<(int)((n + kThreads - 1) / kThreads), kThreads, 0, st>>>(kin, ord, n, depth_key,
                                                                            need_full);
-    // fallback (device-gated, normally an immediate return): full 64-bit sort into vA
-    fallback_sort_kernel<<<1, kFbThreads, 0, st>>>(depth_key, n, need_full, fkA, fkB, vA, vB);
+    // fallback (device-gated, normally an immediate return): full 64-bit sort into ord
+    fallback_sort_kernel<<<1, kFbThreads, 0, st>>>(depth_key, n, need_full, fkA, fkB, ord, vscratch);
     // ---- 2. pair count P (sum of tile counts) -> n_pairs
-    scan_reduce_kernel<<<nbk, kThreads, 0, st>>>(vA, count, n, partial);
+    scan_reduce_kernel<<<nbk, kThreads, 0, st>>>(ord, count, n, partial);
     scan_partials_kernel<<<1, 1024, 0, st>>>(partial, nbk, n_pairs);
     // ---- 3. counting placement by tile (+ optional tile cull flag)
     PairCtx C{};
-    C.order = vA;
+    C.order = ord;
     C.count = count;
     C.rect = (const ushort4 *)rect;
     C.rec = (const float4 *)rec;
@@ -770,7 +789,7 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     C.cap = pair_capacity;
     const size_t cells = (size_t)(ntx + 1) * (nty + 1);
     const size_t sm_hist = 4 * cells;
-    const size_t sm_place = 4 * (size_t)kWarps * cells;
+    const size_t sm_place = 4 * (size_t)(kWarps + 1) * cells;
     if (sm_hist > 48 * 1024)
         cudaFuncSetAttribute(pair_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_hist);
     if (sm_place > 48 * 1024)
