@@ -17,7 +17,7 @@ from .rasterizer import (  # noqa: F401
     RenderOutput, rasterize_backward, rasterize_forward, render_attribute_map,
 )
 from .scene import (  # noqa: F401
-    BasicSceneModel, ComposedScene, DeviceScene, EditState, EffectiveScene, FrameGraph,
+    BasicSceneModel, ComposedScene, DeviceScene, EditState, EffectiveScene, FrameGraph, FramePipeline,
     apply_edits, render_composed,
 )
 from .shading import (  # noqa: F401

@@ -341,8 +341,9 @@ class FrameGraph:
 
     RING = 8
 
-    def __init__(self, ds, width, height, exact=False, headroom=1.3, warm_cam=None):
+    def __init__(self, ds, width, height, exact=False, headroom=1.3, warm_cam=None, slots=1):
         self.ds, self.W, self.H, self.exact = ds, int(width), int(height), exact
+        self.slots = max(1, int(slots))  # graphs with their own output buffers (pipelining)
         dev = ds.dg.device
         S = ds.n_scenes
         nb = ctypes.sizeof(L.FrameParams_t)
@@ -407,13 +408,17 @@ class FrameGraph:
         D.bin_sort(F, ws, capacity=self.capacity)
         D.blend(F, ws, want_state=False, exact=self.exact)
         torch.cuda.synchronize()
-        g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(g):
-            F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=self.d_params)
-            D.bin_sort(F, ws, capacity=self.capacity)
-            D.blend(F, ws, want_state=False, exact=self.exact)
-        F.layout = layout
-        self.F, self.g = F, g
+        self.graphs = []
+        for _ in range(self.slots):  # same work, distinct output buffers (graph pools)
+            g = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(g):
+                F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=self.d_params)
+                D.bin_sort(F, ws, capacity=self.capacity)
+                D.blend(F, ws, want_state=False, exact=self.exact)
+            F.layout = layout
+            self.graphs.append((g, F))
+        self.g, self.F = self.graphs[0]
+        self.K = K
         self._keep = (shading, edits)
 
     def stage(self, cam, **edits):
@@ -449,6 +454,71 @@ class FrameGraph:
     def recapture(self, cam):
         self.capacity = int(int(self.F.n_pairs.item()) * 1.3) + 4096
         self._capture(cam)
+
+
+class FramePipeline:
+    """End-to-end frames with the device->host image copy of frame i
+    overlapping the upload + compute of frame i+1.
+
+    ``submit(cam, **edits)`` stages the frame's parameters (pinned ring, one
+    H2D), replays the slot's captured graph on the compute stream and
+    enqueues the RGBA / contribution-count / pair-count copies into pinned
+    host buffers on a copy stream; ``result(ticket)`` waits for that frame's
+    copies and returns its RenderOutput (views of the slot's pinned buffers,
+    valid until the slot is reused ``slots`` submits later).  A frame whose
+    pair count outgrew the captured capacity is re-rendered synchronously
+    after growing the capacity."""
+
+    def __init__(self, fg: FrameGraph):
+        self.fg = fg
+        n = fg.slots
+        H, W, K = fg.H, fg.W, fg.K
+        self.copy_stream = torch.cuda.Stream(device=fg.ds.dg.device)
+        self.h_out = [torch.empty((H, W, K), dtype=torch.float32, pin_memory=True) for _ in range(n)]
+        self.h_cnt = [torch.empty((H, W), dtype=torch.int32, pin_memory=True) for _ in range(n)]
+        self.h_np = [torch.empty(1, dtype=torch.int32, pin_memory=True) for _ in range(n)]
+        self.done = [None] * n
+        self.k = 0
+
+    def h2d_bytes_per_frame(self):
+        return self.fg.nb + 8 * 4 * self.fg.ds.n_scenes
+
+    def d2h_bytes_per_frame(self):
+        return self.h_out[0].numel() * 4 + self.h_cnt[0].numel() * 4 + 4
+
+    def submit(self, cam, **edits):
+        fg = self.fg
+        k = self.k
+        self.k = (k + 1) % fg.slots
+        main = torch.cuda.current_stream()
+        if self.done[k] is not None:  # the slot's previous image must have left the device
+            main.wait_event(self.done[k])
+        fg._stage(cam, **edits)
+        g, F = fg.graphs[k]
+        g.replay()
+        ev = torch.cuda.Event()
+        ev.record(main)
+        cs = self.copy_stream
+        cs.wait_event(ev)
+        with torch.cuda.stream(cs):
+            self.h_out[k].copy_(F.out, non_blocking=True)
+            self.h_cnt[k].copy_(F.contrib, non_blocking=True)
+            self.h_np[k].copy_(F.n_pairs[:1], non_blocking=True)
+            d = torch.cuda.Event()
+            d.record(cs)
+        self.done[k] = d
+        return (k, cam, edits)
+
+    def result(self, ticket):
+        k, cam, edits = ticket
+        self.done[k].synchronize()
+        fg = self.fg
+        if int(self.h_np[k][0]) > fg.capacity:  # this view needed more pairs: grow, redo
+            torch.cuda.synchronize()
+            fg.capacity = int(int(self.h_np[k][0]) * 1.3) + 4096
+            fg._capture(cam)
+            fg.render_host(cam, self.h_out[k], self.h_cnt[k], **edits)
+        return _unpack(self.h_out[k].numpy(), fg.F.layout, self.h_cnt[k].numpy())
 
 
 def render_composed(scene, cam, channels=("color", "alpha"), attrs=None, dtype=np.float32,
