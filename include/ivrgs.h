@@ -212,13 +212,14 @@ int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_t *order,
  * warp-reduced float32 atomics into caller-zeroed per-Gaussian buffers:
  * g_values (n,k), g_mean2d (n,2), g_conic (n,3), g_opacity (n).
  * out = K3's float32 output (H,W,k); d_out (H,W,k) float32 upstream gradient.
- * rec64 selects dtype=float64 decisions.  flags: IVR_BLEND_PRECULLED. */
+ * rec64 selects dtype=float64 decisions.  tile_order (nullable): CTA -> tile
+ * schedule (ivr_tile_order, heaviest first).  flags: IVR_BLEND_PRECULLED. */
 int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
                   int32_t nty, const float *rec, const float *values, const double *rec64,
                   int32_t k, int32_t width, int32_t height, const float *out,
                   const int32_t *last_pos, const float *d_out, float *g_values,
-                  float *g_mean2d, float *g_conic, float *g_opacity, int32_t flags,
-                  ivr_stream_t stream);
+                  float *g_mean2d, float *g_conic, float *g_opacity,
+                  const int32_t *tile_order, int32_t flags, ivr_stream_t stream);
 
 /* Per-Gaussian backward outputs (float64, NULL = not wanted). */
 typedef struct ivr_grads {
@@ -292,6 +293,20 @@ int ivr_unpack(const uint8_t *src, int64_t count, int32_t kind, void *dst, ivr_s
 
 /* double -> little-endian f32 bytes (_f32_bytes, scene.py:243-244). */
 int ivr_pack_f32(const double *src, int64_t count, uint8_t *dst, ivr_stream_t stream);
+
+/* Photometric objective, losses.ssim + losses.photometric_loss
+ * (losses.py:45-138), float64: pred/gt (H,W,C); window = the reference's
+ * normalized 11-tap Gaussian (sigma 1.5).  Writes
+ *   d_pred = a * sign(pred - gt) + b * d(mean SSIM)/d(pred)   (H,W,C)
+ *   sums[0] = sum of SSIM over valid windows and channels (0 if !with_ssim)
+ *   sums[1] = sum |pred - gt|
+ * (photometric_loss: a = w_l1 / numel, b = -w_ssim).  Scratch from a size
+ * query (three partial maps + per-block partials). */
+size_t ivr_photometric_workspace_size(int32_t height, int32_t width, int32_t channels);
+int ivr_photometric_loss(const double *pred, const double *gt, int32_t height, int32_t width,
+                         int32_t channels, const double window[11], double a, double b,
+                         int32_t with_ssim, double *d_pred, double *sums, void *workspace,
+                         size_t workspace_bytes, ivr_stream_t stream);
 
 #ifdef __cplusplus
 }

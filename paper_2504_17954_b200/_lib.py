@@ -106,7 +106,7 @@ _SIGS = {
                       ctypes.c_int),
     "ivr_tile_order": ([P, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_blend_bwd": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
-                       ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, ctypes.c_int32, P],
+                       ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, P, ctypes.c_int32, P],
                       ctypes.c_int),
     "ivr_preprocess_bwd": ([ctypes.POINTER(Gaussians_t), ctypes.POINTER(Shading_t),
                             ctypes.POINTER(Edits_t), P, ctypes.POINTER(Camera_t),
@@ -124,6 +124,11 @@ _SIGS = {
     "ivr_crc32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
     "ivr_unpack": ([P, ctypes.c_int64, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_pack_f32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
+    "ivr_photometric_workspace_size": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32],
+                                       ctypes.c_size_t),
+    "ivr_photometric_loss": ([P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                              ctypes.POINTER(ctypes.c_double), ctypes.c_double, ctypes.c_double,
+                              ctypes.c_int32, P, P, P, ctypes.c_size_t, P], ctypes.c_int),
 }
 
 _lib = None

@@ -2,9 +2,10 @@
 //
 // K4a blend_bwd_kernel replaces _kernels.composite_backward
 // (_kernels.py:75-135) + the per-Gaussian np.add.at reductions
-// (rasterizer.py:240-243).  One CTA per tile, one thread per pixel; pairs are
-// staged through shared memory exactly as in K3 and each pixel walks its
-// contributors FRONT to back up to last_pos (known from the forward).  With
+// (rasterizer.py:240-243).  One CTA per tile, one thread per pixel, each warp
+// an independent 8x4 pixel block that streams the tile list in 32-pair chunks
+// with the K3 strip cull; each pixel walks its contributors FRONT to back up
+// to last_pos (known from the forward).  With
 // C = forward output and A_i = colour accumulated through contributor i, the
 // colour behind i is C - A_i, so
 //   dL/dalpha_i = sum_k dout_k (T_i v_ik - (C_k - A_ik) / (1 - alpha_i)),
@@ -40,6 +41,7 @@ struct BwdArgs {
     const float *d_out;
     float *g_values, *g_mean, *g_conic, *g_opac;
     int preculled;
+    const int32_t *tile_order;
 };
 
 __device__ __forceinline__ double exact_alpha_b(double dpx, double dpy, double mx, double my,
@@ -86,36 +88,52 @@ __device__ __forceinline__ float warp_transpose_sum(float *x, int lane) {
     return r;
 }
 
+__device__ __forceinline__ float ex2_approx_b(float x) {
+    float y;
+    asm("ex2.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+__device__ __forceinline__ float rcp_approx_b(float x) {
+    float y;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(y) : "f"(x));
+    return y;
+}
+
+// Per-warp staging slots for one 32-pair chunk.
+template <int KMAX, bool F64>
+struct BwdSlots {
+    float4 r0[32], r1[32];
+    float v[32 * KMAX];
+    int sp[32];
+    double r64[F64 ? 32 * 6 : 1];
+};
+
+constexpr int kBwdWarpW = 8;  // warp footprint 8x4 pixels (as K3)
+
+// One CTA per tile, each warp an independent 8x4 block of pixels walking
+// the tile list in 32-pair chunks up to the largest last_pos of its pixels
+// (same strip cull and prefetch as K3; no CTA barrier).
 template <int KMAX, bool F64>
 __global__ void __launch_bounds__(kBwdThreads)
 blend_bwd_kernel(BwdArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
-    float4 *s_r0 = reinterpret_cast<float4 *>(smem);
-    float4 *s_r1 = s_r0 + kBwdThreads;
-    int *s_j = reinterpret_cast<int *>(s_r1 + kBwdThreads);
-    int *s_sp = s_j + kBwdThreads;
-    float *s_v = reinterpret_cast<float *>(s_sp + kBwdThreads);
-    double *s_r64 = reinterpret_cast<double *>(s_v + kBwdThreads * KMAX);
-    __shared__ int s_wsum[kBwdThreads / 32];
-    __shared__ uint32_t s_wmask[(kBwdThreads / 32) * (kBwdThreads / 32)];
-    __shared__ int s_end;
+    BwdSlots<KMAX, F64> &W = reinterpret_cast<BwdSlots<KMAX, F64> *>(smem)[threadIdx.x >> 5];
 
-    const int tile = blockIdx.x;
+    const int tile = A.tile_order ? A.tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % A.ntx, ty = tile / A.ntx;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    const int px = tx * kTile + (tid & 15), py = ty * kTile + (tid >> 4);
+    constexpr int kWH = 32 / kBwdWarpW, kPerRow = kTile / kBwdWarpW;
+    const int sx0 = tx * kTile + kBwdWarpW * (warp % kPerRow);
+    const int sy_raw = ty * kTile + kWH * (warp / kPerRow);
+    const int px = sx0 + (lane % kBwdWarpW), py = sy_raw + lane / kBwdWarpW;
     const bool inside = px < A.W && py < A.H;
+    const int sx1 = min(sx0 + kBwdWarpW - 1, A.W - 1);
+    const int sy0 = min(sy_raw, A.H - 1), sy1 = min(sy_raw + kWH - 1, A.H - 1);
     const int s0 = A.ranges[tile];
     const int K = A.K;
     const int64_t pix = (int64_t)py * A.W + px;
     const int last = inside ? A.last_pos[pix] : s0;
-    if (tid == 0) s_end = s0;
-    __syncthreads();
-    atomicMax(&s_end, last);
-    __syncthreads();
-    const int s_stop = s_end;  // no pixel of this tile contributes past here
-    const int cx0 = tx * kTile, cy0 = ty * kTile;
-    const int cx1 = min(cx0 + kTile - 1, A.W - 1), cy1 = min(cy0 + kTile - 1, A.H - 1);
+    const int stop = __reduce_max_sync(0xffffffffu, last);  // no pixel of the warp contributes past here
 
     float C[KMAX], acc[KMAX], dout[KMAX];
 #pragma unroll
@@ -128,72 +146,48 @@ blend_bwd_kernel(BwdArgs A) {
     const float fpx = (float)px, fpy = (float)py;
     const double dpx = (double)px, dpy = (double)py;
 
-    for (int base = s0; base < s_stop; base += kBwdThreads) {
-        __syncthreads();
-        const int j = base + tid;
-        bool keep = false;
-        float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-        int sp = 0;
-        if (j < s_stop) {
-            sp = A.pair_splat[j];
-            keep = !A.preculled || sp >= 0;
-            if (keep) {
+    int sp = 0;
+    float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
+    auto fetch = [&](int base) {
+        const int j = base + lane;
+        if (j < stop) {
+            sp = __ldg(A.pair_splat + j);  // bit 31: culled for this tile (ivr_bin_sort_cull)
+            if (sp >= 0) {
                 r0 = __ldg(A.rec + 2 * sp);
                 r1 = __ldg(A.rec + 2 * sp + 1);
-                if (!A.preculled) keep = !tile_cull32(r0, r1, cx0, cx1, cy0, cy1);
             }
         }
+    };
+    if (s0 < stop) fetch(s0);
+    for (int base = s0; base < stop; base += 32) {
+        const int j = base + lane;
+        const bool keep = j < stop && sp >= 0 && !tile_cull32(r0, r1, sx0, sx1, sy0, sy1);
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
-        if (lane == 0) s_wsum[warp] = __popc(m);
-        __syncthreads();
-        int off = 0, total = 0;
-#pragma unroll
-        for (int w = 0; w < kBwdThreads / 32; ++w) {
-            const int c = s_wsum[w];
-            off += (w < warp) ? c : 0;
-            total += c;
-        }
         if (keep) {
-            const int q = off + __popc(m & lanemask_lt());
-            s_r0[q] = r0;
-            s_r1[q] = r1;
-            s_j[q] = j;
-            s_sp[q] = sp;
+            W.r0[lane] = r0;
+            W.r1[lane] = r1;
+            W.sp[lane] = sp;
             const float *v = A.values + (int64_t)K * sp;
 #pragma unroll
-            for (int c = 0; c < KMAX; ++c)
-                if (c < K) s_v[q * KMAX + c] = __ldg(v + c);
+            for (int c = 0; c < KMAX; ++c) W.v[lane * KMAX + c] = c < K ? __ldg(v + c) : 0.0f;
             if (F64) {
                 const double *r = A.rec64 + 8 * (int64_t)sp;
 #pragma unroll
-                for (int c = 0; c < 6; ++c) s_r64[q * 6 + c] = __ldg(r + c);
+                for (int c = 0; c < 6; ++c) W.r64[lane * 6 + c] = __ldg(r + c);
             }
         }
-        __syncthreads();
-        // per-warp strip filter (as in K3): survivors that can touch this warp's 16x2 pixels
-        const int nwords = (total + 31) >> 5;
-        {
-            const int wy0 = min(cy0 + 2 * warp, A.H - 1), wy1 = min(cy0 + 2 * warp + 1, A.H - 1);
-            for (int w = 0; w < nwords; ++w) {
-                const int q = (w << 5) + lane;
-                bool t = false;
-                if (q < total) t = !tile_cull32(s_r0[q], s_r1[q], cx0, cx1, wy0, wy1);
-                const uint32_t b = __ballot_sync(0xffffffffu, t);
-                if (lane == 0) s_wmask[warp * (kBwdThreads / 32) + w] = b;
-            }
-            __syncwarp();
-        }
-        for (int w = 0; w < nwords; ++w) {
-          uint32_t mbits = s_wmask[warp * (kBwdThreads / 32) + w];
-          while (mbits) {
-            const int q = (w << 5) + __ffs(mbits) - 1;
+        __syncwarp();
+        if (base + 32 < stop) fetch(base + 32);
+        uint32_t mbits = m;
+        while (mbits) {
+            const int q = __ffs(mbits) - 1;
             mbits &= mbits - 1;
-            const float4 a0 = s_r0[q];
-            const float4 a1 = s_r1[q];
+            const float4 a0 = W.r0[q];
+            const float4 a1 = W.r1[q];
             bool contrib = false;
             float al = 0.f, alu = 0.f, g = 0.f;
             float dx = 0.f, dy = 0.f;
-            if (inside && s_j[q] < last) {
+            if (inside && base + q < last) {
                 dx = fpx - a0.x;
                 dy = fpy - a0.y;
                 const float bdy = a1.y * dy, hcdy = a1.z * dy;
@@ -201,8 +195,8 @@ blend_bwd_kernel(BwdArgs A) {
                 if (!(sig > a0.w)) {
                     float cdx = dx, cdy = dy, cbdy = bdy, chcdy = hcdy, csig = sig;
                     if (F64) {
-                        cdx = (float)dsub(dpx, s_r64[q * 6]);
-                        cdy = (float)dsub(dpy, s_r64[q * 6 + 1]);
+                        cdx = (float)dsub(dpx, W.r64[q * 6]);
+                        cdy = (float)dsub(dpy, W.r64[q * 6 + 1]);
                         cbdy = a1.y * cdy;
                         chcdy = a1.z * cdy;
                         csig = fmaf(fmaf(a1.x, cdx, cbdy), cdx, chcdy * cdy);
@@ -212,14 +206,14 @@ blend_bwd_kernel(BwdArgs A) {
                     const float thr = a1.w;
                     const float tm = 2.4e-7f * fabsf(thr) + 1e-7f;
                     if (csig - E > 0.0f && csig + E < thr - tm) {
-                        g = exp2f(-1.4426950408889634f * csig);
+                        g = ex2_approx_b(-1.4426950408889634f * csig);
                         alu = a0.z * g;
                         al = fminf(alu, 0.99f);
                         contrib = true;
-                    } else if (!(csig - E > thr + tm)) {
+                    } else if (!(csig - E > a0.w)) {
                         double au, gd, ad;
                         if (F64) {
-                            const double *r = s_r64 + q * 6;
+                            const double *r = W.r64 + q * 6;
                             ad = exact_alpha_b(dpx, dpy, r[0], r[1], r[2], r[3], r[4], r[5], au, gd);
                         } else {
                             ad = exact_alpha_b(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
@@ -246,17 +240,15 @@ blend_bwd_kernel(BwdArgs A) {
             for (int c = 0; c < NX; ++c) x[c] = 0.f;
             if (contrib) {
                 const float w = T * al;
-                const float inv = __frcp_rn(1.0f - al);
+                const float inv = rcp_approx_b(1.0f - al);
                 float d_alpha = 0.f;
 #pragma unroll
-                for (int c = 0; c < KMAX; ++c) {
-                    if (c < K) {
-                        const float vk = s_v[q * KMAX + c];
-                        acc[c] = fmaf(w, vk, acc[c]);
-                        const float after = C[c] - acc[c];
-                        d_alpha = fmaf(dout[c], T * vk - after * inv, d_alpha);
-                        x[c] = dout[c] * w;
-                    }
+                for (int c = 0; c < KMAX; ++c) {  // value slots are zero-padded past K
+                    const float vk = W.v[q * KMAX + c];
+                    acc[c] = fmaf(w, vk, acc[c]);
+                    const float after = C[c] - acc[c];
+                    d_alpha = fmaf(dout[c], T * vk - after * inv, d_alpha);
+                    x[c] = dout[c] * w;
                 }
                 if (alu < 0.99f) {
                     const float d_sigma = -alu * d_alpha;
@@ -273,7 +265,7 @@ blend_bwd_kernel(BwdArgs A) {
             if (__any_sync(0xffffffffu, contrib)) {
                 // transpose reduction: lane i ends with the warp total of slot i
                 // (CH-1 shuffles per chunk instead of 5 per slot), then parallel atomics
-                const int s = s_sp[q];
+                const int s = W.sp[q];
 #pragma unroll
                 for (int ch = 0; ch < NX / CH; ++ch) {
                     const float tot = warp_transpose_sum<CH>(x + ch * CH, lane);
@@ -288,15 +280,14 @@ blend_bwd_kernel(BwdArgs A) {
                     }
                 }
             }
-          }
         }
+        __syncwarp();  // slots are rewritten by the next chunk
     }
 }
 
 template <int KMAX, bool F64>
 int launch_bwd(const BwdArgs &A, int ntiles, cudaStream_t st) {
-    const size_t sm = (size_t)kBwdThreads * (16 + 16 + 4 + 4 + 4 * KMAX) +
-                      (F64 ? (size_t)kBwdThreads * 48 : 0);
+    const size_t sm = (kBwdThreads / 32) * sizeof(BwdSlots<KMAX, F64>);
     auto fn = blend_bwd_kernel<KMAX, F64>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     fn<<<ntiles, kBwdThreads, sm, st>>>(A);
@@ -605,7 +596,7 @@ extern "C" int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_spl
                              const double *rec64, int32_t k, int32_t width, int32_t height,
                              const float *out, const int32_t *last_pos, const float *d_out,
                              float *g_values, float *g_mean2d, float *g_conic, float *g_opacity,
-                             int32_t flags, ivr_stream_t stream) {
+                             const int32_t *tile_order, int32_t flags, ivr_stream_t stream) {
     using namespace ivr;
     if (!tile_ranges || !pair_splat || !rec || !values || !out || !last_pos || !d_out ||
         !g_values || !g_mean2d || !g_conic || !g_opacity || k < 1 || k > 32 ||
@@ -631,6 +622,7 @@ extern "C" int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_spl
     A.g_conic = g_conic;
     A.g_opac = g_opacity;
     A.preculled = (flags & IVR_BLEND_PRECULLED) ? 1 : 0;
+    A.tile_order = tile_order;
     cudaStream_t st = (cudaStream_t)stream;
     const int nt = ntx * nty;
     const bool f64 = rec64 != nullptr;

@@ -1,0 +1,280 @@
+// Photometric loss: L1 + (1 - SSIM) with its analytic gradient, float64.
+//
+// Replaces losses.ssim / losses.photometric_loss (losses.py:45-138): an
+// 11x11 Gaussian window (sigma 1.5) evaluated where it fits ("valid"),
+// population statistics, C1 = 0.01^2, C2 = 0.03^2, mean over windows and
+// channels; the gradient is the adjoint ("full") filtering of the per-window
+// partials.  The reference runs 8 scipy convolutions per channel; here two
+// shared-memory tiled kernels do the work of all of them:
+//   A) per 16x32 block of windows: stage the 26x42 input patch of x and y,
+//      horizontal then vertical 11-tap passes for x, y, x^2, y^2, xy, the
+//      SSIM value, and the three partial maps dL/d(ux), dL/d(uxx), dL/d(uxy);
+//   B) per 16x32 block of pixels: stage the 26x42 patch of the three maps
+//      (zero outside the valid windows), full 11-tap passes, then
+//      d_pred = a * sign(x - y) + b * (F(d_ux) + 2x F(d_uxx) + y F(d_uxy))
+//      and the |x - y| sum for the L1 term.
+// Per-block partial sums are reduced in a fixed order (deterministic).
+// Bound: FP64 issue (~ (5 + 3) x 22 DFMA per pixel and channel) and the
+// f64 traffic of x, y, three maps and d_pred (~ 7 x 8 B per pixel-channel).
+#include "ivr_common.cuh"
+
+namespace ivr {
+namespace ssimk {
+
+constexpr int R = 5, WIN = 2 * R + 1;
+constexpr int TH = 16, TW = 32;                 // output tile (windows in A, pixels in B)
+constexpr int IH = TH + WIN - 1, IW = TW + WIN - 1;  // 26 x 42 staged patch
+constexpr int kThreads = 256;
+constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
+
+struct Args {
+    const double *x, *y;  // (H, W, C)
+    int H, W, C, Hv, Wv;
+    double g[WIN];
+    double up;            // 1 / (Hv * Wv * C)
+    double a, b;          // d_pred = a * sign(x - y) + b * d(mean SSIM)/dx
+    double *m_ux, *m_uxx, *m_uxy;  // (C, Hv, Wv)
+    double *partA, *partB;         // per-block partial sums
+    double *d_pred;                // (H, W, C)
+};
+
+__device__ __forceinline__ double block_sum(double v, double *s_red) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    __syncthreads();
+    if (lane == 0) s_red[warp] = v;
+    __syncthreads();
+    double t = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kThreads / 32; ++w) t += s_red[w];
+    return t;
+}
+
+// A: window statistics -> SSIM partial sum + the three partial maps
+__global__ void __launch_bounds__(kThreads) ssim_window_kernel(Args A) {
+    extern __shared__ __align__(16) double sm[];
+    double *sx = sm, *sy = sx + IH * IW;
+    double *hq = sy + IH * IW;  // [5][IH][TW]
+    __shared__ double s_red[kThreads / 32];
+    const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
+    const int tid = threadIdx.x;
+    double ssum = 0.0;
+    for (int c = 0; c < A.C; ++c) {
+        __syncthreads();
+        for (int k = tid; k < IH * IW; k += kThreads) {
+            const int r = k / IW, q = k % IW, gi = i0 + r, gj = j0 + q;
+            const bool ok = gi < A.H && gj < A.W;
+            const int64_t o = ((int64_t)gi * A.W + gj) * A.C + c;
+            sx[k] = ok ? A.x[o] : 0.0;
+            sy[k] = ok ? A.y[o] : 0.0;
+        }
+        __syncthreads();
+        for (int k = tid; k < IH * TW; k += kThreads) {
+            const int r = k / TW, q = k % TW;
+            double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0, h4 = 0.0;
+#pragma unroll
+            for (int t = 0; t < WIN; ++t) {
+                const double xv = sx[r * IW + q + t], yv = sy[r * IW + q + t], g = A.g[t];
+                h0 = fma(g, xv, h0);
+                h1 = fma(g, yv, h1);
+                h2 = fma(g, xv * xv, h2);
+                h3 = fma(g, yv * yv, h3);
+                h4 = fma(g, xv * yv, h4);
+            }
+            hq[0 * IH * TW + k] = h0;
+            hq[1 * IH * TW + k] = h1;
+            hq[2 * IH * TW + k] = h2;
+            hq[3 * IH * TW + k] = h3;
+            hq[4 * IH * TW + k] = h4;
+        }
+        __syncthreads();
+        for (int k = tid; k < TH * TW; k += kThreads) {
+            const int r = k / TW, q = k % TW, wi = i0 + r, wj = j0 + q;
+            if (wi >= A.Hv || wj >= A.Wv) continue;
+            double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+#pragma unroll
+            for (int t = 0; t < WIN; ++t) {
+                const double g = A.g[t];
+#pragma unroll
+                for (int m = 0; m < 5; ++m) u[m] = fma(g, hq[m * IH * TW + (r + t) * TW + q], u[m]);
+            }
+            const double ux = u[0], uy = u[1];
+            const double vx = u[2] - ux * ux, vy = u[3] - uy * uy, vxy = u[4] - ux * uy;
+            const double a1 = 2.0 * ux * uy + kC1, a2 = 2.0 * vxy + kC2;
+            const double b1 = ux * ux + uy * uy + kC1, b2 = vx + vy + kC2;
+            const double bb = b1 * b2;
+            const double s = (a1 * a2) / bb;
+            ssum += s;
+            const double da1 = a2 / bb * A.up, da2 = a1 / bb * A.up;
+            const double db1 = -s / b1 * A.up, db2 = -s / b2 * A.up;
+            const double d_uxy = 2.0 * da2;
+            const double d_uxx = db2;
+            const double d_ux = 2.0 * uy * da1 + 2.0 * ux * db1 - 2.0 * ux * db2 - uy * d_uxy;
+            const int64_t o = ((int64_t)c * A.Hv + wi) * A.Wv + wj;
+            A.m_ux[o] = d_ux;
+            A.m_uxx[o] = d_uxx;
+            A.m_uxy[o] = d_uxy;
+        }
+    }
+    const double t = block_sum(ssum, s_red);
+    if (tid == 0) A.partA[blockIdx.y * gridDim.x + blockIdx.x] = t;
+}
+
+// B: adjoint filtering of the maps -> d_pred, plus the L1 partial sum
+template <bool SSIM>
+__global__ void __launch_bounds__(kThreads) ssim_grad_kernel(Args A) {
+    extern __shared__ __align__(16) double sm[];
+    double *mq = sm;                    // [3][IH][IW]
+    double *hq = mq + 3 * IH * IW;      // [3][IH][TW]
+    __shared__ double s_red[kThreads / 32];
+    const int i0 = blockIdx.y * TH, j0 = blockIdx.x * TW;
+    const int tid = threadIdx.x;
+    double l1 = 0.0;
+    for (int c = 0; c < A.C; ++c) {
+        if (SSIM) {
+            __syncthreads();
+            for (int k = tid; k < IH * IW; k += kThreads) {
+                const int r = k / IW, q = k % IW, wi = i0 - (WIN - 1) + r, wj = j0 - (WIN - 1) + q;
+                const bool ok = wi >= 0 && wj >= 0 && wi < A.Hv && wj < A.Wv;
+                const int64_t o = ((int64_t)c * A.Hv + wi) * A.Wv + wj;
+                mq[0 * IH * IW + k] = ok ? A.m_ux[o] : 0.0;
+                mq[1 * IH * IW + k] = ok ? A.m_uxx[o] : 0.0;
+                mq[2 * IH * IW + k] = ok ? A.m_uxy[o] : 0.0;
+            }
+            __syncthreads();
+            for (int k = tid; k < IH * TW; k += kThreads) {
+                const int r = k / TW, q = k % TW;
+                double h[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                for (int t = 0; t < WIN; ++t) {
+                    const double g = A.g[t];
+#pragma unroll
+                    for (int m = 0; m < 3; ++m)
+                        h[m] = fma(g, mq[m * IH * IW + r * IW + q + (WIN - 1) - t], h[m]);
+                }
+#pragma unroll
+                for (int m = 0; m < 3; ++m) hq[m * IH * TW + k] = h[m];
+            }
+            __syncthreads();
+        }
+        for (int k = tid; k < TH * TW; k += kThreads) {
+            const int r = k / TW, q = k % TW, pi = i0 + r, pj = j0 + q;
+            if (pi >= A.H || pj >= A.W) continue;
+            const int64_t o = ((int64_t)pi * A.W + pj) * A.C + c;
+            const double xv = A.x[o], yv = A.y[o];
+            const double df = xv - yv;
+            l1 += fabs(df);
+            double d = A.a * (df > 0.0 ? 1.0 : (df < 0.0 ? -1.0 : 0.0));
+            if (SSIM) {
+                double f[3] = {0.0, 0.0, 0.0};
+#pragma unroll
+                for (int t = 0; t < WIN; ++t) {
+                    const double g = A.g[t];
+#pragma unroll
+                    for (int m = 0; m < 3; ++m)
+                        f[m] = fma(g, hq[m * IH * TW + (r + (WIN - 1) - t) * TW + q], f[m]);
+                }
+                d += A.b * (f[0] + 2.0 * xv * f[1] + yv * f[2]);
+            }
+            A.d_pred[o] = d;
+        }
+    }
+    const double t = block_sum(l1, s_red);
+    if (tid == 0) A.partB[blockIdx.y * gridDim.x + blockIdx.x] = t;
+}
+
+// sums[0] = sum of SSIM over windows and channels, sums[1] = sum |x - y|
+__global__ void __launch_bounds__(kThreads) ssim_finish_kernel(const double *partA, int na,
+                                                               const double *partB, int nb,
+                                                               double *sums) {
+    __shared__ double s_red[kThreads / 32];
+    double a = 0.0, b = 0.0;
+    for (int i = threadIdx.x; i < na; i += kThreads) a += partA[i];
+    for (int i = threadIdx.x; i < nb; i += kThreads) b += partB[i];
+    const double ta = block_sum(a, s_red);
+    const double tb = block_sum(b, s_red);
+    if (threadIdx.x == 0) {
+        sums[0] = ta;
+        sums[1] = tb;
+    }
+}
+
+struct Plan {
+    int64_t maps;  // doubles per map
+    int na, nb;
+    size_t bytes;
+};
+
+inline Plan plan(int H, int W, int C) {
+    Plan p{};
+    const int Hv = H - WIN + 1 > 0 ? H - WIN + 1 : 0, Wv = W - WIN + 1 > 0 ? W - WIN + 1 : 0;
+    p.maps = (int64_t)C * Hv * Wv;
+    p.na = ((Wv + TW - 1) / TW) * ((Hv + TH - 1) / TH);
+    p.nb = ((W + TW - 1) / TW) * ((H + TH - 1) / TH);
+    p.bytes = 8 * (size_t)(3 * p.maps + p.na + p.nb + 2);
+    return p;
+}
+
+}  // namespace ssimk
+}  // namespace ivr
+
+extern "C" size_t ivr_photometric_workspace_size(int32_t height, int32_t width, int32_t channels) {
+    return ivr::ssimk::plan(height, width, channels).bytes;
+}
+
+extern "C" int ivr_photometric_loss(const double *pred, const double *gt, int32_t height,
+                                    int32_t width, int32_t channels, const double window[11],
+                                    double a, double b, int32_t with_ssim, double *d_pred,
+                                    double *sums, void *workspace, size_t workspace_bytes,
+                                    ivr_stream_t stream) {
+    using namespace ivr;
+    using namespace ivr::ssimk;
+    if (!pred || !gt || !d_pred || !sums || !window || height < 1 || width < 1 || channels < 1 ||
+        (with_ssim && (height < WIN || width < WIN))) {
+        set_error("ivr_photometric_loss: bad argument (images smaller than the 11x11 window?)");
+        return IVR_ERR_ARG;
+    }
+    const Plan p = plan(height, width, channels);
+    if (!workspace || workspace_bytes < p.bytes) {
+        set_error("ivr_photometric_loss: workspace too small");
+        return IVR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    Args A{};
+    A.x = pred;
+    A.y = gt;
+    A.H = height;
+    A.W = width;
+    A.C = channels;
+    A.Hv = height - WIN + 1;
+    A.Wv = width - WIN + 1;
+    for (int t = 0; t < WIN; ++t) A.g[t] = window[t];
+    A.up = with_ssim ? 1.0 / ((double)A.Hv * A.Wv * channels) : 0.0;
+    A.a = a;
+    A.b = b;
+    double *ws = (double *)workspace;
+    A.m_ux = ws;
+    A.m_uxx = ws + p.maps;
+    A.m_uxy = ws + 2 * p.maps;
+    A.partA = ws + 3 * p.maps;
+    A.partB = A.partA + p.na;
+    A.d_pred = d_pred;
+    const size_t smA = 8 * (size_t)(2 * IH * IW + 5 * IH * TW);
+    const size_t smB = 8 * (size_t)(3 * IH * IW + 3 * IH * TW);
+    int na = 0;
+    if (with_ssim) {
+        cudaFuncSetAttribute(ssim_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
+        const dim3 gA((A.Wv + TW - 1) / TW, (A.Hv + TH - 1) / TH);
+        ssim_window_kernel<<<gA, kThreads, smA, st>>>(A);
+        na = p.na;
+        cudaFuncSetAttribute(ssim_grad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
+    }
+    const dim3 gB((width + TW - 1) / TW, (height + TH - 1) / TH);
+    if (with_ssim)
+        ssim_grad_kernel<true><<<gB, kThreads, smB, st>>>(A);
+    else
+        ssim_grad_kernel<false><<<gB, kThreads, 0, st>>>(A);
+    ssim_finish_kernel<<<1, kThreads, 0, st>>>(A.partA, na, A.partB, p.nb, sums);
+    return check_launch("ivr_photometric_loss");
+}

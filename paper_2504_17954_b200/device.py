@@ -298,6 +298,7 @@ def blend_backward(F: Frame, d_out, stream=None):
                                   ptr(F.values), ptr(F.rec64), K, cam.width, cam.height, ptr(out),
                                   ptr(F.last_pos), ptr(d_out), ptr(g["values"]), ptr(g["mean2d"]),
                                   ptr(g["conic"]), ptr(g["opacity"]),
+                                  ptr(getattr(F, "tile_order", None)),
                                   L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0,
                                   stream_handle(stream)), "ivr_blend_bwd")
     return g

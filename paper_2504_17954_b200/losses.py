@@ -1,14 +1,15 @@
 """Training / fitting objectives on the GPU (drop-in for voxsplat/losses.py).
 
 Every function takes numpy arrays or CUDA tensors, computes in float64 on the
-device with torch ops (separable Gaussian SSIM windows as conv2d; these are
-library ops -- the hot path's own kernels are K1-K4), and returns the
-reference's (loss, gradient) pairs with the analytic gradients of
-losses.py:45-268.  Inputs given as numpy come back as numpy.
+device and returns the reference's (loss, gradient) pairs with the analytic
+gradients of losses.py:45-268.  L1 + SSIM (value and gradient) run in two
+fused tiled kernels (csrc/ssim.cu); the small regularizers are torch ops.
+Inputs given as numpy come back as numpy.
 """
 
 from __future__ import annotations
 
+import ctypes
 from dataclasses import dataclass
 
 import numpy as np
@@ -57,59 +58,48 @@ def _out(ref, t):
     return t if isinstance(ref, torch.Tensor) else t.cpu().numpy()
 
 
-_KCACHE = {}
+_WS = {}
 
 
-def _kern(device):
-    k = _KCACHE.get(device)
-    if k is None:
-        k1 = torch.from_numpy(_K1D).to(device)
-        k = (k1.view(1, 1, -1, 1), k1.view(1, 1, 1, -1))
-        _KCACHE[device] = k
-    return k
+def _window_ptr():
+    w = np.ascontiguousarray(_K1D, dtype=np.float64)
+    return w, w.ctypes.data_as(ctypes.POINTER(ctypes.c_double))
 
 
-def _filt(img, full):
-    """Separable 11x11 Gaussian window; img (C,H,W); 'valid' or its adjoint
-    'full' (losses.py:45-54)."""
-    kv, kh = _kern(img.device)
-    x = img.unsqueeze(1)
-    r = SSIM_RADIUS * 2
-    if full:
-        x = torch.nn.functional.conv2d(x, kv, padding=(r, 0))
-        x = torch.nn.functional.conv2d(x, kh, padding=(0, r))
-    else:
-        x = torch.nn.functional.conv2d(x, kv)
-        x = torch.nn.functional.conv2d(x, kh)
-    return x.squeeze(1)
+def _photometric_dev(x, y, a, b, with_ssim):
+    """csrc/ssim.cu on (H, W, C) float64 device tensors: returns
+    (sums = [sum of SSIM over windows and channels, sum |x - y|],
+    d = a * sign(x - y) + b * d(mean SSIM)/dx)."""
+    from . import _lib as L
+    from . import device as D
+    x, y = x.contiguous(), y.contiguous()
+    h, w, nc = x.shape
+    nbytes = L.lib().ivr_photometric_workspace_size(h, w, nc)
+    key = (x.device, nbytes)
+    ws = _WS.get(key)
+    if ws is None:
+        ws = _WS[key] = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=x.device)
+    d = torch.empty_like(x)
+    sums = torch.empty(2, dtype=torch.float64, device=x.device)
+    keep, wp = _window_ptr()
+    L.check(L.lib().ivr_photometric_loss(D.ptr(x), D.ptr(y), h, w, nc, wp, float(a), float(b),
+                                         1 if with_ssim else 0, D.ptr(d), D.ptr(sums), D.ptr(ws),
+                                         nbytes, D.stream_handle()), "ivr_photometric_loss")
+    del keep
+    return sums, d
 
 
 def ssim_t(x, y):
-    """Mean SSIM over channels and its gradient w.r.t. x (torch float64;
-    x, y (H, W, C))."""
+    """Mean SSIM over channels and its gradient w.r.t. x (float64 device
+    tensors (H, W, C)); one fused window pass + one adjoint pass (csrc/ssim.cu)."""
     if x.shape != y.shape:
         raise ShapeMismatch(f"ssim inputs differ: {tuple(x.shape)} vs {tuple(y.shape)}")
     h, w, nc = x.shape
     win = 2 * SSIM_RADIUS + 1
     if h < win or w < win:
         raise ShapeMismatch(f"image {h}x{w} smaller than the {win}x{win} ssim window")
-    X, Y = x.permute(2, 0, 1), y.permute(2, 0, 1)
-    ux, uy = _filt(X, False), _filt(Y, False)
-    uxx, uyy, uxy = _filt(X * X, False), _filt(Y * Y, False), _filt(X * Y, False)
-    vx, vy, vxy = uxx - ux * ux, uyy - uy * uy, uxy - ux * uy
-    a1, a2 = 2.0 * ux * uy + SSIM_C1, 2.0 * vxy + SSIM_C2
-    b1, b2 = ux * ux + uy * uy + SSIM_C1, vx + vy + SSIM_C2
-    s = (a1 * a2) / (b1 * b2)
-    value = s.mean(dim=(1, 2)).sum() / nc
-    n_valid = (h - win + 1) * (w - win + 1)
-    up = 1.0 / (n_valid * nc)
-    da1, da2 = a2 / (b1 * b2) * up, a1 / (b1 * b2) * up
-    db1, db2 = -s / b1 * up, -s / b2 * up
-    d_uxy = 2.0 * da2
-    d_uxx = db2
-    d_ux = 2.0 * uy * da1 + 2.0 * ux * db1 - 2.0 * ux * db2 - uy * d_uxy
-    dX = _filt(d_ux, True) + 2.0 * X * _filt(d_uxx, True) + Y * _filt(d_uxy, True)
-    return value, dX.permute(1, 2, 0)
+    sums, d = _photometric_dev(x, y, 0.0, 1.0, True)
+    return sums[0] / float((h - win + 1) * (w - win + 1) * nc), d
 
 
 def ssim(x, y):
@@ -125,21 +115,26 @@ def ssim(x, y):
 
 
 def photometric_loss_t(pred, gt, weights=None):
-    """0.8 L1 + 0.2 (1 - SSIM) on device tensors; returns (loss tensor, d_pred)."""
+    """0.8 L1 + 0.2 (1 - SSIM) on device tensors; returns (loss tensor, d_pred).
+    L1, SSIM and both gradients come from the fused kernels (csrc/ssim.cu)."""
     weights = weights or LossWeights()
     if pred.shape != gt.shape:
         raise ShapeMismatch(f"prediction {tuple(pred.shape)} vs ground truth {tuple(gt.shape)}")
-    diff = pred - gt
-    loss = weights.l1_weight * diff.abs().mean()
-    d = weights.l1_weight * torch.sign(diff) / diff.numel()
-    if weights.ssim_weight > 0.0:
-        s, ds = ssim_t(pred if pred.dim() == 3 else pred[..., None],
-                       gt if gt.dim() == 3 else gt[..., None])
-        if pred.dim() == 2:
-            ds = ds[..., 0]
+    x = pred if pred.dim() == 3 else pred[..., None]
+    y = gt if gt.dim() == 3 else gt[..., None]
+    h, w, nc = x.shape
+    win = 2 * SSIM_RADIUS + 1
+    with_ssim = weights.ssim_weight > 0.0
+    if with_ssim and (h < win or w < win):
+        raise ShapeMismatch(f"image {h}x{w} smaller than the {win}x{win} ssim window")
+    numel = x.numel()
+    sums, d = _photometric_dev(x.to(torch.float64), y.to(torch.float64),
+                               weights.l1_weight / numel, -weights.ssim_weight, with_ssim)
+    loss = weights.l1_weight * (sums[1] / numel)
+    if with_ssim:
+        s = sums[0] / float((h - win + 1) * (w - win + 1) * nc)
         loss = loss + weights.ssim_weight * (1.0 - s)
-        d = d - weights.ssim_weight * ds
-    return loss, d
+    return loss, (d if pred.dim() == 3 else d[..., 0])
 
 
 def photometric_loss(pred_rgba, gt_rgba, weights=None):
