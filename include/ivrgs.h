@@ -27,7 +27,7 @@ extern "C" {
 
 typedef struct CUstream_st *ivr_stream_t; /* == cudaStream_t */
 
-#define IVR_ABI_VERSION 1
+#define IVR_ABI_VERSION 2
 #define IVR_TILE 16 /* rasterizer.py:24 TILE_SIZE */
 
 typedef enum ivr_status {
@@ -258,8 +258,10 @@ int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *shading,
 /* K5: VQ assignment, vq.assign_nearest (vq.py:90-96): index of the nearest
  * sorted centroid = searchsorted(mids, v, 'left'); NaN -> K-1.
  * Output uint16 (K <= 65536). */
+size_t ivr_vq_assign_workspace_size(void);
 int ivr_vq_assign(const double *values, int64_t n, const double *centroids,
-                  int32_t k, uint16_t *indices, ivr_stream_t stream);
+                  int32_t k, uint16_t *indices, void *workspace, size_t workspace_bytes,
+                  ivr_stream_t stream);
 
 /* K6: codebook decode, Codebook.decode (vq.py:128-134).  bad[0] (device,
  * caller-initialised to -1) receives the largest index >= k, if any; those

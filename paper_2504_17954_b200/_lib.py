@@ -115,7 +115,9 @@ _SIGS = {
     "ivr_bin_sort_cull": ([ctypes.c_int64, P, P, P, P, ctypes.c_int32, ctypes.c_int32,
                            ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P, ctypes.c_size_t, P,
                            P, P, P], ctypes.c_int),
-    "ivr_vq_assign": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P], ctypes.c_int),
+    "ivr_vq_assign_workspace_size": ([], ctypes.c_size_t),
+    "ivr_vq_assign": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P, ctypes.c_size_t, P],
+                      ctypes.c_int),
     "ivr_vq_decode": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P, P], ctypes.c_int),
     "ivr_sh_eval": ([ctypes.c_int64, ctypes.c_int32, P, P, ctypes.POINTER(ctypes.c_double), P, P],
                     ctypes.c_int),

@@ -6,97 +6,208 @@
 // codeword search in 1-D is a binary search, not a distance GEMM: there is no
 // contraction dimension to put on tensor cores (SURVEY.md finding 5), so
 // these kernels are HBM-bound (6 B per value in + out).  Midpoints live in
-// shared memory (K=4096 -> 32 KB); ~12 compares per value.
+// shared memory (K=4096 -> 32 KB) next to a uniform bucket table that cuts
+// the search to ~2 compares per value.
 #include "ivr_common.cuh"
 
 namespace ivr {
 
 constexpr int kVqThreads = 256;
-constexpr int kVqSmemMids = 6144;  // 48 KB of float64 midpoints
+constexpr int kVqSmemMids = 4096;  // 32 KB of float64 midpoints (+16 KB bucket table)
+constexpr int kLut = 8192;         // uniform buckets over [mid_0, mid_last]
+
+__device__ __forceinline__ double vq_mid(const double *c, int i) { return 0.5 * (c[i + 1] + c[i]); }
+
+// lut[b] = number of midpoints < lo + b * w  (b < kLut); params = {lo, w, inv_w}
+__global__ void __launch_bounds__(kVqThreads)
+vq_lut_kernel(const double *__restrict__ cents, int k, uint16_t *lut, double *params) {
+    const int nm = k - 1;
+    const double lo = vq_mid(cents, 0), hi = vq_mid(cents, nm - 1);
+    const double w = (hi - lo) / kLut;
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        params[0] = lo;
+        params[1] = w;
+        params[2] = w > 0.0 ? 1.0 / w : 0.0;
+    }
+    const int b = blockIdx.x * kVqThreads + threadIdx.x;
+    if (b >= kLut) return;
+    const double e = lo + (double)b * w;
+    int a = 0, z = nm;  // count of mids < e
+    while (a < z) {
+        const int m = (a + z) >> 1;
+        if (vq_mid(cents, m) < e) a = m + 1;
+        else z = m;
+    }
+    lut[b] = (uint16_t)a;
+}
+
+// searchsorted(mids, v, 'left') = number of mids < v.  A uniform bucket table
+// narrows the interval to the mids between the edges of the neighbouring
+// buckets (typically 0-3 mids); the answer is then checked against the
+// interval ends with exact float64 compares and, if a rounding corner case
+// put v outside the interval, recomputed by a full binary search.  Midpoints
+// and the table live in shared memory.
+__device__ __forceinline__ int vq_full_search(const double *mid, int nm, double v) {
+    int a = 0, z = nm;
+    while (a < z) {
+        const int m = (a + z) >> 1;
+        if (mid[m] < v) a = m + 1;
+        else z = m;
+    }
+    return a;
+}
 
 template <bool SMEM>
 __global__ void __launch_bounds__(kVqThreads)
 vq_assign_kernel(const double *__restrict__ values, int64_t n, const double *__restrict__ cents,
-                 int k, uint16_t *__restrict__ out) {
+                 int k, const uint16_t *__restrict__ lut, const double *__restrict__ params,
+                 uint16_t *__restrict__ out) {
     __shared__ double s_mid[SMEM ? kVqSmemMids : 1];
+    __shared__ uint16_t s_lut[SMEM ? kLut : 1];
+    const int nm = k - 1;
     if (SMEM) {
-        for (int i = threadIdx.x; i < k - 1; i += kVqThreads)
-            s_mid[i] = 0.5 * (cents[i + 1] + cents[i]);
+        for (int i = threadIdx.x; i < nm; i += kVqThreads) s_mid[i] = vq_mid(cents, i);
+        for (int i = threadIdx.x; i < kLut; i += kVqThreads) s_lut[i] = lut[i];
         __syncthreads();
     }
-    // searchsorted(mids, v, 'left') = number of mids < v.  Fixed-trip-count
-    // binary search over kVqIlp independent values per thread, interleaved so
-    // the shared-memory loads of different values overlap (the search is
-    // latency-bound, not bandwidth-bound).
-    const int nm = k - 1;
-    int top = 1;
-    while ((top << 1) <= nm) top <<= 1;
+    const double lo = params[0], inv_w = params[2];
+    const bool use_lut = SMEM && inv_w > 0.0;
     constexpr int kVqIlp = 8;
     const int64_t chunk = (int64_t)kVqThreads * kVqIlp;
     for (int64_t base = (int64_t)blockIdx.x * chunk; base < n; base += (int64_t)gridDim.x * chunk) {
         double v[kVqIlp];
-        int pos[kVqIlp];
 #pragma unroll
         for (int r = 0; r < kVqIlp; ++r) {
             const int64_t i = base + r * kVqThreads + threadIdx.x;
-            v[r] = i < n ? values[i] : 0.0;
-            pos[r] = 0;
+            v[r] = i < n ? __ldcs(values + i) : 0.0;
         }
-        for (int step = top; step > 0; step >>= 1) {
 #pragma unroll
-            for (int r = 0; r < kVqIlp; ++r) {
-                const int m = pos[r] + step;
-                if (m <= nm) {
-                    const double mid = SMEM ? s_mid[m - 1]
-                                            : 0.5 * (__ldg(cents + m) + __ldg(cents + m - 1));
-                    if (mid < v[r]) pos[r] = m;
+        for (int r = 0; r < kVqIlp; ++r) {
+            const int64_t i = base + r * kVqThreads + threadIdx.x;
+            if (i >= n) continue;
+            int pos;
+            if (v[r] != v[r]) {
+                pos = nm;  // NaN sorts last
+            } else if (SMEM) {
+                if (use_lut) {
+                    const double t = (v[r] - lo) * inv_w;
+                    const int b = t < 0.0 ? 0 : (t >= (double)(kLut - 1) ? kLut - 1 : (int)t);
+                    int a = b >= 1 ? s_lut[b - 1] : 0;
+                    const int zi = b + 2 < kLut ? s_lut[b + 2] : nm;
+                    int z = zi;
+                    const int a0 = a;
+                    while (a < z) {
+                        const int m = (a + z) >> 1;
+                        if (s_mid[m] < v[r]) a = m + 1;
+                        else z = m;
+                    }
+                    pos = a;
+                    const bool ok_lo = pos > a0 || a0 == 0 || s_mid[a0 - 1] < v[r];
+                    const bool ok_hi = pos < zi || zi == nm || !(s_mid[zi] < v[r]);
+                    if (!(ok_lo && ok_hi)) pos = vq_full_search(s_mid, nm, v[r]);
+                } else {
+                    pos = vq_full_search(s_mid, nm, v[r]);
                 }
+            } else {
+                int a = 0, z = nm;
+                while (a < z) {
+                    const int m = (a + z) >> 1;
+                    if (0.5 * (__ldg(cents + m + 1) + __ldg(cents + m)) < v[r]) a = m + 1;
+                    else z = m;
+                }
+                pos = a;
             }
-        }
-#pragma unroll
-        for (int r = 0; r < kVqIlp; ++r) {
-            const int64_t i = base + r * kVqThreads + threadIdx.x;
-            if (i < n) out[i] = (uint16_t)(v[r] != v[r] ? nm : pos[r]);  // NaN sorts last
+            __stcs(out + i, (uint16_t)pos);
         }
     }
 }
 
+// 8 indices per thread per step: one 16-byte load, four 16-byte stores; the
+// codebook is gathered from shared memory (K <= kVqSmemMids + 1)
+template <bool SMEM>
 __global__ void __launch_bounds__(kVqThreads)
 vq_decode_kernel(const uint16_t *__restrict__ idx, int64_t n, const double *__restrict__ cents,
                  int k, double *__restrict__ out, long long *bad) {
-    for (int64_t i = (int64_t)blockIdx.x * kVqThreads + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * kVqThreads) {
-        const int j = idx[i];
-        if (j >= k) {
-            atomicMax(bad, (long long)j);
-            out[i] = 0.0;
-        } else {
-            out[i] = __ldg(cents + j);
+    __shared__ double s_c[SMEM ? kVqSmemMids + 1 : 1];
+    if (SMEM) {
+        for (int i = threadIdx.x; i < k; i += kVqThreads) s_c[i] = cents[i];
+        __syncthreads();
+    }
+    const double *tab = SMEM ? s_c : cents;
+    const int64_t nv = n / 8;
+    const bool aligned = ((reinterpret_cast<uintptr_t>(idx) & 15) == 0) &&
+                         ((reinterpret_cast<uintptr_t>(out) & 15) == 0);
+    const int64_t stride = (int64_t)gridDim.x * kVqThreads;
+    int worst = -1;
+    if (aligned) {
+        for (int64_t t = (int64_t)blockIdx.x * kVqThreads + threadIdx.x; t < nv; t += stride) {
+            const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(idx) + t);
+            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
+            double2 *o = reinterpret_cast<double2 *>(out + 8 * t);
+#pragma unroll
+            for (int p = 0; p < 4; ++p) {
+                const int j0 = (int)(w[p] & 0xffffu), j1 = (int)(w[p] >> 16);
+                if (j0 >= k) worst = max(worst, j0);
+                if (j1 >= k) worst = max(worst, j1);
+                const double d0 = j0 < k ? tab[j0] : 0.0;
+                const double d1 = j1 < k ? tab[j1] : 0.0;
+                __stcs(o + p, make_double2(d0, d1));
+            }
         }
     }
+    for (int64_t i = (aligned ? 8 * nv : 0) + (int64_t)blockIdx.x * kVqThreads + threadIdx.x; i < n;
+         i += stride) {
+        const int j = idx[i];
+        if (j >= k) worst = max(worst, j);
+        out[i] = j < k ? tab[j] : 0.0;
+    }
+    if (worst >= 0) atomicMax(bad, (long long)worst);
 }
 
 static int grid_for(int64_t n) {
+    // persistent-style grid: ~4 CTAs per SM, each staging its tables once
     int64_t b = (n + kVqThreads - 1) / kVqThreads;
-    const int64_t cap = 148 * 16;
+    const int64_t cap = 148 * 4;
     return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
 }  // namespace ivr
 
+extern "C" size_t ivr_vq_assign_workspace_size(void) {
+    return 4 * sizeof(double) + 2 * (size_t)ivr::kLut;
+}
+
 extern "C" int ivr_vq_assign(const double *values, int64_t n, const double *centroids, int32_t k,
-                             uint16_t *indices, ivr_stream_t stream) {
+                             uint16_t *indices, void *workspace, size_t workspace_bytes,
+                             ivr_stream_t stream) {
     using namespace ivr;
     if (n < 0 || k < 1 || k > 65536 || (n > 0 && (!values || !centroids || !indices))) {
         set_error("ivr_vq_assign: bad argument");
         return IVR_ERR_ARG;
     }
     if (n == 0) return IVR_OK;
+    if (k == 1) {  // a single centroid: every index is 0
+        if (cudaMemsetAsync(indices, 0, 2 * (size_t)n, (cudaStream_t)stream) != cudaSuccess)
+            return check_launch("ivr_vq_assign memset");
+        return IVR_OK;
+    }
     cudaStream_t st = (cudaStream_t)stream;
-    if (k - 1 <= kVqSmemMids)
-        vq_assign_kernel<true><<<grid_for(n), kVqThreads, 0, st>>>(values, n, centroids, k, indices);
-    else
-        vq_assign_kernel<false><<<grid_for(n), kVqThreads, 0, st>>>(values, n, centroids, k, indices);
+    if (!workspace || workspace_bytes < ivr_vq_assign_workspace_size()) {
+        set_error("ivr_vq_assign: workspace too small");
+        return IVR_ERR_ARG;
+    }
+    double *params = reinterpret_cast<double *>(workspace);
+    uint16_t *lut = reinterpret_cast<uint16_t *>(params + 4);
+    if (k - 1 <= kVqSmemMids) {
+        vq_lut_kernel<<<(kLut + kVqThreads - 1) / kVqThreads, kVqThreads, 0, st>>>(centroids, k, lut,
+                                                                                  params);
+        vq_assign_kernel<true><<<grid_for(n), kVqThreads, 0, st>>>(values, n, centroids, k, lut,
+                                                                   params, indices);
+    } else {
+        cudaMemsetAsync(params, 0, 4 * sizeof(double), st);
+        vq_assign_kernel<false><<<grid_for(n), kVqThreads, 0, st>>>(values, n, centroids, k, lut,
+                                                                    params, indices);
+    }
     return check_launch("vq_assign_kernel");
 }
 
@@ -108,7 +219,11 @@ extern "C" int ivr_vq_decode(const uint16_t *indices, int64_t n, const double *c
         return IVR_ERR_ARG;
     }
     if (n == 0) return IVR_OK;
-    vq_decode_kernel<<<grid_for(n), kVqThreads, 0, (cudaStream_t)stream>>>(
-        indices, n, centroids, k, out, reinterpret_cast<long long *>(bad));
+    if (k <= kVqSmemMids + 1)
+        vq_decode_kernel<true><<<grid_for(n), kVqThreads, 0, (cudaStream_t)stream>>>(
+            indices, n, centroids, k, out, reinterpret_cast<long long *>(bad));
+    else
+        vq_decode_kernel<false><<<grid_for(n), kVqThreads, 0, (cudaStream_t)stream>>>(
+            indices, n, centroids, k, out, reinterpret_cast<long long *>(bad));
     return check_launch("vq_decode_kernel");
 }

@@ -32,9 +32,16 @@ def assign_device(values_dev, centroids_dev):
     n = values_dev.numel()
     k = centroids_dev.numel()
     out = torch.empty(n, dtype=torch.int16, device=values_dev.device)
+    nb = L.lib().ivr_vq_assign_workspace_size()
+    ws = _WS.get(values_dev.device)
+    if ws is None:
+        ws = _WS[values_dev.device] = torch.empty(nb, dtype=torch.uint8, device=values_dev.device)
     L.check(L.lib().ivr_vq_assign(D.ptr(values_dev), n, D.ptr(centroids_dev), k, D.ptr(out),
-                                  D.stream_handle()), "ivr_vq_assign")
+                                  D.ptr(ws), nb, D.stream_handle()), "ivr_vq_assign")
     return out
+
+
+_WS = {}
 
 
 def decode_device(idx_dev, centroids_dev):

@@ -32,6 +32,32 @@ def test_assign_large_vs_oracle():
         assert np.array_equal(assign_nearest(v, c), O.vq_assign(v, c)), k
 
 
+def test_assign_bucket_table_corner_cases():
+    """Clustered codebooks, values exactly on midpoints and bucket edges, a
+    huge offset with tiny spacing (bucket index rounding), +-inf and NaN."""
+    import oracle as O
+    from paper_2504_17954_b200.vq import assign_nearest
+    rng = np.random.default_rng(3)
+    cases = []
+    c = np.sort(np.concatenate([rng.normal(0, 1e-6, 3000), rng.normal(5, 2, 1000)]))
+    mids = 0.5 * (c[1:] + c[:-1])
+    v = np.concatenate([rng.normal(0, 1e-6, 50_000), rng.normal(5, 3, 50_000), mids,
+                        np.nextafter(mids, np.inf), np.nextafter(mids, -np.inf),
+                        [np.inf, -np.inf, np.nan, 1e300, -1e300, 0.0, -0.0]])
+    cases.append((c, v))
+    c2 = np.sort(1e6 + np.arange(4096) * 1e-9 + rng.uniform(0, 1e-10, 4096))
+    m2 = 0.5 * (c2[1:] + c2[:-1])
+    lo, hi = m2[0], m2[-1]
+    edges = lo + np.arange(8192) * ((hi - lo) / 8192)
+    v2 = np.concatenate([m2, edges, np.nextafter(edges, np.inf), np.nextafter(edges, -np.inf),
+                         rng.uniform(c2[0] - 1e-6, c2[-1] + 1e-6, 100_000)])
+    cases.append((c2, v2))
+    c3 = np.array([-1.0, -1.0, 0.0, 0.0, 0.0, 3.0])  # duplicate centroids
+    cases.append((c3, np.array([-2.0, -1.0, -0.5, 0.0, 1.5, 3.0, 9.0])))
+    for c, v in cases:
+        assert np.array_equal(assign_nearest(v, c), O.vq_assign(v, c))
+
+
 def test_decode_and_corrupt_index():
     from paper_2504_17954_b200 import CorruptIndex
     from paper_2504_17954_b200.vq import Codebook
