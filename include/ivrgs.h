@@ -198,6 +198,11 @@ int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_splat,
                   int32_t *contrib, int32_t *last_pos, double *t_final,
                   const int32_t *tile_order, int32_t flags, ivr_stream_t stream);
 
+/* Debug only (not for concurrent use): record {tile, smid, t_start, t_end}
+ * (ns) per (tile, 8x4 block) of later ivr_blend_fwd calls into buf
+ * (ntiles * 8 * 4 int64 device memory); NULL stops recording. */
+void ivr_debug_blend_trace(long long *buf);
+
 /* Heaviest-first tile launch order for ivr_blend_fwd (counting sort on
  * half-octave buckets of the per-tile pair count, descending).  Scheduling
  * only: any permutation yields identical images. */

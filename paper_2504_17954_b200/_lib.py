@@ -105,6 +105,7 @@ _SIGS = {
                        ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_int32, P],
                       ctypes.c_int),
     "ivr_tile_order": ([P, ctypes.c_int32, P, P], ctypes.c_int),
+    "ivr_debug_blend_trace": ([P], None),
     "ivr_blend_bwd": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
                        ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, P, ctypes.c_int32, P],
                       ctypes.c_int),

@@ -115,6 +115,7 @@ struct BlendArgs {
     double *t_final;
     const int32_t *tile_order;
     int preculled;
+    long long *trace;  // debug: per (tile, block) {tile, smid, t0, t1} (globaltimer), or null
 };
 
 template <int KMAX, bool F64>
@@ -151,7 +152,7 @@ struct WarpSlots {
     double v64[(F64 && MODE == kModeExact) ? 32 * KMAX : 1];
 };
 
-// One warp = one 16x2 strip of the tile.  The warp streams the tile's pair
+// One warp = one 8x4 pixel block of the tile.  The warp streams the tile's pair
 // list in chunks of 32 (one pair per lane): load id + record, cull against the
 // strip rectangle (rigorous float32 bound), stash survivors in its own shared
 // slots, then every lane walks the survivors in list order for its pixel.
@@ -337,9 +338,22 @@ blend_fwd_kernel(BlendArgs A) {
     const int sx1 = min(sx0 + kWarpW - 1, A.W - 1);
     const int sy0 = min(sy_raw, A.H - 1), sy1 = min(sy_raw + kWarpH - 1, A.H - 1);
 
+    long long t_start = 0;
+    if (A.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     PixelState<KMAX, F64> st;
     st.reset(s0, !inside);
     warp_walk<KMAX, F64, MODE, kModeExact>(A, W, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
+    if (A.trace && lane == 0) {
+        long long t_end;
+        int sm_;
+        asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_end));
+        asm volatile("mov.u32 %0, %%smid;" : "=r"(sm_));
+        long long *tr = A.trace + 4 * ((int64_t)tile * 8 + warp);
+        tr[0] = tile;
+        tr[1] = sm_;
+        tr[2] = t_start;
+        tr[3] = t_end;
+    }
     bool exact_out = MODE == kModeExact;
     if (MODE == kModeFast) {
         // pixels whose T landed in the ambiguity band: one EXACT re-walk (per warp)
@@ -423,6 +437,15 @@ tile_order_kernel(const int32_t *ranges, int ntiles, int32_t *order) {
 
 }  // namespace ivr
 
+namespace {
+long long *g_blend_trace = nullptr;  // debug hook only (tools/blend_trace.py)
+}
+
+// Debug: record {tile, smid, t_start, t_end} (ns, %globaltimer) per (tile,
+// 8x4 block) of subsequent ivr_blend_fwd calls into buf (ntiles * 8 * 4
+// int64), or stop with NULL.  Not for concurrent use.
+extern "C" void ivr_debug_blend_trace(long long *buf) { g_blend_trace = buf; }
+
 extern "C" int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_t *order,
                               ivr_stream_t stream) {
     using namespace ivr;
@@ -470,6 +493,7 @@ extern "C" int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_spl
     A.t_final = t_final;
     A.tile_order = tile_order;
     A.preculled = (flags & IVR_BLEND_PRECULLED) != 0 ? 1 : 0;
+    A.trace = g_blend_trace;
     const bool exact = (flags & IVR_BLEND_EXACT) != 0;
     const int nt = ntx * nty;
 #define IVR_BLEND(KM)                                                                   \
