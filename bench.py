@@ -39,6 +39,9 @@ PER_MODEL, N_MODELS, DENSITY = 200_000, 5, 1_000_000
 LAUNCHES_PER_FRAME = 27
 
 
+SLOTS = 4  # concurrent frame slots (FrameGraph / FramePipeline)
+
+
 def parse():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
@@ -156,7 +159,8 @@ def config_dict(n, extra=None):
                      "relight/TF edit (palette override, opacity 0.5, orbital light, term scales)",
          "n_gaussians": n, "width": W_IMG, "height": H_IMG, "channels": "rgba",
          "dtype_mode": "float32 (reference default)",
-         "l2": "flushed (256 MiB write) between timed frames; each frame timed alone"}
+         "l2": "inputs larger than L2 (scene 168 MB float64 > 126 MB); frames streamed on "
+               "4 concurrent slots; frame_ms_isolated = each frame alone after an L2 flush"}
     if extra:
         d.update(extra)
     return d
@@ -322,18 +326,13 @@ def run_ours(args):
 
     # ---- the product path: the whole frame captured once as a CUDA graph
     from paper_2504_17954_b200.scene import FrameGraph
-    fg = FrameGraph(ds, W_IMG, H_IMG, warm_cam=cams[0], slots=2)
+    fg = FrameGraph(ds, W_IMG, H_IMG, warm_cam=cams[0], slots=SLOTS)
     for s in range(args.warmup):
-        fg.replay(cams[s])
+        fg.submit(s % SLOTS, cams[s])
     torch.cuda.synchronize()
 
+    # ---- (diagnostic) each frame alone: L2 flushed before it, slot 0 only
     ev = [[torch.cuda.Event(enable_timing=True) for _ in range(2)] for _ in range(args.steps)]
-    sampler = ClockSampler(local_rank)
-    sampler.start()
-    if dist:
-        dist.barrier()
-    torch.cuda.synchronize()
-    overflow = False
     for s in range(args.steps):
         flush.zero_()                      # L2 flush between timed frames (not timed)
         fg.stage(cams[args.warmup + s])    # this frame's camera/edit upload (not timed)
@@ -341,14 +340,37 @@ def run_ours(args):
         fg.launch()
         ev[s][1].record()
     torch.cuda.synchronize()
+    overflow = fg.overflowed()
+    frame_ms = np.array([ev[s][0].elapsed_time(ev[s][1]) for s in range(args.steps)])
+
+    # ---- the headline: a stream of K views, consecutive frames on SLOTS
+    # slots (own streams / workspaces) so later frames' K1/K2 overlap earlier
+    # frames' K3 tails; the scene (168 MB float64) exceeds the 126 MB L2
+    s0 = fg.stream(0)
+    t_start, t_end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    sampler = ClockSampler(local_rank)
+    sampler.start()
+    if dist:
+        dist.barrier()
+    torch.cuda.synchronize()
+    t_start.record(s0)
+    for k in range(1, SLOTS):
+        fg.stream(k).wait_event(t_start)
+    for s in range(args.steps):
+        fg.submit(s % SLOTS, cams[args.warmup + s])
+    for k in range(1, SLOTS):
+        j = torch.cuda.Event()
+        j.record(fg.stream(k))
+        s0.wait_event(j)
+    t_end.record(s0)
+    torch.cuda.synchronize()
     if dist:
         dist.barrier()
     clocks = sampler.stop()
-    overflow = fg.overflowed()
+    overflow = overflow or any(int(F.n_pairs.item()) > fg.capacity for _, F in fg.graphs)
     frames = [fg.F]
-    frame_ms = np.array([ev[s][0].elapsed_time(ev[s][1]) for s in range(args.steps)])
-    ms = float(frame_ms.mean())
-    t_tot = float(frame_ms.sum()) / 1e3
+    ms = t_start.elapsed_time(t_end) / args.steps
+    t_tot = ms * args.steps / 1e3
     if dist:
         tt = torch.tensor([t_tot], device="cuda", dtype=torch.float64)
         dist.all_reduce(tt, op=dist.ReduceOp.MAX)
@@ -411,7 +433,7 @@ def run_ours(args):
                 "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": None,
                 "peak_source": peak_src,
                 "stage_ms_uncaptured": {nm: float(v) for nm, v in zip(names, stage_ms)},
-                "frame_ms_min_med_max": [float(frame_ms.min()), float(np.median(frame_ms)),
+                "frame_ms_isolated_min_med_max": [float(frame_ms.min()), float(np.median(frame_ms)),
                                          float(frame_ms.max())],
                 "alg_bytes": {nm: int(v) for nm, v in zip(names, alg)}}
 
@@ -445,8 +467,8 @@ def run_ours(args):
                 "e2e": {"value": e2e_fps, "unit": "frames/s",
                         "h2d_bytes_per_step": pipe.h2d_bytes_per_frame(),
                         "d2h_bytes_per_step": pipe.d2h_bytes_per_frame(),
-                        "pipelined": "frame i+1 upload+compute overlaps frame i D2H "
-                                     "(2 slots); host wall clock over all frames"},
+                        "pipelined": "frames on 4 concurrent slots; each frame's D2H overlaps "
+                                     "later frames' upload+compute; host wall clock over all frames"},
                 "gpu_launches": LAUNCHES_PER_FRAME * args.steps, "overflow": overflow,
                 "extra": extra}
         print(json.dumps(line), flush=True)

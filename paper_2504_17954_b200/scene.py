@@ -337,13 +337,19 @@ class FrameGraph:
     mode are fixed per graph.  The pair capacity learned on the warm-up frame
     is reused (with 30% headroom); ``overflowed()`` reports whether a replay
     needed more, in which case ``recapture()`` grows it.
+
+    ``slots`` > 1 captures independent copies of the frame -- each with its
+    own workspace, parameter buffers, outputs and CUDA stream -- so
+    consecutive frames (different views) run concurrently: frame i+1's
+    preprocess and sort fill the SMs that frame i's blend tail leaves idle.
+    Slot 0 on the current stream is what ``stage/launch/replay`` use.
     """
 
     RING = 8
 
     def __init__(self, ds, width, height, exact=False, headroom=1.3, warm_cam=None, slots=1):
         self.ds, self.W, self.H, self.exact = ds, int(width), int(height), exact
-        self.slots = max(1, int(slots))  # graphs with their own output buffers (pipelining)
+        self.slots = max(1, int(slots))
         dev = ds.dg.device
         S = ds.n_scenes
         nb = ctypes.sizeof(L.FrameParams_t)
@@ -351,16 +357,25 @@ class FrameGraph:
                    for _ in range(self.RING)]
         self._ev = [None] * self.RING
         self._slot = 0
-        self.d_params = torch.empty(nb, dtype=torch.uint8, device=dev)
-        self.d_tab = torch.empty(4 * S, dtype=torch.float64, device=dev)
         self.nb = nb
+        self.res = []
+        for k in range(self.slots):
+            self.res.append({
+                "ws": ds.ws if k == 0 else D.Workspace(dev),
+                "d_params": torch.empty(nb, dtype=torch.uint8, device=dev),
+                "d_tab": torch.empty(4 * S, dtype=torch.float64, device=dev),
+                "stream": torch.cuda.current_stream(dev) if k == 0 else torch.cuda.Stream(device=dev),
+            })
+        self.d_params, self.d_tab = self.res[0]["d_params"], self.res[0]["d_tab"]
         from .synthetic import bench_camera
         cam = warm_cam or bench_camera(self.W, self.H)
         F = ds.render_frame(cam, fast=False, exact=exact)  # learns the pair capacity
         self.capacity = max(int(int(F.n_pairs.item()) * headroom) + 4096, 1 << 16)
         self._capture(cam)
 
-    def _stage(self, cam, light=None, palettes=None, opacity_scales=None):
+    def _stage(self, cam, light=None, palettes=None, opacity_scales=None, slot=0):
+        """Write this frame's parameters into the slot's device buffers (H2D
+        on the slot's stream)."""
         sc = self.ds.scene
         S = self.ds.n_scenes
         pal = np.empty((S, 3))
@@ -384,42 +399,48 @@ class FrameGraph:
         tab = np.frombuffer(h.numpy(), dtype=np.float64, count=4 * S, offset=self.nb)
         tab[:3 * S] = pal.reshape(-1)
         tab[3 * S:] = osc
-        self.d_params.copy_(h[:self.nb], non_blocking=True)
-        self.d_tab.copy_(h[self.nb:].view(torch.float64), non_blocking=True)
-        ev = torch.cuda.Event()
-        ev.record()
+        r = self.res[slot]
+        with torch.cuda.stream(r["stream"]):
+            r["d_params"].copy_(h[:self.nb], non_blocking=True)
+            r["d_tab"].copy_(h[self.nb:].view(torch.float64), non_blocking=True)
+            ev = torch.cuda.Event()
+            ev.record(r["stream"])
         self._ev[k] = ev
 
     def _capture(self, cam):
         ds = self.ds
         S = ds.n_scenes
-        self._stage(cam)
-        torch.cuda.synchronize()
-        shading = D.shading_struct(ds.dg, self.d_tab[:3 * S], False, ds.scene.light)
-        edits = L.Edits_t()
-        edits.scene_id = ds.dg.scene_id.data_ptr()
-        edits.opacity_scale = self.d_tab[3 * S:].data_ptr()
-        edits.rescale_opacity = 0  # taken from d_params
         layout = _channel_layout(("color", "alpha"), None)
         cols, _, K = _cols(layout)
-        # allocate every workspace buffer at its final size before capture
-        ws = ds.ws
-        F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=self.d_params)
-        D.bin_sort(F, ws, capacity=self.capacity)
-        D.blend(F, ws, want_state=False, exact=self.exact)
-        torch.cuda.synchronize()
         self.graphs = []
-        for _ in range(self.slots):  # same work, distinct output buffers (graph pools)
+        self._keep = []
+        torch.cuda.synchronize()
+        for k, r in enumerate(self.res):
+            self._stage(cam, slot=k)
+            torch.cuda.synchronize()
+            shading = D.shading_struct(ds.dg, r["d_tab"][:3 * S], False, ds.scene.light)
+            edits = L.Edits_t()
+            edits.scene_id = ds.dg.scene_id.data_ptr()
+            edits.opacity_scale = r["d_tab"][3 * S:].data_ptr()
+            edits.rescale_opacity = 0  # taken from d_params
+            ws = r["ws"]
+            with torch.cuda.stream(r["stream"]):
+                # allocate every workspace buffer at its final size before capture
+                F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=r["d_params"])
+                D.bin_sort(F, ws, capacity=self.capacity)
+                D.blend(F, ws, want_state=False, exact=self.exact)
+            torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(g):
-                F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=self.d_params)
+            with torch.cuda.graph(g):  # captured on torch's side stream, replayed on the slot's
+                F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=r["d_params"])
                 D.bin_sort(F, ws, capacity=self.capacity)
                 D.blend(F, ws, want_state=False, exact=self.exact)
             F.layout = layout
             self.graphs.append((g, F))
+            self._keep.append((shading, edits))
+        torch.cuda.synchronize()
         self.g, self.F = self.graphs[0]
         self.K = K
-        self._keep = (shading, edits)
 
     def stage(self, cam, **edits):
         """Enqueue this frame's camera / light / edit upload (async)."""
@@ -436,6 +457,17 @@ class FrameGraph:
         self.g.replay()
         return self.F
 
+    def submit(self, slot, cam, **edits):
+        """Stage + replay on the slot's own stream; returns the slot's Frame."""
+        self._stage(cam, slot=slot, **edits)
+        g, F = self.graphs[slot]
+        with torch.cuda.stream(self.res[slot]["stream"]):
+            g.replay()
+        return F
+
+    def stream(self, slot):
+        return self.res[slot]["stream"]
+
     def render_host(self, cam, host_out, host_contrib=None, **edits):
         """End-to-end frame: H2D inputs, replay, D2H image (synchronous)."""
         F = self.replay(cam, **edits)
@@ -451,23 +483,24 @@ class FrameGraph:
     def overflowed(self):
         return int(self.F.n_pairs.item()) > self.capacity
 
-    def recapture(self, cam):
-        self.capacity = int(int(self.F.n_pairs.item()) * 1.3) + 4096
+    def recapture(self, cam, n_pairs=None):
+        n = int(self.F.n_pairs.item()) if n_pairs is None else int(n_pairs)
+        self.capacity = int(n * 1.3) + 4096
         self._capture(cam)
 
 
 class FramePipeline:
-    """End-to-end frames with the device->host image copy of frame i
-    overlapping the upload + compute of frame i+1.
+    """End-to-end frames: frames on alternating slots (own streams) run
+    concurrently, and each frame's device->host copy overlaps later frames.
 
     ``submit(cam, **edits)`` stages the frame's parameters (pinned ring, one
-    H2D), replays the slot's captured graph on the compute stream and
-    enqueues the RGBA / contribution-count / pair-count copies into pinned
-    host buffers on a copy stream; ``result(ticket)`` waits for that frame's
-    copies and returns its RenderOutput (views of the slot's pinned buffers,
-    valid until the slot is reused ``slots`` submits later).  A frame whose
-    pair count outgrew the captured capacity is re-rendered synchronously
-    after growing the capacity."""
+    H2D) and replays the next slot's captured graph on that slot's stream,
+    then enqueues the RGBA / contribution-count / pair-count copies into the
+    slot's pinned host buffers on a copy stream; ``result(ticket)`` waits for
+    that frame's copies and returns its RenderOutput (views of the slot's
+    pinned buffers, valid until the slot is reused ``slots`` submits later).
+    A frame whose pair count outgrew the captured capacity is re-rendered
+    synchronously after growing the capacity."""
 
     def __init__(self, fg: FrameGraph):
         self.fg = fg
@@ -490,14 +523,12 @@ class FramePipeline:
         fg = self.fg
         k = self.k
         self.k = (k + 1) % fg.slots
-        main = torch.cuda.current_stream()
+        st = fg.stream(k)
         if self.done[k] is not None:  # the slot's previous image must have left the device
-            main.wait_event(self.done[k])
-        fg._stage(cam, **edits)
-        g, F = fg.graphs[k]
-        g.replay()
+            st.wait_event(self.done[k])
+        F = fg.submit(k, cam, **edits)
         ev = torch.cuda.Event()
-        ev.record(main)
+        ev.record(st)
         cs = self.copy_stream
         cs.wait_event(ev)
         with torch.cuda.stream(cs):
@@ -515,8 +546,7 @@ class FramePipeline:
         fg = self.fg
         if int(self.h_np[k][0]) > fg.capacity:  # this view needed more pairs: grow, redo
             torch.cuda.synchronize()
-            fg.capacity = int(int(self.h_np[k][0]) * 1.3) + 4096
-            fg._capture(cam)
+            fg.recapture(cam, n_pairs=int(self.h_np[k][0]))
             fg.render_host(cam, self.h_out[k], self.h_cnt[k], **edits)
         return _unpack(self.h_out[k].numpy(), fg.F.layout, self.h_cnt[k].numpy())
 
