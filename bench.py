@@ -36,7 +36,15 @@ PER_MODEL, N_MODELS, DENSITY = 200_000, 5, 1_000_000
 # our kernels per frame: K1 (1) + K2 (init, minmax, coarse key, 4x3 radix, fix-up,
 # fallback gate, 3 scan, tile hist, tile rowscan, tile ranges, placement, tile order
 # = 25) + K3 (1)
-LAUNCHES_PER_FRAME = 27
+def launches_per_frame(n):
+    """Kernels in one captured frame: K1; K2 = init + minmax + coarse keys +
+    3 per radix pass + fix-up + fallback gate + 2 scans + hist + rowscan +
+    tile ranges + placement; tile order; K3 (sort.cu / blend.cu)."""
+    lg = 1
+    while (1 << lg) < n:
+        lg += 1
+    passes = min(max((lg + 4 + 7) // 8, 2), 4)
+    return 1 + (3 + 3 * passes + 2 + 2 + 4) + 1 + 1
 
 
 SLOTS = 4  # concurrent frame slots (FrameGraph / FramePipeline)
@@ -469,7 +477,7 @@ def run_ours(args):
                         "d2h_bytes_per_step": pipe.d2h_bytes_per_frame(),
                         "pipelined": "frames on 4 concurrent slots; each frame's D2H overlaps "
                                      "later frames' upload+compute; host wall clock over all frames"},
-                "gpu_launches": LAUNCHES_PER_FRAME * args.steps, "overflow": overflow,
+                "gpu_launches": launches_per_frame(n) * args.steps, "overflow": overflow,
                 "extra": extra}
         print(json.dumps(line), flush=True)
     if dist:
