@@ -315,6 +315,21 @@ int ivr_photometric_loss(const double *pred, const double *gt, int32_t height, i
                          int32_t with_ssim, double *d_pred, double *sums, void *workspace,
                          size_t workspace_bytes, ivr_stream_t stream);
 
+/* Training-step map terms (trainer.py:355-366, losses.py:141-268) in one
+ * pass: d_out (H,W,k float32) = photometric gradient d_rgba (H,W,4 float64,
+ * may be NULL) in the colour / alpha channels + w_normal * d(normal
+ * consistency vs pseudo-normals from the depth map) + w_offset * d(mean
+ * |delta_c|) + w_bil * d(bilateral smoothness of the n_bil maps vs gt
+ * (H,W,4)).  cols = {color, alpha, depth, normal, delta_c} (-1 = absent);
+ * cam_params (device) = {focal, cx, cy, rotation[9]}.  terms (device, 3):
+ * normal loss, mean |delta_c|, bilateral sum over maps. */
+size_t ivr_regularize_workspace_size(int32_t height, int32_t width);
+int ivr_regularize(const float *out, int32_t k, int32_t height, int32_t width,
+                   const int32_t cols[5], const int32_t *bil_cols, int32_t n_bil,
+                   const double *gt, const double *d_rgba, const double *cam_params,
+                   double w_normal, double w_offset, double w_bil, float *d_out, double *terms,
+                   void *workspace, size_t workspace_bytes, ivr_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -127,6 +127,11 @@ _SIGS = {
     "ivr_crc32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
     "ivr_unpack": ([P, ctypes.c_int64, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_pack_f32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
+    "ivr_regularize_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),
+    "ivr_regularize": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                        ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),
+                        ctypes.c_int32, P, P, P, ctypes.c_double, ctypes.c_double, ctypes.c_double,
+                        P, P, P, ctypes.c_size_t, P], ctypes.c_int),
     "ivr_photometric_workspace_size": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32],
                                        ctypes.c_size_t),
     "ivr_photometric_loss": ([P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,

@@ -89,6 +89,33 @@ def _photometric_dev(x, y, a, b, with_ssim):
     return sums, d
 
 
+def regularize_t(out, cols, gt=None, d_rgba=None, cam_params=None, w_normal=0.0, w_offset=0.0,
+                 w_bil=0.0, bil_cols=()):
+    """Fused map terms of a training step (csrc/regularize.cu): returns
+    (terms = [normal loss, mean |delta_c|, bilateral sum], d_out float32
+    (H,W,K)).  ``out`` is K3's float32 (H,W,K) map stack, ``cols`` =
+    (color, alpha, depth, normal, delta_c) columns (-1 absent), ``cam_params``
+    a device float64 block (focal, cx, cy, rotation[9])."""
+    from . import _lib as L
+    from . import device as D
+    h, w, k = out.shape
+    nbytes = L.lib().ivr_regularize_workspace_size(h, w)
+    key = ("reg", out.device, nbytes)
+    ws = _WS.get(key)
+    if ws is None:
+        ws = _WS[key] = torch.empty(nbytes, dtype=torch.uint8, device=out.device)
+    d_out = torch.empty_like(out)
+    terms = torch.empty(3, dtype=torch.float64, device=out.device)
+    c5 = (ctypes.c_int32 * 5)(*cols)
+    nb = len(bil_cols)
+    bc = (ctypes.c_int32 * max(nb, 1))(*(list(bil_cols) or [0]))
+    L.check(L.lib().ivr_regularize(D.ptr(out), k, h, w, c5, bc, nb, D.ptr(gt), D.ptr(d_rgba),
+                                   D.ptr(cam_params), float(w_normal), float(w_offset), float(w_bil),
+                                   D.ptr(d_out), D.ptr(terms), D.ptr(ws), nbytes,
+                                   D.stream_handle()), "ivr_regularize")
+    return terms, d_out
+
+
 def ssim_t(x, y):
     """Mean SSIM over channels and its gradient w.r.t. x (float64 device
     tensors (H, W, C)); one fused window pass + one adjoint pass (csrc/ssim.cu)."""
@@ -173,6 +200,18 @@ def pseudo_normal_from_depth(depth, alpha, cam, alpha_threshold=1e-3):
     return _out(depth, nw), _out(depth, mask)
 
 
+def normal_consistency_t(n, t, m):
+    """Device form of normal_consistency_loss (no host sync): (loss tensor,
+    gradient); n, t (H,W,3) float64, m (H,W) bool."""
+    cnt = m.sum().clamp(min=1).to(n.dtype)
+    diff = (n - t) * m[..., None]
+    norms = torch.linalg.norm(diff, dim=-1)
+    loss = norms.sum() / cnt
+    safe = norms > 1e-12
+    g = torch.where(safe[..., None], diff / torch.where(safe, norms, 1.0)[..., None], 0.0) / cnt
+    return loss, g
+
+
 def normal_consistency_loss(normal_map, target, mask):
     """losses.py:184-206: mean L2 distance over masked pixels, gradient to the map."""
     n, t = _t(normal_map), _t(target)
@@ -180,18 +219,8 @@ def normal_consistency_loss(normal_map, target, mask):
         torch.from_numpy(np.asarray(mask, bool)).to(_dev())
     if n.shape != t.shape:
         raise ShapeMismatch(f"normal maps differ: {tuple(n.shape)} vs {tuple(t.shape)}")
-    cnt = int(m.sum())
-    d_n = torch.zeros_like(n)
-    if cnt == 0:
-        return 0.0, _out(normal_map, d_n)
-    diff = (n - t)[m]
-    norms = torch.linalg.norm(diff, dim=-1)
-    loss = float(norms.sum()) / cnt
-    safe = norms > 1e-12
-    g = torch.zeros_like(diff)
-    g[safe] = diff[safe] / norms[safe, None] / cnt
-    d_n[m] = g
-    return loss, _out(normal_map, d_n)
+    loss, d_n = normal_consistency_t(n, t, m)
+    return float(loss), _out(normal_map, d_n)
 
 
 def _fdiff_abs(img):
@@ -203,29 +232,35 @@ def _fdiff_abs(img):
     return gx + gy
 
 
-def bilateral_smoothness(attr_map, gt_color, mask=None):
-    """losses.py:219-253: edge-aware smoothness and its gradient."""
-    k, c = _t(attr_map), _t(gt_color)
-    if k.shape[:2] != c.shape[:2]:
-        raise ShapeMismatch(f"attribute {tuple(k.shape)} vs color {tuple(c.shape)}")
-    m = torch.ones(k.shape[:2], dtype=torch.bool, device=k.device) if mask is None else _t(mask).bool()
-    cnt = int(m.sum())
+def bilateral_smoothness_t(k, c, m=None):
+    """Device form of bilateral_smoothness (no host sync): (loss tensor, d_k)."""
+    if m is None:
+        m = torch.ones(k.shape[:2], dtype=torch.bool, device=k.device)
+    cnt = m.sum().clamp(min=1).to(k.dtype)
     d_k = torch.zeros_like(k)
-    if cnt == 0:
-        return 0.0, _out(attr_map, d_k)
     weight = torch.exp(-_fdiff_abs(c)) * m / cnt
     k3 = k if k.dim() == 3 else k[..., None]
     d3 = d_k if d_k.dim() == 3 else d_k[..., None]
     gx = k3[:, 1:] - k3[:, :-1]
     gy = k3[1:] - k3[:-1]
-    loss = float((gx.abs().sum(-1) * weight[:, :-1]).sum() + (gy.abs().sum(-1) * weight[:-1]).sum())
+    loss = (gx.abs().sum(-1) * weight[:, :-1]).sum() + (gy.abs().sum(-1) * weight[:-1]).sum()
     sx = torch.sign(gx) * weight[:, :-1, None]
     sy = torch.sign(gy) * weight[:-1, :, None]
     d3[:, 1:] += sx
     d3[:, :-1] -= sx
     d3[1:] += sy
     d3[:-1] -= sy
-    return loss, _out(attr_map, d_k)
+    return loss, d_k
+
+
+def bilateral_smoothness(attr_map, gt_color, mask=None):
+    """losses.py:219-253: edge-aware smoothness and its gradient."""
+    k, c = _t(attr_map), _t(gt_color)
+    if k.shape[:2] != c.shape[:2]:
+        raise ShapeMismatch(f"attribute {tuple(k.shape)} vs color {tuple(c.shape)}")
+    m = None if mask is None else _t(mask).bool()
+    loss, d_k = bilateral_smoothness_t(k, c, m)
+    return float(loss), _out(attr_map, d_k)
 
 
 def offset_sparsity_loss(offset_map):

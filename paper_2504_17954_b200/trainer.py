@@ -32,8 +32,7 @@ import torch
 from . import device as D
 from .errors import DatasetEmpty, DivergedLoss, OutOfRange
 from .gaussians import GaussianGeometry, ShColor
-from .losses import (LossWeights, bilateral_smoothness, normal_consistency_loss,
-                     photometric_loss_t, pseudo_normal_from_depth)
+from .losses import LossWeights, photometric_loss_t, regularize_t
 from .rasterizer import _channel_layout, _cols
 from .scene import STAGE_BASE, STAGE_EDITABLE, BasicSceneModel, DeviceScene
 from .shading import LightConfig, Palette, ShadingAttributes
@@ -139,6 +138,7 @@ class _StageTrainer:
         self.adam = DeviceAdam(self.cfg.adam_eps, self.cfg.adam_betas)
         self.ws = D.Workspace(self.dev)
         self._bad = None
+        self._first_bad = None
 
     @property
     def n(self):
@@ -203,23 +203,71 @@ class _StageTrainer:
         return torch.cat([out[..., c["color"]:c["color"] + 3], out[..., c["alpha"]:c["alpha"] + 1]],
                          dim=-1)
 
-    def _photometric(self, out, cam, gt, weights):
-        """L1+SSIM on RGBA plus the normal-consistency term; returns
-        (loss, d_out (H,W,K) float64, column map)."""
-        H, W = cam.height, cam.width
+    def _cam_params(self, cam):
+        """Device block (focal, cx, cy, rotation[9]) for the pseudo-normal
+        term, staged through pinned memory (no host synchronisation)."""
+        if getattr(self, "_cam_pin", None) is None:
+            self._cam_pin = torch.empty(12, dtype=torch.float64, pin_memory=True)
+            self._cam_dev = torch.empty(12, dtype=torch.float64, device=self.dev)
+            self._cam_ev = None
+        if self._cam_ev is not None:
+            self._cam_ev.synchronize()
+        h = self._cam_pin.numpy()
+        h[0] = 0.5 * cam.height / np.tan(0.5 * cam.fov_y)
+        h[1], h[2] = (cam.width - 1) / 2.0, (cam.height - 1) / 2.0
+        h[3:] = np.asarray(cam.rotation, dtype=np.float64).reshape(9)
+        self._cam_dev.copy_(self._cam_pin, non_blocking=True)
+        self._cam_ev = torch.cuda.Event()
+        self._cam_ev.record()
+        return self._cam_dev
+
+    def _map_terms(self, F, cam, gt, weights, offset=False, bilateral=False):
+        """Photometric L1+SSIM (K7) and the map regularizers (fused kernel):
+        returns (loss tensor, d_out float32 (H,W,K), column map).  No host
+        synchronisation: a non-finite loss is recorded on the device
+        (``check_finite``)."""
         c = {name: c for name, c, w in _cols_named(self.layout)}
-        loss, d_rgba = photometric_loss_t(self._rgba(out), gt, weights)
-        if not torch.isfinite(loss):
-            raise DivergedLoss(f"loss became {float(loss)}")
-        d_out = torch.zeros((H, W, self.K), dtype=torch.float64, device=self.dev)
-        d_out[..., c["color"]:c["color"] + 3] = d_rgba[..., :3]
-        d_out[..., c["alpha"]] = d_rgba[..., 3]
-        if weights.normal_consistency > 0.0:
-            target, mask = pseudo_normal_from_depth(out[..., c["depth"]], out[..., c["alpha"]], cam)
-            nl, d_n = normal_consistency_loss(out[..., c["normal"]:c["normal"] + 3], target, mask)
-            loss = loss + weights.normal_consistency * nl
-            d_out[..., c["normal"]:c["normal"] + 3] = weights.normal_consistency * d_n
+        idx = getattr(self, "_rgba_idx", None)
+        if idx is None:
+            idx = self._rgba_idx = torch.tensor([c["color"], c["color"] + 1, c["color"] + 2,
+                                                 c["alpha"]], device=self.dev)
+        rgba = F.out.index_select(2, idx).double()
+        loss, d_rgba = photometric_loss_t(rgba, gt, weights)
+        self._note_finite(loss)
+        wn = weights.normal_consistency
+        wo = weights.offset_sparsity if offset else 0.0
+        wb = weights.bilateral_smoothness if bilateral else 0.0
+        bil = tuple(c[n] for n in ("k_a", "k_d", "k_s", "beta")) if wb > 0.0 else ()
+        cols = (c["color"], c["alpha"], c.get("depth", -1), c.get("normal", -1),
+                c.get("delta_c", -1))
+        terms, d_out = regularize_t(F.out, cols, gt=gt, d_rgba=d_rgba,
+                                    cam_params=self._cam_params(cam) if wn > 0.0 else None,
+                                    w_normal=wn, w_offset=wo, w_bil=wb, bil_cols=bil)
+        if wn > 0.0:
+            loss = loss + wn * terms[0]
+        if wo > 0.0:
+            loss = loss + wo * terms[1]
+        if wb > 0.0:
+            loss = loss + wb * terms[2]
         return loss, d_out, c
+
+    def _note_finite(self, loss):
+        """Device-side DivergedLoss bookkeeping: the first step whose
+        photometric loss was non-finite (the reference checks it in the step,
+        trainer.py:345-348)."""
+        if self._first_bad is None:
+            self._first_bad = torch.full((), -1, dtype=torch.int64, device=self.dev)
+            self._step_no = torch.zeros((), dtype=torch.int64, device=self.dev)
+        self._step_no += 1
+        bad = ~torch.isfinite(loss) & (self._first_bad < 0)
+        self._first_bad = torch.where(bad, self._step_no, self._first_bad)
+        self._last_bad_loss = torch.where(bad, loss, getattr(self, "_last_bad_loss", loss))
+
+    def check_finite(self):
+        """Raise DivergedLoss if any step so far had a non-finite loss."""
+        if self._first_bad is not None and int(self._first_bad) >= 0:
+            raise DivergedLoss(f"loss became {float(self._last_bad_loss)} at step "
+                               f"{int(self._first_bad)}")
 
 
 class BaseTrainer(_StageTrainer):
@@ -249,8 +297,8 @@ class BaseTrainer(_StageTrainer):
         from .sh import sh_backward_device
         weights = weights or self.cfg.weights
         F, dg = self.forward(cam)
-        loss, d_out, _ = self._photometric(F.out.double(), cam, gt, weights)
-        g = D.blend_backward(F, d_out.float())
+        loss, d_out, _ = self._map_terms(F, cam, gt, weights)
+        g = D.blend_backward(F, d_out)
         want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_mean2d")
         gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, geometry=True, want=want)
         n = self.n
@@ -312,18 +360,8 @@ class EditableTrainer(_StageTrainer):
         all device tensors."""
         weights = weights or self.cfg.weights
         F, S, attrs, dg = self.forward(cam)
-        out = F.out.double()
-        loss, d_out, c = self._photometric(out, cam, gt, weights)
-        if weights.offset_sparsity > 0.0:
-            m = out[..., c["delta_c"]:c["delta_c"] + 3]
-            loss = loss + weights.offset_sparsity * m.abs().mean()
-            d_out[..., c["delta_c"]:c["delta_c"] + 3] = weights.offset_sparsity * torch.sign(m) / m.numel()
-        if weights.bilateral_smoothness > 0.0:
-            for name in ("k_a", "k_d", "k_s", "beta"):
-                bl, d_map = bilateral_smoothness(out[..., c[name]], gt[..., :3])
-                loss = loss + weights.bilateral_smoothness * bl
-                d_out[..., c[name]] = weights.bilateral_smoothness * d_map
-        g = D.blend_backward(F, d_out.float())
+        loss, d_out, c = self._map_terms(F, cam, gt, weights, offset=True, bilateral=True)
+        g = D.blend_backward(F, d_out)
         want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_mean2d", "d_values",
                 "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta")
         gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, shading=S, geometry=True,
@@ -509,6 +547,7 @@ def _run_stage(tr, dataset, cfg, iters, rng, gen, densify_start=None, decay_extr
         view = int(rng.integers(len(dataset)))
         loss, grads, stat = tr.step(dataset.cameras[view], gts[view])
         if it % cfg.log_interval == 0:
+            tr.check_finite()
             D.raise_if_bad(tr._bad, tr.n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw",
                                            "d_colors"))
         tr.apply(grads, it, iters, decay_extra)
@@ -520,6 +559,7 @@ def _run_stage(tr, dataset, cfg, iters, rng, gen, densify_start=None, decay_extr
             stats_sum = torch.zeros(tr.n, dtype=torch.float64, device=tr.dev)
             stats_iters = 0
         if it % cfg.log_interval == 0 or it == iters:
+            tr.check_finite()
             lv = float(loss)
             if not np.isfinite(lv):
                 raise DivergedLoss(f"loss became {lv} at iteration {it}")

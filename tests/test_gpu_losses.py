@@ -53,3 +53,47 @@ def test_small_image_errors():
         photometric_loss(x, x)
     loss, d = photometric_loss(x, x + 0.5, LossWeights(ssim_weight=0.0))  # L1 only: fine
     assert abs(loss - 0.4) < 1e-15 and np.allclose(d, -0.8 / x.size)
+
+
+def test_fused_regularizers_match_loss_functions():
+    """ivr_regularize == the per-term functions (pseudo normals + consistency,
+    offset sparsity, bilateral smoothness on four maps) on random maps."""
+    import torch
+    from paper_2504_17954_b200 import orbit_camera
+    from paper_2504_17954_b200.losses import (bilateral_smoothness, normal_consistency_loss,
+                                              offset_sparsity_loss, pseudo_normal_from_depth,
+                                              regularize_t)
+    rng = np.random.default_rng(11)
+    H, W, K = 37, 45, 15
+    out = rng.uniform(0.05, 1.0, (H, W, K)).astype(np.float32)
+    out[..., 4] = (2.0 + rng.uniform(0, 0.3, (H, W))).astype(np.float32)  # depth
+    out[:5, :7, 3] = 0.0                                                     # alpha holes
+    gt = rng.uniform(0, 1, (H, W, 4))
+    d_rgba = rng.normal(size=(H, W, 4))
+    cam = orbit_camera(np.zeros(3), 2.5, 0.4, -0.3, 0.9, W, H)
+    blk = np.concatenate([[0.5 * H / np.tan(0.5 * cam.fov_y), (W - 1) / 2.0, (H - 1) / 2.0],
+                          cam.rotation.reshape(9)])
+    dev = torch.device("cuda")
+    terms, d_out = regularize_t(torch.from_numpy(out).to(dev), (0, 3, 4, 5, 8),
+                                gt=torch.from_numpy(gt).to(dev), d_rgba=torch.from_numpy(d_rgba).to(dev),
+                                cam_params=torch.from_numpy(blk).to(dev), w_normal=0.01,
+                                w_offset=0.02, w_bil=0.03, bil_cols=(11, 12, 13, 14))
+    terms, d_out = terms.cpu().numpy(), d_out.cpu().numpy()
+    o = out.astype(np.float64)
+    target, mask = pseudo_normal_from_depth(o[..., 4], o[..., 3], cam)
+    nl, dn = normal_consistency_loss(o[..., 5:8], target, mask)
+    assert abs(terms[0] - nl) <= 1e-9 * max(abs(nl), 1e-30)
+    np.testing.assert_allclose(d_out[..., 5:8], (0.01 * dn).astype(np.float32), rtol=1e-5, atol=1e-9)
+    ol, do = offset_sparsity_loss(o[..., 8:11])
+    assert abs(terms[1] - ol) <= 1e-12 * abs(ol)
+    np.testing.assert_allclose(d_out[..., 8:11], (0.02 * do).astype(np.float32), rtol=1e-6)
+    bl = 0.0
+    for ch in (11, 12, 13, 14):
+        b, db = bilateral_smoothness(o[..., ch], gt[..., :3])
+        bl += b
+        np.testing.assert_allclose(d_out[..., ch], (0.03 * db).astype(np.float32), rtol=1e-5,
+                                   atol=1e-12)
+    assert abs(terms[2] - bl) <= 1e-10 * abs(bl)
+    np.testing.assert_allclose(d_out[..., 0:3], d_rgba[..., :3].astype(np.float32))
+    np.testing.assert_allclose(d_out[..., 3], d_rgba[..., 3].astype(np.float32))
+    assert np.all(d_out[..., 4] == 0.0)

@@ -76,3 +76,18 @@ def test_short_training_run_decreases_loss():
     # held-out view (fixed) improves as shading is fitted
     assert log[-1]["psnr"] > log[0]["psnr"]
     assert model.stage == "editable" and len(model) == log[-1]["count"]
+
+
+def test_diverged_loss_raises():
+    """A non-finite loss raises DivergedLoss (checked on the device, reported at
+    the next log point)."""
+    from paper_2504_17954_b200 import (BasicSceneModel, DivergedLoss, LightConfig, ShColor,
+                                       TrainConfig, ViewDataset, orbit_camera, train_editable)
+    from paper_2504_17954_b200.synthetic import editable_model
+    ed = editable_model(5, 500, spread=0.5, density=500)
+    base = BasicSceneModel("base", ed.geometry, sh=ShColor.from_dc(np.full((500, 3), 0.5)))
+    cams = [orbit_camera(np.zeros(3), 2.5, 0.3, az, 0.9, 32, 32) for az in (0.3, 1.9)]
+    imgs = [np.full((32, 32, 4), np.nan), np.full((32, 32, 4), np.nan)]
+    with pytest.raises(DivergedLoss):
+        train_editable(base, ViewDataset(cams, imgs, LightConfig()),
+                       TrainConfig(stage2_iters=10, log_interval=5))

@@ -40,12 +40,22 @@ def main(which):
     for _ in range(3):
         step()
     torch.cuda.synchronize()
+    import time
+    t0 = time.perf_counter()
+    for _ in range(10):
+        step()
+    torch.cuda.synchronize()
+    wall = (time.perf_counter() - t0) / 10
     from torch.profiler import ProfilerActivity, profile
     with profile(activities=[ProfilerActivity.CUDA, ProfilerActivity.CPU]) as prof:
         for _ in range(5):
             step()
         torch.cuda.synchronize()
     print(prof.key_averages().table(sort_by="cuda_time_total", row_limit=35))
+    ev = [e for e in prof.events() if e.device_type == torch.autograd.DeviceType.CUDA]
+    busy = sum(e.device_time for e in ev) / 5 / 1e3
+    print(f"wall {wall * 1e3:.2f} ms/step, GPU kernel time {busy:.2f} ms/step, "
+          f"{len(ev) / 5:.0f} kernels/step")
 
 
 if __name__ == "__main__":
