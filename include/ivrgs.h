@@ -330,6 +330,18 @@ int ivr_regularize(const float *out, int32_t k, int32_t height, int32_t width,
                    double w_normal, double w_offset, double w_bil, float *d_out, double *terms,
                    void *workspace, size_t workspace_bytes, ivr_stream_t stream);
 
+/* Adam (trainer.Adam.step, trainer.py:109-120) over up to 16 parameter
+ * groups in one launch; float64, the reference's evaluation order.
+ * bc1 = 1 - beta1^t, bc2 = 1 - beta2^t (t = the group's step count). */
+typedef struct ivr_adam_group {
+    double *param, *m, *v;
+    const double *grad;
+    int64_t n;
+    double lr, bc1, bc2;
+} ivr_adam_group;
+int ivr_adam_step(const ivr_adam_group *groups, int32_t n_groups, double beta1, double beta2,
+                  double eps, ivr_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -755,6 +755,14 @@ class Adam:
         param -= lr * mh / (np.sqrt(vh) + self.eps)
         return param
 
+    def remap(self, parents, is_new):
+        """trainer.py:122-128: re-index moment rows; new rows reset to 0."""
+        for st in self.state.values():
+            for key in ("m", "v"):
+                arr = st[key][parents].copy()
+                arr[is_new] = 0.0
+                st[key] = arr
+
 
 def inverse_step(geom, shading, scene_ids, light, c_p, opacity_raw, lam, b, polar, azimuth,
                  cam, reference, nthreads=0):

@@ -71,6 +71,11 @@ class ProjOut_t(ctypes.Structure):
                 ("depth", P), ("opacity", P), ("rgb", P), ("radius", P), ("valid", P)]
 
 
+class AdamGroup_t(ctypes.Structure):
+    _fields_ = [("param", P), ("m", P), ("v", P), ("grad", P), ("n", ctypes.c_int64),
+                ("lr", ctypes.c_double), ("bc1", ctypes.c_double), ("bc2", ctypes.c_double)]
+
+
 class Grads_t(ctypes.Structure):
     _fields_ = [("g_values", P), ("g_mean2d", P), ("g_conic", P), ("g_opacity", P),
                 ("d_rgb_extra", P), ("d_mu", P), ("d_q_raw", P), ("d_log_s", P), ("d_o_logit", P),
@@ -127,6 +132,8 @@ _SIGS = {
     "ivr_crc32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
     "ivr_unpack": ([P, ctypes.c_int64, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_pack_f32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
+    "ivr_adam_step": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
+                       ctypes.c_double, ctypes.c_double, P], ctypes.c_int),
     "ivr_regularize_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),
     "ivr_regularize": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),

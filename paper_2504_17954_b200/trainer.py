@@ -29,6 +29,7 @@ from dataclasses import dataclass, field
 import numpy as np
 import torch
 
+from . import _lib as L
 from . import device as D
 from .errors import DatasetEmpty, DivergedLoss, OutOfRange
 from .gaussians import GaussianGeometry, ShColor
@@ -84,23 +85,41 @@ class TrainConfig:
 
 
 class DeviceAdam:
-    """trainer.Adam on device tensors; moments survive densification (remap)."""
+    """trainer.Adam on device tensors (one fused launch for all parameter
+    groups, csrc/adam.cu); moments survive densification (remap)."""
 
     def __init__(self, eps=1e-15, betas=(0.9, 0.999)):
         self.eps, (self.b1, self.b2), self.state = eps, betas, {}
 
-    @torch.no_grad()
     def step(self, name, param, grad, lr):
-        st = self.state.get(name)
-        if st is None:
-            st = self.state[name] = {"m": torch.zeros_like(param), "v": torch.zeros_like(param), "t": 0}
-        st["t"] += 1
-        t = st["t"]
-        st["m"].mul_(self.b1).add_(grad, alpha=1.0 - self.b1)
-        st["v"].mul_(self.b2).addcmul_(grad, grad, value=1.0 - self.b2)
-        mhat = st["m"] / (1.0 - self.b1 ** t)
-        vhat = st["v"] / (1.0 - self.b2 ** t)
-        param.sub_(lr * mhat / (vhat.sqrt() + self.eps))
+        self.step_all([(name, param, grad, lr)])
+
+    @torch.no_grad()
+    def step_all(self, items):
+        """Update every (name, param, grad, lr) of one training step."""
+        arr = (L.AdamGroup_t * len(items))()
+        keep = []
+        for k, (name, param, grad, lr) in enumerate(items):
+            st = self.state.get(name)
+            if st is None:
+                st = self.state[name] = {"m": torch.zeros_like(param), "v": torch.zeros_like(param),
+                                         "t": 0}
+            st["t"] += 1
+            t = st["t"]
+            g = grad.to(torch.float64).contiguous()
+            keep.append(g)
+            if not param.is_contiguous():
+                raise ValueError(f"parameter {name} must be contiguous")
+            a = arr[k]
+            a.param, a.m, a.v, a.grad = (param.data_ptr(), st["m"].data_ptr(), st["v"].data_ptr(),
+                                         g.data_ptr())
+            a.n = param.numel()
+            a.lr = float(lr)
+            a.bc1 = 1.0 - self.b1 ** t
+            a.bc2 = 1.0 - self.b2 ** t
+        L.check(L.lib().ivr_adam_step(arr, len(items), self.b1, self.b2, self.eps,
+                                      D.stream_handle()), "ivr_adam_step")
+        del keep
 
     def remap(self, parents, is_new):
         for st in self.state.values():
@@ -148,13 +167,15 @@ class _StageTrainer:
         """Adam on every group with the reference schedules (trainer.py:491-499)."""
         cfg = self.cfg
         frac = it / max(iters, 1)
+        items = []
         for name, grad in grads.items():
             lr = getattr(cfg, _LR[name])
             if name == "mu" and cfg.lr_mu > 0.0:
                 lr = cfg.lr_mu * (cfg.lr_mu_final / cfg.lr_mu) ** frac
             elif _LR[name] in ("lr_shading", "lr_normal") or name in decay_extra:
                 lr = lr * cfg.lr_decay_floor ** frac
-            self.adam.step(name, self.p[name], grad, lr)
+            items.append((name, self.p[name], grad, lr))
+        self.adam.step_all(items)
 
     @torch.no_grad()
     def densify(self, mean_stat, extent, gen):

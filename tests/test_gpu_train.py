@@ -91,3 +91,33 @@ def test_diverged_loss_raises():
     with pytest.raises(DivergedLoss):
         train_editable(base, ViewDataset(cams, imgs, LightConfig()),
                        TrainConfig(stage2_iters=10, log_interval=5))
+
+
+def test_device_adam_matches_reference_adam():
+    """Fused multi-group Adam == trainer.Adam (oracle restatement) over steps
+    with different learning rates, incl. a densify remap."""
+    import oracle as O
+    import torch
+    from paper_2504_17954_b200.trainer import DeviceAdam
+    rng = np.random.default_rng(2)
+    shapes = {"mu": (500, 3), "q_raw": (500, 4), "o_logit": (500,)}
+    p_dev = {k: torch.from_numpy(rng.normal(size=s)).cuda() for k, s in shapes.items()}
+    p_ref = {k: v.cpu().numpy().copy() for k, v in p_dev.items()}
+    da, ra = DeviceAdam(1e-15, (0.9, 0.999)), O.Adam(1e-15, (0.9, 0.999))
+    for it in range(6):
+        grads = {k: rng.normal(size=s) for k, s in shapes.items()}
+        lrs = {"mu": 1e-3 / (it + 1), "q_raw": 5e-3, "o_logit": 0.05}
+        da.step_all([(k, p_dev[k], torch.from_numpy(grads[k]).cuda(), lrs[k]) for k in shapes])
+        for k in shapes:
+            ra.step(k, p_ref[k], grads[k], lrs[k])
+        if it == 2:  # densify-style remap: rows 0..9 duplicated as new rows
+            parents = np.concatenate([np.arange(500), np.arange(10)])
+            is_new = np.arange(510) >= 500
+            da.remap(torch.from_numpy(parents).cuda(), torch.from_numpy(is_new).cuda())
+            ra.remap(parents, is_new)
+            for k in shapes:
+                p_ref[k] = p_ref[k][parents].copy()
+                p_dev[k] = p_dev[k][torch.from_numpy(parents).cuda()].contiguous()
+            shapes = {k: (510,) + s[1:] for k, s in shapes.items()}
+    for k in shapes:
+        np.testing.assert_allclose(p_dev[k].cpu().numpy(), p_ref[k], rtol=1e-13, atol=1e-15)
