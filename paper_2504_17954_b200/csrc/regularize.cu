@@ -13,8 +13,9 @@
 //     (losses.py:209-253): edge weights exp(-sum |grad gt|) / (H W), gradient
 //     gathered from the 4-neighbourhood (no atomics).
 // The reference / torch restatement builds each of these with tens of full-map
-// array operations; here they are two kernels: a mask count (the normal loss
-// divides by it) and the fused gradient + per-block loss partial sums.
+// array operations; here they are two kernels: a first pass (normal-mask
+// count -- the normal loss divides by it -- and the bilateral edge-weight
+// map) and the fused gradient + per-block loss partial sums.
 #include "ivr_common.cuh"
 
 namespace ivr {
@@ -32,6 +33,7 @@ struct Args {
     const double *camp;    // device: f, cx, cy, rot[9] (world -> camera, row-major)
     double w_normal, w_offset, w_bil;
     int *mask_count;       // device: pixels in the normal mask
+    double *wmap;          // (H, W) bilateral edge weights / (H W), from the first pass
     float *d_out;          // (H, W, K)
     double *part;          // per block: normal, |offset| sum, bilateral sum
 };
@@ -95,22 +97,6 @@ __device__ __forceinline__ double block_sum(double v, double *s_red) {
     return t;
 }
 
-__global__ void __launch_bounds__(kThreads) mask_count_kernel(Args A) {
-    __shared__ int s_c;
-    if (threadIdx.x == 0) s_c = 0;
-    __syncthreads();
-    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    int c = 0;
-    if (i < (int64_t)A.H * A.W) {
-        double nw[3];
-        c = pseudo_normal(A, (int)(i / A.W), (int)(i % A.W), nw) ? 1 : 0;
-    }
-    c = __reduce_add_sync(0xffffffffu, c);
-    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_c, c);
-    __syncthreads();
-    if (threadIdx.x == 0 && s_c) atomicAdd(A.mask_count, s_c);
-}
-
 // bilateral edge weight at (y, x): exp(-sum_c |gt(x+1)-gt| - sum_c |gt(y+1)-gt|)
 __device__ __forceinline__ double edge_weight(const Args &A, int y, int x) {
     const double *g = A.gt + ((int64_t)y * A.W + x) * 4;
@@ -124,6 +110,27 @@ __device__ __forceinline__ double edge_weight(const Args &A, int y, int x) {
         s += fabs(h[0] - g[0]) + fabs(h[1] - g[1]) + fabs(h[2] - g[2]);
     }
     return exp(-s);
+}
+
+__global__ void __launch_bounds__(kThreads) mask_count_kernel(Args A) {
+    __shared__ int s_c;
+    if (threadIdx.x == 0) s_c = 0;
+    __syncthreads();
+    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    int c = 0;
+    if (i < (int64_t)A.H * A.W) {
+        const int y = (int)(i / A.W), x = (int)(i % A.W);
+        if (A.w_normal > 0.0) {
+            double nw[3];
+            c = pseudo_normal(A, y, x, nw) ? 1 : 0;
+        }
+        if (A.w_bil > 0.0 && A.n_bil > 0)
+            A.wmap[i] = edge_weight(A, y, x) * (1.0 / ((double)A.H * A.W));
+    }
+    c = __reduce_add_sync(0xffffffffu, c);
+    if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_c, c);
+    __syncthreads();
+    if (threadIdx.x == 0 && s_c) atomicAdd(A.mask_count, s_c);
 }
 
 __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
@@ -168,10 +175,9 @@ __global__ void __launch_bounds__(kThreads) reg_grad_kernel(Args A) {
             }
         }
         if (A.w_bil > 0.0 && A.n_bil > 0) {
-            const double inv = 1.0 / (double)npx;
-            const double w0 = edge_weight(A, y, x) * inv;
-            const double wl = x > 0 ? edge_weight(A, y, x - 1) * inv : 0.0;
-            const double wu = y > 0 ? edge_weight(A, y - 1, x) * inv : 0.0;
+            const double w0 = A.wmap[i];
+            const double wl = x > 0 ? A.wmap[i - 1] : 0.0;
+            const double wu = y > 0 ? A.wmap[i - A.W] : 0.0;
             for (int b = 0; b < A.n_bil; ++b) {
                 const int c = A.c_bil[b];
                 const double k0 = (double)o[c];
@@ -224,8 +230,9 @@ __global__ void __launch_bounds__(kThreads) reg_finish_kernel(const double *part
 }  // namespace ivr
 
 extern "C" size_t ivr_regularize_workspace_size(int32_t height, int32_t width) {
-    const int64_t nb = ((int64_t)height * width + ivr::regk::kThreads - 1) / ivr::regk::kThreads;
-    return 256 + 8 * (size_t)(3 * nb);
+    const int64_t npx = (int64_t)height * width;
+    const int64_t nb = (npx + ivr::regk::kThreads - 1) / ivr::regk::kThreads;
+    return 256 + 8 * (size_t)(3 * nb) + 8 * (size_t)npx;
 }
 
 extern "C" int ivr_regularize(const float *out, int32_t k, int32_t height, int32_t width,
@@ -272,9 +279,10 @@ extern "C" int ivr_regularize(const float *out, int32_t k, int32_t height, int32
     A.d_out = d_out;
     const int64_t npx = (int64_t)height * width;
     const int nb = (int)((npx + kThreads - 1) / kThreads);
+    A.wmap = A.part + 3 * (int64_t)nb;
     if (cudaMemsetAsync(A.mask_count, 0, sizeof(int), st) != cudaSuccess)
         return check_launch("ivr_regularize memset");
-    if (w_normal > 0.0) mask_count_kernel<<<nb, kThreads, 0, st>>>(A);
+    if (w_normal > 0.0 || (w_bil > 0.0 && n_bil > 0)) mask_count_kernel<<<nb, kThreads, 0, st>>>(A);
     reg_grad_kernel<<<nb, kThreads, 0, st>>>(A);
     reg_finish_kernel<<<1, kThreads, 0, st>>>(A.part, nb, npx, terms);
     return check_launch("ivr_regularize");
