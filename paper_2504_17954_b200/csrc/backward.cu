@@ -321,7 +321,7 @@ struct BwdConst {
     int geometry;
 };
 
-__global__ void __launch_bounds__(128)
+__global__ void __launch_bounds__(128, 4)
 preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *__restrict__ Pd) {
     __shared__ ivr_frame_params P;
     __shared__ double s_glob[10];
