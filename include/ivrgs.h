@@ -27,7 +27,7 @@ extern "C" {
 
 typedef struct CUstream_st *ivr_stream_t; /* == cudaStream_t */
 
-#define IVR_ABI_VERSION 2
+#define IVR_ABI_VERSION 3
 #define IVR_TILE 16 /* rasterizer.py:24 TILE_SIZE */
 
 typedef enum ivr_status {
@@ -57,7 +57,9 @@ typedef struct ivr_gaussians {
     const double *log_s;   /* (n,3) */
     const double *o_logit; /* (n)   */
     const double *n_raw;   /* (n,3) */
+    const double *cache;   /* optional (n,16) from ivr_preprocess_static, or NULL */
 } ivr_gaussians;
+
 
 /* Editable shading inputs: ShadingAttributes (shading.py:89-115), palette,
  * LightConfig (shading.py:42-66) and the optional (lam, b) coefficient
@@ -115,6 +117,14 @@ typedef struct ivr_proj_out {
     double *radius;  /* (n) */
     uint8_t *valid;  /* (n) projection validity */
 } ivr_proj_out;
+
+/* Camera- and edit-independent per-Gaussian values of a resident scene
+ * (cov3d, unit normal, sigmoid(o_logit), the shading sigmoids and beta),
+ * computed by the same code as the per-frame path: with g->cache set,
+ * ivr_preprocess_fwd(_params) and ivr_shade_fwd give bit-identical results
+ * with far less float64 work per frame.  cache: (n,16) float64. */
+int ivr_preprocess_static(const ivr_gaussians *g, const ivr_shading *shading, double *cache,
+                          ivr_stream_t stream);
 
 int ivr_version(void);
 const char *ivr_last_error(void);

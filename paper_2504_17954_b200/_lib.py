@@ -44,7 +44,7 @@ class FrameParams_t(ctypes.Structure):
 
 class Gaussians_t(ctypes.Structure):
     _fields_ = [("n", ctypes.c_int64), ("mu", P), ("q_raw", P), ("log_s", P), ("o_logit", P),
-                ("n_raw", P)]
+                ("n_raw", P), ("cache", P)]
 
 
 class Shading_t(ctypes.Structure):
@@ -132,6 +132,8 @@ _SIGS = {
     "ivr_crc32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
     "ivr_unpack": ([P, ctypes.c_int64, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_pack_f32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
+    "ivr_preprocess_static": ([ctypes.POINTER(Gaussians_t), ctypes.POINTER(Shading_t), P, P],
+                              ctypes.c_int),
     "ivr_adam_step": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
                        ctypes.c_double, ctypes.c_double, P], ctypes.c_int),
     "ivr_regularize_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),

@@ -485,7 +485,7 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
             double nrm[3];
             unit_normal(G, i, nrm);
             ShadeState st;
-            shade_state(B.S, P, i, sid, mu, nrm, st);
+            shade_state(B.S, P, i, sid, mu, nrm, st, G.cache);
             double d_rgb[3];
             for (int k = 0; k < 3; ++k)
                 d_rgb[k] = gv_color[k] + (R.d_rgb_extra ? R.d_rgb_extra[3 * i + k] : 0.0);
@@ -647,6 +647,7 @@ extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *sha
     if (g->n == 0) return IVR_OK;
     BwdConst B{};
     B.G = *g;
+    if (geometry) B.G.cache = nullptr;  // the geometry chain needs q, s, R (not cached)
     if (shading) B.S = *shading;
     B.has_shading = shading != nullptr;
     if (edits) B.E = *edits;

@@ -22,8 +22,8 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
     const ivr_camera &cam = P.cam;
     const int32_t sid = (has_edits && E.scene_id) ? E.scene_id[i] : 0;
     const bool rescale = has_edits && P.rescale_opacity && E.opacity_scale;
-    const double opacity =
-        effective_opacity(G.o_logit[i], rescale, rescale ? E.opacity_scale[sid] : 1.0);
+    const double sig_o = G.cache ? G.cache[kCacheStride * i + 9] : sigmoid_ref(G.o_logit[i]);
+    const double opacity = effective_opacity_s(sig_o, rescale, rescale ? E.opacity_scale[sid] : 1.0);
 
     Proj p;
     project_one(G, i, cam, p);
@@ -67,7 +67,7 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
     ShadeState sh;
     if (has_shading) {
         const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
-        shade_state(S, P, i, sid, mu, nrm, sh);
+        shade_state(S, P, i, sid, mu, nrm, sh, G.cache);
     }
 
     // ---- float32 blend record (rasterizer.py:151-153 casts) + skip bounds
@@ -178,6 +178,35 @@ shade_kernel(ivr_gaussians G, ivr_shading S, const int32_t *scene_id, ivr_frame_
     }
 }
 
+// Camera- and edit-independent per-Gaussian values for repeated frames of a
+// resident scene (same functions as the per-frame path: bit-identical).
+__global__ void __launch_bounds__(256)
+static_kernel(ivr_gaussians G, ivr_shading S, int has_shading, double *cache) {
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= G.n) return;
+    ivr_gaussians Gn = G;
+    Gn.cache = nullptr;
+    Proj p;
+    cov3d_one(Gn, i, p);
+    double nrm[3];
+    unit_normal(Gn, i, nrm);
+    double *c = cache + kCacheStride * i;
+    c[0] = p.C3[0]; c[1] = p.C3[1]; c[2] = p.C3[2];
+    c[3] = p.C3[4]; c[4] = p.C3[5]; c[5] = p.C3[8];
+    for (int k = 0; k < 3; ++k) c[6 + k] = nrm[k];
+    c[9] = sigmoid_ref(G.o_logit[i]);
+    if (has_shading) {
+        c[10] = sigmoid_ref(S.k_a_raw[i]);
+        c[11] = sigmoid_ref(S.k_d_raw[i]);
+        c[12] = sigmoid_ref(S.k_s_raw[i]);
+        c[13] = dadd(exp(S.log_beta[i]), 1.0);
+        c[14] = 1.0;
+    } else {
+        c[10] = c[11] = c[12] = c[13] = c[14] = 0.0;
+    }
+    c[15] = 0.0;
+}
+
 ivr_frame_params params_from(const ivr_camera &cam, const ivr_shading *S, const ivr_edits *E) {
     ivr_frame_params P{};
     P.cam = cam;
@@ -200,6 +229,22 @@ ivr_frame_params params_from(const ivr_camera &cam, const ivr_shading *S, const 
 }
 
 }  // namespace ivr
+
+extern "C" int ivr_preprocess_static(const ivr_gaussians *g, const ivr_shading *shading,
+                                     double *cache, ivr_stream_t stream) {
+    using namespace ivr;
+    if (!g || !cache || g->n < 0 || (g->n > 0 && (!g->q_raw || !g->log_s || !g->o_logit || !g->n_raw))) {
+        set_error("ivr_preprocess_static: bad argument");
+        return IVR_ERR_ARG;
+    }
+    if (g->n == 0) return IVR_OK;
+    ivr_shading S{};
+    if (shading) S = *shading;
+    const int threads = 256;
+    const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
+    static_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(*g, S, shading ? 1 : 0, cache);
+    return check_launch("static_kernel");
+}
 
 extern "C" int ivr_preprocess_fwd(const ivr_gaussians *g, const ivr_shading *shading,
                                   const ivr_edits *edits, const ivr_camera *cam,

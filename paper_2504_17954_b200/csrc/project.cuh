@@ -37,15 +37,43 @@ __device__ __forceinline__ void quat_rot(const double q[4], double R[9]) {
     R[8] = dsub(1.0, dmul(2.0, dadd(dmul(qx, qx), dmul(qy, qy))));
 }
 
-// gaussians.py:302-339, operation by operation.
-__device__ __forceinline__ void project_one(const ivr_gaussians &G, int64_t i,
-                                            const ivr_camera &cam, Proj &p) {
-    const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
+// Camera-independent part of the projection (gaussians.py:222-275, 305-310):
+// unit quaternion, scales, rotation and cov3d = (R S)(R S)^T.
+__device__ __forceinline__ void cov3d_one(const ivr_gaussians &G, int64_t i, Proj &p) {
     const double qr[4] = {G.q_raw[4 * i], G.q_raw[4 * i + 1], G.q_raw[4 * i + 2],
                           G.q_raw[4 * i + 3]};
     const double qn = norm4(qr[0], qr[1], qr[2], qr[3]);
     for (int k = 0; k < 4; ++k) p.q[k] = ddiv(qr[k], qn);
     for (int k = 0; k < 3; ++k) p.s[k] = exp(G.log_s[3 * i + k]);
+    quat_rot(p.q, p.R);
+    double M3[9];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) M3[3 * r + c] = dmul(p.R[3 * r + c], p.s[c]);
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c)
+            p.C3[3 * r + c] = chain3(M3[3 * r], M3[3 * c], M3[3 * r + 1], M3[3 * c + 1],
+                                     M3[3 * r + 2], M3[3 * c + 2]);
+}
+
+// Per-Gaussian static cache (ivr_preprocess_static): cov3d (xx xy xz yy yz
+// zz), unit normal, sigmoid(o_logit), sigmoid(k_a/k_d/k_s raw),
+// exp(log_beta)+1, has-shading flag, pad.
+constexpr int kCacheStride = 16;
+
+// gaussians.py:302-339, operation by operation.  With G.cache the
+// camera-independent cov3d comes from the cache (bit-identical values; q, s,
+// R are then not filled -- the geometry backward never uses a cache).
+__device__ __forceinline__ void project_one(const ivr_gaussians &G, int64_t i,
+                                            const ivr_camera &cam, Proj &p) {
+    const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
+    if (G.cache) {
+        const double *c = G.cache + kCacheStride * i;
+        p.C3[0] = c[0]; p.C3[1] = c[1]; p.C3[2] = c[2];
+        p.C3[3] = c[1]; p.C3[4] = c[3]; p.C3[5] = c[4];
+        p.C3[6] = c[2]; p.C3[7] = c[4]; p.C3[8] = c[5];
+    } else {
+        cov3d_one(G, i, p);
+    }
     const double *W = cam.rotation;
     const double d[3] = {dsub(mu[0], cam.position[0]), dsub(mu[1], cam.position[1]),
                          dsub(mu[2], cam.position[2])};
@@ -56,14 +84,6 @@ __device__ __forceinline__ void project_one(const ivr_gaussians &G, int64_t i,
     const double f = cam.focal;
     p.mx = dadd(ddiv(dmul(f, p.t[0]), p.tzs), cam.cx);
     p.my = dadd(ddiv(dmul(f, p.t[1]), p.tzs), cam.cy);
-    quat_rot(p.q, p.R);
-    double M3[9];
-    for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c) M3[3 * r + c] = dmul(p.R[3 * r + c], p.s[c]);
-    for (int r = 0; r < 3; ++r)
-        for (int c = 0; c < 3; ++c)
-            p.C3[3 * r + c] = chain3(M3[3 * r], M3[3 * c], M3[3 * r + 1], M3[3 * c + 1],
-                                     M3[3 * r + 2], M3[3 * c + 2]);
     const double tzs = p.tzs;
     p.J[0] = ddiv(f, tzs);
     p.J[1] = 0.0;
@@ -96,19 +116,28 @@ __device__ __forceinline__ void project_one(const ivr_gaussians &G, int64_t i,
 
 // GaussianGeometry.normals (eps 1e-12)
 __device__ __forceinline__ void unit_normal(const ivr_gaussians &G, int64_t i, double nrm[3]) {
+    if (G.cache) {
+        const double *c = G.cache + kCacheStride * i;
+        for (int k = 0; k < 3; ++k) nrm[k] = c[6 + k];
+        return;
+    }
     const double nr[3] = {G.n_raw[3 * i], G.n_raw[3 * i + 1], G.n_raw[3 * i + 2]};
     const double nn = dmax(norm3(nr[0], nr[1], nr[2]), 1e-12);
     for (int k = 0; k < 3; ++k) nrm[k] = ddiv(nr[k], nn);
 }
 
-// Effective opacity after the per-scene opacity edit (scene.py:214-220).
-__device__ __forceinline__ double effective_opacity(double o_logit, bool rescale, double scale) {
+// Effective opacity after the per-scene opacity edit (scene.py:214-220);
+// sig_o = sigmoid(o_logit) (computed here or taken from the static cache).
+__device__ __forceinline__ double effective_opacity_s(double sig_o, bool rescale, double scale) {
     if (rescale) {
-        double p = dmul(scale, sigmoid_ref(o_logit));
+        double p = dmul(scale, sig_o);
         p = p < 1e-12 ? 1e-12 : (p > 1.0 - 1e-9 ? 1.0 - 1e-9 : p);
-        o_logit = log(ddiv(p, dsub(1.0, p)));
+        return sigmoid_ref(log(ddiv(p, dsub(1.0, p))));
     }
-    return sigmoid_ref(o_logit);
+    return sig_o;
+}
+__device__ __forceinline__ double effective_opacity(double o_logit, bool rescale, double scale) {
+    return effective_opacity_s(sigmoid_ref(o_logit), rescale, scale);
 }
 
 // Shading forward state (shading.py:236-297) kept for the backward.
@@ -126,7 +155,8 @@ struct ShadeState {
 
 __device__ __forceinline__ void shade_state(const ivr_shading &S, const ivr_frame_params &P,
                                             int64_t i, int32_t sid, const double mu[3],
-                                            const double nrm[3], ShadeState &o) {
+                                            const double nrm[3], ShadeState &o,
+                                            const double *cache = nullptr) {
     const ivr_camera &cam = P.cam;
     for (int k = 0; k < 3; ++k) o.w_cam[k] = dsub(cam.position[k], mu[k]);
     const double wn = dmax(norm3(o.w_cam[0], o.w_cam[1], o.w_cam[2]), 1e-12);
@@ -144,10 +174,18 @@ __device__ __forceinline__ void shade_state(const ivr_shading &S, const ivr_fram
         const double un = dmax(norm3(o.u[0], o.u[1], o.u[2]), 1e-12);
         for (int k = 0; k < 3; ++k) o.h[k] = ddiv(o.u[k], un);
     }
-    o.sig[0] = sigmoid_ref(S.k_a_raw[i]);
-    o.sig[1] = sigmoid_ref(S.k_d_raw[i]);
-    o.sig[2] = sigmoid_ref(S.k_s_raw[i]);
-    o.beta1 = dadd(exp(S.log_beta[i]), 1.0);
+    if (cache && cache[kCacheStride * i + 14] != 0.0) {
+        const double *c = cache + kCacheStride * i;
+        o.sig[0] = c[10];
+        o.sig[1] = c[11];
+        o.sig[2] = c[12];
+        o.beta1 = c[13];
+    } else {
+        o.sig[0] = sigmoid_ref(S.k_a_raw[i]);
+        o.sig[1] = sigmoid_ref(S.k_d_raw[i]);
+        o.sig[2] = sigmoid_ref(S.k_s_raw[i]);
+        o.beta1 = dadd(exp(S.log_beta[i]), 1.0);
+    }
     double t[4];
     for (int k = 0; k < 3; ++k) t[k] = dadd(dmul(P.lam[k], o.sig[k]), P.b[k]);
     t[3] = dadd(dmul(P.lam[3], o.beta1), P.b[3]);

@@ -87,12 +87,38 @@ class DeviceGaussians:
         self.has_shading = shading is not None
         self.scene_id = to_dev(scene_id, torch.int32, dev) if scene_id is not None else None
         self.device = dev
+        self.cache = None
+
+    def build_cache(self):
+        """Camera-/edit-independent per-Gaussian values (ivr_preprocess_static)
+        for a scene rendered many times; later frames read them instead of
+        recomputing (bit-identical).  Invalidate with ``drop_cache`` if the
+        arrays change."""
+        self.cache = torch.empty((max(self.n, 1), 16), dtype=torch.float64, device=self.device)
+        self.cache_ok = False
+        g = self.struct()
+        sh = None
+        if self.has_shading:
+            sh = L.Shading_t()
+            for k in self.SHADE:
+                setattr(sh, k, self.t[k].data_ptr())
+        L.check(L.lib().ivr_preprocess_static(ctypes.byref(g), ctypes.byref(sh) if sh is not None
+                                              else None, ptr(self.cache), stream_handle()),
+                "ivr_preprocess_static")
+        self.cache_ok = True
+        return self
+
+    def drop_cache(self):
+        self.cache = None
+        self.cache_ok = False
 
     def struct(self) -> L.Gaussians_t:
         g = L.Gaussians_t()
         g.n = self.n
         for k in self.GEOM:
             setattr(g, k, self.t[k].data_ptr())
+        c = getattr(self, "cache", None)
+        g.cache = c.data_ptr() if c is not None and getattr(self, "cache_ok", False) else None
         return g
 
 

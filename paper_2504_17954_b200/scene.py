@@ -12,6 +12,7 @@ each render (scene.py:206-212).
 from __future__ import annotations
 
 import ctypes
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -203,6 +204,8 @@ class DeviceScene:
             ids = np.concatenate([np.full(len(m), i, dtype=np.int32) for i, m in enumerate(models)])
             dg = D.DeviceGaussians(geom, shad, ids, device)
         self.dg = dg  # or arrays already resident (ivrg.load_device)
+        if os.environ.get("IVR_STATIC_CACHE", "1") != "0":
+            dg.build_cache()  # frozen scene: camera-independent work done once
         self.n = self.dg.n
         self.n_scenes = len(models)
         self.ws = D.Workspace(self.dg.device)

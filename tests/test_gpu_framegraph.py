@@ -86,3 +86,27 @@ def test_pipeline_grows_pair_capacity():
     ref = ds.render(near, exact=False)
     assert np.array_equal(out.color, ref.color)
     assert fg.capacity > 4096
+
+
+def test_static_cache_is_bit_identical():
+    """K1 / K4b with the per-Gaussian static cache == without it (records,
+    depth keys, float64 parity outputs, images, inverse gradients)."""
+    import torch
+    from paper_2504_17954_b200 import DeviceScene
+    from paper_2504_17954_b200.synthetic import bench_camera
+    ds = DeviceScene(_scene())
+    assert ds.dg.cache is not None and ds.dg.cache_ok
+    cam = bench_camera(96, 80, 1.3)
+    kw = dict(debug=True, want_state=True, palettes=np.array([[0.9, 0.1, 0.1], [0.2, 0.8, 0.3],
+                                                               [0.1, 0.2, 0.9]]),
+              opacity_scales=np.array([1.0, 0.5, 1.7]))
+    a = ds.render_frame(cam, exact=True, **kw)
+    torch.cuda.synchronize()
+    got = {k: v.clone() for k, v in a.dbg.items()}
+    rec, keys, out = a.rec.clone(), a.depth_key.clone(), a.out.clone()
+    ds.dg.drop_cache()
+    b = ds.render_frame(cam, exact=True, **kw)
+    torch.cuda.synchronize()
+    for k, v in b.dbg.items():
+        assert torch.equal(got[k], v), k
+    assert torch.equal(rec, b.rec) and torch.equal(keys, b.depth_key) and torch.equal(out, b.out)
