@@ -217,14 +217,25 @@ def _device_time(fn, steps, warmup=2):
     return float(np.mean(ts)), float(np.median(ts))
 
 
-def bench_train(scene):
+def _max_over_ranks(x, dist):
+    import torch
+    if dist is None:
+        return x
+    t = torch.tensor([x], device="cuda", dtype=torch.float64)
+    dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    return float(t.item())
+
+
+def bench_train(scene, dist=None, world=1, rank=0):
     """C3: stage-2 training step (K=15 channels, fwd + all losses + bwd +
-    Adam) on one 300k-Gaussian basic model at 800x800, one view / iteration."""
+    Adam) on one 300k-Gaussian basic model at 800x800, one view / iteration.
+    With N ranks every rank trains its own basic TF (independent seeds, no
+    communication): aggregate it/s = N / slowest rank's ms per iteration."""
     from paper_2504_17954_b200 import LightConfig
     from paper_2504_17954_b200.device import to_dev
     from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
     from paper_2504_17954_b200.trainer import EditableTrainer, _stage2_init
-    a = editable_arrays(0, 300_000, density=300_000)
+    a = editable_arrays(rank, 300_000, density=300_000)
     light = LightConfig("orbital", 0.45, 0.9)
     cams = [bench_camera(W_IMG, H_IMG, az) for az in np.linspace(-3.0, 3.0, 8)]
     gt_tr = EditableTrainer(a, a["palette"], light)
@@ -240,20 +251,24 @@ def bench_train(scene):
         loss, grads, _ = tr.step(cams[v], gts[v])
         tr.apply(grads, it[0], 10000)
     mean_ms, med_ms = _device_time(step, 10)
+    mean_ms = _max_over_ranks(mean_ms, dist)
     return {"metric": "stage-2 train it/s (300k Gaussians, 800x800, K=15, 1 view/it)",
-            "value": 1000.0 / mean_ms, "unit": "it/s", "ms_per_it": mean_ms,
-            "ms_per_it_median": med_ms, "n_gaussians": 300_000,
+            "value": world * 1000.0 / mean_ms, "unit": "it/s", "ms_per_it": mean_ms,
+            "ms_per_it_median": med_ms, "n_gaussians": 300_000, "n_gpus": world,
+            "scaling": "weak (one basic TF per GPU)",
             "note": "includes fwd (K1-K3), L1+SSIM + normal/offset/bilateral/opacity terms, "
                     "K4a+K4b, Adam; densify excluded"}
 
 
-def bench_inverse(scene):
+def bench_inverse(scene, dist=None, world=1, rank=0):
     """C4: one inverse-exploration iteration on the composed 1M scene (render
-    f64-semantics + loss + transform-only backward + Adam), 1 view."""
+    f64-semantics + loss + transform-only backward + Adam).  N ranks shard N
+    views (one each); the packed transform gradient is all-reduced (NCCL,
+    31 float64) every iteration and every rank applies the same Adam."""
     from paper_2504_17954_b200.inverse import (Adam, InverseFitter, init_transform, reduce_views,
                                                transform_step)
     from paper_2504_17954_b200.synthetic import bench_camera
-    cam = bench_camera(W_IMG, H_IMG, 0.8)
+    cam = bench_camera(W_IMG, H_IMG, 0.8 + 0.7 * rank)
     p_true = init_transform(scene)
     p_true.lam = np.array([1.2, 0.8, 1.0, 1.0])
     fit0 = InverseFitter(scene, [], [])
@@ -265,13 +280,15 @@ def bench_inverse(scene):
 
     def step():
         loss, packed = fit.view_grads(params, 0)
-        mean, lv = reduce_views(packed, loss.reshape(1), 1.0)
+        mean, lv = reduce_views(packed, loss.reshape(1), float(world), dist=dist)
         transform_step(params, fit.unpack(mean), adam, 0.01,
                        ("c_p", "opacity_raw", "lam", "b", "angles"), angles)
     mean_ms, med_ms = _device_time(step, 10)
-    return {"metric": "inverse exploration it/s (composed 1M, 800x800, 1 view)",
-            "value": 1000.0 / mean_ms, "unit": "it/s", "ms_per_it": mean_ms,
-            "ms_per_it_median": med_ms,
+    mean_ms = _max_over_ranks(mean_ms, dist)
+    return {"metric": "inverse exploration it/s (composed 1M, 800x800, 1 view per GPU)",
+            "value": 1000.0 / mean_ms, "unit": "it/s", "views_per_s": world * 1000.0 / mean_ms,
+            "ms_per_it": mean_ms, "ms_per_it_median": med_ms, "n_gpus": world,
+            "scaling": "weak (views sharded, one NCCL all-reduce of 31 float64 per iteration)",
             "note": "includes the per-iteration pair-count sync and host Adam on 30 floats"}
 
 
@@ -300,11 +317,16 @@ def bench_vq(scene):
 def run_ours(args):
     import torch
     rank, local_rank, world = dist_env()
-    torch.cuda.set_device(local_rank)
+    dev_idx = local_rank % max(torch.cuda.device_count(), 1)
+    torch.cuda.set_device(dev_idx)
     dist = None
     if world > 1:
         import torch.distributed as dist
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        backend = os.environ.get("IVR_DIST_BACKEND", "nccl")  # gloo: functional test only
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", dev_idx))
+        else:
+            dist.init_process_group(backend)
     from paper_2504_17954_b200 import DeviceScene
     from paper_2504_17954_b200.synthetic import bench_camera, c2_scene
 
@@ -472,12 +494,15 @@ def run_ours(args):
                          "via oracle/ (numpy + C/OpenMP)"}
 
     extra = None
-    if world == 1 and not args.no_extra:
+    if not args.no_extra:
         extra = {}
-        for name, fn in (("train_c3", bench_train), ("inverse_c4", bench_inverse),
-                         ("vq_c5", bench_vq)):
+        jobs = [("train_c3", lambda: bench_train(scene, dist, world, rank)),
+                ("inverse_c4", lambda: bench_inverse(scene, dist, world, rank))]
+        if world == 1:  # VQ: replicas only, reported at N = 1
+            jobs.append(("vq_c5", lambda: bench_vq(scene)))
+        for name, fn in jobs:
             try:
-                extra[name] = fn(scene)
+                extra[name] = fn()
             except Exception as e:  # report, never hide the headline line
                 extra[name] = {"error": f"{type(e).__name__}: {e}"}
             torch.cuda.empty_cache()
