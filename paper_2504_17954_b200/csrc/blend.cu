@@ -274,13 +274,11 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                     const float au = a0.z * ex2_approx(-1.4426950408889634f * csig);
                     // relative error: sigma bound, argument rounding, ex2.approx, * o
                     const float rel = E + 1.2e-7f * csig + 3.6e-7f;
-                    if (au > 0.99f * (1.0f + rel)) {  // reference capped too: alpha = 0.99
-                        al = 0.99f;
-                        dal = 1.1e-8f;  // |0.99f - 0.99|
-                    } else {
-                        al = fminf(au, 0.99f);
-                        dal = au * rel;
-                    }
+                    // au certainly above the cap: the reference capped too (alpha =
+                    // 0.99, |0.99f - 0.99| < 1.1e-8); otherwise the f32 error bound
+                    const bool capped = au > 0.99f * (1.0f + rel);
+                    al = fminf(au, 0.99f);
+                    dal = capped ? 1.1e-8f : au * rel;
                 } else if (csig - E > a0.w) {
                     continue;  // certainly skipped: sigma_ref >= csig - E > hi >= thr_ref
                 } else {
@@ -297,8 +295,20 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                     dal = 6e-8f * al;
                 }
                 const float w = st.Tf * al;
+                if (KMAX % 4 == 0) {
+                    const float4 *vv = reinterpret_cast<const float4 *>(W.v + q * KMAX);
 #pragma unroll
-                for (int c = 0; c < KMAX; ++c) st.acc[c] = fmaf(w, W.v[q * KMAX + c], st.acc[c]);
+                    for (int c4 = 0; c4 < KMAX / 4; ++c4) {
+                        const float4 v = vv[c4];
+                        st.acc[4 * c4] = fmaf(w, v.x, st.acc[4 * c4]);
+                        st.acc[4 * c4 + 1] = fmaf(w, v.y, st.acc[4 * c4 + 1]);
+                        st.acc[4 * c4 + 2] = fmaf(w, v.z, st.acc[4 * c4 + 2]);
+                        st.acc[4 * c4 + 3] = fmaf(w, v.w, st.acc[4 * c4 + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < KMAX; ++c) st.acc[c] = fmaf(w, W.v[q * KMAX + c], st.acc[c]);
+                }
                 const float om = 1.0f - al;
                 st.Tf = st.Tf * om;
                 // errT carried pre-scaled by 1e-4 (the stop threshold):

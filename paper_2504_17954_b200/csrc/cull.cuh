@@ -17,11 +17,17 @@ __device__ __forceinline__ bool tile_cull32(const float4 r0, const float4 r1, in
     const float ha = r1.x, b = r1.y, hc = r1.z;  // a/2, b, c/2
     const float det4 = 4.0f * ha * hc;
     if (!(ha > 0.0f && hc > 0.0f && det4 - b * b > 1e-4f * det4)) return false;
-    const double mx = r0.x, my = r0.y;
-    const float ex0 = (float)(px0 - mx), ex1 = (float)(px1 - mx);
-    const float ey0 = (float)(py0 - my), ey1 = (float)(py1 - my);
+    // float subtraction of an exactly representable integer: one rounding of
+    // the exact difference, as before in double
+    const float ex0 = (float)px0 - r0.x, ex1 = (float)px1 - r0.x;
+    const float ey0 = (float)py0 - r0.y, ey1 = (float)py1 - r0.y;
     if (ex0 <= 0.0f && ex1 >= 0.0f && ey0 <= 0.0f && ey1 >= 0.0f) return false;
-    const float i2a = 0.5f / ha, i2c = 0.5f / hc;
+    // approximate reciprocals only move the candidate minimiser on each edge
+    // by <= |e| 2^-22 (e within the rectangle): a second-order change of the
+    // quadratic, far below the slack below
+    float i2a, i2c;
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(i2a) : "f"(2.0f * ha));
+    asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(i2c) : "f"(2.0f * hc));
     float best = 3.0e38f;
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
