@@ -516,8 +516,14 @@ __device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, in
             const uint32_t q = k - o_excl;
             const uint32_t tx0 = o_rx & 0xffffu, tx1 = o_rx >> 16, ty0 = o_rz & 0xffffu;
             const uint32_t w = tx1 - tx0 + 1;
-            const int ty = ok ? (int)(ty0 + q / w) : 0;
-            const int tx = ok ? (int)(tx0 + q % w) : 0;
+            // q / w via a float reciprocal (q, w < 2^16) and one correction
+            float rw;
+            asm("rcp.approx.ftz.f32 %0, %1;" : "=f"(rw) : "f"((float)w));
+            uint32_t qy = (uint32_t)((float)q * rw);
+            if (qy * w > q) --qy;
+            else if ((qy + 1) * w <= q) ++qy;
+            const int ty = ok ? (int)(ty0 + qy) : 0;
+            const int tx = ok ? (int)(tx0 + (q - qy * w)) : 0;
             f(ok, o_sp, ok ? ty * C.ntx + tx : -1, tx, ty);
         }
     }
@@ -593,10 +599,22 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
     const uint32_t lt = lanemask_lt();
     const int64_t rb = (int64_t)blockIdx.x * kRanksPerBlock + (int64_t)warp * kRanksPerWarp;
     const int64_t re = rb + kRanksPerWarp < C.n ? rb + kRanksPerWarp : C.n;
-    // phase 1: per-warp tile counts (<= 256 per tile per warp)
-    for (int64_t r = rb + lane; r < re; r += 32) {
-        const uint32_t sp = C.order[r];
-        if (C.count[sp] > 0) diff_add(Dw, w1, C.rect[sp], 1);
+    // phase 1: per-warp tile counts (<= 256 per tile per warp); the warp's
+    // 8 rank loads are issued together, then the dependent count / rect loads
+    {
+        constexpr int kPer = kRanksPerWarp / 32;
+        uint32_t sps[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            const int64_t r = rb + lane + 32 * u;
+            sps[u] = r < re ? __ldg(C.order + r) : 0xffffffffu;
+        }
+        int cnts[kPer];
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) cnts[u] = sps[u] != 0xffffffffu ? __ldg(C.count + sps[u]) : 0;
+#pragma unroll
+        for (int u = 0; u < kPer; ++u)
+            if (cnts[u] > 0) diff_add(Dw, w1, C.rect[sps[u]], 1);
     }
     __syncwarp();
     prefix2d(Dw, w1, h1, lane, 32, [] { __syncwarp(); });
@@ -620,11 +638,12 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
     expand_pairs(C, rb, re, [&](bool ok, uint32_t sp, int tile, int tx, int ty) {
         const uint32_t peers = __match_any_sync(0xffffffffu, tile);
         const int cell = ty * w1 + tx;
+        // the first lane of each equal-tile group advances the warp's running
+        // count for that tile and shares the old value with its peers
+        const int leader = __ffs(peers) - 1;
         int before = 0;
-        if (ok) before = Dw[cell];
-        __syncwarp();
-        if (ok && (peers & lt) == 0) Dw[cell] = before + __popc(peers);
-        __syncwarp();
+        if (ok && lane == leader) before = atomicAdd(&Dw[cell], __popc(peers));
+        before = __shfl_sync(0xffffffffu, before, leader);
         if (ok) {
             const uint32_t pos = s_base[cell] + (uint32_t)before + __popc(peers & lt);
             if ((int64_t)pos < C.cap) {
