@@ -72,6 +72,9 @@ vq_assign_kernel(const double *__restrict__ values, int64_t n, const double *__r
     }
     const double lo = params[0], inv_w = params[2];
     const bool use_lut = SMEM && inv_w > 0.0;
+    // the bucket index only narrows the search (every answer is verified
+    // against exact float64 compares), so it is computed in float32
+    const float lo_f = (float)lo, inv_w_f = (float)inv_w;
     constexpr int kVqIlp = 8;
     const int64_t chunk = (int64_t)kVqThreads * kVqIlp;
     for (int64_t base = (int64_t)blockIdx.x * chunk; base < n; base += (int64_t)gridDim.x * chunk) {
@@ -90,8 +93,8 @@ vq_assign_kernel(const double *__restrict__ values, int64_t n, const double *__r
                 pos = nm;  // NaN sorts last
             } else if (SMEM) {
                 if (use_lut) {
-                    const double t = (v[r] - lo) * inv_w;
-                    const int b = t < 0.0 ? 0 : (t >= (double)(kLut - 1) ? kLut - 1 : (int)t);
+                    const float t = ((float)v[r] - lo_f) * inv_w_f;
+                    const int b = t < 0.0f ? 0 : (t >= (float)(kLut - 1) ? kLut - 1 : (int)t);
                     int a = b >= 1 ? s_lut[b - 1] : 0;
                     const int zi = b + 2 < kLut ? s_lut[b + 2] : nm;
                     int z = zi;
