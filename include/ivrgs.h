@@ -284,6 +284,21 @@ int ivr_vq_assign(const double *values, int64_t n, const double *centroids,
 int ivr_vq_decode(const uint16_t *indices, int64_t n, const double *centroids,
                   int32_t k, double *out, int64_t *bad, ivr_stream_t stream);
 
+/* Fused Lloyd iteration, vq._lloyd (vq.py:75-87): assign every value to
+ * its nearest sorted centroid (as ivr_vq_assign), per-centroid sums and
+ * counts (shared-memory privatised), new = counts > 0 ? sums / counts : old,
+ * shift[0] = max |new - old| (device).  2 <= k <= 4097. */
+size_t ivr_kmeans_lloyd_workspace_size(int32_t k);
+int ivr_kmeans_lloyd_step(const double *values, int64_t n, const double *centroids, int32_t k,
+                          double *new_centroids, double *shift, void *workspace,
+                          size_t workspace_bytes, ivr_stream_t stream);
+
+/* Compose on the device (scene.py:147-186, gaussians.py:98-106): concatenate
+ * n_src (<= 64) row-major float64 arrays of `width` columns (rows[m] rows
+ * each) into dst; scene_id (may be NULL) receives the source index per row. */
+int ivr_concat(const double *const *srcs, const int64_t *rows, int32_t n_src, int32_t width,
+               double *dst, int32_t *scene_id, ivr_stream_t stream);
+
 /* Stage-1 colour: eval_sh(ShColor, view_dirs(mu, cam_pos))
  * (gaussians.py:497-508, 521-524).  coeffs (n, (degree+1)^2, 3) float64,
  * degree 0..3; rgb (n,3) = max(sum_b basis_b * coeffs_b + 0.5, 0). */

@@ -18,7 +18,7 @@ from .rasterizer import (  # noqa: F401
 )
 from .scene import (  # noqa: F401
     BasicSceneModel, ComposedScene, DeviceScene, EditState, EffectiveScene, FrameGraph, FramePipeline,
-    apply_edits, render_composed,
+    apply_edits, compose_device, render_composed,
 )
 from .shading import (  # noqa: F401
     LightConfig, Palette, ShadingAttributes, shade_backward, shade_gaussians,

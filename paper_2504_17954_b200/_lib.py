@@ -134,6 +134,11 @@ _SIGS = {
     "ivr_pack_f32": ([P, ctypes.c_int64, P, P], ctypes.c_int),
     "ivr_preprocess_static": ([ctypes.POINTER(Gaussians_t), ctypes.POINTER(Shading_t), P, P],
                               ctypes.c_int),
+    "ivr_kmeans_lloyd_workspace_size": ([ctypes.c_int32], ctypes.c_size_t),
+    "ivr_kmeans_lloyd_step": ([P, ctypes.c_int64, P, ctypes.c_int32, P, P, P, ctypes.c_size_t, P],
+                              ctypes.c_int),
+    "ivr_concat": ([ctypes.POINTER(P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32,
+                    ctypes.c_int32, P, P, P], ctypes.c_int),
     "ivr_adam_step": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
                        ctypes.c_double, ctypes.c_double, P], ctypes.c_int),
     "ivr_regularize_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),

@@ -176,6 +176,124 @@ static int grid_for(int64_t n) {
 
 }  // namespace ivr
 
+namespace ivr {
+
+// Fused Lloyd step: assign (as K5) + per-centroid sums / counts privatised in
+// shared memory (float64 sums, u32 counts), flushed with one global atomic per
+// centroid per CTA.
+__global__ void __launch_bounds__(kVqThreads)
+lloyd_accum_kernel(const double *__restrict__ values, int64_t n, const double *__restrict__ cents,
+                   int k, const uint16_t *__restrict__ lut, const double *__restrict__ params,
+                   double *sums, unsigned long long *counts) {
+    extern __shared__ __align__(16) double sm_l[];
+    double *s_mid = sm_l;                                   // k - 1
+    double *s_sum = s_mid + kVqSmemMids;                    // k
+    unsigned int *s_cnt = reinterpret_cast<unsigned int *>(s_sum + kVqSmemMids + 1);  // k
+    uint16_t *s_lut = reinterpret_cast<uint16_t *>(s_cnt + kVqSmemMids + 1);        // kLut
+    const int nm = k - 1;
+    for (int i = threadIdx.x; i < nm; i += kVqThreads) s_mid[i] = vq_mid(cents, i);
+    for (int i = threadIdx.x; i < k; i += kVqThreads) {
+        s_sum[i] = 0.0;
+        s_cnt[i] = 0u;
+    }
+    for (int i = threadIdx.x; i < kLut; i += kVqThreads) s_lut[i] = lut[i];
+    __syncthreads();
+    const double lo = params[0], inv_w = params[2];
+    const float lo_f = (float)lo, inv_w_f = (float)inv_w;
+    for (int64_t i = (int64_t)blockIdx.x * kVqThreads + threadIdx.x; i < n;
+         i += (int64_t)gridDim.x * kVqThreads) {
+        const double v = values[i];
+        int pos;
+        if (v != v) {
+            pos = nm;
+        } else if (inv_w > 0.0) {
+            const float t = ((float)v - lo_f) * inv_w_f;
+            const int b = t < 0.0f ? 0 : (t >= (float)(kLut - 1) ? kLut - 1 : (int)t);
+            int a = b >= 1 ? s_lut[b - 1] : 0;
+            const int zi = b + 2 < kLut ? s_lut[b + 2] : nm;
+            int z = zi;
+            const int a0 = a;
+            while (a < z) {
+                const int m = (a + z) >> 1;
+                if (s_mid[m] < v) a = m + 1;
+                else z = m;
+            }
+            pos = a;
+            const bool ok_lo = pos > a0 || a0 == 0 || s_mid[a0 - 1] < v;
+            const bool ok_hi = pos < zi || zi == nm || !(s_mid[zi] < v);
+            if (!(ok_lo && ok_hi)) pos = vq_full_search(s_mid, nm, v);
+        } else {
+            pos = vq_full_search(s_mid, nm, v);
+        }
+        atomicAdd(&s_sum[pos], v);
+        atomicAdd(&s_cnt[pos], 1u);
+    }
+    __syncthreads();
+    for (int i = threadIdx.x; i < k; i += kVqThreads) {
+        if (s_cnt[i]) {
+            atomicAdd(&sums[i], s_sum[i]);
+            atomicAdd(&counts[i], (unsigned long long)s_cnt[i]);
+        }
+    }
+}
+
+// new = counts > 0 ? sums / counts : c (vq.py:81-83); shift[0] = max |new - c|
+__global__ void __launch_bounds__(1024)
+lloyd_finish_kernel(const double *cents, int k, const double *sums, const unsigned long long *counts,
+                    double *out, double *shift) {
+    __shared__ double s_red[32];
+    double m = 0.0;
+    for (int i = threadIdx.x; i < k; i += 1024) {
+        const double nw = counts[i] > 0 ? sums[i] / (double)counts[i] : cents[i];
+        out[i] = nw;
+        m = fmax(m, fabs(nw - cents[i]));
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) m = fmax(m, __shfl_xor_sync(0xffffffffu, m, o));
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = m;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < 32; ++w) t = fmax(t, s_red[w]);
+        *shift = t;
+    }
+}
+
+}  // namespace ivr
+
+extern "C" size_t ivr_kmeans_lloyd_workspace_size(int32_t k) {
+    return 4 * sizeof(double) + 2 * (size_t)ivr::kLut + 256 + 16 * (size_t)(k < 1 ? 1 : k);
+}
+
+extern "C" int ivr_kmeans_lloyd_step(const double *values, int64_t n, const double *centroids,
+                                     int32_t k, double *new_centroids, double *shift,
+                                     void *workspace, size_t workspace_bytes, ivr_stream_t stream) {
+    using namespace ivr;
+    if (n < 1 || k < 2 || k - 1 > kVqSmemMids || !values || !centroids || !new_centroids ||
+        !shift || !workspace || workspace_bytes < ivr_kmeans_lloyd_workspace_size(k)) {
+        set_error("ivr_kmeans_lloyd_step: bad argument (2 <= k <= 4097, workspace)");
+        return IVR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    char *ws = (char *)workspace;
+    double *params = reinterpret_cast<double *>(ws);
+    uint16_t *lut = reinterpret_cast<uint16_t *>(params + 4);
+    char *acc = ws + ((4 * sizeof(double) + 2 * (size_t)kLut + 255) & ~(size_t)255);
+    double *sums = reinterpret_cast<double *>(acc);
+    unsigned long long *counts = reinterpret_cast<unsigned long long *>(sums + k);
+    if (cudaMemsetAsync(acc, 0, 16 * (size_t)k, st) != cudaSuccess)
+        return check_launch("ivr_kmeans_lloyd_step memset");
+    vq_lut_kernel<<<(kLut + kVqThreads - 1) / kVqThreads, kVqThreads, 0, st>>>(centroids, k, lut,
+                                                                              params);
+    const size_t smem = 8 * (size_t)(2 * kVqSmemMids + 1) + 4 * (size_t)(kVqSmemMids + 1) +
+                        2 * (size_t)kLut;
+    cudaFuncSetAttribute(lloyd_accum_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    lloyd_accum_kernel<<<grid_for(n), kVqThreads, smem, st>>>(values, n, centroids, k, lut, params,
+                                                              sums, counts);
+    lloyd_finish_kernel<<<1, 1024, 0, st>>>(centroids, k, sums, counts, new_centroids, shift);
+    return check_launch("ivr_kmeans_lloyd_step");
+}
+
 extern "C" size_t ivr_vq_assign_workspace_size(void) {
     return 4 * sizeof(double) + 2 * (size_t)ivr::kLut;
 }

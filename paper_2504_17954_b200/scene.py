@@ -554,6 +554,44 @@ class FramePipeline:
         return _unpack(self.h_out[k].numpy(), fg.F.layout, self.h_cnt[k].numpy())
 
 
+def compose_device(models, palettes, light=None, metadata=None):
+    """ComposedScene.compose for models already resident in HBM
+    (scene.py:147-186): one batched device copy per attribute (ivr_concat)
+    into the concatenated SoA + scene ids; returns a DeviceScene.  ``models``
+    are DeviceGaussians with shading attributes, ``palettes`` their c_p."""
+    from .ivrg import ResidentModel
+    if not models:
+        raise ShapeMismatch("compose needs at least one model")
+    if any(not m.has_shading for m in models):
+        raise MixedStage("only editable-stage models compose")
+    dev = models[0].device
+    rows = [m.n for m in models]
+    N = sum(rows)
+    widths = {"mu": 3, "q_raw": 4, "log_s": 3, "o_logit": 1, "n_raw": 3, "delta_c": 3,
+              "k_a_raw": 1, "k_d_raw": 1, "k_s_raw": 1, "log_beta": 1}
+    out = {}
+    ids = torch.empty(N, dtype=torch.int32, device=dev)
+    c_rows = (ctypes.c_int64 * len(models))(*rows)
+    for j, (name, w) in enumerate(widths.items()):
+        dst = torch.empty((N, w) if w > 1 else (N,), dtype=torch.float64, device=dev)
+        srcs = (ctypes.c_void_p * len(models))(*[m.t[name].data_ptr() for m in models])
+        L.check(L.lib().ivr_concat(srcs, c_rows, len(models), w, D.ptr(dst),
+                                   D.ptr(ids) if j == 0 else None, D.stream_handle()),
+                "ivr_concat")
+        out[name] = dst
+    dg = D.DeviceGaussians({k: out[k] for k in D.DeviceGaussians.GEOM},
+                           {k: out[k] for k in D.DeviceGaussians.SHADE}, None, dev)
+    dg.scene_id = ids
+    stubs, row = [], 0
+    for i, m in enumerate(models):
+        stubs.append(ResidentModel(STAGE_EDITABLE, m.n, dict((metadata or {}).get(i, {})),
+                                   Palette(np.asarray(palettes[i], np.float64)), None,
+                                   (row, row + m.n)))
+        row += m.n
+    sc = ComposedScene(stubs, [EditState() for _ in models], light or LightConfig())
+    return DeviceScene(sc, dg=dg)
+
+
 def render_composed(scene, cam, channels=("color", "alpha"), attrs=None, dtype=np.float32,
                     sequential=False):
     """Shade and rasterize a composed scene for one camera (scene.py:231-239).

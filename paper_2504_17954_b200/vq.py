@@ -168,13 +168,25 @@ def _lloyd(x, c):
     update with bincount sums (float64)."""
     scale = max(float(x.abs().max()), 1e-12)
     k = c.numel()
+    fused = 2 <= k <= 4097
+    if fused:
+        nb = L.lib().ivr_kmeans_lloyd_workspace_size(k)
+        ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+        shift_d = torch.empty(1, dtype=torch.float64, device=x.device)
     for _ in range(KMEANS_MAX_ITERS):
         c = torch.sort(c).values
-        idx = _assign_idx(x, c)
-        sums = torch.bincount(idx, weights=x, minlength=k)
-        cnt = torch.bincount(idx, minlength=k)
-        new = torch.where(cnt > 0, sums / torch.clamp(cnt, min=1).to(torch.float64), c)
-        shift = float((new - c).abs().max()) / scale
+        if fused:  # assign + sums + counts + update in one pass (csrc/vq.cu)
+            new = torch.empty_like(c)
+            L.check(L.lib().ivr_kmeans_lloyd_step(D.ptr(x), x.numel(), D.ptr(c), k, D.ptr(new),
+                                                  D.ptr(shift_d), D.ptr(ws), nb,
+                                                  D.stream_handle()), "ivr_kmeans_lloyd_step")
+            shift = float(shift_d.item()) / scale
+        else:
+            idx = _assign_idx(x, c)
+            sums = torch.bincount(idx, weights=x, minlength=k)
+            cnt = torch.bincount(idx, minlength=k)
+            new = torch.where(cnt > 0, sums / torch.clamp(cnt, min=1).to(torch.float64), c)
+            shift = float((new - c).abs().max()) / scale
         c = new
         if shift < KMEANS_SHIFT_TOL:
             break

@@ -110,3 +110,22 @@ def test_static_cache_is_bit_identical():
     for k, v in b.dbg.items():
         assert torch.equal(got[k], v), k
     assert torch.equal(rec, b.rec) and torch.equal(keys, b.depth_key) and torch.equal(out, b.out)
+
+
+def test_compose_device_matches_host_compose():
+    """compose_device (ivr_concat of resident models) renders bit-identically
+    to DeviceScene(ComposedScene.compose(host models)) with edits."""
+    from paper_2504_17954_b200 import ComposedScene, DeviceScene, LightConfig, compose_device
+    from paper_2504_17954_b200.device import DeviceGaussians
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_model
+    models = [editable_model(20 + i, 3000 + 500 * i, density=20_000) for i in range(3)]
+    light = LightConfig("orbital", 0.4, 1.0, np.array([1.1, 0.9, 1.0, 1.0]))
+    host = DeviceScene(ComposedScene.compose(models, light))
+    dev = compose_device([DeviceGaussians(m.geometry, m.shading) for m in models],
+                         [m.palette.c_p for m in models], light)
+    assert int(dev.dg.scene_id[-1]) == 2 and dev.n == host.n
+    cam = bench_camera(96, 72, 0.6)
+    kw = dict(palettes=np.array([[0.9, 0.1, 0.1], [0.2, 0.8, 0.3], [0.1, 0.2, 0.9]]),
+              opacity_scales=np.array([1.0, 0.5, 1.0]))
+    a, b = dev.render(cam, **kw), host.render(cam, **kw)
+    assert np.array_equal(a.color, b.color) and np.array_equal(a.alpha, b.alpha)
