@@ -47,7 +47,7 @@ def launches_per_frame(n):
     return 1 + (3 + 3 * passes + 2 + 2 + 4) + 1 + 1
 
 
-SLOTS = 4  # concurrent frame slots (FrameGraph / FramePipeline)
+SLOTS = int(os.environ.get("IVR_SLOTS", "6"))  # concurrent frame slots (FrameGraph / FramePipeline)
 
 
 def parse():
@@ -168,7 +168,7 @@ def config_dict(n, extra=None):
          "n_gaussians": n, "width": W_IMG, "height": H_IMG, "channels": "rgba",
          "dtype_mode": "float32 (reference default)",
          "l2": "inputs larger than L2 (scene 168 MB float64 > 126 MB); frames streamed on "
-               "4 concurrent slots; frame_ms_isolated = each frame alone after an L2 flush"}
+               "6 concurrent slots; frame_ms_isolated = each frame alone after an L2 flush"}
     if extra:
         d.update(extra)
     return d
@@ -517,7 +517,7 @@ def run_ours(args):
                 "e2e": {"value": e2e_fps, "unit": "frames/s",
                         "h2d_bytes_per_step": pipe.h2d_bytes_per_frame(),
                         "d2h_bytes_per_step": pipe.d2h_bytes_per_frame(),
-                        "pipelined": "frames on 4 concurrent slots; each frame's D2H overlaps "
+                        "pipelined": "frames on 6 concurrent slots; each frame's D2H overlaps "
                                      "later frames' upload+compute; host wall clock over all frames"},
                 "gpu_launches": launches_per_frame(n) * args.steps, "overflow": overflow,
                 "extra": extra}
