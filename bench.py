@@ -314,6 +314,31 @@ def bench_vq(scene):
             "alg_bytes_per_value": 10}
 
 
+def bench_service(scene):
+    """§8(f) service frame path: one 800x800 'shaded' frame rendered (float64
+    semantics, as render_mode_image) and delivered as PNG bytes / raw uint8 on
+    the host (device display + PNG assembly, one D2H per frame)."""
+    import time as _t
+    from paper_2504_17954_b200.render_modes import DisplayRenderer
+    from paper_2504_17954_b200.synthetic import bench_camera
+    R = DisplayRenderer(scene)
+    cams = [bench_camera(W_IMG, H_IMG, 0.1 * i) for i in range(12)]
+    res = {}
+    for fmt in ("png", "raw"):
+        for c in cams[:2]:
+            R.frame_bytes(c, "shaded", fmt)
+        t0 = _t.perf_counter()
+        nb = 0
+        for c in cams:
+            nb = len(R.frame_bytes(c, "shaded", fmt))
+        dt = (_t.perf_counter() - t0) / len(cams)
+        res[fmt] = {"frames_per_s": 1.0 / dt, "bytes_per_frame": nb}
+    return {"metric": "service frames/s (800x800 shaded, float64 render, bytes on the host)",
+            "png": res["png"], "raw": res["raw"],
+            "note": "host wall clock per synchronous frame (render + display kernel + device PNG "
+                    "+ D2H); reference: render_mode_image + PIL png_bytes on the CPU"}
+
+
 def run_ours(args):
     import torch
     rank, local_rank, world = dist_env()
@@ -498,8 +523,9 @@ def run_ours(args):
         extra = {}
         jobs = [("train_c3", lambda: bench_train(scene, dist, world, rank)),
                 ("inverse_c4", lambda: bench_inverse(scene, dist, world, rank))]
-        if world == 1:  # VQ: replicas only, reported at N = 1
+        if world == 1:  # VQ / service frames: replicas only, reported at N = 1
             jobs.append(("vq_c5", lambda: bench_vq(scene)))
+            jobs.append(("service_frames", lambda: bench_service(scene)))
         for name, fn in jobs:
             try:
                 extra[name] = fn()

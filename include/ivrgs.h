@@ -326,6 +326,23 @@ int ivr_unpack(const uint8_t *src, int64_t count, int32_t kind, void *dst, ivr_s
 /* double -> little-endian f32 bytes (_f32_bytes, scene.py:243-244). */
 int ivr_pack_f32(const double *src, int64_t count, uint8_t *dst, ivr_stream_t stream);
 
+/* Service frame path (render_modes.py:31-110, service.py:169-187): uint8
+ * display image from a float64 render (H,W,k) with columns cols = {color,
+ * alpha, depth, normal}.  mode 0: shaded RGBA (colour clipped to [0,1]),
+ * 1: alpha (L), 2: unit normal mapped to [0,1] (RGB), 3: depth normalised
+ * over covered pixels (L).  to_uint8 = clip(round(255 x)), round half to
+ * even.  workspace: 64 device bytes. */
+int ivr_display_u8(const double *out, int32_t height, int32_t width, int32_t k,
+                   const int32_t cols[4], int32_t mode, uint8_t *dst, void *workspace,
+                   ivr_stream_t stream);
+
+/* PNG of a uint8 image (1, 3 or 4 channels) built on the device: filter-0
+ * rows in stored deflate blocks, zlib adler32 and chunk CRCs computed in
+ * parallel.  out (device) needs ivr_png_size() bytes; workspace 64 bytes. */
+int64_t ivr_png_size(int32_t height, int32_t width, int32_t channels);
+int ivr_png_encode(const uint8_t *img, int32_t height, int32_t width, int32_t channels,
+                   uint8_t *out, int64_t out_cap, void *workspace, ivr_stream_t stream);
+
 /* Photometric objective, losses.ssim + losses.photometric_loss
  * (losses.py:45-138), float64: pred/gt (H,W,C); window = the reference's
  * normalized 11-tap Gaussian (sigma 1.5).  Writes

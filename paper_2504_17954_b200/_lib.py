@@ -139,6 +139,11 @@ _SIGS = {
                               ctypes.c_int),
     "ivr_concat": ([ctypes.POINTER(P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32,
                     ctypes.c_int32, P, P, P], ctypes.c_int),
+    "ivr_display_u8": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                        ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, P, P, P], ctypes.c_int),
+    "ivr_png_size": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32], ctypes.c_int64),
+    "ivr_png_encode": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32, P, ctypes.c_int64, P, P],
+                       ctypes.c_int),
     "ivr_adam_step": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
                        ctypes.c_double, ctypes.c_double, P], ctypes.c_int),
     "ivr_regularize_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),

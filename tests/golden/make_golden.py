@@ -322,6 +322,31 @@ def ivrg_case():
     print("ivrg")
 
 
+def display_case():
+    """render_modes.render_mode_image for every mode on a composed scene with
+    edits (render_modes.py:31-72) and a base-stage model."""
+    from voxsplat.gaussians import ShColor
+    from voxsplat.render_modes import RENDER_MODES, render_mode_image, to_uint8
+    from voxsplat.scene import STAGE_BASE
+    sc = ComposedScene.compose([model_from(editable_arrays(70 + i, 1500, spread=0.5, density=3000))
+                                for i in range(2)],
+                               LightConfig("orbital", 0.3, 0.7, np.array([1.1, 0.9, 1.0, 1.2])))
+    sc.edits[1] = EditState(np.array([0.2, 0.7, 0.4]), 0.6)
+    cam = orbit_camera(np.zeros(3), 2.4, 0.35, 0.5, 0.9, 40, 32)
+    d = cam_dict(cam)
+    for mode in RENDER_MODES:
+        img = render_mode_image(sc, cam, mode)
+        d["img_" + mode] = img
+        d["u8_" + mode] = to_uint8(img)
+    a = editable_arrays(75, 1200, spread=0.5, density=3000)
+    sh = ShColor(np.random.default_rng(75).normal(0, 0.4, (1200, 4, 3)), 1)
+    base = BasicSceneModel(STAGE_BASE, GaussianGeometry(*(a[k] for k in GEOM_KEYS)), sh=sh)
+    for mode in ("shaded", "alpha", "normal", "depth"):
+        d["base_" + mode] = render_mode_image(base, cam, mode)
+    np.savez_compressed(os.path.join(HERE, "display.npz"), **d)
+    print("display")
+
+
 if __name__ == "__main__":
     import sys as _sys
     if len(_sys.argv) > 1:  # regenerate selected cases only
@@ -346,3 +371,4 @@ if __name__ == "__main__":
     sh_case()
     stage1_case()
     ivrg_case()
+    display_case()
