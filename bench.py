@@ -339,6 +339,28 @@ def bench_service(scene):
                     "+ D2H); reference: render_mode_image + PIL png_bytes on the CPU"}
 
 
+def bench_dvr(scene):
+    """§8(f) 4: ground-truth volume rendering for dataset generation, one
+    800x800 view of a 128^3 'lobes' volume (float64 ray march on the GPU)."""
+    from paper_2504_17954_b200 import LightConfig, orbit_camera
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.dvr import (TransferFunction1D, make_volume, render_view_device,
+                                           union_transfer_functions)
+    vol = make_volume("lobes", (128, 128, 128))
+    tf = union_transfer_functions([TransferFunction1D.basic_bump(0.2, 0.45, (0.9, 0.3, 0.2), 0.8),
+                                   TransferFunction1D.basic_bump(0.55, 0.8, (0.2, 0.5, 0.9), 0.6)])
+    vals = to_dev(vol.values)
+    cams = [orbit_camera(np.zeros(3), 330.0, 0.3, a, 0.8, W_IMG, H_IMG) for a in np.linspace(0, 6, 6)]
+    it = [0]
+
+    def one():
+        render_view_device(vol, tf, cams[it[0] % len(cams)], LightConfig(), dev_values=vals)
+        it[0] += 1
+    mean_ms, med_ms = _device_time(one, 5)
+    return {"metric": "DVR views/s (800x800, 128^3 volume, float64 ray march)",
+            "value": 1000.0 / mean_ms, "unit": "views/s", "ms_per_view": mean_ms}
+
+
 def run_ours(args):
     import torch
     rank, local_rank, world = dist_env()
@@ -526,6 +548,7 @@ def run_ours(args):
         if world == 1:  # VQ / service frames: replicas only, reported at N = 1
             jobs.append(("vq_c5", lambda: bench_vq(scene)))
             jobs.append(("service_frames", lambda: bench_service(scene)))
+            jobs.append(("dvr_views", lambda: bench_dvr(scene)))
         for name, fn in jobs:
             try:
                 extra[name] = fn()

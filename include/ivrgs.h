@@ -326,6 +326,17 @@ int ivr_unpack(const uint8_t *src, int64_t count, int32_t kind, void *dst, ivr_s
 /* double -> little-endian f32 bytes (_f32_bytes, scene.py:243-244). */
 int ivr_pack_f32(const double *src, int64_t count, uint8_t *dst, ivr_stream_t stream);
 
+/* Ground-truth direct volume rendering (dvr.render_view, dvr.py:197-452):
+ * float64 ray march of a (d0,d1,d2) C-order volume centred on the origin
+ * with voxel spacing[3] through an n_tf-point piecewise-linear transfer
+ * function, Blinn-Phong material {k_a, k_d, k_s, beta}, headlight or
+ * light_dir; out (H,W,4) float64 premultiplied RGBA.  One thread per ray. */
+int ivr_dvr_render(const double *values, int32_t d0, int32_t d1, int32_t d2,
+                   const double spacing[3], const double *tf_values, const double *tf_colors,
+                   const double *tf_opacities, int32_t n_tf, const ivr_camera *cam,
+                   int32_t headlight, const double light_dir[3], const double material[4],
+                   double step_scale, double *out, ivr_stream_t stream);
+
 /* Service frame path (render_modes.py:31-110, service.py:169-187): uint8
  * display image from a float64 render (H,W,k) with columns cols = {color,
  * alpha, depth, normal}.  mode 0: shaded RGBA (colour clipped to [0,1]),

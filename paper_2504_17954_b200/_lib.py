@@ -139,6 +139,10 @@ _SIGS = {
                               ctypes.c_int),
     "ivr_concat": ([ctypes.POINTER(P), ctypes.POINTER(ctypes.c_int64), ctypes.c_int32,
                     ctypes.c_int32, P, P, P], ctypes.c_int),
+    "ivr_dvr_render": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                        ctypes.POINTER(ctypes.c_double), P, P, P, ctypes.c_int32,
+                        ctypes.POINTER(Camera_t), ctypes.c_int32, ctypes.POINTER(ctypes.c_double),
+                        ctypes.POINTER(ctypes.c_double), ctypes.c_double, P, P], ctypes.c_int),
     "ivr_display_u8": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                         ctypes.POINTER(ctypes.c_int32), ctypes.c_int32, P, P, P], ctypes.c_int),
     "ivr_png_size": ([ctypes.c_int32, ctypes.c_int32, ctypes.c_int32], ctypes.c_int64),

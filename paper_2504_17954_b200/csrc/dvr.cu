@@ -1,0 +1,235 @@
+// Ground-truth direct volume rendering on the device (dataset generation).
+//
+// Replaces dvr._raymarch_image / _raymarch_ray / _trilinear / _tf_lookup /
+// shade_sample (dvr.py:197-433): one thread per pixel ray, float64 with the
+// reference's operation order (the TU is built with -fmad=false; numba emits
+// no FMA): slab intersection with the volume box, samples every dt from
+// tmin + dt/2, trilinear value (clamped), piecewise-linear transfer function,
+// opacity correction 1 - (1 - a)^(dt / step_ref), central-difference gradient
+// normal (one voxel apart, flat -> view direction), Blinn-Phong, front-to-back
+// compositing with the T < 1e-4 stop.  The volume (a few MB) stays L2/L1
+// resident; the march is FP64 bound (pow and 7 trilinear samples per shaded
+// sample).
+#include <math.h>
+
+#include "ivr_common.cuh"
+
+namespace ivr {
+namespace dvrk {
+
+constexpr double kTStopDvr = 1e-4;
+constexpr double kFlatGradient = 1e-6;
+
+struct Args {
+    const double *values;  // (d0, d1, d2) C order
+    int d0, d1, d2;
+    double origin[3], spacing[3], lo[3], hi[3];
+    const double *tf_v, *tf_rgb, *tf_o;
+    int ntf;
+    double cam_pos[3], rot_t[9];  // rot_t = rotation^T (camera -> world)
+    double focal, cx, cy;
+    int W, H;
+    double dt, step_ref;
+    int headlight;
+    double light_dir[3];
+    double k_a, k_d, k_s, beta;
+    double *out;  // (H, W, 4)
+};
+
+__device__ __forceinline__ double trilinear(const Args &A, const double p[3]) {
+    double fx = (p[0] - A.origin[0]) / A.spacing[0];
+    double fy = (p[1] - A.origin[1]) / A.spacing[1];
+    double fz = (p[2] - A.origin[2]) / A.spacing[2];
+    fx = fmin(fmax(fx, 0.0), A.d0 - 1.000001);
+    fy = fmin(fmax(fy, 0.0), A.d1 - 1.000001);
+    fz = fmin(fmax(fz, 0.0), A.d2 - 1.000001);
+    const int i0 = (int)fx, j0 = (int)fy, k0 = (int)fz;
+    const double tx = fx - i0, ty = fy - j0, tz = fz - k0;
+    auto V = [&](int i, int j, int k) {
+        return __ldg(A.values + ((int64_t)i * A.d1 + j) * A.d2 + k);
+    };
+    const double c00 = V(i0, j0, k0) * (1 - tx) + V(i0 + 1, j0, k0) * tx;
+    const double c10 = V(i0, j0 + 1, k0) * (1 - tx) + V(i0 + 1, j0 + 1, k0) * tx;
+    const double c01 = V(i0, j0, k0 + 1) * (1 - tx) + V(i0 + 1, j0, k0 + 1) * tx;
+    const double c11 = V(i0, j0 + 1, k0 + 1) * (1 - tx) + V(i0 + 1, j0 + 1, k0 + 1) * tx;
+    const double c0 = c00 * (1 - ty) + c10 * ty;
+    const double c1 = c01 * (1 - ty) + c11 * ty;
+    return c0 * (1 - tz) + c1 * tz;
+}
+
+__device__ __forceinline__ double tf_lookup(const Args &A, double v, double rgb[3]) {
+    const int n = A.ntf;
+    if (v <= A.tf_v[0]) {
+        for (int c = 0; c < 3; ++c) rgb[c] = A.tf_rgb[c];
+        return A.tf_o[0];
+    }
+    if (v >= A.tf_v[n - 1]) {
+        for (int c = 0; c < 3; ++c) rgb[c] = A.tf_rgb[3 * (n - 1) + c];
+        return A.tf_o[n - 1];
+    }
+    for (int i = 1; i < n; ++i) {
+        if (v <= A.tf_v[i]) {
+            const double span = A.tf_v[i] - A.tf_v[i - 1];
+            const double t = span <= 0.0 ? 0.0 : (v - A.tf_v[i - 1]) / span;
+            for (int c = 0; c < 3; ++c)
+                rgb[c] = A.tf_rgb[3 * (i - 1) + c] * (1 - t) + A.tf_rgb[3 * i + c] * t;
+            return A.tf_o[i - 1] * (1 - t) + A.tf_o[i] * t;
+        }
+    }
+    return 0.0;
+}
+
+__global__ void __launch_bounds__(128) raymarch_kernel(Args A) {
+    const int64_t pid = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (pid >= (int64_t)A.W * A.H) return;
+    const int py = (int)(pid / A.W), px = (int)(pid % A.W);
+    // ray direction (dvr.py:404-407)
+    const double dx = (px - A.cx) / A.focal, dy = (py - A.cy) / A.focal;
+    const double norm = sqrt(dx * dx + dy * dy + 1.0);
+    double rd[3];
+    for (int a = 0; a < 3; ++a)
+        rd[a] = (A.rot_t[3 * a] * dx + A.rot_t[3 * a + 1] * dy + A.rot_t[3 * a + 2]) / norm;
+    double rgba[4] = {0.0, 0.0, 0.0, 0.0};
+    double *o = A.out + 4 * pid;
+    const double *ro = A.cam_pos;
+    // slab intersection (dvr.py:285-302)
+    double tmin = 0.0, tmax = 1e30;
+    for (int a = 0; a < 3; ++a) {
+        if (fabs(rd[a]) < 1e-12) {
+            if (ro[a] < A.lo[a] || ro[a] > A.hi[a]) {
+                for (int c = 0; c < 4; ++c) o[c] = 0.0;
+                return;
+            }
+        } else {
+            double t0 = (A.lo[a] - ro[a]) / rd[a], t1 = (A.hi[a] - ro[a]) / rd[a];
+            if (t0 > t1) {
+                const double s = t0;
+                t0 = t1;
+                t1 = s;
+            }
+            if (t0 > tmin) tmin = t0;
+            if (t1 < tmax) tmax = t1;
+        }
+    }
+    if (tmax <= tmin) {
+        for (int c = 0; c < 4; ++c) o[c] = 0.0;
+        return;
+    }
+    double transmittance = 1.0;
+    double t = tmin + 0.5 * A.dt;
+    while (t < tmax) {
+        double p[3], cv[3];
+        for (int a = 0; a < 3; ++a) p[a] = ro[a] + t * rd[a];
+        const double value = trilinear(A, p);
+        const double alpha_ref = tf_lookup(A, value, cv);
+        if (alpha_ref > 0.0) {
+            const double alpha = 1.0 - pow(1.0 - alpha_ref, A.dt / A.step_ref);
+            double n[3], pg[3];
+            double gn = 0.0;
+            for (int a = 0; a < 3; ++a) {
+                const double h = A.spacing[a];
+                for (int b = 0; b < 3; ++b) pg[b] = p[b];
+                pg[a] = p[a] + h;
+                const double vp = trilinear(A, pg);
+                pg[a] = p[a] - h;
+                const double vm = trilinear(A, pg);
+                n[a] = (vp - vm) / (2.0 * h);
+                gn += n[a] * n[a];
+            }
+            gn = sqrt(gn);
+            double v_dir[3], l[3];
+            for (int a = 0; a < 3; ++a) v_dir[a] = -rd[a];
+            if (gn < kFlatGradient) {
+                for (int a = 0; a < 3; ++a) n[a] = v_dir[a];
+            } else {
+                for (int a = 0; a < 3; ++a) n[a] = -n[a] / gn;
+            }
+            for (int a = 0; a < 3; ++a) l[a] = A.headlight ? v_dir[a] : A.light_dir[a];
+            // shade_sample (dvr.py:176-194)
+            const double ndl = fabs(n[0] * l[0] + n[1] * l[1] + n[2] * l[2]);
+            double hx = v_dir[0] + l[0], hy = v_dir[1] + l[1], hz = v_dir[2] + l[2];
+            const double hn = sqrt(hx * hx + hy * hy + hz * hz);
+            if (hn > 1e-12) {
+                hx = hx / hn;
+                hy = hy / hn;
+                hz = hz / hn;
+            }
+            const double ndh = fabs(n[0] * hx + n[1] * hy + n[2] * hz);
+            double spec = 0.0;
+            if (ndl > 0.0 && ndh > 0.0) spec = A.k_s * pow(ndh, A.beta);
+            const double w = transmittance * alpha;
+            for (int c = 0; c < 3; ++c) {
+                const double shaded = A.k_a * cv[c] + A.k_d * cv[c] * ndl + spec;
+                rgba[c] += w * shaded;
+            }
+            rgba[3] += w;
+            transmittance *= 1.0 - alpha;
+            if (transmittance < kTStopDvr) break;
+        }
+        t += A.dt;
+    }
+    for (int c = 0; c < 4; ++c) o[c] = rgba[c];
+}
+
+}  // namespace dvrk
+}  // namespace ivr
+
+extern "C" int ivr_dvr_render(const double *values, int32_t d0, int32_t d1, int32_t d2,
+                              const double spacing[3], const double *tf_values,
+                              const double *tf_colors, const double *tf_opacities,
+                              int32_t n_tf, const ivr_camera *cam, int32_t headlight,
+                              const double light_dir[3], const double material[4],
+                              double step_scale, double *out, ivr_stream_t stream) {
+    using namespace ivr;
+    using namespace ivr::dvrk;
+    if (!values || d0 < 2 || d1 < 2 || d2 < 2 || !spacing || !tf_values || !tf_colors ||
+        !tf_opacities || n_tf < 2 || !cam || !material || !out || !(step_scale > 0.0) ||
+        (!headlight && !light_dir)) {
+        set_error("ivr_dvr_render: bad argument");
+        return IVR_ERR_ARG;
+    }
+    Args A{};
+    A.values = values;
+    A.d0 = d0;
+    A.d1 = d1;
+    A.d2 = d2;
+    const int dims[3] = {d0, d1, d2};
+    double smin = spacing[0];
+    for (int a = 0; a < 3; ++a) {
+        if (!(spacing[a] > 0.0)) {
+            set_error("ivr_dvr_render: spacing must be positive");
+            return IVR_ERR_ARG;
+        }
+        A.spacing[a] = spacing[a];
+        // VolumeGrid.origin / bbox (dvr.py:48-60)
+        A.origin[a] = -((double)(dims[a] - 1)) * spacing[a] / 2.0;
+        A.lo[a] = A.origin[a];
+        A.hi[a] = A.origin[a] + (double)(dims[a] - 1) * spacing[a];
+        smin = spacing[a] < smin ? spacing[a] : smin;
+    }
+    A.tf_v = tf_values;
+    A.tf_rgb = tf_colors;
+    A.tf_o = tf_opacities;
+    A.ntf = n_tf;
+    for (int a = 0; a < 3; ++a) A.cam_pos[a] = cam->position[a];
+    for (int r = 0; r < 3; ++r)
+        for (int c = 0; c < 3; ++c) A.rot_t[3 * r + c] = cam->rotation[3 * c + r];
+    A.focal = cam->focal;
+    A.cx = cam->cx;
+    A.cy = cam->cy;
+    A.W = cam->width;
+    A.H = cam->height;
+    A.dt = step_scale * smin;  // _march_args (dvr.py:411-420)
+    A.step_ref = smin;
+    A.headlight = headlight ? 1 : 0;
+    for (int a = 0; a < 3; ++a) A.light_dir[a] = headlight ? 0.0 : light_dir[a];
+    A.k_a = material[0];
+    A.k_d = material[1];
+    A.k_s = material[2];
+    A.beta = material[3];
+    A.out = out;
+    const int64_t npx = (int64_t)A.W * A.H;
+    if (npx == 0) return IVR_OK;
+    raymarch_kernel<<<(unsigned)((npx + 127) / 128), 128, 0, (cudaStream_t)stream>>>(A);
+    return check_launch("raymarch_kernel");
+}

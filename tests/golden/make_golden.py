@@ -347,6 +347,24 @@ def display_case():
     print("display")
 
 
+def dvr_case():
+    """dvr.render_view (dvr.py:424-452) for the three synthetic volumes,
+    headlight and orbital light, a union of two transfer-function bumps."""
+    from voxsplat.dvr import Material, TransferFunction1D, make_volume, render_view, union_transfer_functions
+    tf = union_transfer_functions([TransferFunction1D.basic_bump(0.2, 0.45, (0.9, 0.3, 0.2), 0.8),
+                                   TransferFunction1D.basic_bump(0.55, 0.8, (0.2, 0.5, 0.9), 0.6)])
+    d = {}
+    cam = orbit_camera(np.zeros(3), 3.0 * 16.0, 0.4, 0.7, 0.8, 24, 20)
+    for kind in ("shells", "lobes", "swirl"):
+        vol = make_volume(kind, (24, 20, 28))
+        d[kind + "_head"] = render_view(vol, tf, cam, LightConfig())
+        d[kind + "_orb"] = render_view(vol, tf, cam, LightConfig("orbital", 0.3, -0.8),
+                                       Material(0.3, 0.5, 0.4, 8.0), step_scale=0.35)
+    d.update(cam_dict(cam))
+    np.savez_compressed(os.path.join(HERE, "dvr.npz"), **d)
+    print("dvr")
+
+
 if __name__ == "__main__":
     import sys as _sys
     if len(_sys.argv) > 1:  # regenerate selected cases only
@@ -372,3 +390,4 @@ if __name__ == "__main__":
     stage1_case()
     ivrg_case()
     display_case()
+    dvr_case()
