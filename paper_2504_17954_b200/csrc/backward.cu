@@ -135,12 +135,32 @@ blend_bwd_kernel(BwdArgs A) {
     const int last = inside ? A.last_pos[pix] : s0;
     const int stop = __reduce_max_sync(0xffffffffu, last);  // no pixel of the warp contributes past here
 
-    float C[KMAX], acc[KMAX], dout[KMAX];
+    // d alpha_i = sum_k dout_k (T_i v_ik - (C_k - A_ik) / (1 - alpha_i)) only
+    // needs the dot products D_i = dout . v_i and S = dout . (C - A): with
+    // S_C = dout . C per pixel and a running S_A = dout . A, no per-channel
+    // accumulator is carried
+    float dout[KMAX];
+    float S_C = 0.0f, S_A = 0.0f;
 #pragma unroll
     for (int c = 0; c < KMAX; ++c) {
-        C[c] = (inside && c < K) ? A.out[pix * K + c] : 0.0f;
+        const float Cc = (inside && c < K) ? A.out[pix * K + c] : 0.0f;
         dout[c] = (inside && c < K) ? A.d_out[pix * K + c] : 0.0f;
-        acc[c] = 0.0f;
+        S_C = fmaf(dout[c], Cc, S_C);
+    }
+    // per-lane atomic target for the transposed totals: lane l owns value
+    // slot l (< K) and geometry slot l (< 6: mean2d x, y, conic a, b, c, opacity)
+    float *vbase = lane < K ? A.g_values + lane : nullptr;
+    float *gbase = nullptr;
+    int gstride = 0;
+    if (lane < 2) {
+        gbase = A.g_mean + lane;
+        gstride = 2;
+    } else if (lane < 5) {
+        gbase = A.g_conic + (lane - 2);
+        gstride = 3;
+    } else if (lane == 5) {
+        gbase = A.g_opac;
+        gstride = 1;
     }
     float T = 1.0f;
     const float fpx = (float)px, fpy = (float)py;
@@ -230,55 +250,56 @@ blend_bwd_kernel(BwdArgs A) {
                     dy = cdy;
                 }
             }
-            // per-pixel contributions in fixed slots: [0,K) d_values, KMAX/KMAX+1
-            // d_mean2d, KMAX+2..KMAX+4 d_conic, KMAX+5 d_opacity (zero when not
-            // contributing); reduced in chunks of CH lanes
-            constexpr int CH = KMAX + 6 <= 16 ? 16 : 32;
-            constexpr int NX = (KMAX + 6 + CH - 1) / CH * CH;
-            float x[NX];
+            // per-pixel contributions: xv[c] = d value_c, xg = d mean2d (2),
+            // d conic (3), d opacity (zero when not contributing)
+            float xv[KMAX], xg[8];
 #pragma unroll
-            for (int c = 0; c < NX; ++c) x[c] = 0.f;
+            for (int c = 0; c < KMAX; ++c) xv[c] = 0.f;
+#pragma unroll
+            for (int c = 0; c < 8; ++c) xg[c] = 0.f;
             if (contrib) {
                 const float w = T * al;
                 const float inv = rcp_approx_b(1.0f - al);
-                float d_alpha = 0.f;
+                float Dv = 0.f;  // dout . v
+                if (KMAX % 4 == 0) {
+                    const float4 *vv = reinterpret_cast<const float4 *>(W.v + q * KMAX);
 #pragma unroll
-                for (int c = 0; c < KMAX; ++c) {  // value slots are zero-padded past K
-                    const float vk = W.v[q * KMAX + c];
-                    acc[c] = fmaf(w, vk, acc[c]);
-                    const float after = C[c] - acc[c];
-                    d_alpha = fmaf(dout[c], T * vk - after * inv, d_alpha);
-                    x[c] = dout[c] * w;
+                    for (int c4 = 0; c4 < KMAX / 4; ++c4) {
+                        const float4 v = vv[c4];
+                        Dv = fmaf(dout[4 * c4], v.x, Dv);
+                        Dv = fmaf(dout[4 * c4 + 1], v.y, Dv);
+                        Dv = fmaf(dout[4 * c4 + 2], v.z, Dv);
+                        Dv = fmaf(dout[4 * c4 + 3], v.w, Dv);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < KMAX; ++c) Dv = fmaf(dout[c], W.v[q * KMAX + c], Dv);
                 }
+#pragma unroll
+                for (int c = 0; c < KMAX; ++c) xv[c] = dout[c] * w;
+                S_A = fmaf(w, Dv, S_A);  // dout . A after this contributor
+                const float d_alpha = T * Dv - (S_C - S_A) * inv;
                 if (alu < 0.99f) {
                     const float d_sigma = -alu * d_alpha;
                     const float ca = 2.0f * a1.x, cb = a1.y, cc = 2.0f * a1.z;
-                    x[KMAX] = -d_sigma * (ca * dx + cb * dy);
-                    x[KMAX + 1] = -d_sigma * (cb * dx + cc * dy);
-                    x[KMAX + 2] = 0.5f * dx * dx * d_sigma;
-                    x[KMAX + 3] = dx * dy * d_sigma;
-                    x[KMAX + 4] = 0.5f * dy * dy * d_sigma;
-                    x[KMAX + 5] = g * d_alpha;
+                    xg[0] = -d_sigma * (ca * dx + cb * dy);
+                    xg[1] = -d_sigma * (cb * dx + cc * dy);
+                    xg[2] = 0.5f * dx * dx * d_sigma;
+                    xg[3] = dx * dy * d_sigma;
+                    xg[4] = 0.5f * dy * dy * d_sigma;
+                    xg[5] = g * d_alpha;
                 }
                 T = T * (1.0f - al);
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                // transpose reduction: lane i ends with the warp total of slot i
-                // (CH-1 shuffles per chunk instead of 5 per slot), then parallel atomics
+                // transpose reductions (KMAX-1 and 7 shuffles + the remaining lane
+                // bits): lane l ends with value slot l % KMAX and geometry slot
+                // l % 8; parallel atomics
                 const int s = W.sp[q];
-#pragma unroll
-                for (int ch = 0; ch < NX / CH; ++ch) {
-                    const float tot = warp_transpose_sum<CH>(x + ch * CH, lane);
-                    const int slot = ch * CH + (lane & (CH - 1));
-                    if (lane < CH && tot != 0.f) {
-                        float *dst = nullptr;
-                        if (slot < K) dst = A.g_values + (int64_t)K * s + slot;
-                        else if (slot >= KMAX && slot < KMAX + 2) dst = A.g_mean + 2 * (int64_t)s + (slot - KMAX);
-                        else if (slot >= KMAX + 2 && slot < KMAX + 5) dst = A.g_conic + 3 * (int64_t)s + (slot - KMAX - 2);
-                        else if (slot == KMAX + 5) dst = A.g_opac + s;
-                        if (dst) atomicAdd(dst, tot);
-                    }
-                }
+                const float tv = warp_transpose_sum<KMAX>(xv, lane);
+                const float tg = warp_transpose_sum<8>(xg, lane);
+                if (vbase && tv != 0.f) atomicAdd(vbase + (int64_t)K * s, tv);
+                if (gbase && tg != 0.f) atomicAdd(gbase + (int64_t)gstride * s, tg);
             }
         }
         __syncwarp();  // slots are rewritten by the next chunk
