@@ -114,7 +114,7 @@ constexpr int kBwdWarpW = 8;  // warp footprint 8x4 pixels (as K3)
 // the tile list in 32-pair chunks up to the largest last_pos of its pixels
 // (same strip cull and prefetch as K3; no CTA barrier).
 template <int KMAX, bool F64>
-__global__ void __launch_bounds__(kBwdThreads)
+__global__ void __launch_bounds__(kBwdThreads, KMAX <= 16 ? 3 : 1)
 blend_bwd_kernel(BwdArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     BwdSlots<KMAX, F64> &W = reinterpret_cast<BwdSlots<KMAX, F64> *>(smem)[threadIdx.x >> 5];
