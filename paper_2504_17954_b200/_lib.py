@@ -13,7 +13,7 @@ import os
 from .errors import CorruptIndex, NonFiniteGradient, ShapeMismatch, VoxSplatError
 
 PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(PKG, "libivrgs.so")
+LIB_PATH = os.environ.get("IVR_LIB_PATH") or os.path.join(PKG, "libivrgs.so")  # override: A/B runs
 
 c_double_p = ctypes.POINTER(ctypes.c_double)
 P = ctypes.c_void_p
