@@ -65,9 +65,16 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
     double nrm[3];
     unit_normal(G, i, nrm);
     ShadeState sh;
+    float rgb32[3] = {0.0f, 0.0f, 0.0f};
+    // FAST mode with a shading cache and no float64 colour output: float32 colour
+    const bool fast_rgb = has_shading && !f64_mode && !O.rgb && G.cache &&
+                          G.cache[kCacheStride * i + 14] != 0.0;
     if (has_shading) {
         const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
-        shade_state(S, P, i, sid, mu, nrm, sh, G.cache);
+        if (fast_rgb)
+            shade_rgb_f32(S, P, i, sid, mu, nrm, G.cache + kCacheStride * i, rgb32);
+        else
+            shade_state(S, P, i, sid, mu, nrm, sh, G.cache);
     }
 
     // ---- float32 blend record (rasterizer.py:151-153 casts) + skip bounds
@@ -113,7 +120,8 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
     };
     if (L.col_color >= 0) {
         for (int k = 0; k < 3; ++k)
-            put(L.col_color + k, has_shading ? sh.rgb[k] : (L.colors ? L.colors[3 * i + k] : 0.0));
+            put(L.col_color + k, fast_rgb ? (double)rgb32[k]
+                                 : has_shading ? sh.rgb[k] : (L.colors ? L.colors[3 * i + k] : 0.0));
     }
     if (L.col_alpha >= 0) put(L.col_alpha, 1.0);
     if (L.col_depth >= 0) put(L.col_depth, tz);

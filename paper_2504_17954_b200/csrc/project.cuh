@@ -219,4 +219,45 @@ __device__ __forceinline__ void shade_state(const ivr_shading &S, const ivr_fram
     }
 }
 
+// FAST-mode colour (K1 packs colours as float32 and the image contract is
+// 1e-4): the same Blinn-Phong as shade_state in float32 arithmetic, from the
+// static cache's sigmoids.  Keys, rects and the blend record stay float64.
+__device__ __forceinline__ void shade_rgb_f32(const ivr_shading &S, const ivr_frame_params &P,
+                                              int64_t i, int32_t sid, const double mu[3],
+                                              const double nrm[3], const double *c, float rgb[3]) {
+    const ivr_camera &cam = P.cam;
+    float v[3], l[3], h[3], n[3];
+    for (int k = 0; k < 3; ++k) {
+        v[k] = (float)(cam.position[k] - mu[k]);
+        n[k] = (float)nrm[k];
+    }
+    const float vn = rsqrtf(fmaxf(v[0] * v[0] + v[1] * v[1] + v[2] * v[2], 1e-24f));
+    for (int k = 0; k < 3; ++k) v[k] *= vn;
+    if (!P.orbital) {
+        for (int k = 0; k < 3; ++k) l[k] = h[k] = v[k];
+    } else {
+        for (int k = 0; k < 3; ++k) {
+            l[k] = (float)P.light_dir[k];
+            h[k] = v[k] + l[k];
+        }
+        const float hn = rsqrtf(fmaxf(h[0] * h[0] + h[1] * h[1] + h[2] * h[2], 1e-24f));
+        for (int k = 0; k < 3; ++k) h[k] *= hn;
+    }
+    float kk[4];
+    for (int k = 0; k < 3; ++k) {
+        const float t = (float)P.lam[k] * (float)c[10 + k] + (float)P.b[k];
+        kk[k] = (float)P.term_scales[k] * fminf(fmaxf(t, 0.0f), 1.0f);
+    }
+    kk[3] = (float)P.term_scales[3] * fmaxf((float)P.lam[3] * (float)c[13] + (float)P.b[3], 1.0f);
+    const float a_ndl = fabsf(n[0] * l[0] + n[1] * l[1] + n[2] * l[2]);
+    const float a_ndh = fabsf(n[0] * h[0] + n[1] * h[1] + n[2] * h[2]);
+    const float spow = (a_ndl > 0.0f && a_ndh > 0.0f) ? powf(a_ndh, kk[3]) : 0.0f;
+    const float spec = kk[2] * spow, kdl = kk[1] * a_ndl;
+    const double *cp = S.per_splat_palette ? S.palette + 3 * i : S.palette + 3 * (int64_t)sid;
+    for (int k = 0; k < 3; ++k) {
+        const float cv = fminf(fmaxf((float)(cp[k] + S.delta_c[3 * i + k]), 0.0f), 1.0f);
+        rgb[k] = kk[0] * cv + kdl * cv + spec;
+    }
+}
+
 }  // namespace ivr

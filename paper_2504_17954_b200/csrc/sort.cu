@@ -183,6 +183,35 @@ rowscan_kernel(uint32_t *rows, int ncols, uint32_t *rowtotal, const int32_t *gat
     if (threadIdx.x == 0) rowtotal[blockIdx.x] = carry;
 }
 
+// One warp per row: the same exclusive row scan for short rows (the radix
+// block histograms and the per-tile block counts: a few hundred columns),
+// 32 coalesced columns per step, no CTA barriers.
+constexpr int kRowsPerBlock = 8;
+__global__ void __launch_bounds__(32 * kRowsPerBlock)
+rowscan_warp_kernel(uint32_t *rows, int nrows, int ncols, uint32_t *rowtotal,
+                    const int32_t *gate) {
+    if (gate && *gate == 0) return;
+    const int lane = threadIdx.x & 31;
+    const int r = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
+    if (r >= nrows) return;
+    uint32_t *row = rows + (int64_t)r * ncols;
+    uint32_t carry = 0;
+#pragma unroll 4
+    for (int base = 0; base < ncols; base += 32) {
+        const int i = base + lane;
+        const uint32_t v = i < ncols ? row[i] : 0;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (i < ncols) row[i] = carry + x - v;
+        carry += __shfl_sync(0xffffffffu, x, 31);
+    }
+    if (lane == 0) rowtotal[r] = carry;
+}
+
 template <typename KeyT>
 __global__ void __launch_bounds__(kThreads)
 downsweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
@@ -705,7 +734,10 @@ void radix_pass(cudaStream_t st, const KeyT *k_in, const uint32_t *v_in, KeyT *k
                 uint32_t *v_out, int64_t n, int shift, int nbk, uint32_t *bh, uint32_t *rt,
                 const int32_t *gate) {
     upsweep_kernel<KeyT><<<nbk, kThreads, 0, st>>>(k_in, n, shift, bh, nbk, gate);
-    rowscan_kernel<<<256, 1024, 0, st>>>(bh, nbk, rt, gate);
+    if (nbk <= 2048)
+        rowscan_warp_kernel<<<256 / kRowsPerBlock, 32 * kRowsPerBlock, 0, st>>>(bh, 256, nbk, rt, gate);
+    else
+        rowscan_kernel<<<256, 1024, 0, st>>>(bh, nbk, rt, gate);
     downsweep_kernel<KeyT><<<nbk, kThreads, 0, st>>>(k_in, v_in, n, shift, bh, rt, nbk, k_out, v_out,
                                                      gate);
 }
@@ -814,7 +846,11 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     if (sm_place > 48 * 1024)
         cudaFuncSetAttribute(pair_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_place);
     pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
-    rowscan_kernel<<<ntiles, 1024, 0, st>>>(phist, nbp, ttot, nullptr);
+    if (nbp <= 2048)
+        rowscan_warp_kernel<<<(ntiles + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kRowsPerBlock, 0, st>>>(
+            phist, ntiles, nbp, ttot, nullptr);
+    else
+        rowscan_kernel<<<ntiles, 1024, 0, st>>>(phist, nbp, ttot, nullptr);
     tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges);
     pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, nbp, tile_ranges, pair_splat,
                                                        width, height);
