@@ -395,6 +395,55 @@ typedef struct ivr_adam_group {
 int ivr_adam_step(const ivr_adam_group *groups, int32_t n_groups, double beta1, double beta2,
                   double eps, ivr_stream_t stream);
 
+/* ---- training-step plumbing (csrc/trainstep.cu) ---- */
+
+/* Stage-2 attribute channels (trainer.py:379-404): k_x = sigmoid(k_x_raw)
+ * (_mathutil.py:6-13), beta = exp(log_beta) + 1 (shading.py:132-134). */
+int ivr_stage2_attrs(int64_t n, const double *k_a_raw, const double *k_d_raw,
+                     const double *k_s_raw, const double *log_beta, double *k_a, double *k_d,
+                     double *k_s, double *beta, ivr_stream_t stream);
+
+/* Per-Gaussian tail of _stage1_step / _stage2_step (trainer.py:386-394,
+ * 410-444).  In place on K4b's outputs: d_delta_c += d_values[:, delta_c],
+ * d_k_x_raw += d_values[:, k_x] k_x (1 - k_x), d_log_beta += d_values[:, beta]
+ * (beta - 1), d_o_logit += w o (1 - o) / n (losses.py:263-268); stat =
+ * |d_mean2d| + |d_n_raw| (trainer.py:443); o_partial[b] = per-block sums of
+ * o = sigmoid(o_logit) for the opacity-L1 value (ivr_step_partials(n)
+ * blocks).  Any output may be NULL; a column < 0 skips that chain. */
+typedef struct ivr_step_grads {
+    int64_t n;
+    int32_t k;
+    const double *d_values; /* (n,k) float64 from ivr_preprocess_bwd */
+    int32_t col_delta_c, col_k_a, col_k_d, col_k_s, col_beta;
+    const double *o_logit, *k_a_raw, *k_d_raw, *k_s_raw, *log_beta;
+    double *d_o_logit, *d_delta_c, *d_k_a_raw, *d_k_d_raw, *d_k_s_raw, *d_log_beta;
+    const double *d_mean2d, *d_n_raw;
+    double *stat;
+    double w_opacity_l1;
+    double *o_partial;
+} ivr_step_grads;
+int32_t ivr_step_partials(int64_t n);
+int ivr_step_assemble(const ivr_step_grads *a, ivr_stream_t stream);
+
+/* The step's scalar loss on the device: l1_weight * sums[1] / numel +
+ * ssim_weight * (1 - sums[0] / windows) (photometric, losses.py:118-138)
+ * + w_normal terms[0] + w_offset terms[1] + w_bil terms[2] (ivr_regularize)
+ * + w_opacity_l1 * sum(o_partial) / n.  state (nullable, int64[2] device):
+ * step counter and the first step whose photometric loss was non-finite
+ * (-1 = none; *last_bad = that loss), the reference's DivergedLoss check
+ * (trainer.py:345-348) without a host synchronisation. */
+typedef struct ivr_loss_terms {
+    const double *photo_sums; /* [sum SSIM, sum |x - y|] from ivr_photometric_loss */
+    double l1_weight, ssim_weight, numel, windows;
+    const double *terms;      /* [normal, offset, bilateral] or NULL */
+    double w_normal, w_offset, w_bil;
+    const double *o_partial;
+    int32_t n_partial;
+    double w_opacity_l1, n;
+} ivr_loss_terms;
+int ivr_loss_finalize(const ivr_loss_terms *t, double *loss, int64_t *state, double *last_bad,
+                      ivr_stream_t stream);
+
 #ifdef __cplusplus
 }
 #endif

@@ -86,6 +86,26 @@ class Grads_t(ctypes.Structure):
                 ("dl_da", ctypes.c_double * 3), ("bad", P)]
 
 
+class StepGrads_t(ctypes.Structure):
+    _fields_ = [("n", ctypes.c_int64), ("k", ctypes.c_int32), ("d_values", P),
+                ("col_delta_c", ctypes.c_int32), ("col_k_a", ctypes.c_int32),
+                ("col_k_d", ctypes.c_int32), ("col_k_s", ctypes.c_int32),
+                ("col_beta", ctypes.c_int32), ("o_logit", P), ("k_a_raw", P), ("k_d_raw", P),
+                ("k_s_raw", P), ("log_beta", P), ("d_o_logit", P), ("d_delta_c", P),
+                ("d_k_a_raw", P), ("d_k_d_raw", P), ("d_k_s_raw", P), ("d_log_beta", P),
+                ("d_mean2d", P), ("d_n_raw", P), ("stat", P), ("w_opacity_l1", ctypes.c_double),
+                ("o_partial", P)]
+
+
+class LossTerms_t(ctypes.Structure):
+    _fields_ = [("photo_sums", P), ("l1_weight", ctypes.c_double),
+                ("ssim_weight", ctypes.c_double), ("numel", ctypes.c_double),
+                ("windows", ctypes.c_double), ("terms", P), ("w_normal", ctypes.c_double),
+                ("w_offset", ctypes.c_double), ("w_bil", ctypes.c_double), ("o_partial", P),
+                ("n_partial", ctypes.c_int32), ("w_opacity_l1", ctypes.c_double),
+                ("n", ctypes.c_double)]
+
+
 BAD_IDS = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_k_a_raw",
            "d_k_d_raw", "d_k_s_raw", "d_log_beta", "d_delta_c")
 
@@ -150,6 +170,10 @@ _SIGS = {
                        ctypes.c_int),
     "ivr_adam_step": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
                        ctypes.c_double, ctypes.c_double, P], ctypes.c_int),
+    "ivr_stage2_attrs": ([ctypes.c_int64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
+    "ivr_step_partials": ([ctypes.c_int64], ctypes.c_int32),
+    "ivr_step_assemble": ([ctypes.POINTER(StepGrads_t), P], ctypes.c_int),
+    "ivr_loss_finalize": ([ctypes.POINTER(LossTerms_t), P, P, P, P], ctypes.c_int),
     "ivr_regularize_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),
     "ivr_regularize": ([P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                         ctypes.POINTER(ctypes.c_int32), ctypes.POINTER(ctypes.c_int32),

@@ -313,10 +313,9 @@ def blend_backward(F: Frame, d_out, stream=None):
     d_out (H,W,K float32 device tensor)."""
     n, K = F.n, F.K
     dev = F.depth_key.device
-    g = {"values": torch.zeros(n * K, dtype=torch.float32, device=dev),
-         "mean2d": torch.zeros(2 * n, dtype=torch.float32, device=dev),
-         "conic": torch.zeros(3 * n, dtype=torch.float32, device=dev),
-         "opacity": torch.zeros(n, dtype=torch.float32, device=dev)}
+    arena = torch.zeros(n * (K + 6), dtype=torch.float32, device=dev)  # one memset
+    g = {"values": arena[:n * K], "mean2d": arena[n * K:n * (K + 2)],
+         "conic": arena[n * (K + 2):n * (K + 5)], "opacity": arena[n * (K + 5):]}
     out = F.out if not F.f64 else F.out64.float()
     d_out = d_out.to(torch.float32).contiguous()
     cam = F.cam
@@ -349,23 +348,22 @@ def preprocess_backward(dg: DeviceGaussians, cam, K, cols, g=None, shading=None,
         R.g_conic, R.g_opacity = g["conic"].data_ptr(), g["opacity"].data_ptr()
     if d_rgb is not None:
         R.d_rgb_extra = d_rgb.data_ptr()
-    for name in want:
-        if name in GRAD_SHAPES:
-            out[name] = torch.zeros(n * GRAD_SHAPES[name], dtype=torch.float64, device=dev)
-            setattr(R, name, out[name].data_ptr())
+    # every output is a slice of one zeroed float64 arena (one memset)
+    sizes = [(name, n * GRAD_SHAPES[name]) for name in want if name in GRAD_SHAPES]
     if "d_values" in want:
-        out["d_values"] = torch.zeros(n * K, dtype=torch.float64, device=dev)
-        R.d_values = out["d_values"].data_ptr()
+        sizes.append(("d_values", n * K))
     if "d_c_p" in want:
-        out["d_c_p"] = torch.zeros((n if per_splat_c_p else max(per_scene, 1)) * 3,
-                                   dtype=torch.float64, device=dev)
-        R.d_c_p = out["d_c_p"].data_ptr()
+        sizes.append(("d_c_p", (n if per_splat_c_p else max(per_scene, 1)) * 3))
     if "d_scale" in want:
-        out["d_scale"] = torch.zeros(max(per_scene, 1), dtype=torch.float64, device=dev)
-        R.d_scale = out["d_scale"].data_ptr()
+        sizes.append(("d_scale", max(per_scene, 1)))
     if shading is not None:
-        out["d_globals"] = torch.zeros(10, dtype=torch.float64, device=dev)
-        R.d_globals = out["d_globals"].data_ptr()
+        sizes.append(("d_globals", 10))
+    arena = torch.zeros(sum(sz for _, sz in sizes), dtype=torch.float64, device=dev)
+    o = 0
+    for name, sz in sizes:
+        out[name] = arena[o:o + sz]
+        setattr(R, name, out[name].data_ptr())
+        o += sz
     R.per_scene = 0 if per_splat_c_p else int(per_scene)
     if light is not None and light.mode == "orbital":
         p, a = light.polar, light.azimuth

@@ -22,6 +22,7 @@ communication.
 
 from __future__ import annotations
 
+import ctypes
 import json
 import math
 from dataclasses import dataclass, field
@@ -31,9 +32,9 @@ import torch
 
 from . import _lib as L
 from . import device as D
-from .errors import DatasetEmpty, DivergedLoss, OutOfRange
+from .errors import DatasetEmpty, DivergedLoss, OutOfRange, ShapeMismatch
 from .gaussians import GaussianGeometry, ShColor
-from .losses import LossWeights, photometric_loss_t, regularize_t
+from .losses import SSIM_RADIUS, LossWeights, _photometric_dev, regularize_t
 from .rasterizer import _channel_layout, _cols
 from .scene import STAGE_BASE, STAGE_EDITABLE, BasicSceneModel, DeviceScene
 from .shading import LightConfig, Palette, ShadingAttributes
@@ -244,17 +245,24 @@ class _StageTrainer:
 
     def _map_terms(self, F, cam, gt, weights, offset=False, bilateral=False):
         """Photometric L1+SSIM (K7) and the map regularizers (fused kernel):
-        returns (loss tensor, d_out float32 (H,W,K), column map).  No host
-        synchronisation: a non-finite loss is recorded on the device
-        (``check_finite``)."""
+        returns (loss terms for ivr_loss_finalize, tensors they point to,
+        d_out float32 (H,W,K), column map).  No host synchronisation."""
         c = {name: c for name, c, w in _cols_named(self.layout)}
         idx = getattr(self, "_rgba_idx", None)
         if idx is None:
             idx = self._rgba_idx = torch.tensor([c["color"], c["color"] + 1, c["color"] + 2,
                                                  c["alpha"]], device=self.dev)
         rgba = F.out.index_select(2, idx).double()
-        loss, d_rgba = photometric_loss_t(rgba, gt, weights)
-        self._note_finite(loss)
+        if rgba.shape != gt.shape:
+            raise ShapeMismatch(f"prediction {tuple(rgba.shape)} vs ground truth {tuple(gt.shape)}")
+        h, w, nc = rgba.shape
+        win = 2 * SSIM_RADIUS + 1
+        with_ssim = weights.ssim_weight > 0.0
+        if with_ssim and (h < win or w < win):
+            raise ShapeMismatch(f"image {h}x{w} smaller than the {win}x{win} ssim window")
+        numel = rgba.numel()
+        sums, d_rgba = _photometric_dev(rgba, gt.to(torch.float64), weights.l1_weight / numel,
+                                        -weights.ssim_weight, with_ssim)
         wn = weights.normal_consistency
         wo = weights.offset_sparsity if offset else 0.0
         wb = weights.bilateral_smoothness if bilateral else 0.0
@@ -264,31 +272,64 @@ class _StageTrainer:
         terms, d_out = regularize_t(F.out, cols, gt=gt, d_rgba=d_rgba,
                                     cam_params=self._cam_params(cam) if wn > 0.0 else None,
                                     w_normal=wn, w_offset=wo, w_bil=wb, bil_cols=bil)
-        if wn > 0.0:
-            loss = loss + wn * terms[0]
-        if wo > 0.0:
-            loss = loss + wo * terms[1]
-        if wb > 0.0:
-            loss = loss + wb * terms[2]
-        return loss, d_out, c
+        lt = L.LossTerms_t()
+        lt.photo_sums = sums.data_ptr()
+        lt.l1_weight, lt.ssim_weight = weights.l1_weight, weights.ssim_weight
+        lt.numel = float(numel)
+        lt.windows = float((h - win + 1) * (w - win + 1) * nc)
+        lt.terms = terms.data_ptr()
+        lt.w_normal, lt.w_offset, lt.w_bil = wn, wo, wb
+        return lt, (sums, terms), d_out, c
 
-    def _note_finite(self, loss):
-        """Device-side DivergedLoss bookkeeping: the first step whose
-        photometric loss was non-finite (the reference checks it in the step,
-        trainer.py:345-348)."""
+    def _assemble(self, gr, c=None, weights=None, shading=False):
+        """ivr_step_assemble (value-channel chain rule, opacity L1, densify
+        statistic) in place on K4b's outputs; returns (stat, o partials)."""
+        n, p = self.n, self.p
+        A = L.StepGrads_t()
+        A.n, A.k = n, self.K
+        A.col_delta_c = A.col_k_a = A.col_k_d = A.col_k_s = A.col_beta = -1
+        stat = torch.empty(n, dtype=torch.float64, device=self.dev)
+        A.d_mean2d, A.d_n_raw, A.stat = gr["d_mean2d"].data_ptr(), gr["d_n_raw"].data_ptr(), \
+            stat.data_ptr()
+        part = None
+        if shading:
+            A.d_values = gr["d_values"].data_ptr()
+            A.col_delta_c, A.col_k_a, A.col_k_d = c["delta_c"], c["k_a"], c["k_d"]
+            A.col_k_s, A.col_beta = c["k_s"], c["beta"]
+            for k in ("k_a_raw", "k_d_raw", "k_s_raw", "log_beta"):
+                setattr(A, k, p[k].data_ptr())
+            for k in ("d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta"):
+                setattr(A, k, gr[k].data_ptr())
+            A.o_logit, A.d_o_logit = p["o_logit"].data_ptr(), gr["d_o_logit"].data_ptr()
+            A.w_opacity_l1 = weights.opacity_l1
+            part = torch.empty(int(L.lib().ivr_step_partials(n)), dtype=torch.float64,
+                               device=self.dev)
+            A.o_partial = part.data_ptr()
+        L.check(L.lib().ivr_step_assemble(ctypes.byref(A), D.stream_handle()), "ivr_step_assemble")
+        return stat, part
+
+    def _finalize(self, lt, part=None, w_opacity_l1=0.0):
+        """ivr_loss_finalize: the step's loss (device scalar) + the device-side
+        DivergedLoss bookkeeping (first non-finite photometric loss)."""
         if self._first_bad is None:
-            self._first_bad = torch.full((), -1, dtype=torch.int64, device=self.dev)
-            self._step_no = torch.zeros((), dtype=torch.int64, device=self.dev)
-        self._step_no += 1
-        bad = ~torch.isfinite(loss) & (self._first_bad < 0)
-        self._first_bad = torch.where(bad, self._step_no, self._first_bad)
-        self._last_bad_loss = torch.where(bad, loss, getattr(self, "_last_bad_loss", loss))
+            self._first_bad = torch.tensor([0, -1], dtype=torch.int64, device=self.dev)
+            self._last_bad_loss = torch.zeros((), dtype=torch.float64, device=self.dev)
+        if part is not None:
+            lt.o_partial, lt.n_partial = part.data_ptr(), part.numel()
+            lt.w_opacity_l1, lt.n = w_opacity_l1, float(self.n)
+        loss = torch.empty((), dtype=torch.float64, device=self.dev)
+        L.check(L.lib().ivr_loss_finalize(ctypes.byref(lt), loss.data_ptr(),
+                                          self._first_bad.data_ptr(),
+                                          self._last_bad_loss.data_ptr(), D.stream_handle()),
+                "ivr_loss_finalize")
+        return loss
 
     def check_finite(self):
         """Raise DivergedLoss if any step so far had a non-finite loss."""
-        if self._first_bad is not None and int(self._first_bad) >= 0:
-            raise DivergedLoss(f"loss became {float(self._last_bad_loss)} at step "
-                               f"{int(self._first_bad)}")
+        if self._first_bad is not None:
+            step_no, first = (int(x) for x in self._first_bad.cpu())
+            if first >= 0:
+                raise DivergedLoss(f"loss became {float(self._last_bad_loss)} at step {first}")
 
 
 class BaseTrainer(_StageTrainer):
@@ -318,7 +359,8 @@ class BaseTrainer(_StageTrainer):
         from .sh import sh_backward_device
         weights = weights or self.cfg.weights
         F, dg = self.forward(cam)
-        loss, d_out, _ = self._map_terms(F, cam, gt, weights)
+        lt, keep, d_out, _ = self._map_terms(F, cam, gt, weights)
+        loss = self._finalize(lt)
         g = D.blend_backward(F, d_out)
         want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_mean2d")
         gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, geometry=True, want=want)
@@ -328,8 +370,7 @@ class BaseTrainer(_StageTrainer):
                                   gr["d_colors"].view(n, 3), d_mu=d_mu)
         grads = {"mu": d_mu, "q_raw": gr["d_q_raw"].view(n, 4), "log_s": gr["d_log_s"].view(n, 3),
                  "o_logit": gr["d_o_logit"], "n_raw": gr["d_n_raw"].view(n, 3), "sh": d_sh}
-        stat = torch.linalg.norm(gr["d_mean2d"].view(n, 2), dim=1) + \
-            torch.linalg.norm(grads["n_raw"], dim=1)
+        stat, _ = self._assemble(gr)
         self._bad = bad
         return loss, grads, stat
 
@@ -367,9 +408,16 @@ class EditableTrainer(_StageTrainer):
         dg = dg or self._dg()
         S = D.shading_struct(dg, self.palette, False, self.light)
         p = self.p
-        attrs = {"delta_c": p["delta_c"], "k_a": torch.sigmoid(p["k_a_raw"]),
-                 "k_d": torch.sigmoid(p["k_d_raw"]), "k_s": torch.sigmoid(p["k_s_raw"]),
-                 "beta": torch.exp(p["log_beta"]) + 1.0}
+        n = self.n
+        buf = getattr(self, "_attr_buf", None)
+        if buf is None or buf.shape[1] != n:
+            buf = self._attr_buf = torch.empty((4, n), dtype=torch.float64, device=self.dev)
+        L.check(L.lib().ivr_stage2_attrs(n, p["k_a_raw"].data_ptr(), p["k_d_raw"].data_ptr(),
+                                         p["k_s_raw"].data_ptr(), p["log_beta"].data_ptr(),
+                                         buf[0].data_ptr(), buf[1].data_ptr(), buf[2].data_ptr(),
+                                         buf[3].data_ptr(), D.stream_handle()), "ivr_stage2_attrs")
+        attrs = {"delta_c": p["delta_c"], "k_a": buf[0], "k_d": buf[1], "k_s": buf[2],
+                 "beta": buf[3]}
         attrs_dev = [(attrs[name].reshape(self.n, w).contiguous(), c, w)
                      for name, c, w in self.attr_cols]
         F = D.rasterize_device(dg, cam, self.K, self.cols, self.ws, shading=S, attrs=attrs_dev,
@@ -381,30 +429,20 @@ class EditableTrainer(_StageTrainer):
         all device tensors."""
         weights = weights or self.cfg.weights
         F, S, attrs, dg = self.forward(cam)
-        loss, d_out, c = self._map_terms(F, cam, gt, weights, offset=True, bilateral=True)
+        lt, keep, d_out, c = self._map_terms(F, cam, gt, weights, offset=True, bilateral=True)
         g = D.blend_backward(F, d_out)
         want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_mean2d", "d_values",
                 "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta")
         gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, shading=S, geometry=True,
                                         want=want, light=self.light)
-        n, K = self.n, self.K
-        dv = gr["d_values"].view(n, K)
-        o = torch.sigmoid(self.p["o_logit"])
-        d_o = gr["d_o_logit"]
-        if weights.opacity_l1 > 0.0:
-            loss = loss + weights.opacity_l1 * o.mean()
-            d_o = d_o + weights.opacity_l1 * o * (1.0 - o) / n
-        ka, kd, ks, beta = attrs["k_a"], attrs["k_d"], attrs["k_s"], attrs["beta"]
+        n = self.n
+        stat, part = self._assemble(gr, c, weights, shading=True)
+        loss = self._finalize(lt, part, weights.opacity_l1)
         grads = {"mu": gr["d_mu"].view(n, 3), "q_raw": gr["d_q_raw"].view(n, 4),
-                 "log_s": gr["d_log_s"].view(n, 3), "o_logit": d_o,
-                 "n_raw": gr["d_n_raw"].view(n, 3),
-                 "delta_c": gr["d_delta_c"].view(n, 3) + dv[:, c["delta_c"]:c["delta_c"] + 3],
-                 "k_a_raw": gr["d_k_a_raw"] + dv[:, c["k_a"]] * ka * (1.0 - ka),
-                 "k_d_raw": gr["d_k_d_raw"] + dv[:, c["k_d"]] * kd * (1.0 - kd),
-                 "k_s_raw": gr["d_k_s_raw"] + dv[:, c["k_s"]] * ks * (1.0 - ks),
-                 "log_beta": gr["d_log_beta"] + dv[:, c["beta"]] * (beta - 1.0)}
-        stat = torch.linalg.norm(gr["d_mean2d"].view(n, 2), dim=1) + \
-            torch.linalg.norm(grads["n_raw"], dim=1)
+                 "log_s": gr["d_log_s"].view(n, 3), "o_logit": gr["d_o_logit"],
+                 "n_raw": gr["d_n_raw"].view(n, 3), "delta_c": gr["d_delta_c"].view(n, 3),
+                 "k_a_raw": gr["d_k_a_raw"], "k_d_raw": gr["d_k_d_raw"],
+                 "k_s_raw": gr["d_k_s_raw"], "log_beta": gr["d_log_beta"]}
         self._bad = bad
         return loss, grads, stat
 
