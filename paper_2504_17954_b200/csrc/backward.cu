@@ -70,19 +70,19 @@ __device__ __forceinline__ float warp_sum(float x) {
 // after log2(NS) steps lane l holds slot (l & (NS-1)) summed over its NS-lane
 // group; a final xor over the remaining lane bits completes the warp total.
 // NS-1 (+1 for NS=16) shuffles in place of 5 per slot.
-template <int NS>
-__device__ __forceinline__ float warp_transpose_sum(float *x, int lane) {
+template <int NS, typename T = float>
+__device__ __forceinline__ T warp_transpose_sum(T *x, int lane) {
 #pragma unroll
     for (int h = NS / 2; h >= 1; h >>= 1) {
         const bool up = (lane & h) != 0;
 #pragma unroll
         for (int i = 0; i < h; ++i) {
-            const float send = up ? x[i] : x[i + h];
-            const float keep = up ? x[i + h] : x[i];
+            const T send = up ? x[i] : x[i + h];
+            const T keep = up ? x[i + h] : x[i];
             x[i] = keep + __shfl_xor_sync(0xffffffffu, send, h);
         }
     }
-    float r = x[0];
+    T r = x[0];
 #pragma unroll
     for (int o = NS; o < 32; o <<= 1) r += __shfl_xor_sync(0xffffffffu, r, o);
     return r;
@@ -360,10 +360,19 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
     const ivr_gaussians &G = B.G;
     const ivr_grads &R = B.R;
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i < G.n) {
+    // this thread's contributions to the reductions: [0..9] the 10 global
+    // transform gradients, [10..12] its scene's d_c_p, [13] its d_scale;
+    // warp-reduced (transpose sum) before one shared atomic per slot
+    double red[16];
+#pragma unroll
+    for (int k = 0; k < 16; ++k) red[k] = 0.0;
+    const bool active = i < G.n;
+    int32_t sid_l = -1;
+    if (active) {
         const ivr_camera &cam = P.cam;
         const int K = B.L.k;
         const int32_t sid = (B.has_edits && B.E.scene_id) ? B.E.scene_id[i] : 0;
+        sid_l = sid;
         // ---- per-Gaussian upstream from K4a
         double gv_color[3] = {0, 0, 0}, gv_depth = 0.0, gv_norm[3] = {0, 0, 0};
         double gmean[2] = {0, 0}, gcon[3] = {0, 0, 0}, gop = 0.0;
@@ -402,8 +411,7 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
         flag_bad(R.bad, i, 3, d_o_logit);
         if (R.d_scale && nsc > 0) {
             const double d_p = d_o_logit / (pcl * (1.0 - pcl));
-            const double ds = open_gate ? d_p * o_base : 0.0;
-            atomicAdd(&s_scene[4 * sid + 3], ds);
+            red[13] = open_gate ? d_p * o_base : 0.0;
         }
 
         // ---- geometry (gaussians.project_backward)
@@ -543,8 +551,8 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
                     dp += d_l[k] * R.dl_dp[k];
                     da += d_l[k] * R.dl_da[k];
                 }
-                atomicAdd(&s_glob[8], dp);
-                atomicAdd(&s_glob[9], da);
+                red[8] = dp;
+                red[9] = da;
             }
             double d_w[3];
             normalize_bwd(st.w_cam, d_v, d_w);
@@ -556,14 +564,14 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
             const double e_d = d_k_d * P.term_scales[1] * (st.gates[1] ? 1.0 : 0.0);
             const double e_s = d_k_s * P.term_scales[2] * (st.gates[2] ? 1.0 : 0.0);
             const double e_b = d_beta * P.term_scales[3] * (st.gates[3] ? 1.0 : 0.0);
-            atomicAdd(&s_glob[0], e_a * st.sig[0]);
-            atomicAdd(&s_glob[1], e_d * st.sig[1]);
-            atomicAdd(&s_glob[2], e_s * st.sig[2]);
-            atomicAdd(&s_glob[3], e_b * st.beta1);
-            atomicAdd(&s_glob[4], e_a);
-            atomicAdd(&s_glob[5], e_d);
-            atomicAdd(&s_glob[6], e_s);
-            atomicAdd(&s_glob[7], e_b);
+            red[0] = e_a * st.sig[0];
+            red[1] = e_d * st.sig[1];
+            red[2] = e_s * st.sig[2];
+            red[3] = e_b * st.beta1;
+            red[4] = e_a;
+            red[5] = e_d;
+            red[6] = e_s;
+            red[7] = e_b;
             const double dka = e_a * P.lam[0] * st.sig[0] * (1.0 - st.sig[0]);
             const double dkd = e_d * P.lam[1] * st.sig[1] * (1.0 - st.sig[1]);
             const double dks = e_s * P.lam[2] * st.sig[2] * (1.0 - st.sig[2]);
@@ -577,7 +585,7 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
             if (R.d_delta_c) for (int k = 0; k < 3; ++k) R.d_delta_c[3 * i + k] = dco[k];
             if (R.d_c_p) {
                 if (nsc > 0) {
-                    for (int k = 0; k < 3; ++k) atomicAdd(&s_scene[4 * sid + k], dco[k]);
+                    for (int k = 0; k < 3; ++k) red[10 + k] = dco[k];
                 } else {
                     for (int k = 0; k < 3; ++k) R.d_c_p[3 * i + k] = dco[k];
                 }
@@ -593,6 +601,29 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
         for (int k = 0; k < 3; ++k) {
             flag_bad(R.bad, i, 0, d_mu[k]);
             flag_bad(R.bad, i, 4, d_n_raw[k]);
+        }
+    }
+    {
+        const int lane = threadIdx.x & 31;
+        const unsigned act = __ballot_sync(0xffffffffu, active);
+        if (act) {
+            const int32_t sid0 = __shfl_sync(0xffffffffu, sid_l, __ffs(act) - 1);
+            const bool uni = __all_sync(0xffffffffu, !active || sid_l == sid0);
+            if (!uni) {  // mixed scenes in this warp: per-lane scene atomics
+                if (nsc > 0 && active) {
+#pragma unroll
+                    for (int k = 0; k < 4; ++k)
+                        if (red[10 + k] != 0.0) atomicAdd(&s_scene[4 * sid_l + k], red[10 + k]);
+                }
+#pragma unroll
+                for (int k = 10; k < 14; ++k) red[k] = 0.0;
+            }
+            const double t = warp_transpose_sum<16, double>(red, lane);
+            if (lane < 10) {
+                if (t != 0.0) atomicAdd(&s_glob[lane], t);
+            } else if (lane < 14 && nsc > 0 && uni && t != 0.0) {
+                atomicAdd(&s_scene[4 * sid0 + (lane - 10)], t);
+            }
         }
     }
     __syncthreads();
