@@ -283,13 +283,20 @@ def bench_inverse(scene, dist=None, world=1, rank=0):
         mean, lv = reduce_views(packed, loss.reshape(1), float(world), dist=dist)
         transform_step(params, fit.unpack(mean), adam, 0.01,
                        ("c_p", "opacity_raw", "lam", "b", "angles"), angles)
+    note = "includes the per-iteration pair-count sync and host Adam on 30 floats"
+    if dist is None:
+        # one process: the product path replays whole iterations as a CUDA graph
+        # (device Adam + table refresh, no host round trip per iteration)
+        from paper_2504_17954_b200.inverse import InverseGraph
+        step = InverseGraph(fit, params, 100_000).replay
+        note = "whole iterations replayed as one CUDA graph (InverseGraph: device Adam)"
     mean_ms, med_ms = _device_time(step, 10)
     mean_ms = _max_over_ranks(mean_ms, dist)
     return {"metric": "inverse exploration it/s (composed 1M, 800x800, 1 view per GPU)",
             "value": 1000.0 / mean_ms, "unit": "it/s", "views_per_s": world * 1000.0 / mean_ms,
             "ms_per_it": mean_ms, "ms_per_it_median": med_ms, "n_gpus": world,
             "scaling": "weak (views sharded, one NCCL all-reduce of 31 float64 per iteration)",
-            "note": "includes the per-iteration pair-count sync and host Adam on 30 floats"}
+            "note": note}
 
 
 def bench_vq(scene):

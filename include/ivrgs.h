@@ -27,7 +27,7 @@ extern "C" {
 
 typedef struct CUstream_st *ivr_stream_t; /* == cudaStream_t */
 
-#define IVR_ABI_VERSION 3
+#define IVR_ABI_VERSION 4
 #define IVR_TILE 16 /* rasterizer.py:24 TILE_SIZE */
 
 typedef enum ivr_status {
@@ -151,6 +151,9 @@ typedef struct ivr_frame_params {
     double b[4];
     int32_t orbital;
     int32_t rescale_opacity;
+    /* d light_dir / d polar, d azimuth (orbital): used by ivr_preprocess_bwd
+     * when the params come from device memory (ivr_grads.dl_* otherwise) */
+    double dl_dp[3], dl_da[3];
 } ivr_frame_params;
 
 /* ivr_preprocess_fwd with the camera, light, coefficient transform and the
@@ -251,7 +254,7 @@ typedef struct ivr_grads {
     double *d_scale;   /* (S) opacity-scale chain of inverse._step (inverse.py:174-180) */
     double *d_globals; /* [10] d_lam[4], d_b[4], d_polar, d_azimuth (summed) */
     int32_t per_scene;
-    double dl_dp[3], dl_da[3]; /* orbital light direction derivatives (host) */
+    double dl_dp[3], dl_da[3]; /* orbital light direction derivatives (host-params path) */
     /* [16] first non-finite row per output (init ~0): 0 d_mu, 1 d_q_raw,
      * 2 d_log_s, 3 d_o_logit, 4 d_n_raw, 5 d_colors, 6 d_k_a_raw, 7 d_k_d_raw,
      * 8 d_k_s_raw, 9 d_log_beta, 10 d_delta_c / d_c_p */
@@ -443,6 +446,38 @@ typedef struct ivr_loss_terms {
 } ivr_loss_terms;
 int ivr_loss_finalize(const ivr_loss_terms *t, double *loss, int64_t *state, double *last_bad,
                       ivr_stream_t stream);
+
+/* ---- device-side inverse exploration step (csrc/inverse.cu) ----
+ * State of optimize_to_reference (inverse.py:205-244) kept in device memory so
+ * that complete iterations replay as a CUDA graph.  x = [c_p (3S),
+ * opacity_raw (S), lam (4), b (4), polar, azimuth]; m, v its Adam moments;
+ * t the per-group step counts (c_p, opacity_raw, lam, b, angles); grad and
+ * loss_sum accumulate over the views of one iteration (ivr_inverse_pack) and
+ * are consumed + cleared by ivr_inverse_update, which records losses[iter],
+ * applies Adam per learnable group (bit q of `learnable`) whose mean
+ * gradient exceeds 1e-12, and refreshes tab (palettes (3S), opacity scales
+ * (S)) and the n_views device frame params (lam, b, rescale flag, orbital
+ * light direction + derivatives).  ctl = [iteration, first gated iteration
+ * (-1), reason bits]: a pair-capacity overflow or a non-finite loss gates
+ * that and every later update. */
+#define IVR_INV_OVERFLOW 1
+#define IVR_INV_DIVERGED 2
+typedef struct ivr_inverse_step {
+    int32_t n_scenes, n_views, orbital, learnable;
+    int64_t iters;
+    double *x, *m, *v;
+    int64_t *t;
+    double lr, beta1, beta2, eps;
+    double *grad, *loss_sum, *losses;
+    int64_t *ctl;
+    ivr_frame_params *params; /* n_views, device */
+    double *tab;              /* 4S, device */
+} ivr_inverse_step;
+int ivr_inverse_pack(const ivr_inverse_step *a, const double *photo_sums, double numel,
+                     double windows, const double *d_c_p, const double *d_scale,
+                     const double *d_globals, const int32_t *n_pairs, int64_t pair_capacity,
+                     ivr_stream_t stream);
+int ivr_inverse_update(const ivr_inverse_step *a, ivr_stream_t stream);
 
 #ifdef __cplusplus
 }

@@ -39,7 +39,8 @@ class FrameParams_t(ctypes.Structure):
     _fields_ = [("cam", Camera_t), ("light_dir", ctypes.c_double * 3),
                 ("term_scales", ctypes.c_double * 4), ("lam", ctypes.c_double * 4),
                 ("b", ctypes.c_double * 4), ("orbital", ctypes.c_int32),
-                ("rescale_opacity", ctypes.c_int32)]
+                ("rescale_opacity", ctypes.c_int32), ("dl_dp", ctypes.c_double * 3),
+                ("dl_da", ctypes.c_double * 3)]
 
 
 class Gaussians_t(ctypes.Structure):
@@ -105,6 +106,17 @@ class LossTerms_t(ctypes.Structure):
                 ("n_partial", ctypes.c_int32), ("w_opacity_l1", ctypes.c_double),
                 ("n", ctypes.c_double)]
 
+
+class InverseStep_t(ctypes.Structure):
+    _fields_ = [("n_scenes", ctypes.c_int32), ("n_views", ctypes.c_int32),
+                ("orbital", ctypes.c_int32), ("learnable", ctypes.c_int32),
+                ("iters", ctypes.c_int64), ("x", P), ("m", P), ("v", P), ("t", P),
+                ("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
+                ("eps", ctypes.c_double), ("grad", P), ("loss_sum", P), ("losses", P),
+                ("ctl", P), ("params", P), ("tab", P)]
+
+
+INV_OVERFLOW, INV_DIVERGED = 1, 2
 
 BAD_IDS = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_k_a_raw",
            "d_k_d_raw", "d_k_s_raw", "d_log_beta", "d_delta_c")
@@ -172,6 +184,9 @@ _SIGS = {
                        ctypes.c_double, ctypes.c_double, P], ctypes.c_int),
     "ivr_stage2_attrs": ([ctypes.c_int64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
     "ivr_step_partials": ([ctypes.c_int64], ctypes.c_int32),
+    "ivr_inverse_pack": ([ctypes.POINTER(InverseStep_t), P, ctypes.c_double, ctypes.c_double, P, P,
+                          P, P, ctypes.c_int64, P], ctypes.c_int),
+    "ivr_inverse_update": ([ctypes.POINTER(InverseStep_t), P], ctypes.c_int),
     "ivr_step_assemble": ([ctypes.POINTER(StepGrads_t), P], ctypes.c_int),
     "ivr_loss_finalize": ([ctypes.POINTER(LossTerms_t), P, P, P, P], ctypes.c_int),
     "ivr_regularize_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),

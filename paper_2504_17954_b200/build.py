@@ -17,7 +17,7 @@ PKG = os.path.dirname(os.path.abspath(__file__))
 REPO = os.path.dirname(PKG)
 CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libivrgs.so")
-SOURCES = ["abi.cu", "preprocess.cu", "sort.cu", "blend.cu", "backward.cu", "vq.cu", "sh.cu", "ivrg.cu", "ssim.cu", "regularize.cu", "adam.cu", "concat.cu", "display.cu", "dvr.cu", "trainstep.cu"]
+SOURCES = ["abi.cu", "preprocess.cu", "sort.cu", "blend.cu", "backward.cu", "vq.cu", "sh.cu", "ivrg.cu", "ssim.cu", "regularize.cu", "adam.cu", "concat.cu", "display.cu", "dvr.cu", "trainstep.cu", "inverse.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
 
 

@@ -548,8 +548,8 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
                 }
                 double dp = 0.0, da = 0.0;
                 for (int k = 0; k < 3; ++k) {
-                    dp += d_l[k] * R.dl_dp[k];
-                    da += d_l[k] * R.dl_da[k];
+                    dp += d_l[k] * P.dl_dp[k];
+                    da += d_l[k] * P.dl_da[k];
                 }
                 red[8] = dp;
                 red[9] = da;
@@ -708,7 +708,13 @@ extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *sha
     B.R = *grads;
     B.geometry = geometry;
     ivr_frame_params Pv{};
-    if (!params) Pv = params_from(*cam, shading, edits);
+    if (!params) {
+        Pv = params_from(*cam, shading, edits);
+        for (int k = 0; k < 3; ++k) {
+            Pv.dl_dp[k] = grads->dl_dp[k];
+            Pv.dl_da[k] = grads->dl_da[k];
+        }
+    }
     const int threads = 128;
     const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
     const size_t sm = (size_t)grads->per_scene * 4 * sizeof(double);

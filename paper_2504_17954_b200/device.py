@@ -247,7 +247,18 @@ def frame_params(cam, light=None, lam=None, b=None, rescale_opacity=False) -> L.
     for i in range(4):
         P.term_scales[i], P.lam[i], P.b[i] = float(ts[i]), float(lam[i]), float(b[i])
     P.rescale_opacity = 1 if rescale_opacity else 0
+    if P.orbital:
+        dp, da = light_direction_derivatives(light.polar, light.azimuth)
+        for i in range(3):
+            P.dl_dp[i], P.dl_da[i] = float(dp[i]), float(da[i])
     return P
+
+
+def light_direction_derivatives(polar, azimuth):
+    """d light_direction / d polar, d azimuth (host float64)."""
+    p, a = polar, azimuth
+    return ((-np.sin(p) * np.cos(a), -np.sin(p) * np.sin(a), np.cos(p)),
+            (-np.cos(p) * np.sin(a), np.cos(p) * np.cos(a), 0.0))
 
 
 def bin_sort(F: Frame, ws: Workspace, stream=None, capacity=None):
@@ -366,9 +377,7 @@ def preprocess_backward(dg: DeviceGaussians, cam, K, cols, g=None, shading=None,
         o += sz
     R.per_scene = 0 if per_splat_c_p else int(per_scene)
     if light is not None and light.mode == "orbital":
-        p, a = light.polar, light.azimuth
-        dp = (-np.sin(p) * np.cos(a), -np.sin(p) * np.sin(a), np.cos(p))
-        da = (-np.cos(p) * np.sin(a), np.cos(p) * np.cos(a), 0.0)
+        dp, da = light_direction_derivatives(light.polar, light.azimuth)
         for i in range(3):
             R.dl_dp[i], R.dl_da[i] = float(dp[i]), float(da[i])
     bad = torch.full((16,), -1, dtype=torch.int64, device=dev)  # ~0 as uint64

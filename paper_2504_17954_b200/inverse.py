@@ -17,6 +17,7 @@ the reference exactly.
 
 from __future__ import annotations
 
+import ctypes
 import hashlib
 from dataclasses import dataclass
 
@@ -25,7 +26,7 @@ import torch
 
 from . import device as D
 from .errors import DivergedLoss, OutOfRange, ShapeMismatch
-from .losses import photometric_loss_t
+from .losses import _photometric_dev, photometric_loss_t
 from .scene import ComposedScene, DeviceScene
 from .shading import ORBITAL, LightConfig
 
@@ -217,6 +218,137 @@ def transform_step(params, grads, adam, lr, learnable, angles):
         params.polar, params.azimuth = float(angles[0]), float(angles[1])
 
 
+_LEARN_BITS = {"c_p": 1, "opacity_raw": 2, "lam": 4, "b": 8, "angles": 16}
+
+
+class InverseGraph:
+    """Whole inverse iterations replayed as one CUDA graph: every view's
+    render (K1-K3), L1+SSIM, K4a, transform-only K4b and gradient pack, then
+    the device Adam + table refresh (csrc/inverse.cu).  The transform state
+    (x, Adam moments, per-group step counts) and the frame tables live in HBM,
+    so an iteration needs no host round trip; ``run`` replays and checks the
+    sticky overflow / divergence gate once at the end (growing the pair
+    capacity and resuming from the first gated iteration if needed)."""
+
+    def __init__(self, fit, params, iters, lr=0.01, learnable=None, headroom=1.3):
+        from . import _lib as L
+        self.fit, self.L = fit, L
+        ds = fit.ds
+        dev = ds.dg.device
+        S, V = fit.S, len(fit.cams)
+        N = 4 * S + 10
+        self.S, self.V, self.N, self.iters = S, V, N, int(iters)
+        learnable = learnable or ("c_p", "opacity_raw", "lam", "b", "angles")
+        self.light = _light(fit.scene, params)
+        self.orbital = self.light.mode == ORBITAL  # angle gradients packed (view_grads)
+        if params.light_mode != ORBITAL:  # ... but only stepped for an orbital transform
+            learnable = tuple(k for k in learnable if k != "angles")
+        x0 = np.concatenate([params.c_p.reshape(-1), params.opacity_raw, params.lam, params.b,
+                             [params.polar, params.azimuth]]).astype(np.float64)
+        f64 = dict(dtype=torch.float64, device=dev)
+        self.x = torch.from_numpy(x0).to(dev)
+        self.m, self.v = torch.zeros(N, **f64), torch.zeros(N, **f64)
+        self.t = torch.zeros(5, dtype=torch.int64, device=dev)
+        self.acc = torch.zeros(N + 1, **f64)  # grad (N) + loss sum
+        self.losses = torch.zeros(self.iters, **f64)
+        self.ctl = torch.tensor([0, -1, 0], dtype=torch.int64, device=dev)
+        self.nb = nb = ctypes.sizeof(L.FrameParams_t)
+        scales = softplus(params.opacity_raw)
+        host = bytearray()
+        for cam in fit.cams:
+            P = D.frame_params(cam, self.light, params.lam, params.b,
+                               rescale_opacity=not np.all(scales == 1.0))
+            host += bytes(P)
+        self.params_dev = torch.frombuffer(host, dtype=torch.uint8).to(dev)
+        self.tab = torch.from_numpy(np.concatenate([params.c_p.reshape(-1), scales])).to(dev)
+        self._init = [t.clone() for t in (self.x, self.params_dev, self.tab)]
+        st = L.InverseStep_t()
+        st.n_scenes, st.n_views = S, V
+        st.orbital = 1 if self.orbital else 0
+        st.learnable = sum(_LEARN_BITS[k] for k in learnable)
+        st.iters = self.iters
+        st.x, st.m, st.v, st.t = (self.x.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
+                                  self.t.data_ptr())
+        st.lr, st.beta1, st.beta2, st.eps = float(lr), 0.9, 0.999, 1e-15
+        st.grad, st.loss_sum = self.acc.data_ptr(), self.acc[N:].data_ptr()
+        st.losses, st.ctl = self.losses.data_ptr(), self.ctl.data_ptr()
+        st.params, st.tab = self.params_dev.data_ptr(), self.tab.data_ptr()
+        self.st = st
+        self.shading = D.shading_struct(ds.dg, self.tab[:3 * S], False, self.light, params.lam,
+                                        params.b)
+        self.edits = L.Edits_t()
+        self.edits.scene_id = ds.dg.scene_id.data_ptr()
+        self.edits.opacity_scale = self.tab[3 * S:].data_ptr()
+        # pair capacity from one synchronous render per view (+ headroom)
+        peak = 0
+        for cam in fit.cams:
+            F = fit.render(params, cam, want_state=False)
+            peak = max(peak, int(F.n_pairs.item()))
+        self.capacity = max(int(peak * headroom) + 4096, 1 << 16)
+        self._capture()
+
+    def _iteration(self):
+        L, fit, ds = self.L, self.fit, self.fit.ds
+        ws = ds.ws
+        for v, cam in enumerate(fit.cams):
+            pdev = self.params_dev[v * self.nb:(v + 1) * self.nb]
+            F = D.preprocess(ds.dg, cam, 4, (0, 3, -1, -1), ws, self.shading, self.edits, None, (),
+                             True, params_dev=pdev)
+            D.bin_sort(F, ws, capacity=self.capacity)
+            D.blend(F, ws, want_state=True, exact=fit.exact)
+            h, w, nc = F.out64.shape
+            win = 11
+            sums, d = _photometric_dev(F.out64, fit.refs[v], 0.8 / F.out64.numel(), -0.2, True)
+            g = D.blend_backward(F, d)
+            out, _ = D.preprocess_backward(ds.dg, cam, 4, (0, 3, -1, -1), g=g, shading=self.shading,
+                                           edits=self.edits, params_dev=pdev, geometry=False,
+                                           want=("d_c_p", "d_scale"), per_scene=self.S,
+                                           light=self.light)
+            L.check(L.lib().ivr_inverse_pack(
+                ctypes.byref(self.st), sums.data_ptr(), float(h * w * nc),
+                float((h - win + 1) * (w - win + 1) * nc), out["d_c_p"].data_ptr(),
+                out["d_scale"].data_ptr(), out["d_globals"].data_ptr(), F.n_pairs.data_ptr(),
+                self.capacity, D.stream_handle()), "ivr_inverse_pack")
+        L.check(L.lib().ivr_inverse_update(ctypes.byref(self.st), D.stream_handle()),
+                "ivr_inverse_update")
+
+    def _capture(self):
+        saved = [t.clone() for t in (self.x, self.m, self.v, self.t, self.acc, self.losses,
+                                     self.ctl, self.params_dev, self.tab)]
+        self._iteration()  # sizes every workspace buffer before capture
+        torch.cuda.synchronize()
+        for t, s0 in zip((self.x, self.m, self.v, self.t, self.acc, self.losses, self.ctl,
+                          self.params_dev, self.tab), saved):
+            t.copy_(s0)
+        torch.cuda.synchronize()
+        self.g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g):
+            self._iteration()
+        torch.cuda.synchronize()
+
+    def replay(self):
+        self.g.replay()
+
+    def run(self):
+        """All iterations; returns (TransformParams fields as numpy, losses)."""
+        start = 0
+        while True:
+            for _ in range(self.iters - start):
+                self.g.replay()
+            ctl = self.ctl.cpu().numpy()
+            first, reason = int(ctl[1]), int(ctl[2])
+            if first < 0:
+                break
+            if reason & self.L.INV_OVERFLOW:
+                self.capacity *= 2
+                self.ctl.copy_(torch.tensor([first, -1, 0], dtype=torch.int64))
+                self._capture()
+                start = first
+                continue
+            raise DivergedLoss(f"loss became {float(self.losses[first])}")
+        return self.x.cpu().numpy(), self.losses.cpu().numpy().tolist()
+
+
 def optimize_to_reference(scene, params, reference_rgba, reference_cam, iters=1000, lr=0.01,
                           callback=None, learnable=None, group=None, exact=False):
     """Fit the transform to reference image(s) with Adam on L1 + SSIM
@@ -242,6 +374,19 @@ def optimize_to_reference(scene, params, reference_rgba, reference_cam, iters=10
     if dist:
         dist.all_reduce(n_views, group=group)
     n_views = float(n_views.item())
+    if dist is None and callback is None and iters > 0 and fit.cams:
+        # one process: whole iterations replay as a CUDA graph (no host round trip)
+        G = InverseGraph(fit, params, iters, lr, learnable)
+        x, losses = G.run()
+        S = fit.S
+        params.c_p = x[:3 * S].reshape(S, 3).copy()
+        params.opacity_raw = x[3 * S:4 * S].copy()
+        params.lam, params.b = x[4 * S:4 * S + 4].copy(), x[4 * S + 4:4 * S + 8].copy()
+        if params.light_mode == ORBITAL:
+            params.polar, params.azimuth = float(x[4 * S + 8]), float(x[4 * S + 9])
+        after = _frozen_fingerprint(scene)
+        assert before == after, "primitive attributes changed during inverse fitting"
+        return params, losses
     adam = Adam(eps=1e-15)
     angles = np.array([params.polar, params.azimuth])
     losses = []

@@ -16,7 +16,7 @@ def test_library_loads_and_exports_header_symbols():
     assert "ivr_blend_fwd" in declared and "ivr_bin_sort" in declared
     for name in declared:
         assert hasattr(L, name), f"{name} declared in include/ivrgs.h but not exported"
-    assert _lib.lib().ivr_version() == 3
+    assert _lib.lib().ivr_version() == 4
 
 
 def test_argument_validation_without_gpu():

@@ -95,3 +95,61 @@ def test_multiview_mean_equals_mean_of_single_views():
     l1, g1 = fit.view_grads(p, 1)
     mean = ((g0 + g1) / 2).cpu().numpy()
     assert np.all(np.isfinite(mean)) and np.abs(mean).max() > 0
+
+
+def _orbital_setup(n_views=2):
+    from paper_2504_17954_b200 import LightConfig, orbit_camera
+    from paper_2504_17954_b200.inverse import InverseFitter, init_transform
+    d = golden("inverse")
+    sc = _scene(d)
+    sc.light = LightConfig("orbital", 0.4, 0.7)
+    cams = [orbit_camera(np.zeros(3), 2.5, 0.3, az, 0.9, 40, 40) for az in (0.8, 2.0, 3.1)][:n_views]
+    p = init_transform(sc)
+    p_true = p.copy()
+    p_true.lam = np.array([1.2, 0.8, 1.0, 1.0])
+    p_true.polar, p_true.azimuth = 0.5, 0.9
+    refs = [InverseFitter(sc, [], []).render(p_true, c).out64.cpu().numpy() for c in cams]
+    return sc, p, refs, cams
+
+
+def test_inverse_graph_matches_host_loop():
+    """The graph-replayed loop (device Adam + table refresh) follows the host
+    loop's trajectory (orbital light: angle gradients and light refresh)."""
+    from paper_2504_17954_b200.inverse import optimize_to_reference
+    sc, p, refs, cams = _orbital_setup()
+    seen = []
+    fh, lh = optimize_to_reference(sc, p, refs, cams, iters=6, lr=0.01,
+                                   callback=lambda it, loss, prm: seen.append(it))
+    fg, lg = optimize_to_reference(sc, p, refs, cams, iters=6, lr=0.01)
+    assert seen == list(range(1, 7))
+    # K4a's float32 atomics make each run's gradients differ in the last bits
+    np.testing.assert_allclose(lg, lh, rtol=1e-6)
+    for k in ("c_p", "opacity_raw", "lam", "b", "polar", "azimuth"):
+        np.testing.assert_allclose(getattr(fg, k), getattr(fh, k), rtol=1e-6, atol=1e-8,
+                                   err_msg=k)
+    assert abs(fg.polar - p.polar) > 0  # the angles moved
+
+
+def test_inverse_graph_recovers_from_pair_overflow():
+    """A too-small pair capacity gates the update (sticky), and run() grows the
+    capacity, recaptures and resumes from the first gated iteration."""
+    from paper_2504_17954_b200.inverse import InverseFitter, InverseGraph
+    sc, p, refs, cams = _orbital_setup(1)
+    ref_x, ref_l = InverseGraph(InverseFitter(sc, refs, cams), p, 4).run()
+    G = InverseGraph(InverseFitter(sc, refs, cams), p, 4)
+    G.capacity = 64
+    G._capture()
+    x, losses = G.run()
+    assert G.capacity > 64
+    np.testing.assert_allclose(losses, ref_l, rtol=1e-6)
+    np.testing.assert_allclose(x, ref_x, rtol=1e-6, atol=1e-8)
+
+
+def test_inverse_graph_divergence_raises():
+    from paper_2504_17954_b200 import DivergedLoss
+    from paper_2504_17954_b200.inverse import optimize_to_reference
+    sc, p, refs, cams = _orbital_setup(1)
+    bad = refs[0].copy()
+    bad[0, 0, 0] = np.nan
+    with pytest.raises(DivergedLoss):
+        optimize_to_reference(sc, p, [bad], cams, iters=3)
