@@ -22,8 +22,14 @@ namespace ivr {
 namespace ssimk {
 
 constexpr int R = 5, WIN = 2 * R + 1;
-constexpr int TH = 16, TW = 32;                 // output tile (windows in A, pixels in B)
-constexpr int IH = TH + WIN - 1, IW = TW + WIN - 1;  // 26 x 42 staged patch
+constexpr int TH = 32, TW = 32;                 // output tile (windows in A, pixels in B)
+constexpr int IH = TH + WIN - 1, IW = TW + WIN - 1;  // 42 x 42 staged patch
+// register blocking: every filtering thread produces RB consecutive outputs of
+// its row (horizontal) or column (vertical), streaming the RB + 10 inputs once
+// from shared memory (RB + 10 loads for RB outputs instead of 11 RB); the
+// taps of each output are still accumulated in ascending order
+constexpr int RB = 4;
+static_assert((TH / RB) * TW == 256, "one vertical strip per thread");
 constexpr int kThreads = 256;
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
@@ -70,51 +76,77 @@ __global__ void __launch_bounds__(kThreads) ssim_window_kernel(Args A) {
             sy[k] = ok ? A.y[o] : 0.0;
         }
         __syncthreads();
-        for (int k = tid; k < IH * TW; k += kThreads) {
-            const int r = k / TW, q = k % TW;
-            double h0 = 0.0, h1 = 0.0, h2 = 0.0, h3 = 0.0, h4 = 0.0;
+        for (int k = tid; k < IH * (TW / RB); k += kThreads) {
+            const int r = k / (TW / RB), q0 = (k % (TW / RB)) * RB;
+            double h[5][RB];
 #pragma unroll
-            for (int t = 0; t < WIN; ++t) {
-                const double xv = sx[r * IW + q + t], yv = sy[r * IW + q + t], g = A.g[t];
-                h0 = fma(g, xv, h0);
-                h1 = fma(g, yv, h1);
-                h2 = fma(g, xv * xv, h2);
-                h3 = fma(g, yv * yv, h3);
-                h4 = fma(g, xv * yv, h4);
+            for (int o = 0; o < RB; ++o)
+#pragma unroll
+                for (int m = 0; m < 5; ++m) h[m][o] = 0.0;
+#pragma unroll
+            for (int jj = 0; jj < RB + WIN - 1; ++jj) {
+                const double xv = sx[r * IW + q0 + jj], yv = sy[r * IW + q0 + jj];
+                const double xx = xv * xv, yy = yv * yv, xy = xv * yv;
+#pragma unroll
+                for (int o = 0; o < RB; ++o) {
+                    const int t = jj - o;
+                    if (t < 0 || t >= WIN) continue;
+                    const double g = A.g[t];
+                    h[0][o] = fma(g, xv, h[0][o]);
+                    h[1][o] = fma(g, yv, h[1][o]);
+                    h[2][o] = fma(g, xx, h[2][o]);
+                    h[3][o] = fma(g, yy, h[3][o]);
+                    h[4][o] = fma(g, xy, h[4][o]);
+                }
             }
-            hq[0 * IH * TW + k] = h0;
-            hq[1 * IH * TW + k] = h1;
-            hq[2 * IH * TW + k] = h2;
-            hq[3 * IH * TW + k] = h3;
-            hq[4 * IH * TW + k] = h4;
+#pragma unroll
+            for (int m = 0; m < 5; ++m)
+#pragma unroll
+                for (int o = 0; o < RB; ++o) hq[m * IH * TW + r * TW + q0 + o] = h[m][o];
         }
         __syncthreads();
-        for (int k = tid; k < TH * TW; k += kThreads) {
-            const int r = k / TW, q = k % TW, wi = i0 + r, wj = j0 + q;
-            if (wi >= A.Hv || wj >= A.Wv) continue;
-            double u[5] = {0.0, 0.0, 0.0, 0.0, 0.0};
+        {
+            const int q = tid % TW, r0 = (tid / TW) * RB;
+            double u[5][RB];
 #pragma unroll
-            for (int t = 0; t < WIN; ++t) {
-                const double g = A.g[t];
+            for (int m = 0; m < 5; ++m) {
 #pragma unroll
-                for (int m = 0; m < 5; ++m) u[m] = fma(g, hq[m * IH * TW + (r + t) * TW + q], u[m]);
+                for (int o = 0; o < RB; ++o) u[m][o] = 0.0;
+#pragma unroll
+                for (int ii = 0; ii < RB + WIN - 1; ++ii) {
+                    const double v = hq[m * IH * TW + (r0 + ii) * TW + q];
+#pragma unroll
+                    for (int o = 0; o < RB; ++o) {
+                        const int t = ii - o;
+                        if (t < 0 || t >= WIN) continue;
+                        u[m][o] = fma(A.g[t], v, u[m][o]);
+                    }
+                }
             }
-            const double ux = u[0], uy = u[1];
-            const double vx = u[2] - ux * ux, vy = u[3] - uy * uy, vxy = u[4] - ux * uy;
-            const double a1 = 2.0 * ux * uy + kC1, a2 = 2.0 * vxy + kC2;
-            const double b1 = ux * ux + uy * uy + kC1, b2 = vx + vy + kC2;
-            const double bb = b1 * b2;
-            const double s = (a1 * a2) / bb;
-            ssum += s;
-            const double da1 = a2 / bb * A.up, da2 = a1 / bb * A.up;
-            const double db1 = -s / b1 * A.up, db2 = -s / b2 * A.up;
-            const double d_uxy = 2.0 * da2;
-            const double d_uxx = db2;
-            const double d_ux = 2.0 * uy * da1 + 2.0 * ux * db1 - 2.0 * ux * db2 - uy * d_uxy;
-            const int64_t o = ((int64_t)c * A.Hv + wi) * A.Wv + wj;
-            A.m_ux[o] = d_ux;
-            A.m_uxx[o] = d_uxx;
-            A.m_uxy[o] = d_uxy;
+            const int wj = j0 + q;
+#pragma unroll
+            for (int o = 0; o < RB; ++o) {
+                const int wi = i0 + r0 + o;
+                if (wi >= A.Hv || wj >= A.Wv) continue;
+                const double ux = u[0][o], uy = u[1][o];
+                const double vx = u[2][o] - ux * ux, vy = u[3][o] - uy * uy, vxy = u[4][o] - ux * uy;
+                const double a1 = 2.0 * ux * uy + kC1, a2 = 2.0 * vxy + kC2;
+                const double b1 = ux * ux + uy * uy + kC1, b2 = vx + vy + kC2;
+                const double bb = b1 * b2;
+                const double s = (a1 * a2) / bb;  // the reference's SSIM value
+                ssum += s;
+                // gradient-only partials from one reciprocal (1/b1 = b2/bb, 1/b2 = b1/bb)
+                const double ibb = 1.0 / bb, sup = s * ibb * A.up;
+                const double da1 = a2 * ibb * A.up, da2 = a1 * ibb * A.up;
+                const double db1 = -sup * b2, db2 = -sup * b1;
+                const double d_uxy = 2.0 * da2;
+                const double d_uxx = db2;
+                const double d_ux = 2.0 * uy * da1 + 2.0 * ux * db1 - 2.0 * ux * db2 - uy * d_uxy;
+                const int64_t o2 = ((int64_t)c * A.Hv + wi) * A.Wv + wj;
+                A.m_ux[o2] = d_ux;
+                A.m_uxx[o2] = d_uxx;
+                A.m_uxy[o2] = d_uxy;
+            }
         }
     }
     const double t = block_sum(ssum, s_red);
@@ -143,41 +175,69 @@ __global__ void __launch_bounds__(kThreads) ssim_grad_kernel(Args A) {
                 mq[2 * IH * IW + k] = ok ? A.m_uxy[o] : 0.0;
             }
             __syncthreads();
-            for (int k = tid; k < IH * TW; k += kThreads) {
-                const int r = k / TW, q = k % TW;
-                double h[3] = {0.0, 0.0, 0.0};
+            for (int k = tid; k < IH * (TW / RB); k += kThreads) {
+                const int r = k / (TW / RB), q0 = (k % (TW / RB)) * RB;
+                double h[3][RB];
 #pragma unroll
-                for (int t = 0; t < WIN; ++t) {
-                    const double g = A.g[t];
+                for (int o = 0; o < RB; ++o)
 #pragma unroll
-                    for (int m = 0; m < 3; ++m)
-                        h[m] = fma(g, mq[m * IH * IW + r * IW + q + (WIN - 1) - t], h[m]);
+                    for (int m = 0; m < 3; ++m) h[m][o] = 0.0;
+                // output q0 + o takes tap t from column q0 + o + 10 - t: stream
+                // the columns right to left so every output's taps ascend
+#pragma unroll
+                for (int jj = RB + WIN - 2; jj >= 0; --jj) {
+                    double v[3];
+#pragma unroll
+                    for (int m = 0; m < 3; ++m) v[m] = mq[m * IH * IW + r * IW + q0 + jj];
+#pragma unroll
+                    for (int o = 0; o < RB; ++o) {
+                        const int t = o + (WIN - 1) - jj;
+                        if (t < 0 || t >= WIN) continue;
+                        const double g = A.g[t];
+#pragma unroll
+                        for (int m = 0; m < 3; ++m) h[m][o] = fma(g, v[m], h[m][o]);
+                    }
                 }
 #pragma unroll
-                for (int m = 0; m < 3; ++m) hq[m * IH * TW + k] = h[m];
+                for (int m = 0; m < 3; ++m)
+#pragma unroll
+                    for (int o = 0; o < RB; ++o) hq[m * IH * TW + r * TW + q0 + o] = h[m][o];
             }
             __syncthreads();
         }
-        for (int k = tid; k < TH * TW; k += kThreads) {
-            const int r = k / TW, q = k % TW, pi = i0 + r, pj = j0 + q;
+        const int q = tid % TW, r0 = (tid / TW) * RB;
+        double f[3][RB];
+#pragma unroll
+        for (int m = 0; m < 3; ++m)
+#pragma unroll
+            for (int o = 0; o < RB; ++o) f[m][o] = 0.0;
+        if (SSIM) {
+#pragma unroll
+            for (int m = 0; m < 3; ++m) {
+#pragma unroll
+                for (int ii = RB + WIN - 2; ii >= 0; --ii) {
+                    const double v = hq[m * IH * TW + (r0 + ii) * TW + q];
+#pragma unroll
+                    for (int o = 0; o < RB; ++o) {
+                        const int t = o + (WIN - 1) - ii;
+                        if (t < 0 || t >= WIN) continue;
+                        f[m][o] = fma(A.g[t], v, f[m][o]);
+                    }
+                }
+            }
+        }
+        const int pj = j0 + q;
+#pragma unroll
+        for (int o = 0; o < RB; ++o) {
+            const int pi = i0 + r0 + o;
             if (pi >= A.H || pj >= A.W) continue;
-            const int64_t o = ((int64_t)pi * A.W + pj) * A.C + c;
-            const double xv = A.x[o], yv = A.y[o];
+            const int64_t oo = ((int64_t)pi * A.W + pj) * A.C + c;
+            const double xv = A.x[oo], yv = A.y[oo];
             const double df = xv - yv;
             l1 += fabs(df);
             double d = A.a * (df > 0.0 ? 1.0 : (df < 0.0 ? -1.0 : 0.0));
-            if (SSIM) {
-                double f[3] = {0.0, 0.0, 0.0};
-#pragma unroll
-                for (int t = 0; t < WIN; ++t) {
-                    const double g = A.g[t];
-#pragma unroll
-                    for (int m = 0; m < 3; ++m)
-                        f[m] = fma(g, hq[m * IH * TW + (r + (WIN - 1) - t) * TW + q], f[m]);
-                }
-                d += A.b * (f[0] + 2.0 * xv * f[1] + yv * f[2]);
-            }
-            A.d_pred[o] = d;
+            if (SSIM) d += A.b * (f[0][o] + 2.0 * xv * f[1][o] + yv * f[2][o]);
+            A.d_pred[oo] = d;
         }
     }
     const double t = block_sum(l1, s_red);
