@@ -30,6 +30,7 @@ constexpr int IH = TH + WIN - 1, IW = TW + WIN - 1;  // 42 x 42 staged patch
 // taps of each output are still accumulated in ascending order
 constexpr int RB = 4;
 static_assert((TH / RB) * TW == 256, "one vertical strip per thread");
+constexpr int kStageIt = (IH * IW + 255) / 256;  // staging elements per thread
 constexpr int kThreads = 256;
 constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
@@ -68,12 +69,27 @@ __global__ void __launch_bounds__(kThreads) ssim_window_kernel(Args A) {
     double ssum = 0.0;
     for (int c = 0; c < A.C; ++c) {
         __syncthreads();
-        for (int k = tid; k < IH * IW; k += kThreads) {
-            const int r = k / IW, q = k % IW, gi = i0 + r, gj = j0 + q;
-            const bool ok = gi < A.H && gj < A.W;
-            const int64_t o = ((int64_t)gi * A.W + gj) * A.C + c;
-            sx[k] = ok ? A.x[o] : 0.0;
-            sy[k] = ok ? A.y[o] : 0.0;
+        // staging: fully unrolled so every load of the patch is in flight at once
+        // (a rolled loop serialises one global round trip per 256 elements)
+        {
+            double vx[kStageIt], vy[kStageIt];
+#pragma unroll
+            for (int it = 0; it < kStageIt; ++it) {
+                const int k = it * kThreads + tid;
+                const int r = k / IW, q = k % IW, gi = i0 + r, gj = j0 + q;
+                const bool ok = k < IH * IW && gi < A.H && gj < A.W;
+                const int64_t o = ((int64_t)gi * A.W + gj) * A.C + c;
+                vx[it] = ok ? A.x[o] : 0.0;
+                vy[it] = ok ? A.y[o] : 0.0;
+            }
+#pragma unroll
+            for (int it = 0; it < kStageIt; ++it) {
+                const int k = it * kThreads + tid;
+                if (k < IH * IW) {
+                    sx[k] = vx[it];
+                    sy[k] = vy[it];
+                }
+            }
         }
         __syncthreads();
         for (int k = tid; k < IH * (TW / RB); k += kThreads) {
@@ -166,13 +182,25 @@ __global__ void __launch_bounds__(kThreads) ssim_grad_kernel(Args A) {
     for (int c = 0; c < A.C; ++c) {
         if (SSIM) {
             __syncthreads();
-            for (int k = tid; k < IH * IW; k += kThreads) {
+            double v0[kStageIt], v1[kStageIt], v2[kStageIt];
+#pragma unroll
+            for (int it = 0; it < kStageIt; ++it) {
+                const int k = it * kThreads + tid;
                 const int r = k / IW, q = k % IW, wi = i0 - (WIN - 1) + r, wj = j0 - (WIN - 1) + q;
-                const bool ok = wi >= 0 && wj >= 0 && wi < A.Hv && wj < A.Wv;
+                const bool ok = k < IH * IW && wi >= 0 && wj >= 0 && wi < A.Hv && wj < A.Wv;
                 const int64_t o = ((int64_t)c * A.Hv + wi) * A.Wv + wj;
-                mq[0 * IH * IW + k] = ok ? A.m_ux[o] : 0.0;
-                mq[1 * IH * IW + k] = ok ? A.m_uxx[o] : 0.0;
-                mq[2 * IH * IW + k] = ok ? A.m_uxy[o] : 0.0;
+                v0[it] = ok ? A.m_ux[o] : 0.0;
+                v1[it] = ok ? A.m_uxx[o] : 0.0;
+                v2[it] = ok ? A.m_uxy[o] : 0.0;
+            }
+#pragma unroll
+            for (int it = 0; it < kStageIt; ++it) {
+                const int k = it * kThreads + tid;
+                if (k < IH * IW) {
+                    mq[0 * IH * IW + k] = v0[it];
+                    mq[1 * IH * IW + k] = v1[it];
+                    mq[2 * IH * IW + k] = v2[it];
+                }
             }
             __syncthreads();
             for (int k = tid; k < IH * (TW / RB); k += kThreads) {
