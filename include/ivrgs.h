@@ -459,7 +459,7 @@ int ivr_loss_finalize(const ivr_loss_terms *t, double *loss, int64_t *state, dou
  * (S)) and the n_views device frame params (lam, b, rescale flag, orbital
  * light direction + derivatives).  ctl = [iteration, first gated iteration
  * (-1), reason bits]: a pair-capacity overflow or a non-finite loss gates
- * that and every later update. */
+ * that and every later update.  n_scenes <= 1024. */
 #define IVR_INV_OVERFLOW 1
 #define IVR_INV_DIVERGED 2
 typedef struct ivr_inverse_step {

@@ -91,7 +91,23 @@ __global__ void __launch_bounds__(kThreads) assemble_kernel(ivr_step_grads A) {
     }
 }
 
-__global__ void finalize_kernel(ivr_loss_terms T, double *loss, int64_t *state, double *last_bad) {
+constexpr int kFinThreads = 256;
+
+__global__ void __launch_bounds__(kFinThreads)
+finalize_kernel(ivr_loss_terms T, double *loss, int64_t *state, double *last_bad) {
+    // opacity partials: fixed strided split + fixed-order tree (deterministic);
+    // one thread summing them serially put ~25 us of dependent loads on the
+    // step's critical path
+    __shared__ double s_part[kFinThreads];
+    double ps = 0.0;
+    if (T.o_partial)
+        for (int b = threadIdx.x; b < T.n_partial; b += kFinThreads) ps = dadd(ps, T.o_partial[b]);
+    s_part[threadIdx.x] = ps;
+    __syncthreads();
+    for (int h = kFinThreads / 2; h > 0; h >>= 1) {
+        if (threadIdx.x < h) s_part[threadIdx.x] = dadd(s_part[threadIdx.x], s_part[threadIdx.x + h]);
+        __syncthreads();
+    }
     if (threadIdx.x != 0 || blockIdx.x != 0) return;
     // photometric part (losses.photometric_loss): l1 * mean|x - y| + s * (1 - mean SSIM)
     double photo = dmul(T.l1_weight, ddiv(T.photo_sums[1], T.numel));
@@ -103,11 +119,7 @@ __global__ void finalize_kernel(ivr_loss_terms T, double *loss, int64_t *state, 
         if (T.w_offset > 0.0) L = dadd(L, dmul(T.w_offset, T.terms[1]));
         if (T.w_bil > 0.0) L = dadd(L, dmul(T.w_bil, T.terms[2]));
     }
-    if (T.o_partial && T.w_opacity_l1 > 0.0) {
-        double s = 0.0;
-        for (int b = 0; b < T.n_partial; ++b) s = dadd(s, T.o_partial[b]);
-        L = dadd(L, dmul(T.w_opacity_l1, ddiv(s, T.n)));
-    }
+    if (T.o_partial && T.w_opacity_l1 > 0.0) L = dadd(L, dmul(T.w_opacity_l1, ddiv(s_part[0], T.n)));
     *loss = L;
     if (state) {  // [step count, first step with a non-finite photometric loss or -1]
         state[0] += 1;
@@ -169,6 +181,6 @@ extern "C" int ivr_loss_finalize(const ivr_loss_terms *t, double *loss, int64_t 
         ivr::set_error("ivr_loss_finalize: bad argument");
         return IVR_ERR_ARG;
     }
-    finalize_kernel<<<1, 32, 0, (cudaStream_t)stream>>>(*t, loss, state, last_bad);
+    finalize_kernel<<<1, kFinThreads, 0, (cudaStream_t)stream>>>(*t, loss, state, last_bad);
     return ivr::check_launch("finalize_kernel");
 }

@@ -1,4 +1,6 @@
-"""One C4 inverse iteration between cudaProfilerStart/Stop (ncu)."""
+"""One C4 inverse iteration between cudaProfilerStart/Stop (ncu): one replay
+of the InverseGraph (render + loss + backward + pack + device Adam); ncu
+profiles the graph's kernel nodes one by one."""
 import os
 import sys
 
@@ -6,7 +8,7 @@ sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 
 import torch  # noqa: E402
 
-from paper_2504_17954_b200.inverse import InverseFitter, init_transform  # noqa: E402
+from paper_2504_17954_b200.inverse import InverseFitter, InverseGraph, init_transform  # noqa: E402
 from paper_2504_17954_b200.synthetic import bench_camera, c2_scene  # noqa: E402
 
 sc = c2_scene()
@@ -15,10 +17,11 @@ p0 = init_transform(sc)
 fit0 = InverseFitter(sc, [], [])
 ref = fit0.render(p0, cam).out64.clone() * 0.95
 fit = InverseFitter(sc, [ref], [cam], ds=fit0.ds)
+G = InverseGraph(fit, p0, 1000)
 for _ in range(3):
-    fit.view_grads(p0, 0)
+    G.replay()
 torch.cuda.synchronize()
 torch.cuda.profiler.start()
-fit.view_grads(p0, 0)
+G.replay()
 torch.cuda.synchronize()
 torch.cuda.profiler.stop()

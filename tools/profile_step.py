@@ -1,5 +1,5 @@
 """Kernel-time breakdown (torch.profiler) of one C3 training step or one C4
-inverse iteration.  Usage: python tools/profile_step.py [train|inverse]"""
+inverse iteration.  Usage: python tools/profile_step.py [train|inverse|inverse_host]"""
 import os
 import sys
 
@@ -35,8 +35,12 @@ def main(which):
         ref = fit.render(p0, cam).out64.clone() * 0.95
         fit = InverseFitter(sc, [ref], [cam], ds=fit.ds)
 
-        def step():
-            fit.view_grads(p0, 0)
+        if which == "inverse_host":
+            def step():
+                fit.view_grads(p0, 0)
+        else:  # the product path: one InverseGraph replay per iteration
+            from paper_2504_17954_b200.inverse import InverseGraph
+            step = InverseGraph(fit, p0, 100_000).replay
     for _ in range(3):
         step()
     torch.cuda.synchronize()
