@@ -239,6 +239,24 @@ int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t
                   float *g_mean2d, float *g_conic, float *g_opacity,
                   const int32_t *tile_order, int32_t flags, ivr_stream_t stream);
 
+/* K4a, deterministic (debugging): identical results on every
+ * run.  Each (pair, warp) partial is stored, not atomically added, into
+ * `workspace` (ivr_blend_bwd_det_workspace_size bytes), then one thread per
+ * Gaussian sums them in the reference's pair order (its tile rectangle
+ * row-major; each entry found by binary search on K1's depth key and splat
+ * index) and warp order, in float64.  n, depth_key, count, rect: K1's outputs
+ * for the frame; g_* are overwritten (no zeroing needed). */
+size_t ivr_blend_bwd_det_workspace_size(int64_t pair_capacity, int32_t k);
+int ivr_blend_bwd_deterministic(const int32_t *tile_ranges, const int32_t *pair_splat,
+                                int32_t ntx, int32_t nty, const float *rec, const float *values,
+                                const double *rec64, int32_t k, int32_t width, int32_t height,
+                                const float *out, const int32_t *last_pos, const float *d_out,
+                                int64_t n, const uint64_t *depth_key, const int32_t *count,
+                                const uint16_t *rect, int64_t pair_capacity, void *workspace,
+                                size_t workspace_bytes, float *g_values, float *g_mean2d,
+                                float *g_conic, float *g_opacity, const int32_t *tile_order,
+                                int32_t flags, ivr_stream_t stream);
+
 /* Per-Gaussian backward outputs (float64, NULL = not wanted). */
 typedef struct ivr_grads {
     /* inputs: K4a accumulators (float32, NULL if none) and an optional extra

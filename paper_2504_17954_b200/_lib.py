@@ -143,6 +143,11 @@ _SIGS = {
                       ctypes.c_int),
     "ivr_tile_order": ([P, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_debug_blend_trace": ([P], None),
+    "ivr_blend_bwd_det_workspace_size": ([ctypes.c_int64, ctypes.c_int32], ctypes.c_size_t),
+    "ivr_blend_bwd_deterministic": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
+                                     ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int64, P, P,
+                                     P, ctypes.c_int64, P, ctypes.c_size_t, P, P, P, P, P,
+                                     ctypes.c_int32, P], ctypes.c_int),
     "ivr_blend_bwd": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
                        ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, P, ctypes.c_int32, P],
                       ctypes.c_int),

@@ -42,6 +42,9 @@ struct BwdArgs {
     float *g_values, *g_mean, *g_conic, *g_opac;
     int preculled;
     const int32_t *tile_order;
+    // deterministic mode: per-(pair, warp) partials in place of atomics,
+    // part[((j * 8 + warp) * (K + 6)) + slot], slot = value c | K + geometry
+    float *part;
 };
 
 __device__ __forceinline__ double exact_alpha_b(double dpx, double dpy, double mx, double my,
@@ -298,8 +301,14 @@ blend_bwd_kernel(BwdArgs A) {
                 const int s = W.sp[q];
                 const float tv = warp_transpose_sum<KMAX>(xv, lane);
                 const float tg = warp_transpose_sum<8>(xg, lane);
-                if (vbase && tv != 0.f) atomicAdd(vbase + (int64_t)K * s, tv);
-                if (gbase && tg != 0.f) atomicAdd(gbase + (int64_t)gstride * s, tg);
+                if (A.part) {  // deterministic mode: plain stores, reduced in fixed order later
+                    float *pp = A.part + ((int64_t)(base + q) * (kBwdThreads / 32) + warp) * (K + 6);
+                    if (lane < K && tv != 0.f) pp[lane] = tv;
+                    if (lane < 6 && tg != 0.f) pp[K + lane] = tg;
+                } else {
+                    if (vbase && tv != 0.f) atomicAdd(vbase + (int64_t)K * s, tv);
+                    if (gbase && tg != 0.f) atomicAdd(gbase + (int64_t)gstride * s, tg);
+                }
             }
         }
         __syncwarp();  // slots are rewritten by the next chunk
@@ -313,6 +322,50 @@ int launch_bwd(const BwdArgs &A, int ntiles, cudaStream_t st) {
     if (sm > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     fn<<<ntiles, kBwdThreads, sm, st>>>(A);
     return check_launch("blend_bwd_kernel");
+}
+
+// ----------------------------------------------------------------- deterministic K4a
+// Fixed-order reduction of the per-(pair, warp) partials: one thread per
+// Gaussian walks its tile rectangle row-major (the reference's pair order),
+// finds its entry in each tile list by binary search on (depth key, splat)
+// -- the order K2 produced -- and sums the 8 warp partials of that entry in
+// warp order, in float64.  Same result on every run.
+__global__ void __launch_bounds__(128)
+bwd_reduce_det_kernel(int64_t n, int K, const uint64_t *depth_key, const int32_t *count,
+                      const ushort4 *rect, const int32_t *ranges, const int32_t *pair_splat,
+                      int ntx, int64_t cap, const float *part, float *g_values, float *g_mean,
+                      float *g_conic, float *g_opac) {
+    const int64_t s = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (s >= n) return;
+    double acc[32 + 6];
+    for (int c = 0; c < K + 6; ++c) acc[c] = 0.0;
+    if (count[s] > 0) {
+        const ushort4 rc = rect[s];
+        const uint64_t key = depth_key[s];
+        for (int ty = rc.z; ty <= rc.w; ++ty)
+            for (int tx = rc.x; tx <= rc.y; ++tx) {
+                const int t = ty * ntx + tx;
+                int lo = ranges[t], hi = ranges[t + 1];
+                lo = lo < cap ? lo : (int)cap;
+                hi = hi < cap ? hi : (int)cap;
+                while (lo < hi) {  // first entry not below (key, s)
+                    const int mid = (lo + hi) >> 1;
+                    const uint32_t sp = (uint32_t)pair_splat[mid] & 0x7fffffffu;
+                    const uint64_t km = depth_key[sp];
+                    if (km < key || (km == key && (int64_t)sp < s)) lo = mid + 1;
+                    else hi = mid;
+                }
+                if (lo >= (int)cap || ((uint32_t)pair_splat[lo] & 0x7fffffffu) != (uint32_t)s) continue;
+                const float *pp = part + (int64_t)lo * (kBwdThreads / 32) * (K + 6);
+                for (int w = 0; w < kBwdThreads / 32; ++w)
+                    for (int c = 0; c < K + 6; ++c) acc[c] += (double)pp[w * (K + 6) + c];
+            }
+    }
+    for (int c = 0; c < K; ++c) g_values[s * K + c] = (float)acc[c];
+    g_mean[2 * s] = (float)acc[K];
+    g_mean[2 * s + 1] = (float)acc[K + 1];
+    for (int c = 0; c < 3; ++c) g_conic[3 * s + c] = (float)acc[K + 2 + c];
+    g_opac[s] = (float)acc[K + 5];
 }
 
 // ----------------------------------------------------------------- K4b helpers
@@ -643,12 +696,13 @@ ivr_frame_params params_from(const ivr_camera &cam, const ivr_shading *S, const 
 
 }  // namespace ivr
 
-extern "C" int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
-                             int32_t nty, const float *rec, const float *values,
-                             const double *rec64, int32_t k, int32_t width, int32_t height,
-                             const float *out, const int32_t *last_pos, const float *d_out,
-                             float *g_values, float *g_mean2d, float *g_conic, float *g_opacity,
-                             const int32_t *tile_order, int32_t flags, ivr_stream_t stream) {
+namespace {
+int blend_bwd_impl(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
+                   int32_t nty, const float *rec, const float *values, const double *rec64,
+                   int32_t k, int32_t width, int32_t height, const float *out,
+                   const int32_t *last_pos, const float *d_out, float *g_values, float *g_mean2d,
+                   float *g_conic, float *g_opacity, const int32_t *tile_order, int32_t flags,
+                   float *part, ivr_stream_t stream) {
     using namespace ivr;
     if (!tile_ranges || !pair_splat || !rec || !values || !out || !last_pos || !d_out ||
         !g_values || !g_mean2d || !g_conic || !g_opacity || k < 1 || k > 32 ||
@@ -675,6 +729,7 @@ extern "C" int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_spl
     A.g_opac = g_opacity;
     A.preculled = (flags & IVR_BLEND_PRECULLED) ? 1 : 0;
     A.tile_order = tile_order;
+    A.part = part;
     cudaStream_t st = (cudaStream_t)stream;
     const int nt = ntx * nty;
     const bool f64 = rec64 != nullptr;
@@ -684,6 +739,53 @@ extern "C" int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_spl
     if (k <= 16) { IVR_BWD(16); }
     IVR_BWD(32);
 #undef IVR_BWD
+}
+}  // namespace
+
+extern "C" int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
+                             int32_t nty, const float *rec, const float *values,
+                             const double *rec64, int32_t k, int32_t width, int32_t height,
+                             const float *out, const int32_t *last_pos, const float *d_out,
+                             float *g_values, float *g_mean2d, float *g_conic, float *g_opacity,
+                             const int32_t *tile_order, int32_t flags, ivr_stream_t stream) {
+    return blend_bwd_impl(tile_ranges, pair_splat, ntx, nty, rec, values, rec64, k, width, height,
+                          out, last_pos, d_out, g_values, g_mean2d, g_conic, g_opacity,
+                          tile_order, flags, nullptr, stream);
+}
+
+extern "C" size_t ivr_blend_bwd_det_workspace_size(int64_t pair_capacity, int32_t k) {
+    if (pair_capacity < 0 || k < 1 || k > 32) return 0;
+    return (size_t)pair_capacity * (ivr::kBwdThreads / 32) * (size_t)(k + 6) * sizeof(float);
+}
+
+extern "C" int ivr_blend_bwd_deterministic(
+    const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx, int32_t nty,
+    const float *rec, const float *values, const double *rec64, int32_t k, int32_t width,
+    int32_t height, const float *out, const int32_t *last_pos, const float *d_out,
+    int64_t n, const uint64_t *depth_key, const int32_t *count, const uint16_t *rect,
+    int64_t pair_capacity, void *workspace, size_t workspace_bytes, float *g_values,
+    float *g_mean2d, float *g_conic, float *g_opacity, const int32_t *tile_order, int32_t flags,
+    ivr_stream_t stream) {
+    using namespace ivr;
+    const size_t need = ivr_blend_bwd_det_workspace_size(pair_capacity, k);
+    if (n < 0 || !depth_key || !count || !rect || pair_capacity < 1 ||
+        pair_capacity > 0x7fffffffll || !workspace || workspace_bytes < need) {
+        set_error("ivr_blend_bwd_deterministic: bad argument or workspace too small");
+        return IVR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(workspace, 0, need, st) != cudaSuccess) {
+        set_error("ivr_blend_bwd_deterministic: memset failed");
+        return IVR_ERR_CUDA;
+    }
+    const int rc = blend_bwd_impl(tile_ranges, pair_splat, ntx, nty, rec, values, rec64, k, width,
+                                  height, out, last_pos, d_out, g_values, g_mean2d, g_conic,
+                                  g_opacity, tile_order, flags, (float *)workspace, stream);
+    if (rc != IVR_OK || n == 0) return rc;
+    bwd_reduce_det_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
+        n, k, depth_key, count, (const ushort4 *)rect, tile_ranges, pair_splat, ntx,
+        pair_capacity, (const float *)workspace, g_values, g_mean2d, g_conic, g_opacity);
+    return check_launch("bwd_reduce_det_kernel");
 }
 
 extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *shading,

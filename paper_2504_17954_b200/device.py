@@ -319,9 +319,12 @@ def blend(F: Frame, ws: Workspace, want_state=True, stream=None, out=None, exact
     return F
 
 
-def blend_backward(F: Frame, d_out, stream=None):
+def blend_backward(F: Frame, d_out, stream=None, deterministic=None):
     """K4a: per-Gaussian float32 accumulators from the upstream image gradient
-    d_out (H,W,K float32 device tensor)."""
+    d_out (H,W,K float32 device tensor).  deterministic (default: env
+    IVR_DETERMINISTIC=1): fixed-order reduction, identical on every run."""
+    if deterministic is None:
+        deterministic = os.environ.get("IVR_DETERMINISTIC", "0") == "1"
     n, K = F.n, F.K
     dev = F.depth_key.device
     arena = torch.zeros(n * (K + 6), dtype=torch.float32, device=dev)  # one memset
@@ -330,6 +333,18 @@ def blend_backward(F: Frame, d_out, stream=None):
     out = F.out if not F.f64 else F.out64.float()
     d_out = d_out.to(torch.float32).contiguous()
     cam = F.cam
+    if deterministic:
+        nb = int(L.lib().ivr_blend_bwd_det_workspace_size(F.capacity, K))
+        ws = torch.empty(max(nb, 8), dtype=torch.uint8, device=dev)
+        L.check(L.lib().ivr_blend_bwd_deterministic(
+            ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec), ptr(F.values),
+            ptr(F.rec64), K, cam.width, cam.height, ptr(out), ptr(F.last_pos), ptr(d_out), n,
+            ptr(F.depth_key), ptr(F.count), ptr(F.rect), F.capacity, ptr(ws), nb,
+            ptr(g["values"]), ptr(g["mean2d"]), ptr(g["conic"]), ptr(g["opacity"]),
+            ptr(getattr(F, "tile_order", None)),
+            L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0,
+            stream_handle(stream)), "ivr_blend_bwd_deterministic")
+        return g
     L.check(L.lib().ivr_blend_bwd(ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec),
                                   ptr(F.values), ptr(F.rec64), K, cam.width, cam.height, ptr(out),
                                   ptr(F.last_pos), ptr(d_out), ptr(g["values"]), ptr(g["mean2d"]),

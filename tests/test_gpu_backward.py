@@ -158,3 +158,51 @@ def test_finite_differences_small_scene():
             flat[i] = o
             fd = (lp - lm) / (2 * eps)
             assert abs(fd - gf[i]) <= 1e-3 * max(abs(fd), abs(gf[i]), 1e-2), (key, i, fd, gf[i])
+
+
+def test_deterministic_blend_backward(monkeypatch):
+    """IVR_DETERMINISTIC=1: fixed-order reduction gives
+    bit-identical gradients on every run, within float32 rounding of the
+    atomic path, and the reference gradients still match."""
+    from paper_2504_17954_b200 import GaussianGeometry, rasterize_backward, rasterize_forward
+    d = golden("backward_small")
+    geom = GaussianGeometry(d["mu"], d["q_raw"], d["log_s"], d["o_logit"], d["n_raw"])
+    w = {k: d["w_" + k] for k in ("color", "alpha", "depth", "normal", "ka")}
+
+    def grads():
+        out, st = rasterize_forward(geom, d["colors"], _cam(d),
+                                    channels=("color", "alpha", "depth", "normal"),
+                                    attrs={"ka": d["attr_ka"]}, dtype=np.float64)
+        return rasterize_backward(st, w)
+    g_atomic = grads()
+    monkeypatch.setenv("IVR_DETERMINISTIC", "1")
+    g1, g2 = grads(), grads()
+    for k in ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors", "d_mean2d"):
+        assert np.array_equal(g1[k], g2[k]), k
+        _close(g1[k], d[k], name=k)
+        _close(g1[k], g_atomic[k], rel=1e-5, name=k)
+    assert np.array_equal(g1["d_attrs"]["ka"], g2["d_attrs"]["ka"])
+
+
+def test_deterministic_training_step(monkeypatch):
+    """The stage-2 step under IVR_DETERMINISTIC=1 repeats bit for bit."""
+    import torch
+    from paper_2504_17954_b200 import LightConfig
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
+    from paper_2504_17954_b200.trainer import EditableTrainer, _stage2_init
+    monkeypatch.setenv("IVR_DETERMINISTIC", "1")
+    a = editable_arrays(0, 20_000, density=20_000)
+    light = LightConfig("orbital", 0.45, 0.9)
+    cam = bench_camera(96, 80, 0.3)
+    gt = EditableTrainer(a, a["palette"], light).render_rgba(cam).clone()
+    p = {k: a[k] for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw")}
+    p.update(_stage2_init(20_000))
+    outs = []
+    for _ in range(2):
+        tr = EditableTrainer(p, a["palette"], light)
+        loss, grads, stat = tr.step(cam, gt * 0.9)
+        torch.cuda.synchronize()
+        outs.append((float(loss), {k: v.cpu().numpy() for k, v in grads.items()}))
+    assert outs[0][0] == outs[1][0]
+    for k in outs[0][1]:
+        assert np.array_equal(outs[0][1][k], outs[1][1][k]), k
