@@ -204,6 +204,8 @@ int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int32_t *count
  * certified decisions (same contributors, values within ~1e-6). */
 #define IVR_BLEND_EXACT 1     /* flags: every non-skipped pair in reference float64 */
 #define IVR_BLEND_PRECULLED 2 /* flags: pair_splat carries ivr_bin_sort_cull's bit 31 */
+#define IVR_BLEND_NO_GEOMETRY 4 /* ivr_blend_bwd flags: only g_values / g_opacity (transform
+                                 * fits); g_mean2d / g_conic may be NULL */
 int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_splat,
                   int32_t ntx, int32_t nty, const float *rec, const float *values,
                   const double *rec64, const double *values64, int32_t k,
@@ -231,7 +233,8 @@ int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_t *order,
  * g_values (n,k), g_mean2d (n,2), g_conic (n,3), g_opacity (n).
  * out = K3's float32 output (H,W,k); d_out (H,W,k) float32 upstream gradient.
  * rec64 selects dtype=float64 decisions.  tile_order (nullable): CTA -> tile
- * schedule (ivr_tile_order, heaviest first).  flags: IVR_BLEND_PRECULLED. */
+ * schedule (ivr_tile_order, heaviest first).  flags: IVR_BLEND_PRECULLED,
+ * IVR_BLEND_NO_GEOMETRY. */
 int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
                   int32_t nty, const float *rec, const float *values, const double *rec64,
                   int32_t k, int32_t width, int32_t height, const float *out,

@@ -20,6 +20,7 @@ P = ctypes.c_void_p
 MAX_ATTRS = 8
 BLEND_EXACT = 1
 BLEND_PRECULLED = 2
+BLEND_NO_GEOMETRY = 4
 
 IVR_OK, IVR_ERR_ARG, IVR_ERR_SHAPE, IVR_ERR_NONFINITE, IVR_ERR_CORRUPT_INDEX, IVR_ERR_CUDA, \
     IVR_ERR_CAPACITY = 0, -1, -2, -3, -4, -5, -6

@@ -116,7 +116,7 @@ constexpr int kBwdWarpW = 8;  // warp footprint 8x4 pixels (as K3)
 // One CTA per tile, each warp an independent 8x4 block of pixels walking
 // the tile list in 32-pair chunks up to the largest last_pos of its pixels
 // (same strip cull and prefetch as K3; no CTA barrier).
-template <int KMAX, bool F64>
+template <int KMAX, bool F64, bool GEOM>
 __global__ void __launch_bounds__(kBwdThreads, KMAX <= 16 ? 3 : 1)
 blend_bwd_kernel(BwdArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
@@ -155,7 +155,12 @@ blend_bwd_kernel(BwdArgs A) {
     float *vbase = lane < K ? A.g_values + lane : nullptr;
     float *gbase = nullptr;
     int gstride = 0;
-    if (lane < 2) {
+    if (!GEOM) {  // opacity only (transform fits): lane 0 adds the warp sum
+        if (lane == 0) {
+            gbase = A.g_opac;
+            gstride = 1;
+        }
+    } else if (lane < 2) {
         gbase = A.g_mean + lane;
         gstride = 2;
     } else if (lane < 5) {
@@ -283,13 +288,15 @@ blend_bwd_kernel(BwdArgs A) {
                 S_A = fmaf(w, Dv, S_A);  // dout . A after this contributor
                 const float d_alpha = T * Dv - (S_C - S_A) * inv;
                 if (alu < 0.99f) {
-                    const float d_sigma = -alu * d_alpha;
-                    const float ca = 2.0f * a1.x, cb = a1.y, cc = 2.0f * a1.z;
-                    xg[0] = -d_sigma * (ca * dx + cb * dy);
-                    xg[1] = -d_sigma * (cb * dx + cc * dy);
-                    xg[2] = 0.5f * dx * dx * d_sigma;
-                    xg[3] = dx * dy * d_sigma;
-                    xg[4] = 0.5f * dy * dy * d_sigma;
+                    if (GEOM) {
+                        const float d_sigma = -alu * d_alpha;
+                        const float ca = 2.0f * a1.x, cb = a1.y, cc = 2.0f * a1.z;
+                        xg[0] = -d_sigma * (ca * dx + cb * dy);
+                        xg[1] = -d_sigma * (cb * dx + cc * dy);
+                        xg[2] = 0.5f * dx * dx * d_sigma;
+                        xg[3] = dx * dy * d_sigma;
+                        xg[4] = 0.5f * dy * dy * d_sigma;
+                    }
                     xg[5] = g * d_alpha;
                 }
                 T = T * (1.0f - al);
@@ -300,11 +307,13 @@ blend_bwd_kernel(BwdArgs A) {
                 // l % 8; parallel atomics
                 const int s = W.sp[q];
                 const float tv = warp_transpose_sum<KMAX>(xv, lane);
-                const float tg = warp_transpose_sum<8>(xg, lane);
+                const float tg = GEOM ? warp_transpose_sum<8>(xg, lane) : warp_sum(xg[5]);
                 if (A.part) {  // deterministic mode: plain stores, reduced in fixed order later
                     float *pp = A.part + ((int64_t)(base + q) * (kBwdThreads / 32) + warp) * (K + 6);
                     if (lane < K && tv != 0.f) pp[lane] = tv;
-                    if (lane < 6 && tg != 0.f) pp[K + lane] = tg;
+                    if (GEOM ? (lane < 6) : (lane == 0)) {
+                        if (tg != 0.f) pp[K + (GEOM ? lane : 5)] = tg;
+                    }
                 } else {
                     if (vbase && tv != 0.f) atomicAdd(vbase + (int64_t)K * s, tv);
                     if (gbase && tg != 0.f) atomicAdd(gbase + (int64_t)gstride * s, tg);
@@ -316,9 +325,9 @@ blend_bwd_kernel(BwdArgs A) {
 }
 
 template <int KMAX, bool F64>
-int launch_bwd(const BwdArgs &A, int ntiles, cudaStream_t st) {
+int launch_bwd(const BwdArgs &A, int ntiles, bool geom, cudaStream_t st) {
     const size_t sm = (kBwdThreads / 32) * sizeof(BwdSlots<KMAX, F64>);
-    auto fn = blend_bwd_kernel<KMAX, F64>;
+    auto fn = geom ? blend_bwd_kernel<KMAX, F64, true> : blend_bwd_kernel<KMAX, F64, false>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     fn<<<ntiles, kBwdThreads, sm, st>>>(A);
     return check_launch("blend_bwd_kernel");
@@ -362,9 +371,12 @@ bwd_reduce_det_kernel(int64_t n, int K, const uint64_t *depth_key, const int32_t
             }
     }
     for (int c = 0; c < K; ++c) g_values[s * K + c] = (float)acc[c];
-    g_mean[2 * s] = (float)acc[K];
-    g_mean[2 * s + 1] = (float)acc[K + 1];
-    for (int c = 0; c < 3; ++c) g_conic[3 * s + c] = (float)acc[K + 2 + c];
+    if (g_mean) {
+        g_mean[2 * s] = (float)acc[K];
+        g_mean[2 * s + 1] = (float)acc[K + 1];
+    }
+    if (g_conic)
+        for (int c = 0; c < 3; ++c) g_conic[3 * s + c] = (float)acc[K + 2 + c];
     g_opac[s] = (float)acc[K + 5];
 }
 
@@ -705,7 +717,8 @@ int blend_bwd_impl(const int32_t *tile_ranges, const int32_t *pair_splat, int32_
                    float *part, ivr_stream_t stream) {
     using namespace ivr;
     if (!tile_ranges || !pair_splat || !rec || !values || !out || !last_pos || !d_out ||
-        !g_values || !g_mean2d || !g_conic || !g_opacity || k < 1 || k > 32 ||
+        !g_values || !g_opacity || k < 1 || k > 32 ||
+        (!(flags & IVR_BLEND_NO_GEOMETRY) && (!g_mean2d || !g_conic)) ||
         ntx != (width + kTile - 1) / kTile || nty != (height + kTile - 1) / kTile) {
         set_error("ivr_blend_bwd: bad argument");
         return IVR_ERR_ARG;
@@ -733,7 +746,8 @@ int blend_bwd_impl(const int32_t *tile_ranges, const int32_t *pair_splat, int32_
     cudaStream_t st = (cudaStream_t)stream;
     const int nt = ntx * nty;
     const bool f64 = rec64 != nullptr;
-#define IVR_BWD(KM) return f64 ? launch_bwd<KM, true>(A, nt, st) : launch_bwd<KM, false>(A, nt, st)
+    const bool geom = (flags & IVR_BLEND_NO_GEOMETRY) == 0;
+#define IVR_BWD(KM) return f64 ? launch_bwd<KM, true>(A, nt, geom, st) : launch_bwd<KM, false>(A, nt, geom, st)
     if (k <= 4) { IVR_BWD(4); }
     if (k <= 8) { IVR_BWD(8); }
     if (k <= 16) { IVR_BWD(16); }

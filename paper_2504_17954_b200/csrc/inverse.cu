@@ -61,7 +61,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(ivr_inverse_step A) {
     const int S = A.n_scenes, N = 4 * S + 10;
     const int tid = threadIdx.x;
     __shared__ double s_g[4 * kMaxScenes + 10];
-    __shared__ double s_max[5][kThreads];
+    __shared__ double s_max[5][kThreads / 32];
     __shared__ double s_bc[5][2];  // per group: 1 - beta^t (0 = group not stepped)
     __shared__ int s_gate, s_rescale;
     const double nv = (double)A.n_views;
@@ -76,7 +76,15 @@ __global__ void __launch_bounds__(kThreads) update_kernel(ivr_inverse_step A) {
         const int q = group(j);
         mx[q] = fabs(gj) > mx[q] ? fabs(gj) : mx[q];
     }
-    for (int q = 0; q < 5; ++q) s_max[q][tid] = mx[q];
+    for (int q = 0; q < 5; ++q) {  // per-warp max, then 4 entries per group below
+        double m = mx[q];
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            const double y = __shfl_xor_sync(0xffffffffu, m, o);
+            m = y > m ? y : m;
+        }
+        if ((tid & 31) == 0) s_max[q][tid >> 5] = m;
+    }
     if (tid == 0) s_rescale = 0;
     __syncthreads();
     if (tid == 0) {
@@ -94,7 +102,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(ivr_inverse_step A) {
         if (it < A.iters) A.losses[it] = loss;
         for (int q = 0; q < 5; ++q) {
             double gm = 0.0;
-            for (int k = 0; k < kThreads; ++k) gm = s_max[q][k] > gm ? s_max[q][k] : gm;
+            for (int k = 0; k < kThreads / 32; ++k) gm = s_max[q][k] > gm ? s_max[q][k] : gm;
             s_bc[q][0] = s_bc[q][1] = 0.0;
             const bool learn = (A.learnable & (1 << q)) && (q != 4 || A.orbital);
             if (gate || !learn || !(gm > 1e-12)) continue;

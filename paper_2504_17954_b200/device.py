@@ -319,10 +319,12 @@ def blend(F: Frame, ws: Workspace, want_state=True, stream=None, out=None, exact
     return F
 
 
-def blend_backward(F: Frame, d_out, stream=None, deterministic=None):
+def blend_backward(F: Frame, d_out, stream=None, deterministic=None, geometry=True):
     """K4a: per-Gaussian float32 accumulators from the upstream image gradient
     d_out (H,W,K float32 device tensor).  deterministic (default: env
-    IVR_DETERMINISTIC=1): fixed-order reduction, identical on every run."""
+    IVR_DETERMINISTIC=1): fixed-order reduction, identical on every run.
+    geometry=False: only the value and opacity accumulators (transform fits;
+    mean2d / conic stay zero)."""
     if deterministic is None:
         deterministic = os.environ.get("IVR_DETERMINISTIC", "0") == "1"
     n, K = F.n, F.K
@@ -342,7 +344,8 @@ def blend_backward(F: Frame, d_out, stream=None, deterministic=None):
             ptr(F.depth_key), ptr(F.count), ptr(F.rect), F.capacity, ptr(ws), nb,
             ptr(g["values"]), ptr(g["mean2d"]), ptr(g["conic"]), ptr(g["opacity"]),
             ptr(getattr(F, "tile_order", None)),
-            L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0,
+            (L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0) |
+            (0 if geometry else L.BLEND_NO_GEOMETRY),
             stream_handle(stream)), "ivr_blend_bwd_deterministic")
         return g
     L.check(L.lib().ivr_blend_bwd(ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec),
@@ -350,7 +353,8 @@ def blend_backward(F: Frame, d_out, stream=None, deterministic=None):
                                   ptr(F.last_pos), ptr(d_out), ptr(g["values"]), ptr(g["mean2d"]),
                                   ptr(g["conic"]), ptr(g["opacity"]),
                                   ptr(getattr(F, "tile_order", None)),
-                                  L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0,
+                                  (L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0) |
+                                  (0 if geometry else L.BLEND_NO_GEOMETRY),
                                   stream_handle(stream)), "ivr_blend_bwd")
     return g
 

@@ -155,7 +155,7 @@ class InverseFitter:
         F = self.render(params, cam, want_state=True)
         rgba = F.out64 if F.f64 else F.out.double()
         loss, d = photometric_loss_t(rgba, ref)
-        g = D.blend_backward(F, d)
+        g = D.blend_backward(F, d, geometry=False)
         shading, edits = F._keep_tabs
         light = _light(self.scene, params)
         out, _ = D.preprocess_backward(self.ds.dg, cam, 4, (0, 3, -1, -1), g=g, shading=shading,
@@ -299,7 +299,7 @@ class InverseGraph:
             h, w, nc = F.out64.shape
             win = 11
             sums, d = _photometric_dev(F.out64, fit.refs[v], 0.8 / F.out64.numel(), -0.2, True)
-            g = D.blend_backward(F, d)
+            g = D.blend_backward(F, d, geometry=False)
             out, _ = D.preprocess_backward(ds.dg, cam, 4, (0, 3, -1, -1), g=g, shading=self.shading,
                                            edits=self.edits, params_dev=pdev, geometry=False,
                                            want=("d_c_p", "d_scale"), per_scene=self.S,
