@@ -244,20 +244,23 @@ def bench_train(scene, dist=None, world=1, rank=0):
     p.update(_stage2_init(300_000))
     tr = EditableTrainer(p, a["palette"], light)
     it = [0]
+    # the product path: the whole step (fwd, losses, bwd, Adam) as one CUDA graph
+    from paper_2504_17954_b200.trainer import StepGraph
+    G = StepGraph(tr, cams[0], gts[0])
 
     def step():
         v = it[0] % len(cams)
         it[0] += 1
-        loss, grads, _ = tr.step(cams[v], gts[v])
-        tr.apply(grads, it[0], 10000)
+        G.step(cams[v], gts[v], it[0], 10000)
     mean_ms, med_ms = _device_time(step, 10)
+    G.flush()
     mean_ms = _max_over_ranks(mean_ms, dist)
     return {"metric": "stage-2 train it/s (300k Gaussians, 800x800, K=15, 1 view/it)",
             "value": world * 1000.0 / mean_ms, "unit": "it/s", "ms_per_it": mean_ms,
             "ms_per_it_median": med_ms, "n_gaussians": 300_000, "n_gpus": world,
             "scaling": "weak (one basic TF per GPU)",
-            "note": "includes fwd (K1-K3), L1+SSIM + normal/offset/bilateral/opacity terms, "
-                    "K4a+K4b, Adam; densify excluded"}
+            "note": "StepGraph replay: fwd (K1-K3), L1+SSIM + normal/offset/bilateral/opacity "
+                    "terms, K4a+K4b, gradient assembly, Adam; densify excluded"}
 
 
 def bench_inverse(scene, dist=None, world=1, rank=0):

@@ -176,7 +176,8 @@ int ivr_shade_fwd(const ivr_gaussians *g, const ivr_shading *shading,
  * np.lexsort((depth[pair_splat], pair_tile)) (rasterizer.py:129) and
  * np.searchsorted tile ranges (rasterizer.py:132), bit-exactly.
  * Writes n_pairs[0] (device) = P; if P > pair_capacity nothing past the
- * capacity is written and the caller must retry with a larger buffer. */
+ * capacity is written, tile_ranges are clamped to the capacity (so K3/K4 stay
+ * in bounds) and the caller must retry with a larger buffer. */
 size_t ivr_bin_sort_workspace_size(int64_t n, int64_t pair_capacity, int32_t ntiles);
 int ivr_bin_sort(int64_t n, const uint64_t *depth_key, const int32_t *count,
                  const uint16_t *rect, int32_t ntx, int32_t nty,
@@ -418,6 +419,13 @@ typedef struct ivr_adam_group {
 } ivr_adam_group;
 int ivr_adam_step(const ivr_adam_group *groups, int32_t n_groups, double beta1, double beta2,
                   double eps, ivr_stream_t stream);
+/* ivr_adam_step for CUDA-graph replay: each group's (lr, bc1, bc2) is read
+ * from sched (device, 3 doubles per group, refreshed before every replay)
+ * instead of the struct, and a nonzero *skip (device, nullable) makes the
+ * step a no-op (a gated step, e.g. one whose pair list overflowed). */
+int ivr_adam_step_sched(const ivr_adam_group *groups, int32_t n_groups, double beta1,
+                        double beta2, double eps, const double *sched, const int32_t *skip,
+                        ivr_stream_t stream);
 
 /* ---- training-step plumbing (csrc/trainstep.cu) ---- */
 

@@ -188,6 +188,8 @@ _SIGS = {
                        ctypes.c_int),
     "ivr_adam_step": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
                        ctypes.c_double, ctypes.c_double, P], ctypes.c_int),
+    "ivr_adam_step_sched": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
+                             ctypes.c_double, ctypes.c_double, P, P, P], ctypes.c_int),
     "ivr_stage2_attrs": ([ctypes.c_int64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
     "ivr_step_partials": ([ctypes.c_int64], ctypes.c_int32),
     "ivr_inverse_pack": ([ctypes.POINTER(InverseStep_t), P, ctypes.c_double, ctypes.c_double, P, P,

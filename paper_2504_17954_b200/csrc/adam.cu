@@ -18,10 +18,18 @@ struct AdamGroups {
     ivr_adam_group g[kAdamMaxGroups];
     int n;
     double b1, b2, eps;
+    const double *sched;  // device [lr, bc1, bc2] per group (graph replay), or null
+    const int32_t *skip;  // device flag: nonzero = no update (gated step), or null
 };
 
 __global__ void __launch_bounds__(256) adam_kernel(AdamGroups A) {
-    const ivr_adam_group G = A.g[blockIdx.y];
+    if (A.skip && *A.skip) return;
+    ivr_adam_group G = A.g[blockIdx.y];
+    if (A.sched) {
+        G.lr = A.sched[3 * blockIdx.y];
+        G.bc1 = A.sched[3 * blockIdx.y + 1];
+        G.bc2 = A.sched[3 * blockIdx.y + 2];
+    }
     const double b1 = A.b1, b2 = A.b2, c1 = 1.0 - A.b1, c2 = 1.0 - A.b2;
     // m / bc as m * (1 / bc): within 1 ulp of the reference's division, and
     // two IEEE divides fewer per element (the kernel is FP64-issue bound)
@@ -40,8 +48,9 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamGroups A) {
 
 }  // namespace ivr
 
-extern "C" int ivr_adam_step(const ivr_adam_group *groups, int32_t n_groups, double beta1,
-                             double beta2, double eps, ivr_stream_t stream) {
+namespace {
+int adam_impl(const ivr_adam_group *groups, int32_t n_groups, double beta1, double beta2,
+              double eps, const double *sched, const int32_t *skip, ivr_stream_t stream) {
     using namespace ivr;
     if (!groups || n_groups < 0 || n_groups > kAdamMaxGroups) {
         set_error("ivr_adam_step: bad argument (at most 16 groups)");
@@ -51,8 +60,8 @@ extern "C" int ivr_adam_step(const ivr_adam_group *groups, int32_t n_groups, dou
     int64_t nmax = 0;
     for (int k = 0; k < n_groups; ++k) {
         const ivr_adam_group &g = groups[k];
-        if (g.n < 0 || (g.n > 0 && (!g.param || !g.m || !g.v || !g.grad)) || !(g.bc1 > 0.0) ||
-            !(g.bc2 > 0.0)) {
+        if (g.n < 0 || (g.n > 0 && (!g.param || !g.m || !g.v || !g.grad)) ||
+            (!sched && (!(g.bc1 > 0.0) || !(g.bc2 > 0.0)))) {
             set_error("ivr_adam_step: bad group");
             return IVR_ERR_ARG;
         }
@@ -63,9 +72,27 @@ extern "C" int ivr_adam_step(const ivr_adam_group *groups, int32_t n_groups, dou
     A.b1 = beta1;
     A.b2 = beta2;
     A.eps = eps;
+    A.sched = sched;
+    A.skip = skip;
     if (n_groups == 0 || nmax == 0) return IVR_OK;
     int64_t bx = (nmax + 255) / 256;
     if (bx > 148 * 8) bx = 148 * 8;
     adam_kernel<<<dim3((unsigned)bx, (unsigned)n_groups), 256, 0, (cudaStream_t)stream>>>(A);
     return check_launch("adam_kernel");
+}
+}  // namespace
+
+extern "C" int ivr_adam_step(const ivr_adam_group *groups, int32_t n_groups, double beta1,
+                             double beta2, double eps, ivr_stream_t stream) {
+    return adam_impl(groups, n_groups, beta1, beta2, eps, nullptr, nullptr, stream);
+}
+
+extern "C" int ivr_adam_step_sched(const ivr_adam_group *groups, int32_t n_groups, double beta1,
+                                   double beta2, double eps, const double *sched,
+                                   const int32_t *skip, ivr_stream_t stream) {
+    if (!sched) {
+        ivr::set_error("ivr_adam_step_sched: sched is required");
+        return IVR_ERR_ARG;
+    }
+    return adam_impl(groups, n_groups, beta1, beta2, eps, sched, skip, stream);
 }

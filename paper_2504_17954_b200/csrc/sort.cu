@@ -582,7 +582,7 @@ pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
 
 // tile_ranges = exclusive scan of tile totals (single block)
 __global__ void __launch_bounds__(1024)
-tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges) {
+tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges, uint32_t cap) {
     __shared__ uint32_t s_warp[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     uint32_t carry = 0;
@@ -606,11 +606,13 @@ tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges) {
         }
         __syncthreads();
         const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0);
-        if (i < ntiles) ranges[i] = (int32_t)(carry + incl - v);
+        // clamped to the pair capacity: an overflowed frame (n_pairs > capacity,
+        // detected by the caller) never makes K3/K4 read past pair_splat
+        if (i < ntiles) ranges[i] = (int32_t)min(carry + incl - v, cap);
         carry += s_warp[31];
         __syncthreads();
     }
-    if (threadIdx.x == 0) ranges[ntiles] = (int32_t)carry;
+    if (threadIdx.x == 0) ranges[ntiles] = (int32_t)min(carry, cap);
 }
 
 // stable placement: warp w of block b owns ranks [b*2048 + w*256, +256).
@@ -851,7 +853,7 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
             phist, ntiles, nbp, ttot, nullptr);
     else
         rowscan_kernel<<<ntiles, 1024, 0, st>>>(phist, nbp, ttot, nullptr);
-    tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges);
+    tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges, (uint32_t)pair_capacity);
     pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, nbp, tile_ranges, pair_splat,
                                                        width, height);
     return ivr::check_launch("ivr_bin_sort");

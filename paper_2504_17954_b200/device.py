@@ -426,12 +426,21 @@ def raise_if_bad(bad, n, order):
 
 
 def rasterize_device(dg, cam, K, cols, ws, shading=None, edits=None, colors=None, attrs=(),
-                     f64=False, want_state=True, debug=False, stream=None, exact=True):
+                     f64=False, want_state=True, debug=False, stream=None, exact=True,
+                     params_dev=None, capacity=None):
     """K1 + K2 + K3 with pair-capacity overflow handling (synchronizes once to
-    read the pair count)."""
-    F = preprocess(dg, cam, K, cols, ws, shading, edits, colors, attrs, f64, debug, stream)
+    read the pair count).  With ``capacity`` (CUDA-graph capture) there is no
+    host synchronisation: the caller checks ``F.n_pairs`` against it later;
+    ``params_dev`` takes the camera / light from device memory."""
+    F = preprocess(dg, cam, K, cols, ws, shading, edits, colors, attrs, f64, debug, stream,
+                   params_dev=params_dev)
     if dg.n == 0:
         F.empty = True
+        return F
+    if capacity is not None:
+        bin_sort(F, ws, stream, capacity=capacity)
+        F.P, F.empty = None, False
+        blend(F, ws, want_state, stream, exact=exact)
         return F
     bin_sort(F, ws, stream)
     P = int(F.n_pairs.item())

@@ -25,6 +25,7 @@ from __future__ import annotations
 import ctypes
 import json
 import math
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -122,6 +123,38 @@ class DeviceAdam:
                                       D.stream_handle()), "ivr_adam_step")
         del keep
 
+    def groups(self, items):
+        """ivr_adam_group array for (name, param, grad) items (state created
+        on first use); the pointers stay valid while the tensors live."""
+        arr = (L.AdamGroup_t * len(items))()
+        for k, (name, param, grad) in enumerate(items):
+            st = self.state.get(name)
+            if st is None:
+                st = self.state[name] = {"m": torch.zeros_like(param), "v": torch.zeros_like(param),
+                                         "t": 0}
+            if not (param.is_contiguous() and grad.is_contiguous() and grad.dtype == torch.float64):
+                raise ValueError(f"parameter {name}: contiguous float64 param and gradient required")
+            a = arr[k]
+            a.param, a.m, a.v, a.grad = (param.data_ptr(), st["m"].data_ptr(), st["v"].data_ptr(),
+                                         grad.data_ptr())
+            a.n = param.numel()
+        return arr
+
+    def ensure(self, named_params):
+        for name, param in named_params:
+            if name not in self.state:
+                self.state[name] = {"m": torch.zeros_like(param), "v": torch.zeros_like(param),
+                                    "t": 0}
+
+    def schedule(self, names_lrs):
+        """Advance each group's step count; returns [lr, bc1, bc2] per group."""
+        out = []
+        for name, lr in names_lrs:
+            st = self.state[name]
+            st["t"] += 1
+            out += [float(lr), 1.0 - self.b1 ** st["t"], 1.0 - self.b2 ** st["t"]]
+        return out
+
     def remap(self, parents, is_new):
         for st in self.state.values():
             for key in ("m", "v"):
@@ -164,18 +197,21 @@ class _StageTrainer:
     def n(self):
         return int(self.p["mu"].shape[0])
 
-    def apply(self, grads, it, iters, decay_extra=()):
-        """Adam on every group with the reference schedules (trainer.py:491-499)."""
+    def lr(self, name, it, iters, decay_extra=()):
+        """The reference's per-group learning-rate schedule (trainer.py:491-499)."""
         cfg = self.cfg
         frac = it / max(iters, 1)
-        items = []
-        for name, grad in grads.items():
-            lr = getattr(cfg, _LR[name])
-            if name == "mu" and cfg.lr_mu > 0.0:
-                lr = cfg.lr_mu * (cfg.lr_mu_final / cfg.lr_mu) ** frac
-            elif _LR[name] in ("lr_shading", "lr_normal") or name in decay_extra:
-                lr = lr * cfg.lr_decay_floor ** frac
-            items.append((name, self.p[name], grad, lr))
+        lr = getattr(cfg, _LR[name])
+        if name == "mu" and cfg.lr_mu > 0.0:
+            lr = cfg.lr_mu * (cfg.lr_mu_final / cfg.lr_mu) ** frac
+        elif _LR[name] in ("lr_shading", "lr_normal") or name in decay_extra:
+            lr = lr * cfg.lr_decay_floor ** frac
+        return lr
+
+    def apply(self, grads, it, iters, decay_extra=()):
+        """Adam on every group with the reference schedules (trainer.py:491-499)."""
+        items = [(name, self.p[name], grad, self.lr(name, it, iters, decay_extra))
+                 for name, grad in grads.items()]
         self.adam.step_all(items)
 
     @torch.no_grad()
@@ -243,7 +279,7 @@ class _StageTrainer:
         self._cam_ev.record()
         return self._cam_dev
 
-    def _map_terms(self, F, cam, gt, weights, offset=False, bilateral=False):
+    def _map_terms(self, F, cam, gt, weights, offset=False, bilateral=False, cam_dev=None):
         """Photometric L1+SSIM (K7) and the map regularizers (fused kernel):
         returns (loss terms for ivr_loss_finalize, tensors they point to,
         d_out float32 (H,W,K), column map).  No host synchronisation."""
@@ -270,7 +306,8 @@ class _StageTrainer:
         cols = (c["color"], c["alpha"], c.get("depth", -1), c.get("normal", -1),
                 c.get("delta_c", -1))
         terms, d_out = regularize_t(F.out, cols, gt=gt, d_rgba=d_rgba,
-                                    cam_params=self._cam_params(cam) if wn > 0.0 else None,
+                                    cam_params=(cam_dev if cam_dev is not None else
+                                                self._cam_params(cam)) if wn > 0.0 else None,
                                     w_normal=wn, w_offset=wo, w_bil=wb, bil_cols=bil)
         lt = L.LossTerms_t()
         lt.photo_sums = sums.data_ptr()
@@ -404,7 +441,7 @@ class EditableTrainer(_StageTrainer):
         return D.DeviceGaussians({k: self.p[k] for k in GEOM}, {k: self.p[k] for k in SHADE},
                                  None, self.dev)
 
-    def forward(self, cam, want_state=True, dg=None):
+    def forward(self, cam, want_state=True, dg=None, graph=None):
         dg = dg or self._dg()
         S = D.shading_struct(dg, self.palette, False, self.light)
         p = self.p
@@ -420,21 +457,28 @@ class EditableTrainer(_StageTrainer):
                  "beta": buf[3]}
         attrs_dev = [(attrs[name].reshape(self.n, w).contiguous(), c, w)
                      for name, c, w in self.attr_cols]
-        F = D.rasterize_device(dg, cam, self.K, self.cols, self.ws, shading=S, attrs=attrs_dev,
-                               f64=False, want_state=want_state, exact=False)
+        F = D.rasterize_device(dg, cam, self.K, self.cols, graph.ws if graph else self.ws,
+                               shading=S, attrs=attrs_dev, f64=False, want_state=want_state,
+                               exact=False, params_dev=graph.params_dev if graph else None,
+                               capacity=graph.capacity if graph else None)
         return F, S, attrs, dg
 
-    def step(self, cam, gt, weights=None):
+    def step(self, cam, gt, weights=None, graph=None):
         """One _stage2_step (trainer.py:397-444): (loss, grads, densify stat),
-        all device tensors."""
+        all device tensors.  ``graph``: the StepGraph being captured (camera
+        and pseudo-normal block from its device buffers, no host sync)."""
         weights = weights or self.cfg.weights
-        F, S, attrs, dg = self.forward(cam)
-        lt, keep, d_out, c = self._map_terms(F, cam, gt, weights, offset=True, bilateral=True)
+        F, S, attrs, dg = self.forward(cam, graph=graph)
+        lt, keep, d_out, c = self._map_terms(F, cam, gt, weights, offset=True, bilateral=True,
+                                             cam_dev=graph.cam_dev if graph else None)
         g = D.blend_backward(F, d_out)
         want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_mean2d", "d_values",
                 "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta")
         gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, shading=S, geometry=True,
-                                        want=want, light=self.light)
+                                        want=want, light=self.light,
+                                        params_dev=graph.params_dev if graph else None)
+        if graph is not None:
+            graph.n_pairs = F.n_pairs
         n = self.n
         stat, part = self._assemble(gr, c, weights, shading=True)
         loss = self._finalize(lt, part, weights.opacity_l1)
@@ -537,6 +581,172 @@ def _project_px(points, cam):
     return np.nonzero(ok)[0], px, py
 
 
+class StepGraph:
+    """One stage-2 training step -- K1-K3, L1+SSIM, map regularizers, K4a/K4b,
+    gradient assembly, loss, Adam on every group -- captured once as a CUDA
+    graph for the trainer's current Gaussian count (recapture after densify).
+
+    Per step the host writes the view's ``ivr_frame_params``, its
+    pseudo-normal camera block and the Adam schedule (lr, bias corrections)
+    into a pinned ring slot, copies them and the view's ground truth into the
+    graph's fixed device buffers, and replays: one launch instead of ~43 and
+    no host synchronisation.  The pair capacity learned at capture (+30%) is
+    verified when a step retires (its pair count is copied back
+    asynchronously); an overflowed step and every later one are gated on the
+    device (Adam and the densify statistic skip them), and the host then
+    recaptures with a larger capacity and replays the gated steps in order,
+    so the update sequence is exactly the eager one."""
+
+    RING = 4
+
+    def __init__(self, tr, cam, gt, weights=None, decay_extra=(), headroom=1.3):
+        if not isinstance(tr, EditableTrainer):
+            raise OutOfRange("StepGraph captures the stage-2 (EditableTrainer) step")
+        self.tr, self.weights, self.decay_extra = tr, weights or tr.cfg.weights, decay_extra
+        self.headroom = headroom
+        dev = tr.dev
+        self.W, self.H = int(cam.width), int(cam.height)
+        self.nb = ctypes.sizeof(L.FrameParams_t)
+        self.names = list(tr.p.keys())
+        G = len(self.names)
+        # own workspace: eager renders between replays (holdout logging) must
+        # never reallocate a buffer the graph captured
+        self.ws = D.Workspace(dev)
+        self.params_dev = torch.empty(self.nb, dtype=torch.uint8, device=dev)
+        self.cam_dev = torch.empty(12, dtype=torch.float64, device=dev)
+        self.sched_dev = torch.empty(3 * G, dtype=torch.float64, device=dev)
+        self.gt_dev = torch.empty((self.H, self.W, 4), dtype=torch.float64, device=dev)
+        self.gate = torch.zeros(1, dtype=torch.int32, device=dev)
+        self.stat_sum = torch.zeros(tr.n, dtype=torch.float64, device=dev)
+        slot_bytes = self.nb + 12 * 8 + 3 * G * 8
+        self._pin = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True)
+                     for _ in range(self.RING)]
+        self._np = [torch.zeros(1, dtype=torch.int32, pin_memory=True) for _ in range(self.RING)]
+        self._pending = []  # (slot, event, it, iters, cam, gt, t-before per group)
+        self._k = 0
+        # pair capacity from one synchronising forward of this view
+        F, _, _, _ = tr.forward(cam, want_state=False)
+        self.capacity = max(int(int(F.n_pairs.item()) * headroom) + 4096, tr.ws.pair_capacity)
+        self._capture(cam, gt)
+
+    # -- staging -------------------------------------------------------------
+    def _stage(self, cam, gt, it, iters):
+        k = self._k
+        self._k = (k + 1) % self.RING
+        while any(p[0] == k for p in self._pending):  # reuse a slot once its step retired
+            self._retire_oldest()
+        tr = self.tr
+        h = self._pin[k].numpy()
+        P = D.frame_params(cam, tr.light)
+        ctypes.memmove(h.ctypes.data, ctypes.addressof(P), self.nb)
+        f = np.frombuffer(h, dtype=np.float64, offset=self.nb)
+        f[0] = 0.5 * cam.height / np.tan(0.5 * cam.fov_y)
+        f[1], f[2] = (cam.width - 1) / 2.0, (cam.height - 1) / 2.0
+        f[3:12] = np.asarray(cam.rotation, dtype=np.float64).reshape(9)
+        t_before = {n: tr.adam.state[n]["t"] for n in self.names}
+        f[12:] = tr.adam.schedule([(n, tr.lr(n, it, iters, self.decay_extra)) for n in self.names])
+        pin = self._pin[k]
+        self.params_dev.copy_(pin[:self.nb], non_blocking=True)
+        self.cam_dev.copy_(pin[self.nb:self.nb + 96].view(torch.float64), non_blocking=True)
+        self.sched_dev.copy_(pin[self.nb + 96:].view(torch.float64), non_blocking=True)
+        self.gt_dev.copy_(gt, non_blocking=True)
+        return k, t_before
+
+    def _capture(self, cam, gt):
+        tr = self.tr
+        self._cam0 = cam
+        tr.adam.ensure([(n, tr.p[n]) for n in self.names])
+        saved_t = {n: tr.adam.state[n]["t"] for n in self.names}
+        self._stage(cam, gt, 1, 1)
+        self._body(capturing=False)  # sizes every buffer before capture
+        torch.cuda.synchronize()
+        # undo the warm-up step: parameters, moments, step counts, statistics
+        for n in self.names:
+            tr.adam.state[n]["t"] = saved_t[n]
+        self._restore()
+        self.g = torch.cuda.CUDAGraph()
+        with torch.cuda.graph(self.g):
+            self._body(capturing=True)
+        torch.cuda.synchronize()
+
+    def _snapshot(self):
+        tr = self.tr
+        self._snap = ({n: v.clone() for n, v in tr.p.items()},
+                      {n: (st["m"].clone(), st["v"].clone()) for n, st in tr.adam.state.items()})
+
+    def _restore(self):
+        tr = self.tr
+        p, mv = self._snap
+        for n, v in p.items():
+            tr.p[n].copy_(v)
+        for n, (m, v) in mv.items():
+            tr.adam.state[n]["m"].copy_(m)
+            tr.adam.state[n]["v"].copy_(v)
+        self.stat_sum.zero_()
+        self.gate.zero_()
+
+    def _body(self, capturing):
+        tr = self.tr
+        if not capturing:
+            self._snapshot()
+        loss, grads, stat = tr.step(self._cam0, self.gt_dev, self.weights, graph=self)
+        # sticky gate: this step's pair list overflowed (or an earlier one did)
+        torch.maximum(self.gate, (self.n_pairs[:1] > self.capacity).to(torch.int32),
+                      out=self.gate)
+        items = [(n, tr.p[n], grads[n]) for n in self.names]
+        self._groups = tr.adam.groups(items)
+        self._keep = grads
+        L.check(L.lib().ivr_adam_step_sched(self._groups, len(items), tr.adam.b1, tr.adam.b2,
+                                            tr.adam.eps, self.sched_dev.data_ptr(),
+                                            self.gate.data_ptr(), D.stream_handle()),
+                "ivr_adam_step_sched")
+        self.stat_sum.add_(stat * (1 - self.gate).to(torch.float64))
+        self.loss = loss
+
+    # -- running ---------------------------------------------------------------
+    def step(self, cam, gt, it, iters):
+        """Stage and replay one step; returns the step's loss (device scalar,
+        overwritten by the next replay)."""
+        k, t_before = self._stage(cam, gt, it, iters)
+        self.g.replay()
+        self._np[k].copy_(self.n_pairs[:1], non_blocking=True)
+        ev = torch.cuda.Event()
+        ev.record()
+        self._pending.append((k, ev, it, iters, cam, gt, t_before))
+        return self.loss
+
+    def _retire_oldest(self):
+        """Retire the oldest pending step; on an overflow, recapture with a
+        larger capacity and replay the gated steps."""
+        k, ev = self._pending[0][:2]
+        ev.synchronize()
+        if int(self._np[k][0]) > self.capacity:
+            self._redo()
+        else:
+            self._pending.pop(0)
+
+    def _redo(self):
+        """The oldest pending step overflowed: every pending step was gated."""
+        torch.cuda.synchronize()
+        redo = self._pending
+        self._pending = []
+        tr = self.tr
+        for n in self.names:
+            tr.adam.state[n]["t"] = redo[0][6][n]
+        peak = max(int(self._np[r[0]][0]) for r in redo)
+        self.capacity = max(int(peak * self.headroom) + 4096, 2 * self.capacity)
+        stat_sum = self.stat_sum.clone()
+        self._capture(redo[0][4], redo[0][5])
+        self.stat_sum.copy_(stat_sum)
+        for r in redo:
+            self.step(r[4], r[5], r[2], r[3])
+
+    def flush(self):
+        """Retire every pending step (host synchronisation point)."""
+        while self._pending:
+            self._retire_oldest()
+
+
 def _dc_colors_from_view(points, cam, image):
     """rgb of the training pixel each point projects to, else mid grey
     (trainer.py:264-279)."""
@@ -602,22 +812,43 @@ def _run_stage(tr, dataset, cfg, iters, rng, gen, densify_start=None, decay_extr
     stats_sum = torch.zeros(tr.n, dtype=torch.float64, device=tr.dev)
     stats_iters = 0
     log = []
+    # stage 2: whole steps replay as a CUDA graph (recaptured after densify)
+    use_graph = isinstance(tr, EditableTrainer) and os.environ.get("IVR_TRAIN_GRAPH", "1") != "0"
+    G = None
     for it in range(1, iters + 1):
         view = int(rng.integers(len(dataset)))
-        loss, grads, stat = tr.step(dataset.cameras[view], gts[view])
-        if it % cfg.log_interval == 0:
-            tr.check_finite()
-            D.raise_if_bad(tr._bad, tr.n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw",
-                                           "d_colors"))
-        tr.apply(grads, it, iters, decay_extra)
-        stats_sum += stat
+        if use_graph:
+            if G is None:
+                G = StepGraph(tr, dataset.cameras[view], gts[view], decay_extra=decay_extra)
+            loss = G.step(dataset.cameras[view], gts[view], it, iters)
+            if it % cfg.log_interval == 0:
+                G.flush()
+                tr.check_finite()
+                D.raise_if_bad(tr._bad, tr.n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit",
+                                               "d_n_raw", "d_colors"))
+        else:
+            loss, grads, stat = tr.step(dataset.cameras[view], gts[view])
+            if it % cfg.log_interval == 0:
+                tr.check_finite()
+                D.raise_if_bad(tr._bad, tr.n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit",
+                                               "d_n_raw", "d_colors"))
+            tr.apply(grads, it, iters, decay_extra)
+            stats_sum += stat
         stats_iters += 1
         if it % cfg.densify_interval == 0:
+            if G is not None:
+                G.flush()
+                stats_sum = G.stat_sum
             if start <= it <= until:
                 tr.densify(stats_sum / max(stats_iters, 1), extent, gen)
+                G = None  # parameter tensors replaced: recapture on the next step
+            elif G is not None:
+                G.stat_sum.zero_()
             stats_sum = torch.zeros(tr.n, dtype=torch.float64, device=tr.dev)
             stats_iters = 0
         if it % cfg.log_interval == 0 or it == iters:
+            if G is not None:
+                G.flush()
             tr.check_finite()
             lv = float(loss)
             if not np.isfinite(lv):

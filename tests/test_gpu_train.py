@@ -121,3 +121,66 @@ def test_device_adam_matches_reference_adam():
             shapes = {k: (510,) + s[1:] for k, s in shapes.items()}
     for k in shapes:
         np.testing.assert_allclose(p_dev[k].cpu().numpy(), p_ref[k], rtol=1e-13, atol=1e-15)
+
+
+def _graph_setup(n=20_000, W=96, H=80):
+    from paper_2504_17954_b200 import LightConfig
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
+    from paper_2504_17954_b200.trainer import EditableTrainer, _stage2_init
+    a = editable_arrays(0, n, density=n)
+    light = LightConfig("orbital", 0.45, 0.9)
+    cams = [bench_camera(W, H, az) for az in (0.3, 1.1, 2.0, -0.7)]
+    gt_tr = EditableTrainer(a, a["palette"], light)
+    gts = [gt_tr.render_rgba(c).clone() * 0.9 for c in cams]
+    p = {k: a[k] for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw")}
+    p.update(_stage2_init(n))
+    return (lambda: EditableTrainer(p, a["palette"], light)), cams, gts
+
+
+def test_step_graph_matches_eager_steps():
+    """StepGraph replays (device schedule, gated Adam) follow the eager
+    step + apply sequence (views and lr schedule vary per step)."""
+    import torch
+    from paper_2504_17954_b200.trainer import StepGraph
+    make, cams, gts = _graph_setup()
+    eager, graph = make(), make()
+    losses_e = []
+    for it in range(1, 7):
+        v = it % len(cams)
+        loss, grads, _ = eager.step(cams[v], gts[v])
+        eager.apply(grads, it, 20)
+        losses_e.append(float(loss))
+    G = StepGraph(graph, cams[1], gts[1])
+    losses_g = []
+    for it in range(1, 7):
+        v = it % len(cams)
+        loss = G.step(cams[v], gts[v], it, 20)
+        torch.cuda.synchronize()
+        losses_g.append(float(loss))
+    G.flush()
+    np.testing.assert_allclose(losses_g, losses_e, rtol=1e-5)
+    for k in eager.p:
+        a, b = eager.p[k].cpu().numpy(), graph.p[k].cpu().numpy()
+        assert np.linalg.norm(a - b) <= 1e-5 * max(np.linalg.norm(a), 1e-12), k
+
+
+def test_step_graph_recovers_from_pair_overflow():
+    """A too-small capacity gates the step (and the ones after it); flush()
+    recaptures with a larger capacity and replays them in order."""
+    from paper_2504_17954_b200.trainer import StepGraph
+    make, cams, gts = _graph_setup()
+    ref, tr = make(), make()
+    G0 = StepGraph(ref, cams[0], gts[0])
+    for it in range(1, 5):
+        G0.step(cams[it % 4], gts[it % 4], it, 10)
+    G0.flush()
+    G = StepGraph(tr, cams[0], gts[0])
+    G.capacity = 64
+    G._capture(cams[0], gts[0])
+    for it in range(1, 5):
+        G.step(cams[it % 4], gts[it % 4], it, 10)
+    G.flush()
+    assert G.capacity > 64
+    for k in ref.p:
+        a, b = ref.p[k].cpu().numpy(), tr.p[k].cpu().numpy()
+        assert np.linalg.norm(a - b) <= 1e-5 * max(np.linalg.norm(a), 1e-12), k
