@@ -329,7 +329,7 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
 }
 
 template <int KMAX, bool F64, int MODE>
-__global__ void __launch_bounds__(kBlendThreads, 3)
+__global__ void __launch_bounds__(kBlendThreads, (KMAX <= 4 && !F64) ? 4 : 3)
 blend_fwd_kernel(BlendArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Slots = WarpSlots<KMAX, F64, kModeExact>;  // EXACT layout also serves FAST
