@@ -38,13 +38,13 @@ PER_MODEL, N_MODELS, DENSITY = 200_000, 5, 1_000_000
 # = 25) + K3 (1)
 def launches_per_frame(n):
     """Kernels in one captured frame: K1; K2 = init + minmax + coarse keys +
-    3 per radix pass + fix-up + fallback gate + 2 scans + hist + rowscan +
-    tile ranges + placement; tile order; K3 (sort.cu / blend.cu)."""
+    3 per radix pass + fix-up + fallback gate + hist + rowscan + tile ranges
+    (also P) + placement; tile order; K3 (sort.cu / blend.cu)."""
     lg = 1
     while (1 << lg) < n:
         lg += 1
     passes = min(max((lg + 4 + 7) // 8, 2), 4)
-    return 1 + (3 + 3 * passes + 2 + 2 + 4) + 1 + 1
+    return 1 + (3 + 3 * passes + 2 + 4) + 1 + 1
 
 
 SLOTS = int(os.environ.get("IVR_SLOTS", "6"))  # concurrent frame slots (FrameGraph / FramePipeline)

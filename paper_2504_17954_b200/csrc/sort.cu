@@ -407,54 +407,6 @@ fallback_sort_kernel(const uint64_t *depth_key, int64_t n, const int32_t *need_f
     // result in kA/vA after 8 passes (pass 7 writes A)
 }
 
-// ----------------------------------------------------------------- rank offsets
-__global__ void __launch_bounds__(kThreads)
-scan_reduce_kernel(const uint32_t *order, const int32_t *count, int64_t n, uint32_t *partial) {
-    __shared__ uint32_t s_warp[kWarps];
-    const int64_t base = (int64_t)blockIdx.x * kChunk;
-    uint32_t sum = 0;
-#pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const int64_t idx = base + r * kThreads + threadIdx.x;
-        if (idx < n) sum += (uint32_t)count[order[idx]];
-    }
-    uint32_t tot;
-    block_incl_scan(sum, s_warp, tot);
-    if (threadIdx.x == 0) partial[blockIdx.x] = tot;
-}
-
-__global__ void __launch_bounds__(1024)
-scan_partials_kernel(uint32_t *partial, int nb, int32_t *n_pairs) {
-    __shared__ uint32_t s_warp[32];
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t carry = 0;
-    for (int base = 0; base < nb; base += 1024) {
-        const int i = base + threadIdx.x;
-        const uint32_t v = i < nb ? partial[i] : 0;
-        uint32_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_warp[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = s_warp[lane];
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            s_warp[lane] = w;
-        }
-        __syncthreads();
-        const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0);
-        if (i < nb) partial[i] = (uint32_t)carry + incl - v;
-        carry += s_warp[31];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) *n_pairs = carry > 0x7fffffffull ? 0x7fffffff : (int32_t)carry;
-}
-
 // ----------------------------------------------------------------- placement
 constexpr int kRanksPerWarp = 256;
 constexpr int kRanksPerBlock = kRanksPerWarp * kWarps;  // 2048 ranks per block
@@ -582,10 +534,11 @@ pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
 
 // tile_ranges = exclusive scan of tile totals (single block)
 __global__ void __launch_bounds__(1024)
-tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges, uint32_t cap) {
+tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges, uint32_t cap,
+                   int32_t *n_pairs) {
     __shared__ uint32_t s_warp[32];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint32_t carry = 0;
+    uint64_t carry = 0;
     for (int base = 0; base < ntiles; base += 1024) {
         const int i = base + threadIdx.x;
         const uint32_t v = i < ntiles ? totals[i] : 0;
@@ -608,11 +561,15 @@ tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges, uint32_t
         const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0);
         // clamped to the pair capacity: an overflowed frame (n_pairs > capacity,
         // detected by the caller) never makes K3/K4 read past pair_splat
-        if (i < ntiles) ranges[i] = (int32_t)min(carry + incl - v, cap);
+        if (i < ntiles) ranges[i] = (int32_t)min(carry + incl - v, (uint64_t)cap);
         carry += s_warp[31];
         __syncthreads();
     }
-    if (threadIdx.x == 0) ranges[ntiles] = (int32_t)min(carry, cap);
+    if (threadIdx.x == 0) {
+        ranges[ntiles] = (int32_t)min(carry, (uint64_t)cap);
+        // P = the sum of all tile counts (unclamped; saturated to int32)
+        *n_pairs = carry > 0x7fffffffull ? 0x7fffffff : (int32_t)carry;
+    }
 }
 
 // stable placement: warp w of block b owns ranks [b*2048 + w*256, +256).
@@ -714,7 +671,7 @@ Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
         al(4 * (size_t)n), al(4 * (size_t)n),                    // 2,3 vals A/B
         al(8 * (size_t)n), al(8 * (size_t)n),                    // 4,5 full keys (fallback) A/B
         al(4),                                                   // 6 (unused)
-        al(4 * (size_t)(L.nbk + 1)),                             // 7 scan partials
+        al(4),                                                   // 7 (unused)
         al(4 * (size_t)256 * (L.nbk + 1)),                       // 8 radix blockhist
         al(4 * 256),                                             // 9 radix rowtotal
         al(4 * (size_t)ntiles * (L.nbp + 1)),                    // 10 pair tile hist
@@ -790,7 +747,6 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     uint32_t *ckA = (uint32_t *)(ws + L.off[0]), *ckB = (uint32_t *)(ws + L.off[1]);
     uint32_t *vA = (uint32_t *)(ws + L.off[2]), *vB = (uint32_t *)(ws + L.off[3]);
     uint64_t *fkA = (uint64_t *)(ws + L.off[4]), *fkB = (uint64_t *)(ws + L.off[5]);
-    uint32_t *partial = (uint32_t *)(ws + L.off[7]);
     uint32_t *bh = (uint32_t *)(ws + L.off[8]);
     uint32_t *rt = (uint32_t *)(ws + L.off[9]);
     uint32_t *phist = (uint32_t *)(ws + L.off[10]);
@@ -826,10 +782,8 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
                                                                            need_full);
     // fallback (device-gated, normally an immediate return): full 64-bit sort into ord
     fallback_sort_kernel<<<1, kFbThreads, 0, st>>>(depth_key, n, need_full, fkA, fkB, ord, vscratch);
-    // ---- 2. pair count P (sum of tile counts) -> n_pairs
-    scan_reduce_kernel<<<nbk, kThreads, 0, st>>>(ord, count, n, partial);
-    scan_partials_kernel<<<1, 1024, 0, st>>>(partial, nbk, n_pairs);
-    // ---- 3. counting placement by tile (+ optional tile cull flag)
+    // ---- 2. counting placement by tile (+ optional tile cull flag); the
+    // tile-range scan also yields P = n_pairs
     PairCtx C{};
     C.order = ord;
     C.count = count;
@@ -853,7 +807,8 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
             phist, ntiles, nbp, ttot, nullptr);
     else
         rowscan_kernel<<<ntiles, 1024, 0, st>>>(phist, nbp, ttot, nullptr);
-    tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges, (uint32_t)pair_capacity);
+    tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges, (uint32_t)pair_capacity,
+                                           n_pairs);
     pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, nbp, tile_ranges, pair_splat,
                                                        width, height);
     return ivr::check_launch("ivr_bin_sort");
