@@ -37,14 +37,15 @@ PER_MODEL, N_MODELS, DENSITY = 200_000, 5, 1_000_000
 # fallback gate, 3 scan, tile hist, tile rowscan, tile ranges, placement, tile order
 # = 25) + K3 (1)
 def launches_per_frame(n):
-    """Kernels in one captured frame: K1; K2 = init + minmax + coarse keys +
-    3 per radix pass + fix-up + fallback gate + hist + rowscan + tile ranges
-    (also P) + placement; tile order; K3 (sort.cu / blend.cu)."""
+    """Kernels in one captured frame: K1; K2 = init + minmax + 3 per radix
+    pass (the first upsweep also maps the coarse keys) + fix-up + fallback
+    gate + hist + rowscan + tile ranges (also P) + placement; tile order; K3
+    (sort.cu / blend.cu)."""
     lg = 1
     while (1 << lg) < n:
         lg += 1
     passes = min(max((lg + 4 + 7) // 8, 2), 4)
-    return 1 + (3 + 3 * passes + 2 + 4) + 1 + 1
+    return 1 + (2 + 3 * passes + 2 + 4) + 1 + 1
 
 
 SLOTS = int(os.environ.get("IVR_SLOTS", "6"))  # concurrent frame slots (FrameGraph / FramePipeline)

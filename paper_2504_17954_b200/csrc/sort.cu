@@ -102,22 +102,6 @@ minmax_kernel(const uint64_t *keys, int64_t n, unsigned long long *mm /* [min, m
     }
 }
 
-// Visible keys get `vbits` bits ((bits - min) >> s < 2^vbits); invisible
-// splats carry all ones, above every visible key in the sorted digits.
-__global__ void __launch_bounds__(kThreads)
-coarse_key_kernel(const uint64_t *keys, int64_t n, const unsigned long long *mm, int vbits,
-                  uint32_t *ck) {
-    const unsigned long long lo = mm[0], hi = mm[1];
-    const unsigned long long range = hi >= lo ? hi - lo : 0ull;
-    const int bits = range ? 64 - __clzll((long long)range) : 0;
-    const int s = bits > vbits ? bits - vbits : 0;
-    for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
-         i += (int64_t)gridDim.x * kThreads) {
-        const unsigned long long k = keys[i];
-        ck[i] = k == ~0ull ? kInvisible : (uint32_t)((k - lo) >> s);
-    }
-}
-
 // ----------------------------------------------------------------- radix passes
 // Stable LSD pass (8-bit digit at `shift`) of (key, value) pairs.  vals_in ==
 // nullptr means identity values.  `gate` (device int, may be null): the pass
@@ -141,6 +125,40 @@ upsweep_kernel(const KeyT *keys, int64_t n, int shift, uint32_t *blockhist, int 
     for (int r = 0; r < kItems; ++r) {
         const int64_t idx = base + r * kThreads + threadIdx.x;
         if (idx < n) atomicAdd(&s[(uint32_t)(k[r] >> shift) & 255u], 1u);
+    }
+    __syncthreads();
+    blockhist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = s[threadIdx.x];
+}
+
+// First pass's upsweep fused with the coarse-key mapping: visible keys get
+// `vbits` bits ((bits - min) >> s < 2^vbits), invisible splats all ones (above
+// every visible key).  Reads the 64-bit depth keys, writes the 32-bit coarse
+// keys the pass's downsweep consumes, and builds the pass-0 digit histogram.
+__global__ void __launch_bounds__(kThreads)
+upsweep_coarse_kernel(const uint64_t *full, int64_t n, const unsigned long long *mm, int vbits,
+                      uint32_t *ck, uint32_t *blockhist, int nblocks) {
+    __shared__ uint32_t s[kRadix];
+    s[threadIdx.x] = 0;
+    const unsigned long long lo = mm[0], hi = mm[1];
+    const unsigned long long range = hi >= lo ? hi - lo : 0ull;
+    const int bits = range ? 64 - __clzll((long long)range) : 0;
+    const int sh = bits > vbits ? bits - vbits : 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    unsigned long long k[kItems];
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int64_t idx = base + r * kThreads + threadIdx.x;
+        k[r] = idx < n ? full[idx] : 0ull;
+    }
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int64_t idx = base + r * kThreads + threadIdx.x;
+        if (idx < n) {
+            const uint32_t c = k[r] == ~0ull ? kInvisible : (uint32_t)((k[r] - lo) >> sh);
+            ck[idx] = c;
+            atomicAdd(&s[c & 255u], 1u);
+        }
     }
     __syncthreads();
     blockhist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = s[threadIdx.x];
@@ -689,10 +707,14 @@ Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
 }
 
 template <typename KeyT>
-void radix_pass(cudaStream_t st, const KeyT *k_in, const uint32_t *v_in, KeyT *k_out,
+void radix_pass(cudaStream_t st, KeyT *k_in, const uint32_t *v_in, KeyT *k_out,
                 uint32_t *v_out, int64_t n, int shift, int nbk, uint32_t *bh, uint32_t *rt,
-                const int32_t *gate) {
-    upsweep_kernel<KeyT><<<nbk, kThreads, 0, st>>>(k_in, n, shift, bh, nbk, gate);
+                const int32_t *gate, const uint64_t *full = nullptr,
+                const unsigned long long *mm = nullptr, int vbits = 0) {
+    if (full)  // k_in is written here from the 64-bit keys (first pass, KeyT = uint32_t)
+        upsweep_coarse_kernel<<<nbk, kThreads, 0, st>>>(full, n, mm, vbits, (uint32_t *)k_in, bh, nbk);
+    else
+        upsweep_kernel<KeyT><<<nbk, kThreads, 0, st>>>(k_in, n, shift, bh, nbk, gate);
     if (nbk <= 2048)
         rowscan_warp_kernel<<<256 / kRowsPerBlock, 32 * kRowsPerBlock, 0, st>>>(bh, 256, nbk, rt, gate);
     else
@@ -766,10 +788,13 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     int gb = (int)((n + kThreads * 8 - 1) / (kThreads * 8));
     gb = gb < 1 ? 1 : (gb > 1184 ? 1184 : gb);
     minmax_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm);
-    coarse_key_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm, vbits, ckA);
     uint32_t *kin = ckA, *kout = ckB, *vin = nullptr, *vout = vB;
     for (int p = 0; p < passes; ++p) {
-        radix_pass<uint32_t>(st, kin, vin, kout, vout, n, 8 * p, nbk, bh, rt, nullptr);
+        if (p == 0)  // coarse keys produced by the first upsweep
+            radix_pass<uint32_t>(st, kin, vin, kout, vout, n, 0, nbk, bh, rt, nullptr,
+                                 depth_key, mm, vbits);
+        else
+            radix_pass<uint32_t>(st, kin, vin, kout, vout, n, 8 * p, nbk, bh, rt, nullptr);
         uint32_t *t = kin;
         kin = kout;
         kout = t;
