@@ -149,6 +149,8 @@ struct WarpSlots {
     float4 r0[32], r1[32];
     float v[32 * KMAX];
     double r64[F64 ? 32 * 6 : 1];                           // mx, my, a, b, c, o
+    float2 lo[F64 ? 32 : 1];  // FAST float64 mode: mean - float32(mean), per pair
+    int sp[F64 ? 32 : 1];     // FAST float64 mode: splat (band pairs read rec64 lazily)
     double v64[(F64 && MODE == kModeExact) ? 32 * KMAX : 1];
 };
 
@@ -209,9 +211,18 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
             }
             if (F64) {
                 const double *r = A.rec64 + 8 * (int64_t)sp;
+                if (MODE == kModeExact) {
 #pragma unroll
-                for (int c = 0; c < 6; ++c) W.r64[lane * 6 + c] = __ldg(r + c);
-                if (WMODE == kModeExact) {
+                    for (int c = 0; c < 6; ++c) W.r64[lane * 6 + c] = __ldg(r + c);
+                } else {
+                    // mean - float32(mean) is exact in float64 and tiny: the
+                    // candidate dx = (px - mx32) - lo carries <= ~1 ulp (the
+                    // error bound budgets 5 ulp for dx)
+                    W.lo[lane] = make_float2((float)(__ldg(r) - (double)r0.x),
+                                             (float)(__ldg(r + 1) - (double)r0.y));
+                    W.sp[lane] = sp;
+                }
+                if (MODE == kModeExact) {  // FAST walks accumulate the float32 values
                     const double *v64 = A.values64 + (int64_t)K * sp;
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c) W.v64[lane * KMAX + c] = c < K ? __ldg(v64 + c) : 0.0;
@@ -261,8 +272,9 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                 // candidate: in dtype=float64 mode recompute dx, dy from the float64 mean
                 float cdx = dx, cdy = dy, cbdy = bdy, chcdy = hcdy, csig = sig;
                 if (F64) {
-                    cdx = (float)dsub(dpx, W.r64[q * 6]);
-                    cdy = (float)dsub(dpy, W.r64[q * 6 + 1]);
+                    const float2 lo = W.lo[q];
+                    cdx = dx - lo.x;
+                    cdy = dy - lo.y;
                     cbdy = a1.y * cdy;
                     chcdy = a1.z * cdy;
                     csig = fmaf(fmaf(a1.x, cdx, cbdy), cdx, chcdy * cdy);
@@ -284,8 +296,9 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
                 } else {
                     double ad;
                     if (F64) {
-                        const double *r = W.r64 + q * 6;
-                        ad = exact_alpha(dpx, dpy, r[0], r[1], r[2], r[3], r[4], r[5]);
+                        const double *r = A.rec64 + 8 * (int64_t)W.sp[q];
+                        ad = exact_alpha(dpx, dpy, __ldg(r), __ldg(r + 1), __ldg(r + 2),
+                                         __ldg(r + 3), __ldg(r + 4), __ldg(r + 5));
                     } else {
                         ad = exact_alpha(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
                                          2.0 * (double)a1.z, a0.z);
