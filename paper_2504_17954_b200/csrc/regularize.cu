@@ -15,7 +15,8 @@
 // The reference / torch restatement builds each of these with tens of full-map
 // array operations; here they are two kernels: a first pass (normal-mask
 // count -- the normal loss divides by it -- and the bilateral edge-weight
-// map) and the fused gradient + per-block loss partial sums.
+// map, and the pseudo normals it needs, stored for the second pass) and the
+// fused gradient + per-block loss partial sums.
 #include "ivr_common.cuh"
 
 namespace ivr {
@@ -34,6 +35,7 @@ struct Args {
     double w_normal, w_offset, w_bil;
     int *mask_count;       // device: pixels in the normal mask
     double *wmap;          // (H, W) bilateral edge weights / (H W), from the first pass
+    double4 *nmap;         // (H, W) world pseudo normal + mask flag, from the first pass
     float *d_out;          // (H, W, K)
     double *part;          // per block: normal, |offset| sum, bilateral sum
 };
@@ -123,6 +125,7 @@ __global__ void __launch_bounds__(kThreads) mask_count_kernel(Args A) {
         if (A.w_normal > 0.0) {
             double nw[3];
             c = pseudo_normal(A, y, x, nw) ? 1 : 0;
+            A.nmap[i] = make_double4(nw[0], nw[1], nw[2], (double)c);
         }
         if (A.w_bil > 0.0 && A.n_bil > 0)
             A.wmap[i] = edge_weight(A, y, x) * (1.0 / ((double)A.H * A.W));
@@ -153,8 +156,9 @@ __global__ void __launch_bounds__(kThreads) reg_grad_kernel(Args A) {
             d[A.c_alpha] = (float)g[3];
         }
         if (A.w_normal > 0.0) {
-            double nw[3];
-            const bool m = pseudo_normal(A, y, x, nw);
+            const double4 nm = A.nmap[i];  // computed once by the first pass
+            const double nw[3] = {nm.x, nm.y, nm.z};
+            const bool m = nm.w != 0.0;
             const double cnt = (double)max(*A.mask_count, 1);
             if (m) {
                 double df[3];
@@ -232,7 +236,7 @@ __global__ void __launch_bounds__(kThreads) reg_finish_kernel(const double *part
 extern "C" size_t ivr_regularize_workspace_size(int32_t height, int32_t width) {
     const int64_t npx = (int64_t)height * width;
     const int64_t nb = (npx + ivr::regk::kThreads - 1) / ivr::regk::kThreads;
-    return 256 + 8 * (size_t)(3 * nb) + 8 * (size_t)npx;
+    return 256 + 8 * (size_t)(3 * nb) + 8 * (size_t)npx + 32 + 32 * (size_t)npx;
 }
 
 extern "C" int ivr_regularize(const float *out, int32_t k, int32_t height, int32_t width,
@@ -280,6 +284,7 @@ extern "C" int ivr_regularize(const float *out, int32_t k, int32_t height, int32
     const int64_t npx = (int64_t)height * width;
     const int nb = (int)((npx + kThreads - 1) / kThreads);
     A.wmap = A.part + 3 * (int64_t)nb;
+    A.nmap = reinterpret_cast<double4 *>(((uintptr_t)(A.wmap + npx) + 31) & ~(uintptr_t)31);
     if (cudaMemsetAsync(A.mask_count, 0, sizeof(int), st) != cudaSuccess)
         return check_launch("ivr_regularize memset");
     if (w_normal > 0.0 || (w_bil > 0.0 && n_bil > 0)) mask_count_kernel<<<nb, kThreads, 0, st>>>(A);
