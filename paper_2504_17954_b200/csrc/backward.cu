@@ -109,6 +109,14 @@ struct BwdSlots {
     float v[32 * KMAX];
     int sp[32];
     double r64[F64 ? 32 * 6 : 1];
+    // deferred value gradients: a batch of up to kBatch contributing pairs
+    // keeps each pixel's blend weight w (bw[pair][pixel], padded rows:
+    // conflict-free reads); at a flush lanes i and i + 16 form pair i's K sums
+    // sum_p bw[i][p] * dout[p][c] (one half of the channels each) from the
+    // warp's dout table
+    float bw[16 * 33];
+    __align__(16) float dout[32 * KMAX];
+    int bsp[16], bj[16];
 };
 
 constexpr int kBwdWarpW = 8;  // warp footprint 8x4 pixels (as K3)
@@ -149,10 +157,54 @@ blend_bwd_kernel(BwdArgs A) {
         const float Cc = (inside && c < K) ? A.out[pix * K + c] : 0.0f;
         dout[c] = (inside && c < K) ? A.d_out[pix * K + c] : 0.0f;
         S_C = fmaf(dout[c], Cc, S_C);
+        W.dout[lane * KMAX + c] = dout[c];
     }
-    // per-lane atomic target for the transposed totals: lane l owns value
-    // slot l (< K) and geometry slot l (< 6: mean2d x, y, conic a, b, c, opacity)
-    float *vbase = lane < K ? A.g_values + lane : nullptr;
+    int nbat = 0;  // pairs in the deferred value batch (warp-uniform)
+    // flush: lanes i and i + 16 reduce pair i of the batch over the 32 pixels
+    constexpr int KH = KMAX / 2;  // channels per lane at a flush
+    auto flush = [&]() {
+        __syncwarp();
+        const int bi = lane & 15, c0 = (lane >> 4) * KH;
+        if (bi < nbat) {
+            float acc[KH];
+#pragma unroll
+            for (int c = 0; c < KH; ++c) acc[c] = 0.f;
+            const float *row = W.bw + bi * 33;
+#pragma unroll 4
+            for (int p2 = 0; p2 < 32; ++p2) {
+                const float wv = row[p2];
+                const float *dr = W.dout + p2 * KMAX + c0;
+                if (KH % 4 == 0) {
+#pragma unroll
+                    for (int c4 = 0; c4 < KH / 4; ++c4) {
+                        const float4 d = reinterpret_cast<const float4 *>(dr)[c4];
+                        acc[4 * c4] = fmaf(wv, d.x, acc[4 * c4]);
+                        acc[4 * c4 + 1] = fmaf(wv, d.y, acc[4 * c4 + 1]);
+                        acc[4 * c4 + 2] = fmaf(wv, d.z, acc[4 * c4 + 2]);
+                        acc[4 * c4 + 3] = fmaf(wv, d.w, acc[4 * c4 + 3]);
+                    }
+                } else {
+#pragma unroll
+                    for (int c = 0; c < KH; ++c) acc[c] = fmaf(wv, dr[c], acc[c]);
+                }
+            }
+            if (A.part) {
+                float *pp = A.part + ((int64_t)W.bj[bi] * (kBwdThreads / 32) + warp) * (K + 6);
+#pragma unroll
+                for (int c = 0; c < KH; ++c)
+                    if (c0 + c < K && acc[c] != 0.f) pp[c0 + c] = acc[c];
+            } else {
+                float *gv = A.g_values + (int64_t)K * W.bsp[bi] + c0;
+#pragma unroll
+                for (int c = 0; c < KH; ++c)
+                    if (c0 + c < K && acc[c] != 0.f) atomicAdd(gv + c, acc[c]);
+            }
+        }
+        __syncwarp();
+        nbat = 0;
+    };
+    // per-lane atomic target for the transposed geometry totals: lane l owns
+    // slot l (< 6: mean2d x, y, conic a, b, c, opacity)
     float *gbase = nullptr;
     int gstride = 0;
     if (!GEOM) {  // opacity only (transform fits): lane 0 adds the warp sum
@@ -258,11 +310,10 @@ blend_bwd_kernel(BwdArgs A) {
                     dy = cdy;
                 }
             }
-            // per-pixel contributions: xv[c] = d value_c, xg = d mean2d (2),
-            // d conic (3), d opacity (zero when not contributing)
-            float xv[KMAX], xg[8];
-#pragma unroll
-            for (int c = 0; c < KMAX; ++c) xv[c] = 0.f;
+            // per-pixel contributions: w (the value gradients dout_c * w are
+            // reduced per batch), xg = d mean2d (2), d conic (3), d opacity
+            // (zero when not contributing)
+            float wpix = 0.f, xg[8];
 #pragma unroll
             for (int c = 0; c < 8; ++c) xg[c] = 0.f;
             if (contrib) {
@@ -283,8 +334,7 @@ blend_bwd_kernel(BwdArgs A) {
 #pragma unroll
                     for (int c = 0; c < KMAX; ++c) Dv = fmaf(dout[c], W.v[q * KMAX + c], Dv);
                 }
-#pragma unroll
-                for (int c = 0; c < KMAX; ++c) xv[c] = dout[c] * w;
+                wpix = w;
                 S_A = fmaf(w, Dv, S_A);  // dout . A after this contributor
                 const float d_alpha = T * Dv - (S_C - S_A) * inv;
                 if (alu < 0.99f) {
@@ -302,26 +352,30 @@ blend_bwd_kernel(BwdArgs A) {
                 T = T * (1.0f - al);
             }
             if (__any_sync(0xffffffffu, contrib)) {
-                // transpose reductions (KMAX-1 and 7 shuffles + the remaining lane
-                // bits): lane l ends with value slot l % KMAX and geometry slot
-                // l % 8; parallel atomics
+                // value gradients: this pair's pixel weights join the batch;
+                // geometry: transpose reduction (7 shuffles + the remaining lane
+                // bits, lane l ends with slot l % 8) and parallel atomics
                 const int s = W.sp[q];
-                const float tv = warp_transpose_sum<KMAX>(xv, lane);
+                W.bw[nbat * 33 + lane] = wpix;
+                if (lane == 0) {
+                    W.bsp[nbat] = s;
+                    W.bj[nbat] = base + q;
+                }
+                if (++nbat == 16) flush();
                 const float tg = GEOM ? warp_transpose_sum<8>(xg, lane) : warp_sum(xg[5]);
                 if (A.part) {  // deterministic mode: plain stores, reduced in fixed order later
                     float *pp = A.part + ((int64_t)(base + q) * (kBwdThreads / 32) + warp) * (K + 6);
-                    if (lane < K && tv != 0.f) pp[lane] = tv;
                     if (GEOM ? (lane < 6) : (lane == 0)) {
                         if (tg != 0.f) pp[K + (GEOM ? lane : 5)] = tg;
                     }
                 } else {
-                    if (vbase && tv != 0.f) atomicAdd(vbase + (int64_t)K * s, tv);
                     if (gbase && tg != 0.f) atomicAdd(gbase + (int64_t)gstride * s, tg);
                 }
             }
         }
         __syncwarp();  // slots are rewritten by the next chunk
     }
+    if (nbat > 0) flush();
 }
 
 template <int KMAX, bool F64>
