@@ -173,19 +173,28 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
     constexpr int KPF = KMAX <= 4 ? KMAX : 0;  // values prefetched with the record (K <= 4)
     float pv[KPF > 0 ? KPF : 1];
-    auto fetch = [&](int base) {
+    // two-stage prefetch: a chunk's pair ids are loaded one chunk before its
+    // records, so the dependent id -> record round trips of the list stream
+    // overlap two walks instead of one (bit 31 of an id: culled for this tile
+    // by ivr_bin_sort_cull; -1 past the list end)
+    auto fetch_ids = [&](int base) {
         const int j = base + lane;
-        if (j < s1) {
-            sp = __ldg(A.pair_splat + j);  // bit 31: culled for this tile by ivr_bin_sort_cull
-            if (sp >= 0) {
-                r0 = __ldg(A.rec + 2 * sp);
-                r1 = __ldg(A.rec + 2 * sp + 1);
+        return j < s1 ? __ldg(A.pair_splat + j) : -1;
+    };
+    auto fetch_recs = [&](int id) {
+        sp = id;
+        if (id >= 0) {
+            r0 = __ldg(A.rec + 2 * id);
+            r1 = __ldg(A.rec + 2 * id + 1);
 #pragma unroll
-                for (int c = 0; c < KPF; ++c) pv[c] = c < K ? __ldg(A.values + (int64_t)K * sp + c) : 0.0f;
-            }
+            for (int c = 0; c < KPF; ++c) pv[c] = c < K ? __ldg(A.values + (int64_t)K * id + c) : 0.0f;
         }
     };
-    if (s0 < s1) fetch(s0);
+    int spn = -1;  // ids of the next chunk
+    if (s0 < s1) {
+        fetch_recs(fetch_ids(s0));
+        if (s0 + 32 < s1) spn = fetch_ids(s0 + 32);
+    }
     for (int base = s0; base < s1; base += 32) {
         if (__all_sync(0xffffffffu, st.done)) break;
         const int j = base + lane;
@@ -230,7 +239,10 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
             }
         }
         __syncwarp();
-        if (base + 32 < s1) fetch(base + 32);  // prefetch the next chunk during the walk
+        if (base + 32 < s1) {  // prefetch during the walk: next records, ids after that
+            fetch_recs(spn);
+            spn = base + 64 < s1 ? fetch_ids(base + 64) : -1;
+        }
         uint32_t mbits = st.done ? 0u : m;
         while (mbits) {
             const int q = __ffs(mbits) - 1;
