@@ -228,17 +228,24 @@ blend_bwd_kernel(BwdArgs A) {
 
     int sp = 0;
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
-    auto fetch = [&](int base) {
+    // two-stage prefetch as in K3: ids one chunk ahead of their records
+    // (bit 31: culled for this tile by ivr_bin_sort_cull; -1 past the stop)
+    auto fetch_ids = [&](int base) {
         const int j = base + lane;
-        if (j < stop) {
-            sp = __ldg(A.pair_splat + j);  // bit 31: culled for this tile (ivr_bin_sort_cull)
-            if (sp >= 0) {
-                r0 = __ldg(A.rec + 2 * sp);
-                r1 = __ldg(A.rec + 2 * sp + 1);
-            }
+        return j < stop ? __ldg(A.pair_splat + j) : -1;
+    };
+    auto fetch_recs = [&](int id) {
+        sp = id;
+        if (id >= 0) {
+            r0 = __ldg(A.rec + 2 * id);
+            r1 = __ldg(A.rec + 2 * id + 1);
         }
     };
-    if (s0 < stop) fetch(s0);
+    int spn = -1;
+    if (s0 < stop) {
+        fetch_recs(fetch_ids(s0));
+        if (s0 + 32 < stop) spn = fetch_ids(s0 + 32);
+    }
     for (int base = s0; base < stop; base += 32) {
         const int j = base + lane;
         const bool keep = j < stop && sp >= 0 && !tile_cull32(r0, r1, sx0, sx1, sy0, sy1);
@@ -257,7 +264,10 @@ blend_bwd_kernel(BwdArgs A) {
             }
         }
         __syncwarp();
-        if (base + 32 < stop) fetch(base + 32);
+        if (base + 32 < stop) {
+            fetch_recs(spn);
+            spn = base + 64 < stop ? fetch_ids(base + 64) : -1;
+        }
         uint32_t mbits = m;
         while (mbits) {
             const int q = __ffs(mbits) - 1;
