@@ -44,3 +44,31 @@ def test_missing_library_fails_loudly(monkeypatch):
     monkeypatch.setattr(_lib, "LIB_PATH", "/nonexistent/libivrgs.so")
     with pytest.raises(_lib.NativeLibraryMissing):
         _lib.lib()
+
+
+def test_training_and_inverse_plumbing_validation_without_gpu():
+    """The step / inverse / deterministic-backward entry points reject bad
+    arguments before any CUDA call."""
+    if not os.path.exists(_lib.LIB_PATH):
+        pytest.skip("libivrgs.so not built")
+    L = _lib.lib()
+    E = _lib.IVR_ERR_ARG
+    assert L.ivr_stage2_attrs(-1, None, None, None, None, None, None, None, None, None) == E
+    assert L.ivr_step_assemble(None, None) == E
+    a = _lib.StepGrads_t()
+    a.n, a.k = 10, 4
+    a.stat = 1  # stat without its inputs
+    assert L.ivr_step_assemble(ctypes.byref(a), None) == E
+    assert L.ivr_step_partials(1000) >= 1
+    assert L.ivr_loss_finalize(None, None, None, None, None) == E
+    assert L.ivr_inverse_update(None, None) == E
+    st = _lib.InverseStep_t()
+    st.n_scenes, st.n_views = 2000, 1  # > 1024 scenes
+    assert L.ivr_inverse_update(ctypes.byref(st), None) == E
+    groups = (_lib.AdamGroup_t * 1)()
+    assert L.ivr_adam_step_sched(groups, 1, 0.9, 0.999, 1e-15, None, None, None) == E
+    assert L.ivr_blend_bwd_det_workspace_size(100, 15) == 100 * 8 * 21 * 4
+    assert L.ivr_blend_bwd_det_workspace_size(100, 33) == 0
+    assert L.ivr_blend_bwd_deterministic(None, None, 1, 1, None, None, None, 4, 16, 16, None, None,
+                                         None, 10, None, None, None, 100, None, 0, None, None,
+                                         None, None, None, 0, None) == E
