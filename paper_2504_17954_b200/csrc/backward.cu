@@ -471,7 +471,10 @@ struct BwdConst {
     int geometry;
 };
 
-__global__ void __launch_bounds__(128, 4)
+// GEOM: the projection / covariance / quaternion backward is compiled in
+// (training); transform fits instantiate without it (fewer registers).
+template <bool GEOM>
+__global__ void __launch_bounds__(128, GEOM ? 4 : 5)
 preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *__restrict__ Pd) {
     __shared__ ivr_frame_params P;
     __shared__ double s_glob[10];
@@ -544,7 +547,7 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
         }
 
         // ---- geometry (gaussians.project_backward)
-        if (B.geometry) {
+        if (GEOM) {
             Proj p;
             project_one(G, i, cam, p);
             double dq[4] = {0, 0, 0, 0}, dls[3] = {0, 0, 0};
@@ -898,6 +901,9 @@ extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *sha
     const int threads = 128;
     const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
     const size_t sm = (size_t)grads->per_scene * 4 * sizeof(double);
-    preprocess_bwd_kernel<<<blocks, threads, sm, (cudaStream_t)stream>>>(B, Pv, params);
+    if (geometry)
+        preprocess_bwd_kernel<true><<<blocks, threads, sm, (cudaStream_t)stream>>>(B, Pv, params);
+    else
+        preprocess_bwd_kernel<false><<<blocks, threads, sm, (cudaStream_t)stream>>>(B, Pv, params);
     return check_launch("preprocess_bwd_kernel");
 }
