@@ -189,7 +189,9 @@ int ivr_bin_sort(int64_t n, const uint64_t *depth_key, const int32_t *count,
  * alpha 1/255 over their whole tile (float64 minimum of the exponent over the
  * tile rectangle vs the record's bound) get bit 31 set in pair_splat;
  * (pair_splat & 0x7fffffff) is still the reference list.  rec is K1's float32
- * record; width/height the frame size.  ntiles <= 8192. */
+ * record; width/height the frame size.  Any frame size: a tile grid too
+ * large for the shared-memory placement tables is placed in bands of tile
+ * rows (same lists). */
 int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int32_t *count,
                       const uint16_t *rect, const float *rec, int32_t ntx, int32_t nty,
                       int32_t width, int32_t height, int64_t pair_capacity,

@@ -437,7 +437,23 @@ struct PairCtx {
     int64_t n;
     int ntx, nty, ntiles;
     int64_t cap;
+    // tile-row band [ty_lo, ty_lo + bh) handled by this launch (frames whose
+    // per-warp difference arrays exceed shared memory are placed band by band);
+    // banded = false: the whole grid (bh = nty)
+    int ty_lo, bh;
+    bool banded;
 };
+
+// Clip a tile rectangle to the launch's band; rows become band-local.
+// Returns false when the rectangle misses the band.
+__device__ __forceinline__ bool band_clip(const PairCtx &C, ushort4 &rc) {
+    if (!C.banded) return true;
+    const int z = max((int)rc.z, C.ty_lo), w = min((int)rc.w, C.ty_lo + C.bh - 1);
+    if (z > w) return false;
+    rc.z = (unsigned short)(z - C.ty_lo);
+    rc.w = (unsigned short)(w - C.ty_lo);
+    return true;
+}
 
 // 2-D difference-array update for one tile rectangle (D is (nty+1) x (ntx+1)).
 __device__ __forceinline__ void diff_add(int *D, int w1, const ushort4 rc, int v) {
@@ -485,9 +501,14 @@ __device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, in
             sp = C.order[r];
             cnt = (uint32_t)C.count[sp];
             if (cnt) {
-                const ushort4 rc = C.rect[sp];
-                rx = (uint32_t)rc.x | ((uint32_t)rc.y << 16);
-                rz = (uint32_t)rc.z | ((uint32_t)rc.w << 16);
+                ushort4 rc = C.rect[sp];
+                if (band_clip(C, rc)) {
+                    cnt = (uint32_t)(rc.y - rc.x + 1) * (uint32_t)(rc.w - rc.z + 1);
+                    rx = (uint32_t)rc.x | ((uint32_t)rc.y << 16);
+                    rz = (uint32_t)rc.z | ((uint32_t)rc.w << 16);
+                } else {
+                    cnt = 0;
+                }
             }
         }
         uint32_t incl = cnt;
@@ -497,7 +518,10 @@ __device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, in
             if (lane >= o) incl += y;
         }
         const uint32_t G = __shfl_sync(0xffffffffu, incl, 31);
-        if (G == 0) break;  // invisible ranks (count 0) sort last: nothing further
+        if (G == 0) {
+            if (C.banded) continue;  // this group misses the band; later ones may not
+            break;                   // invisible ranks (count 0) sort last: nothing further
+        }
         const uint32_t excl = incl - cnt;
         for (uint32_t k0 = 0; k0 < G; k0 += 32) {
             const uint32_t k = k0 + lane;
@@ -521,7 +545,7 @@ __device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, in
             uint32_t qy = (uint32_t)((float)q * rw);
             if (qy * w > q) --qy;
             else if ((qy + 1) * w <= q) ++qy;
-            const int ty = ok ? (int)(ty0 + qy) : 0;
+            const int ty = ok ? (int)(ty0 + qy) + C.ty_lo : 0;  // global tile row
             const int tx = ok ? (int)(tx0 + (q - qy * w)) : 0;
             f(ok, o_sp, ok ? ty * C.ntx + tx : -1, tx, ty);
         }
@@ -533,7 +557,7 @@ __device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, in
 __global__ void __launch_bounds__(kThreads)
 pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
     extern __shared__ int smem_i32[];
-    const int w1 = C.ntx + 1, h1 = C.nty + 1;
+    const int w1 = C.ntx + 1, h1 = C.bh + 1;
     int *D = smem_i32;
     for (int i = threadIdx.x; i < w1 * h1; i += kThreads) D[i] = 0;
     __syncthreads();
@@ -542,12 +566,16 @@ pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
         const int64_t r = r0 + k;
         if (r >= C.n) break;
         const uint32_t sp = C.order[r];
-        if (C.count[sp] > 0) diff_add(D, w1, C.rect[sp], 1);
+        if (C.count[sp] > 0) {
+            ushort4 rc = C.rect[sp];
+            if (band_clip(C, rc)) diff_add(D, w1, rc, 1);
+        }
     }
     __syncthreads();
     prefix2d(D, w1, h1, threadIdx.x, kThreads, [] { __syncthreads(); });
-    for (int t = threadIdx.x; t < C.ntiles; t += kThreads)
-        hist[(int64_t)t * nblocks + blockIdx.x] = (uint32_t)D[(t / C.ntx) * w1 + t % C.ntx];
+    const int tb = C.ty_lo * C.ntx;  // first tile of the band
+    for (int t = threadIdx.x; t < C.ntx * C.bh; t += kThreads)
+        hist[(int64_t)(tb + t) * nblocks + blockIdx.x] = (uint32_t)D[(t / C.ntx) * w1 + t % C.ntx];
 }
 
 // tile_ranges = exclusive scan of tile totals (single block)
@@ -597,7 +625,7 @@ __global__ void __launch_bounds__(kThreads)
 pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *ranges,
                   int32_t *pair_splat, int W, int H) {
     extern __shared__ int smem_i32[];
-    const int w1 = C.ntx + 1, h1 = C.nty + 1, cells = w1 * h1;
+    const int w1 = C.ntx + 1, h1 = C.bh + 1, cells = w1 * h1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < kWarps * cells; i += kThreads) smem_i32[i] = 0;
     __syncthreads();
@@ -619,8 +647,12 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
 #pragma unroll
         for (int u = 0; u < kPer; ++u) cnts[u] = sps[u] != 0xffffffffu ? __ldg(C.count + sps[u]) : 0;
 #pragma unroll
-        for (int u = 0; u < kPer; ++u)
-            if (cnts[u] > 0) diff_add(Dw, w1, C.rect[sps[u]], 1);
+        for (int u = 0; u < kPer; ++u) {
+            if (cnts[u] > 0) {
+                ushort4 rc = C.rect[sps[u]];
+                if (band_clip(C, rc)) diff_add(Dw, w1, rc, 1);
+            }
+        }
     }
     __syncwarp();
     prefix2d(Dw, w1, h1, lane, 32, [] { __syncwarp(); });
@@ -628,8 +660,9 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
     // phase 2: exclusive scan across warps, per tile (block total <= 2048), and
     // the block's global base per tile (tile start + earlier blocks) in smem
     uint32_t *s_base = reinterpret_cast<uint32_t *>(smem_i32 + kWarps * cells);
-    for (int t = tid; t < C.ntiles; t += kThreads) {
-        const int cell = (t / C.ntx) * w1 + t % C.ntx;
+    const int tb = C.ty_lo * C.ntx;  // first tile of the band
+    for (int tl = tid; tl < C.ntx * C.bh; tl += kThreads) {
+        const int cell = (tl / C.ntx) * w1 + tl % C.ntx, t = tb + tl;
         int run = 0;
 #pragma unroll
         for (int w = 0; w < kWarps; ++w) {
@@ -643,7 +676,7 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
     // phase 3: expand once, place (and cull-flag) every pair
     expand_pairs(C, rb, re, [&](bool ok, uint32_t sp, int tile, int tx, int ty) {
         const uint32_t peers = __match_any_sync(0xffffffffu, tile);
-        const int cell = ty * w1 + tx;
+        const int cell = (ty - C.ty_lo) * w1 + tx;
         // the first lane of each equal-tile group advances the warp's running
         // count for that tile and shares the old value with its peers
         const int leader = __ffs(peers) - 1;
@@ -743,9 +776,13 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
                                  int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int32_t ntiles = ntx * nty;
-    // placement keeps 8 per-warp int32 difference arrays of (ntx+1)(nty+1) cells
-    // plus one table of per-tile block bases in smem
-    const bool fits = (int64_t)(ntx + 1) * (nty + 1) * 4 * (kWarps + 1) <= 220 * 1024;
+    // placement keeps 8 per-warp int32 difference arrays of (ntx+1)(rows+1)
+    // cells plus one table of per-tile block bases in smem: frames whose tile
+    // grid does not fit are placed in bands of `bh` tile rows
+    const int64_t max_cells = (int64_t)(220 * 1024) / (4 * (kWarps + 1));
+    int band_rows = (int)(max_cells / (ntx + 1)) - 1;
+    band_rows = band_rows > nty ? nty : band_rows;
+    const bool fits = band_rows >= 1;
     if (n < 0 || pair_capacity < 1 || ntx < 1 || nty < 1 || !fits || !tile_ranges ||
         !n_pairs || !pair_splat || !workspace || (rec && (width < 1 || height < 1))) {
         ivr::set_error("ivr_bin_sort: bad argument");
@@ -819,14 +856,19 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     C.nty = nty;
     C.ntiles = ntiles;
     C.cap = pair_capacity;
-    const size_t cells = (size_t)(ntx + 1) * (nty + 1);
+    C.banded = band_rows < nty;
+    const size_t cells = (size_t)(ntx + 1) * (band_rows + 1);
     const size_t sm_hist = 4 * cells;
     const size_t sm_place = 4 * (size_t)(kWarps + 1) * cells;
     if (sm_hist > 48 * 1024)
         cudaFuncSetAttribute(pair_hist_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_hist);
     if (sm_place > 48 * 1024)
         cudaFuncSetAttribute(pair_place_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_place);
-    pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
+    for (int y0 = 0; y0 < nty; y0 += band_rows) {  // one band unless the grid is too large
+        C.ty_lo = y0;
+        C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
+        pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
+    }
     if (nbp <= 2048)
         rowscan_warp_kernel<<<(ntiles + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kRowsPerBlock, 0, st>>>(
             phist, ntiles, nbp, ttot, nullptr);
@@ -834,7 +876,11 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
         rowscan_kernel<<<ntiles, 1024, 0, st>>>(phist, nbp, ttot, nullptr);
     tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges, (uint32_t)pair_capacity,
                                            n_pairs);
-    pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, nbp, tile_ranges, pair_splat,
-                                                       width, height);
+    for (int y0 = 0; y0 < nty; y0 += band_rows) {
+        C.ty_lo = y0;
+        C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
+        pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, nbp, tile_ranges, pair_splat,
+                                                           width, height);
+    }
     return ivr::check_launch("ivr_bin_sort");
 }
