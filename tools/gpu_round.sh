@@ -16,11 +16,12 @@ python - <<'PY'
 import csv, collections
 rows = [r for r in csv.reader(open("gpurun_out/prof/launches.csv")) if len(r) > 10]
 h = rows[0]
-ik, iv = h.index("Kernel Name"), h.index("Metric Value")
+ik, iv, iu = h.index("Kernel Name"), h.index("Metric Value"), h.index("Metric Unit")
+scale = {"nsecond": 1e-3, "usecond": 1.0, "msecond": 1e3}
 tot = collections.defaultdict(lambda: [0, 0.0])
 for r in rows[1:]:
     try:
-        v = float(r[iv].replace(",", ""))
+        v = float(r[iv].replace(",", "")) * scale.get(r[iu], 1e-3)
     except ValueError:
         continue
     t = tot[r[ik][:90]]
@@ -29,6 +30,6 @@ for r in rows[1:]:
 with open("gpurun_out/prof/r01_launch_list_bench.md", "w") as f:
     f.write("| kernel | launches | total us (ncu, serialised) |\n|---|---|---|\n")
     for k, (c, v) in sorted(tot.items(), key=lambda x: -x[1][1]):
-        f.write(f"| {k} | {c} | {v / 1e3:.1f} |\n")
+        f.write(f"| {k} | {c} | {v:.1f} |\n")
 PY
 ls -la gpurun_out/prof
