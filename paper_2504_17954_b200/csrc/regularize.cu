@@ -138,16 +138,33 @@ __global__ void __launch_bounds__(kThreads) mask_count_kernel(Args A) {
 
 __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.0 ? -1.0 : 0.0); }
 
+// The block's 256 consecutive pixels (their K-channel rows are contiguous) are
+// staged through shared memory in both directions: coalesced loads of the
+// rendered maps and coalesced stores of d_out, instead of K scattered 4-byte
+// accesses per pixel at a 4K-byte stride.
 __global__ void __launch_bounds__(kThreads) reg_grad_kernel(Args A) {
     __shared__ double s_red[kThreads / 32];
-    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    extern __shared__ float s_reg[];  // [kThreads * K] maps in, [kThreads * K] d_out
+    const int tid = threadIdx.x;
+    const int64_t p0 = (int64_t)blockIdx.x * kThreads;
+    const int64_t i = p0 + tid;
     const int64_t npx = (int64_t)A.H * A.W;
+    const int nloc = (int)(npx - p0 < kThreads ? npx - p0 : kThreads);
+    const int K = A.K, nflt = nloc * K;
+    float *s_in = s_reg, *s_out = s_reg + kThreads * K;
+    for (int q = tid; q < nflt; q += kThreads) {
+        s_in[q] = A.out[p0 * K + q];
+        s_out[q] = 0.0f;
+    }
+    __syncthreads();
     double l_normal = 0.0, l_offset = 0.0, l_bil = 0.0;
     if (i < npx) {
         const int y = (int)(i / A.W), x = (int)(i % A.W);
-        const float *o = A.out + i * A.K;
-        float *d = A.d_out + i * A.K;
-        for (int c = 0; c < A.K; ++c) d[c] = 0.0f;
+        const float *o = s_in + tid * K;
+        float *d = s_out + tid * K;
+        // x-neighbours from the staged rows when inside the block, else global
+        auto left = [&](int c) { return tid > 0 ? o[c - K] : A.out[(i - 1) * K + c]; };
+        auto right = [&](int c) { return tid + 1 < nloc ? o[K + c] : A.out[(i + 1) * K + c]; };
         if (A.d_rgba) {
             const double *g = A.d_rgba + 4 * i;
             d[A.c_color] = (float)g[0];
@@ -187,21 +204,23 @@ __global__ void __launch_bounds__(kThreads) reg_grad_kernel(Args A) {
                 const double k0 = (double)o[c];
                 double g = 0.0;
                 if (x + 1 < A.W) {
-                    const double gx = (double)o[A.K + c] - k0;
+                    const double gx = (double)right(c) - k0;
                     l_bil += fabs(gx) * w0;
                     g -= sgn(gx) * w0;
                 }
                 if (y + 1 < A.H) {
-                    const double gy = (double)o[(int64_t)A.W * A.K + c] - k0;
+                    const double gy = (double)A.out[(i + A.W) * K + c] - k0;
                     l_bil += fabs(gy) * w0;
                     g -= sgn(gy) * w0;
                 }
-                if (x > 0) g += sgn(k0 - (double)o[c - A.K]) * wl;
-                if (y > 0) g += sgn(k0 - (double)o[c - (int64_t)A.W * A.K]) * wu;
+                if (x > 0) g += sgn(k0 - (double)left(c)) * wl;
+                if (y > 0) g += sgn(k0 - (double)A.out[(i - A.W) * K + c]) * wu;
                 d[c] = (float)(A.w_bil * g);
             }
         }
     }
+    __syncthreads();
+    for (int q = tid; q < nflt; q += kThreads) A.d_out[p0 * K + q] = s_out[q];
     const double a = block_sum(l_normal, s_red);
     const double b = block_sum(l_offset, s_red);
     const double c = block_sum(l_bil, s_red);
@@ -288,7 +307,10 @@ extern "C" int ivr_regularize(const float *out, int32_t k, int32_t height, int32
     if (cudaMemsetAsync(A.mask_count, 0, sizeof(int), st) != cudaSuccess)
         return check_launch("ivr_regularize memset");
     if (w_normal > 0.0 || (w_bil > 0.0 && n_bil > 0)) mask_count_kernel<<<nb, kThreads, 0, st>>>(A);
-    reg_grad_kernel<<<nb, kThreads, 0, st>>>(A);
+    const size_t sm_grad = 2 * (size_t)kThreads * k * sizeof(float);
+    if (sm_grad > 48 * 1024)
+        cudaFuncSetAttribute(reg_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_grad);
+    reg_grad_kernel<<<nb, kThreads, sm_grad, st>>>(A);
     reg_finish_kernel<<<1, kThreads, 0, st>>>(A.part, nb, npx, terms);
     return check_launch("ivr_regularize");
 }
