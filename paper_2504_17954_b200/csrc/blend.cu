@@ -415,9 +415,17 @@ blend_fwd_kernel(BlendArgs A) {
             if (c < K) o[c] = exact_out ? st.acc64[c] : (double)st.acc[c];
     } else {
         float *o = A.out + pix * K;
+        if (K == KMAX && KMAX % 4 == 0) {  // 16-byte aligned rows: vector stores
 #pragma unroll
-        for (int c = 0; c < KMAX; ++c)
-            if (c < K) o[c] = st.acc[c];
+            for (int c4 = 0; c4 < KMAX / 4; ++c4)
+                reinterpret_cast<float4 *>(o)[c4] =
+                    make_float4(st.acc[4 * c4], st.acc[4 * c4 + 1], st.acc[4 * c4 + 2],
+                                st.acc[4 * c4 + 3]);
+        } else {
+#pragma unroll
+            for (int c = 0; c < KMAX; ++c)
+                if (c < K) o[c] = st.acc[c];
+        }
     }
     if (A.contrib) A.contrib[pix] = st.nc;
     if (A.last_pos) A.last_pos[pix] = st.last;
