@@ -15,6 +15,8 @@
 
 namespace ivr {
 
+constexpr int kK1Threads = 128;
+
 __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr_shading &S,
                                                int has_shading, const ivr_edits &E, int has_edits,
                                                const ivr_frame_params &P, const ivr_layout &L,
@@ -153,7 +155,7 @@ __device__ __forceinline__ void stage_params(const ivr_frame_params *src, ivr_fr
     __syncthreads();
 }
 
-__global__ void __launch_bounds__(256)
+__global__ void __launch_bounds__(kK1Threads)
 preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E, int has_edits,
                   ivr_frame_params Pv, const ivr_frame_params *__restrict__ Pd, ivr_layout L,
                   ivr_proj_out O, int f64_mode) {
@@ -276,7 +278,7 @@ extern "C" int ivr_preprocess_fwd(const ivr_gaussians *g, const ivr_shading *sha
     ivr_edits E{};
     if (shading) S = *shading;
     if (edits) E = *edits;
-    const int threads = 256;
+    const int threads = ivr::kK1Threads;
     const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
     ivr_frame_params P = ivr::params_from(*cam, shading, edits);
     ivr::preprocess_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
@@ -304,7 +306,7 @@ extern "C" int ivr_preprocess_fwd_params(const ivr_gaussians *g, const ivr_shadi
     ivr_edits E{};
     if (shading) S = *shading;
     if (edits) E = *edits;
-    const int threads = 256;
+    const int threads = ivr::kK1Threads;
     const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
     ivr_frame_params Pv{};
     Pv.cam.width = width;
