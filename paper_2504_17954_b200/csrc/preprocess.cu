@@ -15,7 +15,7 @@
 
 namespace ivr {
 
-constexpr int kK1Threads = 128;
+constexpr int kK1Threads = 64;
 
 __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr_shading &S,
                                                int has_shading, const ivr_edits &E, int has_edits,
