@@ -96,7 +96,20 @@ minmax_kernel(const uint64_t *keys, int64_t n, unsigned long long *mm /* [min, m
         lo = a < lo ? a : lo;
         hi = b > hi ? b : hi;
     }
+    // block reduction first: one atomic pair per block (per-warp atomics on
+    // the same two words serialise in L2)
+    __shared__ unsigned long long s_lo[kWarps], s_hi[kWarps];
+    const int warp = threadIdx.x >> 5;
     if ((threadIdx.x & 31) == 0) {
+        s_lo[warp] = lo;
+        s_hi[warp] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kWarps; ++w) {
+            lo = s_lo[w] < lo ? s_lo[w] : lo;
+            hi = s_hi[w] > hi ? s_hi[w] : hi;
+        }
         atomicMin(mm, lo);
         atomicMax(mm + 1, hi);
     }
