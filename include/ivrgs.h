@@ -283,7 +283,14 @@ typedef struct ivr_grads {
      * 2 d_log_s, 3 d_o_logit, 4 d_n_raw, 5 d_colors, 6 d_k_a_raw, 7 d_k_d_raw,
      * 8 d_k_s_raw, 9 d_log_beta, 10 d_delta_c / d_c_p */
     unsigned long long *bad;
+    /* optional (NULL = atomics): ivr_preprocess_bwd_scratch_len(n, per_scene)
+     * doubles for per-block partials of d_globals / d_c_p / d_scale, summed in
+     * a fixed order (no contended atomics; identical run to run); the sums are
+     * added to the outputs */
+    double *scratch;
+    int64_t scratch_len;
 } ivr_grads;
+int64_t ivr_preprocess_bwd_scratch_len(int64_t n, int32_t per_scene);
 
 /* K4b: per-Gaussian backward in float64: conic -> cov2d chain
  * (rasterizer.py:245-255), channel unpack (rasterizer.py:257-270),

@@ -85,7 +85,8 @@ class Grads_t(ctypes.Structure):
                 ("d_delta_c", P), ("d_k_a_raw", P), ("d_k_d_raw", P), ("d_k_s_raw", P),
                 ("d_log_beta", P), ("d_c_p", P), ("d_scale", P), ("d_globals", P),
                 ("per_scene", ctypes.c_int32), ("dl_dp", ctypes.c_double * 3),
-                ("dl_da", ctypes.c_double * 3), ("bad", P)]
+                ("dl_da", ctypes.c_double * 3), ("bad", P), ("scratch", P),
+                ("scratch_len", ctypes.c_int64)]
 
 
 class StepGrads_t(ctypes.Structure):
@@ -190,6 +191,7 @@ _SIGS = {
                        ctypes.c_double, ctypes.c_double, P], ctypes.c_int),
     "ivr_adam_step_sched": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
                              ctypes.c_double, ctypes.c_double, P, P, P], ctypes.c_int),
+    "ivr_preprocess_bwd_scratch_len": ([ctypes.c_int64, ctypes.c_int32], ctypes.c_int64),
     "ivr_stage2_attrs": ([ctypes.c_int64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
     "ivr_step_partials": ([ctypes.c_int64], ctypes.c_int32),
     "ivr_inverse_pack": ([ctypes.POINTER(InverseStep_t), P, ctypes.c_double, ctypes.c_double, P, P,

@@ -735,7 +735,7 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
             flag_bad(R.bad, i, 4, d_n_raw[k]);
         }
     }
-    {
+    if (R.d_globals || nsc > 0) {  // transform gradients requested (fits, shade_backward)
         const int lane = threadIdx.x & 31;
         const unsigned act = __ballot_sync(0xffffffffu, active);
         if (act) {
@@ -759,6 +759,13 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
         }
     }
     __syncthreads();
+    if (R.scratch) {  // per-block partials; bwd_sums_kernel adds them in a fixed order
+        const int nsl = 10 + 4 * nsc;
+        double *pb = R.scratch + (int64_t)blockIdx.x * nsl;
+        for (int k = threadIdx.x; k < nsl; k += blockDim.x)
+            pb[k] = k < 10 ? (B.has_shading ? s_glob[k] : 0.0) : s_scene[k - 10];
+        return;
+    }
     if (R.d_globals && B.has_shading && threadIdx.x < 10) atomicAdd(&R.d_globals[threadIdx.x], s_glob[threadIdx.x]);
     for (int k = threadIdx.x; k < 4 * nsc; k += blockDim.x) {
         const double v = s_scene[k];
@@ -767,6 +774,36 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
             if (R.d_scale) atomicAdd(&R.d_scale[k >> 2], v);
         } else if (R.d_c_p) {
             atomicAdd(&R.d_c_p[3 * (k >> 2) + (k & 3)], v);
+        }
+    }
+}
+
+// Fixed-order sums of K4b's per-block partials (one block per slot): the 10
+// global transform gradients and the per-scene d_c_p / d_scale, without
+// contended float64 atomics and identical run to run.
+__global__ void __launch_bounds__(256)
+bwd_sums_kernel(const double *part, int nblocks, int nsc, int has_globals, double *d_globals,
+                double *d_c_p, double *d_scale) {
+    __shared__ double s[256];
+    const int nsl = 10 + 4 * nsc, slot = blockIdx.x;
+    double t = 0.0;
+    for (int b = threadIdx.x; b < nblocks; b += 256) t += part[(int64_t)b * nsl + slot];
+    s[threadIdx.x] = t;
+    __syncthreads();
+    for (int h = 128; h > 0; h >>= 1) {
+        if (threadIdx.x < h) s[threadIdx.x] += s[threadIdx.x + h];
+        __syncthreads();
+    }
+    if (threadIdx.x != 0) return;
+    const double v = s[0];
+    if (slot < 10) {
+        if (d_globals && has_globals) d_globals[slot] += v;
+    } else {
+        const int k = slot - 10;
+        if ((k & 3) == 3) {
+            if (d_scale) d_scale[k >> 2] += v;
+        } else if (d_c_p) {
+            d_c_p[3 * (k >> 2) + (k & 3)] += v;
         }
     }
 }
@@ -869,6 +906,11 @@ extern "C" int ivr_blend_bwd_deterministic(
     return check_launch("bwd_reduce_det_kernel");
 }
 
+extern "C" int64_t ivr_preprocess_bwd_scratch_len(int64_t n, int32_t per_scene) {
+    if (n < 0 || per_scene < 0) return 0;
+    return ((n + 127) / 128) * (int64_t)(10 + 4 * per_scene);
+}
+
 extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *shading,
                                   const ivr_edits *edits, const ivr_frame_params *params,
                                   const ivr_camera *cam, const ivr_layout *layout, ivr_grads *grads,
@@ -880,6 +922,11 @@ extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *sha
         return IVR_ERR_ARG;
     }
     if (g->n == 0) return IVR_OK;
+    if (grads->scratch &&
+        grads->scratch_len < ivr_preprocess_bwd_scratch_len(g->n, grads->per_scene)) {
+        set_error("ivr_preprocess_bwd: scratch too small");
+        return IVR_ERR_ARG;
+    }
     BwdConst B{};
     B.G = *g;
     if (geometry) B.G.cache = nullptr;  // the geometry chain needs q, s, R (not cached)
@@ -905,5 +952,11 @@ extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *sha
         preprocess_bwd_kernel<true><<<blocks, threads, sm, (cudaStream_t)stream>>>(B, Pv, params);
     else
         preprocess_bwd_kernel<false><<<blocks, threads, sm, (cudaStream_t)stream>>>(B, Pv, params);
+    if (grads->scratch) {
+        const int nsl = 10 + 4 * grads->per_scene;
+        bwd_sums_kernel<<<nsl, 256, 0, (cudaStream_t)stream>>>(
+            grads->scratch, (int)blocks, grads->per_scene, shading ? 1 : 0, grads->d_globals,
+            grads->per_scene > 0 ? grads->d_c_p : nullptr, grads->d_scale);
+    }
     return check_launch("preprocess_bwd_kernel");
 }

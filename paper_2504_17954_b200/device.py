@@ -386,7 +386,7 @@ def preprocess_backward(dg: DeviceGaussians, cam, K, cols, g=None, shading=None,
         sizes.append(("d_c_p", (n if per_splat_c_p else max(per_scene, 1)) * 3))
     if "d_scale" in want:
         sizes.append(("d_scale", max(per_scene, 1)))
-    if shading is not None:
+    if shading is not None and "d_globals" in want:
         sizes.append(("d_globals", 10))
     arena = torch.zeros(sum(sz for _, sz in sizes), dtype=torch.float64, device=dev)
     o = 0
@@ -401,6 +401,11 @@ def preprocess_backward(dg: DeviceGaussians, cam, K, cols, g=None, shading=None,
             R.dl_dp[i], R.dl_da[i] = float(dp[i]), float(da[i])
     bad = torch.full((16,), -1, dtype=torch.int64, device=dev)  # ~0 as uint64
     R.bad = bad.data_ptr()
+    if "d_globals" in out or R.per_scene > 0:
+        # fixed-order sums of the transform gradients (no contended atomics)
+        ns = int(L.lib().ivr_preprocess_bwd_scratch_len(n, R.per_scene))
+        scratch = torch.empty(max(ns, 1), dtype=torch.float64, device=dev)
+        R.scratch, R.scratch_len = scratch.data_ptr(), ns  # stream-ordered reuse is safe
     lay = L.Layout_t()
     lay.k = K
     lay.col_color, lay.col_alpha, lay.col_depth, lay.col_normal = cols

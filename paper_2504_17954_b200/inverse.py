@@ -159,7 +159,7 @@ class InverseFitter:
         shading, edits = F._keep_tabs
         light = _light(self.scene, params)
         out, _ = D.preprocess_backward(self.ds.dg, cam, 4, (0, 3, -1, -1), g=g, shading=shading,
-                                       edits=edits, geometry=False, want=("d_c_p", "d_scale"),
+                                       edits=edits, geometry=False, want=("d_c_p", "d_scale", "d_globals"),
                                        per_scene=self.S, light=light)
         S = self.S
         sig = torch.from_numpy(_sigmoid(params.opacity_raw)).to(out["d_scale"].device)
@@ -302,7 +302,7 @@ class InverseGraph:
             g = D.blend_backward(F, d, geometry=False)
             out, _ = D.preprocess_backward(ds.dg, cam, 4, (0, 3, -1, -1), g=g, shading=self.shading,
                                            edits=self.edits, params_dev=pdev, geometry=False,
-                                           want=("d_c_p", "d_scale"), per_scene=self.S,
+                                           want=("d_c_p", "d_scale", "d_globals"), per_scene=self.S,
                                            light=self.light)
             L.check(L.lib().ivr_inverse_pack(
                 ctypes.byref(self.st), sums.data_ptr(), float(h * w * nc),

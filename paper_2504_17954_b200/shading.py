@@ -214,7 +214,7 @@ def shade_backward(cache, d_rgb):
                          cache["b"])
     d_rgb_dev = D.to_dev(np.asarray(d_rgb, dtype=np.float64).reshape(n, 3))
     want = ("d_mu", "d_n_raw", "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta",
-            "d_c_p")
+            "d_c_p", "d_globals")
     out, bad = D.preprocess_backward(dg, cache["cam"], 1, (-1, -1, -1, -1), shading=S,
                                      d_rgb=d_rgb_dev, geometry=False, want=want, per_scene=1,
                                      per_splat_c_p=cache["per_splat_palette"], light=light)

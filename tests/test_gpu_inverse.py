@@ -153,3 +153,17 @@ def test_inverse_graph_divergence_raises():
     bad[0, 0, 0] = np.nan
     with pytest.raises(DivergedLoss):
         optimize_to_reference(sc, p, [bad], cams, iters=3)
+
+
+def test_inverse_step_deterministic(monkeypatch):
+    """IVR_DETERMINISTIC=1: K4a's fixed-order reduction plus K4b's fixed-order
+    transform sums make the inverse gradient identical run to run."""
+    from paper_2504_17954_b200.inverse import init_transform, inverse_step
+    monkeypatch.setenv("IVR_DETERMINISTIC", "1")
+    d = golden("inverse")
+    sc = _scene(d)
+    l1, g1 = inverse_step(sc, init_transform(sc), _cam(d), d["reference"])
+    l2, g2 = inverse_step(sc, init_transform(sc), _cam(d), d["reference"])
+    assert l1 == l2
+    for k in g1:
+        assert np.array_equal(np.asarray(g1[k]), np.asarray(g2[k])), k
