@@ -34,7 +34,7 @@ namespace sortk {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 8;                  // per thread in radix passes
+constexpr int kItems = 16;                 // per thread in radix passes
 constexpr int kChunk = kThreads * kItems;  // 2048 keys per radix block
 constexpr int kRadix = 256;
 constexpr int kMaxRun = 64;
