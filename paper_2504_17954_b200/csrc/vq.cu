@@ -18,7 +18,8 @@ constexpr int kLut = 8192;         // uniform buckets over [mid_0, mid_last]
 
 __device__ __forceinline__ double vq_mid(const double *c, int i) { return 0.5 * (c[i + 1] + c[i]); }
 
-// lut[b] = number of midpoints < lo + b * w  (b < kLut); params = {lo, w, inv_w}
+// lut[b] = number of midpoints < lo + b * w  (b < kLut); params = {lo, w, inv_w,
+// float32 buckets safe}
 __global__ void __launch_bounds__(kVqThreads)
 vq_lut_kernel(const double *__restrict__ cents, int k, uint16_t *lut, double *params) {
     const int nm = k - 1;
@@ -28,6 +29,12 @@ vq_lut_kernel(const double *__restrict__ cents, int k, uint16_t *lut, double *pa
         params[0] = lo;
         params[1] = w;
         params[2] = w > 0.0 ? 1.0 / w : 0.0;
+        // 1 when the float32 bucket of any value inside [lo, hi] is within a
+        // quarter bucket of its true bucket (|v| 2^-23 relative rounding of v,
+        // lo and the product, over the bucket width): the [b-1, b+2) window
+        // then provably holds the answer and the edge checks can be skipped
+        const double mag = fmax(fabs(lo), fabs(hi));
+        params[3] = (w > 0.0 && mag * 4.0 * 1.1920928955078125e-07 + w * 1e-6 < 0.25 * w) ? 1.0 : 0.0;
     }
     const int b = blockIdx.x * kVqThreads + threadIdx.x;
     if (b >= kLut) return;
@@ -72,6 +79,7 @@ vq_assign_kernel(const double *__restrict__ values, int64_t n, const double *__r
     }
     const double lo = params[0], inv_w = params[2];
     const bool use_lut = SMEM && inv_w > 0.0;
+    const bool exact_buckets = params[3] != 0.0;
     // the bucket index only narrows the search (every answer is verified
     // against exact float64 compares), so it is computed in float32
     const float lo_f = (float)lo, inv_w_f = (float)inv_w;
@@ -105,9 +113,14 @@ vq_assign_kernel(const double *__restrict__ values, int64_t n, const double *__r
                         else z = m;
                     }
                     pos = a;
-                    const bool ok_lo = pos > a0 || a0 == 0 || s_mid[a0 - 1] < v[r];
-                    const bool ok_hi = pos < zi || zi == nm || !(s_mid[zi] < v[r]);
-                    if (!(ok_lo && ok_hi)) pos = vq_full_search(s_mid, nm, v[r]);
+                    // values outside [lo, hi] land in the clamped edge buckets,
+                    // whose windows end at 0 / nm: no check needed there either
+                    const bool inside = t >= 0.0f && t < (float)(kLut - 1);
+                    if (!(exact_buckets && inside)) {
+                        const bool ok_lo = pos > a0 || a0 == 0 || s_mid[a0 - 1] < v[r];
+                        const bool ok_hi = pos < zi || zi == nm || !(s_mid[zi] < v[r]);
+                        if (!(ok_lo && ok_hi)) pos = vq_full_search(s_mid, nm, v[r]);
+                    }
                 } else {
                     pos = vq_full_search(s_mid, nm, v[r]);
                 }
