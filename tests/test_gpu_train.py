@@ -184,3 +184,25 @@ def test_step_graph_recovers_from_pair_overflow():
     for k in ref.p:
         a, b = ref.p[k].cpu().numpy(), tr.p[k].cpu().numpy()
         assert np.linalg.norm(a - b) <= 1e-5 * max(np.linalg.norm(a), 1e-12), k
+
+
+def test_training_loop_graph_equals_eager(monkeypatch):
+    """_run_stage with the captured step (default) follows the eager loop
+    (IVR_TRAIN_GRAPH=0) through densify/prune recaptures."""
+    from paper_2504_17954_b200 import BasicSceneModel, LightConfig, ShColor, orbit_camera
+    from paper_2504_17954_b200.synthetic import editable_model
+    from paper_2504_17954_b200.trainer import TrainConfig, ViewDataset, render_model, train_editable
+    gt_model = editable_model(4, 1500, spread=0.5, density=1500)
+    light = LightConfig()
+    cams = [orbit_camera(np.zeros(3), 2.5, 0.3, az, 0.9, 40, 40) for az in (0.3, 1.9, 3.0)]
+    imgs = [render_model(gt_model, c, light, dtype=np.float64) for c in cams]
+    ed = editable_model(4, 1500, spread=0.5, density=1500)
+    base = BasicSceneModel("base", ed.geometry, sh=ShColor.from_dc(np.full((1500, 3), 0.5)))
+    cfg = TrainConfig(stage2_iters=60, log_interval=20, densify_interval=20)
+    _, log_g = train_editable(base, ViewDataset(cams, imgs, light), cfg)
+    monkeypatch.setenv("IVR_TRAIN_GRAPH", "0")
+    _, log_e = train_editable(base, ViewDataset(cams, imgs, light), cfg)
+    assert len(log_g) == len(log_e)
+    for a, b in zip(log_g, log_e):
+        assert abs(a["count"] - b["count"]) <= 0.02 * b["count"]
+        assert abs(a["loss"] - b["loss"]) <= 1e-3 * abs(b["loss"]) + 1e-9
