@@ -612,13 +612,16 @@ class StepGraph:
         # own workspace: eager renders between replays (holdout logging) must
         # never reallocate a buffer the graph captured
         self.ws = D.Workspace(dev)
-        self.params_dev = torch.empty(self.nb, dtype=torch.uint8, device=dev)
-        self.cam_dev = torch.empty(12, dtype=torch.float64, device=dev)
-        self.sched_dev = torch.empty(3 * G, dtype=torch.float64, device=dev)
+        # one device staging block (one H2D per step): frame params | camera
+        # block for the pseudo normals | Adam schedule
+        slot_bytes = self.nb + 12 * 8 + 3 * G * 8
+        self.stage_dev = torch.empty(slot_bytes, dtype=torch.uint8, device=dev)
+        self.params_dev = self.stage_dev[:self.nb]
+        self.cam_dev = self.stage_dev[self.nb:self.nb + 96].view(torch.float64)
+        self.sched_dev = self.stage_dev[self.nb + 96:].view(torch.float64)
         self.gt_dev = torch.empty((self.H, self.W, 4), dtype=torch.float64, device=dev)
         self.gate = torch.zeros(1, dtype=torch.int32, device=dev)
         self.stat_sum = torch.zeros(tr.n, dtype=torch.float64, device=dev)
-        slot_bytes = self.nb + 12 * 8 + 3 * G * 8
         self._pin = [torch.empty(slot_bytes, dtype=torch.uint8, pin_memory=True)
                      for _ in range(self.RING)]
         self._np = [torch.zeros(1, dtype=torch.int32, pin_memory=True) for _ in range(self.RING)]
@@ -646,9 +649,7 @@ class StepGraph:
         t_before = {n: tr.adam.state[n]["t"] for n in self.names}
         f[12:] = tr.adam.schedule([(n, tr.lr(n, it, iters, self.decay_extra)) for n in self.names])
         pin = self._pin[k]
-        self.params_dev.copy_(pin[:self.nb], non_blocking=True)
-        self.cam_dev.copy_(pin[self.nb:self.nb + 96].view(torch.float64), non_blocking=True)
-        self.sched_dev.copy_(pin[self.nb + 96:].view(torch.float64), non_blocking=True)
+        self.stage_dev.copy_(pin, non_blocking=True)
         self.gt_dev.copy_(gt, non_blocking=True)
         return k, t_before
 
