@@ -365,10 +365,13 @@ class FrameGraph:
         for k in range(self.slots):
             self.res.append({
                 "ws": ds.ws if k == 0 else D.Workspace(dev),
-                "d_params": torch.empty(nb, dtype=torch.uint8, device=dev),
-                "d_tab": torch.empty(4 * S, dtype=torch.float64, device=dev),
+                # one device block per slot (one H2D per frame): params | tables
+                "d_stage": torch.empty(nb + 8 * 4 * S, dtype=torch.uint8, device=dev),
                 "stream": torch.cuda.current_stream(dev) if k == 0 else torch.cuda.Stream(device=dev),
             })
+        for r in self.res:  # views of the slot's staging block
+            r["d_params"] = r["d_stage"][:nb]
+            r["d_tab"] = r["d_stage"][nb:].view(torch.float64)
         self.d_params, self.d_tab = self.res[0]["d_params"], self.res[0]["d_tab"]
         from .synthetic import bench_camera
         cam = warm_cam or bench_camera(self.W, self.H)
@@ -404,8 +407,7 @@ class FrameGraph:
         tab[3 * S:] = osc
         r = self.res[slot]
         with torch.cuda.stream(r["stream"]):
-            r["d_params"].copy_(h[:self.nb], non_blocking=True)
-            r["d_tab"].copy_(h[self.nb:].view(torch.float64), non_blocking=True)
+            r["d_stage"].copy_(h, non_blocking=True)
             ev = torch.cuda.Event()
             ev.record(r["stream"])
         self._ev[k] = ev
