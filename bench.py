@@ -268,9 +268,8 @@ def bench_inverse(scene, dist=None, world=1, rank=0):
     """C4: one inverse-exploration iteration on the composed 1M scene (render
     f64-semantics + loss + transform-only backward + Adam).  N ranks shard N
     views (one each); the packed transform gradient is all-reduced (NCCL,
-    31 float64) every iteration and every rank applies the same Adam."""
-    from paper_2504_17954_b200.inverse import (Adam, InverseFitter, init_transform, reduce_views,
-                                               transform_step)
+    4S+12 float64) every iteration and every rank applies the same Adam."""
+    from paper_2504_17954_b200.inverse import InverseFitter, InverseGraph, init_transform
     from paper_2504_17954_b200.synthetic import bench_camera
     cam = bench_camera(W_IMG, H_IMG, 0.8 + 0.7 * rank)
     p_true = init_transform(scene)
@@ -279,27 +278,19 @@ def bench_inverse(scene, dist=None, world=1, rank=0):
     ref = fit0.render(p_true, cam).out64.clone()
     fit = InverseFitter(scene, [ref], [cam], ds=fit0.ds)
     params = init_transform(scene)
-    adam = Adam(eps=1e-15)
-    angles = np.array([params.polar, params.azimuth])
-
-    def step():
-        loss, packed = fit.view_grads(params, 0)
-        mean, lv = reduce_views(packed, loss.reshape(1), float(world), dist=dist)
-        transform_step(params, fit.unpack(mean), adam, 0.01,
-                       ("c_p", "opacity_raw", "lam", "b", "angles"), angles)
-    note = "includes the per-iteration pair-count sync and host Adam on 30 floats"
-    if dist is None:
-        # one process: the product path replays whole iterations as a CUDA graph
-        # (device Adam + table refresh, no host round trip per iteration)
-        from paper_2504_17954_b200.inverse import InverseGraph
-        step = InverseGraph(fit, params, 100_000).replay
-        note = "whole iterations replayed as one CUDA graph (InverseGraph: device Adam)"
+    # the product path: whole iterations replayed as CUDA graphs (InverseGraph:
+    # device Adam + table refresh, no host round trip); with N ranks one
+    # stream-ordered NCCL all-reduce of the packed gradient per iteration
+    step = InverseGraph(fit, params, 100_000, dist=dist, view_div=float(world)).replay
+    note = ("whole iterations replayed as CUDA graphs (InverseGraph: device Adam)" +
+            ("; views sharded, one NCCL all-reduce per iteration between the compute "
+             "and update graphs" if dist is not None else ""))
     mean_ms, med_ms = _device_time(step, 10)
     mean_ms = _max_over_ranks(mean_ms, dist)
     return {"metric": "inverse exploration it/s (composed 1M, 800x800, 1 view per GPU)",
             "value": 1000.0 / mean_ms, "unit": "it/s", "views_per_s": world * 1000.0 / mean_ms,
             "ms_per_it": mean_ms, "ms_per_it_median": med_ms, "n_gpus": world,
-            "scaling": "weak (views sharded, one NCCL all-reduce of 31 float64 per iteration)",
+            "scaling": "weak (views sharded, one NCCL all-reduce of 4S+12 float64 per iteration)",
             "note": note}
 
 

@@ -283,10 +283,10 @@ typedef struct ivr_grads {
      * 2 d_log_s, 3 d_o_logit, 4 d_n_raw, 5 d_colors, 6 d_k_a_raw, 7 d_k_d_raw,
      * 8 d_k_s_raw, 9 d_log_beta, 10 d_delta_c / d_c_p */
     unsigned long long *bad;
-    /* optional (NULL = atomics): ivr_preprocess_bwd_scratch_len(n, per_scene)
-     * doubles for per-block partials of d_globals / d_c_p / d_scale, summed in
-     * a fixed order (no contended atomics; identical run to run); the sums are
-     * added to the outputs */
+    /* optional (NULL = global atomics): ivr_preprocess_bwd_scratch_len(n,
+     * per_scene) doubles for per-block partials of d_globals / d_c_p /
+     * d_scale, summed across blocks in a fixed order and added to the outputs
+     * (used by the deterministic mode) */
     double *scratch;
     int64_t scratch_len;
 } ivr_grads;
@@ -490,7 +490,9 @@ int ivr_loss_finalize(const ivr_loss_terms *t, double *loss, int64_t *state, dou
  * that complete iterations replay as a CUDA graph.  x = [c_p (3S),
  * opacity_raw (S), lam (4), b (4), polar, azimuth]; m, v its Adam moments;
  * t the per-group step counts (c_p, opacity_raw, lam, b, angles); grad and
- * loss_sum accumulate over the views of one iteration (ivr_inverse_pack) and
+ * loss_sum[0..1] (loss, pair-overflow count) accumulate over the views of one
+ * iteration (ivr_inverse_pack; with sharded views the caller all-reduces
+ * grad..loss_sum[1], contiguous) and
  * are consumed + cleared by ivr_inverse_update, which records losses[iter],
  * applies Adam per learnable group (bit q of `learnable`) whose mean
  * gradient exceeds 1e-12, and refreshes tab (palettes (3S), opacity scales
@@ -503,6 +505,7 @@ int ivr_loss_finalize(const ivr_loss_terms *t, double *loss, int64_t *state, dou
 typedef struct ivr_inverse_step {
     int32_t n_scenes, n_views, orbital, learnable;
     int64_t iters;
+    double view_div; /* views over all ranks (mean divisor); <= 0: n_views */
     double *x, *m, *v;
     int64_t *t;
     double lr, beta1, beta2, eps;

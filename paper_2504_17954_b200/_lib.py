@@ -112,7 +112,8 @@ class LossTerms_t(ctypes.Structure):
 class InverseStep_t(ctypes.Structure):
     _fields_ = [("n_scenes", ctypes.c_int32), ("n_views", ctypes.c_int32),
                 ("orbital", ctypes.c_int32), ("learnable", ctypes.c_int32),
-                ("iters", ctypes.c_int64), ("x", P), ("m", P), ("v", P), ("t", P),
+                ("iters", ctypes.c_int64), ("view_div", ctypes.c_double), ("x", P), ("m", P),
+                ("v", P), ("t", P),
                 ("lr", ctypes.c_double), ("beta1", ctypes.c_double), ("beta2", ctypes.c_double),
                 ("eps", ctypes.c_double), ("grad", P), ("loss_sum", P), ("losses", P),
                 ("ctl", P), ("params", P), ("tab", P)]

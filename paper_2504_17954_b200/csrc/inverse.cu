@@ -49,7 +49,9 @@ pack_kernel(ivr_inverse_step A, const double *photo_sums, double numel, double w
         const double l1 = dmul(0.8, ddiv(photo_sums[1], numel));
         const double loss = dadd(l1, dmul(0.2, dsub(1.0, ddiv(photo_sums[0], windows))));
         *A.loss_sum = dadd(*A.loss_sum, loss);
-        if ((int64_t)*n_pairs > capacity) A.ctl[2] |= IVR_INV_OVERFLOW;
+        // overflow count next to the loss: all-reduced with the gradient when
+        // views are sharded, so every rank gates the same iterations
+        if ((int64_t)*n_pairs > capacity) A.loss_sum[1] = dadd(A.loss_sum[1], 1.0);
     }
 }
 
@@ -64,7 +66,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(ivr_inverse_step A) {
     __shared__ double s_max[5][kThreads / 32];
     __shared__ double s_bc[5][2];  // per group: 1 - beta^t (0 = group not stepped)
     __shared__ int s_gate, s_rescale;
-    const double nv = (double)A.n_views;
+    const double nv = A.view_div > 0.0 ? A.view_div : (double)A.n_views;
     // groups: c_p, opacity_raw, lam, b, angles (inverse.py:229-238)
     auto group = [S](int j) {
         return j < 3 * S ? 0 : (j < 4 * S ? 1 : (j < 4 * S + 4 ? 2 : (j < 4 * S + 8 ? 3 : 4)));
@@ -92,6 +94,7 @@ __global__ void __launch_bounds__(kThreads) update_kernel(ivr_inverse_step A) {
         const int64_t it = ctl[0];
         const double loss = ddiv(*A.loss_sum, nv);
         bool gate = ctl[1] >= 0;
+        if (A.loss_sum[1] > 0.0) ctl[2] |= IVR_INV_OVERFLOW;
         if (!gate) {
             if (!isfinite(loss)) ctl[2] |= IVR_INV_DIVERGED;
             if (ctl[2] != 0) {
@@ -112,7 +115,8 @@ __global__ void __launch_bounds__(kThreads) update_kernel(ivr_inverse_step A) {
         }
         s_gate = gate ? 1 : 0;
         ctl[0] = it + 1;
-        *A.loss_sum = 0.0;
+        A.loss_sum[0] = 0.0;
+        A.loss_sum[1] = 0.0;
     }
     __syncthreads();
     if (s_gate) {

@@ -401,8 +401,9 @@ def preprocess_backward(dg: DeviceGaussians, cam, K, cols, g=None, shading=None,
             R.dl_dp[i], R.dl_da[i] = float(dp[i]), float(da[i])
     bad = torch.full((16,), -1, dtype=torch.int64, device=dev)  # ~0 as uint64
     R.bad = bad.data_ptr()
-    if "d_globals" in out or R.per_scene > 0:
-        # fixed-order sums of the transform gradients (no contended atomics)
+    if ("d_globals" in out or R.per_scene > 0) and \
+            os.environ.get("IVR_DETERMINISTIC", "0") == "1":
+        # fixed-order sums of the per-block transform-gradient partials
         ns = int(L.lib().ivr_preprocess_bwd_scratch_len(n, R.per_scene))
         scratch = torch.empty(max(ns, 1), dtype=torch.float64, device=dev)
         R.scratch, R.scratch_len = scratch.data_ptr(), ns  # stream-ordered reuse is safe

@@ -19,6 +19,7 @@ from __future__ import annotations
 
 import ctypes
 import hashlib
+import os
 from dataclasses import dataclass
 
 import numpy as np
@@ -228,11 +229,19 @@ class InverseGraph:
     (x, Adam moments, per-group step counts) and the frame tables live in HBM,
     so an iteration needs no host round trip; ``run`` replays and checks the
     sticky overflow / divergence gate once at the end (growing the pair
-    capacity and resuming from the first gated iteration if needed)."""
+    capacity and resuming from the first gated iteration if needed).
 
-    def __init__(self, fit, params, iters, lr=0.01, learnable=None, headroom=1.3):
+    With ``dist`` (views sharded over ranks) an iteration is two graphs: the
+    views' compute + pack, then -- after one stream-ordered all-reduce of the
+    packed gradient, loss and overflow count (4S+12 float64) -- the update,
+    so every rank applies the identical step and gates the same iterations;
+    ``view_div`` is the global view count."""
+
+    def __init__(self, fit, params, iters, lr=0.01, learnable=None, headroom=1.3, dist=None,
+                 group=None, view_div=None):
         from . import _lib as L
         self.fit, self.L = fit, L
+        self.dist, self.group = dist, group
         ds = fit.ds
         dev = ds.dg.device
         S, V = fit.S, len(fit.cams)
@@ -249,7 +258,7 @@ class InverseGraph:
         self.x = torch.from_numpy(x0).to(dev)
         self.m, self.v = torch.zeros(N, **f64), torch.zeros(N, **f64)
         self.t = torch.zeros(5, dtype=torch.int64, device=dev)
-        self.acc = torch.zeros(N + 1, **f64)  # grad (N) + loss sum
+        self.acc = torch.zeros(N + 2, **f64)  # grad (N), loss sum, overflow count
         self.losses = torch.zeros(self.iters, **f64)
         self.ctl = torch.tensor([0, -1, 0], dtype=torch.int64, device=dev)
         self.nb = nb = ctypes.sizeof(L.FrameParams_t)
@@ -267,6 +276,7 @@ class InverseGraph:
         st.orbital = 1 if self.orbital else 0
         st.learnable = sum(_LEARN_BITS[k] for k in learnable)
         st.iters = self.iters
+        st.view_div = float(view_div) if view_div else 0.0
         st.x, st.m, st.v, st.t = (self.x.data_ptr(), self.m.data_ptr(), self.v.data_ptr(),
                                   self.t.data_ptr())
         st.lr, st.beta1, st.beta2, st.eps = float(lr), 0.9, 0.999, 1e-15
@@ -287,7 +297,8 @@ class InverseGraph:
         self.capacity = max(int(peak * headroom) + 4096, 1 << 16)
         self._capture()
 
-    def _iteration(self):
+    def _views(self):
+        """Every view: render, loss, backward, pack into self.acc."""
         L, fit, ds = self.L, self.fit, self.fit.ds
         ws = ds.ws
         for v, cam in enumerate(fit.cams):
@@ -309,32 +320,55 @@ class InverseGraph:
                 float((h - win + 1) * (w - win + 1) * nc), out["d_c_p"].data_ptr(),
                 out["d_scale"].data_ptr(), out["d_globals"].data_ptr(), F.n_pairs.data_ptr(),
                 self.capacity, D.stream_handle()), "ivr_inverse_pack")
+
+    def _update(self):
+        L = self.L
         L.check(L.lib().ivr_inverse_update(ctypes.byref(self.st), D.stream_handle()),
                 "ivr_inverse_update")
+
+    def _reduce(self):
+        """Sum the packed gradient, loss and overflow count over the ranks
+        (stream-ordered, no host synchronisation)."""
+        if self.dist is not None:
+            self.dist.all_reduce(self.acc, group=self.group)
 
     def _capture(self):
         saved = [t.clone() for t in (self.x, self.m, self.v, self.t, self.acc, self.losses,
                                      self.ctl, self.params_dev, self.tab)]
-        self._iteration()  # sizes every workspace buffer before capture
+        self._views()  # sizes every workspace buffer before capture
+        self._reduce()
+        self._update()
         torch.cuda.synchronize()
         for t, s0 in zip((self.x, self.m, self.v, self.t, self.acc, self.losses, self.ctl,
                           self.params_dev, self.tab), saved):
             t.copy_(s0)
         torch.cuda.synchronize()
         self.g = torch.cuda.CUDAGraph()
-        with torch.cuda.graph(self.g):
-            self._iteration()
+        if self.dist is None:
+            with torch.cuda.graph(self.g):
+                self._views()
+                self._update()
+        else:  # the collective stays outside the graphs
+            self.g2 = torch.cuda.CUDAGraph()
+            with torch.cuda.graph(self.g):
+                self._views()
+            with torch.cuda.graph(self.g2):
+                self._update()
         torch.cuda.synchronize()
 
     def replay(self):
+        """One iteration."""
         self.g.replay()
+        if self.dist is not None:
+            self._reduce()
+            self.g2.replay()
 
     def run(self):
         """All iterations; returns (TransformParams fields as numpy, losses)."""
         start = 0
         while True:
             for _ in range(self.iters - start):
-                self.g.replay()
+                self.replay()
             ctl = self.ctl.cpu().numpy()
             first, reason = int(ctl[1]), int(ctl[2])
             if first < 0:
@@ -374,9 +408,12 @@ def optimize_to_reference(scene, params, reference_rgba, reference_cam, iters=10
     if dist:
         dist.all_reduce(n_views, group=group)
     n_views = float(n_views.item())
-    if dist is None and callback is None and iters > 0 and fit.cams:
-        # one process: whole iterations replay as a CUDA graph (no host round trip)
-        G = InverseGraph(fit, params, iters, lr, learnable)
+    use_graph = os.environ.get("IVR_INVERSE_GRAPH", "1") != "0"
+    if use_graph and callback is None and iters > 0 and fit.cams:
+        # whole iterations replay as CUDA graphs (no host round trip); sharded
+        # views add one stream-ordered all-reduce per iteration
+        G = InverseGraph(fit, params, iters, lr, learnable, dist=dist, group=group,
+                         view_div=n_views)
         x, losses = G.run()
         S = fit.S
         params.c_p = x[:3 * S].reshape(S, 3).copy()
