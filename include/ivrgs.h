@@ -263,6 +263,18 @@ int ivr_blend_bwd_deterministic(const int32_t *tile_ranges, const int32_t *pair_
                                 float *g_conic, float *g_opacity, const int32_t *tile_order,
                                 int32_t flags, ivr_stream_t stream);
 
+/* K4a per list entry (the reference's composite_backward outputs,
+ * _kernels.py:75-135): pair_grads (n_pairs, k+6) float32 = [d values (k),
+ * d mean2d (2), d conic (3: a/2-, b-, c/2-weighted as the reference), d
+ * opacity] per pair_splat entry, each the fixed-order sum of the walk's
+ * warp partials.  workspace: ivr_blend_bwd_det_workspace_size(n_pairs, k). */
+int ivr_blend_bwd_pairs(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
+                        int32_t nty, const float *rec, const float *values, const double *rec64,
+                        int32_t k, int32_t width, int32_t height, const float *out,
+                        const int32_t *last_pos, const float *d_out, int64_t n_pairs,
+                        void *workspace, size_t workspace_bytes, float *pair_grads,
+                        ivr_stream_t stream);
+
 /* Per-Gaussian backward outputs (float64, NULL = not wanted). */
 typedef struct ivr_grads {
     /* inputs: K4a accumulators (float32, NULL if none) and an optional extra
@@ -336,6 +348,11 @@ int ivr_concat(const double *const *srcs, const int64_t *rows, int32_t n_src, in
 /* Stage-1 colour: eval_sh(ShColor, view_dirs(mu, cam_pos))
  * (gaussians.py:497-508, 521-524).  coeffs (n, (degree+1)^2, 3) float64,
  * degree 0..3; rgb (n,3) = max(sum_b basis_b * coeffs_b + 0.5, 0). */
+/* gaussians.sh_basis (gaussians.py:429-494) on unit directions (n,3):
+ * basis (n,(degree+1)^2) and, when dbasis != NULL, its derivatives
+ * (n,(degree+1)^2,3). */
+int ivr_sh_basis(int64_t n, int32_t degree, const double *dirs, double *basis, double *dbasis,
+                 ivr_stream_t stream);
 int ivr_sh_eval(int64_t n, int32_t degree, const double *mu, const double *coeffs,
                 const double cam_pos[3], double *rgb, ivr_stream_t stream);
 

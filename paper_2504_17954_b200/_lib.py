@@ -151,6 +151,9 @@ _SIGS = {
                                      ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int64, P, P,
                                      P, ctypes.c_int64, P, ctypes.c_size_t, P, P, P, P, P,
                                      ctypes.c_int32, P], ctypes.c_int),
+    "ivr_blend_bwd_pairs": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
+                             ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int64, P,
+                             ctypes.c_size_t, P, P], ctypes.c_int),
     "ivr_blend_bwd": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
                        ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, P, P, ctypes.c_int32, P],
                       ctypes.c_int),
@@ -193,6 +196,7 @@ _SIGS = {
     "ivr_adam_step_sched": ([ctypes.POINTER(AdamGroup_t), ctypes.c_int32, ctypes.c_double,
                              ctypes.c_double, ctypes.c_double, P, P, P], ctypes.c_int),
     "ivr_preprocess_bwd_scratch_len": ([ctypes.c_int64, ctypes.c_int32], ctypes.c_int64),
+    "ivr_sh_basis": ([ctypes.c_int64, ctypes.c_int32, P, P, P, P], ctypes.c_int),
     "ivr_stage2_attrs": ([ctypes.c_int64, P, P, P, P, P, P, P, P, P], ctypes.c_int),
     "ivr_step_partials": ([ctypes.c_int64], ctypes.c_int32),
     "ivr_inverse_pack": ([ctypes.POINTER(InverseStep_t), P, ctypes.c_double, ctypes.c_double, P, P,

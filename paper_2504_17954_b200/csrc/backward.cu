@@ -906,6 +906,52 @@ extern "C" int ivr_blend_bwd_deterministic(
     return check_launch("bwd_reduce_det_kernel");
 }
 
+// per-pair gradients (the reference's composite_backward outputs): the 8
+// warp partials of each list entry summed in warp order
+__global__ void __launch_bounds__(256)
+pair_sum_kernel(const float *part, int64_t npairs, int stride, float *pair_out) {
+    const int64_t q = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    if (q >= npairs * stride) return;
+    const int64_t j = q / stride, c = q % stride;
+    float t = 0.0f;
+    constexpr int kW = ivr::kBwdThreads / 32;
+    for (int w = 0; w < kW; ++w) t += part[(j * kW + w) * stride + c];
+    pair_out[q] = t;
+}
+
+extern "C" int ivr_blend_bwd_pairs(const int32_t *tile_ranges, const int32_t *pair_splat,
+                                   int32_t ntx, int32_t nty, const float *rec,
+                                   const float *values, const double *rec64, int32_t k,
+                                   int32_t width, int32_t height, const float *out,
+                                   const int32_t *last_pos, const float *d_out, int64_t n_pairs,
+                                   void *workspace, size_t workspace_bytes, float *pair_grads,
+                                   ivr_stream_t stream) {
+    using namespace ivr;
+    const size_t need = ivr_blend_bwd_det_workspace_size(n_pairs, k);
+    if (n_pairs < 0 || n_pairs > 0x7fffffffll || !pair_grads || !workspace ||
+        workspace_bytes < need) {
+        set_error("ivr_blend_bwd_pairs: bad argument or workspace too small");
+        return IVR_ERR_ARG;
+    }
+    if (n_pairs == 0) return IVR_OK;
+    cudaStream_t st = (cudaStream_t)stream;
+    if (cudaMemsetAsync(workspace, 0, need, st) != cudaSuccess) {
+        set_error("ivr_blend_bwd_pairs: memset failed");
+        return IVR_ERR_CUDA;
+    }
+    // the walk only writes the partials in this mode; the per-Gaussian
+    // accumulator arguments are never touched (any valid pointer passes)
+    const int rc = blend_bwd_impl(tile_ranges, pair_splat, ntx, nty, rec, values, rec64, k,
+                                  width, height, out, last_pos, d_out, pair_grads, pair_grads,
+                                  pair_grads, pair_grads, nullptr, 0, (float *)workspace, stream);
+    if (rc != IVR_OK) return rc;
+    const int stride = k + 6;
+    const int64_t tot = n_pairs * stride;
+    pair_sum_kernel<<<(unsigned)((tot + 255) / 256), 256, 0, st>>>((const float *)workspace,
+                                                                   n_pairs, stride, pair_grads);
+    return check_launch("pair_sum_kernel");
+}
+
 extern "C" int64_t ivr_preprocess_bwd_scratch_len(int64_t n, int32_t per_scene) {
     if (n < 0 || per_scene < 0) return 0;
     return ((n + 127) / 128) * (int64_t)(10 + 4 * per_scene);

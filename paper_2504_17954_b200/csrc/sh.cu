@@ -165,6 +165,23 @@ __global__ void __launch_bounds__(128) sh_bwd_kernel(ShArgs A) {
     }
 }
 
+// sh_basis as an array function: basis (n, NB) and its direction
+// derivatives (n, NB, 3) for given unit directions (gaussians.py:429-494)
+template <int DEG>
+__global__ void __launch_bounds__(128)
+sh_basis_kernel(int64_t n, const double *dirs, double *basis, double *dbasis) {
+    constexpr int NB = (DEG + 1) * (DEG + 1);
+    const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    if (i >= n) return;
+    double B[NB], D[NB][3];
+    sh_basis<DEG>(dirs[3 * i], dirs[3 * i + 1], dirs[3 * i + 2], B, D);
+    for (int b = 0; b < NB; ++b) {
+        basis[(int64_t)NB * i + b] = B[b];
+        if (dbasis)
+            for (int k = 0; k < 3; ++k) dbasis[((int64_t)NB * i + b) * 3 + k] = D[b][k];
+    }
+}
+
 static int sh_launch(bool bwd, int degree, const ShArgs &A, cudaStream_t st) {
     const int blocks = (int)((A.n + 127) / 128);
 #define IVR_SH_CASE(DG)                                                          \
@@ -220,4 +237,23 @@ extern "C" int ivr_sh_bwd(int64_t n, int32_t degree, const double *mu, const dou
     A.d_coeffs = d_coeffs;
     A.d_mu = d_mu;
     return sh_launch(true, degree, A, (cudaStream_t)stream);
+}
+
+extern "C" int ivr_sh_basis(int64_t n, int32_t degree, const double *dirs, double *basis,
+                            double *dbasis, ivr_stream_t stream) {
+    using namespace ivr;
+    if (n < 0 || degree < 0 || degree > 3 || (n > 0 && (!dirs || !basis))) {
+        set_error("ivr_sh_basis: bad argument (degree must be 0..3)");
+        return IVR_ERR_ARG;
+    }
+    if (n == 0) return IVR_OK;
+    const int blocks = (int)((n + 127) / 128);
+    cudaStream_t st = (cudaStream_t)stream;
+    switch (degree) {
+        case 0: sh_basis_kernel<0><<<blocks, 128, 0, st>>>(n, dirs, basis, dbasis); break;
+        case 1: sh_basis_kernel<1><<<blocks, 128, 0, st>>>(n, dirs, basis, dbasis); break;
+        case 2: sh_basis_kernel<2><<<blocks, 128, 0, st>>>(n, dirs, basis, dbasis); break;
+        default: sh_basis_kernel<3><<<blocks, 128, 0, st>>>(n, dirs, basis, dbasis); break;
+    }
+    return check_launch("sh_basis_kernel");
 }

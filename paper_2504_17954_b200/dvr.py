@@ -173,6 +173,21 @@ class Material:
     beta: float = 16.0
 
 
+def shade_sample(c_v, n, l, v, k_a, k_d, k_s, beta):
+    """Blinn-Phong colour of one shaded sample (dvr.py:216-232), the formula
+    K13 evaluates per sample: ambient + diffuse |n.l| + white specular
+    |n.h|^beta (h = normalized v + l when |v + l| > 1e-12)."""
+    h = np.asarray(v, np.float64) + np.asarray(l, np.float64)
+    hn = float(np.sqrt(np.dot(h, h)))
+    if hn > 1e-12:
+        h = h / hn
+    ndl = abs(float(np.dot(n, l)))
+    ndh = abs(float(np.dot(n, h)))
+    spec = k_s * ndh ** beta if (ndl > 0.0 and ndh > 0.0) else 0.0
+    c = np.asarray(c_v, np.float64)
+    return k_a * c + k_d * c * ndl + spec
+
+
 def render_view_device(volume, tf, cam, light, material=None, step_scale=0.5, dev_values=None):
     """Ray-march one camera on the GPU; returns the (H, W, 4) float64 device
     tensor (premultiplied colour, resolved alpha)."""

@@ -188,7 +188,9 @@ def project_gaussians(geom, cam, near=NEAR_PLANE):
     if near != NEAR_PLANE:
         raise ValueError("the GPU projection uses the reference near plane 0.01")
     from .rasterizer import _project_only
-    return _project_only(geom, cam)
+    out = _project_only(geom, cam)
+    out["geom"], out["cam"] = geom, cam  # what project_backward needs
+    return out
 
 
 def project_gaussian(geom, cam, index=0):
@@ -204,3 +206,154 @@ def project_gaussian(geom, cam, index=0):
 def view_dirs(mu, cam_position):
     """Unit directions from the camera to each primitive."""
     return _unit_rows(mu - np.asarray(cam_position)[None, :], eps=1e-12)
+
+
+# ---------------------------------------------------------------------------
+# per-Gaussian building blocks of the projection / colour (gaussians.py:222-289,
+# 349-400, 429-529) as array functions.  The render and training paths run
+# them fused inside K1 / K4b / K8; these entry points evaluate the same
+# expressions batched on the GPU (torch float64) for API compatibility.
+
+def _dev(x):
+    from . import device as D
+    return D.to_dev(np.ascontiguousarray(np.asarray(x, dtype=np.float64)))
+
+
+def _rot_t(q):
+    w, x, y, z = q.unbind(1)
+    return __import__("torch").stack([
+        1 - 2 * (y * y + z * z), 2 * (x * y - w * z), 2 * (x * z + w * y),
+        2 * (x * y + w * z), 1 - 2 * (x * x + z * z), 2 * (y * z - w * x),
+        2 * (x * z - w * y), 2 * (y * z + w * x), 1 - 2 * (x * x + y * y)], 1).view(-1, 3, 3)
+
+
+def _rot_backward_t(q, g):
+    import torch
+    w, x, y, z = q.unbind(1)
+    G = lambda r, c: g[:, r, c]  # noqa: E731
+    dw = 2 * (-z * G(0, 1) + y * G(0, 2) + z * G(1, 0) - x * G(1, 2) - y * G(2, 0) + x * G(2, 1))
+    dx = 2 * (y * G(0, 1) + z * G(0, 2) + y * G(1, 0) - 2 * x * G(1, 1) - w * G(1, 2)
+              + z * G(2, 0) + w * G(2, 1) - 2 * x * G(2, 2))
+    dy = 2 * (-2 * y * G(0, 0) + x * G(0, 1) + w * G(0, 2) + x * G(1, 0) + z * G(1, 2)
+              - w * G(2, 0) + z * G(2, 1) - 2 * y * G(2, 2))
+    dz = 2 * (-2 * z * G(0, 0) - w * G(0, 1) + x * G(0, 2) + w * G(1, 0) - 2 * z * G(1, 1)
+              + y * G(1, 2) + x * G(2, 0) + y * G(2, 1))
+    return torch.stack([dw, dx, dy, dz], 1)
+
+
+def quat_to_rot(q):
+    """Unit quaternions (N,4) w-first -> rotations (N,3,3) (gaussians.py:222-236)."""
+    return _rot_t(_dev(np.atleast_2d(q))).cpu().numpy()
+
+
+def quat_to_rot_backward(q, dR):
+    """d/dq of quat_to_rot for the upstream dR (N,3,3) (gaussians.py:239-264)."""
+    return _rot_backward_t(_dev(np.atleast_2d(q)), _dev(dR).view(-1, 3, 3)).cpu().numpy()
+
+
+def build_covariance(q, s):
+    """Sigma = R diag(s)^2 R^T (gaussians.py:267-275); a single q gives (3,3)."""
+    single = np.asarray(q).ndim == 1
+    R = _rot_t(_dev(np.atleast_2d(q)))
+    M = R * _dev(np.atleast_2d(s))[:, None, :]
+    cov = (M @ M.transpose(1, 2)).cpu().numpy()
+    return cov[0] if single else cov
+
+
+def covariance_backward(q, s, d_cov):
+    """(dq, ds) of build_covariance for the full dL/dSigma (gaussians.py:278-289)."""
+    import torch
+    qt, st = _dev(np.atleast_2d(q)), _dev(np.atleast_2d(s))
+    R = _rot_t(qt)
+    M = R * st[:, None, :]
+    dc = _dev(d_cov).view(-1, 3, 3)
+    dM = (dc + dc.transpose(1, 2)) @ M
+    ds = torch.einsum("nik,nik->nk", dM, R)
+    dq = _rot_backward_t(qt, dM * st[:, None, :])
+    return dq.cpu().numpy(), ds.cpu().numpy()
+
+
+def sh_basis(dirs, degree):
+    """Real SH basis (N,B) and its direction derivatives (N,B,3) for unit
+    directions (gaussians.py:429-494), from csrc/sh.cu (ivr_sh_basis)."""
+    import torch
+    from . import _lib as L
+    from . import device as D
+    d = _dev(np.atleast_2d(dirs)).contiguous()
+    n, nb = d.shape[0], (int(degree) + 1) ** 2
+    B = torch.empty((n, nb), dtype=torch.float64, device=d.device)
+    dB = torch.empty((n, nb, 3), dtype=torch.float64, device=d.device)
+    L.check(L.lib().ivr_sh_basis(n, int(degree), D.ptr(d), D.ptr(B), D.ptr(dB),
+                                 D.stream_handle()), "ivr_sh_basis")
+    return B.cpu().numpy(), dB.cpu().numpy()
+
+
+def eval_sh(color, view_dirs):
+    """SH colour along unit ``view_dirs`` with the +0.5 offset, clamped at 0
+    from below (gaussians.py:497-507).  Returns (rgb (N,3), cache)."""
+    B, dB = sh_basis(view_dirs, color.degree)
+    coeffs = np.asarray(color.coefficients, np.float64)
+    raw = np.einsum("nb,nbc->nc", B, coeffs) + 0.5
+    return np.maximum(raw, 0.0), {"basis": B, "dbasis": dB, "raw": raw, "coeffs": coeffs}
+
+
+def eval_sh_backward(cache, d_rgb):
+    """(d_coeffs (N,B,3), d_dir (N,3)) of eval_sh (gaussians.py:510-518)."""
+    g = np.asarray(d_rgb, np.float64) * (cache["raw"] > 0)
+    d_coeffs = cache["basis"][:, :, None] * g[:, None, :]
+    inner = np.einsum("nbc,nc->nb", cache["coeffs"], g)
+    return d_coeffs, np.einsum("nb,nbk->nk", inner, cache["dbasis"])
+
+
+def view_dirs_backward(mu, cam_position, d_dir):
+    """d/dmu of view_dirs (gaussians.py:527-529)."""
+    from ._mathutil import normalize_rows_backward
+    v = np.asarray(mu, np.float64) - np.asarray(cam_position, np.float64)[None, :]
+    return normalize_rows_backward(v, np.asarray(d_dir, np.float64))
+
+
+def project_backward(cache, d_mean2d, d_cov2d, d_depth):
+    """Chain d_mean2d (N,2), the full d_cov2d (N,2,2) and d_depth (N,) back to
+    (d_mu, d_q_raw, d_log_s) (gaussians.py:349-400), batched on the GPU.
+    ``cache`` is the dict project_gaussians returns."""
+    import torch
+    geom, cam = cache["geom"], cache["cam"]
+    q_raw = _dev(geom.q_raw)
+    qn = q_raw / torch.linalg.norm(q_raw, dim=1, keepdim=True)
+    s = torch.exp(_dev(geom.log_s))
+    R = _rot_t(qn)
+    M3 = R * s[:, None, :]
+    cov3d = M3 @ M3.transpose(1, 2)
+    Wr = _dev(cam.rotation)
+    f = float(cam.focal)
+    t = (_dev(geom.mu) - _dev(cam.position)[None, :]) @ Wr.T
+    valid = torch.from_numpy(np.asarray(cache["valid"], bool)).to(t.device)
+    tz = torch.where(valid, t[:, 2], torch.ones_like(t[:, 2]))
+    n = t.shape[0]
+    J = torch.zeros((n, 2, 3), dtype=torch.float64, device=t.device)
+    J[:, 0, 0] = f / tz
+    J[:, 0, 2] = -f * t[:, 0] / tz ** 2
+    J[:, 1, 1] = f / tz
+    J[:, 1, 2] = -f * t[:, 1] / tz ** 2
+    M = J @ Wr
+    dm = torch.where(valid[:, None], _dev(d_mean2d).view(n, 2), 0.0)
+    dc = torch.where(valid[:, None, None], _dev(d_cov2d).view(n, 2, 2), 0.0)
+    dd = torch.where(valid, _dev(d_depth).view(n), 0.0)
+    d_cov3d = M.transpose(1, 2) @ dc @ M
+    dM = dc @ M @ cov3d.transpose(1, 2) + dc.transpose(1, 2) @ M @ cov3d
+    dJ = dM @ Wr.T
+    dt = torch.zeros((n, 3), dtype=torch.float64, device=t.device)
+    dt[:, 0] = dJ[:, 0, 2] * (-f / tz ** 2) + dm[:, 0] * f / tz
+    dt[:, 1] = dJ[:, 1, 2] * (-f / tz ** 2) + dm[:, 1] * f / tz
+    dt[:, 2] = (dJ[:, 0, 0] * (-f / tz ** 2) + dJ[:, 1, 1] * (-f / tz ** 2)
+                + dJ[:, 0, 2] * (2 * f * t[:, 0] / tz ** 3) + dJ[:, 1, 2] * (2 * f * t[:, 1] / tz ** 3)
+                - dm[:, 0] * f * t[:, 0] / tz ** 2 - dm[:, 1] * f * t[:, 1] / tz ** 2 + dd)
+    d_mu = dt @ Wr
+    dMc = (d_cov3d + d_cov3d.transpose(1, 2)) @ M3
+    ds = torch.einsum("nik,nik->nk", dMc, R)
+    dq_unit = _rot_backward_t(qn, dMc * s[:, None, :])
+    nq = torch.linalg.norm(q_raw, dim=1, keepdim=True)
+    u = q_raw / nq
+    d_q_raw = (dq_unit - (dq_unit * u).sum(1, keepdim=True) * u) / nq
+    return {"d_mu": d_mu.cpu().numpy(), "d_q_raw": d_q_raw.cpu().numpy(),
+            "d_log_s": (ds * s).cpu().numpy()}

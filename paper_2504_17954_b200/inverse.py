@@ -107,24 +107,7 @@ def init_transform(scene: ComposedScene) -> TransformParams:
                            scene.light.polar, scene.light.azimuth, scene.light.mode)
 
 
-class Adam:
-    """trainer.Adam (trainer.py:100-128) on host float64 arrays."""
-
-    def __init__(self, eps=1e-15, betas=(0.9, 0.999)):
-        self.eps = eps
-        self.b1, self.b2 = betas
-        self.state = {}
-
-    def step(self, name, param, grad, lr):
-        st = self.state.setdefault(name, {"m": np.zeros_like(param), "v": np.zeros_like(param),
-                                          "t": 0})
-        st["t"] += 1
-        st["m"] = self.b1 * st["m"] + (1.0 - self.b1) * grad
-        st["v"] = self.b2 * st["v"] + (1.0 - self.b2) * grad * grad
-        mhat = st["m"] / (1.0 - self.b1 ** st["t"])
-        vhat = st["v"] / (1.0 - self.b2 ** st["t"])
-        param -= lr * mhat / (np.sqrt(vhat) + self.eps)
-        return param
+from .trainer import Adam  # noqa: E402  (trainer.Adam, trainer.py:100-128)
 
 
 def _light(scene, params):

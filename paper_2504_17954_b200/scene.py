@@ -602,3 +602,15 @@ def render_composed(scene, cam, channels=("color", "alpha"), attrs=None, dtype=n
     many frames of the same scene without re-uploading."""
     del sequential
     return DeviceScene(scene).render(cam, channels, attrs, dtype)
+
+
+def save_model(model, path):
+    """scene.save_model (scene.py:242-347): the IVRG writer (ivrg.py)."""
+    from .ivrg import save_model as _save
+    return _save(model, path)
+
+
+def load_model(path):
+    """scene.load_model (scene.py:349-436): the IVRG reader (ivrg.py)."""
+    from .ivrg import load_model as _load
+    return _load(path)

@@ -152,6 +152,40 @@ class ShadingAttributes:
                                              "log_beta")))
 
 
+def resolve_light_direction(light, cam, mu):
+    """Per-point unit light direction (shading.py:186-196): from the camera
+    towards each point for a headlight, the constant orbital direction
+    otherwise."""
+    mu = np.asarray(mu, dtype=np.float64)
+    if light.mode != ORBITAL:
+        d = np.asarray(cam.position, dtype=np.float64) - mu
+        return d / np.maximum(np.linalg.norm(d, axis=-1, keepdims=True), 1e-12)
+    l = light_direction_from_angles(light.polar, light.azimuth)
+    return np.broadcast_to(l, mu.shape).copy() if mu.ndim > 1 else l
+
+
+def blinn_phong(c_v, n, l, v, k_a, k_d, k_s, beta):
+    """The reflection formula shared by splat shading and volume rendering
+    (shading.py:199-222), on host arrays with numpy broadcasting over the
+    leading axes: ambient k_a c_v, diffuse k_d |n.l| c_v, white specular
+    k_s |n.h|^beta with h = normalize(v + l) (eps 1e-12), gated on |n.l| > 0.
+    Returns (rgb, ambient, diffuse, specular).  A host utility: the GPU
+    paths evaluate the same expression inside K1 / K13."""
+    c_v = np.asarray(c_v, dtype=np.float64)
+    n, l, v = (np.asarray(x, dtype=np.float64) for x in (n, l, v))
+    k_a, k_d, k_s, beta = (np.asarray(x, dtype=np.float64) for x in (k_a, k_d, k_s, beta))
+    u = v + l
+    h = u / np.maximum(np.linalg.norm(u, axis=-1, keepdims=True), 1e-12)
+    a_ndl = np.abs(np.sum(n * l, axis=-1))
+    a_ndh = np.abs(np.sum(n * h, axis=-1))
+    spow = np.where(a_ndh > 0.0, np.power(np.maximum(a_ndh, 1e-300), beta), 0.0)
+    spow = np.where(a_ndl > 0.0, spow, 0.0)
+    ambient = k_a[..., None] * c_v
+    diffuse = (k_d * a_ndl)[..., None] * c_v
+    specular = (k_s * spow)[..., None] * WHITE
+    return ambient + diffuse + specular, ambient, diffuse, specular
+
+
 def light_direction_from_angles(polar, azimuth):
     return D.light_direction(polar, azimuth)
 

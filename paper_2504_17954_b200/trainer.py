@@ -86,6 +86,37 @@ class TrainConfig:
         return self.densify_until_iter if self.densify_until_iter is not None else stage_iters // 2
 
 
+class Adam:
+    """trainer.Adam (trainer.py:100-128): per-parameter Adam on host float64
+    arrays (in place), moments surviving densification.  The training loops
+    use DeviceAdam / the captured Adam kernel; this is the reference's host
+    optimizer object (also driving the small transform vector of the
+    multi-rank inverse host loop)."""
+
+    def __init__(self, eps=1e-15, betas=(0.9, 0.999)):
+        self.eps = eps
+        self.b1, self.b2 = betas
+        self.state = {}
+
+    def step(self, name, param, grad, lr):
+        st = self.state.setdefault(name, {"m": np.zeros_like(param), "v": np.zeros_like(param),
+                                          "t": 0})
+        st["t"] += 1
+        st["m"] = self.b1 * st["m"] + (1.0 - self.b1) * grad
+        st["v"] = self.b2 * st["v"] + (1.0 - self.b2) * grad * grad
+        mhat = st["m"] / (1.0 - self.b1 ** st["t"])
+        vhat = st["v"] / (1.0 - self.b2 ** st["t"])
+        param -= lr * mhat / (np.sqrt(vhat) + self.eps)
+        return param
+
+    def remap(self, parents, is_new):
+        for st in self.state.values():
+            for key in ("m", "v"):
+                arr = st[key][parents].copy()
+                arr[is_new] = 0.0
+                st[key] = arr
+
+
 class DeviceAdam:
     """trainer.Adam on device tensors (one fused launch for all parameter
     groups, csrc/adam.cu); moments survive densification (remap)."""
@@ -746,6 +777,32 @@ class StepGraph:
         """Retire every pending step (host synchronisation point)."""
         while self._pending:
             self._retire_oldest()
+
+
+def densify_and_prune(model, grad_stats, cfg, extent=None, rng=None):
+    """One round of adaptive density control on a scene model
+    (trainer.py:241-261): clone / split (at scale / 1.6) the primitives whose
+    mean gradient statistic exceeds the threshold, prune low opacity; on the
+    GPU (the trainers' ``densify``).  Split offsets come from a device
+    generator seeded from ``rng``.  Returns (new model, info)."""
+    rng = rng if rng is not None else np.random.default_rng(cfg.seed)
+    extent = extent if extent is not None else scene_extent(np.asarray(model.geometry.mu))
+    g = model.geometry
+    params = {k: getattr(g, k) for k in GEOM}
+    if model.stage == STAGE_EDITABLE:
+        params.update({k: getattr(model.shading, k) for k in SHADE})
+        tr = EditableTrainer(params, model.palette.c_p, LightConfig(), cfg)
+    else:
+        params["sh"] = np.asarray(model.sh.coefficients, np.float64)
+        tr = BaseTrainer(params, model.sh.degree, cfg)
+    gen = torch.Generator(device=tr.dev).manual_seed(int(rng.integers(2 ** 62)))
+    stats = D.to_dev(np.asarray(grad_stats, np.float64).reshape(-1))
+    info = tr.densify(stats, extent, gen)
+    if model.stage == STAGE_EDITABLE:
+        new = tr.model(model.palette.c_p, dict(model.metadata))
+    else:
+        new = tr.model(dict(model.metadata))
+    return new, info
 
 
 def _dc_colors_from_view(points, cam, image):
