@@ -153,3 +153,33 @@ def test_inverse_step_and_fit():
     assert loss == float(d["loss0"])
     for k, v in g.items():
         np.testing.assert_array_equal(v, d["g_" + k], err_msg=k)
+
+
+def test_blinn_phong_worked_example():
+    """The reference's scalar worked example (n.l = 0.5, n.h = 0.9)."""
+    from paper_2504_17954_b200.dvr import shade_sample
+    from paper_2504_17954_b200.shading import blinn_phong
+    n = np.array([0.0, 0.0, 1.0])
+    l = np.array([np.sqrt(3) / 2, 0.0, 0.5])
+    h = np.array([np.sqrt(0.19), 0.0, 0.9])
+    v = 2.0 * np.dot(h, l) * h - l
+    c_v = np.array([0.6, 0.0, 0.0])
+    rgb, amb, dif, spec = blinn_phong(c_v, n, l, v, np.array(0.2), np.array(0.5), np.array(0.3),
+                                      np.array(8.0))
+    expected = 0.2 * c_v + 0.5 * c_v * 0.5 + 0.3 * np.ones(3) * 0.9 ** 8
+    np.testing.assert_allclose(rgb, expected, atol=1e-12)
+    np.testing.assert_allclose(amb, [0.12, 0.0, 0.0])
+    np.testing.assert_allclose(shade_sample(c_v, n, l, v, 0.2, 0.5, 0.3, 8.0), expected, atol=1e-12)
+
+
+def test_mathutil_helpers():
+    from paper_2504_17954_b200 import _mathutil as M
+    x = np.array([-800.0, -3.0, 0.0, 2.5, 800.0])
+    s = M.sigmoid(x)
+    assert np.all(np.isfinite(s)) and s[2] == 0.5
+    np.testing.assert_allclose(M.inv_sigmoid(M.sigmoid(x[1:4])), x[1:4], atol=1e-12)
+    np.testing.assert_allclose(M.inv_softplus(M.softplus(x[1:4])), x[1:4], atol=1e-12)
+    v = np.array([[3.0, 4.0, 0.0]])
+    np.testing.assert_allclose(M.normalize_rows(v), [[0.6, 0.8, 0.0]])
+    d = M.normalize_rows_backward(v, np.array([[1.0, 0.0, 0.0]]))
+    np.testing.assert_allclose(d @ M.normalize_rows(v).T, [[0.0]], atol=1e-15)
