@@ -217,3 +217,24 @@ def test_large_frames_banded_placement(W, H):
     assert np.array_equal(F.tile_ranges.cpu().numpy(), ref["tile_ranges"])
     assert np.array_equal(out.per_pixel_contrib_count, ref["contrib"])
     assert np.abs(out.color - O.maps(ref)["color"]).max() <= IMG_TOL
+
+
+@pytest.mark.parametrize("counts", [(50,), (60, 45, 30)])
+def test_composed_render_equals_union_rasterization(counts):
+    """The reference's compose contract (tests/test_scene.py:41-78): rendering
+    a composed scene equals shading the concatenated primitives and
+    rasterizing the union list, bit for bit (float64)."""
+    from paper_2504_17954_b200 import (ComposedScene, GaussianGeometry, ShadingAttributes,
+                                       rasterize_forward, render_composed, shade_gaussians)
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_model
+    models = [editable_model(30 + i, c, spread=0.5, density=400) for i, c in enumerate(counts)]
+    sc = ComposedScene.compose(models)
+    cam = bench_camera(64, 48, 0.5)
+    img = render_composed(sc, cam, dtype=np.float64)
+    geom = GaussianGeometry.concat([m.geometry for m in sc.models])
+    attrs = ShadingAttributes.concat([m.shading for m in sc.models])
+    palette = np.concatenate([np.broadcast_to(m.palette.c_p, (len(m), 3)) for m in sc.models])
+    rgb, _, _ = shade_gaussians(geom, attrs, palette, sc.light, cam)
+    union, _ = rasterize_forward(geom, rgb, cam, dtype=np.float64)
+    assert np.array_equal(img.color, union.color)
+    assert np.array_equal(img.alpha, union.alpha)
