@@ -45,17 +45,19 @@ __device__ __forceinline__ double depth_at(const Args &A, int y, int x) {
 }
 
 // camera-space point of pixel (y, x) (losses.py:157-161 order: (px - cx) * d / f)
-__device__ __forceinline__ void point(const Args &A, double f, double cx, double cy, int y, int x,
-                                      double p[3]) {
+// (px - cx) * d / f with 1/f hoisted (one ulp from the reference's division;
+// the pseudo normal is normalised afterwards)
+__device__ __forceinline__ void point(const Args &A, double inv_f, double cx, double cy, int y,
+                                      int x, double p[3]) {
     const double d = depth_at(A, y, x);
-    p[0] = ((double)x - cx) * d / f;
-    p[1] = ((double)y - cy) * d / f;
+    p[0] = ((double)x - cx) * d * inv_f;
+    p[1] = ((double)y - cy) * d * inv_f;
     p[2] = d;
 }
 
 // pseudo normal (world) at (y, x) and whether it is in the mask
 __device__ __forceinline__ bool pseudo_normal(const Args &A, int y, int x, double nw[3]) {
-    const double f = A.camp[0], cx = A.camp[1], cy = A.camp[2];
+    const double f = 1.0 / A.camp[0], cx = A.camp[1], cy = A.camp[2];  // f holds 1/focal
     const double *rot = A.camp + 3;
     double p[3], q[3], dx[3], dy[3];
     point(A, f, cx, cy, y, x, p);
@@ -79,7 +81,8 @@ __device__ __forceinline__ bool pseudo_normal(const Args &A, int y, int x, doubl
                    dx[0] * dy[1] - dx[1] * dy[0]};
     const double nn = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
     const bool good = nn > 1e-12;
-    for (int k = 0; k < 3; ++k) n[k] = good ? n[k] / nn : 0.0;
+    const double inv_nn = good ? 1.0 / nn : 0.0;
+    for (int k = 0; k < 3; ++k) n[k] = n[k] * inv_nn;
     if (n[0] * p[0] + n[1] * p[1] + n[2] * p[2] > 0.0)
         for (int k = 0; k < 3; ++k) n[k] = -n[k];
     for (int j = 0; j < 3; ++j) nw[j] = n[0] * rot[j] + n[1] * rot[3 + j] + n[2] * rot[6 + j];
