@@ -447,10 +447,10 @@ bwd_reduce_det_kernel(int64_t n, int K, const uint64_t *depth_key, const int32_t
 // ----------------------------------------------------------------- K4b helpers
 __device__ __forceinline__ void normalize_bwd(const double v[3], const double d[3], double out[3]) {
     // _mathutil.normalize_rows_backward: (d - (d.u) u) / |v|
-    const double n = sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
-    const double u[3] = {v[0] / n, v[1] / n, v[2] / n};
+    const double in = 1.0 / sqrt(v[0] * v[0] + v[1] * v[1] + v[2] * v[2]);
+    const double u[3] = {v[0] * in, v[1] * in, v[2] * in};
     const double pr = d[0] * u[0] + d[1] * u[1] + d[2] * u[2];
-    for (int k = 0; k < 3; ++k) out[k] = (d[k] - pr * u[k]) / n;
+    for (int k = 0; k < 3; ++k) out[k] = (d[k] - pr * u[k]) * in;
 }
 
 __device__ __forceinline__ double sgn(double x) { return x > 0.0 ? 1.0 : (x < 0.0 ? -1.0 : 0.0); }
@@ -589,13 +589,14 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
                     for (int k = 0; k < 3; ++k)
                         dJ[3 * r + k] = dM[3 * r] * W[3 * k] + dM[3 * r + 1] * W[3 * k + 1] +
                                         dM[3 * r + 2] * W[3 * k + 2];
-                const double tz2 = tz * tz, tz3 = tz2 * tz;
+                // one reciprocal instead of ten divisions (gradient tolerance 1e-3)
+                const double itz = 1.0 / tz, f1 = f * itz, f2 = f1 * itz, f3 = f2 * itz;
                 double dt[3];
-                dt[0] = dJ[2] * (-f / tz2) + gmean[0] * f / tz;
-                dt[1] = dJ[5] * (-f / tz2) + gmean[1] * f / tz;
-                dt[2] = dJ[0] * (-f / tz2) + dJ[4] * (-f / tz2) + dJ[2] * (2 * f * p.t[0] / tz3) +
-                        dJ[5] * (2 * f * p.t[1] / tz3) - gmean[0] * f * p.t[0] / tz2 -
-                        gmean[1] * f * p.t[1] / tz2 + gv_depth;
+                dt[0] = dJ[2] * (-f2) + gmean[0] * f1;
+                dt[1] = dJ[5] * (-f2) + gmean[1] * f1;
+                dt[2] = dJ[0] * (-f2) + dJ[4] * (-f2) + dJ[2] * (2 * p.t[0] * f3) +
+                        dJ[5] * (2 * p.t[1] * f3) - gmean[0] * p.t[0] * f2 -
+                        gmean[1] * p.t[1] * f2 + gv_depth;
                 for (int j = 0; j < 3; ++j)
                     d_mu[j] += dt[0] * W[j] + dt[1] * W[3 + j] + dt[2] * W[6 + j];
                 // covariance_backward (gaussians.py:278-289)
@@ -630,8 +631,9 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
                                        qraw[3] * qraw[3]);
                 const double dqv[4] = {qw, qx, qy, qz};
                 double pr = 0.0;
-                for (int k = 0; k < 4; ++k) pr += dqv[k] * (qraw[k] / qn);
-                for (int k = 0; k < 4; ++k) dq[k] = (dqv[k] - pr * (qraw[k] / qn)) / qn;
+                const double iqn = 1.0 / qn;
+                for (int k = 0; k < 4; ++k) pr += dqv[k] * (qraw[k] * iqn);
+                for (int k = 0; k < 4; ++k) dq[k] = (dqv[k] - pr * (qraw[k] * iqn)) * iqn;
                 for (int k = 0; k < 3; ++k) dls[k] = ds[k] * p.s[k];
             }
             if (R.d_q_raw) for (int k = 0; k < 4; ++k) R.d_q_raw[4 * i + k] = dq[k];
