@@ -648,7 +648,7 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
             double nrm[3];
             unit_normal(G, i, nrm);
             ShadeState st;
-            shade_state(B.S, P, i, sid, mu, nrm, st, G.cache);
+            shade_state<false>(B.S, P, i, sid, mu, nrm, st, G.cache);
             double d_rgb[3];
             for (int k = 0; k < 3; ++k)
                 d_rgb[k] = gv_color[k] + (R.d_rgb_extra ? R.d_rgb_extra[3 * i + k] : 0.0);

@@ -153,6 +153,10 @@ struct ShadeState {
     bool gate;
 };
 
+// EXACT (K1, shade_kernel): the reference's operations; EXACT = false (K4b's
+// gradient-only recomputation): the two unit vectors use one reciprocal each
+// instead of three IEEE divisions (<= 1 ulp; gradient tolerance 1e-3)
+template <bool EXACT = true>
 __device__ __forceinline__ void shade_state(const ivr_shading &S, const ivr_frame_params &P,
                                             int64_t i, int32_t sid, const double mu[3],
                                             const double nrm[3], ShadeState &o,
@@ -160,7 +164,12 @@ __device__ __forceinline__ void shade_state(const ivr_shading &S, const ivr_fram
     const ivr_camera &cam = P.cam;
     for (int k = 0; k < 3; ++k) o.w_cam[k] = dsub(cam.position[k], mu[k]);
     const double wn = dmax(norm3(o.w_cam[0], o.w_cam[1], o.w_cam[2]), 1e-12);
-    for (int k = 0; k < 3; ++k) o.v[k] = ddiv(o.w_cam[k], wn);
+    if (EXACT) {
+        for (int k = 0; k < 3; ++k) o.v[k] = ddiv(o.w_cam[k], wn);
+    } else {
+        const double iw = 1.0 / wn;
+        for (int k = 0; k < 3; ++k) o.v[k] = o.w_cam[k] * iw;
+    }
     if (!P.orbital) {
         for (int k = 0; k < 3; ++k) {
             o.l[k] = o.h[k] = o.v[k];
@@ -172,7 +181,12 @@ __device__ __forceinline__ void shade_state(const ivr_shading &S, const ivr_fram
             o.u[k] = dadd(o.v[k], o.l[k]);
         }
         const double un = dmax(norm3(o.u[0], o.u[1], o.u[2]), 1e-12);
-        for (int k = 0; k < 3; ++k) o.h[k] = ddiv(o.u[k], un);
+        if (EXACT) {
+            for (int k = 0; k < 3; ++k) o.h[k] = ddiv(o.u[k], un);
+        } else {
+            const double iu = 1.0 / un;
+            for (int k = 0; k < 3; ++k) o.h[k] = o.u[k] * iu;
+        }
     }
     if (cache && cache[kCacheStride * i + 14] != 0.0) {
         const double *c = cache + kCacheStride * i;
