@@ -418,6 +418,15 @@ int ivr_photometric_loss(const double *pred, const double *gt, int32_t height, i
                          int32_t channels, const double window[11], double a, double b,
                          int32_t with_ssim, double *d_pred, double *sums, void *workspace,
                          size_t workspace_bytes, ivr_stream_t stream);
+/* Same, reading the prediction in place from K3's float32 (H, W, frame_k)
+ * frame: channel c = frame[pixel * frame_k + cols[c]] (cols: host array of
+ * `channels` <= 4 entries) -- the trainer's rgba columns without a gather /
+ * f64 copy (trainer.py:355-358 slices them out of the render). */
+int ivr_photometric_loss_frame(const float *frame, int32_t frame_k, const int32_t *cols,
+                               const double *gt, int32_t height, int32_t width,
+                               int32_t channels, const double window[11], double a, double b,
+                               int32_t with_ssim, double *d_pred, double *sums, void *workspace,
+                               size_t workspace_bytes, ivr_stream_t stream);
 
 /* Training-step map terms (trainer.py:355-366, losses.py:141-268) in one
  * pass: d_out (H,W,k float32) = photometric gradient d_rgba (H,W,4 float64,

@@ -214,6 +214,11 @@ _SIGS = {
     "ivr_photometric_loss": ([P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
                               ctypes.POINTER(ctypes.c_double), ctypes.c_double, ctypes.c_double,
                               ctypes.c_int32, P, P, P, ctypes.c_size_t, P], ctypes.c_int),
+    "ivr_photometric_loss_frame": ([P, ctypes.c_int32, ctypes.POINTER(ctypes.c_int32), P,
+                                    ctypes.c_int32, ctypes.c_int32, ctypes.c_int32,
+                                    ctypes.POINTER(ctypes.c_double), ctypes.c_double,
+                                    ctypes.c_double, ctypes.c_int32, P, P, P, ctypes.c_size_t,
+                                    P], ctypes.c_int),
 }
 
 _lib = None

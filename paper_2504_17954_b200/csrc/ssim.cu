@@ -36,6 +36,10 @@ constexpr double kC1 = 0.01 * 0.01, kC2 = 0.03 * 0.03;
 
 struct Args {
     const double *x, *y;  // (H, W, C)
+    // optional prediction source: channel c of pixel p = xf[p * xs + xcol[c]]
+    // (K3's float32 (H, W, k) frame read in place; promotion to f64 is exact)
+    const float *xf;
+    int xs, xcol[4];
     int H, W, C, Hv, Wv;
     double g[WIN];
     double up;            // 1 / (Hv * Wv * C)
@@ -44,6 +48,10 @@ struct Args {
     double *partA, *partB;         // per-block partial sums
     double *d_pred;                // (H, W, C)
 };
+
+__device__ __forceinline__ double load_x(const Args &A, int64_t pix, int c) {
+    return A.xf ? (double)__ldg(A.xf + pix * A.xs + A.xcol[c]) : A.x[pix * A.C + c];
+}
 
 __device__ __forceinline__ double block_sum(double v, double *s_red) {
 #pragma unroll
@@ -78,8 +86,8 @@ __global__ void __launch_bounds__(kThreads) ssim_window_kernel(Args A) {
                 const int k = it * kThreads + tid;
                 const int r = k / IW, q = k % IW, gi = i0 + r, gj = j0 + q;
                 const bool ok = k < IH * IW && gi < A.H && gj < A.W;
-                const int64_t o = ((int64_t)gi * A.W + gj) * A.C + c;
-                vx[it] = ok ? A.x[o] : 0.0;
+                const int64_t px = (int64_t)gi * A.W + gj, o = px * A.C + c;
+                vx[it] = ok ? load_x(A, px, c) : 0.0;
                 vy[it] = ok ? A.y[o] : 0.0;
             }
 #pragma unroll
@@ -259,8 +267,8 @@ __global__ void __launch_bounds__(kThreads) ssim_grad_kernel(Args A) {
         for (int o = 0; o < RB; ++o) {
             const int pi = i0 + r0 + o;
             if (pi >= A.H || pj >= A.W) continue;
-            const int64_t oo = ((int64_t)pi * A.W + pj) * A.C + c;
-            const double xv = A.x[oo], yv = A.y[oo];
+            const int64_t px = (int64_t)pi * A.W + pj, oo = px * A.C + c;
+            const double xv = load_x(A, px, c), yv = A.y[oo];
             const double df = xv - yv;
             l1 += fabs(df);
             double d = A.a * (df > 0.0 ? 1.0 : (df < 0.0 ? -1.0 : 0.0));
@@ -311,14 +319,14 @@ extern "C" size_t ivr_photometric_workspace_size(int32_t height, int32_t width, 
     return ivr::ssimk::plan(height, width, channels).bytes;
 }
 
-extern "C" int ivr_photometric_loss(const double *pred, const double *gt, int32_t height,
-                                    int32_t width, int32_t channels, const double window[11],
-                                    double a, double b, int32_t with_ssim, double *d_pred,
-                                    double *sums, void *workspace, size_t workspace_bytes,
-                                    ivr_stream_t stream) {
+static int photometric(const double *pred, const float *frame, int32_t frame_k,
+                       const int32_t *cols, const double *gt, int32_t height, int32_t width,
+                       int32_t channels, const double window[11], double a, double b,
+                       int32_t with_ssim, double *d_pred, double *sums, void *workspace,
+                       size_t workspace_bytes, ivr_stream_t stream) {
     using namespace ivr;
     using namespace ivr::ssimk;
-    if (!pred || !gt || !d_pred || !sums || !window || height < 1 || width < 1 || channels < 1 ||
+    if ((!pred && !frame) || !gt || !d_pred || !sums || !window || height < 1 || width < 1 || channels < 1 ||
         (with_ssim && (height < WIN || width < WIN))) {
         set_error("ivr_photometric_loss: bad argument (images smaller than the 11x11 window?)");
         return IVR_ERR_ARG;
@@ -331,6 +339,21 @@ extern "C" int ivr_photometric_loss(const double *pred, const double *gt, int32_
     cudaStream_t st = (cudaStream_t)stream;
     Args A{};
     A.x = pred;
+    A.xf = frame;
+    if (frame) {
+        if (channels > 4 || !cols || frame_k < 1) {
+            set_error("ivr_photometric_loss_frame: needs 1..4 channels and a column map");
+            return IVR_ERR_ARG;
+        }
+        A.xs = frame_k;
+        for (int c = 0; c < channels; ++c) {
+            if (cols[c] < 0 || cols[c] >= frame_k) {
+                set_error("ivr_photometric_loss_frame: column out of range");
+                return IVR_ERR_ARG;
+            }
+            A.xcol[c] = cols[c];
+        }
+    }
     A.y = gt;
     A.H = height;
     A.W = width;
@@ -365,4 +388,32 @@ extern "C" int ivr_photometric_loss(const double *pred, const double *gt, int32_
         ssim_grad_kernel<false><<<gB, kThreads, 0, st>>>(A);
     ssim_finish_kernel<<<1, kThreads, 0, st>>>(A.partA, na, A.partB, p.nb, sums);
     return check_launch("ivr_photometric_loss");
+}
+
+extern "C" int ivr_photometric_loss(const double *pred, const double *gt, int32_t height,
+                                    int32_t width, int32_t channels, const double window[11],
+                                    double a, double b, int32_t with_ssim, double *d_pred,
+                                    double *sums, void *workspace, size_t workspace_bytes,
+                                    ivr_stream_t stream) {
+    if (!pred) {
+        ivr::set_error("ivr_photometric_loss: bad argument (null prediction)");
+        return IVR_ERR_ARG;
+    }
+    return photometric(pred, nullptr, 0, nullptr, gt, height, width, channels, window, a, b,
+                       with_ssim, d_pred, sums, workspace, workspace_bytes, stream);
+}
+
+extern "C" int ivr_photometric_loss_frame(const float *frame, int32_t frame_k,
+                                          const int32_t *cols, const double *gt, int32_t height,
+                                          int32_t width, int32_t channels,
+                                          const double window[11], double a, double b,
+                                          int32_t with_ssim, double *d_pred, double *sums,
+                                          void *workspace, size_t workspace_bytes,
+                                          ivr_stream_t stream) {
+    if (!frame) {
+        ivr::set_error("ivr_photometric_loss_frame: bad argument (null frame)");
+        return IVR_ERR_ARG;
+    }
+    return photometric(nullptr, frame, frame_k, cols, gt, height, width, channels, window, a, b,
+                       with_ssim, d_pred, sums, workspace, workspace_bytes, stream);
 }

@@ -89,6 +89,36 @@ def _photometric_dev(x, y, a, b, with_ssim):
     return sums, d
 
 
+def _photometric_frame_dev(frame, cols, y, a, b, with_ssim):
+    """``_photometric_dev`` with the prediction read in place from K3's
+    float32 (H, W, k) frame at columns ``cols`` (ivr_photometric_loss_frame):
+    the same sums and d as on ``frame[..., cols].double()``, without the
+    gather and the float64 copy."""
+    import ctypes
+    from . import _lib as L
+    from . import device as D
+    frame, y = frame.contiguous(), y.contiguous()
+    h, w, k = frame.shape
+    nc = len(cols)
+    if tuple(y.shape) != (h, w, nc):
+        raise ShapeMismatch(f"prediction {(h, w, nc)} vs ground truth {tuple(y.shape)}")
+    nbytes = L.lib().ivr_photometric_workspace_size(h, w, nc)
+    key = (y.device, nbytes)
+    ws = _WS.get(key)
+    if ws is None:
+        ws = _WS[key] = torch.empty(max(nbytes, 8), dtype=torch.uint8, device=y.device)
+    d = torch.empty((h, w, nc), dtype=torch.float64, device=y.device)
+    sums = torch.empty(2, dtype=torch.float64, device=y.device)
+    keep, wp = _window_ptr()
+    cm = (ctypes.c_int32 * nc)(*[int(c) for c in cols])
+    L.check(L.lib().ivr_photometric_loss_frame(D.ptr(frame), k, cm, D.ptr(y), h, w, nc, wp,
+                                               float(a), float(b), 1 if with_ssim else 0,
+                                               D.ptr(d), D.ptr(sums), D.ptr(ws), nbytes,
+                                               D.stream_handle()), "ivr_photometric_loss_frame")
+    del keep
+    return sums, d
+
+
 def regularize_t(out, cols, gt=None, d_rgba=None, cam_params=None, w_normal=0.0, w_offset=0.0,
                  w_bil=0.0, bil_cols=()):
     """Fused map terms of a training step (csrc/regularize.cu): returns

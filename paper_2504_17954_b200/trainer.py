@@ -35,7 +35,7 @@ from . import _lib as L
 from . import device as D
 from .errors import DatasetEmpty, DivergedLoss, OutOfRange, ShapeMismatch
 from .gaussians import GaussianGeometry, ShColor
-from .losses import SSIM_RADIUS, LossWeights, _photometric_dev, regularize_t
+from .losses import SSIM_RADIUS, LossWeights, _photometric_frame_dev, regularize_t
 from .rasterizer import _channel_layout, _cols
 from .scene import STAGE_BASE, STAGE_EDITABLE, BasicSceneModel, DeviceScene
 from .shading import LightConfig, Palette, ShadingAttributes
@@ -315,21 +315,20 @@ class _StageTrainer:
         returns (loss terms for ivr_loss_finalize, tensors they point to,
         d_out float32 (H,W,K), column map).  No host synchronisation."""
         c = {name: c for name, c, w in _cols_named(self.layout)}
-        idx = getattr(self, "_rgba_idx", None)
-        if idx is None:
-            idx = self._rgba_idx = torch.tensor([c["color"], c["color"] + 1, c["color"] + 2,
-                                                 c["alpha"]], device=self.dev)
-        rgba = F.out.index_select(2, idx).double()
-        if rgba.shape != gt.shape:
-            raise ShapeMismatch(f"prediction {tuple(rgba.shape)} vs ground truth {tuple(gt.shape)}")
-        h, w, nc = rgba.shape
+        rgba_cols = (c["color"], c["color"] + 1, c["color"] + 2, c["alpha"])
+        h, w, nc = F.out.shape[0], F.out.shape[1], len(rgba_cols)
+        if (h, w, nc) != tuple(gt.shape):
+            raise ShapeMismatch(f"prediction {(h, w, nc)} vs ground truth {tuple(gt.shape)}")
         win = 2 * SSIM_RADIUS + 1
         with_ssim = weights.ssim_weight > 0.0
         if with_ssim and (h < win or w < win):
             raise ShapeMismatch(f"image {h}x{w} smaller than the {win}x{win} ssim window")
-        numel = rgba.numel()
-        sums, d_rgba = _photometric_dev(rgba, gt.to(torch.float64), weights.l1_weight / numel,
-                                        -weights.ssim_weight, with_ssim)
+        numel = h * w * nc
+        # K7 reads the rgba columns of the float32 frame in place (exact f64
+        # promotion; same values as frame[..., cols].double())
+        sums, d_rgba = _photometric_frame_dev(F.out, rgba_cols, gt.to(torch.float64),
+                                              weights.l1_weight / numel, -weights.ssim_weight,
+                                              with_ssim)
         wn = weights.normal_consistency
         wo = weights.offset_sparsity if offset else 0.0
         wb = weights.bilateral_smoothness if bilateral else 0.0

@@ -97,3 +97,24 @@ def test_fused_regularizers_match_loss_functions():
     np.testing.assert_allclose(d_out[..., 0:3], d_rgba[..., :3].astype(np.float32))
     np.testing.assert_allclose(d_out[..., 3], d_rgba[..., 3].astype(np.float32))
     assert np.all(d_out[..., 4] == 0.0)
+
+
+@pytest.mark.parametrize("with_ssim", [True, False])
+def test_photometric_frame_source_is_bit_identical(with_ssim):
+    """ivr_photometric_loss_frame (prediction read in place from a float32
+    (H,W,k) frame at a column map) == ivr_photometric_loss on the gathered
+    float64 copy, bit for bit (f32 -> f64 promotion is exact)."""
+    import torch
+    from paper_2504_17954_b200 import ShapeMismatch
+    from paper_2504_17954_b200.losses import _photometric_dev, _photometric_frame_dev
+    g = torch.Generator().manual_seed(3)
+    frame = torch.rand((67, 91, 15), generator=g).cuda()
+    gt = torch.rand((67, 91, 4), generator=g, dtype=torch.float64).cuda()
+    cols = (4, 5, 6, 11)
+    s0, d0 = _photometric_dev(frame[..., list(cols)].double(), gt, 0.3, -0.7, with_ssim)
+    s1, d1 = _photometric_frame_dev(frame, cols, gt, 0.3, -0.7, with_ssim)
+    assert torch.equal(s0, s1) and torch.equal(d0, d1)
+    with pytest.raises(ShapeMismatch):
+        _photometric_frame_dev(frame, cols[:3], gt, 0.3, -0.7, with_ssim)
+    with pytest.raises(Exception):
+        _photometric_frame_dev(frame, (0, 1, 2, 15), gt, 0.3, -0.7, with_ssim)
