@@ -421,7 +421,7 @@ int ivr_photometric_loss(const double *pred, const double *gt, int32_t height, i
 /* Same, reading the prediction in place from K3's float32 (H, W, frame_k)
  * frame: channel c = frame[pixel * frame_k + cols[c]] (cols: host array of
  * `channels` <= 4 entries) -- the trainer's rgba columns without a gather /
- * f64 copy (trainer.py:355-358 slices them out of the render). */
+ * f64 copy (trainer.py:347-352 stacks them out of the render). */
 int ivr_photometric_loss_frame(const float *frame, int32_t frame_k, const int32_t *cols,
                                const double *gt, int32_t height, int32_t width,
                                int32_t channels, const double window[11], double a, double b,
