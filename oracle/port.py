@@ -27,6 +27,8 @@ __all__ = [
     "shade", "effective_o_logit", "channel_layout", "rasterize",
     "maps", "light_dir", "rasterize_backward", "project_backward", "shade_backward", "vq_assign",
     "vq_decode", "kmeans", "sh_basis", "sh_colors", "sh_colors_backward", "ssim", "photometric_loss", "inverse_step", "Adam",
+    "pseudo_normal_from_depth", "normal_consistency_loss", "bilateral_smoothness", "stage2_step",
+    "naive_composite",
     "lib", "max_threads",
 ]
 
@@ -483,6 +485,32 @@ def rasterize(mu, q_raw, log_s, o_logit, n_raw, colors, cam, channels=("color", 
     return st
 
 
+def naive_composite(mean2d, conic, opacity, depth, values, width, height):
+    """The reference's independent test compositor (pkg/tests/oracles.py:16-43):
+    ALL splats sorted globally by depth (stable), every pixel composited
+    vectorised with the same cap / skip / stop constants; no tiles, no lists.
+    Returns (out (H,W,K), contributor count (H,W))."""
+    n, k = values.shape
+    ys, xs = np.mgrid[0:height, 0:width]
+    xs, ys = xs.astype(np.float64), ys.astype(np.float64)
+    out = np.zeros((height, width, k))
+    T = np.ones((height, width))
+    alive = np.ones((height, width), bool)
+    count = np.zeros((height, width), np.int64)
+    for i in np.argsort(depth, kind="stable"):
+        dx, dy = xs - mean2d[i, 0], ys - mean2d[i, 1]
+        a, b, c = conic[i]
+        sig = 0.5 * (a * dx * dx + c * dy * dy) + b * dx * dy
+        al = np.minimum(np.where(sig >= 0, opacity[i] * np.exp(-sig), 0.0), ALPHA_CAP)
+        m = alive & (al >= ALPHA_SKIP)
+        w = np.where(m, T * al, 0.0)
+        out += w[:, :, None] * values[i][None, None, :]
+        T = np.where(m, T * (1.0 - al), T)
+        count += m
+        alive &= T >= T_STOP
+    return out, count
+
+
 def maps(st):
     """Unpack the packed output like rasterizer.py:167-182 (in ``dtype``)."""
     out = st["out"].astype(st["dtype"])
@@ -737,6 +765,127 @@ def photometric_loss(pred, gt, l1_w=0.8, ssim_w=0.2):
         loss += ssim_w * (1.0 - s)
         d = d - ssim_w * ds
     return loss, d
+
+
+def pseudo_normal_from_depth(depth, alpha, cam, alpha_threshold=1e-3):
+    """losses.py:141-186: camera-space points from the depth map, forward
+    differences (backward on the last row/column), cross product, oriented to
+    the camera, rotated to world; mask = alpha > threshold and |n| > 1e-12."""
+    cam = ocam(cam)
+    depth, alpha = np.asarray(depth, np.float64), np.asarray(alpha, np.float64)
+    h, w = depth.shape
+    px, py = np.meshgrid(np.arange(w, dtype=np.float64), np.arange(h, dtype=np.float64))
+    cx, cy = cam.center_px
+    f = cam.focal
+    pts = np.stack([(px - cx) * depth / f, (py - cy) * depth / f, depth], axis=-1)
+    dx = np.empty_like(pts)
+    dx[:, :-1] = pts[:, 1:] - pts[:, :-1]
+    dx[:, -1] = pts[:, -1] - pts[:, -2]
+    dy = np.empty_like(pts)
+    dy[:-1] = pts[1:] - pts[:-1]
+    dy[-1] = pts[-1] - pts[-2]
+    nrm = np.cross(dx, dy)
+    ln = np.linalg.norm(nrm, axis=-1, keepdims=True)
+    good = ln[..., 0] > 1e-12
+    nrm = np.where(good[..., None], nrm / np.maximum(ln, 1e-12), 0.0)
+    away = np.sum(nrm * pts, axis=-1) > 0.0
+    nrm[away] = -nrm[away]
+    n_world = nrm @ cam.rotation
+    mask = (alpha > alpha_threshold) & good
+    n_world[~mask] = 0.0
+    return n_world, mask
+
+
+def normal_consistency_loss(normal_map, target, mask):
+    """losses.py:189-206: mean L2 distance over the mask; gradient to the map."""
+    n, t = np.asarray(normal_map, np.float64), np.asarray(target, np.float64)
+    count = int(mask.sum())
+    d_n = np.zeros_like(n)
+    if count == 0:
+        return 0.0, d_n
+    diff = (n - t)[mask]
+    ln = np.linalg.norm(diff, axis=-1)
+    safe = ln > 1e-12
+    g = np.zeros_like(diff)
+    g[safe] = diff[safe] / ln[safe, None] / count
+    d_n[mask] = g
+    return ln.sum() / count, d_n
+
+
+def bilateral_smoothness(attr_map, gt_color):
+    """losses.py:219-253 (no mask): mean |grad K| exp(-|grad c_gt|), forward
+    differences, L1 over components and directions."""
+    k, c = np.asarray(attr_map, np.float64), np.asarray(gt_color, np.float64)
+    c3 = c if c.ndim == 3 else c[..., None]
+    gxc = np.zeros(c3.shape[:2])
+    gyc = np.zeros(c3.shape[:2])
+    gxc[:, :-1] = np.sum(np.abs(c3[:, 1:] - c3[:, :-1]), axis=-1)
+    gyc[:-1] = np.sum(np.abs(c3[1:] - c3[:-1]), axis=-1)
+    count = k.shape[0] * k.shape[1]
+    weight = np.exp(-(gxc + gyc)) * np.ones(k.shape[:2], bool) / count
+    d_k = np.zeros_like(k)
+    k3 = k if k.ndim == 3 else k[..., None]
+    d3 = d_k if d_k.ndim == 3 else d_k[..., None]
+    gx = k3[:, 1:] - k3[:, :-1]
+    gy = k3[1:] - k3[:-1]
+    loss = float(np.sum(np.abs(gx).sum(-1) * weight[:, :-1]) + np.sum(np.abs(gy).sum(-1) * weight[:-1]))
+    sx = np.sign(gx) * weight[:, :-1, None]
+    sy = np.sign(gy) * weight[:-1, :, None]
+    d3[:, 1:] += sx
+    d3[:, :-1] -= sx
+    d3[1:] += sy
+    d3[:-1] -= sy
+    return loss, d_k
+
+
+def stage2_step(params, palette, light, cam, gt, nthreads=0, w_nc=0.01, w_off=0.01, w_bil=0.01,
+                w_op=0.1):
+    """trainer._stage2_step, trainer.py:397-444 with LossWeights defaults
+    (losses.py:28-37): K=15 render (colour, alpha, depth, normal, delta_c,
+    k_a, k_d, k_s, beta), photometric + normal consistency + offset sparsity +
+    bilateral smoothness x4 + opacity L1, full backward.
+    Returns (loss, grads, stat)."""
+    p = params
+    rgb, cache = shade(p["mu"], p["n_raw"], p["delta_c"], p["k_a_raw"], p["k_d_raw"],
+                       p["k_s_raw"], p["log_beta"], palette, light, cam)
+    k_a, k_d, k_s = sigmoid(p["k_a_raw"]), sigmoid(p["k_d_raw"]), sigmoid(p["k_s_raw"])
+    beta = np.exp(p["log_beta"]) + 1.0
+    attrs = {"delta_c": p["delta_c"], "k_a": k_a, "k_d": k_d, "k_s": k_s, "beta": beta}
+    st = rasterize(p["mu"], p["q_raw"], p["log_s"], p["o_logit"], p["n_raw"], rgb, cam,
+                   channels=("color", "alpha", "depth", "normal"), attrs=attrs,
+                   dtype=np.float32, nthreads=nthreads)
+    mp = maps(st)
+    rgba = np.concatenate([mp["color"].astype(np.float64),
+                           mp["alpha"].astype(np.float64)[..., None]], axis=-1)
+    loss, d_rgba = photometric_loss(rgba, gt)
+    d_maps = {"color": d_rgba[..., :3], "alpha": d_rgba[..., 3]}
+    tgt, mask = pseudo_normal_from_depth(mp["depth"], mp["alpha"], cam)
+    nl, d_n = normal_consistency_loss(mp["normal"], tgt, mask)
+    d_maps["normal"] = w_nc * d_n
+    loss += w_nc * nl
+    off = np.asarray(mp["delta_c"], np.float64)
+    loss += w_off * float(np.mean(np.abs(off)))
+    d_maps["delta_c"] = w_off * (np.sign(off) / off.size)
+    gt_rgb = np.asarray(gt)[..., :3]
+    for name in ("k_a", "k_d", "k_s", "beta"):
+        bl, dm = bilateral_smoothness(mp[name], gt_rgb)
+        loss += w_bil * bl
+        d_maps[name] = w_bil * dm
+    g = rasterize_backward(st, d_maps, nthreads=nthreads)
+    sg = shade_backward(cache, g["d_colors"])
+    da = g["d_attrs"]
+    o = sigmoid(p["o_logit"])
+    loss += w_op * float(o.mean())
+    d_o_logit = g["d_o_logit"] + w_op * (o * (1.0 - o) / o.size)
+    grads = {"mu": g["d_mu"] + sg["d_mu"], "q_raw": g["d_q_raw"], "log_s": g["d_log_s"],
+             "o_logit": d_o_logit, "n_raw": g["d_n_raw"] + sg["d_n_raw"],
+             "delta_c": sg["d_delta_c"] + da["delta_c"],
+             "k_a_raw": sg["d_k_a_raw"] + da["k_a"] * k_a * (1.0 - k_a),
+             "k_d_raw": sg["d_k_d_raw"] + da["k_d"] * k_d * (1.0 - k_d),
+             "k_s_raw": sg["d_k_s_raw"] + da["k_s"] * k_s * (1.0 - k_s),
+             "log_beta": sg["d_log_beta"] + da["beta"] * (beta - 1.0)}
+    stat = np.linalg.norm(g["d_mean2d"], axis=1) + np.linalg.norm(grads["n_raw"], axis=1)
+    return loss, grads, stat
 
 
 class Adam:

@@ -227,6 +227,7 @@ class InverseGraph:
         self.dist, self.group = dist, group
         ds = fit.ds
         dev = ds.dg.device
+        self.ws = D.Workspace(dev)
         S, V = fit.S, len(fit.cams)
         N = 4 * S + 10
         self.S, self.V, self.N, self.iters = S, V, N, int(iters)
@@ -251,6 +252,8 @@ class InverseGraph:
             P = D.frame_params(cam, self.light, params.lam, params.b,
                                rescale_opacity=not np.all(scales == 1.0))
             host += bytes(P)
+        if not host:  # a rank without views still runs the update
+            host = bytearray(nb)
         self.params_dev = torch.frombuffer(host, dtype=torch.uint8).to(dev)
         self.tab = torch.from_numpy(np.concatenate([params.c_p.reshape(-1), scales])).to(dev)
         self._init = [t.clone() for t in (self.x, self.params_dev, self.tab)]
@@ -283,7 +286,7 @@ class InverseGraph:
     def _views(self):
         """Every view: render, loss, backward, pack into self.acc."""
         L, fit, ds = self.L, self.fit, self.fit.ds
-        ws = ds.ws
+        ws = self.ws  # owned: eager renders on ds.ws cannot move captured buffers
         for v, cam in enumerate(fit.cams):
             pdev = self.params_dev[v * self.nb:(v + 1) * self.nb]
             F = D.preprocess(ds.dg, cam, 4, (0, 3, -1, -1), ws, self.shading, self.edits, None, (),
@@ -333,18 +336,22 @@ class InverseGraph:
                 self._update()
         else:  # the collective stays outside the graphs
             self.g2 = torch.cuda.CUDAGraph()
-            with torch.cuda.graph(self.g):
-                self._views()
+            if self.V:
+                with torch.cuda.graph(self.g):
+                    self._views()
             with torch.cuda.graph(self.g2):
                 self._update()
         torch.cuda.synchronize()
 
     def replay(self):
-        """One iteration."""
-        self.g.replay()
-        if self.dist is not None:
-            self._reduce()
-            self.g2.replay()
+        """One iteration (a rank without views only joins the all-reduce)."""
+        if self.dist is None:
+            self.g.replay()
+            return
+        if self.V:
+            self.g.replay()
+        self._reduce()
+        self.g2.replay()
 
     def run(self):
         """All iterations; returns (TransformParams fields as numpy, losses)."""
@@ -391,8 +398,13 @@ def optimize_to_reference(scene, params, reference_rgba, reference_cam, iters=10
     if dist:
         dist.all_reduce(n_views, group=group)
     n_views = float(n_views.item())
-    use_graph = os.environ.get("IVR_INVERSE_GRAPH", "1") != "0"
-    if use_graph and callback is None and iters > 0 and fit.cams:
+    use_graph = os.environ.get("IVR_INVERSE_GRAPH", "1") != "0" and callback is None and iters > 0
+    if dist:  # one decision for all ranks: the two paths issue different collectives
+        flag = torch.tensor([1.0 if use_graph else 0.0], dtype=torch.float64,
+                            device=fit.ds.dg.device)
+        dist.all_reduce(flag, op=dist.ReduceOp.MIN, group=group)
+        use_graph = bool(flag.item() > 0.5)
+    if use_graph:
         # whole iterations replay as CUDA graphs (no host round trip); sharded
         # views add one stream-ordered all-reduce per iteration
         G = InverseGraph(fit, params, iters, lr, learnable, dist=dist, group=group,

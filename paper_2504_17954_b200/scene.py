@@ -364,7 +364,9 @@ class FrameGraph:
         self.res = []
         for k in range(self.slots):
             self.res.append({
-                "ws": ds.ws if k == 0 else D.Workspace(dev),
+                # every slot owns its workspace: an eager render on ds.ws at
+                # another size must never reallocate buffers a graph replays
+                "ws": D.Workspace(dev),
                 # one device block per slot (one H2D per frame): params | tables
                 "d_stage": torch.empty(nb + 8 * 4 * S, dtype=torch.uint8, device=dev),
                 "stream": torch.cuda.current_stream(dev) if k == 0 else torch.cuda.Stream(device=dev),

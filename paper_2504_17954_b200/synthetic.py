@@ -18,7 +18,9 @@ SHADE_KEYS = ("delta_c", "k_a_raw", "k_d_raw", "k_s_raw", "log_beta")
 
 
 def editable_arrays(seed, n, spread=0.6, density=None, f32=False):
-    rng = np.random.default_rng(seed)
+    """``seed`` is an int or a numpy Generator (drawn in place, like the
+    reference fixtures that draw several models from one stream)."""
+    rng = seed if isinstance(seed, np.random.Generator) else np.random.default_rng(seed)
     q = rng.normal(size=(n, 4))
     mu = rng.uniform(-spread, spread, size=(n, 3))
     log_s = rng.uniform(-2.2, -0.7, size=(n, 3))

@@ -246,8 +246,15 @@ class _StageTrainer:
         self.adam.step_all(items)
 
     @torch.no_grad()
-    def densify(self, mean_stat, extent, gen):
-        """_densify_params (trainer.py:135-193) on the device."""
+    def densify(self, mean_stat, extent, rng, keep_if_empty=True):
+        """_densify_params (trainer.py:135-193) on the device.  The split
+        offsets are drawn on the host from the reference's numpy stream
+        (``rng.standard_normal((2*ns, 3))``, trainer.py:176), the same
+        Generator that picks each iteration's view, and uploaded, so a seeded
+        run follows the reference's view sequence through every split.
+        keep_if_empty: when every row would be pruned, keep the current
+        parameters (the reference's _run_stage guard, trainer.py:510-513);
+        otherwise apply (densify_and_prune returns the empty model)."""
         cfg, p = self.cfg, self.p
         n = self.n
         over = mean_stat >= cfg.densify_grad_threshold
@@ -274,18 +281,18 @@ class _StageTrainer:
             q = p["q_raw"][sp]
             q = q / torch.clamp(torch.linalg.norm(q, dim=1, keepdim=True), min=1e-12)
             R = _quat_rot_t(q)
-            offs = torch.randn((2 * ns, 3), generator=gen, dtype=torch.float64,
-                               device=self.dev) * scales[sp]
+            offs = torch.from_numpy(rng.standard_normal((2 * ns, 3))).to(self.dev) * scales[sp]
             out["mu"][-2 * ns:] = p["mu"][sp] + torch.einsum("nij,nj->ni", R, offs)
             out["log_s"][-2 * ns:] = p["log_s"][sp] - math.log(1.6)
         alive = torch.sigmoid(out["o_logit"]) >= cfg.prune_opacity_threshold
         is_new = torch.arange(parents.numel(), device=self.dev) >= keep.numel()
-        if int(alive.sum()) == 0:
-            return {"cloned": 0, "split": 0, "pruned": 0, "count": n}
+        info = {"cloned": int(c_idx.numel()), "split": int(ns),
+                "pruned": int((~alive).sum()), "count": int(alive.sum())}
+        if info["count"] == 0 and keep_if_empty:
+            return info
         self.p = {k: v[alive].contiguous() for k, v in out.items()}
         self.adam.remap(parents[alive], is_new[alive])
-        return {"cloned": int(c_idx.numel()), "split": int(ns),
-                "pruned": int((~alive).sum()), "count": self.n}
+        return info
 
     def _rgba(self, out):
         c = {name: c for name, c, w in _cols_named(self.layout)}
@@ -782,8 +789,9 @@ def densify_and_prune(model, grad_stats, cfg, extent=None, rng=None):
     """One round of adaptive density control on a scene model
     (trainer.py:241-261): clone / split (at scale / 1.6) the primitives whose
     mean gradient statistic exceeds the threshold, prune low opacity; on the
-    GPU (the trainers' ``densify``).  Split offsets come from a device
-    generator seeded from ``rng``.  Returns (new model, info)."""
+    GPU (the trainers' ``densify``).  Split offsets come from ``rng``
+    exactly as in the reference.  Returns (new model, info); an all-pruned
+    round returns the empty model with count 0."""
     rng = rng if rng is not None else np.random.default_rng(cfg.seed)
     extent = extent if extent is not None else scene_extent(np.asarray(model.geometry.mu))
     g = model.geometry
@@ -794,9 +802,10 @@ def densify_and_prune(model, grad_stats, cfg, extent=None, rng=None):
     else:
         params["sh"] = np.asarray(model.sh.coefficients, np.float64)
         tr = BaseTrainer(params, model.sh.degree, cfg)
-    gen = torch.Generator(device=tr.dev).manual_seed(int(rng.integers(2 ** 62)))
-    stats = D.to_dev(np.asarray(grad_stats, np.float64).reshape(-1))
-    info = tr.densify(stats, extent, gen)
+    stats = np.asarray(grad_stats, np.float64)
+    if stats.shape != (len(model),):
+        raise OutOfRange(f"grad stats must be ({len(model)},), got {stats.shape}")
+    info = tr.densify(D.to_dev(stats), extent, rng, keep_if_empty=False)
     if model.stage == STAGE_EDITABLE:
         new = tr.model(model.palette.c_p, dict(model.metadata))
     else:
@@ -854,7 +863,7 @@ def initialize_base(dataset, cfg, rng):
     return geom, sh
 
 
-def _run_stage(tr, dataset, cfg, iters, rng, gen, densify_start=None, decay_extra=()):
+def _run_stage(tr, dataset, cfg, iters, rng, densify_start=None, decay_extra=()):
     """The shared optimisation loop (trainer.py:463-526) over a device
     trainer: one random view per iteration, Adam with the schedules,
     densify/prune on the trailing interval's mean statistic, holdout PSNR
@@ -897,7 +906,7 @@ def _run_stage(tr, dataset, cfg, iters, rng, gen, densify_start=None, decay_extr
                 G.flush()
                 stats_sum = G.stat_sum
             if start <= it <= until:
-                tr.densify(stats_sum / max(stats_iters, 1), extent, gen)
+                tr.densify(stats_sum / max(stats_iters, 1), extent, rng)
                 G = None  # parameter tensors replaced: recapture on the next step
             elif G is not None:
                 G.stat_sum.zero_()
@@ -924,11 +933,10 @@ def train_base(dataset, cfg=None, init=None):
         raise DatasetEmpty("training needs at least two views")
     rng = np.random.default_rng(cfg.seed)
     geom, sh = init if init is not None else initialize_base(dataset, cfg, rng)
-    gen = torch.Generator(device=D.cuda_device()).manual_seed(cfg.seed)
     params = {k: getattr(geom, k) for k in GEOM}
     params["sh"] = np.asarray(sh.coefficients, np.float64)
     tr = BaseTrainer(params, sh.degree, cfg)
-    log = _run_stage(tr, dataset, cfg, cfg.stage1_iters, rng, gen)
+    log = _run_stage(tr, dataset, cfg, cfg.stage1_iters, rng)
     return tr.model({"stage1_iters": cfg.stage1_iters, "seed": cfg.seed}), log
 
 
@@ -944,7 +952,6 @@ def train_editable(base, dataset, cfg=None):
     if base.stage != STAGE_BASE:
         raise OutOfRange("stage-2 training expects a base-stage model")
     rng = np.random.default_rng(cfg.seed + 1)
-    gen = torch.Generator(device=D.cuda_device()).manual_seed(cfg.seed + 1)
     if len(dataset) < 2:
         raise DatasetEmpty("training needs at least two views")
     palette = foreground_mean_color(dataset)
@@ -953,7 +960,7 @@ def train_editable(base, dataset, cfg=None):
     params = {k: getattr(g, k) for k in GEOM}
     params.update(_stage2_init(len(g)))
     tr = EditableTrainer(params, palette, light, cfg)
-    log = _run_stage(tr, dataset, cfg, cfg.stage2_iters, rng, gen,
+    log = _run_stage(tr, dataset, cfg, cfg.stage2_iters, rng,
                      densify_start=cfg.densify_interval, decay_extra=("o_logit",))
     model = tr.model(palette, {"stage2_iters": cfg.stage2_iters, "seed": cfg.seed,
                                "light": light.to_dict(),

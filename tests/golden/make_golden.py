@@ -365,6 +365,48 @@ def dvr_case():
     print("dvr")
 
 
+def densify_case():
+    """trainer.densify_and_prune (trainer.py:241-261 -> _densify_params
+    :135-193): clone small / split large over-threshold primitives (offsets
+    from the numpy stream), budget cap, opacity prune; plus the all-pruned
+    round (empty model) and a stage-1 (SH) model."""
+    from voxsplat import trainer as ref_trainer
+    from voxsplat.gaussians import ShColor
+    d = {}
+    a = editable_arrays(51, 400, spread=0.5)
+    a["o_logit"][::7] = -9.0  # below the prune threshold
+    rng = np.random.default_rng(13)
+    stats = rng.uniform(0.0, 4e-4, 400)
+    m = model_from(a)
+    cases = {"edit": (m, ref_trainer.TrainConfig(max_primitives=500, seed=3), 30.0),
+             "nobudget": (m, ref_trainer.TrainConfig(max_primitives=400, seed=4), 0.8)}
+    geom = GaussianGeometry(*(a[k] for k in GEOM_KEYS))
+    sh = ShColor(rng.normal(0, 0.5, (400, 4, 3)), 1)
+    cases["base"] = (BasicSceneModel("base", geom, sh=sh), ref_trainer.TrainConfig(seed=5), 40.0)
+    for tag, (model, cfg, extent) in cases.items():
+        new, info = ref_trainer.densify_and_prune(model, stats, cfg, extent=extent,
+                                                  rng=np.random.default_rng(cfg.seed))
+        for k in GEOM_KEYS:
+            d[f"{tag}_{k}"] = getattr(new.geometry, k)
+        if new.shading is not None:
+            for k in SHADE_KEYS:
+                d[f"{tag}_{k}"] = getattr(new.shading, k)
+        if new.sh is not None:
+            d[f"{tag}_sh"] = new.sh.coefficients
+        for k, v in info.items():
+            d[f"{tag}_info_{k}"] = np.int64(v)
+    b = dict(a)
+    b["o_logit"] = np.full(400, -9.0)
+    new, info = ref_trainer.densify_and_prune(model_from(b), stats, ref_trainer.TrainConfig(),
+                                              extent=0.8, rng=np.random.default_rng(0))
+    d["empty_count"] = np.int64(len(new.geometry.mu))
+    for k, v in info.items():
+        d[f"empty_info_{k}"] = np.int64(v)
+    d.update({k: a[k] for k in a}, stats=stats, sh=sh.coefficients)
+    np.savez_compressed(os.path.join(HERE, "densify.npz"), **d)
+    print("densify", {k: int(v) for k, v in d.items() if "_info_" in k})
+
+
 if __name__ == "__main__":
     import sys as _sys
     if len(_sys.argv) > 1:  # regenerate selected cases only
@@ -391,3 +433,4 @@ if __name__ == "__main__":
     ivrg_case()
     display_case()
     dvr_case()
+    densify_case()

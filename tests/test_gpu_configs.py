@@ -1,0 +1,218 @@
+"""GPU parity at the BASELINE configs the bench reports.
+
+Every case runs the product path at its full size and compares it with the
+CPU oracle (oracle/, pinned bit-exactly to the real reference by
+tests/test_oracle_golden.py) on the same seeded inputs:
+
+* C2  -- composed 5 x 200k editable Gaussians (density 1M), 800x800, the
+  SURVEY 8(d) edit sequence (palette override, opacity 0.5, orbital light,
+  term scales); FAST (the bench's mode, eager and the captured FrameGraph)
+  and EXACT blends.  pair_splat, tile_ranges, contributor counts and
+  last_pos bit-exact, image within 1e-4 (north_star).
+  Reference: scene.py:231-239, rasterizer.py:88-157, _kernels.py:19-72.
+* C3  -- one stage-2 training step of a 300k model at 800x800 (K=15, all
+  regularizers): loss, every per-Gaussian gradient and the densify
+  statistic within 1e-3 relative (trainer.py:397-444).
+* C4  -- one inverse-exploration step on the composed 1M scene (float64
+  render, transform-only backward; inverse.py:161-190).
+* C5  -- VQ assign over the 60M scalar attribute values of a 4M editable
+  model at K=4096, bit-exact vs searchsorted on the float64 midpoints, and
+  decode equal to the direct codebook read (vq.py:90-134).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+IMG_TOL = 1e-4   # north_star: max abs pixel error
+GRAD_TOL = 1e-3  # north_star: relative gradient error
+W = H = 800
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2504_17954_b200 import _lib
+    _lib.lib()
+
+
+def _host_arrays(scene):
+    """Concatenated SoA + per-splat edit columns of a composed scene (what
+    the reference's apply_edits builds, scene.py:199-228)."""
+    ms = scene.models
+    a = {k: np.concatenate([getattr(m.geometry, k) for m in ms])
+         for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw")}
+    a.update({k: np.concatenate([getattr(m.shading, k) for m in ms])
+              for k in ("delta_c", "k_a_raw", "k_d_raw", "k_s_raw", "log_beta")})
+    a["palette_rgb"] = np.concatenate([
+        np.broadcast_to(e.palette_override if e.palette_override is not None else m.palette.c_p,
+                        (len(m), 3)) for m, e in zip(ms, scene.edits)])
+    a["opacity_scale"] = np.concatenate([np.full(len(m), e.opacity_scale)
+                                         for m, e in zip(ms, scene.edits)])
+    a["scene_ids"] = np.concatenate([np.full(len(m), i) for i, m in enumerate(ms)])
+    lt = scene.light
+    a["light"] = (lt.mode, lt.polar, lt.azimuth, lt.term_scales)
+    return a
+
+
+@pytest.fixture(scope="module")
+def c2():
+    import oracle as O
+    from paper_2504_17954_b200.synthetic import bench_camera, c2_scene
+    scene = c2_scene()
+    a = _host_arrays(scene)
+    cam = bench_camera(W, H, 0.8)
+    o_eff = O.effective_o_logit(a["o_logit"], a["opacity_scale"])
+    rgb, _ = O.shade(a["mu"], a["n_raw"], a["delta_c"], a["k_a_raw"], a["k_d_raw"],
+                     a["k_s_raw"], a["log_beta"], a["palette_rgb"], a["light"], cam)
+    ref = O.rasterize(a["mu"], a["q_raw"], a["log_s"], o_eff, a["n_raw"], rgb, cam,
+                      dtype=np.float32)
+    return scene, cam, ref, O.maps(ref)
+
+
+def _check_frame(F, ref, mp, tag):
+    P = int(F.n_pairs.item())
+    assert P == ref["pair_splat"].size, tag
+    assert P > 3_000_000, tag  # the headline regime: ~3.8M pairs, heavy tiles
+    assert np.array_equal(F.pairs(), ref["pair_splat"]), tag
+    assert np.array_equal(F.tile_ranges.cpu().numpy(), ref["tile_ranges"]), tag
+    assert np.array_equal(F.contrib.cpu().numpy(), ref["contrib"]), tag
+    if F.last_pos is not None:
+        assert np.array_equal(F.last_pos.cpu().numpy(), ref["last_pos"]), tag
+        assert np.abs(F.t_final.cpu().numpy() - ref["t_final"]).max() <= 1e-5, tag
+    out = F.out.cpu().numpy()
+    rgba = np.concatenate([mp["color"], mp["alpha"][..., None]], axis=-1)
+    err = float(np.abs(out - rgba).max())
+    assert err <= IMG_TOL, (tag, err)
+    return err, float(np.mean(out == rgba))
+
+
+@pytest.mark.parametrize("exact", [False, True])
+def test_c2_frame_matches_oracle(c2, exact):
+    from paper_2504_17954_b200 import DeviceScene
+    scene, cam, ref, mp = c2
+    ds = DeviceScene(scene)
+    ds.render_frame(cam, fast=False)  # learn the pair capacity
+    F = ds.render_frame(cam, fast=True, exact=exact, want_state=True)
+    assert not ds.check_overflow(F)
+    err, same = _check_frame(F, ref, mp, f"c2 exact={exact}")
+    if exact:
+        assert same > 0.999, same
+    print(f"C2 exact={exact}: max abs err {err:.3g}, identical values {same:.5f}")
+
+
+def test_c2_framegraph_matches_oracle(c2):
+    """The bench's headline path: the captured frame replayed on 2 slots."""
+    import torch
+    from paper_2504_17954_b200 import DeviceScene
+    from paper_2504_17954_b200.scene import FrameGraph
+    from paper_2504_17954_b200.synthetic import bench_camera
+    scene, cam, ref, mp = c2
+    ds = DeviceScene(scene)
+    fg = FrameGraph(ds, W, H, warm_cam=bench_camera(W, H, 0.3), slots=2)
+    F1 = fg.submit(1, cam)
+    F0 = fg.submit(0, bench_camera(W, H, 0.3))
+    torch.cuda.synchronize()
+    assert int(F1.n_pairs.item()) <= fg.capacity
+    _check_frame(F1, ref, mp, "c2 framegraph slot 1")
+    # an eager frame at another resolution must not disturb the captured slots
+    ds.render(bench_camera(1920, 1080, 0.5))
+    F1 = fg.submit(1, cam)
+    torch.cuda.synchronize()
+    _check_frame(F1, ref, mp, "c2 framegraph after eager 1080p")
+    del F0
+
+
+def test_c3_stage2_step_matches_oracle():
+    import oracle as O
+    from paper_2504_17954_b200 import LightConfig
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
+    from paper_2504_17954_b200.trainer import EditableTrainer
+    n = 300_000
+    a = editable_arrays(0, n, density=n)
+    cam = bench_camera(W, H, 1.1)
+    gt = np.random.default_rng(7).uniform(0.0, 1.0, (H, W, 4))
+    ts = np.array([1.0, 1.1, 0.9, 1.0])
+    light = LightConfig("orbital", 0.45, 0.9, ts)
+    keys = ("mu", "q_raw", "log_s", "o_logit", "n_raw", "delta_c", "k_a_raw", "k_d_raw",
+            "k_s_raw", "log_beta")
+    tr = EditableTrainer({k: a[k] for k in keys}, a["palette"], light)
+    loss, grads, stat = tr.step(cam, to_dev(gt))
+    r_loss, r_g, r_stat = O.stage2_step({k: a[k] for k in keys}, a["palette"],
+                                        ("orbital", 0.45, 0.9, ts), cam, gt)
+    assert abs(float(loss) - r_loss) <= 1e-6 * abs(r_loss), (float(loss), r_loss)
+    for k in keys:
+        got = grads[k].cpu().numpy().reshape(r_g[k].shape)
+        err = np.linalg.norm(got - r_g[k]) / max(np.linalg.norm(r_g[k]), 1e-300)
+        assert err <= GRAD_TOL, (k, err)
+    s = stat.cpu().numpy()
+    assert np.linalg.norm(s - r_stat) <= GRAD_TOL * np.linalg.norm(r_stat)
+
+
+def test_c4_inverse_step_matches_oracle(c2):
+    import oracle as O
+    from paper_2504_17954_b200.inverse import init_transform, inverse_step
+    scene, cam, _, _ = c2
+    a = _host_arrays(scene)
+    p = init_transform(scene)
+    # reference image: the known edit of SURVEY 8(d) C4 (c_p0, scale_1, lam)
+    p_true = p.copy()
+    p_true.c_p[0] = (0.2, 0.6, 0.9)
+    p_true.opacity_raw[1] = O.inv_softplus(0.5)
+    p_true.lam = np.array([1.2, 0.8, 1.0, 1.0])
+    geom = tuple(a[k] for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw"))
+    shad = tuple(a[k] for k in ("delta_c", "k_a_raw", "k_d_raw", "k_s_raw", "log_beta"))
+    ids = a["scene_ids"]
+    lt = scene.light
+
+    def oracle_render(q):
+        sc = O.softplus(q.opacity_raw)[ids]
+        o_eff = O.effective_o_logit(a["o_logit"], sc)
+        rgb, _ = O.shade(a["mu"], a["n_raw"], *shad, np.asarray(q.c_p)[ids],
+                         (lt.mode, q.polar, q.azimuth, lt.term_scales), cam,
+                         coeff_transform=(q.lam, q.b))
+        st = O.rasterize(*geom, rgb, cam, dtype=np.float64)
+        mp = O.maps(st)
+        return np.concatenate([mp["color"], mp["alpha"][..., None]], axis=-1)
+
+    reference = oracle_render(p_true)
+    loss, g = inverse_step(scene, p, cam, reference)
+    r_loss, r_g, _ = O.inverse_step(geom, shad, ids, (lt.mode, lt.polar, lt.azimuth, lt.term_scales),
+                                    p.c_p, p.opacity_raw, p.lam, p.b, p.polar, p.azimuth, cam,
+                                    reference)
+    assert abs(loss - r_loss) <= 1e-9 * abs(r_loss), (loss, r_loss)
+    for k in ("c_p", "opacity_raw", "lam", "b", "angles"):
+        ref = np.asarray(r_g[k])
+        err = np.linalg.norm(np.asarray(g[k]) - ref) / max(np.linalg.norm(ref), 1e-300)
+        assert err <= GRAD_TOL, (k, err, g[k], ref)
+
+
+def test_c5_assign_decode_60m_bit_exact():
+    import torch
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.synthetic import editable_arrays
+    from paper_2504_17954_b200.vq import QUANTIZED_ATTRIBUTES, assign_device, decode_device
+    a = editable_arrays(0, 4_000_000, density=4_000_000)
+    total = 0
+    for name, _ in QUANTIZED_ATTRIBUTES:
+        v = np.ascontiguousarray(a[name].reshape(-1))
+        # a 4096-entry sorted codebook spanning the attribute (quantiles + ties)
+        c = np.sort(np.quantile(v, np.linspace(0.0, 1.0, 4096)))
+        c[100:104] = c[100]  # duplicated centroids: searchsorted tie-breaking
+        mids = 0.5 * (c[1:] + c[:-1])
+        ref = np.searchsorted(mids, v, side="left")
+        vd, cd = to_dev(v), to_dev(c)
+        idx = assign_device(vd, cd)
+        got = idx.cpu().numpy().view(np.uint16).astype(np.int64)
+        assert np.array_equal(got, ref), name
+        dec, bad = decode_device(idx, cd)
+        assert int(bad.item()) < 0
+        assert np.array_equal(dec.cpu().numpy(), c[ref]), name
+        total += v.size
+        del vd, idx, dec
+        torch.cuda.empty_cache()
+    assert total == 60_000_000

@@ -1,0 +1,336 @@
+"""The reference's behavioural gates, run on the GPU path.
+
+Ported from the reference's own test suite (pkg/tests/): the same scenes,
+edits, iteration counts and thresholds, with the product (CUDA) path in
+place of voxsplat:
+
+* inverse fitting: self-referential edit recovery >= 35 dB after 1000
+  iterations with c_p[0] and the opacity scale within 0.05, novel-view
+  transfer, frozen primitives, descending loss windows, fixed point,
+  palette-only convex recovery, orbital light-angle recovery
+  (tests/test_inverse.py:101-200);
+* edits: invertible, and a palette edit only touches the pixels the edited
+  scene contributes to (tests/test_scene.py:123-148);
+* compositor: tile rasterizer vs the naive global-sort compositor on 50
+  random scenes at 1e-5 (tests/test_acceptance.py:154-168);
+* gradients: finite differences on 10 random scenes for every rasterizer
+  input and every shading input (tests/test_acceptance.py:80-147).
+"""
+
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module", autouse=True)
+def _cuda():
+    import torch
+    if not torch.cuda.is_available():
+        pytest.skip("no CUDA device")
+    from paper_2504_17954_b200 import _lib
+    _lib.lib()
+
+
+def psnr(a, b):
+    """metrics.psnr (metrics.py:18-29): rgb channels, capped at 99 dB."""
+    a, b = np.asarray(a, np.float64)[..., :3], np.asarray(b, np.float64)[..., :3]
+    mse = np.mean((a - b) ** 2)
+    return 99.0 if mse <= 0.0 else min(10.0 * np.log10(1.0 / mse), 99.0)
+
+
+def _camera(azimuth=0.8, size=40):
+    from paper_2504_17954_b200 import orbit_camera
+    return orbit_camera(np.zeros(3), 2.5, 0.3, azimuth, 0.9, size, size)
+
+
+def _model(rng, n, spread=0.5):
+    from paper_2504_17954_b200.synthetic import editable_model
+    return editable_model(rng, n, spread=spread)
+
+
+def _scene(seed=0, n=60, n_models=2, light=None):
+    """tests/test_inverse.py:29-32: models drawn in turn from one stream."""
+    from paper_2504_17954_b200 import ComposedScene, LightConfig
+    rng = np.random.default_rng(seed)
+    return ComposedScene.compose([_model(rng, n) for _ in range(n_models)], light or LightConfig())
+
+
+# --------------------------------------------------------------- inverse
+@pytest.fixture(scope="module")
+def self_referential_fit():
+    from paper_2504_17954_b200 import EditState
+    from paper_2504_17954_b200.inverse import (init_transform, optimize_to_reference,
+                                               render_with_transform)
+    scene = _scene(seed=1)
+    cam = _camera()
+    gt = scene.copy()
+    gt.edits[0] = EditState(palette_override=np.array([0.2, 0.6, 0.9]))
+    gt.edits[1] = EditState(opacity_scale=0.5)
+    gt_params = init_transform(gt)
+    gt_params.lam = np.array([1.2, 0.8, 1.0, 1.0])
+    ref = render_with_transform(gt, gt_params, cam, dtype=np.float64)
+    before = [m.geometry.mu.copy() for m in scene.models]
+    before += [m.shading.k_a_raw.copy() for m in scene.models]
+    fitted, losses = optimize_to_reference(scene, init_transform(scene), ref, cam, iters=1000,
+                                           lr=0.01, learnable=("c_p", "opacity_raw", "lam"))
+    return scene, gt, gt_params, cam, ref, fitted, losses, before
+
+
+def test_self_referential_edit_recovery(self_referential_fit):
+    from paper_2504_17954_b200.inverse import render_with_transform
+    scene, _, _, cam, ref, fitted, _, _ = self_referential_fit
+    img = render_with_transform(scene, fitted, cam, dtype=np.float64)
+    assert psnr(img, ref) >= 35.0
+    assert np.abs(fitted.c_p[0] - [0.2, 0.6, 0.9]).max() < 0.05
+    assert abs(fitted.opacity_scale[1] - 0.5) < 0.05
+
+
+def test_novel_view_transfer(self_referential_fit):
+    from paper_2504_17954_b200.inverse import render_with_transform
+    scene, gt, gt_params, cam, ref, fitted, _, _ = self_referential_fit
+    ref_psnr = psnr(render_with_transform(scene, fitted, cam, dtype=np.float64), ref)
+    novel = _camera(azimuth=2.1)
+    novel_gt = render_with_transform(gt, gt_params, novel, dtype=np.float64)
+    novel_psnr = psnr(render_with_transform(scene, fitted, novel, dtype=np.float64), novel_gt)
+    assert novel_psnr >= ref_psnr - 2.0
+
+
+def test_primitive_attributes_frozen(self_referential_fit):
+    scene, _, _, _, _, _, _, before = self_referential_fit
+    after = [m.geometry.mu for m in scene.models] + [m.shading.k_a_raw for m in scene.models]
+    for a, b in zip(before, after):
+        assert np.array_equal(a, b)
+
+
+def test_loss_non_increasing_over_100_iteration_windows(self_referential_fit):
+    from paper_2504_17954_b200.inverse import init_transform, optimize_to_reference
+    scene, _, _, cam, ref, _, _, _ = self_referential_fit
+    _, losses = optimize_to_reference(scene, init_transform(scene), ref, cam, iters=600, lr=0.003,
+                                      learnable=("c_p", "opacity_raw", "lam"))
+    medians = [np.median(losses[i:i + 100]) for i in range(0, len(losses), 100)]
+    assert all(b <= a for a, b in zip(medians, medians[1:]))
+
+
+def test_fixed_point_when_reference_equals_render():
+    from paper_2504_17954_b200.inverse import (init_transform, optimize_to_reference,
+                                               render_with_transform)
+    scene = _scene(seed=3, n=40, n_models=1)
+    cam = _camera()
+    ref = render_with_transform(scene, init_transform(scene), cam, dtype=np.float64)
+    fitted, losses = optimize_to_reference(scene, init_transform(scene), ref, cam, iters=60,
+                                           lr=0.01)
+    assert losses[0] < 1e-8
+    ident = init_transform(scene)
+    assert np.abs(fitted.c_p - ident.c_p).max() < 1e-3
+    assert np.abs(fitted.lam - 1.0).max() < 1e-3
+    assert np.abs(fitted.b).max() < 1e-3
+    assert np.abs(fitted.opacity_scale - 1.0).max() < 1e-3
+
+
+def test_palette_only_fit_convex_recovery():
+    from paper_2504_17954_b200 import ComposedScene, EditState, LightConfig
+    from paper_2504_17954_b200.inverse import (init_transform, optimize_to_reference,
+                                               render_with_transform)
+    m = _model(np.random.default_rng(1), 50)
+    m.shading.k_s_raw[:] = -50.0  # no specular: rendering is affine in c_p
+    scene = ComposedScene.compose([m], LightConfig())
+    cam = _camera()
+    gt = scene.copy()
+    gt.edits[0] = EditState(palette_override=np.array([0.3, 0.7, 0.4]))
+    ref = render_with_transform(gt, init_transform(gt), cam, dtype=np.float64)
+    fitted, _ = optimize_to_reference(scene, init_transform(scene), ref, cam, iters=1000, lr=0.01,
+                                      learnable=("c_p",))
+    fitted, _ = optimize_to_reference(scene, fitted, ref, cam, iters=500, lr=0.001,
+                                      learnable=("c_p",))
+    assert np.abs(fitted.c_p[0] - [0.3, 0.7, 0.4]).max() < 1e-3
+
+
+def test_orbital_light_angles_recovered():
+    from paper_2504_17954_b200 import LightConfig
+    from paper_2504_17954_b200.inverse import (init_transform, optimize_to_reference,
+                                               render_with_transform)
+    scene = _scene(seed=2, n=50, n_models=1, light=LightConfig("orbital", 0.2, 0.5))
+    cam = _camera()
+    gt = scene.copy()
+    gt.light.polar, gt.light.azimuth = 0.45, 0.9
+    ref = render_with_transform(gt, init_transform(gt), cam, dtype=np.float64)
+    fitted, _ = optimize_to_reference(scene, init_transform(scene), ref, cam, iters=800, lr=0.01)
+    assert abs(fitted.polar - 0.45) < 0.02
+    assert abs(fitted.azimuth - 0.9) < 0.02
+
+
+# --------------------------------------------------------------- edits
+def _two_models(seed, counts=(40, 30)):
+    """tests/test_scene.py:34-37: models drawn in turn from one stream."""
+    rng = np.random.default_rng(seed)
+    return [_model(rng, c, spread=0.6) for c in counts]
+
+
+def _scene_cam():
+    """tests/test_scene.py:32."""
+    from paper_2504_17954_b200 import Camera
+    return Camera.look_at((0.0, -4.0, 1.5), (0.0, 0.0, 0.0), 0.8, 48, 48)
+
+
+def test_edits_are_invertible():
+    from paper_2504_17954_b200 import ComposedScene, EditState, render_composed
+    cam = _scene_cam()
+    scene = ComposedScene.compose(_two_models(6))
+    before = render_composed(scene, cam, dtype=np.float64)
+    scene.edits[0] = EditState(palette_override=(0.9, 0.1, 0.1), opacity_scale=0.5)
+    edited = render_composed(scene, cam, dtype=np.float64)
+    assert not np.array_equal(edited.color, before.color)
+    scene.edits[0] = EditState()
+    after = render_composed(scene, cam, dtype=np.float64)
+    assert np.array_equal(after.color, before.color)
+    assert np.array_equal(after.alpha, before.alpha)
+
+
+def test_palette_edit_only_touches_contributing_pixels():
+    from paper_2504_17954_b200 import (ComposedScene, EditState, apply_edits, render_attribute_map,
+                                       render_composed)
+    cam = _scene_cam()
+    scene = ComposedScene.compose(_two_models(7))
+    eff = apply_edits(scene)
+    weight = render_attribute_map(eff.geometry, (eff.scene_ids == 1).astype(np.float64), cam,
+                                  dtype=np.float64)
+    before = render_composed(scene, cam, dtype=np.float64)
+    scene.edits[1] = EditState(palette_override=(1.0, 0.0, 0.0))
+    after = render_composed(scene, cam, dtype=np.float64)
+    untouched = weight == 0.0
+    assert untouched.any() and (~untouched).any()
+    assert np.array_equal(before.color[untouched], after.color[untouched])
+    assert not np.array_equal(before.color[~untouched], after.color[~untouched])
+
+
+def test_zero_opacity_scale_hides_a_scene():
+    from paper_2504_17954_b200 import ComposedScene, EditState, render_composed
+    cam = _scene_cam()
+    a, b = _two_models(4)
+    solo = render_composed(ComposedScene.compose([a]), cam, dtype=np.float64)
+    scene = ComposedScene.compose([a, b])
+    scene.edits[1] = EditState(opacity_scale=0.0)
+    both = render_composed(scene, cam, dtype=np.float64)
+    assert np.abs(both.color - solo.color).max() < 1e-6
+    assert np.abs(both.alpha - solo.alpha).max() < 1e-6
+
+
+# --------------------------------------------------------------- compositor
+def test_tile_rasterizer_matches_naive_compositor_on_50_scenes():
+    """tests/test_acceptance.py:154-168 (random_scene stream, 64x64, f64)."""
+    import oracle as O
+    from paper_2504_17954_b200 import GaussianGeometry, orbit_camera, rasterize_forward
+    for seed in range(50):
+        rng = np.random.default_rng(seed)
+        n = int(rng.integers(5, 501))
+        q = rng.normal(size=(n, 4))
+        mu = rng.uniform(-0.6, 0.6, size=(n, 3))
+        log_s = rng.uniform(-2.2, -0.7, size=(n, 3))
+        u = rng.uniform(0.15, 0.85, size=n)
+        n_raw = rng.normal(size=(n, 3))
+        geom = GaussianGeometry(mu, q, log_s, np.log(u / (1 - u)), n_raw)
+        colors = rng.uniform(0, 1, size=(n, 3))
+        cam = orbit_camera(np.zeros(3), 3.0, float(rng.uniform(-1.2, 1.2)),
+                           float(rng.uniform(-np.pi, np.pi)), np.pi / 3, 64, 64)
+        out, _ = rasterize_forward(geom, colors, cam, channels=("color", "alpha"),
+                                   dtype=np.float64)
+        pr = O.project(mu, q, log_s, cam)
+        keep = pr["valid"]
+        vals = np.concatenate([colors, np.ones((n, 1))], axis=1)
+        ref, _ = O.naive_composite(pr["mean2d"][keep], pr["conic"][keep],
+                                   O.sigmoid(np.log(u / (1 - u)))[keep], pr["depth"][keep],
+                                   vals[keep], 64, 64)
+        np.testing.assert_allclose(out.color, ref[..., :3], atol=1e-5, err_msg=str(seed))
+        np.testing.assert_allclose(out.alpha, ref[..., 3], atol=1e-5, err_msg=str(seed))
+
+
+# --------------------------------------------------------------- gradients
+def _fd_check(loss_fn, arr, analytic, eps=1e-4, rel=1e-3):
+    """tests/test_acceptance.py:64-77."""
+    flat = arr.reshape(-1)
+    gflat = np.asarray(analytic).reshape(-1)
+    for idx in range(flat.size):
+        orig = flat[idx]
+        flat[idx] = orig + eps
+        lp = loss_fn()
+        flat[idx] = orig - eps
+        lm = loss_fn()
+        flat[idx] = orig
+        fd = (lp - lm) / (2 * eps)
+        denom = max(abs(fd), abs(gflat[idx]), 1e-4)
+        assert abs(fd - gflat[idx]) / denom < rel, (idx, fd, gflat[idx])
+
+
+def test_rasterizer_gradients_on_random_scenes():
+    """tests/test_acceptance.py:80-110 (seed 9 skipped there: its probe step
+    crosses the alpha-skip threshold)."""
+    from paper_2504_17954_b200 import Camera, GaussianGeometry, rasterize_backward, rasterize_forward
+    cam = Camera.look_at((0, 0, -4.0), (0, 0, 0), np.pi / 3, 16, 16)
+    for seed in (0, 1, 2, 3, 4, 5, 6, 7, 8, 10):
+        rng = np.random.default_rng(seed)
+        q = rng.normal(size=(10, 4))
+        mu = rng.uniform(-0.5, 0.5, size=(10, 3))
+        log_s = rng.uniform(-2.2, -0.7, size=(10, 3))
+        u = rng.uniform(0.2, 0.8, size=10)
+        geom = GaussianGeometry(mu, q, log_s, np.log(u / (1 - u)), rng.normal(size=(10, 3)))
+        colors = rng.uniform(0.1, 0.9, size=(10, 3))
+        attrs = {"ka": rng.uniform(0.1, 0.9, size=10)}
+        w = {"color": rng.normal(size=(16, 16, 3)), "alpha": rng.normal(size=(16, 16)),
+             "depth": rng.normal(size=(16, 16)) * 0.1, "normal": rng.normal(size=(16, 16, 3)),
+             "ka": rng.normal(size=(16, 16))}
+
+        def run():
+            out, st = rasterize_forward(geom, colors, cam,
+                                        channels=("color", "alpha", "depth", "normal"),
+                                        attrs=attrs, dtype=np.float64)
+            tot = sum(float(np.sum(getattr(out, k) * w[k]))
+                      for k in ("color", "alpha", "depth", "normal"))
+            return tot + float(np.sum(out.attr["ka"] * w["ka"])), st
+
+        _, st = run()
+        g = rasterize_backward(st, w)
+
+        def loss():
+            return run()[0]
+
+        _fd_check(loss, geom.mu, g["d_mu"])
+        _fd_check(loss, geom.q_raw, g["d_q_raw"])
+        _fd_check(loss, geom.log_s, g["d_log_s"])
+        _fd_check(loss, geom.o_logit, g["d_o_logit"])
+        _fd_check(loss, geom.n_raw, g["d_n_raw"])
+        _fd_check(loss, colors, g["d_colors"])
+        _fd_check(loss, attrs["ka"], g["d_attrs"]["ka"])
+
+
+def test_shading_gradients_on_random_scenes():
+    """tests/test_acceptance.py:113-147 (both light modes, (lam, b) transform)."""
+    from paper_2504_17954_b200 import Camera, GaussianGeometry, LightConfig, shade_backward, shade_gaussians
+    for seed in range(10):
+        rng = np.random.default_rng(100 + seed)
+        mode = "headlight" if seed % 2 == 0 else "orbital"
+        n = 10
+        q = rng.normal(size=(n, 4))
+        mu = rng.uniform(-0.5, 0.5, size=(n, 3))
+        log_s = rng.uniform(-2.2, -0.7, size=(n, 3))
+        u = rng.uniform(0.15, 0.85, size=n)
+        geom = GaussianGeometry(mu, q, log_s, np.log(u / (1 - u)), rng.normal(size=(n, 3)))
+        model = _model(rng, n)
+        attrs, palette = model.shading, model.palette
+        lam = rng.uniform(0.8, 1.2, 4)
+        b = rng.uniform(-0.05, 0.05, 4)
+        light = LightConfig(mode, 0.3, 0.7, term_scales=rng.uniform(0.8, 1.2, 4))
+        cam = Camera.look_at((1.0, -3.0, 2.5), (0, 0, 0), np.pi / 3, 16, 16)
+        w = rng.normal(size=(n, 3))
+
+        def loss():
+            rgb, _, _ = shade_gaussians(geom, attrs, palette, light, cam, coeff_transform=(lam, b))
+            return float(np.sum(w * np.asarray(rgb)))
+
+        _, _, cache = shade_gaussians(geom, attrs, palette, light, cam, coeff_transform=(lam, b))
+        g = shade_backward(cache, w)
+        for arr, key in ((attrs.delta_c, "d_delta_c"), (attrs.k_a_raw, "d_k_a_raw"),
+                         (attrs.k_d_raw, "d_k_d_raw"), (attrs.k_s_raw, "d_k_s_raw"),
+                         (attrs.log_beta, "d_log_beta"), (geom.mu, "d_mu"), (geom.n_raw, "d_n_raw"),
+                         (palette.c_p, "d_c_p"), (lam, "d_lam"), (b, "d_b")):
+            _fd_check(loss, arr, g[key], eps=1e-6)

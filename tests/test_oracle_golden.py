@@ -183,3 +183,16 @@ def test_mathutil_helpers():
     np.testing.assert_allclose(M.normalize_rows(v), [[0.6, 0.8, 0.0]])
     d = M.normalize_rows_backward(v, np.array([[1.0, 0.0, 0.0]]))
     np.testing.assert_allclose(d @ M.normalize_rows(v).T, [[0.0]], atol=1e-15)
+
+
+def test_stage2_step():
+    """oracle.stage2_step (the C3 parity checker) vs the reference's
+    trainer._stage2_step (trainer.py:397-444) with all regularizers."""
+    d = golden("stage2")
+    light = ("orbital", 0.3, -0.7, np.array([1.0, 1.1, 0.9, 1.0]))
+    loss, g, stat = O.stage2_step({k: d[k] for k in GEOM + SHADE}, d["palette"], light, Cam(d),
+                                  d["gt"])
+    assert loss == float(d["loss"])
+    for k, v in g.items():
+        np.testing.assert_array_equal(v, d["g_" + k], err_msg=k)
+    np.testing.assert_array_equal(stat, d["stat"])
