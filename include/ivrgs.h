@@ -134,7 +134,12 @@ const char *ivr_last_error(void);
  * (scene.py:199-228), shading.shade_gaussians (shading.py:225-329),
  * gaussians.project_gaussians (gaussians.py:296-346) and the binning prologue
  * of rasterizer.rasterize_forward (rasterizer.py:88-121, 134-153).
- * shading / edits may be NULL.  f64_mode selects dtype=float64 semantics. */
+ * shading / edits may be NULL.  f64_mode is a bit set: IVR_PRE_F64 selects
+ * dtype=float64 semantics; IVR_PRE_EXACT_RGB keeps the float64 shading chain
+ * (the reference's rgb, rounded once to float32) when a static cache would
+ * otherwise select the float32 colour path of FAST frames. */
+#define IVR_PRE_F64 1
+#define IVR_PRE_EXACT_RGB 2
 int ivr_preprocess_fwd(const ivr_gaussians *g, const ivr_shading *shading,
                        const ivr_edits *edits, const ivr_camera *cam,
                        const ivr_layout *layout, ivr_proj_out *out,

@@ -19,6 +19,7 @@ c_double_p = ctypes.POINTER(ctypes.c_double)
 P = ctypes.c_void_p
 MAX_ATTRS = 8
 BLEND_EXACT = 1
+PRE_F64, PRE_EXACT_RGB = 1, 2  # ivr_preprocess_fwd mode bits
 BLEND_PRECULLED = 2
 BLEND_NO_GEOMETRY = 4
 

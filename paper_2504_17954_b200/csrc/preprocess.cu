@@ -20,7 +20,10 @@ constexpr int kK1Threads = 64;
 __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr_shading &S,
                                                int has_shading, const ivr_edits &E, int has_edits,
                                                const ivr_frame_params &P, const ivr_layout &L,
-                                               const ivr_proj_out &O, int f64_mode, int64_t i) {
+                                               const ivr_proj_out &O, int mode, int64_t i) {
+    // mode bit 0 (IVR_PRE_F64): dtype=float64 semantics; bit 1
+    // (IVR_PRE_EXACT_RGB): the float64 shading chain even with a static cache
+    const bool f64_mode = (mode & IVR_PRE_F64) != 0;
     const ivr_camera &cam = P.cam;
     const int32_t sid = (has_edits && E.scene_id) ? E.scene_id[i] : 0;
     const bool rescale = has_edits && P.rescale_opacity && E.opacity_scale;
@@ -69,7 +72,7 @@ __device__ __forceinline__ void preprocess_one(const ivr_gaussians &G, const ivr
     ShadeState sh;
     float rgb32[3] = {0.0f, 0.0f, 0.0f};
     // FAST mode with a shading cache and no float64 colour output: float32 colour
-    const bool fast_rgb = has_shading && !f64_mode && !O.rgb && G.cache &&
+    const bool fast_rgb = has_shading && !f64_mode && !(mode & IVR_PRE_EXACT_RGB) && !O.rgb && G.cache &&
                           G.cache[kCacheStride * i + 14] != 0.0;
     if (has_shading) {
         const double mu[3] = {G.mu[3 * i], G.mu[3 * i + 1], G.mu[3 * i + 2]};
@@ -269,7 +272,7 @@ extern "C" int ivr_preprocess_fwd(const ivr_gaussians *g, const ivr_shading *sha
         ivr::set_error("ivr_preprocess_fwd: missing output buffer or bad layout");
         return IVR_ERR_ARG;
     }
-    if (f64_mode && (!out->rec64 || !out->values64)) {
+    if ((f64_mode & IVR_PRE_F64) && (!out->rec64 || !out->values64)) {
         ivr::set_error("ivr_preprocess_fwd: float64 mode needs rec64 and values64");
         return IVR_ERR_ARG;
     }
@@ -297,7 +300,7 @@ extern "C" int ivr_preprocess_fwd_params(const ivr_gaussians *g, const ivr_shadi
     }
     if (!out->depth_key || !out->count || !out->rect || !out->rec || !out->values || layout->k < 1 ||
         layout->n_attr < 0 || layout->n_attr > IVR_MAX_ATTRS ||
-        (f64_mode && (!out->rec64 || !out->values64))) {
+        ((f64_mode & IVR_PRE_F64) && (!out->rec64 || !out->values64))) {
         ivr::set_error("ivr_preprocess_fwd_params: missing output buffer or bad layout");
         return IVR_ERR_ARG;
     }

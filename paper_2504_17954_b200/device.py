@@ -171,7 +171,8 @@ class Frame:
 
 
 def preprocess(dg: DeviceGaussians, cam, K, cols, ws: Workspace, shading=None, edits=None,
-               colors=None, attrs=(), f64=False, debug=False, stream=None, params_dev=None):
+               colors=None, attrs=(), f64=False, debug=False, stream=None, params_dev=None,
+               exact_rgb=False):
     """Launch K1; returns a Frame with the per-splat buffers.  With
     ``params_dev`` (a device tensor holding an ivr_frame_params) the camera
     and light come from device memory (CUDA-graph replay); ``cam`` then only
@@ -217,15 +218,16 @@ def preprocess(dg: DeviceGaussians, cam, K, cols, ws: Workspace, shading=None, e
     g = dg.struct()
     sh = ctypes.byref(shading) if shading is not None else None
     ed = ctypes.byref(edits) if edits is not None else None
+    mode = (L.PRE_F64 if f64 else 0) | (L.PRE_EXACT_RGB if exact_rgb else 0)
     if params_dev is not None:
         L.check(L.lib().ivr_preprocess_fwd_params(
             ctypes.byref(g), sh, ed, ptr(params_dev), int(cam.width), int(cam.height),
-            ctypes.byref(lay), ctypes.byref(out), 1 if f64 else 0, stream_handle(stream)),
+            ctypes.byref(lay), ctypes.byref(out), mode, stream_handle(stream)),
             "ivr_preprocess_fwd_params")
     else:
         cs = camera_struct(cam)
         L.check(L.lib().ivr_preprocess_fwd(ctypes.byref(g), sh, ed, ctypes.byref(cs),
-                                           ctypes.byref(lay), ctypes.byref(out), 1 if f64 else 0,
+                                           ctypes.byref(lay), ctypes.byref(out), mode,
                                            stream_handle(stream)), "ivr_preprocess_fwd")
     return F
 
@@ -439,7 +441,7 @@ def rasterize_device(dg, cam, K, cols, ws, shading=None, edits=None, colors=None
     host synchronisation: the caller checks ``F.n_pairs`` against it later;
     ``params_dev`` takes the camera / light from device memory."""
     F = preprocess(dg, cam, K, cols, ws, shading, edits, colors, attrs, f64, debug, stream,
-                   params_dev=params_dev)
+                   params_dev=params_dev, exact_rgb=exact)
     if dg.n == 0:
         F.empty = True
         return F

@@ -287,7 +287,7 @@ class DeviceScene:
             if events:
                 events[0].record()
             F = D.preprocess(self.dg, cam, K, cols, self.ws, shading, edits, None, attrs_dev, f64,
-                             debug, stream)
+                             debug, stream, exact_rgb=exact)
             if events:
                 events[1].record()
             D.bin_sort(F, self.ws, stream)
@@ -433,13 +433,15 @@ class FrameGraph:
             ws = r["ws"]
             with torch.cuda.stream(r["stream"]):
                 # allocate every workspace buffer at its final size before capture
-                F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=r["d_params"])
+                F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=r["d_params"],
+                                 exact_rgb=self.exact)
                 D.bin_sort(F, ws, capacity=self.capacity)
                 D.blend(F, ws, want_state=False, exact=self.exact)
             torch.cuda.synchronize()
             g = torch.cuda.CUDAGraph()
             with torch.cuda.graph(g):  # captured on torch's side stream, replayed on the slot's
-                F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=r["d_params"])
+                F = D.preprocess(ds.dg, cam, K, cols, ws, shading, edits, params_dev=r["d_params"],
+                                 exact_rgb=self.exact)
                 D.bin_sort(F, ws, capacity=self.capacity)
                 D.blend(F, ws, want_state=False, exact=self.exact)
             F.layout = layout
