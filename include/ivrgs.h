@@ -234,18 +234,20 @@ int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_t *order,
 
 /* K4a: blend backward.  Replaces _kernels.composite_backward
  * (_kernels.py:75-135) and the np.add.at per-Gaussian reductions
- * (rasterizer.py:240-243).  Walks each pixel's contributors front to back up
- * to last_pos with the same certified decisions as K3 (the remaining colour
- * is out - accumulated, so no division by 1 - alpha), and accumulates with
- * warp-reduced float32 atomics into caller-zeroed per-Gaussian buffers:
+ * (rasterizer.py:240-243).  Walks each pixel's contributors back to front
+ * from last_pos, recovering the transmittance from t_final by division and
+ * accumulating the colour behind each contributor as the reference does,
+ * with the same certified decisions as K3, and accumulates with warp-reduced
+ * float32 atomics into caller-zeroed per-Gaussian buffers:
  * g_values (n,k), g_mean2d (n,2), g_conic (n,3), g_opacity (n).
- * out = K3's float32 output (H,W,k); d_out (H,W,k) float32 upstream gradient.
+ * last_pos / t_final = K3's per-pixel state (H,W) int32 / float64; d_out
+ * (H,W,k) float32 upstream gradient.
  * rec64 selects dtype=float64 decisions.  tile_order (nullable): CTA -> tile
  * schedule (ivr_tile_order, heaviest first).  flags: IVR_BLEND_PRECULLED,
  * IVR_BLEND_NO_GEOMETRY. */
 int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
                   int32_t nty, const float *rec, const float *values, const double *rec64,
-                  int32_t k, int32_t width, int32_t height, const float *out,
+                  int32_t k, int32_t width, int32_t height, const double *t_final,
                   const int32_t *last_pos, const float *d_out, float *g_values,
                   float *g_mean2d, float *g_conic, float *g_opacity,
                   const int32_t *tile_order, int32_t flags, ivr_stream_t stream);
@@ -261,7 +263,7 @@ size_t ivr_blend_bwd_det_workspace_size(int64_t pair_capacity, int32_t k);
 int ivr_blend_bwd_deterministic(const int32_t *tile_ranges, const int32_t *pair_splat,
                                 int32_t ntx, int32_t nty, const float *rec, const float *values,
                                 const double *rec64, int32_t k, int32_t width, int32_t height,
-                                const float *out, const int32_t *last_pos, const float *d_out,
+                                const double *t_final, const int32_t *last_pos, const float *d_out,
                                 int64_t n, const uint64_t *depth_key, const int32_t *count,
                                 const uint16_t *rect, int64_t pair_capacity, void *workspace,
                                 size_t workspace_bytes, float *g_values, float *g_mean2d,
@@ -275,7 +277,7 @@ int ivr_blend_bwd_deterministic(const int32_t *tile_ranges, const int32_t *pair_
  * warp partials.  workspace: ivr_blend_bwd_det_workspace_size(n_pairs, k). */
 int ivr_blend_bwd_pairs(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
                         int32_t nty, const float *rec, const float *values, const double *rec64,
-                        int32_t k, int32_t width, int32_t height, const float *out,
+                        int32_t k, int32_t width, int32_t height, const double *t_final,
                         const int32_t *last_pos, const float *d_out, int64_t n_pairs,
                         void *workspace, size_t workspace_bytes, float *pair_grads,
                         ivr_stream_t stream);

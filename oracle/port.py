@@ -839,7 +839,7 @@ def bilateral_smoothness(attr_map, gt_color):
 
 
 def stage2_step(params, palette, light, cam, gt, nthreads=0, w_nc=0.01, w_off=0.01, w_bil=0.01,
-                w_op=0.1):
+                w_op=0.1, aux=None):
     """trainer._stage2_step, trainer.py:397-444 with LossWeights defaults
     (losses.py:28-37): K=15 render (colour, alpha, depth, normal, delta_c,
     k_a, k_d, k_s, beta), photometric + normal consistency + offset sparsity +
@@ -885,6 +885,8 @@ def stage2_step(params, palette, light, cam, gt, nthreads=0, w_nc=0.01, w_off=0.
              "k_s_raw": sg["d_k_s_raw"] + da["k_s"] * k_s * (1.0 - k_s),
              "log_beta": sg["d_log_beta"] + da["beta"] * (beta - 1.0)}
     stat = np.linalg.norm(g["d_mean2d"], axis=1) + np.linalg.norm(grads["n_raw"], axis=1)
+    if aux is not None:  # intermediates for diagnostics
+        aux.update(raster=g, d_maps=d_maps, state=st)
     return loss, grads, stat
 
 

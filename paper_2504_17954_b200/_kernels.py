@@ -120,7 +120,8 @@ def composite_backward(tile_ranges, pair_splat, mean2d, conic, opacity, values, 
     """Per-pair gradients of composite_forward (_kernels.py:75-135) into the
     caller's (zeroed) pair_dv (P,K), pair_dmean (P,2), pair_dconic (P,3),
     pair_dopac (P,).  The forward is re-run on the device (EXACT, identical
-    decisions) for the colour the front-to-back backward needs."""
+    decisions) for the blend records; the walk starts from the caller's
+    t_final, back to front like the reference."""
     _check_tile(tile_size)
     tr, ps, R, o32, o64, cnt, last, tf, K, nty = _forward(
         tile_ranges, pair_splat, mean2d, conic, opacity, values, width, height, ntx)
@@ -133,10 +134,11 @@ def composite_backward(tile_ranges, pair_splat, mean2d, conic, opacity, values, 
     nb = int(L.lib().ivr_blend_bwd_det_workspace_size(P, K))
     ws = torch.empty(max(nb, 8), dtype=torch.uint8, device=d.device)
     g = torch.empty((P, K + 6), dtype=torch.float32, device=d.device)
+    tfd = _t(np.asarray(t_final, np.float64).reshape(int(height), int(width)), torch.float64)
     L.check(L.lib().ivr_blend_bwd_pairs(D.ptr(tr), D.ptr(ps), int(ntx), nty, D.ptr(R["rec"]),
                                         D.ptr(R["values"]), D.ptr(R.get("rec64")), K,
-                                        int(width), int(height), D.ptr(o32.contiguous()),
-                                        D.ptr(last), D.ptr(d), P, D.ptr(ws), nb, D.ptr(g),
+                                        int(width), int(height), D.ptr(tfd), D.ptr(last), D.ptr(d),
+                                        P, D.ptr(ws), nb, D.ptr(g),
                                         D.stream_handle()), "ivr_blend_bwd_pairs")
     h = g.double().cpu().numpy()
     pair_dv += h[:, :K]

@@ -4,16 +4,17 @@
 // (_kernels.py:75-135) + the per-Gaussian np.add.at reductions
 // (rasterizer.py:240-243).  One CTA per tile, one thread per pixel, each warp
 // an independent 8x4 pixel block that streams the tile list in 32-pair chunks
-// with the K3 strip cull; each pixel walks its contributors FRONT to back up
-// to last_pos (known from the forward).  With
-// C = forward output and A_i = colour accumulated through contributor i, the
-// colour behind i is C - A_i, so
-//   dL/dalpha_i = sum_k dout_k (T_i v_ik - (C_k - A_ik) / (1 - alpha_i)),
-// the same quantity the reference obtains by walking back to front and
-// recovering T by division.  Decisions (skip / contribute) use the certified
-// float32-with-bound test of K3, so the contributor set is the reference's.
-// Per (splat, warp) the 32 pixel contributions are warp-reduced and added
-// with one float32 atomic per component.
+// with the K3 strip cull; each pixel walks its contributors BACK to front
+// from last_pos, as the reference does: the transmittance in front of
+// contributor i is recovered from the forward's t_final by division,
+// T_i = T_{i+1} / (1 - alpha_i), and the colour behind i is the suffix sum
+// accumulated on the way (small terms first, so it keeps its relative
+// precision where the front-to-back form C - A_i cancels), giving
+//   dL/dalpha_i = sum_k dout_k (T_i v_ik - suffix_ik / (1 - alpha_i)).
+// Decisions (skip / contribute) use the certified float32-with-bound test of
+// K3, so the contributor set is the reference's.  Per (splat, warp) the 32
+// pixel contributions are warp-reduced and added with one float32 atomic per
+// component.
 //
 // K4b preprocess_bwd_kernel (one thread per Gaussian, float64) chains the
 // per-Gaussian accumulators through conic -> cov2d, the channel unpack,
@@ -36,7 +37,7 @@ struct BwdArgs {
     const float *values;
     const double *rec64;
     int K, W, H;
-    const float *out;
+    const double *t_final;
     const int32_t *last_pos;
     const float *d_out;
     float *g_values, *g_mean, *g_conic, *g_opac;
@@ -146,17 +147,14 @@ blend_bwd_kernel(BwdArgs A) {
     const int last = inside ? A.last_pos[pix] : s0;
     const int stop = __reduce_max_sync(0xffffffffu, last);  // no pixel of the warp contributes past here
 
-    // d alpha_i = sum_k dout_k (T_i v_ik - (C_k - A_ik) / (1 - alpha_i)) only
-    // needs the dot products D_i = dout . v_i and S = dout . (C - A): with
-    // S_C = dout . C per pixel and a running S_A = dout . A, no per-channel
-    // accumulator is carried
+    // d alpha_i = sum_k dout_k (T_i v_ik - suffix_ik / (1 - alpha_i)) only
+    // needs the dot products D_i = dout . v_i and the scalar suffix
+    // S_i = dout . suffix_i = sum_{j > i} w_j D_j, accumulated back to front
     float dout[KMAX];
-    float S_C = 0.0f, S_A = 0.0f;
+    float S = 0.0f;
 #pragma unroll
     for (int c = 0; c < KMAX; ++c) {
-        const float Cc = (inside && c < K) ? A.out[pix * K + c] : 0.0f;
         dout[c] = (inside && c < K) ? A.d_out[pix * K + c] : 0.0f;
-        S_C = fmaf(dout[c], Cc, S_C);
         W.dout[lane * KMAX + c] = dout[c];
     }
     int nbat = 0;  // pairs in the deferred value batch (warp-uniform)
@@ -222,14 +220,15 @@ blend_bwd_kernel(BwdArgs A) {
         gbase = A.g_opac;
         gstride = 1;
     }
-    float T = 1.0f;
+    float T = inside && last > s0 ? (float)A.t_final[pix] : 0.0f;  // behind the last contributor
     const float fpx = (float)px, fpy = (float)py;
     const double dpx = (double)px, dpy = (double)py;
 
     int sp = 0;
     float4 r0 = make_float4(0.f, 0.f, 0.f, 0.f), r1 = r0;
     // two-stage prefetch as in K3: ids one chunk ahead of their records
-    // (bit 31: culled for this tile by ivr_bin_sort_cull; -1 past the stop)
+    // (bit 31: culled for this tile by ivr_bin_sort_cull; -1 past the stop),
+    // chunks visited from the last one back to the tile start
     auto fetch_ids = [&](int base) {
         const int j = base + lane;
         return j < stop ? __ldg(A.pair_splat + j) : -1;
@@ -241,12 +240,13 @@ blend_bwd_kernel(BwdArgs A) {
             r1 = __ldg(A.rec + 2 * id + 1);
         }
     };
+    const int top = s0 < stop ? s0 + 32 * ((stop - 1 - s0) / 32) : s0 - 32;  // last chunk
     int spn = -1;
-    if (s0 < stop) {
-        fetch_recs(fetch_ids(s0));
-        if (s0 + 32 < stop) spn = fetch_ids(s0 + 32);
+    if (top >= s0) {
+        fetch_recs(fetch_ids(top));
+        if (top - 32 >= s0) spn = fetch_ids(top - 32);
     }
-    for (int base = s0; base < stop; base += 32) {
+    for (int base = top; base >= s0; base -= 32) {
         const int j = base + lane;
         const bool keep = j < stop && sp >= 0 && !tile_cull32(r0, r1, sx0, sx1, sy0, sy1);
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
@@ -264,14 +264,14 @@ blend_bwd_kernel(BwdArgs A) {
             }
         }
         __syncwarp();
-        if (base + 32 < stop) {
+        if (base - 32 >= s0) {
             fetch_recs(spn);
-            spn = base + 64 < stop ? fetch_ids(base + 64) : -1;
+            spn = base - 64 >= s0 ? fetch_ids(base - 64) : -1;
         }
         uint32_t mbits = m;
-        while (mbits) {
-            const int q = __ffs(mbits) - 1;
-            mbits &= mbits - 1;
+        while (mbits) {  // back to front inside the chunk
+            const int q = 31 - __clz(mbits);
+            mbits &= ~(1u << q);
             const float4 a0 = W.r0[q];
             const float4 a1 = W.r1[q];
             bool contrib = false;
@@ -327,8 +327,13 @@ blend_bwd_kernel(BwdArgs A) {
 #pragma unroll
             for (int c = 0; c < 8; ++c) xg[c] = 0.f;
             if (contrib) {
+                // T in front of this contributor: T / (1 - alpha) (approximate
+                // reciprocal + one Newton step, ~0.5 ulp)
+                const float om = 1.0f - al;
+                float inv = rcp_approx_b(om);
+                inv = fmaf(inv, fmaf(-om, inv, 1.0f), inv);
+                T = T * inv;
                 const float w = T * al;
-                const float inv = rcp_approx_b(1.0f - al);
                 float Dv = 0.f;  // dout . v
                 if (KMAX % 4 == 0) {
                     const float4 *vv = reinterpret_cast<const float4 *>(W.v + q * KMAX);
@@ -345,8 +350,8 @@ blend_bwd_kernel(BwdArgs A) {
                     for (int c = 0; c < KMAX; ++c) Dv = fmaf(dout[c], W.v[q * KMAX + c], Dv);
                 }
                 wpix = w;
-                S_A = fmaf(w, Dv, S_A);  // dout . A after this contributor
-                const float d_alpha = T * Dv - (S_C - S_A) * inv;
+                const float d_alpha = T * Dv - S * inv;
+                S = fmaf(w, Dv, S);  // suffix seen by the contributors in front
                 if (alu < 0.99f) {
                     if (GEOM) {
                         const float d_sigma = -alu * d_alpha;
@@ -359,7 +364,6 @@ blend_bwd_kernel(BwdArgs A) {
                     }
                     xg[5] = g * d_alpha;
                 }
-                T = T * (1.0f - al);
             }
             if (__any_sync(0xffffffffu, contrib)) {
                 // value gradients: this pair's pixel weights join the batch;
@@ -817,12 +821,12 @@ ivr_frame_params params_from(const ivr_camera &cam, const ivr_shading *S, const 
 namespace {
 int blend_bwd_impl(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
                    int32_t nty, const float *rec, const float *values, const double *rec64,
-                   int32_t k, int32_t width, int32_t height, const float *out,
+                   int32_t k, int32_t width, int32_t height, const double *t_final,
                    const int32_t *last_pos, const float *d_out, float *g_values, float *g_mean2d,
                    float *g_conic, float *g_opacity, const int32_t *tile_order, int32_t flags,
                    float *part, ivr_stream_t stream) {
     using namespace ivr;
-    if (!tile_ranges || !pair_splat || !rec || !values || !out || !last_pos || !d_out ||
+    if (!tile_ranges || !pair_splat || !rec || !values || !t_final || !last_pos || !d_out ||
         !g_values || !g_opacity || k < 1 || k > 32 ||
         (!(flags & IVR_BLEND_NO_GEOMETRY) && (!g_mean2d || !g_conic)) ||
         ntx != (width + kTile - 1) / kTile || nty != (height + kTile - 1) / kTile) {
@@ -839,7 +843,7 @@ int blend_bwd_impl(const int32_t *tile_ranges, const int32_t *pair_splat, int32_
     A.K = k;
     A.W = width;
     A.H = height;
-    A.out = out;
+    A.t_final = t_final;
     A.last_pos = last_pos;
     A.d_out = d_out;
     A.g_values = g_values;
@@ -865,11 +869,11 @@ int blend_bwd_impl(const int32_t *tile_ranges, const int32_t *pair_splat, int32_
 extern "C" int ivr_blend_bwd(const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx,
                              int32_t nty, const float *rec, const float *values,
                              const double *rec64, int32_t k, int32_t width, int32_t height,
-                             const float *out, const int32_t *last_pos, const float *d_out,
+                             const double *t_final, const int32_t *last_pos, const float *d_out,
                              float *g_values, float *g_mean2d, float *g_conic, float *g_opacity,
                              const int32_t *tile_order, int32_t flags, ivr_stream_t stream) {
     return blend_bwd_impl(tile_ranges, pair_splat, ntx, nty, rec, values, rec64, k, width, height,
-                          out, last_pos, d_out, g_values, g_mean2d, g_conic, g_opacity,
+                          t_final, last_pos, d_out, g_values, g_mean2d, g_conic, g_opacity,
                           tile_order, flags, nullptr, stream);
 }
 
@@ -881,7 +885,7 @@ extern "C" size_t ivr_blend_bwd_det_workspace_size(int64_t pair_capacity, int32_
 extern "C" int ivr_blend_bwd_deterministic(
     const int32_t *tile_ranges, const int32_t *pair_splat, int32_t ntx, int32_t nty,
     const float *rec, const float *values, const double *rec64, int32_t k, int32_t width,
-    int32_t height, const float *out, const int32_t *last_pos, const float *d_out,
+    int32_t height, const double *t_final, const int32_t *last_pos, const float *d_out,
     int64_t n, const uint64_t *depth_key, const int32_t *count, const uint16_t *rect,
     int64_t pair_capacity, void *workspace, size_t workspace_bytes, float *g_values,
     float *g_mean2d, float *g_conic, float *g_opacity, const int32_t *tile_order, int32_t flags,
@@ -899,7 +903,7 @@ extern "C" int ivr_blend_bwd_deterministic(
         return IVR_ERR_CUDA;
     }
     const int rc = blend_bwd_impl(tile_ranges, pair_splat, ntx, nty, rec, values, rec64, k, width,
-                                  height, out, last_pos, d_out, g_values, g_mean2d, g_conic,
+                                  height, t_final, last_pos, d_out, g_values, g_mean2d, g_conic,
                                   g_opacity, tile_order, flags, (float *)workspace, stream);
     if (rc != IVR_OK || n == 0) return rc;
     bwd_reduce_det_kernel<<<(unsigned)((n + 127) / 128), 128, 0, st>>>(
@@ -924,7 +928,7 @@ pair_sum_kernel(const float *part, int64_t npairs, int stride, float *pair_out) 
 extern "C" int ivr_blend_bwd_pairs(const int32_t *tile_ranges, const int32_t *pair_splat,
                                    int32_t ntx, int32_t nty, const float *rec,
                                    const float *values, const double *rec64, int32_t k,
-                                   int32_t width, int32_t height, const float *out,
+                                   int32_t width, int32_t height, const double *t_final,
                                    const int32_t *last_pos, const float *d_out, int64_t n_pairs,
                                    void *workspace, size_t workspace_bytes, float *pair_grads,
                                    ivr_stream_t stream) {
@@ -944,7 +948,7 @@ extern "C" int ivr_blend_bwd_pairs(const int32_t *tile_ranges, const int32_t *pa
     // the walk only writes the partials in this mode; the per-Gaussian
     // accumulator arguments are never touched (any valid pointer passes)
     const int rc = blend_bwd_impl(tile_ranges, pair_splat, ntx, nty, rec, values, rec64, k,
-                                  width, height, out, last_pos, d_out, pair_grads, pair_grads,
+                                  width, height, t_final, last_pos, d_out, pair_grads, pair_grads,
                                   pair_grads, pair_grads, nullptr, 0, (float *)workspace, stream);
     if (rc != IVR_OK) return rc;
     const int stride = k + 6;

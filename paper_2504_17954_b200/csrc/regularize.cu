@@ -44,20 +44,23 @@ __device__ __forceinline__ double depth_at(const Args &A, int y, int x) {
     return (double)A.out[((int64_t)y * A.W + x) * A.K + A.c_depth];
 }
 
-// camera-space point of pixel (y, x) (losses.py:157-161 order: (px - cx) * d / f)
-// (px - cx) * d / f with 1/f hoisted (one ulp from the reference's division;
-// the pseudo normal is normalised afterwards)
-__device__ __forceinline__ void point(const Args &A, double inv_f, double cx, double cy, int y,
-                                      int x, double p[3]) {
+// camera-space point of pixel (y, x), evaluated as numpy does
+// (losses.py:157-161: (px - cx) * d / f, each operation rounded).  The pseudo
+// normal is a cross product of neighbour differences: where the surface is
+// nearly flat those differences cancel and one ulp in a point moves the normal
+// (and the mask / facing decisions) visibly, so every step keeps the
+// reference's rounding.
+__device__ __forceinline__ void point(const Args &A, double f, double cx, double cy, int y, int x,
+                                      double p[3]) {
     const double d = depth_at(A, y, x);
-    p[0] = ((double)x - cx) * d * inv_f;
-    p[1] = ((double)y - cy) * d * inv_f;
+    p[0] = ((double)x - cx) * d / f;
+    p[1] = ((double)y - cy) * d / f;
     p[2] = d;
 }
 
 // pseudo normal (world) at (y, x) and whether it is in the mask
 __device__ __forceinline__ bool pseudo_normal(const Args &A, int y, int x, double nw[3]) {
-    const double f = 1.0 / A.camp[0], cx = A.camp[1], cy = A.camp[2];  // f holds 1/focal
+    const double f = A.camp[0], cx = A.camp[1], cy = A.camp[2];
     const double *rot = A.camp + 3;
     double p[3], q[3], dx[3], dy[3];
     point(A, f, cx, cy, y, x, p);
@@ -77,15 +80,17 @@ __device__ __forceinline__ bool pseudo_normal(const Args &A, int y, int x, doubl
         point(A, f, cx, cy, y - 1, x, r);
         for (int k = 0; k < 3; ++k) dy[k] = p[k] - r[k];
     }
+    // np.cross (products rounded, then the difference)
     double n[3] = {dx[1] * dy[2] - dx[2] * dy[1], dx[2] * dy[0] - dx[0] * dy[2],
                    dx[0] * dy[1] - dx[1] * dy[0]};
+    // np.linalg.norm: sqrt((n0^2 + n1^2) + n2^2); n / max(norm, 1e-12)
     const double nn = sqrt(n[0] * n[0] + n[1] * n[1] + n[2] * n[2]);
     const bool good = nn > 1e-12;
-    const double inv_nn = good ? 1.0 / nn : 0.0;
-    for (int k = 0; k < 3; ++k) n[k] = n[k] * inv_nn;
+    for (int k = 0; k < 3; ++k) n[k] = good ? n[k] / fmax(nn, 1e-12) : 0.0;
     if (n[0] * p[0] + n[1] * p[1] + n[2] * p[2] > 0.0)
         for (int k = 0; k < 3; ++k) n[k] = -n[k];
-    for (int j = 0; j < 3; ++j) nw[j] = n[0] * rot[j] + n[1] * rot[3 + j] + n[2] * rot[6 + j];
+    // n @ R (OpenBLAS dgemm: the k-ascending FMA chain, ivr_common.cuh chain3)
+    for (int j = 0; j < 3; ++j) nw[j] = fma(n[2], rot[6 + j], fma(n[1], rot[3 + j], n[0] * rot[j]));
     const double alpha = (double)A.out[((int64_t)y * A.W + x) * A.K + A.c_alpha];
     return good && alpha > 1e-3;
 }
@@ -131,7 +136,7 @@ __global__ void __launch_bounds__(kThreads) mask_count_kernel(Args A) {
             A.nmap[i] = make_double4(nw[0], nw[1], nw[2], (double)c);
         }
         if (A.w_bil > 0.0 && A.n_bil > 0)
-            A.wmap[i] = edge_weight(A, y, x) * (1.0 / ((double)A.H * A.W));
+            A.wmap[i] = edge_weight(A, y, x) / ((double)A.H * A.W);  // losses.py:239
     }
     c = __reduce_add_sync(0xffffffffu, c);
     if ((threadIdx.x & 31) == 0 && c) atomicAdd(&s_c, c);

@@ -334,7 +334,8 @@ def blend_backward(F: Frame, d_out, stream=None, deterministic=None, geometry=Tr
     arena = torch.zeros(n * (K + 6), dtype=torch.float32, device=dev)  # one memset
     g = {"values": arena[:n * K], "mean2d": arena[n * K:n * (K + 2)],
          "conic": arena[n * (K + 2):n * (K + 5)], "opacity": arena[n * (K + 5):]}
-    out = F.out if not F.f64 else F.out64.float()
+    if F.t_final is None:
+        raise ValueError("blend_backward needs the forward state (render with want_state=True)")
     d_out = d_out.to(torch.float32).contiguous()
     cam = F.cam
     if deterministic:
@@ -342,7 +343,7 @@ def blend_backward(F: Frame, d_out, stream=None, deterministic=None, geometry=Tr
         ws = torch.empty(max(nb, 8), dtype=torch.uint8, device=dev)
         L.check(L.lib().ivr_blend_bwd_deterministic(
             ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec), ptr(F.values),
-            ptr(F.rec64), K, cam.width, cam.height, ptr(out), ptr(F.last_pos), ptr(d_out), n,
+            ptr(F.rec64), K, cam.width, cam.height, ptr(F.t_final), ptr(F.last_pos), ptr(d_out), n,
             ptr(F.depth_key), ptr(F.count), ptr(F.rect), F.capacity, ptr(ws), nb,
             ptr(g["values"]), ptr(g["mean2d"]), ptr(g["conic"]), ptr(g["opacity"]),
             ptr(getattr(F, "tile_order", None)),
@@ -351,8 +352,9 @@ def blend_backward(F: Frame, d_out, stream=None, deterministic=None, geometry=Tr
             stream_handle(stream)), "ivr_blend_bwd_deterministic")
         return g
     L.check(L.lib().ivr_blend_bwd(ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec),
-                                  ptr(F.values), ptr(F.rec64), K, cam.width, cam.height, ptr(out),
-                                  ptr(F.last_pos), ptr(d_out), ptr(g["values"]), ptr(g["mean2d"]),
+                                  ptr(F.values), ptr(F.rec64), K, cam.width, cam.height,
+                                  ptr(F.t_final), ptr(F.last_pos), ptr(d_out), ptr(g["values"]),
+                                  ptr(g["mean2d"]),
                                   ptr(g["conic"]), ptr(g["opacity"]),
                                   ptr(getattr(F, "tile_order", None)),
                                   (L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0) |

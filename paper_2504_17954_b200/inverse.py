@@ -133,18 +133,26 @@ class InverseFitter:
                                     palettes=params.c_p, opacity_scales=params.opacity_scale,
                                     exact=self.exact)
 
-    def view_grads(self, params, v):
-        """(loss, packed gradient (4S+10,) float64 device tensor) for view v."""
+    def view_grads(self, params, v, events=None):
+        """(loss, packed gradient (4S+10,) float64 device tensor) for view v.
+        ``events``: 5 CUDA events around render (K1-K3), loss (K7), K4a, K4b."""
+        rec = (lambda j: events[j].record()) if events else (lambda j: None)
         cam, ref = self.cams[v], self.refs[v]
+        rec(0)
         F = self.render(params, cam, want_state=True)
+        rec(1)
         rgba = F.out64 if F.f64 else F.out.double()
         loss, d = photometric_loss_t(rgba, ref)
+        rec(2)
         g = D.blend_backward(F, d, geometry=False)
+        rec(3)
+        self._last_pairs = F.n_pairs
         shading, edits = F._keep_tabs
         light = _light(self.scene, params)
         out, _ = D.preprocess_backward(self.ds.dg, cam, 4, (0, 3, -1, -1), g=g, shading=shading,
                                        edits=edits, geometry=False, want=("d_c_p", "d_scale", "d_globals"),
                                        per_scene=self.S, light=light)
+        rec(4)
         S = self.S
         sig = torch.from_numpy(_sigmoid(params.opacity_raw)).to(out["d_scale"].device)
         gl = out["d_globals"]

@@ -223,6 +223,11 @@ class _StageTrainer:
         self.ws = D.Workspace(self.dev)
         self._bad = None
         self._first_bad = None
+        # blend mode of the training forward: FAST (certified float32, the
+        # default) or EXACT (the reference's float64 arithmetic, bit-faithful
+        # maps: the loss terms built on sign() / normalisation then see the
+        # reference's exact inputs)
+        self.exact = False
 
     @property
     def n(self):
@@ -425,7 +430,7 @@ class BaseTrainer(_StageTrainer):
         dg = self._dg()
         rgb = sh_eval_device(self.p["mu"], self.p["sh"], self.degree, cam.position)
         F = D.rasterize_device(dg, cam, self.K, self.cols, self.ws, colors=rgb, f64=False,
-                               want_state=want_state, exact=False)
+                               want_state=want_state, exact=self.exact)
         return F, dg
 
     def step(self, cam, gt, weights=None):
@@ -496,29 +501,40 @@ class EditableTrainer(_StageTrainer):
                      for name, c, w in self.attr_cols]
         F = D.rasterize_device(dg, cam, self.K, self.cols, graph.ws if graph else self.ws,
                                shading=S, attrs=attrs_dev, f64=False, want_state=want_state,
-                               exact=False, params_dev=graph.params_dev if graph else None,
+                               exact=self.exact, params_dev=graph.params_dev if graph else None,
                                capacity=graph.capacity if graph else None)
         return F, S, attrs, dg
 
-    def step(self, cam, gt, weights=None, graph=None):
+    def step(self, cam, gt, weights=None, graph=None, events=None):
         """One _stage2_step (trainer.py:397-444): (loss, grads, densify stat),
         all device tensors.  ``graph``: the StepGraph being captured (camera
-        and pseudo-normal block from its device buffers, no host sync)."""
+        and pseudo-normal block from its device buffers, no host sync).
+        ``events``: 6 CUDA events recorded around forward (K14 attrs + K1-K3),
+        losses (K7 + K10), K4a, K4b and assembly/loss (K14) -- the bench's
+        per-kernel split."""
         weights = weights or self.cfg.weights
+        rec = (lambda j: events[j].record()) if events else (lambda j: None)
+        rec(0)
         F, S, attrs, dg = self.forward(cam, graph=graph)
+        rec(1)
         lt, keep, d_out, c = self._map_terms(F, cam, gt, weights, offset=True, bilateral=True,
                                              cam_dev=graph.cam_dev if graph else None)
+        rec(2)
         g = D.blend_backward(F, d_out)
+        rec(3)
         want = ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_mean2d", "d_values",
                 "d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta")
         gr, bad = D.preprocess_backward(dg, cam, self.K, self.cols, g=g, shading=S, geometry=True,
                                         want=want, light=self.light,
                                         params_dev=graph.params_dev if graph else None)
+        rec(4)
         if graph is not None:
             graph.n_pairs = F.n_pairs
         n = self.n
         stat, part = self._assemble(gr, c, weights, shading=True)
         loss = self._finalize(lt, part, weights.opacity_l1)
+        rec(5)
+        self._last_pairs = F.n_pairs
         grads = {"mu": gr["d_mu"].view(n, 3), "q_raw": gr["d_q_raw"].view(n, 4),
                  "log_s": gr["d_log_s"].view(n, 3), "o_logit": gr["d_o_logit"],
                  "n_raw": gr["d_n_raw"].view(n, 3), "delta_c": gr["d_delta_c"].view(n, 3),
