@@ -131,10 +131,12 @@ class ClockSampler:
 # ------------------------------------------------------------------ CPU side
 def cpu_frames(scene_arrays, cam, frames, nthreads=0):
     """The reference algorithm for one C2 frame on the host (oracle/ port:
-    numpy per-Gaussian math + C/OpenMP compositor).  Returns (sec/frame, threads)."""
+    numpy per-Gaussian math + C/OpenMP compositor).  Returns (sec/frame,
+    threads, last frame's state)."""
     import oracle as O
     a = scene_arrays
     times = []
+    st = None
     for _ in range(frames):
         t0 = time.perf_counter()
         o_eff = O.effective_o_logit(a["o_logit"], a["opacity_scale"])
@@ -142,9 +144,9 @@ def cpu_frames(scene_arrays, cam, frames, nthreads=0):
                          a["k_s_raw"], a["log_beta"], a["palette_rgb"], a["light"], cam)
         st = O.rasterize(a["mu"], a["q_raw"], a["log_s"], o_eff, a["n_raw"], rgb, cam,
                          dtype=np.float32, nthreads=nthreads)
-        O.maps(st)
+        st["maps"] = O.maps(st)
         times.append(time.perf_counter() - t0)
-    return float(np.mean(times)), O.max_threads() if nthreads <= 0 else nthreads
+    return float(np.mean(times)), O.max_threads() if nthreads <= 0 else nthreads, st
 
 
 def host_scene_arrays(scene):
@@ -158,9 +160,103 @@ def host_scene_arrays(scene):
                         (len(m), 3)) for m, e in zip(models, scene.edits)])
     cat["opacity_scale"] = np.concatenate([np.full(len(m), e.opacity_scale)
                                            for m, e in zip(models, scene.edits)])
+    cat["scene_ids"] = np.concatenate([np.full(len(m), i) for i, m in enumerate(models)])
     lt = scene.light
     cat["light"] = (lt.mode, lt.polar, lt.azimuth, lt.term_scales)
     return cat
+
+
+C3_N = 300_000
+C3_LIGHT = ("orbital", 0.45, 0.9)
+
+
+def c3_params(seed=0):
+    """The C3 workload: a 300k basic model (geometry of the seeded scene,
+    neutral stage-2 shading, trainer.py:562-577) -- the parameters the GPU
+    training bench steps."""
+    from paper_2504_17954_b200.synthetic import editable_arrays
+    from paper_2504_17954_b200.trainer import _stage2_init
+    a = editable_arrays(seed, C3_N, density=C3_N)
+    p = {k: a[k] for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw")}
+    p.update(_stage2_init(C3_N))
+    return a, p
+
+
+def cpu_extras(scene, arrays):
+    """Same-run CPU baselines of the other configs on the host cores
+    (BASELINE.md 4): the oracle's stage-2 step + Adam at 300k (C3), one
+    inverse step on the composed 1M scene in float64 (C4), assign + decode
+    over the 60M values of a 4M model at K=4096 (C5; k-means++ seeding timed
+    on a 1M subsample and extrapolated)."""
+    import oracle as O
+    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
+    res = {}
+    cores = O.max_threads()
+    # C3
+    a, p = c3_params(0)
+    cam = bench_camera(W_IMG, H_IMG, 0.3)
+    gt = np.random.default_rng(5).uniform(0.0, 1.0, (H_IMG, W_IMG, 4))
+    light = C3_LIGHT + (np.ones(4),)
+    adam = O.Adam()
+    t0 = time.perf_counter()
+    _, g, _ = O.stage2_step(p, a["palette"], light, cam, gt)
+    t1 = time.perf_counter()
+    for k, v in g.items():
+        adam.step(k, p[k], v, 1e-3)
+    t2 = time.perf_counter()
+    res["train_c3"] = {"value": 1.0 / (t2 - t0), "unit": "it/s", "step_s": t1 - t0,
+                       "adam_s": t2 - t1, "cores": cores, "kind": "port",
+                       "sample": "1 stage-2 step (oracle.stage2_step: K=15 render, all losses, "
+                                 "backward) + Adam over the 10 groups, 300k Gaussians, 800x800"}
+    del a, p, g
+    # C4
+    cam = bench_camera(W_IMG, H_IMG, 0.8)
+    geom = tuple(arrays[k] for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw"))
+    shad = tuple(arrays[k] for k in ("delta_c", "k_a_raw", "k_d_raw", "k_s_raw", "log_beta"))
+    ids = arrays["scene_ids"]
+    S = int(ids.max()) + 1
+    c_p = np.stack([arrays["palette_rgb"][np.argmax(ids == s)] for s in range(S)])
+    sc = np.array([arrays["opacity_scale"][np.argmax(ids == s)] for s in range(S)])
+    o_raw = O.inv_softplus(np.maximum(sc, 1e-6))
+    mode, pol, az, ts = arrays["light"]
+    ref = np.random.default_rng(6).uniform(0.0, 1.0, (H_IMG, W_IMG, 4))
+    t0 = time.perf_counter()
+    O.inverse_step(geom, shad, ids, arrays["light"], c_p, o_raw, np.ones(4), np.zeros(4), pol, az,
+                   cam, ref)
+    dt = time.perf_counter() - t0
+    res["inverse_c4"] = {"value": 1.0 / dt, "unit": "it/s", "cores": cores, "kind": "port",
+                         "sample": "1 inverse step (oracle.inverse_step: float64 render, L1+SSIM, "
+                                   "backward, per-scene reductions), composed 1M, 800x800"}
+    # C5
+    v = editable_arrays(0, 4_000_000, density=4_000_000)
+    from paper_2504_17954_b200.vq import QUANTIZED_ATTRIBUTES
+    vals = np.concatenate([np.ascontiguousarray(v[nm]).reshape(-1) for nm, _ in QUANTIZED_ATTRIBUTES])
+    del v
+    cents = np.sort(np.quantile(vals[::97], np.linspace(0.0, 1.0, 4096)))
+    t0 = time.perf_counter()
+    idx = O.vq_assign(vals, cents)
+    t1 = time.perf_counter()
+    O.vq_decode(idx.astype(np.uint16), cents)
+    t2 = time.perf_counter()
+    # k-means++ seeding (vq.py:60-72): 32 steps on a 1M subsample, per-step cost
+    rng = np.random.default_rng(0)
+    x = vals[:1_000_000].copy()
+    d2 = (x - x[0]) ** 2
+    t3 = time.perf_counter()
+    for _ in range(32):
+        c = x[rng.choice(x.size, p=d2 / d2.sum())]
+        d2 = np.minimum(d2, (x - c) ** 2)
+    step = (time.perf_counter() - t3) / 32
+    res["vq_c5"] = {"assign_s": t1 - t0, "decode_s": t2 - t1, "values": int(vals.size),
+                    "assign_gbs_alg": vals.size * 6 / (t1 - t0) / 1e9,
+                    "cores": cores, "kind": "port",
+                    "kmeans_seed_step_s_per_1M": step,
+                    "kmeans_full_estimate_s": step * 4095 * (vals.size / 1e6) * 5,
+                    "sample": "assign (C/OpenMP searchsorted on float64 mids) + decode over all "
+                              "60M values of the 8 attributes of a 4M model, K=4096; k-means "
+                              "extrapolated from 32 k-means++ steps on 1M samples x 4095 steps x "
+                              "60 (M values) x 5 restarts"}
+    return res
 
 
 def config_dict(n, extra=None):
@@ -185,8 +281,9 @@ def run_reference(args):
     cam = bench_camera(W_IMG, H_IMG, view_azimuth(0, 0))
     cpu_frames(arrays, cam, 1)  # warm (first-touch, thread pool)
     steps = max(1, min(args.steps, 3))
-    sec, thr = cpu_frames(arrays, cam, steps)
+    sec, thr, _ = cpu_frames(arrays, cam, steps)
     fps = 1.0 / sec
+    extra = None if args.no_extra else cpu_extras(scene, arrays)
     line = {"metric": METRIC, "value": fps, "unit": "frames/s", "n_gpus": args.gpus,
             "steps": steps, "warmup": 1, "ms_per_step": sec * 1e3, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f64", "data": "synthetic",
@@ -195,8 +292,34 @@ def run_reference(args):
                              "sample": f"{steps} full C2 frames (1M Gaussians, 800x800) through "
                                        "oracle/ (numpy + C/OpenMP compositor)"},
             "e2e": {"value": fps, "unit": "frames/s", "h2d_bytes_per_step": 0,
-                    "d2h_bytes_per_step": 0}}
+                    "d2h_bytes_per_step": 0},
+            "extra": extra}
     print(json.dumps(line), flush=True)
+
+
+NCU_FILES = ("r02_ncu_c2_frame", "r02_ncu_c3_train_step", "r02_ncu_c4_inverse_step", "r02_ncu_c5_vq",
+             "r01_ncu_c2_frame", "r01_ncu_c3_train_step", "r01_ncu_c4_inverse_step", "r01_ncu_c5_vq")
+
+
+def load_ncu():
+    """Kernel-name substring -> the first matching record of the committed
+    ncu --set full summaries (profiles/, newest round first)."""
+    recs = []
+    for f in NCU_FILES:
+        path = os.path.join(REPO, "profiles", f + ".json")
+        if os.path.exists(path):
+            for r in json.load(open(path))["kernels"]:
+                r = dict(r)
+                r["source"] = "profiles/" + f + ".json"
+                recs.append(r)
+
+    class Lookup(dict):
+        def get(self, key, default=None):
+            for r in recs:
+                if key in r["kernel"]:
+                    return r
+            return default
+    return Lookup()
 
 
 def _device_time(fn, steps, warmup=2):
@@ -227,41 +350,75 @@ def _max_over_ranks(x, dist):
     return float(t.item())
 
 
+def _split_events(fn, n_ev, reps=5):
+    """Mean device ms between consecutive events of fn(events) over `reps`
+    calls (L2 flushed before each)."""
+    import torch
+    flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    rows = []
+    for _ in range(reps):
+        flush.zero_()
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(n_ev)]
+        fn(ev)
+        torch.cuda.synchronize()
+        rows.append([ev[i].elapsed_time(ev[i + 1]) for i in range(n_ev - 1)])
+    return np.mean(np.array(rows), axis=0)
+
+
 def bench_train(scene, dist=None, world=1, rank=0):
     """C3: stage-2 training step (K=15 channels, fwd + all losses + bwd +
     Adam) on one 300k-Gaussian basic model at 800x800, one view / iteration.
     With N ranks every rank trains its own basic TF (independent seeds, no
-    communication): aggregate it/s = N / slowest rank's ms per iteration."""
+    communication): aggregate it/s = N / slowest rank's ms per iteration.
+    Also: the eager step split by CUDA events (per-kernel table) and the
+    EXACT-blend step (bit-faithful maps) for comparison."""
+    import torch
     from paper_2504_17954_b200 import LightConfig
-    from paper_2504_17954_b200.device import to_dev
-    from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
-    from paper_2504_17954_b200.trainer import EditableTrainer, _stage2_init
-    a = editable_arrays(rank, 300_000, density=300_000)
-    light = LightConfig("orbital", 0.45, 0.9)
+    from paper_2504_17954_b200.synthetic import bench_camera
+    from paper_2504_17954_b200.trainer import EditableTrainer, StepGraph
+    a, p = c3_params(rank)
+    light = LightConfig(*C3_LIGHT)
     cams = [bench_camera(W_IMG, H_IMG, az) for az in np.linspace(-3.0, 3.0, 8)]
     gt_tr = EditableTrainer(a, a["palette"], light)
     gts = [gt_tr.render_rgba(c).clone() for c in cams]
-    p = {k: a[k] for k in ("mu", "q_raw", "log_s", "o_logit", "n_raw")}
-    p.update(_stage2_init(300_000))
-    tr = EditableTrainer(p, a["palette"], light)
-    it = [0]
-    # the product path: the whole step (fwd, losses, bwd, Adam) as one CUDA graph
-    from paper_2504_17954_b200.trainer import StepGraph
-    G = StepGraph(tr, cams[0], gts[0])
+    del gt_tr
+    res = {}
+    for exact in (False, True):
+        tr = EditableTrainer(p, a["palette"], light)
+        tr.exact = exact
+        it = [0]
+        # the product path: the whole step (fwd, losses, bwd, Adam) as one CUDA graph
+        G = StepGraph(tr, cams[0], gts[0])
 
-    def step():
-        v = it[0] % len(cams)
-        it[0] += 1
-        G.step(cams[v], gts[v], it[0], 10000)
-    mean_ms, med_ms = _device_time(step, 10)
-    G.flush()
-    mean_ms = _max_over_ranks(mean_ms, dist)
+        def step():
+            v = it[0] % len(cams)
+            it[0] += 1
+            G.step(cams[v], gts[v], it[0], 10000)
+        mean_ms, med_ms = _device_time(step, 10)
+        G.flush()
+        res[exact] = (_max_over_ranks(mean_ms, dist), med_ms, tr)
+    mean_ms, med_ms, tr = res[False]
+    # per-kernel split of the (eager) FAST step
+    tr.exact = False
+
+    def eager(ev):
+        loss, grads, stat = tr.step(cams[1], gts[1], events=ev[:6])
+        tr.apply(grads, 1, 10000)
+        ev[6].record()
+    split = _split_events(eager, 7)
+    P = int(tr._last_pairs.item())
+    parts = dict(zip(("forward(K14 attrs, K1, K2, K3)", "losses(K7 L1+SSIM, K10 regularizers)",
+                      "K4a blend_bwd", "K4b preprocess_bwd", "K14 assemble+loss", "K11 adam"),
+                     [float(x) for x in split]))
     return {"metric": "stage-2 train it/s (300k Gaussians, 800x800, K=15, 1 view/it)",
             "value": world * 1000.0 / mean_ms, "unit": "it/s", "ms_per_it": mean_ms,
-            "ms_per_it_median": med_ms, "n_gaussians": 300_000, "n_gpus": world,
+            "ms_per_it_median": med_ms, "n_gaussians": C3_N, "n_gpus": world, "pairs": P,
+            "exact_blend": {"value": world * 1000.0 / res[True][0], "ms_per_it": res[True][0],
+                            "note": "same StepGraph with the EXACT (bit-faithful float64) blend"},
+            "split_ms_eager": parts,
             "scaling": "weak (one basic TF per GPU)",
             "note": "StepGraph replay: fwd (K1-K3), L1+SSIM + normal/offset/bilateral/opacity "
-                    "terms, K4a+K4b, gradient assembly, Adam; densify excluded"}
+                    "terms, K4a+K4b, gradient assembly, Adam; densify excluded; FAST blend"}
 
 
 def bench_inverse(scene, dist=None, world=1, rank=0):
@@ -287,33 +444,40 @@ def bench_inverse(scene, dist=None, world=1, rank=0):
              "and update graphs" if dist is not None else ""))
     mean_ms, med_ms = _device_time(step, 10)
     mean_ms = _max_over_ranks(mean_ms, dist)
+    split = _split_events(lambda ev: fit.view_grads(params, 0, events=ev), 5)
+    P = int(fit._last_pairs.item())
+    parts = dict(zip(("render(K1, K2, K3 float64 semantics)", "loss(K7)", "K4a blend_bwd",
+                      "K4b preprocess_bwd (transform only)"), [float(x) for x in split]))
     return {"metric": "inverse exploration it/s (composed 1M, 800x800, 1 view per GPU)",
             "value": 1000.0 / mean_ms, "unit": "it/s", "views_per_s": world * 1000.0 / mean_ms,
-            "ms_per_it": mean_ms, "ms_per_it_median": med_ms, "n_gpus": world,
+            "ms_per_it": mean_ms, "ms_per_it_median": med_ms, "n_gpus": world, "pairs": P,
+            "split_ms_eager": parts,
             "scaling": "weak (views sharded, one NCCL all-reduce of 4S+12 float64 per iteration)",
             "note": note}
 
 
 def bench_vq(scene):
     """C5: K5 assign + K6 decode over the 60M scalar attribute values of a 4M
-    editable model with a 4096-entry codebook (HBM-bound)."""
+    editable model (the 8 quantized attributes, vq.py:19-28) with a
+    4096-entry codebook (HBM-bound)."""
     import torch
-    from paper_2504_17954_b200.vq import assign_device, decode_device
-    n_vals = 4_000_000 * 15
-    g = torch.Generator(device="cuda").manual_seed(0)
-    vals = torch.randn(n_vals, dtype=torch.float64, device="cuda", generator=g)
-    cents = torch.sort(torch.randn(4096, dtype=torch.float64, device="cuda", generator=g)).values
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.synthetic import editable_arrays
+    from paper_2504_17954_b200.vq import QUANTIZED_ATTRIBUTES, assign_device, decode_device
+    v = editable_arrays(0, 4_000_000, density=4_000_000)
+    host = np.concatenate([np.ascontiguousarray(v[nm]).reshape(-1) for nm, _ in QUANTIZED_ATTRIBUTES])
+    del v
+    vals = to_dev(host)
+    cents = to_dev(np.sort(np.quantile(host[::97], np.linspace(0.0, 1.0, 4096))))
+    n_vals = vals.numel()
     out = {}
     a_ms, _ = _device_time(lambda: out.__setitem__("idx", assign_device(vals, cents)), 5)
     d_ms, _ = _device_time(lambda: decode_device(out["idx"], cents), 5)
-    hbm = float(json.load(open(os.path.join(REPO, "MEASURED_PEAKS.json"))).get("hbm_gbs", 6650.0)) \
-        if os.path.exists(os.path.join(REPO, "MEASURED_PEAKS.json")) else 6650.0
-    a_gbs = n_vals * 10 / (a_ms * 1e-3) / 1e9
-    d_gbs = n_vals * 10 / (d_ms * 1e-3) / 1e9
-    return {"metric": "VQ assign/decode over 60M values, K=4096", "assign_ms": a_ms,
-            "decode_ms": d_ms, "assign_gbs": a_gbs, "decode_gbs": d_gbs,
-            "assign_hbm_frac": a_gbs / hbm, "decode_hbm_frac": d_gbs / hbm,
-            "alg_bytes_per_value": 10}
+    del vals
+    torch.cuda.empty_cache()
+    return {"metric": "VQ assign/decode over 60M values (8 attributes of a 4M model), K=4096",
+            "values": int(n_vals), "assign_ms": a_ms, "decode_ms": d_ms,
+            "assign_values_per_s": n_vals / (a_ms * 1e-3), "decode_values_per_s": n_vals / (d_ms * 1e-3)}
 
 
 def bench_service(scene):
@@ -485,62 +649,77 @@ def run_ours(args):
         t_e2e = float(tt.item())
     e2e_fps = world * e2e_steps / t_e2e
 
-    # ---- roofline of the dominant kernel (stage with the largest time)
-    import json as _json
-    with open(os.path.join(REPO, "MEASURED_PEAKS.json")) if os.path.exists(
-            os.path.join(REPO, "MEASURED_PEAKS.json")) else open(os.devnull) as f:
+    peaks = {}
+    pk_path = os.path.join(REPO, "MEASURED_PEAKS.json")
+    if os.path.exists(pk_path):
         try:
-            peaks = _json.load(f)
+            peaks = json.load(open(pk_path))
         except Exception:
             peaks = {}
     hbm_peak = float(peaks.get("hbm_gbs", 6650.0))
-    peak_src = "measured" if "hbm_gbs" in peaks else "fallback"
+    peak_src = "measured (MEASURED_PEAKS.json hbm_gbs)" if "hbm_gbs" in peaks else \
+        "fallback (B200_PROFILING.md 6.65 TB/s)"
     P = int(frames[-1].n_pairs.item())
-    K = 4
     stage_ms = stage.mean(axis=0)
-    names = ["preprocess(K1)", "bin_sort(K2)", "blend(K3)"]
-    # algorithmic bytes per launch: K1 reads 168 B/Gaussian
-    # (float64 SoA + shading) + 4 B scene id, writes 8+4+8+32+4K B; K2 moves ~176 B per
-    # Gaussian (min/max, coarse key, 4 radix passes, fix-up, count scan, 2 placement
-    # walks incl. the 32 B record for the tile cull) + 4 B per pair written; K3 reads
-    # 4 B pair id + 32 B record + 4K B values per pair, writes 4K+4 B per pixel.
-    alg = [n * (172 + 52 + 4 * K), n * 176 + P * 4,
-           P * (4 + 32 + 4 * K) + W_IMG * H_IMG * (4 * K + 4)]
-    dom = int(np.argmax(stage_ms))
-    achieved = alg[dom] / (stage_ms[dom] * 1e-3) / 1e9
-    # DRAM traffic per launch and issue utilisation of the dominant kernel from
-    # the committed ncu --set full capture of one C2 frame (profiles/)
-    traffic, issue = None, None
-    ncu_path = os.path.join(REPO, "profiles", "r01_ncu_c2_frame.json")
-    if os.path.exists(ncu_path):
-        kern = {"preprocess(K1)": "preprocess_kernel", "bin_sort(K2)": "pair_place_kernel",
-                "blend(K3)": "blend_fwd_kernel"}[names[dom]]
-        for rec in _json.load(open(ncu_path))["kernels"]:
-            if kern in rec["kernel"]:
-                traffic = rec["dram_read_bytes"] + rec["dram_write_bytes"]
-                issue = {"issue_active_pct": rec["issue_active_pct"],
-                         "sm_active_over_elapsed": rec["sm_active_over_elapsed"],
-                         "source": "profiles/r01_ncu_c2_frame.json (ncu --set full, cold)"}
-    roofline = {"kernel": names[dom], "bound": "hbm", "achieved": achieved, "peak": hbm_peak,
-                "unit": "GB/s", "frac": achieved / hbm_peak, "traffic": traffic,
-                "peak_source": peak_src,
-                "note": "K3 is bound by FP32/MUFU instruction issue and the longest 8x4 block "
-                        "walk, not HBM: its pair lists and records are L2-resident "
-                        "(traffic << algorithmic bytes); see 'issue'",
-                "issue": issue,
-                "stage_ms_uncaptured": {nm: float(v) for nm, v in zip(names, stage_ms)},
-                "frame_ms_isolated_min_med_max": [float(frame_ms.min()), float(np.median(frame_ms)),
-                                         float(frame_ms.max())],
-                "alg_bytes": {nm: int(v) for nm, v in zip(names, alg)}}
+    WH = W_IMG * H_IMG
 
-    cpu = None
+    # ---- parity of the headline path with the CPU reference, same camera
+    cpu, parity = None, None
     if rank == 0 and world == 1 and not args.no_cpu_baseline:
         arrays = host_scene_arrays(scene)
         cam = cams[0]
-        sec, thr = cpu_frames(arrays, cam, max(1, args.cpu_frames))
+        sec, thr, ref = cpu_frames(arrays, cam, max(1, args.cpu_frames))
         cpu = {"value": 1.0 / sec, "unit": "frames/s", "cores": thr, "kind": "port",
                "sample": f"{max(1, args.cpu_frames)} full C2 frames (1M Gaussians, 800x800) "
                          "via oracle/ (numpy + C/OpenMP)"}
+        Fg = fg.submit(0, cam)  # the captured headline frame (FAST blend) of this camera
+        torch.cuda.synchronize()
+        Fe = ds.render_frame(cam, fast=True, want_state=True)  # + last_pos / t_final
+        torch.cuda.synchronize()
+        rgba = np.concatenate([ref["maps"]["color"], ref["maps"]["alpha"][..., None]], axis=-1)
+        img = Fg.out.cpu().numpy()
+        parity = {"camera": "cams[0] (orbit azimuth 0.8)", "mode": "FAST (headline FrameGraph)",
+                  "pairs": int(ref["pair_splat"].size),
+                  "pairs_equal": bool(int(Fg.n_pairs.item()) == ref["pair_splat"].size and
+                                      np.array_equal(Fg.pairs(), ref["pair_splat"])),
+                  "tile_ranges_equal": bool(np.array_equal(Fg.tile_ranges.cpu().numpy(),
+                                                           ref["tile_ranges"])),
+                  "contrib_equal": bool(np.array_equal(Fg.contrib.cpu().numpy(), ref["contrib"])),
+                  "last_pos_equal": bool(np.array_equal(Fe.last_pos.cpu().numpy(), ref["last_pos"])),
+                  "max_abs": float(np.abs(img - rgba).max()),
+                  "identical_values": float(np.mean(img == rgba)),
+                  "tolerance": 1e-4}
+
+    # ---- per-kernel roofline table (CUDA-event times from this run; algorithmic
+    # bytes per SURVEY 8(d) for the C2 kernels, DESIGN.md 3 for the others;
+    # DRAM traffic / issue from the committed ncu captures, same kernel scope)
+    ncu = load_ncu()
+    kern = []
+
+    def row(name, ms, alg, basis, ncu_key=None, launches=1, bound="hbm", note=None):
+        ach = alg / (ms * 1e-3) / 1e9
+        r = {"kernel": name, "us": ms * 1e3, "alg_bytes": int(alg), "alg_basis": basis,
+             "achieved_gbs": ach, "frac": ach / hbm_peak, "bound": bound}
+        rec = ncu.get(ncu_key) if ncu_key else None
+        if rec:
+            r["traffic"] = (rec["dram_read_bytes"] + rec["dram_write_bytes"]) * launches
+            r["traffic_over_alg"] = r["traffic"] / alg
+            r["ncu"] = {k: rec[k] for k in ("duration_us", "issue_active_pct",
+                                            "sm_active_over_elapsed", "warps_active_pct")}
+            r["ncu"]["source"] = rec["source"]
+        if note:
+            r["note"] = note
+        kern.append(r)
+        return r
+
+    row("K1 preprocess (C2)", stage_ms[0], 136 * n, "SURVEY 8(d): 136 B/Gaussian (in 88 + out 48)",
+        "preprocess_kernel")
+    row("K2 bin/sort stage (C2, all launches)", stage_ms[1], 24 * n + 12 * P,
+        "SURVEY 8(d): 24 B/Gaussian (depth-rank sort) + 12 B/pair (key gen / placement)",
+        None, note="whole ivr_bin_sort_cull + ivr_tile_order stage")
+    k3 = row("K3 blend_fwd (C2)", stage_ms[2], 40 * P + 16 * WH,
+             "SURVEY 8(d): 40 B/pair (id + record + rgba gather) + 16 B/pixel (RGBA f32 out)",
+             "blend_fwd_kernel<4, 0, 1>", bound="issue (FP32/MUFU) + longest 8x4 block walk")
 
     extra = None
     if not args.no_extra:
@@ -557,14 +736,70 @@ def run_ours(args):
             except Exception as e:  # report, never hide the headline line
                 extra[name] = {"error": f"{type(e).__name__}: {e}"}
             torch.cuda.empty_cache()
+        t3 = extra.get("train_c3", {})
+        if "split_ms_eager" in t3:
+            sp, P3, N3, K3 = t3["split_ms_eager"], t3["pairs"], C3_N, 15
+            row("K4a blend_bwd (C3, K=15)", sp["K4a blend_bwd"],
+                P3 * (4 + 32 + 4 * K3) + WH * (4 * K3 + 12) + N3 * (K3 + 6) * 4,
+                "DESIGN 3: 96 B/pair gather + 72 B/pixel (d_out, last_pos, t_final) + "
+                "84 B/Gaussian accumulators", "blend_bwd_kernel<16, 0, 1>")
+            row("K4b preprocess_bwd (C3)", sp["K4b preprocess_bwd"], N3 * (168 + 84 + 224),
+                "DESIGN 3: 168 B params + 84 B accumulators in, 224 B gradients out per Gaussian",
+                "preprocess_bwd_kernel<1>")
+            row("losses K7+K10 (C3)", sp["losses(K7 L1+SSIM, K10 regularizers)"],
+                WH * 4 * 56 + WH * (4 * K3 * 2 + 64),
+                "DESIGN 3: K7 56 B/pixel-channel (4 ch) + K10 (maps in, d_out out, normals)")
+            row("K11 adam (C3)", sp["K11 adam"], N3 * 24 * 8 * 7,
+                "DESIGN 3: 24 float64 parameters x 7 accesses per Gaussian "
+                "(SURVEY 8(d) counts 672 B at float32)", "adam_kernel")
+        t4 = extra.get("inverse_c4", {})
+        if "split_ms_eager" in t4:
+            sp, P4 = t4["split_ms_eager"], t4["pairs"]
+            row("K3 blend_fwd (C4, float64 semantics)", sp["render(K1, K2, K3 float64 semantics)"],
+                136 * n + 24 * n + 12 * P4 + 40 * P4 + 16 * WH,
+                "SURVEY 8(d) C4: render 160 N + 52 P + 16 WH (whole render, K1-K3)")
+            row("K4a blend_bwd (C4, no geometry)", sp["K4a blend_bwd"], 40 * P4 + 16 * WH,
+                "SURVEY 8(d) C4: 40 P + 16 WH read", "blend_bwd_kernel<4, 1, 0>")
+            row("K4b preprocess_bwd (C4, transform only)", sp["K4b preprocess_bwd (transform only)"],
+                (16 + 100) * n, "SURVEY 8(d) C4: 16 B/Gaussian atomics + 100 B shade-bwd read",
+                "preprocess_bwd_kernel<0>")
+        v5 = extra.get("vq_c5", {})
+        if "assign_ms" in v5:
+            row("K5 vq_assign (C5)", v5["assign_ms"], 6 * v5["values"],
+                "SURVEY 8(d) C5: 4 B in + 2 B out per value (float64 storage moves 10 B)",
+                "vq_assign_kernel", note="implementation bytes 10/value: frac x 10/6")
+            row("K6 vq_decode (C5)", v5["decode_ms"], 6 * v5["values"],
+                "SURVEY 8(d) C5: 2 B in + 4 B out per value (float64 storage moves 10 B)",
+                "vq_decode_kernel", note="implementation bytes 10/value: frac x 10/6")
+
+    roofline = {"kernel": "K3 blend_fwd (C2)", "bound": "hbm", "achieved": k3["achieved_gbs"],
+                "peak": hbm_peak, "unit": "GB/s", "frac": k3["frac"],
+                "traffic": k3.get("traffic"), "peak_source": peak_src,
+                "alg_bytes": k3["alg_bytes"], "alg_basis": k3["alg_basis"], "us": k3["us"],
+                "why_dominant": "largest single kernel by CUDA-event time (and ncu share) of a C2 frame",
+                "note": "K3 is bound by FP32/MUFU issue and the longest 8x4 block walk, not HBM "
+                        "(its lists and records are L2-resident); see kernels[] / ncu",
+                "frame_bytes_survey": int(160 * n + 52 * P + 16 * WH),
+                "frame_frac_isolated": (160 * n + 52 * P + 16 * WH) / (float(np.median(frame_ms)) * 1e-3) / 1e9 / hbm_peak,
+                "stage_ms_uncaptured": {"K1": float(stage_ms[0]), "K2": float(stage_ms[1]),
+                                        "K3": float(stage_ms[2])},
+                "frame_ms_isolated_min_med_max": [float(frame_ms.min()), float(np.median(frame_ms)),
+                                                  float(frame_ms.max())]}
+    if cpu is not None and extra is not None and world == 1:
+        try:
+            cpu["extra"] = cpu_extras(scene, host_scene_arrays(scene))
+        except Exception as e:
+            cpu["extra"] = {"error": f"{type(e).__name__}: {e}"}
 
     if rank == 0:
         line = {"metric": METRIC, "value": fps_total, "unit": "frames/s", "n_gpus": world,
                 "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms,
-                "higher_is_better": True, "scaling": "weak", "vs_baseline": None, "dtype": "f64",
+                "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+                "dtype": "f32 blend (certified decisions); f64 keys / preprocess",
                 "data": "synthetic (seeded editable Gaussians, SURVEY.md 8(d))",
                 "config": config_dict(n, {"pairs": P, "parallelism": f"replicas x{world} (views)"}),
-                "clocks": clocks, "roofline": roofline, "cpu_baseline": cpu,
+                "clocks": clocks, "roofline": roofline, "kernels": kern, "parity": parity,
+                "cpu_baseline": cpu,
                 "e2e": {"value": e2e_fps, "unit": "frames/s",
                         "h2d_bytes_per_step": pipe.h2d_bytes_per_frame(),
                         "d2h_bytes_per_step": pipe.d2h_bytes_per_frame(),
