@@ -355,6 +355,9 @@ def _split_events(fn, n_ev, reps=5):
     calls (L2 flushed before each)."""
     import torch
     flush = torch.empty(256 << 20, dtype=torch.uint8, device="cuda")
+    for _ in range(2):  # warm-up: workspaces and caching-allocator blocks
+        fn([torch.cuda.Event(enable_timing=True) for _ in range(n_ev)])
+    torch.cuda.synchronize()
     rows = []
     for _ in range(reps):
         flush.zero_()
@@ -755,7 +758,7 @@ def run_ours(args):
         t4 = extra.get("inverse_c4", {})
         if "split_ms_eager" in t4:
             sp, P4 = t4["split_ms_eager"], t4["pairs"]
-            row("K3 blend_fwd (C4, float64 semantics)", sp["render(K1, K2, K3 float64 semantics)"],
+            row("render K1-K3 (C4, float64 semantics)", sp["render(K1, K2, K3 float64 semantics)"],
                 136 * n + 24 * n + 12 * P4 + 40 * P4 + 16 * WH,
                 "SURVEY 8(d) C4: render 160 N + 52 P + 16 WH (whole render, K1-K3)")
             row("K4a blend_bwd (C4, no geometry)", sp["K4a blend_bwd"], 40 * P4 + 16 * WH,

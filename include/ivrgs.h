@@ -116,6 +116,10 @@ typedef struct ivr_proj_out {
     double *rgb;     /* (n,3) shaded colour */
     double *radius;  /* (n) */
     uint8_t *valid;  /* (n) projection validity */
+    /* optional [min, max] of the visible depth keys, reduced with atomics
+     * (must hold {~0, 0} or a superset; ivr_bin_sort_frame consumes and
+     * re-arms it) */
+    unsigned long long *depth_minmax;
 } ivr_proj_out;
 
 /* Camera- and edit-independent per-Gaussian values of a resident scene
@@ -202,6 +206,22 @@ int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int32_t *count
                       int32_t width, int32_t height, int64_t pair_capacity,
                       void *workspace, size_t workspace_bytes, int32_t *pair_splat,
                       int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream);
+
+/* K2 for a K1 frame: as ivr_bin_sort_cull (rec may be NULL), plus
+ * depth_minmax (nullable): the [min, max] of the visible depth keys that
+ * ivr_proj_out.depth_minmax made K1 reduce (block-reduced atomics); K2
+ * re-arms it to {~0, 0} for the next frame, so it must start as {~0, 0} or
+ * as any superset of the keys' range (a wider range only costs sort runs,
+ * never correctness).  NULL: K2 reduces the range itself (two more kernels).
+ * tile_order (nullable): receives the heaviest-first tile schedule for K3/K4
+ * (ivr_tile_order's) from K2's tile-range kernel.  8 kernels + one memset of
+ * K2's control block per call at 1M splats. */
+int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key, unsigned long long *depth_minmax,
+                       const int32_t *count, const uint16_t *rect, const float *rec, int32_t ntx,
+                       int32_t nty, int32_t width, int32_t height, int64_t pair_capacity,
+                       void *workspace, size_t workspace_bytes, int32_t *pair_splat,
+                       int32_t *tile_ranges, int32_t *n_pairs, int32_t *tile_order,
+                       ivr_stream_t stream);
 
 /* K3: per-tile front-to-back blend.  Replaces _kernels.composite_forward
  * (_kernels.py:31-72).  out (H,W,k) float32 (out64 float64 in f64 mode),

@@ -71,7 +71,8 @@ class Layout_t(ctypes.Structure):
 class ProjOut_t(ctypes.Structure):
     _fields_ = [("depth_key", P), ("count", P), ("rect", P), ("rec", P), ("values", P),
                 ("rec64", P), ("values64", P), ("mean2d", P), ("conic", P), ("cov2d", P),
-                ("depth", P), ("opacity", P), ("rgb", P), ("radius", P), ("valid", P)]
+                ("depth", P), ("opacity", P), ("rgb", P), ("radius", P), ("valid", P),
+                ("depth_minmax", P)]
 
 
 class AdamGroup_t(ctypes.Structure):
@@ -142,6 +143,9 @@ _SIGS = {
     "ivr_bin_sort_workspace_size": ([ctypes.c_int64, ctypes.c_int64, ctypes.c_int32], ctypes.c_size_t),
     "ivr_bin_sort": ([ctypes.c_int64, P, P, P, ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P,
                       ctypes.c_size_t, P, P, P, P], ctypes.c_int),
+    "ivr_bin_sort_frame": ([ctypes.c_int64, P, P, P, P, P, ctypes.c_int32, ctypes.c_int32,
+                            ctypes.c_int32, ctypes.c_int32, ctypes.c_int64, P, ctypes.c_size_t, P,
+                            P, P, P, P], ctypes.c_int),
     "ivr_blend_fwd": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, P, ctypes.c_int32,
                        ctypes.c_int32, ctypes.c_int32, P, P, P, P, P, P, ctypes.c_int32, P],
                       ctypes.c_int),

@@ -165,8 +165,36 @@ preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E, 
     __shared__ ivr_frame_params sp;
     stage_params(Pd ? Pd : &Pv, sp);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-    if (i >= G.n) return;
-    preprocess_one(G, S, has_shading, E, has_edits, sp, L, O, f64_mode, i);
+    if (i < G.n) preprocess_one(G, S, has_shading, E, has_edits, sp, L, O, f64_mode, i);
+    if (!O.depth_minmax) return;
+    // [min, max] of the visible depth keys for K2's coarse keys: warp and
+    // block reduction, one atomic pair per block
+    const unsigned long long key = i < G.n ? O.depth_key[i] : ~0ull;
+    unsigned long long lo = key, hi = key == ~0ull ? 0ull : key;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long a = __shfl_xor_sync(0xffffffffu, lo, o);
+        const unsigned long long b = __shfl_xor_sync(0xffffffffu, hi, o);
+        lo = a < lo ? a : lo;
+        hi = b > hi ? b : hi;
+    }
+    constexpr int kW = kK1Threads / 32;
+    __shared__ unsigned long long s_lo[kW], s_hi[kW];
+    if ((threadIdx.x & 31) == 0) {
+        s_lo[threadIdx.x >> 5] = lo;
+        s_hi[threadIdx.x >> 5] = hi;
+    }
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < kW; ++w) {
+            lo = s_lo[w] < lo ? s_lo[w] : lo;
+            hi = s_hi[w] > hi ? s_hi[w] : hi;
+        }
+        if (lo != ~0ull) {
+            atomicMin(O.depth_minmax, lo);
+            atomicMax(O.depth_minmax + 1, hi);
+        }
+    }
 }
 
 __global__ void __launch_bounds__(256)

@@ -6,27 +6,34 @@
 //
 //  1. depth ranks.  Positive float64 depths order like their bit patterns.
 //     The bits are shifted into a "coarse" key (bits - min) >> s of about
-//     log2(n) + 3 bits (~8 buckets per splat), the coarse keys are
-//     radix-sorted stably (8-bit LSD passes, 3 for 1M splats; invisible
-//     splats carry all ones and sort last), and runs of equal coarse keys
-//     are re-ordered by the full 64-bit key (insertion sort, stable).  If a
-//     run is longer than kMaxRun the whole order is recomputed with a full
-//     64-bit LSD sort (8 passes) -- correctness never depends on the data.
-//     Ties keep index order = lexsort's tie break on fill_pairs' order.
-//  2. P = sum of the per-splat tile counts.
-//  3. counting placement: each block owns 2048 consecutive depth ranks; its
+//     log2(n) + 3 bits (~8 buckets per splat; the [min, max] of the visible
+//     keys comes from K1's block-reduced atomics, or from a min/max kernel
+//     when the keys are supplied directly).  One histogram kernel maps the
+//     keys and counts every pass's 8-bit digits; each stable LSD pass is then
+//     ONE kernel (onesweep: 4096-key blocks take virtual ids in start order,
+//     publish their digit counts and find their exclusive prefix per digit by
+//     decoupled look-back over their predecessors, then scatter through
+//     shared memory).  Invisible splats carry all ones and sort last.  Runs
+//     of equal coarse keys are re-ordered by the full 64-bit key (insertion
+//     sort, stable); if a run is longer than kMaxRun the last block of that
+//     kernel recomputes the whole order with a full 64-bit LSD sort --
+//     correctness never depends on the data.  Ties keep index order =
+//     lexsort's tie break on fill_pairs' order.
+//  2. counting placement: each block owns 2048 consecutive depth ranks; its
 //     warps expand their ranks' pairs in fill_pairs order (load-balanced
 //     warp expansion, no per-pair global searches), build a per-tile
 //     histogram that is scanned per tile across blocks, and write each pair
 //     once to tile_start[t] + block offset + its stable rank inside the block
-//     (warp match_any ranking).  Tile ranges are the exclusive scan of the
-//     tile totals.
-//  4. optional tile cull: while placing, each pair is tested in float64 for
+//     (warp match_any ranking).  The per-tile scan kernel's last block turns
+//     the tile totals into the tile ranges (P = their sum) and the K3/K4
+//     tile schedule, and re-arms the min/max words for the next frame.
+//  3. optional tile cull: while placing, each pair is tested in float64 for
 //     whether its splat can reach alpha >= 1/255 anywhere in the tile; pairs
 //     that cannot are marked with bit 31 (pair_splat & 0x7fffffff is the
 //     reference list), letting the blend skip them without loading records.
 // All data-dependent sizes live in device memory: the sequence is
-// stream-ordered and CUDA-graph capturable.
+// stream-ordered and CUDA-graph capturable (8 kernels + one control-block
+// memset per frame at 1M splats).
 #include "cull.cuh"
 
 namespace ivr {
@@ -35,15 +42,27 @@ namespace sortk {
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
 constexpr int kItems = 16;                 // per thread in radix passes
-constexpr int kChunk = kThreads * kItems;  // 2048 keys per radix block
+constexpr int kChunk = kThreads * kItems;  // 4096 keys per radix block
 constexpr int kRadix = 256;
 constexpr int kMaxRun = 64;
 constexpr uint32_t kInvisible = 0xffffffffu;
 
-__global__ void init_minmax_kernel(unsigned long long *mm, int32_t *flag) {
+__global__ void init_minmax_kernel(unsigned long long *mm) {
     mm[0] = ~0ull;
     mm[1] = 0ull;
-    *flag = 0;
+}
+
+// Look-back status words: 2 flag bits (1 = block aggregate, 2 = inclusive
+// prefix) over a 30-bit count; 0 = not yet published.
+constexpr uint32_t kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValMask = (1u << 30) - 1;
+
+__device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
+    uint32_t v;
+    asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
+    return v;
+}
+__device__ __forceinline__ void st_volatile(uint32_t *p, uint32_t v) {
+    asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 
 __device__ __forceinline__ int64_t load_n(const int32_t *n_dev, int64_t n_host, int64_t cap) {
@@ -116,42 +135,17 @@ minmax_kernel(const uint64_t *keys, int64_t n, unsigned long long *mm /* [min, m
 }
 
 // ----------------------------------------------------------------- radix passes
-// Stable LSD pass (8-bit digit at `shift`) of (key, value) pairs.  vals_in ==
-// nullptr means identity values.  `gate` (device int, may be null): the pass
-// runs only when *gate != 0.
-template <typename KeyT>
+// Coarse keys + every pass's digit histogram in one read of the 64-bit keys:
+// visible keys get `vbits` bits ((bits - min) >> s < 2^vbits), invisible
+// splats all ones (above every visible key); per-block shared histograms are
+// added into the global per-pass digit counts gdig[pass][256] (zeroed by the
+// frame's control-block memset).
 __global__ void __launch_bounds__(kThreads)
-upsweep_kernel(const KeyT *keys, int64_t n, int shift, uint32_t *blockhist, int nblocks,
-               const int32_t *gate) {
-    if (gate && *gate == 0) return;
-    __shared__ uint32_t s[kRadix];
-    s[threadIdx.x] = 0;
-    __syncthreads();
-    const int64_t base = (int64_t)blockIdx.x * kChunk;
-    KeyT k[kItems];
+hist_coarse_kernel(const uint64_t *full, int64_t n, const unsigned long long *mm, int vbits,
+                   int passes, uint32_t *ck, uint32_t *gdig) {
+    __shared__ uint32_t s[4][kRadix];
 #pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const int64_t idx = base + r * kThreads + threadIdx.x;
-        k[r] = idx < n ? keys[idx] : (KeyT)0;
-    }
-#pragma unroll
-    for (int r = 0; r < kItems; ++r) {
-        const int64_t idx = base + r * kThreads + threadIdx.x;
-        if (idx < n) atomicAdd(&s[(uint32_t)(k[r] >> shift) & 255u], 1u);
-    }
-    __syncthreads();
-    blockhist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = s[threadIdx.x];
-}
-
-// First pass's upsweep fused with the coarse-key mapping: visible keys get
-// `vbits` bits ((bits - min) >> s < 2^vbits), invisible splats all ones (above
-// every visible key).  Reads the 64-bit depth keys, writes the 32-bit coarse
-// keys the pass's downsweep consumes, and builds the pass-0 digit histogram.
-__global__ void __launch_bounds__(kThreads)
-upsweep_coarse_kernel(const uint64_t *full, int64_t n, const unsigned long long *mm, int vbits,
-                      uint32_t *ck, uint32_t *blockhist, int nblocks) {
-    __shared__ uint32_t s[kRadix];
-    s[threadIdx.x] = 0;
+    for (int p = 0; p < 4; ++p) s[p][threadIdx.x] = 0;
     const unsigned long long lo = mm[0], hi = mm[1];
     const unsigned long long range = hi >= lo ? hi - lo : 0ull;
     const int bits = range ? 64 - __clzll((long long)range) : 0;
@@ -170,95 +164,41 @@ upsweep_coarse_kernel(const uint64_t *full, int64_t n, const unsigned long long 
         if (idx < n) {
             const uint32_t c = k[r] == ~0ull ? kInvisible : (uint32_t)((k[r] - lo) >> sh);
             ck[idx] = c;
-            atomicAdd(&s[c & 255u], 1u);
+            for (int p = 0; p < passes; ++p) atomicAdd(&s[p][(c >> (8 * p)) & 255u], 1u);
         }
     }
     __syncthreads();
-    blockhist[(int64_t)threadIdx.x * nblocks + blockIdx.x] = s[threadIdx.x];
+    for (int p = 0; p < passes; ++p)
+        if (s[p][threadIdx.x]) atomicAdd(&gdig[p * kRadix + threadIdx.x], s[p][threadIdx.x]);
 }
 
-// grid = #rows: exclusive scan of row[0..ncols) in place, row total -> rowtotal.
-__global__ void __launch_bounds__(1024)
-rowscan_kernel(uint32_t *rows, int ncols, uint32_t *rowtotal, const int32_t *gate) {
-    if (gate && *gate == 0) return;
-    __shared__ uint32_t s_warp[32];
-    uint32_t *row = rows + (int64_t)blockIdx.x * ncols;
-    uint32_t carry = 0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    for (int base = 0; base < ncols; base += 1024) {
-        const int i = base + threadIdx.x;
-        const uint32_t v = i < ncols ? row[i] : 0;
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_warp[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = s_warp[lane];
-#pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
-            }
-            s_warp[lane] = w;
-        }
-        __syncthreads();
-        const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0);
-        if (i < ncols) row[i] = carry + incl - v;
-        carry += s_warp[31];
-        __syncthreads();
-    }
-    if (threadIdx.x == 0) rowtotal[blockIdx.x] = carry;
-}
-
-// One warp per row: the same exclusive row scan for short rows (the radix
-// block histograms and the per-tile block counts: a few hundred columns),
-// 32 coalesced columns per step, no CTA barriers.
-constexpr int kRowsPerBlock = 8;
-__global__ void __launch_bounds__(32 * kRowsPerBlock)
-rowscan_warp_kernel(uint32_t *rows, int nrows, int ncols, uint32_t *rowtotal,
-                    const int32_t *gate) {
-    if (gate && *gate == 0) return;
-    const int lane = threadIdx.x & 31;
-    const int r = blockIdx.x * kRowsPerBlock + (threadIdx.x >> 5);
-    if (r >= nrows) return;
-    uint32_t *row = rows + (int64_t)r * ncols;
-    uint32_t carry = 0;
-#pragma unroll 4
-    for (int base = 0; base < ncols; base += 32) {
-        const int i = base + lane;
-        const uint32_t v = i < ncols ? row[i] : 0;
-        uint32_t x = v;
-#pragma unroll
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (i < ncols) row[i] = carry + x - v;
-        carry += __shfl_sync(0xffffffffu, x, 31);
-    }
-    if (lane == 0) rowtotal[r] = carry;
-}
-
+// One stable LSD pass (8-bit digit at `shift`) of (key, value) pairs as a
+// single kernel.  vals_in == nullptr means identity values.  Blocks take
+// virtual ids in the order they start (so every predecessor is running and
+// look-back cannot deadlock), rank their 4096 keys by digit (warp match_any),
+// publish per-digit counts, and obtain each digit's exclusive prefix over the
+// earlier blocks by decoupled look-back on status[block][digit]; the digit
+// bases come from the pass's global histogram (hist_coarse_kernel).
 template <typename KeyT>
 __global__ void __launch_bounds__(kThreads)
-downsweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
-                 const uint32_t *blockhist, const uint32_t *rowtotal, int nblocks, KeyT *dkeys,
-                 uint32_t *dvals, const int32_t *gate) {
-    if (gate && *gate == 0) return;
-    const int64_t base = (int64_t)blockIdx.x * kChunk;
-    if (base >= n) return;
+onesweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
+                const uint32_t *gdig, uint32_t *status, uint32_t *vctr, KeyT *dkeys,
+                uint32_t *dvals) {
     __shared__ uint32_t s_wcnt[kWarps][kRadix];
     __shared__ uint32_t s_gbase[kRadix];
     __shared__ uint32_t s_lstart[kRadix];
     __shared__ uint32_t s_warp[kWarps];
+    __shared__ uint32_t s_bid;
     __shared__ KeyT s_keys[kChunk];
     __shared__ uint32_t s_vals[kChunk];
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+    if (tid == 0) s_bid = atomicAdd(vctr, 1u);
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s_wcnt[w][tid] = 0;
+    __syncthreads();
+    const uint32_t bid = s_bid;
+    const int64_t base = (int64_t)bid * kChunk;
     KeyT k[kItems];
     uint32_t v[kItems];
 #pragma unroll
@@ -268,14 +208,6 @@ downsweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
         k[r] = ok ? keys[idx] : (KeyT)0;
         v[r] = ok ? (vals ? vals[idx] : (uint32_t)idx) : 0u;
     }
-#pragma unroll
-    for (int w = 0; w < kWarps; ++w) s_wcnt[w][tid] = 0;
-    uint32_t tot;
-    const uint32_t rt = rowtotal[tid];
-    const uint32_t incl = block_incl_scan(rt, s_warp, tot);
-    s_gbase[tid] = incl - rt + blockhist[(int64_t)tid * nblocks + blockIdx.x];
-    __syncthreads();
-
     uint32_t dig[kItems], rank[kItems];
     const uint32_t lt = lanemask_lt();
 #pragma unroll
@@ -292,6 +224,7 @@ downsweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
         rank[r] = before + __popc(peers & lt);
     }
     __syncthreads();
+    uint32_t cnt;  // this block's count of digit tid
     {
         uint32_t run = 0;
 #pragma unroll
@@ -300,8 +233,30 @@ downsweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
             s_wcnt[w][tid] = run;
             run += c;
         }
-        const uint32_t inc = block_incl_scan(run, s_warp, tot);
-        s_lstart[tid] = inc - run;
+        cnt = run;
+    }
+    // publish the aggregate (block 0: already the inclusive prefix), then look back
+    uint32_t *my = status + (int64_t)bid * kRadix + tid;
+    st_volatile(my, (bid == 0 ? kFlagPrefix : kFlagAgg) | cnt);
+    uint32_t excl = 0;
+    if (bid > 0) {
+        int64_t j = (int64_t)bid - 1;
+        while (true) {
+            const uint32_t w = ld_volatile(status + j * kRadix + tid);
+            if ((w & ~kValMask) == 0) continue;  // predecessor not published yet
+            excl += w & kValMask;
+            if (w & kFlagPrefix) break;
+            --j;
+        }
+        st_volatile(my, kFlagPrefix | (excl + cnt));
+    }
+    uint32_t tot;
+    const uint32_t gd = gdig[tid];
+    const uint32_t ginc = block_incl_scan(gd, s_warp, tot);
+    s_gbase[tid] = ginc - gd + excl;
+    {
+        const uint32_t inc = block_incl_scan(cnt, s_warp, tot);
+        s_lstart[tid] = inc - cnt;
     }
     __syncthreads();
 #pragma unroll
@@ -324,59 +279,15 @@ downsweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
 }
 
 // ----------------------------------------------------------------- run fix-up
-// Re-order runs of equal coarse keys by the full 64-bit key (stable).  Runs
-// longer than kMaxRun set *need_full (the 64-bit fallback sort then runs).
-__global__ void __launch_bounds__(kThreads)
-fixup_kernel(const uint32_t *ck, uint32_t *idx, int64_t n, const uint64_t *full,
-             int32_t *need_full) {
-    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    if (i >= n) return;
-    const uint32_t k = ck[i];
-    if (k == kInvisible) return;
-    if (i > 0 && ck[i - 1] == k) return;        // not a run head
-    if (i + 1 >= n || ck[i + 1] != k) return;   // run of one
-    int64_t e = i + 1;
-    while (e < n && ck[e] == k && e - i <= kMaxRun) ++e;
-    if (e - i > kMaxRun) {
-        *need_full = 1;
-        return;
-    }
-    const int len = (int)(e - i);
-    uint32_t v[kMaxRun];
-    uint64_t key[kMaxRun];
-    for (int a = 0; a < len; ++a) {
-        v[a] = idx[i + a];
-        key[a] = full[v[a]];
-    }
-    for (int a = 1; a < len; ++a) {  // stable insertion sort (indices ascending on ties)
-        const uint32_t tv = v[a];
-        const uint64_t tk = key[a];
-        int b = a - 1;
-        while (b >= 0 && key[b] > tk) {
-            key[b + 1] = key[b];
-            v[b + 1] = v[b];
-            --b;
-        }
-        key[b + 1] = tk;
-        v[b + 1] = tv;
-    }
-    for (int a = 0; a < len; ++a) idx[i + a] = v[a];
-}
-
-// ----------------------------------------------------------------- fallback
 // Rare path (a coarse-key run longer than kMaxRun, i.e. many depths packed
-// into one 31-bit bucket by an extreme depth range): one CTA recomputes the
-// whole order with a stable 8 x 8-bit LSD sort of the full 64-bit keys.
-// Launched every frame; returns immediately unless *need_full.
-constexpr int kFbThreads = 1024;
-constexpr int kFbWarps = kFbThreads / 32;
-
-__global__ void __launch_bounds__(kFbThreads, 1)
-fallback_sort_kernel(const uint64_t *depth_key, int64_t n, const int32_t *need_full,
-                     uint64_t *kA, uint64_t *kB, uint32_t *vA, uint32_t *vB) {
-    if (*need_full == 0) return;
+// into one bucket by an extreme depth range): one CTA recomputes the whole
+// order with a stable 8 x 8-bit LSD sort of the full 64-bit keys.
+template <int NT>
+__device__ void full_sort_block(const uint64_t *depth_key, int64_t n, uint64_t *kA, uint64_t *kB,
+                                uint32_t *vA, uint32_t *vB) {
+    constexpr int NW = NT / 32;
     __shared__ uint32_t s_off[kRadix];
-    __shared__ uint32_t s_wc[kFbWarps][kRadix];
+    __shared__ uint32_t s_wc[NW][kRadix];
     const int tid = threadIdx.x, warp = tid >> 5;
     const uint32_t lt = lanemask_lt();
     for (int p = 0; p < 8; ++p) {
@@ -386,9 +297,9 @@ fallback_sort_kernel(const uint64_t *depth_key, int64_t n, const int32_t *need_f
         uint32_t *vo = (p & 1) ? vA : vB;
         const int sh = 8 * p;
         // digit histogram -> exclusive offsets
-        if (tid < kRadix) s_off[tid] = 0;
+        for (int d = tid; d < kRadix; d += NT) s_off[d] = 0;
         __syncthreads();
-        for (int64_t i = tid; i < n; i += kFbThreads) atomicAdd(&s_off[(ki[i] >> sh) & 255], 1u);
+        for (int64_t i = tid; i < n; i += NT) atomicAdd(&s_off[(ki[i] >> sh) & 255], 1u);
         __syncthreads();
         if (tid == 0) {
             uint32_t run = 0;
@@ -399,9 +310,9 @@ fallback_sort_kernel(const uint64_t *depth_key, int64_t n, const int32_t *need_f
             }
         }
         __syncthreads();
-        // stable scatter, one 1024-element tile at a time
-        for (int64_t base = 0; base < n; base += kFbThreads) {
-            for (int i = tid; i < kFbWarps * kRadix; i += kFbThreads) (&s_wc[0][0])[i] = 0;
+        // stable scatter, one NT-element tile at a time
+        for (int64_t base = 0; base < n; base += NT) {
+            for (int i = tid; i < NW * kRadix; i += NT) (&s_wc[0][0])[i] = 0;
             __syncthreads();
             const int64_t i = base + tid;
             const bool ok = i < n;
@@ -411,11 +322,11 @@ fallback_sort_kernel(const uint64_t *depth_key, int64_t n, const int32_t *need_f
             const uint32_t peers = __match_any_sync(0xffffffffu, d);
             if (ok && (peers & lt) == 0) s_wc[warp][d] = __popc(peers);
             __syncthreads();
-            if (tid < kRadix) {  // exclusive scan across warps for digit tid
+            for (int dd = tid; dd < kRadix; dd += NT) {  // exclusive scan across warps
                 uint32_t run = 0;
-                for (int w = 0; w < kFbWarps; ++w) {
-                    const uint32_t c = s_wc[w][tid];
-                    s_wc[w][tid] = run;
+                for (int w = 0; w < NW; ++w) {
+                    const uint32_t c = s_wc[w][dd];
+                    s_wc[w][dd] = run;
                     run += c;
                 }
             }
@@ -427,15 +338,63 @@ fallback_sort_kernel(const uint64_t *depth_key, int64_t n, const int32_t *need_f
             }
             __syncthreads();
             // advance the digit offsets by this tile's per-digit totals
-            if (tid < kRadix) s_wc[1][tid] = 0;
+            for (int dd = tid; dd < kRadix; dd += NT) s_wc[0][dd] = 0;
             __syncthreads();
-            if (ok) atomicAdd(&s_wc[1][d], 1u);
+            if (ok) atomicAdd(&s_wc[0][d], 1u);
             __syncthreads();
-            if (tid < kRadix) s_off[tid] += s_wc[1][tid];
+            for (int dd = tid; dd < kRadix; dd += NT) s_off[dd] += s_wc[0][dd];
             __syncthreads();
         }
     }
     // result in kA/vA after 8 passes (pass 7 writes A)
+}
+
+// Re-order runs of equal coarse keys by the full 64-bit key (stable).  A run
+// longer than kMaxRun sets *need_full; the kernel's last block to finish then
+// recomputes the whole order (full_sort_block) into idx.
+__global__ void __launch_bounds__(kThreads)
+fixup_kernel(const uint32_t *ck, uint32_t *idx, int64_t n, const uint64_t *full,
+             int32_t *need_full, uint32_t *done, uint64_t *fkA, uint64_t *fkB, uint32_t *vscratch) {
+    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
+    const uint32_t k = i < n ? ck[i] : kInvisible;
+    const bool head = k != kInvisible && (i == 0 || ck[i - 1] != k) && i + 1 < n && ck[i + 1] == k;
+    if (head) {
+        int64_t e = i + 1;
+        while (e < n && ck[e] == k && e - i <= kMaxRun) ++e;
+        if (e - i > kMaxRun) {
+            *need_full = 1;
+        } else {
+            const int len = (int)(e - i);
+            uint32_t v[kMaxRun];
+            uint64_t key[kMaxRun];
+            for (int a = 0; a < len; ++a) {
+                v[a] = idx[i + a];
+                key[a] = full[v[a]];
+            }
+            for (int a = 1; a < len; ++a) {  // stable insertion sort (indices ascending on ties)
+                const uint32_t tv = v[a];
+                const uint64_t tk = key[a];
+                int b = a - 1;
+                while (b >= 0 && key[b] > tk) {
+                    key[b + 1] = key[b];
+                    v[b + 1] = v[b];
+                    --b;
+                }
+                key[b + 1] = tk;
+                v[b + 1] = tv;
+            }
+            for (int a = 0; a < len; ++a) idx[i + a] = v[a];
+        }
+    }
+    // last block to finish: the full sort if any run was too long
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last || ld_volatile((const uint32_t *)need_full) == 0) return;
+    __threadfence();
+    full_sort_block<kThreads>(full, n, fkA, fkB, idx, vscratch);
 }
 
 // ----------------------------------------------------------------- placement
@@ -591,44 +550,89 @@ pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
         hist[(int64_t)(tb + t) * nblocks + blockIdx.x] = (uint32_t)D[(t / C.ntx) * w1 + t % C.ntx];
 }
 
-// tile_ranges = exclusive scan of tile totals (single block)
-__global__ void __launch_bounds__(1024)
-tile_ranges_kernel(const uint32_t *totals, int ntiles, int32_t *ranges, uint32_t cap,
-                   int32_t *n_pairs) {
-    __shared__ uint32_t s_warp[32];
+// Per-tile exclusive scan of the per-block pair counts (hist[tile][block],
+// one warp per tile row, 32 coalesced columns per step) -> tile totals; the
+// kernel's last block to finish then writes tile_ranges = exclusive scan of
+// the totals (P = their sum, ranges clamped to the pair capacity so an
+// overflowed frame never makes K3/K4 read past pair_splat), the optional
+// heaviest-first tile schedule for K3/K4 (a 64-bucket counting sort of the
+// tile pair counts; scheduling only), and re-arms the depth min/max words
+// that K1 of the next frame reduces into.
+constexpr int kOrderBuckets = 64;
+
+__global__ void __launch_bounds__(kThreads)
+tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, uint32_t *totals, uint32_t *done,
+                 int32_t *ranges, uint32_t cap, int32_t *n_pairs, int32_t *order,
+                 unsigned long long *mm) {
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    uint64_t carry = 0;
-    for (int base = 0; base < ntiles; base += 1024) {
-        const int i = base + threadIdx.x;
-        const uint32_t v = i < ntiles ? totals[i] : 0;
-        uint32_t x = v;
-        for (int o = 1; o < 32; o <<= 1) {
-            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-            if (lane >= o) x += y;
-        }
-        if (lane == 31) s_warp[warp] = x;
-        __syncthreads();
-        if (warp == 0) {
-            uint32_t w = s_warp[lane];
+    const int r = blockIdx.x * kWarps + warp;
+    if (r < ntiles) {
+        uint32_t *row = hist + (int64_t)r * nblocks;
+        uint32_t carry = 0;
+#pragma unroll 4
+        for (int base = 0; base < nblocks; base += 32) {
+            const int i = base + lane;
+            const uint32_t v = i < nblocks ? row[i] : 0;
+            uint32_t x = v;
+#pragma unroll
             for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
-                if (lane >= o) w += y;
+                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+                if (lane >= o) x += y;
             }
-            s_warp[lane] = w;
+            if (i < nblocks) row[i] = carry + x - v;
+            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        __syncthreads();
-        const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0);
-        // clamped to the pair capacity: an overflowed frame (n_pairs > capacity,
-        // detected by the caller) never makes K3/K4 read past pair_splat
+        if (lane == 0) totals[r] = carry;
+    }
+    __shared__ bool s_last;
+    __threadfence();
+    __syncthreads();
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    __shared__ uint32_t s_warp[kWarps];
+    uint64_t carry = 0;
+    for (int base = 0; base < ntiles; base += kThreads) {
+        const int i = base + threadIdx.x;
+        const uint32_t v = i < ntiles ? __ldcg(totals + i) : 0;
+        uint32_t tot;
+        const uint32_t incl = block_incl_scan(v, s_warp, tot);
         if (i < ntiles) ranges[i] = (int32_t)min(carry + incl - v, (uint64_t)cap);
-        carry += s_warp[31];
-        __syncthreads();
+        carry += tot;
     }
     if (threadIdx.x == 0) {
         ranges[ntiles] = (int32_t)min(carry, (uint64_t)cap);
         // P = the sum of all tile counts (unclamped; saturated to int32)
         *n_pairs = carry > 0x7fffffffull ? 0x7fffffff : (int32_t)carry;
+        if (mm) {
+            mm[0] = ~0ull;
+            mm[1] = 0ull;
+        }
     }
+    if (!order) return;
+    __syncthreads();
+    __shared__ int s_hist[kOrderBuckets];
+    if (threadIdx.x < kOrderBuckets) s_hist[threadIdx.x] = 0;
+    __syncthreads();
+    auto bucket = [](int cnt) {
+        const int b = (int)(2.0f * __log2f((float)cnt + 1.0f));
+        return kOrderBuckets - 1 - (b < kOrderBuckets - 1 ? b : kOrderBuckets - 1);
+    };
+    for (int t = threadIdx.x; t < ntiles; t += kThreads)
+        atomicAdd(&s_hist[bucket(ranges[t + 1] - ranges[t])], 1);
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int b = 0; b < kOrderBuckets; ++b) {
+            const int c = s_hist[b];
+            s_hist[b] = run;
+            run += c;
+        }
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += kThreads)
+        order[atomicAdd(&s_hist[bucket(ranges[t + 1] - ranges[t])], 1)] = t;
 }
 
 // stable placement: warp w of block b owns ranks [b*2048 + w*256, +256).
@@ -724,24 +728,30 @@ struct Plan {
     size_t off[16];
     size_t total;
     int nbk, nbp;
+    size_t ctrl_bytes;  // zeroed per frame: digit histograms, counters, flags, look-back words
 };
+
+// control block (offset 8): gdig[4][256] | vctr[4] | done_fix | done_tiles |
+// need_full | pad | status[4][nbk][256]
+constexpr size_t kCtrlHead = 4 * 256 * 4 + 64;
 
 Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
     Plan L{};
     L.nbk = (int)((n + kChunk - 1) / kChunk);
     L.nbp = (int)((n + kRanksPerBlock - 1) / kRanksPerBlock);
+    L.ctrl_bytes = kCtrlHead + (size_t)4 * L.nbk * kRadix * 4;
     size_t sz[16] = {
         al(4 * (size_t)n), al(4 * (size_t)n),                    // 0,1 coarse keys A/B
         al(4 * (size_t)n), al(4 * (size_t)n),                    // 2,3 vals A/B
         al(8 * (size_t)n), al(8 * (size_t)n),                    // 4,5 full keys (fallback) A/B
         al(4),                                                   // 6 (unused)
         al(4),                                                   // 7 (unused)
-        al(4 * (size_t)256 * (L.nbk + 1)),                       // 8 radix blockhist
-        al(4 * 256),                                             // 9 radix rowtotal
+        al(L.ctrl_bytes),                                        // 8 control block
+        al(4),                                                   // 9 (unused)
         al(4 * (size_t)ntiles * (L.nbp + 1)),                    // 10 pair tile hist
         al(4 * (size_t)(ntiles + 1)),                            // 11 tile totals
-        al(16),                                                  // 12 minmax
-        al(16),                                                  // 13 flags
+        al(16),                                                  // 12 minmax (keys supplied directly)
+        al(16),                                                  // 13 (unused)
         0, 0};
     size_t o = 0;
     for (int i = 0; i < 16; ++i) {
@@ -750,23 +760,6 @@ Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
     }
     L.total = o;
     return L;
-}
-
-template <typename KeyT>
-void radix_pass(cudaStream_t st, KeyT *k_in, const uint32_t *v_in, KeyT *k_out,
-                uint32_t *v_out, int64_t n, int shift, int nbk, uint32_t *bh, uint32_t *rt,
-                const int32_t *gate, const uint64_t *full = nullptr,
-                const unsigned long long *mm = nullptr, int vbits = 0) {
-    if (full)  // k_in is written here from the 64-bit keys (first pass, KeyT = uint32_t)
-        upsweep_coarse_kernel<<<nbk, kThreads, 0, st>>>(full, n, mm, vbits, (uint32_t *)k_in, bh, nbk);
-    else
-        upsweep_kernel<KeyT><<<nbk, kThreads, 0, st>>>(k_in, n, shift, bh, nbk, gate);
-    if (nbk <= 2048)
-        rowscan_warp_kernel<<<256 / kRowsPerBlock, 32 * kRowsPerBlock, 0, st>>>(bh, 256, nbk, rt, gate);
-    else
-        rowscan_kernel<<<256, 1024, 0, st>>>(bh, nbk, rt, gate);
-    downsweep_kernel<KeyT><<<nbk, kThreads, 0, st>>>(k_in, v_in, n, shift, bh, rt, nbk, k_out, v_out,
-                                                     gate);
 }
 }  // namespace
 
@@ -778,8 +771,9 @@ extern "C" int ivr_bin_sort(int64_t n, const uint64_t *depth_key, const int32_t 
                             const uint16_t *rect, int32_t ntx, int32_t nty, int64_t pair_capacity,
                             void *workspace, size_t workspace_bytes, int32_t *pair_splat,
                             int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream) {
-    return ivr_bin_sort_cull(n, depth_key, count, rect, nullptr, ntx, nty, 0, 0, pair_capacity,
-                             workspace, workspace_bytes, pair_splat, tile_ranges, n_pairs, stream);
+    return ivr_bin_sort_frame(n, depth_key, nullptr, count, rect, nullptr, ntx, nty, 0, 0,
+                              pair_capacity, workspace, workspace_bytes, pair_splat, tile_ranges,
+                              n_pairs, nullptr, stream);
 }
 
 extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int32_t *count,
@@ -787,6 +781,18 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
                                  int32_t width, int32_t height, int64_t pair_capacity,
                                  void *workspace, size_t workspace_bytes, int32_t *pair_splat,
                                  int32_t *tile_ranges, int32_t *n_pairs, ivr_stream_t stream) {
+    return ivr_bin_sort_frame(n, depth_key, nullptr, count, rect, rec, ntx, nty, width, height,
+                              pair_capacity, workspace, workspace_bytes, pair_splat, tile_ranges,
+                              n_pairs, nullptr, stream);
+}
+
+extern "C" int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key,
+                                  unsigned long long *depth_minmax, const int32_t *count,
+                                  const uint16_t *rect, const float *rec, int32_t ntx, int32_t nty,
+                                  int32_t width, int32_t height, int64_t pair_capacity,
+                                  void *workspace, size_t workspace_bytes, int32_t *pair_splat,
+                                  int32_t *tile_ranges, int32_t *n_pairs, int32_t *tile_order,
+                                  ivr_stream_t stream) {
     cudaStream_t st = (cudaStream_t)stream;
     const int32_t ntiles = ntx * nty;
     // placement keeps 8 per-warp int32 difference arrays of (ntx+1)(rows+1)
@@ -801,8 +807,8 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
         ivr::set_error("ivr_bin_sort: bad argument");
         return IVR_ERR_ARG;
     }
-    if (n > 0x7fffffffll || pair_capacity > 0x7fffffffll) {
-        ivr::set_error("ivr_bin_sort: sizes must fit int32");
+    if (n >= (1ll << 30) || pair_capacity > 0x7fffffffll) {
+        ivr::set_error("ivr_bin_sort: n must be below 2^30 and the capacity fit int32");
         return IVR_ERR_ARG;
     }
     const Plan L = plan(n < 1 ? 1 : n, pair_capacity, ntiles);
@@ -813,52 +819,58 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
     if (n == 0) {
         cudaMemsetAsync(n_pairs, 0, 4, st);
         cudaMemsetAsync(tile_ranges, 0, 4 * (size_t)(ntiles + 1), st);
+        if (tile_order) ivr_tile_order(tile_ranges, ntiles, tile_order, stream);
         return ivr::check_launch("ivr_bin_sort(empty)");
     }
     char *ws = (char *)workspace;
     uint32_t *ckA = (uint32_t *)(ws + L.off[0]), *ckB = (uint32_t *)(ws + L.off[1]);
     uint32_t *vA = (uint32_t *)(ws + L.off[2]), *vB = (uint32_t *)(ws + L.off[3]);
     uint64_t *fkA = (uint64_t *)(ws + L.off[4]), *fkB = (uint64_t *)(ws + L.off[5]);
-    uint32_t *bh = (uint32_t *)(ws + L.off[8]);
-    uint32_t *rt = (uint32_t *)(ws + L.off[9]);
+    char *ctrl = ws + L.off[8];
+    uint32_t *gdig = (uint32_t *)ctrl;
+    uint32_t *vctr = gdig + 4 * 256;
+    uint32_t *done_fix = vctr + 4, *done_tiles = vctr + 5;
+    int32_t *need_full = (int32_t *)(vctr + 6);
+    uint32_t *status = (uint32_t *)(ctrl + kCtrlHead);
     uint32_t *phist = (uint32_t *)(ws + L.off[10]);
     uint32_t *ttot = (uint32_t *)(ws + L.off[11]);
-    unsigned long long *mm = (unsigned long long *)(ws + L.off[12]);
-    int32_t *need_full = (int32_t *)(ws + L.off[13]);
     const int nbk = L.nbk, nbp = L.nbp;
+    const size_t status_pass = (size_t)nbk * kRadix;
 
     // ---- 1. depth ranks: coarse keys with ~8 buckets per splat (at least
-    //      log2(n) + 3 bits; 8-bit digits), stable LSD passes, run fix-up
+    //      log2(n) + 3 bits; 8-bit digits), one onesweep kernel per pass, run fix-up
     int lg = 1;
     while (lg < 62 && (1ll << lg) < n) ++lg;
     int passes = (lg + 4 + 7) / 8;
     passes = passes < 2 ? 2 : (passes > 4 ? 4 : passes);
     const int vbits = 8 * passes - 1;
-    init_minmax_kernel<<<1, 1, 0, st>>>(mm, need_full);
-    int gb = (int)((n + kThreads * 8 - 1) / (kThreads * 8));
-    gb = gb < 1 ? 1 : (gb > 1184 ? 1184 : gb);
-    minmax_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm);
+    cudaMemsetAsync(ctrl, 0, kCtrlHead + (size_t)passes * status_pass * 4, st);
+    unsigned long long *mm = depth_minmax;
+    if (!mm) {  // keys supplied directly: reduce their range here
+        mm = (unsigned long long *)(ws + L.off[12]);
+        init_minmax_kernel<<<1, 1, 0, st>>>(mm);
+        int gb = (int)((n + kThreads * 8 - 1) / (kThreads * 8));
+        gb = gb < 1 ? 1 : (gb > 1184 ? 1184 : gb);
+        minmax_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm);
+    }
+    hist_coarse_kernel<<<nbk, kThreads, 0, st>>>(depth_key, n, mm, vbits, passes, ckA, gdig);
     uint32_t *kin = ckA, *kout = ckB, *vin = nullptr, *vout = vB;
     for (int p = 0; p < passes; ++p) {
-        if (p == 0)  // coarse keys produced by the first upsweep
-            radix_pass<uint32_t>(st, kin, vin, kout, vout, n, 0, nbk, bh, rt, nullptr,
-                                 depth_key, mm, vbits);
-        else
-            radix_pass<uint32_t>(st, kin, vin, kout, vout, n, 8 * p, nbk, bh, rt, nullptr);
+        onesweep_kernel<uint32_t><<<nbk, kThreads, 0, st>>>(kin, vin, n, 8 * p, gdig + 256 * p,
+                                                           status + p * status_pass, vctr + p,
+                                                           kout, vout);
         uint32_t *t = kin;
         kin = kout;
         kout = t;
         vin = vout;
         vout = (vout == vB) ? vA : vB;
     }
-    // sorted (key, order) now in (kin, vin)
+    // sorted (key, order) now in (kin, vin); runs fixed, long runs -> full sort
     uint32_t *ord = vin, *vscratch = (vin == vA) ? vB : vA;
-    fixup_kernel<<<(int)((n + kThreads - 1) / kThreads), kThreads, 0, st>>>(kin, ord, n, depth_key,
-                                                                           need_full);
-    // fallback (device-gated, normally an immediate return): full 64-bit sort into ord
-    fallback_sort_kernel<<<1, kFbThreads, 0, st>>>(depth_key, n, need_full, fkA, fkB, ord, vscratch);
+    fixup_kernel<<<(int)((n + kThreads - 1) / kThreads), kThreads, 0, st>>>(
+        kin, ord, n, depth_key, need_full, done_fix, fkA, fkB, vscratch);
     // ---- 2. counting placement by tile (+ optional tile cull flag); the
-    // tile-range scan also yields P = n_pairs
+    // tile scan's last block writes the ranges, P = n_pairs and the schedule
     PairCtx C{};
     C.order = ord;
     C.count = count;
@@ -882,13 +894,9 @@ extern "C" int ivr_bin_sort_cull(int64_t n, const uint64_t *depth_key, const int
         C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
         pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
     }
-    if (nbp <= 2048)
-        rowscan_warp_kernel<<<(ntiles + kRowsPerBlock - 1) / kRowsPerBlock, 32 * kRowsPerBlock, 0, st>>>(
-            phist, ntiles, nbp, ttot, nullptr);
-    else
-        rowscan_kernel<<<ntiles, 1024, 0, st>>>(phist, nbp, ttot, nullptr);
-    tile_ranges_kernel<<<1, 1024, 0, st>>>(ttot, ntiles, tile_ranges, (uint32_t)pair_capacity,
-                                           n_pairs);
+    tile_scan_kernel<<<(ntiles + kWarps - 1) / kWarps, kThreads, 0, st>>>(
+        phist, ntiles, nbp, ttot, done_tiles, tile_ranges, (uint32_t)pair_capacity, n_pairs,
+        tile_order, depth_minmax);
     for (int y0 = 0; y0 < nty; y0 += band_rows) {
         C.ty_lo = y0;
         C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;

@@ -160,6 +160,14 @@ class Workspace:
             self.bufs[name] = t
         return t[:numel]
 
+    def depth_minmax(self):
+        """K1 -> K2 depth-range words, armed to {~0, 0} once; K2 re-arms them
+        after every frame (ivr_bin_sort_frame)."""
+        t = self.bufs.get("depth_mm")
+        if t is None:
+            t = self.bufs["depth_mm"] = torch.tensor([-1, 0], dtype=torch.int64, device=self.device)
+        return t
+
 
 class Frame:
     """Device outputs of one rasterization (kept alive for the backward)."""
@@ -200,6 +208,8 @@ def preprocess(dg: DeviceGaussians, cam, K, cols, ws: Workspace, shading=None, e
         F._keep.append(t)
     out = L.ProjOut_t()
     out.depth_key, out.count, out.rect = F.depth_key.data_ptr(), F.count.data_ptr(), F.rect.data_ptr()
+    F.depth_mm = ws.depth_minmax()
+    out.depth_minmax = F.depth_mm.data_ptr()
     out.rec, out.values = F.rec.data_ptr(), F.values.data_ptr()
     if f64:
         out.rec64, out.values64 = F.rec64.data_ptr(), F.values64.data_ptr()
@@ -278,19 +288,19 @@ def bin_sort(F: Frame, ws: Workspace, stream=None, capacity=None):
     F.n_pairs = ws.get("n_pairs", 1, torch.int32)
     F.capacity = cap
     # K2; the per-(splat, tile) cull runs in K3/K4 staging (precull=False) or
-    # here as bit 31 of pair_splat (precull=True; masked in .pairs())
+    # here as bit 31 of pair_splat (precull=True; masked in .pairs()).  K1's
+    # depth range and the K3/K4 tile schedule ride along (ivr_bin_sort_frame).
     precull = os.environ.get("IVR_PRECULL", "0") == "1"
-    L.check(L.lib().ivr_bin_sort_cull(n, ptr(F.depth_key), ptr(F.count), ptr(F.rect),
-                                      ptr(F.rec) if precull else None, ntx, nty, cam.width,
-                                      cam.height, cap, ptr(scratch), nbytes, ptr(F.pair_splat),
-                                      ptr(F.tile_ranges), ptr(F.n_pairs), stream_handle(stream)),
-            "ivr_bin_sort_cull")
-    F.preculled = precull
     F.tile_order = None
     if os.environ.get("IVR_TILE_ORDER", "1") != "0":
         F.tile_order = ws.get("tile_order", ntx * nty, torch.int32)
-        L.check(L.lib().ivr_tile_order(ptr(F.tile_ranges), ntx * nty, ptr(F.tile_order),
-                                       stream_handle(stream)), "ivr_tile_order")
+    mm = getattr(F, "depth_mm", None)
+    L.check(L.lib().ivr_bin_sort_frame(n, ptr(F.depth_key), ptr(mm), ptr(F.count), ptr(F.rect),
+                                       ptr(F.rec) if precull else None, ntx, nty, cam.width,
+                                       cam.height, cap, ptr(scratch), nbytes, ptr(F.pair_splat),
+                                       ptr(F.tile_ranges), ptr(F.n_pairs), ptr(F.tile_order),
+                                       stream_handle(stream)), "ivr_bin_sort_frame")
+    F.preculled = precull
     return F
 
 
@@ -455,6 +465,7 @@ def rasterize_device(dg, cam, K, cols, ws, shading=None, edits=None, colors=None
     bin_sort(F, ws, stream)
     P = int(F.n_pairs.item())
     if P > F.capacity:
+        F.depth_mm = None  # consumed (re-armed) by the first pass: K2 reduces the range itself
         bin_sort(F, ws, stream, capacity=int(P * 1.25) + 4096)
         P = int(F.n_pairs.item())
     F.P = P
