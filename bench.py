@@ -33,19 +33,14 @@ sys.path.insert(0, REPO)
 METRIC = "800x800 render FPS (composed 1M Gaussians), train it/s, % HBM roofline, 1-8 GPU"
 W_IMG = H_IMG = 800
 PER_MODEL, N_MODELS, DENSITY = 200_000, 5, 1_000_000
-# our kernels per frame: K1 (1) + K2 (init, minmax, coarse key, 4x3 radix, fix-up,
-# fallback gate, 3 scan, tile hist, tile rowscan, tile ranges, placement, tile order
-# = 25) + K3 (1)
 def launches_per_frame(n):
-    """Kernels in one captured frame: K1; K2 = init + minmax + 3 per radix
-    pass (the first upsweep also maps the coarse keys) + fix-up + fallback
-    gate + hist + rowscan + tile ranges (also P) + placement; tile order; K3
-    (sort.cu / blend.cu)."""
-    lg = 1
-    while (1 << lg) < n:
-        lg += 1
-    passes = min(max((lg + 4 + 7) // 8, 2), 4)
-    return 1 + (2 + 3 * passes + 2 + 4) + 1 + 1
+    """Kernels in one captured frame (sort.cu / blend.cu): K1; K2 = bucket
+    count, bucket scan, bucket scatter, bucket sort (+ long-run fallback in
+    its last block), tile histogram, tile scan (+ ranges / P / schedule /
+    re-arm in its last block), placement; K3.  Plus one memset node (K2's
+    control block)."""
+    del n
+    return 1 + 7 + 1
 
 
 SLOTS = int(os.environ.get("IVR_SLOTS", "6"))  # concurrent frame slots (FrameGraph / FramePipeline)

@@ -5,20 +5,17 @@
 // np.searchsorted (rasterizer.py:132), without materialising a composite key:
 //
 //  1. depth ranks.  Positive float64 depths order like their bit patterns.
-//     The bits are shifted into a "coarse" key (bits - min) >> s of about
-//     log2(n) + 3 bits (~8 buckets per splat; the [min, max] of the visible
+//     The bits are shifted into a "coarse" key (bits - min) >> s of
+//     log2(n) + 1 bits (~2 buckets per splat; the [min, max] of the visible
 //     keys comes from K1's block-reduced atomics, or from a min/max kernel
-//     when the keys are supplied directly).  One histogram kernel maps the
-//     keys and counts every pass's 8-bit digits; each stable LSD pass is then
-//     ONE kernel (onesweep: 4096-key blocks take virtual ids in start order,
-//     publish their digit counts and find their exclusive prefix per digit by
-//     decoupled look-back over their predecessors, then scatter through
-//     shared memory).  Invisible splats carry all ones and sort last.  Runs
-//     of equal coarse keys are re-ordered by the full 64-bit key (insertion
-//     sort, stable); if a run is longer than kMaxRun the last block of that
-//     kernel recomputes the whole order with a full 64-bit LSD sort --
-//     correctness never depends on the data.  Ties keep index order =
-//     lexsort's tie break on fill_pairs' order.
+//     when the keys are supplied directly) and the splats are counting-sorted
+//     by it: bucket counts by atomics, one exclusive scan, a scatter that
+//     claims slots with an atomic cursor per bucket, then every bucket is
+//     sorted by (full 64-bit key, index) -- exactly lexsort's order, ties by
+//     index = fill_pairs' order (_kernels.py:21-28).  Invisible splats fill a
+//     last bucket.  A bucket longer than kMaxRun (extreme depth clustering)
+//     makes the sort kernel's last block recompute the whole order with a
+//     full 64-bit LSD sort -- correctness never depends on the data.
 //  2. counting placement: each block owns 2048 consecutive depth ranks; its
 //     warps expand their ranks' pairs in fill_pairs order (load-balanced
 //     warp expansion, no per-pair global searches), build a per-tile
@@ -32,8 +29,8 @@
 //     that cannot are marked with bit 31 (pair_splat & 0x7fffffff is the
 //     reference list), letting the blend skip them without loading records.
 // All data-dependent sizes live in device memory: the sequence is
-// stream-ordered and CUDA-graph capturable (8 kernels + one control-block
-// memset per frame at 1M splats).
+// stream-ordered and CUDA-graph capturable (7 kernels + one control-block
+// memset per frame).
 #include "cull.cuh"
 
 namespace ivr {
@@ -41,28 +38,20 @@ namespace sortk {
 
 constexpr int kThreads = 256;
 constexpr int kWarps = kThreads / 32;
-constexpr int kItems = 16;                 // per thread in radix passes
-constexpr int kChunk = kThreads * kItems;  // 4096 keys per radix block
+constexpr int kItems = 16;                 // per thread in the bucket passes
+constexpr int kChunk = kThreads * kItems;  // 4096 keys / counts per block
 constexpr int kRadix = 256;
 constexpr int kMaxRun = 64;
-constexpr uint32_t kInvisible = 0xffffffffu;
 
 __global__ void init_minmax_kernel(unsigned long long *mm) {
     mm[0] = ~0ull;
     mm[1] = 0ull;
 }
 
-// Look-back status words: 2 flag bits (1 = block aggregate, 2 = inclusive
-// prefix) over a 30-bit count; 0 = not yet published.
-constexpr uint32_t kFlagAgg = 1u << 30, kFlagPrefix = 2u << 30, kValMask = (1u << 30) - 1;
-
 __device__ __forceinline__ uint32_t ld_volatile(const uint32_t *p) {
     uint32_t v;
     asm volatile("ld.volatile.global.u32 %0, [%1];" : "=r"(v) : "l"(p));
     return v;
-}
-__device__ __forceinline__ void st_volatile(uint32_t *p, uint32_t v) {
-    asm volatile("st.volatile.global.u32 [%0], %1;" ::"l"(p), "r"(v));
 }
 
 __device__ __forceinline__ int64_t load_n(const int32_t *n_dev, int64_t n_host, int64_t cap) {
@@ -134,23 +123,22 @@ minmax_kernel(const uint64_t *keys, int64_t n, unsigned long long *mm /* [min, m
     }
 }
 
-// ----------------------------------------------------------------- radix passes
-// Coarse keys + every pass's digit histogram in one read of the 64-bit keys:
-// visible keys get `vbits` bits ((bits - min) >> s < 2^vbits), invisible
-// splats all ones (above every visible key); per-block shared histograms are
-// added into the global per-pass digit counts gdig[pass][256] (zeroed by the
-// frame's control-block memset).
+// ----------------------------------------------------------------- bucket ranks
+// Depth ranks by one counting sort on the coarse key: nb = 2^vbits buckets
+// (~2 per splat) + one for the invisible splats (last).  Bucket counts by
+// global atomics, an exclusive scan of the counts (single pass, decoupled
+// look-back), a scatter that claims each splat's slot with an atomic on its
+// bucket cursor (so the order inside a bucket is arbitrary), and a per-bucket
+// sort by (full 64-bit key, index) -- lexsort's order, ties by index -- in
+// fixup_buckets_kernel.
 __global__ void __launch_bounds__(kThreads)
-hist_coarse_kernel(const uint64_t *full, int64_t n, const unsigned long long *mm, int vbits,
-                   int passes, uint32_t *ck, uint32_t *gdig) {
-    __shared__ uint32_t s[4][kRadix];
-#pragma unroll
-    for (int p = 0; p < 4; ++p) s[p][threadIdx.x] = 0;
+bucket_count_kernel(const uint64_t *full, int64_t n, const unsigned long long *mm, int vbits,
+                    uint32_t *ck, uint32_t *counts) {
     const unsigned long long lo = mm[0], hi = mm[1];
     const unsigned long long range = hi >= lo ? hi - lo : 0ull;
     const int bits = range ? 64 - __clzll((long long)range) : 0;
     const int sh = bits > vbits ? bits - vbits : 0;
-    __syncthreads();
+    const uint32_t nb = 1u << vbits;
     const int64_t base = (int64_t)blockIdx.x * kChunk;
     unsigned long long k[kItems];
 #pragma unroll
@@ -162,119 +150,86 @@ hist_coarse_kernel(const uint64_t *full, int64_t n, const unsigned long long *mm
     for (int r = 0; r < kItems; ++r) {
         const int64_t idx = base + r * kThreads + threadIdx.x;
         if (idx < n) {
-            const uint32_t c = k[r] == ~0ull ? kInvisible : (uint32_t)((k[r] - lo) >> sh);
+            const uint32_t c = k[r] == ~0ull ? nb : (uint32_t)((k[r] - lo) >> sh);
             ck[idx] = c;
-            for (int p = 0; p < passes; ++p) atomicAdd(&s[p][(c >> (8 * p)) & 255u], 1u);
+            atomicAdd(counts + c, 1u);
         }
     }
-    __syncthreads();
-    for (int p = 0; p < passes; ++p)
-        if (s[p][threadIdx.x]) atomicAdd(&gdig[p * kRadix + threadIdx.x], s[p][threadIdx.x]);
 }
 
-// One stable LSD pass (8-bit digit at `shift`) of (key, value) pairs as a
-// single kernel.  vals_in == nullptr means identity values.  Blocks take
-// virtual ids in the order they start (so every predecessor is running and
-// look-back cannot deadlock), rank their 4096 keys by digit (warp match_any),
-// publish per-digit counts, and obtain each digit's exclusive prefix over the
-// earlier blocks by decoupled look-back on status[block][digit]; the digit
-// bases come from the pass's global histogram (hist_coarse_kernel).
-template <typename KeyT>
+// Exclusive scan of counts[0..m): each block scans its 4096 counts in place
+// (block-local offsets) and leaves its total in boff[block]; the kernel's last
+// block to finish turns boff into the exclusive block offsets (so a bucket
+// c starts at boff[c >> 12] + counts[c]).
 __global__ void __launch_bounds__(kThreads)
-onesweep_kernel(const KeyT *keys, const uint32_t *vals, int64_t n, int shift,
-                const uint32_t *gdig, uint32_t *status, uint32_t *vctr, KeyT *dkeys,
-                uint32_t *dvals) {
-    __shared__ uint32_t s_wcnt[kWarps][kRadix];
-    __shared__ uint32_t s_gbase[kRadix];
-    __shared__ uint32_t s_lstart[kRadix];
+bucket_scan_kernel(uint32_t *counts, int64_t m, uint32_t *boff, uint32_t *done) {
     __shared__ uint32_t s_warp[kWarps];
-    __shared__ uint32_t s_bid;
-    __shared__ KeyT s_keys[kChunk];
-    __shared__ uint32_t s_vals[kChunk];
-
-    const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
-    if (tid == 0) s_bid = atomicAdd(vctr, 1u);
+    __shared__ bool s_last;
+    __shared__ uint32_t s_c[kChunk + kChunk / 32];  // padded: conflict-free row reads
+    const int tid = threadIdx.x;
+    const int64_t b0 = (int64_t)blockIdx.x * kChunk;
+    auto pad = [](int i) { return i + (i >> 5); };
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) s_wcnt[w][tid] = 0;
-    __syncthreads();
-    const uint32_t bid = s_bid;
-    const int64_t base = (int64_t)bid * kChunk;
-    KeyT k[kItems];
-    uint32_t v[kItems];
-#pragma unroll
-    for (int r = 0; r < kItems; ++r) {  // all loads first (memory-level parallelism)
-        const int64_t idx = base + warp * (32 * kItems) + r * 32 + lane;
-        const bool ok = idx < n;
-        k[r] = ok ? keys[idx] : (KeyT)0;
-        v[r] = ok ? (vals ? vals[idx] : (uint32_t)idx) : 0u;
+    for (int r = 0; r < kItems; ++r) {  // coalesced in, each thread then owns 16 in a row
+        const int i = r * kThreads + tid;
+        s_c[pad(i)] = b0 + i < m ? counts[b0 + i] : 0u;
     }
-    uint32_t dig[kItems], rank[kItems];
-    const uint32_t lt = lanemask_lt();
+    __syncthreads();
+    uint32_t v[kItems];
+    uint32_t sum = 0;
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
-        const int64_t idx = base + warp * (32 * kItems) + r * 32 + lane;
-        const bool ok = idx < n;
-        dig[r] = ok ? ((uint32_t)(k[r] >> shift) & 255u) : 256u;
-        const uint32_t peers = __match_any_sync(0xffffffffu, dig[r]);
-        uint32_t before = 0;
-        if (ok) before = s_wcnt[warp][dig[r]];
-        __syncwarp();
-        if (ok && (peers & lt) == 0) s_wcnt[warp][dig[r]] = before + __popc(peers);
-        __syncwarp();
-        rank[r] = before + __popc(peers & lt);
-    }
-    __syncthreads();
-    uint32_t cnt;  // this block's count of digit tid
-    {
-        uint32_t run = 0;
-#pragma unroll
-        for (int w = 0; w < kWarps; ++w) {
-            const uint32_t c = s_wcnt[w][tid];
-            s_wcnt[w][tid] = run;
-            run += c;
-        }
-        cnt = run;
-    }
-    // publish the aggregate (block 0: already the inclusive prefix), then look back
-    uint32_t *my = status + (int64_t)bid * kRadix + tid;
-    st_volatile(my, (bid == 0 ? kFlagPrefix : kFlagAgg) | cnt);
-    uint32_t excl = 0;
-    if (bid > 0) {
-        int64_t j = (int64_t)bid - 1;
-        while (true) {
-            const uint32_t w = ld_volatile(status + j * kRadix + tid);
-            if ((w & ~kValMask) == 0) continue;  // predecessor not published yet
-            excl += w & kValMask;
-            if (w & kFlagPrefix) break;
-            --j;
-        }
-        st_volatile(my, kFlagPrefix | (excl + cnt));
+        v[r] = s_c[pad(tid * kItems + r)];
+        sum += v[r];
     }
     uint32_t tot;
-    const uint32_t gd = gdig[tid];
-    const uint32_t ginc = block_incl_scan(gd, s_warp, tot);
-    s_gbase[tid] = ginc - gd + excl;
-    {
-        const uint32_t inc = block_incl_scan(cnt, s_warp, tot);
-        s_lstart[tid] = inc - cnt;
+    const uint32_t incl = block_incl_scan(sum, s_warp, tot);
+    uint32_t run = incl - sum;
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        s_c[pad(tid * kItems + r)] = run;
+        run += v[r];
     }
     __syncthreads();
 #pragma unroll
     for (int r = 0; r < kItems; ++r) {
-        if (dig[r] < 256u) {
-            const uint32_t lp = s_lstart[dig[r]] + s_wcnt[warp][dig[r]] + rank[r];
-            s_keys[lp] = k[r];
-            s_vals[lp] = v[r];
-        }
+        const int i = r * kThreads + tid;
+        if (b0 + i < m) counts[b0 + i] = s_c[pad(i)];
     }
+    if (tid == 0) boff[blockIdx.x] = tot;
+    __threadfence();
     __syncthreads();
-    const int nvalid = (int)((n - base) < kChunk ? (n - base) : kChunk);
-    for (int i = tid; i < nvalid; i += kThreads) {
-        const KeyT kk = s_keys[i];
-        const uint32_t d = (uint32_t)(kk >> shift) & 255u;
-        const uint32_t g = s_gbase[d] + (uint32_t)i - s_lstart[d];
-        dkeys[g] = kk;
-        dvals[g] = s_vals[i];
+    if (tid == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    __syncthreads();
+    if (!s_last) return;
+    __threadfence();
+    const int nb = gridDim.x;
+    uint32_t carry = 0;
+    for (int b0 = 0; b0 < nb; b0 += kThreads) {
+        const int b = b0 + tid;
+        const uint32_t x = b < nb ? __ldcg(boff + b) : 0u;
+        const uint32_t inc = block_incl_scan(x, s_warp, tot);
+        if (b < nb) boff[b] = carry + inc - x;
+        carry += tot;
+    }
+}
+
+// Scatter: each splat claims the next slot of its bucket (cursor = the
+// scanned offset; afterwards cursor[c] = the start of bucket c + 1).
+__global__ void __launch_bounds__(kThreads)
+bucket_scatter_kernel(const uint32_t *ck, int64_t n, uint32_t *cursor, const uint32_t *boff,
+                      uint32_t *idx) {
+    const int64_t base = (int64_t)blockIdx.x * kChunk;
+    uint32_t c[kItems];
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int64_t i = base + r * kThreads + threadIdx.x;
+        c[r] = i < n ? ck[i] : 0u;
+    }
+#pragma unroll
+    for (int r = 0; r < kItems; ++r) {
+        const int64_t i = base + r * kThreads + threadIdx.x;
+        if (i < n) idx[boff[c[r] / kChunk] + atomicAdd(cursor + c[r], 1u)] = (uint32_t)i;
     }
 }
 
@@ -349,52 +304,96 @@ __device__ void full_sort_block(const uint64_t *depth_key, int64_t n, uint64_t *
     // result in kA/vA after 8 passes (pass 7 writes A)
 }
 
-// Re-order runs of equal coarse keys by the full 64-bit key (stable).  A run
-// longer than kMaxRun sets *need_full; the kernel's last block to finish then
-// recomputes the whole order (full_sort_block) into idx.
-__global__ void __launch_bounds__(kThreads)
-fixup_kernel(const uint32_t *ck, uint32_t *idx, int64_t n, const uint64_t *full,
-             int32_t *need_full, uint32_t *done, uint64_t *fkA, uint64_t *fkB, uint32_t *vscratch) {
-    const int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x;
-    const uint32_t k = i < n ? ck[i] : kInvisible;
-    const bool head = k != kInvisible && (i == 0 || ck[i - 1] != k) && i + 1 < n && ck[i + 1] == k;
-    if (head) {
-        int64_t e = i + 1;
-        while (e < n && ck[e] == k && e - i <= kMaxRun) ++e;
-        if (e - i > kMaxRun) {
-            *need_full = 1;
-        } else {
-            const int len = (int)(e - i);
-            uint32_t v[kMaxRun];
-            uint64_t key[kMaxRun];
-            for (int a = 0; a < len; ++a) {
-                v[a] = idx[i + a];
-                key[a] = full[v[a]];
-            }
-            for (int a = 1; a < len; ++a) {  // stable insertion sort (indices ascending on ties)
-                const uint32_t tv = v[a];
-                const uint64_t tk = key[a];
-                int b = a - 1;
-                while (b >= 0 && key[b] > tk) {
-                    key[b + 1] = key[b];
-                    v[b + 1] = v[b];
-                    --b;
-                }
-                key[b + 1] = tk;
-                v[b + 1] = tv;
-            }
-            for (int a = 0; a < len; ++a) idx[i + a] = v[a];
+// Sort a run of <= M ranks in registers by (full key, index).
+template <int M>
+__device__ __forceinline__ void sort_run(uint32_t *idx, int64_t i, int len, const uint64_t *full) {
+    uint32_t v[M];
+    uint64_t key[M];
+#pragma unroll
+    for (int a = 0; a < M; ++a) {
+        v[a] = a < len ? idx[i + a] : 0xffffffffu;
+        key[a] = a < len ? full[v[a]] : ~0ull;
+    }
+    // insertion network; padding entries (key ~0, index ~0) stay last
+#pragma unroll
+    for (int a = 1; a < M; ++a) {
+#pragma unroll
+        for (int b = a; b > 0; --b) {
+            const bool sw = key[b - 1] > key[b] || (key[b - 1] == key[b] && v[b - 1] > v[b]);
+            const uint64_t k0 = key[b - 1], k1 = key[b];
+            const uint32_t v0 = v[b - 1], v1 = v[b];
+            key[b - 1] = sw ? k1 : k0;
+            key[b] = sw ? k0 : k1;
+            v[b - 1] = sw ? v1 : v0;
+            v[b] = sw ? v0 : v1;
         }
     }
-    // last block to finish: the full sort if any run was too long
+#pragma unroll
+    for (int a = 0; a < M; ++a)
+        if (a < len) idx[i + a] = v[a];
+}
+
+// Per-bucket sort by (full key, index) after the scatter (bucket c spans
+// [end[c - 1], end[c]) with end = the advanced cursors); a bucket larger than
+// kMaxRun sets *need_full and the last block recomputes the whole order.
+constexpr int kFixThreads = 1024;
+constexpr int kFixPer = 4;  // buckets per thread
+__global__ void __launch_bounds__(kFixThreads)
+fixup_buckets_kernel(const uint32_t *end, const uint32_t *boff, uint32_t nb, uint32_t *idx,
+                     int64_t n, const uint64_t *full, int32_t *need_full, uint32_t *done,
+                     uint64_t *fkA, uint64_t *fkB, uint32_t *vscratch) {
+    bool flagged = false;
+    const int64_t c0 = ((int64_t)blockIdx.x * kFixThreads + threadIdx.x) * kFixPer;
+    uint32_t ends[kFixPer + 1];
+#pragma unroll
+    for (int q = 0; q <= kFixPer; ++q) {
+        const int64_t c = c0 + q - 1;  // ends[q] = end of bucket c0 + q - 1
+        ends[q] = c < 0 ? 0u : (c < nb ? boff[c / kChunk] + end[c] : 0u);
+    }
+#pragma unroll
+    for (int q = 0; q < kFixPer; ++q) {
+        const int64_t c = c0 + q;
+        if (c >= nb) break;
+        const uint32_t b = ends[q], e = ends[q + 1];
+        const int len = (int)(e - b);
+        if (len > kMaxRun) {
+            *need_full = 1;
+            flagged = true;
+        } else if (len >= 2) {
+            if (len <= 4) {
+                sort_run<4>(idx, b, len, full);
+            } else if (len <= 8) {
+                sort_run<8>(idx, b, len, full);
+            } else {
+                uint32_t v[kMaxRun];
+                uint64_t key[kMaxRun];
+                for (int a = 0; a < len; ++a) {
+                    v[a] = idx[b + a];
+                    key[a] = full[v[a]];
+                }
+                for (int a = 1; a < len; ++a) {  // insertion sort by (key, index)
+                    const uint32_t tv = v[a];
+                    const uint64_t tk = key[a];
+                    int z = a - 1;
+                    while (z >= 0 && (key[z] > tk || (key[z] == tk && v[z] > tv))) {
+                        key[z + 1] = key[z];
+                        v[z + 1] = v[z];
+                        --z;
+                    }
+                    key[z + 1] = tk;
+                    v[z + 1] = tv;
+                }
+                for (int a = 0; a < len; ++a) idx[b + a] = v[a];
+            }
+        }
+    }
     __shared__ bool s_last;
-    __threadfence();
-    __syncthreads();
+    if (__syncthreads_or(flagged)) __threadfence();
     if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last || ld_volatile((const uint32_t *)need_full) == 0) return;
     __threadfence();
-    full_sort_block<kThreads>(full, n, fkA, fkB, idx, vscratch);
+    full_sort_block<kFixThreads>(full, n, fkA, fkB, idx, vscratch);
 }
 
 // ----------------------------------------------------------------- placement
@@ -464,25 +463,16 @@ __device__ __forceinline__ void prefix2d(int *D, int w1, int h1, int t, int nt, 
 // the group's inclusive count prefix.  f(ok, splat, tile, tx, ty) is called
 // by all 32 lanes for each 32-pair chunk (convergent; ok marks real pairs).
 template <typename Fn>
-__device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, int64_t rend, Fn &&f) {
+__device__ __forceinline__ void expand_pairs(const PairCtx &C, const uint32_t *sps,
+                                             const uint32_t *cnts, const uint32_t *rxs,
+                                             const uint32_t *rzs, Fn &&f) {
+    // group u = the warp's ranks rb + 32u .. + 31, lane l holding rank rb + 32u + l
+    // (already loaded and band-clipped by the caller: cnt 0 = no pairs)
     const int lane = threadIdx.x & 31;
-    for (int64_t g = rbase; g < rend; g += 32) {
-        const int64_t r = g + lane;
-        uint32_t sp = 0, cnt = 0, rx = 0, rz = 0;
-        if (r < rend) {
-            sp = C.order[r];
-            cnt = (uint32_t)C.count[sp];
-            if (cnt) {
-                ushort4 rc = C.rect[sp];
-                if (band_clip(C, rc)) {
-                    cnt = (uint32_t)(rc.y - rc.x + 1) * (uint32_t)(rc.w - rc.z + 1);
-                    rx = (uint32_t)rc.x | ((uint32_t)rc.y << 16);
-                    rz = (uint32_t)rc.z | ((uint32_t)rc.w << 16);
-                } else {
-                    cnt = 0;
-                }
-            }
-        }
+    constexpr int kPer = kRanksPerWarp / 32;
+#pragma unroll 1
+    for (int u = 0; u < kPer; ++u) {
+        const uint32_t sp = sps[u], cnt = cnts[u], rx = rxs[u], rz = rzs[u];
         uint32_t incl = cnt;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -524,7 +514,7 @@ __device__ __forceinline__ void expand_pairs(const PairCtx &C, int64_t rbase, in
     }
 }
 
-// per-block tile histogram -> hist[tile * nblocks + block], from a 2-D
+// per-block tile histogram -> hist[block * ntiles + tile] (coalesced rows), from a 2-D
 // difference array of the block's tile rectangles (no pair expansion)
 __global__ void __launch_bounds__(kThreads)
 pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
@@ -534,72 +524,120 @@ pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
     for (int i = threadIdx.x; i < w1 * h1; i += kThreads) D[i] = 0;
     __syncthreads();
     const int64_t r0 = (int64_t)blockIdx.x * kRanksPerBlock;
-    for (int k = threadIdx.x; k < kRanksPerBlock; k += kThreads) {
-        const int64_t r = r0 + k;
-        if (r >= C.n) break;
-        const uint32_t sp = C.order[r];
-        if (C.count[sp] > 0) {
-            ushort4 rc = C.rect[sp];
-            if (band_clip(C, rc)) diff_add(D, w1, rc, 1);
-        }
+    // the thread's 8 ranks: rank loads together, then count and rectangle
+    // loads together (K1 writes a rectangle for every splat)
+    constexpr int kPer = kRanksPerBlock / kThreads;
+    uint32_t sps[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int64_t r = r0 + threadIdx.x + (int64_t)kThreads * u;
+        sps[u] = r < C.n ? __ldg(C.order + r) : 0xffffffffu;
     }
+    int cnts[kPer];
+    ushort4 rcs[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const bool ok = sps[u] != 0xffffffffu;
+        cnts[u] = ok ? __ldg(C.count + sps[u]) : 0;
+        rcs[u] = ok ? C.rect[sps[u]] : make_ushort4(0, 0, 0, 0);
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u)
+        if (cnts[u] > 0 && band_clip(C, rcs[u])) diff_add(D, w1, rcs[u], 1);
     __syncthreads();
     prefix2d(D, w1, h1, threadIdx.x, kThreads, [] { __syncthreads(); });
     const int tb = C.ty_lo * C.ntx;  // first tile of the band
     for (int t = threadIdx.x; t < C.ntx * C.bh; t += kThreads)
-        hist[(int64_t)(tb + t) * nblocks + blockIdx.x] = (uint32_t)D[(t / C.ntx) * w1 + t % C.ntx];
+        hist[(int64_t)blockIdx.x * C.ntiles + tb + t] = (uint32_t)D[(t / C.ntx) * w1 + t % C.ntx];
 }
 
-// Per-tile exclusive scan of the per-block pair counts (hist[tile][block],
-// one warp per tile row, 32 coalesced columns per step) -> tile totals; the
-// kernel's last block to finish then writes tile_ranges = exclusive scan of
-// the totals (P = their sum, ranges clamped to the pair capacity so an
-// overflowed frame never makes K3/K4 read past pair_splat), the optional
-// heaviest-first tile schedule for K3/K4 (a 64-bucket counting sort of the
-// tile pair counts; scheduling only), and re-arms the depth min/max words
-// that K1 of the next frame reduces into.
+// Per-tile exclusive scan of the per-block pair counts hist[block][tile]:
+// thread (tile t, chunk c) scans blocks [c * bpc, (c + 1) * bpc) in place
+// (coalesced over tiles) and leaves the chunk total in ctot[c][t]; the
+// kernel's last block to finish scans the chunk totals per tile (ctot becomes
+// the chunk offsets; pair_place adds both), then writes tile_ranges =
+// exclusive scan of the tile totals (P = their sum, ranges clamped to the
+// pair capacity so an overflowed frame never makes K3/K4 read past
+// pair_splat), the optional heaviest-first tile schedule for K3/K4 (a
+// 64-bucket counting sort of the tile pair counts; scheduling only), and
+// re-arms the depth min/max words that K1 of the next frame reduces into.
 constexpr int kOrderBuckets = 64;
 
-__global__ void __launch_bounds__(kThreads)
-tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, uint32_t *totals, uint32_t *done,
-                 int32_t *ranges, uint32_t cap, int32_t *n_pairs, int32_t *order,
-                 unsigned long long *mm) {
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
-    const int r = blockIdx.x * kWarps + warp;
-    if (r < ntiles) {
-        uint32_t *row = hist + (int64_t)r * nblocks;
-        uint32_t carry = 0;
-#pragma unroll 4
-        for (int base = 0; base < nblocks; base += 32) {
-            const int i = base + lane;
-            const uint32_t v = i < nblocks ? row[i] : 0;
-            uint32_t x = v;
+constexpr int kScanThreads = 1024;
+constexpr int kScanChunks = 16;  // tile scan: block chunks per tile
+constexpr int kScanWarps = kScanThreads / 32;
+
+__global__ void __launch_bounds__(kScanThreads)
+tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, int bpc, uint32_t *ctot,
+                 uint32_t *totals, uint32_t *done, int32_t *ranges, uint32_t cap, int32_t *n_pairs,
+                 int32_t *order, unsigned long long *mm) {
+    const int t = blockIdx.x * kScanThreads + threadIdx.x;
+    const int c = blockIdx.y;
+    if (t < ntiles) {
+        const int b0 = c * bpc, b1 = min(b0 + bpc, nblocks);
+        uint32_t run = 0;
+        for (int bb = b0; bb < b1; bb += 8) {  // 8 independent loads, then the scan
+            uint32_t v[8];
 #pragma unroll
-            for (int o = 1; o < 32; o <<= 1) {
-                const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
-                if (lane >= o) x += y;
+            for (int q = 0; q < 8; ++q) v[q] = bb + q < b1 ? hist[(int64_t)(bb + q) * ntiles + t] : 0u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) {
+                if (bb + q < b1) hist[(int64_t)(bb + q) * ntiles + t] = run;
+                run += v[q];
             }
-            if (i < nblocks) row[i] = carry + x - v;
-            carry += __shfl_sync(0xffffffffu, x, 31);
         }
-        if (lane == 0) totals[r] = carry;
+        ctot[(int64_t)c * ntiles + t] = run;
     }
     __shared__ bool s_last;
     __threadfence();
     __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    __shared__ uint32_t s_warp[kWarps];
+    const int nch = gridDim.y;
+    for (int tt = threadIdx.x; tt < ntiles; tt += kScanThreads) {
+        uint32_t v[kScanChunks];
+#pragma unroll
+        for (int cc = 0; cc < kScanChunks; ++cc)
+            v[cc] = cc < nch ? __ldcg(ctot + (int64_t)cc * ntiles + tt) : 0u;
+        uint32_t run = 0;
+#pragma unroll
+        for (int cc = 0; cc < kScanChunks; ++cc) {
+            if (cc < nch) ctot[(int64_t)cc * ntiles + tt] = run;
+            run += v[cc];
+        }
+        totals[tt] = run;
+    }
+    __syncthreads();
+    __shared__ uint32_t s_warp[32];
     uint64_t carry = 0;
-    for (int base = 0; base < ntiles; base += kThreads) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    for (int base = 0; base < ntiles; base += kScanThreads) {
         const int i = base + threadIdx.x;
-        const uint32_t v = i < ntiles ? __ldcg(totals + i) : 0;
-        uint32_t tot;
-        const uint32_t incl = block_incl_scan(v, s_warp, tot);
+        const uint32_t v = i < ntiles ? totals[i] : 0;
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        if (lane == 31) s_warp[warp] = x;
+        __syncthreads();
+        if (warp == 0) {
+            uint32_t w = s_warp[lane];
+#pragma unroll
+            for (int o = 1; o < 32; o <<= 1) {
+                const uint32_t y = __shfl_up_sync(0xffffffffu, w, o);
+                if (lane >= o) w += y;
+            }
+            s_warp[lane] = w;
+        }
+        __syncthreads();
+        const uint32_t incl = x + (warp > 0 ? s_warp[warp - 1] : 0);
         if (i < ntiles) ranges[i] = (int32_t)min(carry + incl - v, (uint64_t)cap);
-        carry += tot;
+        carry += s_warp[31];
+        __syncthreads();
     }
     if (threadIdx.x == 0) {
         ranges[ntiles] = (int32_t)min(carry, (uint64_t)cap);
@@ -619,7 +657,7 @@ tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, uint32_t *totals, uint
         const int b = (int)(2.0f * __log2f((float)cnt + 1.0f));
         return kOrderBuckets - 1 - (b < kOrderBuckets - 1 ? b : kOrderBuckets - 1);
     };
-    for (int t = threadIdx.x; t < ntiles; t += kThreads)
+    for (int t = threadIdx.x; t < ntiles; t += kScanThreads)
         atomicAdd(&s_hist[bucket(ranges[t + 1] - ranges[t])], 1);
     __syncthreads();
     if (threadIdx.x == 0) {
@@ -631,7 +669,7 @@ tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, uint32_t *totals, uint
         }
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < ntiles; t += kThreads)
+    for (int t = threadIdx.x; t < ntiles; t += kScanThreads)
         order[atomicAdd(&s_hist[bucket(ranges[t + 1] - ranges[t])], 1)] = t;
 }
 
@@ -639,8 +677,8 @@ tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, uint32_t *totals, uint
 // Per-warp tile counts come from per-warp 2-D difference arrays; the pairs
 // are expanded once, ranked within the warp by match_any and written.
 __global__ void __launch_bounds__(kThreads)
-pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *ranges,
-                  int32_t *pair_splat, int W, int H) {
+pair_place_kernel(PairCtx C, const uint32_t *hist, const uint32_t *ctot, int bpc,
+                  const int32_t *ranges, int32_t *pair_splat, int W, int H) {
     extern __shared__ int smem_i32[];
     const int w1 = C.ntx + 1, h1 = C.bh + 1, cells = w1 * h1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -651,24 +689,36 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
     const int64_t rb = (int64_t)blockIdx.x * kRanksPerBlock + (int64_t)warp * kRanksPerWarp;
     const int64_t re = rb + kRanksPerWarp < C.n ? rb + kRanksPerWarp : C.n;
     // phase 1: per-warp tile counts (<= 256 per tile per warp); the warp's
-    // 8 rank loads are issued together, then the dependent count / rect loads
+    // 8 rank loads are issued together, then the dependent count / rect
+    // loads; the band-clipped rectangles stay in registers for phase 3
+    constexpr int kPer = kRanksPerWarp / 32;
+    uint32_t sps[kPer], cnts[kPer], rxs[kPer], rzs[kPer];
     {
-        constexpr int kPer = kRanksPerWarp / 32;
-        uint32_t sps[kPer];
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
             const int64_t r = rb + lane + 32 * u;
             sps[u] = r < re ? __ldg(C.order + r) : 0xffffffffu;
         }
-        int cnts[kPer];
-#pragma unroll
-        for (int u = 0; u < kPer; ++u) cnts[u] = sps[u] != 0xffffffffu ? __ldg(C.count + sps[u]) : 0;
+        ushort4 rcs[kPer];
 #pragma unroll
         for (int u = 0; u < kPer; ++u) {
-            if (cnts[u] > 0) {
-                ushort4 rc = C.rect[sps[u]];
-                if (band_clip(C, rc)) diff_add(Dw, w1, rc, 1);
+            const bool ok = sps[u] != 0xffffffffu;
+            cnts[u] = ok ? (uint32_t)__ldg(C.count + sps[u]) : 0u;
+            rcs[u] = ok ? C.rect[sps[u]] : make_ushort4(0, 0, 0, 0);
+        }
+#pragma unroll
+        for (int u = 0; u < kPer; ++u) {
+            ushort4 rc = rcs[u];
+            if (cnts[u] > 0 && band_clip(C, rc)) {
+                diff_add(Dw, w1, rc, 1);
+                cnts[u] = (uint32_t)(rc.y - rc.x + 1) * (uint32_t)(rc.w - rc.z + 1);
+                rxs[u] = (uint32_t)rc.x | ((uint32_t)rc.y << 16);
+                rzs[u] = (uint32_t)rc.z | ((uint32_t)rc.w << 16);
+            } else {
+                cnts[u] = 0u;
+                rxs[u] = rzs[u] = 0u;
             }
+            if (sps[u] == 0xffffffffu) sps[u] = 0u;
         }
     }
     __syncwarp();
@@ -687,11 +737,13 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, int nblocks, const int32_t *r
             smem_i32[w * cells + cell] = run;
             run += c;
         }
-        s_base[cell] = run ? (uint32_t)ranges[t] + hist[(int64_t)t * nblocks + blockIdx.x] : 0u;
+        s_base[cell] = run ? (uint32_t)ranges[t] + hist[(int64_t)blockIdx.x * C.ntiles + t] +
+                                 ctot[(int64_t)(blockIdx.x / bpc) * C.ntiles + t]
+                           : 0u;
     }
     __syncthreads();
     // phase 3: expand once, place (and cull-flag) every pair
-    expand_pairs(C, rb, re, [&](bool ok, uint32_t sp, int tile, int tx, int ty) {
+    expand_pairs(C, sps, cnts, rxs, rzs, [&](bool ok, uint32_t sp, int tile, int tx, int ty) {
         const uint32_t peers = __match_any_sync(0xffffffffu, tile);
         const int cell = (ty - C.ty_lo) * w1 + tx;
         // the first lane of each equal-tile group advances the warp's running
@@ -728,26 +780,34 @@ struct Plan {
     size_t off[16];
     size_t total;
     int nbk, nbp;
-    size_t ctrl_bytes;  // zeroed per frame: digit histograms, counters, flags, look-back words
+    int vbits;          // coarse-key bits: 2^vbits depth buckets (~2 per splat)
+    int64_t nbuckets;   // 2^vbits + 1 (the invisible splats' bucket last)
+    int64_t nscan;      // bucket-scan blocks
+    size_t ctrl_bytes;  // zeroed per frame: counters, flags, bucket counts, look-back words
 };
 
-// control block (offset 8): gdig[4][256] | vctr[4] | done_fix | done_tiles |
-// need_full | pad | status[4][nbk][256]
-constexpr size_t kCtrlHead = 4 * 256 * 4 + 64;
+// control block (offset 8): vctr | done_fix | done_tiles | need_full | pad (64 B)
+// | bucket counts (nbuckets) | scan look-back words (nscan)
+constexpr size_t kCtrlHead = 64;
 
 Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
     Plan L{};
     L.nbk = (int)((n + kChunk - 1) / kChunk);
     L.nbp = (int)((n + kRanksPerBlock - 1) / kRanksPerBlock);
-    L.ctrl_bytes = kCtrlHead + (size_t)4 * L.nbk * kRadix * 4;
+    int lg = 1;
+    while (lg < 29 && (1ll << lg) < n) ++lg;
+    L.vbits = lg + 1;
+    L.nbuckets = (1ll << L.vbits) + 1;
+    L.nscan = (L.nbuckets + kChunk - 1) / kChunk;
+    L.ctrl_bytes = kCtrlHead + 4 * (size_t)L.nbuckets + 4 * (size_t)L.nscan;
     size_t sz[16] = {
-        al(4 * (size_t)n), al(4 * (size_t)n),                    // 0,1 coarse keys A/B
-        al(4 * (size_t)n), al(4 * (size_t)n),                    // 2,3 vals A/B
+        al(4 * (size_t)n), al(4),                                // 0 coarse keys, 1 (unused)
+        al(4 * (size_t)n), al(4 * (size_t)n),                    // 2,3 order / fallback scratch
         al(8 * (size_t)n), al(8 * (size_t)n),                    // 4,5 full keys (fallback) A/B
         al(4),                                                   // 6 (unused)
         al(4),                                                   // 7 (unused)
         al(L.ctrl_bytes),                                        // 8 control block
-        al(4),                                                   // 9 (unused)
+        al(4 * (size_t)kScanChunks * ntiles),                    // 9 tile-scan chunk totals
         al(4 * (size_t)ntiles * (L.nbp + 1)),                    // 10 pair tile hist
         al(4 * (size_t)(ntiles + 1)),                            // 11 tile totals
         al(16),                                                  // 12 minmax (keys supplied directly)
@@ -823,28 +883,22 @@ extern "C" int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key,
         return ivr::check_launch("ivr_bin_sort(empty)");
     }
     char *ws = (char *)workspace;
-    uint32_t *ckA = (uint32_t *)(ws + L.off[0]), *ckB = (uint32_t *)(ws + L.off[1]);
-    uint32_t *vA = (uint32_t *)(ws + L.off[2]), *vB = (uint32_t *)(ws + L.off[3]);
+    uint32_t *ck = (uint32_t *)(ws + L.off[0]);
+    uint32_t *ord = (uint32_t *)(ws + L.off[2]), *vscratch = (uint32_t *)(ws + L.off[3]);
     uint64_t *fkA = (uint64_t *)(ws + L.off[4]), *fkB = (uint64_t *)(ws + L.off[5]);
     char *ctrl = ws + L.off[8];
-    uint32_t *gdig = (uint32_t *)ctrl;
-    uint32_t *vctr = gdig + 4 * 256;
-    uint32_t *done_fix = vctr + 4, *done_tiles = vctr + 5;
-    int32_t *need_full = (int32_t *)(vctr + 6);
-    uint32_t *status = (uint32_t *)(ctrl + kCtrlHead);
+    uint32_t *vctr = (uint32_t *)ctrl;  // bucket-scan done counter
+    uint32_t *done_fix = vctr + 1, *done_tiles = vctr + 2;
+    int32_t *need_full = (int32_t *)(vctr + 3);
+    uint32_t *bcount = (uint32_t *)(ctrl + kCtrlHead);
+    uint32_t *sstatus = bcount + L.nbuckets;  // per scan block: total, then offset
     uint32_t *phist = (uint32_t *)(ws + L.off[10]);
     uint32_t *ttot = (uint32_t *)(ws + L.off[11]);
     const int nbk = L.nbk, nbp = L.nbp;
-    const size_t status_pass = (size_t)nbk * kRadix;
 
-    // ---- 1. depth ranks: coarse keys with ~8 buckets per splat (at least
-    //      log2(n) + 3 bits; 8-bit digits), one onesweep kernel per pass, run fix-up
-    int lg = 1;
-    while (lg < 62 && (1ll << lg) < n) ++lg;
-    int passes = (lg + 4 + 7) / 8;
-    passes = passes < 2 ? 2 : (passes > 4 ? 4 : passes);
-    const int vbits = 8 * passes - 1;
-    cudaMemsetAsync(ctrl, 0, kCtrlHead + (size_t)passes * status_pass * 4, st);
+    // ---- 1. depth ranks: counting sort on a coarse key of log2(n) + 1 bits
+    //      (~2 buckets per splat), then each bucket sorted by (key, index)
+    cudaMemsetAsync(ctrl, 0, L.ctrl_bytes, st);
     unsigned long long *mm = depth_minmax;
     if (!mm) {  // keys supplied directly: reduce their range here
         mm = (unsigned long long *)(ws + L.off[12]);
@@ -853,22 +907,14 @@ extern "C" int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key,
         gb = gb < 1 ? 1 : (gb > 1184 ? 1184 : gb);
         minmax_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm);
     }
-    hist_coarse_kernel<<<nbk, kThreads, 0, st>>>(depth_key, n, mm, vbits, passes, ckA, gdig);
-    uint32_t *kin = ckA, *kout = ckB, *vin = nullptr, *vout = vB;
-    for (int p = 0; p < passes; ++p) {
-        onesweep_kernel<uint32_t><<<nbk, kThreads, 0, st>>>(kin, vin, n, 8 * p, gdig + 256 * p,
-                                                           status + p * status_pass, vctr + p,
-                                                           kout, vout);
-        uint32_t *t = kin;
-        kin = kout;
-        kout = t;
-        vin = vout;
-        vout = (vout == vB) ? vA : vB;
-    }
-    // sorted (key, order) now in (kin, vin); runs fixed, long runs -> full sort
-    uint32_t *ord = vin, *vscratch = (vin == vA) ? vB : vA;
-    fixup_kernel<<<(int)((n + kThreads - 1) / kThreads), kThreads, 0, st>>>(
-        kin, ord, n, depth_key, need_full, done_fix, fkA, fkB, vscratch);
+    bucket_count_kernel<<<nbk, kThreads, 0, st>>>(depth_key, n, mm, L.vbits, ck, bcount);
+    bucket_scan_kernel<<<(int)L.nscan, kThreads, 0, st>>>(bcount, L.nbuckets, sstatus, vctr);
+    bucket_scatter_kernel<<<nbk, kThreads, 0, st>>>(ck, n, bcount, sstatus, ord);
+    const uint32_t nb_vis = (uint32_t)(L.nbuckets - 1);
+    const int64_t fix_threads = (nb_vis + kFixPer - 1) / kFixPer;
+    fixup_buckets_kernel<<<(int)((fix_threads + kFixThreads - 1) / kFixThreads), kFixThreads, 0,
+                           st>>>(bcount, sstatus, nb_vis, ord, n, depth_key, need_full, done_fix,
+                                 fkA, fkB, vscratch);
     // ---- 2. counting placement by tile (+ optional tile cull flag); the
     // tile scan's last block writes the ranges, P = n_pairs and the schedule
     PairCtx C{};
@@ -894,14 +940,17 @@ extern "C" int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key,
         C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
         pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
     }
-    tile_scan_kernel<<<(ntiles + kWarps - 1) / kWarps, kThreads, 0, st>>>(
-        phist, ntiles, nbp, ttot, done_tiles, tile_ranges, (uint32_t)pair_capacity, n_pairs,
-        tile_order, depth_minmax);
+    const int nch = nbp < kScanChunks ? nbp : kScanChunks;
+    const int bpc = (nbp + nch - 1) / nch;
+    uint32_t *ctot = (uint32_t *)(ws + L.off[9]);
+    tile_scan_kernel<<<dim3((ntiles + kScanThreads - 1) / kScanThreads, nch), kScanThreads, 0, st>>>(
+        phist, ntiles, nbp, bpc, ctot, ttot, done_tiles, tile_ranges, (uint32_t)pair_capacity,
+        n_pairs, tile_order, depth_minmax);
     for (int y0 = 0; y0 < nty; y0 += band_rows) {
         C.ty_lo = y0;
         C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
-        pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, nbp, tile_ranges, pair_splat,
-                                                           width, height);
+        pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, ctot, bpc, tile_ranges,
+                                                           pair_splat, width, height);
     }
     return ivr::check_launch("ivr_bin_sort");
 }
