@@ -436,16 +436,19 @@ def bench_inverse(scene, dist=None, world=1, rank=0):
     # the product path: whole iterations replayed as CUDA graphs (InverseGraph:
     # device Adam + table refresh, no host round trip); with N ranks one
     # stream-ordered NCCL all-reduce of the packed gradient per iteration
-    step = InverseGraph(fit, params, 100_000, dist=dist, view_div=float(world)).replay
+    G = InverseGraph(fit, params, 100_000, dist=dist, view_div=float(world))
+    step = G.replay
     note = ("whole iterations replayed as CUDA graphs (InverseGraph: device Adam)" +
             ("; views sharded, one NCCL all-reduce per iteration between the compute "
              "and update graphs" if dist is not None else ""))
     mean_ms, med_ms = _device_time(step, 10)
     mean_ms = _max_over_ranks(mean_ms, dist)
-    split = _split_events(lambda ev: fit.view_grads(params, 0, events=ev), 5)
-    P = int(fit._last_pairs.item())
-    parts = dict(zip(("render(K1, K2, K3 float64 semantics)", "loss(K7)", "K4a blend_bwd",
-                      "K4b preprocess_bwd (transform only)"), [float(x) for x in split]))
+    # the graph's launch sequence run eagerly with events between the kernels
+    split = _split_events(lambda ev: G._views(events=ev), 7)
+    P = int(G._last_pairs.item())
+    parts = dict(zip(("K1 preprocess (float64 semantics)", "K2 bin/sort", "K3 blend_fwd",
+                      "loss(K7)", "K4a blend_bwd", "K4b preprocess_bwd (transform only) + pack"),
+                     [float(x) for x in split]))
     return {"metric": "inverse exploration it/s (composed 1M, 800x800, 1 view per GPU)",
             "value": 1000.0 / mean_ms, "unit": "it/s", "views_per_s": world * 1000.0 / mean_ms,
             "ms_per_it": mean_ms, "ms_per_it_median": med_ms, "n_gpus": world, "pairs": P,
@@ -753,12 +756,11 @@ def run_ours(args):
         t4 = extra.get("inverse_c4", {})
         if "split_ms_eager" in t4:
             sp, P4 = t4["split_ms_eager"], t4["pairs"]
-            row("render K1-K3 (C4, float64 semantics)", sp["render(K1, K2, K3 float64 semantics)"],
-                136 * n + 24 * n + 12 * P4 + 40 * P4 + 16 * WH,
-                "SURVEY 8(d) C4: render 160 N + 52 P + 16 WH (whole render, K1-K3)")
+            row("K3 blend_fwd (C4, float64 semantics)", sp["K3 blend_fwd"], 40 * P4 + 16 * WH,
+                "SURVEY 8(d): 40 B/pair + 16 B/pixel", "blend_fwd_kernel<4, 1, 1>")
             row("K4a blend_bwd (C4, no geometry)", sp["K4a blend_bwd"], 40 * P4 + 16 * WH,
                 "SURVEY 8(d) C4: 40 P + 16 WH read", "blend_bwd_kernel<4, 1, 0>")
-            row("K4b preprocess_bwd (C4, transform only)", sp["K4b preprocess_bwd (transform only)"],
+            row("K4b preprocess_bwd (C4, transform only)", sp["K4b preprocess_bwd (transform only) + pack"],
                 (16 + 100) * n, "SURVEY 8(d) C4: 16 B/Gaussian atomics + 100 B shade-bwd read",
                 "preprocess_bwd_kernel<0>")
         v5 = extra.get("vq_c5", {})

@@ -19,6 +19,12 @@ CSRC = os.path.join(PKG, "csrc")
 LIB = os.path.join(PKG, "libivrgs.so")
 SOURCES = ["abi.cu", "preprocess.cu", "sort.cu", "blend.cu", "backward.cu", "vq.cu", "sh.cu", "ivrg.cu", "ssim.cu", "regularize.cu", "adam.cu", "concat.cu", "display.cu", "dvr.cu", "trainstep.cu", "inverse.cu"]
 ARCH = ["-gencode", "arch=compute_100a,code=sm_100a"]
+# Translation units whose float64 chains must reproduce numpy's rounding op by
+# op (K1 preprocess, K8 SH colour, K10 pseudo normals): no FMA contraction.
+# Everywhere else the reference-exact steps use the explicitly rounded
+# intrinsics of ivr_common.cuh (dmul/dadd/...), so the rest of the code may
+# contract a*b+c into FMAs.
+EXACT_TUS = {"preprocess.cu", "sh.cu", "regularize.cu"}
 
 
 def nvcc():
@@ -46,7 +52,7 @@ def build(verbose=False, force=False):
         return LIB
     objdir = os.path.join(PKG, "_obj")
     os.makedirs(objdir, exist_ok=True)
-    flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-fmad=false", "-Xcompiler", "-fPIC",
+    flags = ARCH + ["-O3", "-lineinfo", "-std=c++17", "-Xcompiler", "-fPIC",
                     "-I" + os.path.join(REPO, "include"), "--expt-relaxed-constexpr"]
     if verbose:
         flags += ["-Xptxas", "-v"]
@@ -55,7 +61,8 @@ def build(verbose=False, force=False):
     for src in sources():
         obj = os.path.join(objdir, os.path.basename(src).replace(".cu", ".o"))
         objs.append(obj)
-        procs.append((src, subprocess.Popen([nvcc(), *flags, "-c", src, "-o", obj],
+        fmad = "-fmad=false" if os.path.basename(src) in EXACT_TUS else "-fmad=true"
+        procs.append((src, subprocess.Popen([nvcc(), *flags, fmad, "-c", src, "-o", obj],
                                             stdout=subprocess.PIPE, stderr=subprocess.STDOUT)))
     failed = False
     for src, p in procs:

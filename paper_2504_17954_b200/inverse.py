@@ -291,20 +291,30 @@ class InverseGraph:
         self.capacity = max(int(peak * headroom) + 4096, 1 << 16)
         self._capture()
 
-    def _views(self):
-        """Every view: render, loss, backward, pack into self.acc."""
+    def _views(self, events=None):
+        """Every view: render, loss, backward, pack into self.acc.  ``events``
+        (eager diagnostics, outside capture): 7 CUDA events recorded around
+        K1, K2, K3, K7, K4a, K4b + pack of the first view."""
         L, fit, ds = self.L, self.fit, self.fit.ds
         ws = self.ws  # owned: eager renders on ds.ws cannot move captured buffers
         for v, cam in enumerate(fit.cams):
+            rec = (lambda j: events[j].record()) if events and v == 0 else (lambda j: None)
             pdev = self.params_dev[v * self.nb:(v + 1) * self.nb]
+            rec(0)
             F = D.preprocess(ds.dg, cam, 4, (0, 3, -1, -1), ws, self.shading, self.edits, None, (),
                              True, params_dev=pdev)
+            rec(1)
             D.bin_sort(F, ws, capacity=self.capacity)
+            rec(2)
             D.blend(F, ws, want_state=True, exact=fit.exact)
+            rec(3)
             h, w, nc = F.out64.shape
             win = 11
             sums, d = _photometric_dev(F.out64, fit.refs[v], 0.8 / F.out64.numel(), -0.2, True)
+            rec(4)
             g = D.blend_backward(F, d, geometry=False)
+            rec(5)
+            self._last_pairs = F.n_pairs
             out, _ = D.preprocess_backward(ds.dg, cam, 4, (0, 3, -1, -1), g=g, shading=self.shading,
                                            edits=self.edits, params_dev=pdev, geometry=False,
                                            want=("d_c_p", "d_scale", "d_globals"), per_scene=self.S,
@@ -314,6 +324,7 @@ class InverseGraph:
                 float((h - win + 1) * (w - win + 1) * nc), out["d_c_p"].data_ptr(),
                 out["d_scale"].data_ptr(), out["d_globals"].data_ptr(), F.n_pairs.data_ptr(),
                 self.capacity, D.stream_handle()), "ivr_inverse_pack")
+            rec(6)
 
     def _update(self):
         L = self.L

@@ -72,6 +72,9 @@ def _photometric_dev(x, y, a, b, with_ssim):
     d = a * sign(x - y) + b * d(mean SSIM)/dx)."""
     from . import _lib as L
     from . import device as D
+    if x.dtype != torch.float64 or y.dtype != torch.float64 or x.dim() != 3 or x.shape != y.shape:
+        raise ShapeMismatch(f"prediction / ground truth must be float64 (H, W, C) tensors of one "
+                            f"shape, got {x.dtype} {tuple(x.shape)} and {y.dtype} {tuple(y.shape)}")
     x, y = x.contiguous(), y.contiguous()
     h, w, nc = x.shape
     nbytes = L.lib().ivr_photometric_workspace_size(h, w, nc)
@@ -97,9 +100,14 @@ def _photometric_frame_dev(frame, cols, y, a, b, with_ssim):
     import ctypes
     from . import _lib as L
     from . import device as D
+    if frame.dtype != torch.float32 or frame.dim() != 3:
+        raise ShapeMismatch(f"frame must be a float32 (H, W, k) tensor, got {frame.dtype} "
+                            f"{tuple(frame.shape)}")
     frame, y = frame.contiguous(), y.contiguous()
     h, w, k = frame.shape
     nc = len(cols)
+    if any(not 0 <= int(c) < k for c in cols):
+        raise ShapeMismatch(f"columns {list(cols)} outside the frame's {k} channels")
     if tuple(y.shape) != (h, w, nc):
         raise ShapeMismatch(f"prediction {(h, w, nc)} vs ground truth {tuple(y.shape)}")
     nbytes = L.lib().ivr_photometric_workspace_size(h, w, nc)
