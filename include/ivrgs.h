@@ -234,6 +234,8 @@ int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key, unsigned long long 
 #define IVR_BLEND_PRECULLED 2 /* flags: pair_splat carries ivr_bin_sort_cull's bit 31 */
 #define IVR_BLEND_NO_GEOMETRY 4 /* ivr_blend_bwd flags: only g_values / g_opacity (transform
                                  * fits); g_mean2d / g_conic may be NULL */
+#define IVR_BLEND_DOUT_F64 8 /* ivr_blend_bwd* flags: d_out points to (H,W,k) float64 (the
+                              * photometric gradient as ivr_photometric_loss writes it) */
 int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_splat,
                   int32_t ntx, int32_t nty, const float *rec, const float *values,
                   const double *rec64, const double *values64, int32_t k,
@@ -515,6 +517,14 @@ typedef struct ivr_step_grads {
     double *stat;
     double w_opacity_l1;
     double *o_partial;
+    /* captured training steps (nullable): the sticky overflow gate
+     * (*gate |= *n_pairs > pair_capacity, read by ivr_adam_step_sched's skip)
+     * and the densify statistic accumulated while the step is not gated
+     * (stat_sum += stat) */
+    int32_t *gate;
+    const int32_t *n_pairs;
+    int64_t pair_capacity;
+    double *stat_sum;
 } ivr_step_grads;
 int32_t ivr_step_partials(int64_t n);
 int ivr_step_assemble(const ivr_step_grads *a, ivr_stream_t stream);

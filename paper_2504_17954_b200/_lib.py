@@ -22,6 +22,7 @@ BLEND_EXACT = 1
 PRE_F64, PRE_EXACT_RGB = 1, 2  # ivr_preprocess_fwd mode bits
 BLEND_PRECULLED = 2
 BLEND_NO_GEOMETRY = 4
+BLEND_DOUT_F64 = 8
 
 IVR_OK, IVR_ERR_ARG, IVR_ERR_SHAPE, IVR_ERR_NONFINITE, IVR_ERR_CORRUPT_INDEX, IVR_ERR_CUDA, \
     IVR_ERR_CAPACITY = 0, -1, -2, -3, -4, -5, -6
@@ -99,7 +100,8 @@ class StepGrads_t(ctypes.Structure):
                 ("k_s_raw", P), ("log_beta", P), ("d_o_logit", P), ("d_delta_c", P),
                 ("d_k_a_raw", P), ("d_k_d_raw", P), ("d_k_s_raw", P), ("d_log_beta", P),
                 ("d_mean2d", P), ("d_n_raw", P), ("stat", P), ("w_opacity_l1", ctypes.c_double),
-                ("o_partial", P)]
+                ("o_partial", P), ("gate", P), ("n_pairs", P), ("pair_capacity", ctypes.c_int64),
+                ("stat_sum", P)]
 
 
 class LossTerms_t(ctypes.Structure):

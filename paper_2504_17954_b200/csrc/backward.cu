@@ -40,6 +40,7 @@ struct BwdArgs {
     const double *t_final;
     const int32_t *last_pos;
     const float *d_out;
+    const double *d_out64;  // IVR_BLEND_DOUT_F64: the upstream gradient in float64 instead
     float *g_values, *g_mean, *g_conic, *g_opac;
     int preculled;
     const int32_t *tile_order;
@@ -154,7 +155,8 @@ blend_bwd_kernel(BwdArgs A) {
     float S = 0.0f;
 #pragma unroll
     for (int c = 0; c < KMAX; ++c) {
-        dout[c] = (inside && c < K) ? A.d_out[pix * K + c] : 0.0f;
+        dout[c] = (inside && c < K) ? (A.d_out64 ? (float)A.d_out64[pix * K + c] : A.d_out[pix * K + c])
+                                    : 0.0f;
         W.dout[lane * KMAX + c] = dout[c];
     }
     int nbat = 0;  // pairs in the deferred value batch (warp-uniform)
@@ -845,7 +847,9 @@ int blend_bwd_impl(const int32_t *tile_ranges, const int32_t *pair_splat, int32_
     A.H = height;
     A.t_final = t_final;
     A.last_pos = last_pos;
-    A.d_out = d_out;
+    const bool dout64 = (flags & IVR_BLEND_DOUT_F64) != 0;
+    A.d_out = dout64 ? nullptr : d_out;
+    A.d_out64 = dout64 ? reinterpret_cast<const double *>(d_out) : nullptr;
     A.g_values = g_values;
     A.g_mean = g_mean2d;
     A.g_conic = g_conic;

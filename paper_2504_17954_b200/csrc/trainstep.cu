@@ -48,6 +48,13 @@ __global__ void __launch_bounds__(kThreads) assemble_kernel(ivr_step_grads A) {
     double osum = 0.0;
     const int K = A.k;
     const double dn = (double)A.n;
+    // captured steps: sticky overflow gate (0 -> 1 only, so blocks reading the
+    // word before or after block 0 updates it compute the same value)
+    bool gated = false;
+    if (A.gate) {
+        gated = *A.gate != 0 || (int64_t)*A.n_pairs > A.pair_capacity;
+        if (blockIdx.x == 0 && threadIdx.x == 0) *A.gate = gated ? 1 : 0;
+    }
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < A.n;
          i += (int64_t)gridDim.x * kThreads) {
         const double *dv = A.d_values ? A.d_values + (int64_t)K * i : nullptr;
@@ -75,8 +82,10 @@ __global__ void __launch_bounds__(kThreads) assemble_kernel(ivr_step_grads A) {
         }
         if (A.stat) {
             const double *m = A.d_mean2d + 2 * i, *r = A.d_n_raw + 3 * i;
-            A.stat[i] = dadd(sqrt(dadd(dmul(m[0], m[0]), dmul(m[1], m[1]))),
-                             norm3(r[0], r[1], r[2]));
+            const double st = dadd(sqrt(dadd(dmul(m[0], m[0]), dmul(m[1], m[1]))),
+                                   norm3(r[0], r[1], r[2]));
+            A.stat[i] = st;
+            if (A.stat_sum && !gated) A.stat_sum[i] = dadd(A.stat_sum[i], st);
         }
     }
     if (!A.o_partial) return;

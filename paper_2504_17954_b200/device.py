@@ -346,7 +346,9 @@ def blend_backward(F: Frame, d_out, stream=None, deterministic=None, geometry=Tr
          "conic": arena[n * (K + 2):n * (K + 5)], "opacity": arena[n * (K + 5):]}
     if F.t_final is None:
         raise ValueError("blend_backward needs the forward state (render with want_state=True)")
-    d_out = d_out.to(torch.float32).contiguous()
+    # float64 upstream gradients (the photometric loss's) are read in place
+    dflag = L.BLEND_DOUT_F64 if d_out.dtype == torch.float64 else 0
+    d_out = d_out.contiguous() if dflag else d_out.to(torch.float32).contiguous()
     cam = F.cam
     if deterministic:
         nb = int(L.lib().ivr_blend_bwd_det_workspace_size(F.capacity, K))
@@ -358,7 +360,7 @@ def blend_backward(F: Frame, d_out, stream=None, deterministic=None, geometry=Tr
             ptr(g["values"]), ptr(g["mean2d"]), ptr(g["conic"]), ptr(g["opacity"]),
             ptr(getattr(F, "tile_order", None)),
             (L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0) |
-            (0 if geometry else L.BLEND_NO_GEOMETRY),
+            (0 if geometry else L.BLEND_NO_GEOMETRY) | dflag,
             stream_handle(stream)), "ivr_blend_bwd_deterministic")
         return g
     L.check(L.lib().ivr_blend_bwd(ptr(F.tile_ranges), ptr(F.pair_splat), F.ntx, F.nty, ptr(F.rec),
@@ -368,7 +370,7 @@ def blend_backward(F: Frame, d_out, stream=None, deterministic=None, geometry=Tr
                                   ptr(g["conic"]), ptr(g["opacity"]),
                                   ptr(getattr(F, "tile_order", None)),
                                   (L.BLEND_PRECULLED if getattr(F, "preculled", False) else 0) |
-                                  (0 if geometry else L.BLEND_NO_GEOMETRY),
+                                  (0 if geometry else L.BLEND_NO_GEOMETRY) | dflag,
                                   stream_handle(stream)), "ivr_blend_bwd")
     return g
 
@@ -392,7 +394,19 @@ def preprocess_backward(dg: DeviceGaussians, cam, K, cols, g=None, shading=None,
         R.g_conic, R.g_opacity = g["conic"].data_ptr(), g["opacity"].data_ptr()
     if d_rgb is not None:
         R.d_rgb_extra = d_rgb.data_ptr()
-    # every output is a slice of one zeroed float64 arena (one memset)
+    # outputs K4b stores for every Gaussian in this configuration share one
+    # uninitialised arena; the atomically reduced ones (per-scene d_c_p,
+    # d_scale, d_globals) and any the kernel would not reach live in a small
+    # zeroed arena
+    stored = {"d_colors", "d_mean2d", "d_o_logit", "d_mu", "d_n_raw"}
+    if g is not None:
+        stored.add("d_values")
+    if geometry:
+        stored.update(("d_q_raw", "d_log_s"))
+    if shading is not None:
+        stored.update(("d_delta_c", "d_k_a_raw", "d_k_d_raw", "d_k_s_raw", "d_log_beta"))
+        if per_splat_c_p:
+            stored.add("d_c_p")
     sizes = [(name, n * GRAD_SHAPES[name]) for name in want if name in GRAD_SHAPES]
     if "d_values" in want:
         sizes.append(("d_values", n * K))
@@ -402,12 +416,16 @@ def preprocess_backward(dg: DeviceGaussians, cam, K, cols, g=None, shading=None,
         sizes.append(("d_scale", max(per_scene, 1)))
     if shading is not None and "d_globals" in want:
         sizes.append(("d_globals", 10))
-    arena = torch.zeros(sum(sz for _, sz in sizes), dtype=torch.float64, device=dev)
-    o = 0
-    for name, sz in sizes:
-        out[name] = arena[o:o + sz]
-        setattr(R, name, out[name].data_ptr())
-        o += sz
+    for part, alloc in (([x for x in sizes if x[0] in stored], torch.empty),
+                        ([x for x in sizes if x[0] not in stored], torch.zeros)):
+        if not part:
+            continue
+        arena = alloc(sum(sz for _, sz in part), dtype=torch.float64, device=dev)
+        o = 0
+        for name, sz in part:
+            out[name] = arena[o:o + sz]
+            setattr(R, name, out[name].data_ptr())
+            o += sz
     R.per_scene = 0 if per_splat_c_p else int(per_scene)
     if light is not None and light.mode == "orbital":
         dp, da = light_direction_derivatives(light.polar, light.azimuth)

@@ -360,11 +360,16 @@ class _StageTrainer:
         lt.w_normal, lt.w_offset, lt.w_bil = wn, wo, wb
         return lt, (sums, terms), d_out, c
 
-    def _assemble(self, gr, c=None, weights=None, shading=False):
+    def _assemble(self, gr, c=None, weights=None, shading=False, graph=None):
         """ivr_step_assemble (value-channel chain rule, opacity L1, densify
-        statistic) in place on K4b's outputs; returns (stat, o partials)."""
+        statistic) in place on K4b's outputs; returns (stat, o partials).
+        ``graph`` (a StepGraph being captured): the kernel also updates the
+        sticky overflow gate and adds the statistic into graph.stat_sum."""
         n, p = self.n, self.p
         A = L.StepGrads_t()
+        if graph is not None:
+            A.gate, A.n_pairs = graph.gate.data_ptr(), graph.n_pairs.data_ptr()
+            A.pair_capacity, A.stat_sum = int(graph.capacity), graph.stat_sum.data_ptr()
         A.n, A.k = n, self.K
         A.col_delta_c = A.col_k_a = A.col_k_d = A.col_k_s = A.col_beta = -1
         stat = torch.empty(n, dtype=torch.float64, device=self.dev)
@@ -531,7 +536,7 @@ class EditableTrainer(_StageTrainer):
         if graph is not None:
             graph.n_pairs = F.n_pairs
         n = self.n
-        stat, part = self._assemble(gr, c, weights, shading=True)
+        stat, part = self._assemble(gr, c, weights, shading=True, graph=graph)
         loss = self._finalize(lt, part, weights.opacity_l1)
         rec(5)
         self._last_pairs = F.n_pairs
@@ -743,10 +748,10 @@ class StepGraph:
         tr = self.tr
         if not capturing:
             self._snapshot()
+        # the step's assembly kernel also raises the sticky gate (this step's
+        # pair list overflowed, or an earlier one did) and adds the densify
+        # statistic of ungated steps into stat_sum
         loss, grads, stat = tr.step(self._cam0, self.gt_dev, self.weights, graph=self)
-        # sticky gate: this step's pair list overflowed (or an earlier one did)
-        torch.maximum(self.gate, (self.n_pairs[:1] > self.capacity).to(torch.int32),
-                      out=self.gate)
         items = [(n, tr.p[n], grads[n]) for n in self.names]
         self._groups = tr.adam.groups(items)
         self._keep = grads
@@ -754,7 +759,6 @@ class StepGraph:
                                             tr.adam.eps, self.sched_dev.data_ptr(),
                                             self.gate.data_ptr(), D.stream_handle()),
                 "ivr_adam_step_sched")
-        self.stat_sum.add_(stat * (1 - self.gate).to(torch.float64))
         self.loss = loss
 
     # -- running ---------------------------------------------------------------
