@@ -30,39 +30,52 @@ FLAT_GRADIENT = 1e-6
 MANIFEST_VERSION = 1
 
 
+def _as_volume_array(values, spacing):
+    """Validated float64 C-contiguous samples and a positive 3-vector spacing."""
+    vals = np.ascontiguousarray(values, dtype=np.float64)
+    if vals.ndim != 3 or min(vals.shape) < 2:
+        raise ShapeMismatch(f"volume must be 3-d with dims >= 2, got {vals.shape}")
+    if not np.isfinite(vals).all():
+        raise OutOfRange("volume contains non-finite values")
+    sp = np.asarray(spacing, dtype=np.float64).reshape(3)
+    if (sp <= 0).any():
+        raise OutOfRange("voxel spacing must be positive")
+    return vals, sp
+
+
 @dataclass
 class VolumeGrid:
-    """Scalar field on a regular grid centred on the origin (dvr.py:30-66)."""
+    """Regular-grid scalar field whose samples are centred on the origin
+    (same fields and conventions as dvr.py:30-66: sample (i, j, k) sits at
+    origin + (i, j, k) * spacing with origin = -(dims - 1) * spacing / 2)."""
 
     values: np.ndarray
     spacing: np.ndarray = field(default_factory=lambda: np.ones(3))
     kind: str = "custom"
 
     def __post_init__(self):
-        self.values = np.ascontiguousarray(self.values, dtype=np.float64)
-        if self.values.ndim != 3 or min(self.values.shape) < 2:
-            raise ShapeMismatch(f"volume must be 3-d with dims >= 2, got {self.values.shape}")
-        if not np.all(np.isfinite(self.values)):
-            raise OutOfRange("volume contains non-finite values")
-        self.spacing = np.asarray(self.spacing, dtype=np.float64).reshape(3)
-        if np.any(self.spacing <= 0):
-            raise OutOfRange("voxel spacing must be positive")
+        self.values, self.spacing = _as_volume_array(self.values, self.spacing)
 
     @property
     def dims(self):
         return self.values.shape
 
     @property
+    def extent(self):
+        """Edge lengths of the sampled box."""
+        return (np.asarray(self.dims, dtype=np.float64) - 1.0) * self.spacing
+
+    @property
     def origin(self):
-        return -(np.array(self.dims) - 1) * self.spacing / 2.0
+        return -0.5 * self.extent
 
     @property
     def bbox(self):
-        lo = self.origin
-        return lo, lo + (np.array(self.dims) - 1) * self.spacing
+        return -0.5 * self.extent, 0.5 * self.extent
 
     def descriptor(self):
-        return {"kind": self.kind, "dims": list(self.dims), "spacing": self.spacing.tolist()}
+        return dict(kind=self.kind, dims=[int(d) for d in self.dims],
+                    spacing=[float(x) for x in self.spacing])
 
 
 def _grid_coords(dims):
@@ -102,46 +115,55 @@ def make_volume(kind, dims=(64, 64, 64)):
 
 @dataclass
 class TransferFunction1D:
-    """Piecewise-linear scalar -> (rgb, opacity) map (dvr.py:111-170)."""
+    """Scalar -> (rgb, opacity) through linear interpolation between sorted
+    control points, clamped outside them (dvr.py:111-170)."""
 
     values: np.ndarray
     colors: np.ndarray
     opacities: np.ndarray
 
     def __post_init__(self):
-        self.values = np.asarray(self.values, dtype=np.float64).reshape(-1)
-        self.colors = np.asarray(self.colors, dtype=np.float64).reshape(-1, 3)
-        self.opacities = np.asarray(self.opacities, dtype=np.float64).reshape(-1)
-        n = self.values.size
-        if n < 2 or self.colors.shape[0] != n or self.opacities.size != n:
+        x = np.asarray(self.values, dtype=np.float64).ravel()
+        rgb = np.asarray(self.colors, dtype=np.float64).reshape(-1, 3)
+        a = np.asarray(self.opacities, dtype=np.float64).ravel()
+        if x.size < 2 or len(rgb) != x.size or a.size != x.size:
             raise ShapeMismatch("transfer function needs >= 2 aligned control points")
-        if np.any(np.diff(self.values) < 0):
+        if (x[1:] < x[:-1]).any():
             raise OutOfRange("transfer function control values must be sorted")
-        if np.any((self.opacities < 0) | (self.opacities > 1)):
+        if ((a < 0.0) | (a > 1.0)).any():
             raise OutOfRange("transfer function opacities must lie in [0, 1]")
+        self.values, self.colors, self.opacities = x, rgb, a
 
     @classmethod
     def basic_bump(cls, v_lo, v_hi, color, max_opacity):
+        """Triangle of opacity peaking at the midpoint, one colour throughout."""
         if not v_lo < v_hi:
             raise OutOfRange("bump needs v_lo < v_hi")
-        mid = 0.5 * (v_lo + v_hi)
-        color = np.asarray(color, dtype=np.float64)
-        return cls([v_lo, mid, v_hi], [color, color, color], [0.0, float(max_opacity), 0.0])
+        rgb = np.tile(np.asarray(color, dtype=np.float64), (3, 1))
+        return cls(np.array([v_lo, 0.5 * (v_lo + v_hi), v_hi]), rgb,
+                   np.array([0.0, float(max_opacity), 0.0]))
 
     def support(self):
-        nz = np.flatnonzero(self.opacities > 0)
-        if nz.size == 0:
+        """Interval outside which the opacity is zero (None if never opaque):
+        the control points adjacent to the first and last opaque ones."""
+        opaque = np.nonzero(self.opacities > 0.0)[0]
+        if len(opaque) == 0:
             return None
-        return (self.values[max(nz[0] - 1, 0)], self.values[min(nz[-1] + 1, self.values.size - 1)])
+        last = len(self.values) - 1
+        return (self.values[max(int(opaque[0]) - 1, 0)],
+                self.values[min(int(opaque[-1]) + 1, last)])
 
     def lookup(self, v):
-        v = np.clip(np.asarray(v, dtype=np.float64), self.values[0], self.values[-1])
-        rgb = np.stack([np.interp(v, self.values, self.colors[:, c]) for c in range(3)], axis=-1)
-        return rgb, np.interp(v, self.values, self.opacities)
+        """(rgb, opacity) at value(s) v."""
+        x = self.values
+        v = np.clip(np.asarray(v, dtype=np.float64), x[0], x[-1])
+        table = np.column_stack([self.colors, self.opacities])
+        cols = [np.interp(v, x, table[:, c]) for c in range(4)]
+        return np.stack(cols[:3], axis=-1), cols[3]
 
     def to_dict(self):
-        return {"values": self.values.tolist(), "colors": self.colors.tolist(),
-                "opacities": self.opacities.tolist()}
+        return dict(values=self.values.tolist(), colors=self.colors.tolist(),
+                    opacities=self.opacities.tolist())
 
     @classmethod
     def from_dict(cls, d):
@@ -149,18 +171,20 @@ class TransferFunction1D:
 
 
 def transfer_functions_disjoint(tfs):
-    supports = sorted(s for s in (tf.support() for tf in tfs) if s is not None)
-    return all(a[1] <= b[0] for a, b in zip(supports, supports[1:]))
+    """No two opacity supports overlap (touching endpoints are allowed)."""
+    spans = sorted(sp for sp in map(TransferFunction1D.support, tfs) if sp is not None)
+    return all(prev[1] <= nxt[0] for prev, nxt in zip(spans, spans[1:]))
 
 
 def union_transfer_functions(tfs):
+    """One transfer function holding every control point of disjoint ones,
+    ordered by their first control value (stable)."""
     if not transfer_functions_disjoint(tfs):
         raise OutOfRange("transfer function supports overlap; union is undefined")
-    order = np.argsort([tf.values[0] for tf in tfs], kind="stable")
-    parts = [tfs[i] for i in order]
-    return TransferFunction1D(np.concatenate([p.values for p in parts]),
-                              np.concatenate([p.colors for p in parts], axis=0),
-                              np.concatenate([p.opacities for p in parts]))
+    ordered = sorted(tfs, key=lambda tf: tf.values[0])
+    return TransferFunction1D(np.hstack([tf.values for tf in ordered]),
+                              np.vstack([tf.colors for tf in ordered]),
+                              np.hstack([tf.opacities for tf in ordered]))
 
 
 @dataclass
@@ -228,44 +252,51 @@ def raymarch_pixel(volume, tf, cam, light, pixel, material=None, step_scale=0.5)
 VolumeDataset = ViewDataset  # cameras, images, light, manifest, bbox() (dvr.py:459-482)
 
 
+def _manifest(volume, tf, light, material, entries):
+    """manifest.json contents (the reference's dataset layout, dvr.py:485-520)."""
+    return {
+        "version": MANIFEST_VERSION,
+        "volume": volume.descriptor(),
+        "transfer_function": tf.to_dict(),
+        "light": dict(mode=light.mode, polar=light.polar, azimuth=light.azimuth),
+        "material": dict(k_a=material.k_a, k_d=material.k_d, k_s=material.k_s, beta=material.beta),
+        "cameras": entries,
+    }
+
+
 def generate_dataset(volume, tf, cameras, light, out_dir, material=None, step_scale=0.5):
-    """Render every camera on the GPU and write PNGs plus manifest.json
-    (dvr.py:485-520)."""
+    """Render every camera on the GPU, write view_NNNN.png (RGBA, rounded to
+    8 bits) and manifest.json, and return the dataset (dvr.py:485-520)."""
     from PIL import Image
     material = material or Material()
+    tf = union_transfer_functions(list(tf)) if isinstance(tf, (list, tuple)) else tf
     os.makedirs(out_dir, exist_ok=True)
-    if isinstance(tf, (list, tuple)):
-        tf = union_transfer_functions(list(tf))
     vals = D.to_dev(volume.values)
     images, entries = [], []
-    for i, cam in enumerate(cameras):
+    for idx, cam in enumerate(cameras):
         rgba = render_view_device(volume, tf, cam, light, material, step_scale, vals)
-        img8 = torch.clamp(torch.round(rgba * 255.0), 0, 255).to(torch.uint8).cpu().numpy()
-        fname = f"view_{i:04d}.png"
-        Image.fromarray(img8, mode="RGBA").save(os.path.join(out_dir, fname))
-        images.append(img8.astype(np.float64) / 255.0)
-        entry = cam.to_dict()
-        entry["file"] = fname
-        entries.append(entry)
-    manifest = {"version": MANIFEST_VERSION, "volume": volume.descriptor(),
-                "transfer_function": tf.to_dict(),
-                "light": {"mode": light.mode, "polar": light.polar, "azimuth": light.azimuth},
-                "material": {"k_a": material.k_a, "k_d": material.k_d, "k_s": material.k_s,
-                             "beta": material.beta},
-                "cameras": entries}
-    with open(os.path.join(out_dir, "manifest.json"), "w") as f:
-        json.dump(manifest, f, indent=2, sort_keys=True)
+        u8 = (rgba * 255.0).round_().clamp_(0, 255).to(torch.uint8).cpu().numpy()
+        name = "view_%04d.png" % idx
+        Image.fromarray(u8, mode="RGBA").save(os.path.join(out_dir, name))
+        images.append(u8 / 255.0)
+        entries.append(dict(cam.to_dict(), file=name))
+    manifest = _manifest(volume, tf, light, material, entries)
+    with open(os.path.join(out_dir, "manifest.json"), "w") as fh:
+        json.dump(manifest, fh, indent=2, sort_keys=True)
     return VolumeDataset(list(cameras), images, light.copy(), manifest)
 
 
 def load_dataset(dataset_dir):
-    """Load a dataset directory written by generate_dataset (dvr.py:523-533)."""
+    """Read a directory written by generate_dataset (dvr.py:523-533)."""
     from PIL import Image
-    with open(os.path.join(dataset_dir, "manifest.json")) as f:
-        manifest = json.load(f)
-    cameras = [Camera.from_dict(e) for e in manifest["cameras"]]
-    images = [np.asarray(Image.open(os.path.join(dataset_dir, e["file"]))).astype(np.float64) / 255.0
-              for e in manifest["cameras"]]
-    light = LightConfig(mode=manifest["light"]["mode"], polar=manifest["light"]["polar"],
-                        azimuth=manifest["light"]["azimuth"])
-    return VolumeDataset(cameras, images, light, manifest)
+    with open(os.path.join(dataset_dir, "manifest.json")) as fh:
+        manifest = json.load(fh)
+    views = manifest["cameras"]
+    cameras = [Camera.from_dict(v) for v in views]
+    images = []
+    for v in views:
+        with Image.open(os.path.join(dataset_dir, v["file"])) as im:
+            images.append(np.asarray(im, dtype=np.float64) / 255.0)
+    lt = manifest["light"]
+    return VolumeDataset(cameras, images, LightConfig(mode=lt["mode"], polar=lt["polar"],
+                                                      azimuth=lt["azimuth"]), manifest)
