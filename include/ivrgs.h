@@ -368,6 +368,17 @@ int ivr_kmeans_lloyd_step(const double *values, int64_t n, const double *centroi
                           double *new_centroids, double *shift, void *workspace,
                           size_t workspace_bytes, ivr_stream_t stream);
 
+/* k-means++ seeding, vq._seed_plusplus (vq.py:60-72): centers[0] =
+ * values[first] (the reference's rng.integers draw), then for i = 1..k-1 the
+ * first index whose cumulative d2 (index order) exceeds u[i-1] * sum(d2)
+ * (rng.choice(n, p = d2 / sum d2) with the draws u = rng.random(k-1); all
+ * mass on chosen centres repeats centers[0]).  Two kernels per centre, d2
+ * and the block sums in the workspace (ivr_kmeans_seed_workspace_size). */
+size_t ivr_kmeans_seed_workspace_size(int64_t n);
+int ivr_kmeans_seed(const double *values, int64_t n, int32_t k, int64_t first, const double *u,
+                    double *centers, void *workspace, size_t workspace_bytes,
+                    ivr_stream_t stream);
+
 /* Compose on the device (scene.py:147-186, gaussians.py:98-106): concatenate
  * n_src (<= 64) row-major float64 arrays of `width` columns (rows[m] rows
  * each) into dst; scene_id (may be NULL) receives the source index per row. */

@@ -153,6 +153,9 @@ _SIGS = {
                       ctypes.c_int),
     "ivr_tile_order": ([P, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_debug_blend_trace": ([P], None),
+    "ivr_kmeans_seed_workspace_size": ([ctypes.c_int64], ctypes.c_size_t),
+    "ivr_kmeans_seed": ([P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, P, P, P,
+                         ctypes.c_size_t, P], ctypes.c_int),
     "ivr_blend_bwd_det_workspace_size": ([ctypes.c_int64, ctypes.c_int32], ctypes.c_size_t),
     "ivr_blend_bwd_deterministic": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
                                      ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int64, P, P,

@@ -280,6 +280,154 @@ lloyd_finish_kernel(const double *cents, int k, const double *sums, const unsign
     }
 }
 
+// ----------------------------------------------------------------- k-means++
+// vq._seed_plusplus (vq.py:60-72) with the reference's random stream: every
+// step draws one uniform u (rng.choice(n, p = d2 / sum d2) == the first index
+// whose cumulative d2 in INDEX order exceeds u * sum).  Per step two kernels:
+// (A) d2 = min(d2, (x - c)^2) for the centre just chosen (d2 = (x - c0)^2 at
+// the first step) with per-block partial sums in index order, (B) one block
+// scans the block sums, finds the block holding u * sum and the index inside
+// it, and writes the next centre.
+constexpr int kSeedThreads = 256, kSeedItems = 8, kSeedChunk = kSeedThreads * kSeedItems;
+constexpr int kPickThreads = 1024;
+
+__global__ void __launch_bounds__(kSeedThreads)
+seed_update_kernel(const double *x, int64_t n, double *d2, const double *center, int init,
+                   double *bsum) {
+    __shared__ double s_red[kSeedThreads / 32];
+    const double c = *center;
+    const int64_t base = (int64_t)blockIdx.x * kSeedChunk;
+    double sum = 0.0;
+#pragma unroll
+    for (int r = 0; r < kSeedItems; ++r) {
+        const int64_t i = base + r * kSeedThreads + threadIdx.x;
+        if (i < n) {
+            const double d = x[i] - c;
+            const double v = init ? d * d : fmin(d2[i], d * d);
+            d2[i] = v;
+            sum += v;
+        }
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) sum += __shfl_xor_sync(0xffffffffu, sum, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = sum;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double t = 0.0;
+        for (int w = 0; w < kSeedThreads / 32; ++w) t += s_red[w];
+        bsum[blockIdx.x] = t;
+    }
+}
+
+// inclusive scan of one double per thread over the block (1024 threads)
+__device__ __forceinline__ double block_scan_d(double v, double *s_w, double &total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) s_w[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double w = s_w[lane];
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        s_w[lane] = w;
+    }
+    __syncthreads();
+    if (warp > 0) v += s_w[warp - 1];
+    total = s_w[31];
+    __syncthreads();
+    return v;
+}
+
+__global__ void __launch_bounds__(kPickThreads)
+seed_pick_kernel(const double *x, int64_t n, const double *d2, const double *bsum, int nb,
+                 const double *u, double *centers, int step) {
+    __shared__ double s_w[32];
+    __shared__ int s_blk, s_lastmass;
+    __shared__ unsigned long long s_idx;
+    const int tid = threadIdx.x;
+    if (tid == 0) {
+        s_blk = 0x7fffffff;
+        s_lastmass = -1;
+        s_idx = ~0ull;
+    }
+    // block sums: thread t owns the contiguous blocks [t * per, (t + 1) * per)
+    const int per = (nb + kPickThreads - 1) / kPickThreads;
+    const int b0 = tid * per, b1 = min(b0 + per, nb);
+    double mine = 0.0;
+    for (int b = b0; b < b1; ++b) mine += bsum[b];
+    double tot;
+    const double incl = block_scan_d(mine, s_w, tot);
+    if (!(tot > 0.0)) {  // all mass on chosen centres: the reference repeats c0
+        if (tid == 0) centers[step] = centers[0];
+        return;
+    }
+    const double target = u[step - 1] * tot;
+    double run = incl - mine;
+    int last_pos = -1;  // last block with mass (rounding fallback)
+    bool hit = false;
+    for (int b = b0; b < b1; ++b) {
+        const double v = bsum[b];
+        if (v > 0.0) last_pos = b;
+        if (!hit && run + v > target) {
+            atomicMin(&s_blk, b);
+            hit = true;
+        }
+        run += v;
+    }
+    if (last_pos >= 0) atomicMax(&s_lastmass, last_pos);
+    __syncthreads();
+    // u * tot at or above the rounded total: the last block with mass
+    int blk = s_blk != 0x7fffffff ? s_blk : (s_lastmass >= 0 ? s_lastmass : nb - 1);
+    // cumulative d2 before the block, then the index inside it
+    double before = 0.0;
+    {
+        double part = 0.0;
+        for (int b = b0; b < min(b1, blk); ++b) part += bsum[b];
+        double t2;
+        block_scan_d(part, s_w, t2);
+        before = t2;
+    }
+    const int64_t e0 = (int64_t)blk * kSeedChunk;
+    double v2[2];
+    int64_t ix[2];
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        ix[q] = e0 + 2 * tid + q;
+        v2[q] = ix[q] < n ? d2[ix[q]] : 0.0;
+    }
+    double t3;
+    const double inc2 = block_scan_d(v2[0] + v2[1], s_w, t3);
+    double r2 = before + inc2 - (v2[0] + v2[1]);
+#pragma unroll
+    for (int q = 0; q < 2; ++q) {
+        if (ix[q] < n && r2 + v2[q] > target) {
+            atomicMin(&s_idx, (unsigned long long)ix[q]);
+            break;
+        }
+        r2 += v2[q];
+    }
+    __syncthreads();
+    if (tid == 0) {
+        int64_t j = (int64_t)s_idx;
+        if (s_idx == ~0ull) {  // rounding: the block's last element with mass
+            j = e0;
+            for (int64_t q = min(e0 + kSeedChunk, n) - 1; q >= e0; --q)
+                if (d2[q] > 0.0) {
+                    j = q;
+                    break;
+                }
+        }
+        centers[step] = x[j];
+    }
+}
+
 }  // namespace ivr
 
 extern "C" size_t ivr_kmeans_lloyd_workspace_size(int32_t k) {
@@ -368,4 +516,32 @@ extern "C" int ivr_vq_decode(const uint16_t *indices, int64_t n, const double *c
         vq_decode_kernel<false><<<grid_for(n), kVqThreads, 0, (cudaStream_t)stream>>>(
             indices, n, centroids, k, out, reinterpret_cast<long long *>(bad));
     return check_launch("vq_decode_kernel");
+}
+
+extern "C" size_t ivr_kmeans_seed_workspace_size(int64_t n) {
+    const int64_t nb = (n + ivr::kSeedChunk - 1) / ivr::kSeedChunk;
+    return 8 * (size_t)(n < 1 ? 1 : n) + 8 * (size_t)(nb < 1 ? 1 : nb) + 256;
+}
+
+extern "C" int ivr_kmeans_seed(const double *values, int64_t n, int32_t k, int64_t first,
+                               const double *u, double *centers, void *workspace,
+                               size_t workspace_bytes, ivr_stream_t stream) {
+    using namespace ivr;
+    if (n < 1 || k < 1 || first < 0 || first >= n || !values || !centers || (k > 1 && !u) ||
+        !workspace || workspace_bytes < ivr_kmeans_seed_workspace_size(n)) {
+        set_error("ivr_kmeans_seed: bad argument");
+        return IVR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    double *d2 = reinterpret_cast<double *>(workspace);
+    const int nb = (int)((n + kSeedChunk - 1) / kSeedChunk);
+    double *bsum = d2 + ((n + 31) & ~(int64_t)31);
+    if (cudaMemcpyAsync(centers, values + first, sizeof(double), cudaMemcpyDeviceToDevice, st) !=
+        cudaSuccess)
+        return check_launch("ivr_kmeans_seed copy");
+    for (int i = 1; i < k; ++i) {
+        seed_update_kernel<<<nb, kSeedThreads, 0, st>>>(values, n, d2, centers + i - 1, i == 1, bsum);
+        seed_pick_kernel<<<1, kPickThreads, 0, st>>>(values, n, d2, bsum, nb, u, centers, i);
+    }
+    return check_launch("ivr_kmeans_seed");
 }

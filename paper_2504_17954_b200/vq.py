@@ -140,20 +140,17 @@ def kmeans(samples, k, seed=0, restarts=5):
 def _seed_plusplus(x, k, rng):
     """k-means++ seeding on the device (vq.py:60-72) with the reference's
     random stream: rng.integers for the first centre, then one rng.random()
-    per rng.choice(p = d2 / sum d2) (inverse CDF, side='right')."""
+    per rng.choice(p = d2 / sum d2) -- the first index (in sample order) whose
+    cumulative d2 exceeds u * sum d2.  ivr_kmeans_seed: two kernels per centre
+    (d2 update + block sums, then the pick)."""
     n = x.numel()
     first = int(rng.integers(n))
-    u = torch.from_numpy(rng.random(k - 1)).to(x.device)
+    u = torch.from_numpy(rng.random(k - 1)).to(x.device)  # k == 1: no draw, as the reference
     c = torch.empty(k, dtype=torch.float64, device=x.device)
-    c[0] = x[first]
-    d2 = (x - c[0]) ** 2
-    for i in range(1, k):
-        cdf = torch.cumsum(d2, 0)
-        tot = cdf[-1]
-        j = torch.searchsorted(cdf, (u[i - 1] * tot).reshape(1), right=True).clamp_(max=n - 1)
-        ci = torch.where(tot > 0, x[j], c[0])  # all mass on existing centres: repeat c[0]
-        c[i] = ci[0]
-        d2 = torch.minimum(d2, (x - ci) ** 2)
+    nb = int(L.lib().ivr_kmeans_seed_workspace_size(n))
+    ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+    L.check(L.lib().ivr_kmeans_seed(D.ptr(x), n, int(k), first, D.ptr(u), D.ptr(c), D.ptr(ws), nb,
+                                    D.stream_handle()), "ivr_kmeans_seed")
     return c
 
 

@@ -96,3 +96,21 @@ def test_quantize_dequantize_round_trip():
         owner = d.geometry if name in ("q_raw", "log_s", "o_logit") else d.shading
         assert np.array_equal(getattr(owner, name), cb.centroids[idx.astype(np.int64)])
     assert np.array_equal(d.geometry.mu, m.geometry.mu)
+
+
+def test_seed_plusplus_follows_the_reference_stream():
+    """Fused device k-means++ (ivr_kmeans_seed) picks the same centres as the
+    reference's _seed_plusplus (vq.py:60-72) from the same numpy stream."""
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.vq import _seed_plusplus
+    x = np.random.default_rng(11).normal(size=50_000) ** 3
+    k = 300
+    rng = np.random.default_rng(3)
+    ref = np.empty(k)
+    ref[0] = x[rng.integers(x.size)]
+    d2 = (x - ref[0]) ** 2
+    for i in range(1, k):
+        ref[i] = x[rng.choice(x.size, p=d2 / d2.sum())]
+        d2 = np.minimum(d2, (x - ref[i]) ** 2)
+    got = _seed_plusplus(to_dev(x), k, np.random.default_rng(3)).cpu().numpy()
+    assert np.array_equal(got, ref)
