@@ -6,7 +6,7 @@
 //
 //  1. depth ranks.  Positive float64 depths order like their bit patterns.
 //     The bits are shifted into a "coarse" key (bits - min) >> s of
-//     log2(n) + 1 bits (~2 buckets per splat; the [min, max] of the visible
+//     ceil(log2 n) bits (~1-2 buckets per splat; the [min, max] of the visible
 //     keys comes from K1's block-reduced atomics, or from a min/max kernel
 //     when the keys are supplied directly) and the splats are counting-sorted
 //     by it: bucket counts by atomics, one exclusive scan, a scatter that
@@ -780,7 +780,7 @@ struct Plan {
     size_t off[16];
     size_t total;
     int nbk, nbp;
-    int vbits;          // coarse-key bits: 2^vbits depth buckets (~2 per splat)
+    int vbits;          // coarse-key bits: 2^vbits depth buckets (1-2 per splat)
     int64_t nbuckets;   // 2^vbits + 1 (the invisible splats' bucket last)
     int64_t nscan;      // bucket-scan blocks
     size_t ctrl_bytes;  // zeroed per frame: counters, flags, bucket counts, look-back words
@@ -796,7 +796,7 @@ Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
     L.nbp = (int)((n + kRanksPerBlock - 1) / kRanksPerBlock);
     int lg = 1;
     while (lg < 29 && (1ll << lg) < n) ++lg;
-    L.vbits = lg + 1;
+    L.vbits = lg;
     L.nbuckets = (1ll << L.vbits) + 1;
     L.nscan = (L.nbuckets + kChunk - 1) / kChunk;
     L.ctrl_bytes = kCtrlHead + 4 * (size_t)L.nbuckets + 4 * (size_t)L.nscan;
@@ -896,8 +896,8 @@ extern "C" int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key,
     uint32_t *ttot = (uint32_t *)(ws + L.off[11]);
     const int nbk = L.nbk, nbp = L.nbp;
 
-    // ---- 1. depth ranks: counting sort on a coarse key of log2(n) + 1 bits
-    //      (~2 buckets per splat), then each bucket sorted by (key, index)
+    // ---- 1. depth ranks: counting sort on a coarse key of ceil(log2 n) bits
+    //      (1-2 buckets per splat), then each bucket sorted by (key, index)
     cudaMemsetAsync(ctrl, 0, L.ctrl_bytes, st);
     unsigned long long *mm = depth_minmax;
     if (!mm) {  // keys supplied directly: reduce their range here

@@ -190,3 +190,41 @@ def test_inverse_graph_sharded_views_equal_single_process(tmp_path):
     f, losses = optimize_to_reference(sc, p, refs, cams, iters=4, lr=0.01)
     ref = np.concatenate([f.c_p.ravel(), f.opacity_raw, f.lam, f.b, [f.polar, f.azimuth], losses])
     np.testing.assert_allclose(r0, ref, rtol=1e-6, atol=1e-9)
+
+
+def _dist_fit_uneven_worker(rank, world, port, out_dir):
+    import os
+    import torch.distributed as tdist
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    tdist.init_process_group("gloo", rank=rank, world_size=world)
+    from paper_2504_17954_b200.inverse import optimize_to_reference
+    sc, p, refs, cams = _orbital_setup(2)
+    mine = [0, 1] if rank == 0 else []  # rank 1 holds no view
+    fitted, losses = optimize_to_reference(sc, p, [refs[v] for v in mine], [cams[v] for v in mine],
+                                           iters=4, lr=0.01)
+    np.save(os.path.join(out_dir, f"u{rank}.npy"),
+            np.concatenate([fitted.c_p.ravel(), fitted.opacity_raw, fitted.lam, fitted.b,
+                            [fitted.polar, fitted.azimuth], losses]))
+    tdist.barrier()
+    tdist.destroy_process_group()
+
+
+def test_inverse_graph_rank_without_views(tmp_path):
+    """A rank holding no view takes the same (graph) path as the others and
+    only joins the all-reduce + update: both ranks end on the single-process
+    2-view trajectory (the collectives stay matched)."""
+    import socket
+    import torch.multiprocessing as mp
+    from paper_2504_17954_b200.inverse import optimize_to_reference
+    s = socket.socket()
+    s.bind(("127.0.0.1", 0))
+    port = s.getsockname()[1]
+    s.close()
+    mp.spawn(_dist_fit_uneven_worker, args=(2, port, str(tmp_path)), nprocs=2, join=True)
+    r0, r1 = np.load(tmp_path / "u0.npy"), np.load(tmp_path / "u1.npy")
+    np.testing.assert_allclose(r0, r1, rtol=1e-12, atol=1e-15)
+    sc, p, refs, cams = _orbital_setup(2)
+    f, losses = optimize_to_reference(sc, p, refs, cams, iters=4, lr=0.01)
+    ref = np.concatenate([f.c_p.ravel(), f.opacity_raw, f.lam, f.b, [f.polar, f.azimuth], losses])
+    np.testing.assert_allclose(r0, ref, rtol=1e-6, atol=1e-9)
