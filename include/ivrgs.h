@@ -579,7 +579,8 @@ int ivr_loss_finalize(const ivr_loss_terms *t, double *loss, int64_t *state, dou
 typedef struct ivr_inverse_step {
     int32_t n_scenes, n_views, orbital, learnable;
     int64_t iters;
-    double view_div; /* views over all ranks (mean divisor); <= 0: n_views */
+    double view_div; /* views over all ranks (mean divisor); <= 0: n_views.  A rank
+                      * holding no view (n_views = 0) needs view_div > 0 */
     double *x, *m, *v;
     int64_t *t;
     double lr, beta1, beta2, eps;

@@ -177,8 +177,11 @@ __global__ void __launch_bounds__(kThreads) update_kernel(ivr_inverse_step A) {
 }  // namespace ivr
 
 namespace {
+// n_views may be 0 on a rank that holds no view of a sharded fit (it only
+// joins the all-reduce and applies the update; view_div > 0 then)
 bool bad_state(const ivr_inverse_step *a) {
-    return !a || a->n_scenes < 1 || a->n_scenes > ivr::invk::kMaxScenes || a->n_views < 1 ||
+    return !a || a->n_scenes < 1 || a->n_scenes > ivr::invk::kMaxScenes || a->n_views < 0 ||
+           (a->n_views == 0 && !(a->view_div > 0.0)) ||
            !a->x || !a->m || !a->v || !a->t || !a->grad || !a->loss_sum || !a->losses || !a->ctl || !a->params || !a->tab ||
            a->iters < 1;
 }
@@ -188,7 +191,7 @@ extern "C" int ivr_inverse_pack(const ivr_inverse_step *a, const double *photo_s
                                 double windows, const double *d_c_p, const double *d_scale,
                                 const double *d_globals, const int32_t *n_pairs,
                                 int64_t pair_capacity, ivr_stream_t stream) {
-    if (bad_state(a) || !photo_sums || !d_c_p || !d_scale || !d_globals || !n_pairs ||
+    if (bad_state(a) || a->n_views < 1 || !photo_sums || !d_c_p || !d_scale || !d_globals || !n_pairs ||
         !(numel > 0.0) || !(windows > 0.0)) {
         ivr::set_error("ivr_inverse_pack: bad argument");
         return IVR_ERR_ARG;
