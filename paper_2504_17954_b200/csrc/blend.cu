@@ -353,12 +353,159 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
     }
 }
 
+// ------------------------------------------------- FAST float32, K <= 4
+// The same walk with the list records staged by asynchronous copies
+// (cp.async, Ampere-style LDGSTS gathers: the records of a chunk are not
+// contiguous, so a bulk/TMA copy does not apply) into a kStages-deep per-warp
+// ring in shared memory: chunk c + kStages is requested as soon as chunk c
+// has been walked, and its pair ids one chunk earlier, so two walks hide the
+// dependent id -> record L2 round trips (the register prefetch of warp_walk
+// hid one: ncu showed ~14% of K3's warp samples in long-scoreboard stalls
+// at the chunk boundary), with no prefetch registers held across the walk.
+constexpr int kStages = 3;
+
+template <int KMAX>
+struct StageSlots {
+    float4 r0[kStages][32], r1[kStages][32];
+    float v[kStages][32 * KMAX];
+};
+
+__device__ __forceinline__ void cp_async16(void *dst, const void *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 16;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async4(void *dst, const void *src) {
+    const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
+    asm volatile("cp.async.ca.shared.global [%0], [%1], 4;" ::"r"(d), "l"(src) : "memory");
+}
+__device__ __forceinline__ void cp_async_commit() { asm volatile("cp.async.commit_group;" ::: "memory"); }
+template <int N>
+__device__ __forceinline__ void cp_async_wait() {
+    asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
+}
+
+template <int KMAX>
+__device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<KMAX> &S, int s0,
+                                                 int s1, int px, int py, int sx0, int sx1,
+                                                 int sy0, int sy1, PixelState<KMAX, false> &st) {
+    const int lane = threadIdx.x & 31;
+    const int K = A.K;
+    const float fpx = (float)px, fpy = (float)py;
+    const double dpx = (double)px, dpy = (double)py;
+    const int nch = (s1 - s0 + 31) >> 5;
+    auto fetch_id = [&](int c) {
+        const int j = s0 + 32 * c + lane;
+        return c < nch && j < s1 ? __ldg(A.pair_splat + j) : -1;
+    };
+    // request chunk c's records (id < 0: culled for the tile or past the end)
+    auto request = [&](int c, int id) {
+        if (id >= 0) {
+            const int g = c % kStages;
+            cp_async16(&S.r0[g][lane], A.rec + 2 * id);
+            cp_async16(&S.r1[g][lane], A.rec + 2 * id + 1);
+            if (KMAX == 4 && K == 4) {
+                cp_async16(&S.v[g][lane * 4], A.values + 4 * (int64_t)id);
+            } else {
+#pragma unroll
+                for (int c2 = 0; c2 < KMAX; ++c2)
+                    if (c2 < K) cp_async4(&S.v[g][lane * KMAX + c2], A.values + (int64_t)K * id + c2);
+            }
+        }
+        cp_async_commit();  // one group per chunk, possibly empty
+    };
+    int i0 = fetch_id(0), i1 = fetch_id(1), i2 = fetch_id(2);
+    request(0, i0);
+    request(1, i1);
+    request(2, i2);
+    int in = fetch_id(3);
+    for (int c = 0; c < nch; ++c) {
+        if (__all_sync(0xffffffffu, st.done)) break;
+        cp_async_wait<kStages - 1>();  // this lane's copies of chunk c landed
+        __syncwarp();                  // ... and every lane's
+        const int g = c % kStages;
+        const int base = s0 + 32 * c;
+        bool keep = false;
+        if (i0 >= 0) {
+            const float4 r0 = S.r0[g][lane], r1 = S.r1[g][lane];
+            keep = !tile_cull32(r0, r1, sx0, sx1, sy0, sy1);
+            // the walk reads thr_lo = thr - (thr rounding + margins) in place of thr
+            if (keep) S.r1[g][lane].w = r1.w - (2.4e-7f * fabsf(r1.w) + 1e-7f);
+        }
+        const uint32_t m = __ballot_sync(0xffffffffu, keep);
+        __syncwarp();
+        uint32_t mbits = st.done ? 0u : m;
+        while (mbits) {
+            const int q = __ffs(mbits) - 1;
+            mbits &= mbits - 1;
+            const float4 a0 = S.r0[g][q];
+            const float4 a1 = S.r1[g][q];
+            const float dx = fpx - a0.x, dy = fpy - a0.y;
+            const float bdy = a1.y * dy, hcdy = a1.z * dy;
+            const float sig = fmaf(fmaf(a1.x, dx, bdy), dx, hcdy * dy);
+            if (sig > a0.w) continue;  // reference alpha < 1/255 for certain
+            const float terms = fmaf(a1.x * dx, dx, fmaf(hcdy, dy, fabsf(bdy * dx)));
+            const float E = kSigmaErr * terms + 1e-30f;
+            float al, dal;
+            if (sig - E > 0.0f && sig + E < a1.w) {
+                const float au = a0.z * ex2_approx(-1.4426950408889634f * sig);
+                const float rel = E + 1.2e-7f * sig + 3.6e-7f;
+                const bool capped = au > 0.99f * (1.0f + rel);
+                al = fminf(au, 0.99f);
+                dal = capped ? 1.1e-8f : au * rel;
+            } else if (sig - E > a0.w) {
+                continue;
+            } else {
+                const double ad = exact_alpha(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
+                                              2.0 * (double)a1.z, a0.z);
+                if (ad < 0.0) continue;
+                al = (float)ad;
+                dal = 6e-8f * al;
+            }
+            const float w = st.Tf * al;
+            if (KMAX == 4) {
+                const float4 v = *reinterpret_cast<const float4 *>(&S.v[g][q * 4]);
+                st.acc[0] = fmaf(w, v.x, st.acc[0]);
+                st.acc[1] = fmaf(w, v.y, st.acc[1]);
+                st.acc[2] = fmaf(w, v.z, st.acc[2]);
+                st.acc[3] = fmaf(w, v.w, st.acc[3]);
+            } else {
+#pragma unroll
+                for (int c2 = 0; c2 < KMAX; ++c2) st.acc[c2] = fmaf(w, S.v[g][q * KMAX + c2], st.acc[c2]);
+            }
+            const float om = 1.0f - al;
+            st.Tf = st.Tf * om;
+            st.errT = fmaf(dal * rcp_approx(om), 1.01e-4f, st.errT + 1.3e-11f);
+            ++st.nc;
+            st.last = base + q + 1;
+            if (st.Tf < 1.0000001e-4f + st.errT) {
+                st.done = true;
+                st.replay = !(st.Tf < 0.9999999e-4f - st.errT);
+                break;
+            }
+        }
+        __syncwarp();  // every lane is done reading stage g
+        request(c + kStages, in);
+        i0 = i1;
+        i1 = i2;
+        i2 = in;
+        in = fetch_id(c + kStages + 1);
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // the ring may be reused (EXACT re-walk)
+    __syncwarp();
+}
+
+template <int KMAX, bool F64, int MODE>
+constexpr bool kStaged = MODE == kModeFast && !F64 && KMAX <= 4;
+
 template <int KMAX, bool F64, int MODE>
 __global__ void __launch_bounds__(kBlendThreads, (KMAX <= 4 && !F64) ? 4 : 3)
 blend_fwd_kernel(BlendArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Slots = WarpSlots<KMAX, F64, kModeExact>;  // EXACT layout also serves FAST
-    Slots &W = reinterpret_cast<Slots *>(smem)[threadIdx.x >> 5];
+    // per-warp region: WarpSlots, or (staged FAST walk) the StageSlots ring
+    constexpr size_t kRegion = (kStaged<KMAX, F64, MODE> && sizeof(StageSlots<KMAX>) > sizeof(Slots))
+                                   ? sizeof(StageSlots<KMAX>) : sizeof(Slots);
+    Slots &W = *reinterpret_cast<Slots *>(smem + (threadIdx.x >> 5) * kRegion);
 
     const int tile = A.tile_order ? A.tile_order[blockIdx.x] : (int)blockIdx.x;
     const int tx = tile % A.ntx, ty = tile / A.ntx;
@@ -377,7 +524,13 @@ blend_fwd_kernel(BlendArgs A) {
     if (A.trace) asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t_start));
     PixelState<KMAX, F64> st;
     st.reset(s0, !inside);
-    warp_walk<KMAX, F64, MODE, kModeExact>(A, W, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
+    if constexpr (kStaged<KMAX, F64, MODE>) {
+        // the ring aliases the warp's WarpSlots region (warp_walk runs after it)
+        StageSlots<KMAX> &S = *reinterpret_cast<StageSlots<KMAX> *>(smem + warp * kRegion);
+        warp_walk_staged<KMAX>(A, S, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
+    } else {
+        warp_walk<KMAX, F64, MODE, kModeExact>(A, W, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
+    }
     if (A.trace && lane == 0) {
         long long t_end;
         int sm_;
@@ -432,14 +585,16 @@ blend_fwd_kernel(BlendArgs A) {
     if (A.t_final) A.t_final[pix] = st.T;
 }
 
-template <int KMAX, bool F64>
+template <int KMAX, bool F64, int MODE>
 size_t blend_smem_bytes() {
-    return (kBlendThreads / 32) * sizeof(WarpSlots<KMAX, F64, kModeExact>);
+    const size_t slots = sizeof(WarpSlots<KMAX, F64, kModeExact>);
+    const size_t ring = kStaged<KMAX, F64, MODE> ? sizeof(StageSlots<KMAX>) : 0;
+    return (kBlendThreads / 32) * (ring > slots ? ring : slots);
 }
 
 template <int KMAX, bool F64, int MODE>
 int launch_blend(const BlendArgs &A, int ntiles, cudaStream_t st) {
-    const size_t sm = blend_smem_bytes<KMAX, F64>();
+    const size_t sm = blend_smem_bytes<KMAX, F64, MODE>();
     auto fn = blend_fwd_kernel<KMAX, F64, MODE>;
     if (sm > 48 * 1024) cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
     fn<<<ntiles, kBlendThreads, sm, st>>>(A);
