@@ -413,11 +413,12 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
         }
         cp_async_commit();  // one group per chunk, possibly empty
     };
-    int i0 = fetch_id(0), i1 = fetch_id(1), i2 = fetch_id(2);
-    request(0, i0);
-    request(1, i1);
-    request(2, i2);
-    int in = fetch_id(3);
+    int ids[kStages];  // ids[k]: pair ids of chunk c + k (constant indices: registers)
+#pragma unroll
+    for (int k = 0; k < kStages; ++k) ids[k] = fetch_id(k);
+#pragma unroll
+    for (int k = 0; k < kStages; ++k) request(k, ids[k]);
+    int in = fetch_id(kStages);
     for (int c = 0; c < nch; ++c) {
         if (__all_sync(0xffffffffu, st.done)) break;
         cp_async_wait<kStages - 1>();  // this lane's copies of chunk c landed
@@ -425,7 +426,7 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
         const int g = c % kStages;
         const int base = s0 + 32 * c;
         bool keep = false;
-        if (i0 >= 0) {
+        if (ids[0] >= 0) {
             const float4 r0 = S.r0[g][lane], r1 = S.r1[g][lane];
             keep = !tile_cull32(r0, r1, sx0, sx1, sy0, sy1);
             // the walk reads thr_lo = thr - (thr rounding + margins) in place of thr
@@ -485,9 +486,9 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
         }
         __syncwarp();  // every lane is done reading stage g
         request(c + kStages, in);
-        i0 = i1;
-        i1 = i2;
-        i2 = in;
+#pragma unroll
+        for (int k = 0; k + 1 < kStages; ++k) ids[k] = ids[k + 1];
+        ids[kStages - 1] = in;
         in = fetch_id(c + kStages + 1);
     }
     asm volatile("cp.async.wait_all;" ::: "memory");  // the ring may be reused (EXACT re-walk)
