@@ -20,11 +20,12 @@ __device__ __forceinline__ double vq_mid(const double *c, int i) { return 0.5 * 
 
 // lut[b] = number of midpoints < lo + b * w  (b < kLut); params = {lo, w, inv_w,
 // float32 buckets safe}
+template <int NB = kLut>
 __global__ void __launch_bounds__(kVqThreads)
 vq_lut_kernel(const double *__restrict__ cents, int k, uint16_t *lut, double *params) {
     const int nm = k - 1;
     const double lo = vq_mid(cents, 0), hi = vq_mid(cents, nm - 1);
-    const double w = (hi - lo) / kLut;
+    const double w = (hi - lo) / NB;
     if (blockIdx.x == 0 && threadIdx.x == 0) {
         params[0] = lo;
         params[1] = w;
@@ -37,7 +38,7 @@ vq_lut_kernel(const double *__restrict__ cents, int k, uint16_t *lut, double *pa
         params[3] = (w > 0.0 && mag * 4.0 * 1.1920928955078125e-07 + w * 1e-6 < 0.25 * w) ? 1.0 : 0.0;
     }
     const int b = blockIdx.x * kVqThreads + threadIdx.x;
-    if (b >= kLut) return;
+    if (b >= NB) return;
     const double e = lo + (double)b * w;
     int a = 0, z = nm;  // count of mids < e
     while (a < z) {
@@ -138,6 +139,123 @@ vq_assign_kernel(const double *__restrict__ values, int64_t n, const double *__r
     }
 }
 
+// Assign, windowed form (K - 1 <= kVqSmemMids, at least one midpoint): the
+// bucket table (kLutWin) is widened in shared memory to one word per bucket
+// holding its search window [lut[b - 1], lut[b + 2]), and the window is
+// searched by four branch-free binary-lifting steps (windows of <= 15
+// midpoints: all of the C5 attribute values; wider windows,
+// and the corner cases the float32 bucket index can hit, take the verified
+// full search).  A warp moves 256 contiguous values per step: four 16-byte
+// loads and four 4-byte stores (two indices each) per lane.
+constexpr int kWinSteps = 4;
+constexpr int kLutWin = 8192;  // buckets of the windowed search (32 KB of windows)
+
+template <int NB>
+__device__ __forceinline__ int vq_pos_win(const double *mid, const uint32_t *win, int nm, double v,
+                                          float lo_f, float inv_w_f, bool exact_buckets,
+                                          bool use_lut, bool &ok) {
+    const float t = ((float)v - lo_f) * inv_w_f;
+    const float tc = fminf(fmaxf(t, 0.0f), (float)(NB - 1));  // NaN -> 0 (handled by the caller)
+    const uint32_t w = win[(int)tc];
+    const int a0 = (int)(w & 0xffffu), zi = (int)(w >> 16);
+    int pos = a0;
+#pragma unroll
+    for (int s = kWinSteps - 1; s >= 0; --s) {
+        const int m = pos + (1 << s) - 1;
+        const bool in = m < zi;
+        const double x = mid[in ? m : 0];
+        if (in && x < v) pos = m + 1;
+    }
+    ok = use_lut && zi - a0 < (1 << kWinSteps);
+    const bool inside = t >= 0.0f && t < (float)(NB - 1);
+    if (ok && !(exact_buckets && inside)) {
+        const bool ok_lo = pos > a0 || a0 == 0 || mid[a0 - 1] < v;
+        const bool ok_hi = pos < zi || zi == nm || !(mid[zi] < v);
+        ok = ok_lo && ok_hi;
+    }
+    return pos;
+}
+
+constexpr int kWinThreads = 512;  // larger CTAs: more warps per SM under the 64 KB of tables
+constexpr int kWinR = 2;          // 16-byte value loads per lane per step
+constexpr int kWinTile = 64 * kWinR;  // values per warp per step
+
+template <int NB>
+__global__ void __launch_bounds__(kWinThreads, 3)
+vq_assign_win_kernel(const double *__restrict__ values, int64_t n, const double *__restrict__ cents,
+                     int k, const uint16_t *__restrict__ lut, const double *__restrict__ params,
+                     uint16_t *__restrict__ out) {
+    extern __shared__ __align__(16) unsigned char sm_w[];
+    double *s_mid = reinterpret_cast<double *>(sm_w);
+    uint32_t *s_win = reinterpret_cast<uint32_t *>(s_mid + kVqSmemMids);
+    const int nm = k - 1;
+    for (int i = threadIdx.x; i < nm; i += kWinThreads) s_mid[i] = vq_mid(cents, i);
+    for (int b = threadIdx.x; b < NB; b += kWinThreads) {
+        const uint32_t a = b >= 1 ? lut[b - 1] : 0u;
+        const uint32_t z = b + 2 < NB ? lut[b + 2] : (uint32_t)nm;
+        s_win[b] = a | (z << 16);
+    }
+    __syncthreads();
+    const double lo = params[0], inv_w = params[2];
+    const bool use_lut = inv_w > 0.0;
+    const bool exact_buckets = params[3] != 0.0;
+    const float lo_f = (float)lo, inv_w_f = (float)inv_w;
+    const int lane = threadIdx.x & 31;
+    constexpr int kWarpsPerCta = kWinThreads / 32;
+    const int64_t gw = (int64_t)blockIdx.x * kWarpsPerCta + (threadIdx.x >> 5);
+    const int64_t step = (int64_t)gridDim.x * kWarpsPerCta * kWinTile;
+    // the next tile's values are loaded before this tile is searched
+    auto load = [&](int64_t t, double2 *v) {
+        if (t + kWinTile <= n) {
+#pragma unroll
+            for (int r = 0; r < kWinR; ++r)
+                v[r] = __ldcs(reinterpret_cast<const double2 *>(values + t + 64 * r + 2 * lane));
+        }
+    };
+    double2 nxt[kWinR];
+    load(gw * kWinTile, nxt);
+    for (int64_t tile = gw * kWinTile; tile < n; tile += step) {
+        if (tile + kWinTile <= n) {
+            double2 v[kWinR];
+#pragma unroll
+            for (int r = 0; r < kWinR; ++r) v[r] = nxt[r];
+            load(tile + step, nxt);
+            // every window search first (independent chains overlap), the rare
+            // verified full searches after
+            int p[2 * kWinR];
+            bool ok[2 * kWinR];
+#pragma unroll
+            for (int r = 0; r < kWinR; ++r) {
+                p[2 * r] = vq_pos_win<NB>(s_mid, s_win, nm, v[r].x, lo_f, inv_w_f, exact_buckets,
+                                          use_lut, ok[2 * r]);
+                p[2 * r + 1] = vq_pos_win<NB>(s_mid, s_win, nm, v[r].y, lo_f, inv_w_f, exact_buckets,
+                                              use_lut, ok[2 * r + 1]);
+            }
+#pragma unroll
+            for (int q = 0; q < 2 * kWinR; ++q) {
+                const double x = (q & 1) ? v[q >> 1].y : v[q >> 1].x;
+                if (!ok[q]) p[q] = vq_full_search(s_mid, nm, x);
+                if (x != x) p[q] = nm;  // NaN sorts last
+            }
+#pragma unroll
+            for (int r = 0; r < kWinR; ++r)
+                __stcs(reinterpret_cast<uint32_t *>(out + tile + 64 * r + 2 * lane),
+                       (uint32_t)p[2 * r] | ((uint32_t)p[2 * r + 1] << 16));
+        } else {
+            for (int j = 0; j < 2 * kWinR; ++j) {
+                const int64_t i = tile + 64 * (j >> 1) + 2 * lane + (j & 1);
+                if (i >= n) continue;
+                const double x = values[i];
+                bool okq;
+                int p = vq_pos_win<NB>(s_mid, s_win, nm, x, lo_f, inv_w_f, exact_buckets, use_lut, okq);
+                if (!okq) p = vq_full_search(s_mid, nm, x);
+                if (x != x) p = nm;
+                out[i] = (uint16_t)p;
+            }
+        }
+    }
+}
+
 // 8 indices per thread per step: one 16-byte load, four 16-byte stores; the
 // codebook is gathered from shared memory (K <= kVqSmemMids + 1)
 template <bool SMEM>
@@ -156,10 +274,18 @@ vq_decode_kernel(const uint16_t *__restrict__ idx, int64_t n, const double *__re
     const int64_t stride = (int64_t)gridDim.x * kVqThreads;
     int worst = -1;
     if (aligned) {
-        for (int64_t t = (int64_t)blockIdx.x * kVqThreads + threadIdx.x; t < nv; t += stride) {
-            const uint4 q = __ldcs(reinterpret_cast<const uint4 *>(idx) + t);
-            const uint32_t w[4] = {q.x, q.y, q.z, q.w};
-            double2 *o = reinterpret_cast<double2 *>(out + 8 * t);
+        // a warp decodes 256 contiguous indices per step; every load and
+        // store instruction covers one contiguous span (128 B of indices,
+        // 512 B of values), lane l holding entries 64 p + 2 l and + 1
+        const int lane = threadIdx.x & 31;
+        const int64_t nw = nv / 32;  // whole 256-index tiles
+        const int64_t wstride = stride / 32;
+        for (int64_t tw = ((int64_t)blockIdx.x * kVqThreads + threadIdx.x) / 32; tw < nw; tw += wstride) {
+            const uint32_t *src = reinterpret_cast<const uint32_t *>(idx + 256 * tw) + lane;
+            double2 *o = reinterpret_cast<double2 *>(out + 256 * tw) + lane;
+            uint32_t w[4];
+#pragma unroll
+            for (int p = 0; p < 4; ++p) w[p] = __ldcs(src + 32 * p);
 #pragma unroll
             for (int p = 0; p < 4; ++p) {
                 const int j0 = (int)(w[p] & 0xffffu), j1 = (int)(w[p] >> 16);
@@ -167,12 +293,12 @@ vq_decode_kernel(const uint16_t *__restrict__ idx, int64_t n, const double *__re
                 if (j1 >= k) worst = max(worst, j1);
                 const double d0 = j0 < k ? tab[j0] : 0.0;
                 const double d1 = j1 < k ? tab[j1] : 0.0;
-                __stcs(o + p, make_double2(d0, d1));
+                __stcs(o + 32 * p, make_double2(d0, d1));
             }
         }
     }
-    for (int64_t i = (aligned ? 8 * nv : 0) + (int64_t)blockIdx.x * kVqThreads + threadIdx.x; i < n;
-         i += stride) {
+    for (int64_t i = (aligned ? 256 * (nv / 32) : 0) + (int64_t)blockIdx.x * kVqThreads + threadIdx.x;
+         i < n; i += stride) {
         const int j = idx[i];
         if (j >= k) worst = max(worst, j);
         out[i] = j < k ? tab[j] : 0.0;
@@ -184,7 +310,7 @@ vq_decode_kernel(const uint16_t *__restrict__ idx, int64_t n, const double *__re
 // 4, 7}: 0.195, 0.149, 0.153, 0.160, 0.235 ms for 60M values)
 static int grid_for_decode(int64_t n) {
     int64_t b = (n / 8 + kVqThreads - 1) / kVqThreads;
-    const int64_t cap = 148 * 2;
+    const int64_t cap = 148 * 4;  // 2 -> 4 CTAs per SM: 128 -> 111 us at C5 (more stores in flight)
     return (int)(b < 1 ? 1 : (b > cap ? cap : b));
 }
 
@@ -464,7 +590,7 @@ extern "C" int ivr_kmeans_lloyd_step(const double *values, int64_t n, const doub
 }
 
 extern "C" size_t ivr_vq_assign_workspace_size(void) {
-    return 4 * sizeof(double) + 2 * (size_t)ivr::kLut;
+    return 8 * sizeof(double) + 2 * (size_t)ivr::kLut + 2 * (size_t)ivr::kLutWin;
 }
 
 extern "C" int ivr_vq_assign(const double *values, int64_t n, const double *centroids, int32_t k,
@@ -489,10 +615,28 @@ extern "C" int ivr_vq_assign(const double *values, int64_t n, const double *cent
     double *params = reinterpret_cast<double *>(workspace);
     uint16_t *lut = reinterpret_cast<uint16_t *>(params + 4);
     if (k - 1 <= kVqSmemMids) {
-        vq_lut_kernel<<<(kLut + kVqThreads - 1) / kVqThreads, kVqThreads, 0, st>>>(centroids, k, lut,
-                                                                                  params);
-        vq_assign_kernel<true><<<grid_for(n), kVqThreads, 0, st>>>(values, n, centroids, k, lut,
-                                                                   params, indices);
+        const bool aligned = ((reinterpret_cast<uintptr_t>(values) & 15) == 0) &&
+                             ((reinterpret_cast<uintptr_t>(indices) & 3) == 0);
+        if (aligned) {
+            double *params_w = params + 4 + kLut / 4;  // after the kLut table
+            uint16_t *lut_w = reinterpret_cast<uint16_t *>(params_w + 4);
+            vq_lut_kernel<kLutWin><<<(kLutWin + kVqThreads - 1) / kVqThreads, kVqThreads, 0, st>>>(
+                centroids, k, lut_w, params_w);
+            auto fn = vq_assign_win_kernel<kLutWin>;
+            const size_t sm = kVqSmemMids * sizeof(double) + kLutWin * sizeof(uint32_t);
+            cudaFuncSetAttribute(fn, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm);
+            int per_sm = 0;
+            cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, fn, kWinThreads, sm);
+            int64_t b = (n + kWinTile - 1) / kWinTile / (kWinThreads / 32);
+            const int64_t cap = 148 * (int64_t)(per_sm > 0 ? per_sm : 1);
+            b = b < 1 ? 1 : (b > cap ? cap : b);
+            fn<<<(int)b, kWinThreads, sm, st>>>(values, n, centroids, k, lut_w, params_w, indices);
+        } else {
+            vq_lut_kernel<<<(kLut + kVqThreads - 1) / kVqThreads, kVqThreads, 0, st>>>(centroids, k,
+                                                                                      lut, params);
+            vq_assign_kernel<true><<<grid_for(n), kVqThreads, 0, st>>>(values, n, centroids, k, lut,
+                                                                       params, indices);
+        }
     } else {
         cudaMemsetAsync(params, 0, 4 * sizeof(double), st);
         vq_assign_kernel<false><<<grid_for(n), kVqThreads, 0, st>>>(values, n, centroids, k, lut,
