@@ -29,6 +29,12 @@
 
 #include "cull.cuh"
 
+// K3 FAST walk: pair ids through the bulk-copy engine (A/B switch, see
+// warp_walk_staged)
+#ifndef IVR_K3_BULK_IDS
+#define IVR_K3_BULK_IDS 0
+#endif
+
 namespace ivr {
 
 constexpr int kBlendThreads = 256;
@@ -116,6 +122,10 @@ struct BlendArgs {
     const int32_t *tile_order;
     int preculled;
     long long *trace;  // debug: per (tile, block) {tile, smid, t0, t1} (globaltimer), or null
+#if IVR_K3_BULK_IDS
+    int ntx_nty;       // tile count: ranges[ntx_nty] = pairs in the frame
+    int *bulk_fault;   // set when a bulk id copy never completed
+#endif
 };
 
 template <int KMAX, bool F64>
@@ -368,7 +378,47 @@ template <int KMAX>
 struct StageSlots {
     float4 r0[kStages][32], r1[kStages][32];
     float v[kStages][32 * KMAX];
+#if IVR_K3_BULK_IDS
+    int ids[2][40];                 // bulk-copied pair-id windows (36 ints used)
+    unsigned long long bar[2];      // their mbarriers
+#endif
 };
+
+#if IVR_K3_BULK_IDS
+// Pair ids by the bulk-copy engine (cp.async.bulk + mbarrier): the ids of a
+// chunk are contiguous, so lane 0 requests the 16-byte-aligned 144-byte
+// window around them; the wait is bounded (a lost completion marks the
+// frame bad instead of hanging the SM).
+__device__ __forceinline__ uint32_t smem_u32(const void *p) {
+    return (uint32_t)__cvta_generic_to_shared(p);
+}
+__device__ __forceinline__ void bar_init(unsigned long long *b) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bar_inval(unsigned long long *b) {
+    asm volatile("mbarrier.inval.shared::cta.b64 [%0];" ::"r"(smem_u32(b)) : "memory");
+}
+__device__ __forceinline__ void bulk_ids(int *dst, const int32_t *src, unsigned long long *b) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], 144;" ::"r"(smem_u32(b)) : "memory");
+    asm volatile(
+        "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], 144, [%2];" ::"r"(
+            smem_u32(dst)),
+        "l"(src), "r"(smem_u32(b))
+        : "memory");
+}
+__device__ __forceinline__ bool bar_wait(unsigned long long *b, uint32_t phase) {
+    for (int n = 0; n < (1 << 22); ++n) {
+        uint32_t done;
+        asm volatile(
+            "{\n.reg .pred p;\nmbarrier.try_wait.parity.shared::cta.b64 p, [%1], %2;\nselp.u32 %0, 1, 0, p;\n}"
+            : "=r"(done)
+            : "r"(smem_u32(b)), "r"(phase)
+            : "memory");
+        if (done) return true;
+    }
+    return false;
+}
+#endif
 
 __device__ __forceinline__ void cp_async16(void *dst, const void *src) {
     const unsigned d = (unsigned)__cvta_generic_to_shared(dst);
@@ -419,6 +469,27 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
 #pragma unroll
     for (int k = 0; k < kStages; ++k) request(k, ids[k]);
     int in = fetch_id(kStages);
+#if IVR_K3_BULK_IDS
+    // chunks q >= kStages + 1 come through the bulk ring: slot (q - q0) & 1,
+    // parity ((q - q0) >> 1) & 1; a chunk whose 144-byte window would read
+    // past the frame's last pair is loaded directly instead
+    constexpr int q0 = kStages + 1;
+    const int n_all = A.ranges[A.ntx_nty];
+    auto bulk_ok = [&](int q) { return q < nch && ((s0 + 32 * q) & ~3) + 36 <= n_all; };
+    auto bulk_issue = [&](int q) {
+        if (lane == 0 && bulk_ok(q))
+            bulk_ids(S.ids[(q - q0) & 1], A.pair_splat + ((s0 + 32 * q) & ~3), &S.bar[(q - q0) & 1]);
+    };
+    if (lane == 0) {
+        bar_init(&S.bar[0]);
+        bar_init(&S.bar[1]);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    }
+    __syncwarp();
+    bulk_issue(q0);
+    bulk_issue(q0 + 1);
+    int c_end = 0;
+#endif
     for (int c = 0; c < nch; ++c) {
         if (__all_sync(0xffffffffu, st.done)) break;
         cp_async_wait<kStages - 1>();  // this lane's copies of chunk c landed
@@ -489,8 +560,42 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
 #pragma unroll
         for (int k = 0; k + 1 < kStages; ++k) ids[k] = ids[k + 1];
         ids[kStages - 1] = in;
+#if IVR_K3_BULK_IDS
+        {
+            const int q = c + kStages + 1;
+            if (bulk_ok(q)) {
+                const int sl = (q - q0) & 1;
+                if (!bar_wait(&S.bar[sl], (uint32_t)(((q - q0) >> 1) & 1))) {
+                    if (lane == 0) atomicExch(A.bulk_fault, 1);
+                    in = -1;
+                } else {
+                    const int j = s0 + 32 * q + lane;
+                    in = j < s1 ? S.ids[sl][((s0 + 32 * q) & 3) + lane] : -1;
+                }
+                __syncwarp();
+                asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                bulk_issue(q + 2);
+            } else {
+                in = fetch_id(q);
+            }
+        }
+        c_end = c + 1;
+#else
         in = fetch_id(c + kStages + 1);
+#endif
     }
+#if IVR_K3_BULK_IDS
+    // drain the (at most two) bulk copies issued but not consumed
+    for (int q = c_end + kStages + 1; q <= c_end + kStages + 2; ++q) {
+        if (bulk_ok(q) && !bar_wait(&S.bar[(q - q0) & 1], (uint32_t)(((q - q0) >> 1) & 1)) && lane == 0)
+            atomicExch(A.bulk_fault, 1);
+    }
+    __syncwarp();
+    if (lane == 0) {
+        bar_inval(&S.bar[0]);
+        bar_inval(&S.bar[1]);
+    }
+#endif
     asm volatile("cp.async.wait_all;" ::: "memory");  // the ring may be reused (EXACT re-walk)
     __syncwarp();
 }
@@ -693,6 +798,15 @@ extern "C" int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_spl
     A.tile_order = tile_order;
     A.preculled = (flags & IVR_BLEND_PRECULLED) != 0 ? 1 : 0;
     A.trace = g_blend_trace;
+#if IVR_K3_BULK_IDS
+    A.ntx_nty = ntx * nty;
+    static int *fault = nullptr;
+    if (!fault) {
+        cudaMalloc(&fault, sizeof(int));
+        cudaMemset(fault, 0, sizeof(int));
+    }
+    A.bulk_fault = fault;
+#endif
     const bool exact = (flags & IVR_BLEND_EXACT) != 0;
     const int nt = ntx * nty;
 #define IVR_BLEND(KM)                                                                   \
