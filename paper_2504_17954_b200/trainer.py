@@ -244,6 +244,33 @@ class _StageTrainer:
             lr = lr * cfg.lr_decay_floor ** frac
         return lr
 
+    def step_views(self, cams, gts, weights=None):
+        """Batch-of-views step (BASELINE configs[2]; an extension of the
+        reference's one view per iteration, SURVEY.md finding 6): the mean
+        over the views of the per-view loss and gradients of ``step`` (the
+        per-view densify statistics are summed), to be applied with one
+        ``apply``.  Its parity is the mean of the reference's per-view step
+        gradients; with one view it is ``step``."""
+        cams, gts = list(cams), list(gts)
+        if not cams or len(cams) != len(gts):
+            raise ValueError("step_views: need one ground-truth image per camera")
+        loss_acc = grads_acc = stat_acc = None
+        for cam, gt in zip(cams, gts):
+            loss, grads, stat = self.step(cam, gt, weights)
+            if grads_acc is None:  # step reuses its buffers: keep copies
+                loss_acc = loss.clone()
+                grads_acc = {k: g.clone() for k, g in grads.items()}
+                stat_acc = stat.clone()
+            else:
+                loss_acc += loss
+                for k, g in grads.items():
+                    grads_acc[k] += g
+                stat_acc += stat
+        inv = 1.0 / len(cams)
+        for g in grads_acc.values():
+            g.mul_(inv)
+        return loss_acc * inv, grads_acc, stat_acc
+
     def apply(self, grads, it, iters, decay_extra=()):
         """Adam on every group with the reference schedules (trainer.py:491-499)."""
         items = [(name, self.p[name], grad, self.lr(name, it, iters, decay_extra))

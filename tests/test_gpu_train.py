@@ -206,3 +206,25 @@ def test_training_loop_graph_equals_eager(monkeypatch):
     for a, b in zip(log_g, log_e):
         assert abs(a["count"] - b["count"]) <= 0.02 * b["count"]
         assert abs(a["loss"] - b["loss"]) <= 1e-3 * abs(b["loss"]) + 1e-9
+
+
+def test_step_views_is_the_mean_of_single_view_steps():
+    """Batch-of-views step (BASELINE configs[2], an extension): loss and
+    gradients are the means of the per-view steps, densify stats the sum."""
+    make, cams, gts = _graph_setup()
+    tr = make()
+    views = [0, 1, 2]
+    singles = []
+    for v in views:
+        loss, grads, stat = tr.step(cams[v], gts[v])
+        singles.append((float(loss), {k: g.clone() for k, g in grads.items()}, stat.clone()))
+    loss, grads, stat = tr.step_views([cams[v] for v in views], [gts[v] for v in views])
+    np.testing.assert_allclose(float(loss), np.mean([s[0] for s in singles]), rtol=1e-12)
+    for k, g in grads.items():
+        ref = sum(s[1][k] for s in singles) / len(views)
+        err = float((g - ref).norm() / max(float(ref.norm()), 1e-300))
+        assert err <= 1e-5, (k, err)  # float32 atomics: run-to-run order only
+    ref_stat = sum(s[2] for s in singles)
+    assert float((stat - ref_stat).norm()) <= 1e-5 * float(ref_stat.norm())
+    one = tr.step_views([cams[0]], [gts[0]])
+    np.testing.assert_allclose(float(one[0]), singles[0][0], rtol=1e-12)
