@@ -744,6 +744,8 @@ def run_ours(args):
             r["traffic_over_alg"] = r["traffic"] / alg
             r["ncu"] = {k: rec[k] for k in ("duration_us", "issue_active_pct",
                                             "sm_active_over_elapsed", "warps_active_pct")}
+            if "pipe_pct" in rec:  # FP32 FMA / ALU / XU / FP64 pipe, % of peak (active cycles)
+                r["ncu"]["pipe_pct"] = rec["pipe_pct"]
             r["ncu"]["source"] = rec["source"]
         if note:
             r["note"] = note
