@@ -248,6 +248,12 @@ int ivr_blend_fwd(const int32_t *tile_ranges, const int32_t *pair_splat,
  * (ntiles * 8 * 4 int64 device memory); NULL stops recording. */
 void ivr_debug_blend_trace(long long *buf);
 
+/* Test only: maximal relative errors of ex2.approx.ftz.f32 over [-126, 0]
+ * (every multiple of 2^-16) and rcp.approx.ftz.f32 over every float in
+ * [1/128, 1], against float64 -- the instruction bounds FAST mode's certified
+ * decisions assume.  out: 2 doubles of device memory, zeroed by the caller. */
+int ivr_debug_mufu_error(double *out, ivr_stream_t stream);
+
 /* Heaviest-first tile launch order for ivr_blend_fwd (counting sort on
  * half-octave buckets of the per-tile pair count, descending).  Scheduling
  * only: any permutation yields identical images. */

@@ -762,6 +762,46 @@ long long *g_blend_trace = nullptr;  // debug hook only (tools/blend_trace.py)
 // int64), or stop with NULL.  Not for concurrent use.
 extern "C" void ivr_debug_blend_trace(long long *buf) { g_blend_trace = buf; }
 
+namespace ivr {
+// Measured error of the two approximate MUFU instructions K3/K4 certify
+// against (FAST mode): ex2.approx.ftz over every multiple of 2^-16 in
+// [-126, 0] (alpha = o 2^(-sigma log2 e)) and rcp.approx.ftz over every
+// float32 in [1/128, 1] (1 / (1 - alpha)), relative to float64; maxima as
+// ordered bit patterns of positive doubles.
+__global__ void mufu_err_kernel(unsigned long long *out) {
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    double m_ex2 = 0.0, m_rcp = 0.0;
+    for (int64_t k = t0; k <= 126ll << 16; k += stride) {
+        const float x = -(float)k * 0x1p-16f;
+        const double ref = exp2((double)x);
+        const double rel = fabs((double)ex2_approx(x) - ref) / ref;
+        m_ex2 = rel > m_ex2 ? rel : m_ex2;
+    }
+    const uint32_t lo = __float_as_uint(0x1p-7f), hi = __float_as_uint(1.0f);
+    for (int64_t k = t0; k <= (int64_t)(hi - lo); k += stride) {
+        const float x = __uint_as_float(lo + (uint32_t)k);
+        const double ref = 1.0 / (double)x;
+        const double rel = fabs((double)rcp_approx(x) - ref) / ref;
+        m_rcp = rel > m_rcp ? rel : m_rcp;
+    }
+    atomicMax(out, (unsigned long long)__double_as_longlong(m_ex2));
+    atomicMax(out + 1, (unsigned long long)__double_as_longlong(m_rcp));
+}
+}  // namespace ivr
+
+// Debug / test: out (device, 2 doubles, caller-zeroed) receives the maximal
+// relative errors of ex2.approx and rcp.approx over the ranges K3/K4 use.
+extern "C" int ivr_debug_mufu_error(double *out, ivr_stream_t stream) {
+    if (!out) {
+        ivr::set_error("ivr_debug_mufu_error: bad argument");
+        return IVR_ERR_ARG;
+    }
+    ivr::mufu_err_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+        reinterpret_cast<unsigned long long *>(out));
+    return ivr::check_launch("mufu_err_kernel");
+}
+
 extern "C" int ivr_tile_order(const int32_t *tile_ranges, int32_t ntiles, int32_t *order,
                               ivr_stream_t stream) {
     using namespace ivr;
