@@ -254,6 +254,12 @@ void ivr_debug_blend_trace(long long *buf);
  * decisions assume.  out: 2 doubles of device memory, zeroed by the caller. */
 int ivr_debug_mufu_error(double *out, ivr_stream_t stream);
 
+/* Test only: maximal |sigma32 - sigma_ref| / (|a/2 dx^2| + |b dx dy| +
+ * |c/2 dy^2|) of K3's float32 exponent vs float64 on the same float32 record,
+ * over n seeded random (record, pixel) samples -- the ratio kSigmaErr (4e-7)
+ * bounds.  out: 1 double of device memory, zeroed by the caller. */
+int ivr_debug_sigma_error(int64_t n, uint32_t seed, double *out, ivr_stream_t stream);
+
 /* Heaviest-first tile launch order for ivr_blend_fwd (counting sort on
  * half-octave buckets of the per-tile pair count, descending).  Scheduling
  * only: any permutation yields identical images. */

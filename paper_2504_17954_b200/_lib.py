@@ -154,6 +154,7 @@ _SIGS = {
     "ivr_tile_order": ([P, ctypes.c_int32, P, P], ctypes.c_int),
     "ivr_debug_blend_trace": ([P], None),
     "ivr_debug_mufu_error": ([P, P], ctypes.c_int),
+    "ivr_debug_sigma_error": ([ctypes.c_int64, ctypes.c_uint32, P, P], ctypes.c_int),
     "ivr_kmeans_seed_workspace_size": ([ctypes.c_int64], ctypes.c_size_t),
     "ivr_kmeans_seed": ([P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, P, P, P,
                          ctypes.c_size_t, P], ctypes.c_int),

@@ -788,7 +788,64 @@ __global__ void mufu_err_kernel(unsigned long long *out) {
     atomicMax(out, (unsigned long long)__double_as_longlong(m_ex2));
     atomicMax(out + 1, (unsigned long long)__double_as_longlong(m_rcp));
 }
+
+// Measured |sigma32 - sigma_ref| / (|a/2 dx^2| + |b dx dy| + |c/2 dy^2|) of
+// the FAST walk's float32 exponent against the reference's float64 one on
+// the same float32 record (random conics with condition <= 1e4, means up to
+// 4096 px, pixels out to sigma ~ 40): the ratio kSigmaErr bounds.
+__device__ __forceinline__ uint32_t hash32(uint32_t x) {
+    x ^= x >> 16;
+    x *= 0x7feb352dU;
+    x ^= x >> 15;
+    x *= 0x846ca68bU;
+    x ^= x >> 16;
+    return x;
+}
+__device__ __forceinline__ float urand(uint32_t &st) {
+    st = hash32(st + 0x9e3779b9U);
+    return (float)(st >> 8) * 0x1p-24f;
+}
+__global__ void sigma_err_kernel(int64_t n, uint32_t seed, unsigned long long *out) {
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    double worst = 0.0;
+    for (int64_t i = t0; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+        uint32_t st = hash32((uint32_t)i * 2654435761u ^ seed);
+        const float mx = 4096.0f * urand(st), my = 4096.0f * urand(st);
+        const float a = exp2f(-13.0f + 16.0f * urand(st)), c = a * exp2f(-6.0f + 12.0f * urand(st));
+        const float b = (2.0f * urand(st) - 1.0f) * 0.999f * sqrtf(a * c);
+        // a pixel at exponent up to ~40 from the mean
+        const float r = sqrtf(80.0f / fminf(a, c)) * urand(st), th = 6.2831853f * urand(st);
+        const int px = (int)floorf(mx + r * cosf(th)), py = (int)floorf(my + r * sinf(th));
+        // FAST walk (float32 record a/2, b, c/2)
+        const float ha = 0.5f * a, hc = 0.5f * c;
+        const float dx = (float)px - mx, dy = (float)py - my;
+        const float bdy = b * dy, hcdy = hc * dy;
+        const float sig = fmaf(fmaf(ha, dx, bdy), dx, hcdy * dy);
+        // reference: float64 on the same float32 values
+        const double ddx = (double)px - (double)mx, ddy = (double)py - (double)my;
+        const double sref = 0.5 * ((double)a * ddx * ddx + (double)c * ddy * ddy) + (double)b * ddx * ddy;
+        const double terms = 0.5 * (double)a * ddx * ddx + fabs((double)b * ddx * ddy) +
+                             0.5 * (double)c * ddy * ddy;
+        if (terms > 0.0) {
+            const double q = fabs((double)sig - sref) / terms;
+            worst = q > worst ? q : worst;
+        }
+    }
+    atomicMax(out, (unsigned long long)__double_as_longlong(worst));
+}
 }  // namespace ivr
+
+// Debug / test: maximal |sigma32 - sigma_ref| / terms over n random
+// (record, pixel) samples into out[0] (device, caller-zeroed).
+extern "C" int ivr_debug_sigma_error(int64_t n, uint32_t seed, double *out, ivr_stream_t stream) {
+    if (!out || n < 1) {
+        ivr::set_error("ivr_debug_sigma_error: bad argument");
+        return IVR_ERR_ARG;
+    }
+    ivr::sigma_err_kernel<<<148 * 8, 256, 0, (cudaStream_t)stream>>>(
+        n, seed, reinterpret_cast<unsigned long long *>(out));
+    return ivr::check_launch("sigma_err_kernel");
+}
 
 // Debug / test: out (device, 2 doubles, caller-zeroed) receives the maximal
 // relative errors of ex2.approx and rcp.approx over the ranges K3/K4 use.
