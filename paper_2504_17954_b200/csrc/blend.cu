@@ -436,14 +436,75 @@ __device__ __forceinline__ void cp_async_wait() {
     asm volatile("cp.async.wait_group %0;" ::"n"(N) : "memory");
 }
 
+// FAST float32 walk of one staged chunk: the survivors `mbits` (records r0,
+// r1 with thr_lo in r1.w, values v zero-padded to KMAX) in list order for
+// this lane's pixel; sets st.done (+ st.replay when ambiguous) at the stop.
+template <int KMAX>
+__device__ __forceinline__ void walk_chunk_fast(const float4 *r0s, const float4 *r1s,
+                                                const float *vs, uint32_t mbits, int base, int px,
+                                                int py, PixelState<KMAX, false> &st) {
+    const float fpx = (float)px, fpy = (float)py;
+    while (mbits) {
+        const int q = __ffs(mbits) - 1;
+        mbits &= mbits - 1;
+        const float4 a0 = r0s[q];
+        const float4 a1 = r1s[q];
+        const float dx = fpx - a0.x, dy = fpy - a0.y;
+        const float bdy = a1.y * dy, hcdy = a1.z * dy;
+        const float sig = fmaf(fmaf(a1.x, dx, bdy), dx, hcdy * dy);
+        if (sig > a0.w) continue;  // reference alpha < 1/255 for certain
+        const float terms = fmaf(a1.x * dx, dx, fmaf(hcdy, dy, fabsf(bdy * dx)));
+        const float E = kSigmaErr * terms + 1e-30f;
+        float al, dal;
+        if (sig - E > 0.0f && sig + E < a1.w) {
+            const float au = a0.z * ex2_approx(-1.4426950408889634f * sig);
+            const float rel = E + 1.2e-7f * sig + 3.6e-7f;
+            const bool capped = au > 0.99f * (1.0f + rel);
+            al = fminf(au, 0.99f);
+            dal = capped ? 1.1e-8f : au * rel;
+        } else if (sig - E > a0.w) {
+            continue;
+        } else {
+            const double ad = exact_alpha((double)px, (double)py, a0.x, a0.y, 2.0 * (double)a1.x,
+                                          a1.y, 2.0 * (double)a1.z, a0.z);
+            if (ad < 0.0) continue;
+            al = (float)ad;
+            dal = 6e-8f * al;
+        }
+        const float w = st.Tf * al;
+        if (KMAX % 4 == 0) {
+            const float4 *vv = reinterpret_cast<const float4 *>(vs + q * KMAX);
+#pragma unroll
+            for (int c4 = 0; c4 < KMAX / 4; ++c4) {
+                const float4 v = vv[c4];
+                st.acc[4 * c4] = fmaf(w, v.x, st.acc[4 * c4]);
+                st.acc[4 * c4 + 1] = fmaf(w, v.y, st.acc[4 * c4 + 1]);
+                st.acc[4 * c4 + 2] = fmaf(w, v.z, st.acc[4 * c4 + 2]);
+                st.acc[4 * c4 + 3] = fmaf(w, v.w, st.acc[4 * c4 + 3]);
+            }
+        } else {
+#pragma unroll
+            for (int c2 = 0; c2 < KMAX; ++c2) st.acc[c2] = fmaf(w, vs[q * KMAX + c2], st.acc[c2]);
+        }
+        const float om = 1.0f - al;
+        st.Tf = st.Tf * om;
+        st.errT = fmaf(dal * rcp_approx(om), 1.01e-4f, st.errT + 1.3e-11f);
+        ++st.nc;
+        st.last = base + q + 1;
+        if (st.Tf < 1.0000001e-4f + st.errT) {
+            st.done = true;
+            st.replay = !(st.Tf < 0.9999999e-4f - st.errT);
+            return;
+        }
+    }
+}
+
 template <int KMAX>
 __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<KMAX> &S, int s0,
                                                  int s1, int px, int py, int sx0, int sx1,
                                                  int sy0, int sy1, PixelState<KMAX, false> &st) {
     const int lane = threadIdx.x & 31;
     const int K = A.K;
-    const float fpx = (float)px, fpy = (float)py;
-    const double dpx = (double)px, dpy = (double)py;
     const int nch = (s1 - s0 + 31) >> 5;
     auto fetch_id = [&](int c) {
         const int j = s0 + 32 * c + lane;
@@ -507,56 +568,7 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
         }
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
         __syncwarp();
-        uint32_t mbits = st.done ? 0u : m;
-        while (mbits) {
-            const int q = __ffs(mbits) - 1;
-            mbits &= mbits - 1;
-            const float4 a0 = S.r0[g][q];
-            const float4 a1 = S.r1[g][q];
-            const float dx = fpx - a0.x, dy = fpy - a0.y;
-            const float bdy = a1.y * dy, hcdy = a1.z * dy;
-            const float sig = fmaf(fmaf(a1.x, dx, bdy), dx, hcdy * dy);
-            if (sig > a0.w) continue;  // reference alpha < 1/255 for certain
-            const float terms = fmaf(a1.x * dx, dx, fmaf(hcdy, dy, fabsf(bdy * dx)));
-            const float E = kSigmaErr * terms + 1e-30f;
-            float al, dal;
-            if (sig - E > 0.0f && sig + E < a1.w) {
-                const float au = a0.z * ex2_approx(-1.4426950408889634f * sig);
-                const float rel = E + 1.2e-7f * sig + 3.6e-7f;
-                const bool capped = au > 0.99f * (1.0f + rel);
-                al = fminf(au, 0.99f);
-                dal = capped ? 1.1e-8f : au * rel;
-            } else if (sig - E > a0.w) {
-                continue;
-            } else {
-                const double ad = exact_alpha(dpx, dpy, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
-                                              2.0 * (double)a1.z, a0.z);
-                if (ad < 0.0) continue;
-                al = (float)ad;
-                dal = 6e-8f * al;
-            }
-            const float w = st.Tf * al;
-            if (KMAX == 4) {
-                const float4 v = *reinterpret_cast<const float4 *>(&S.v[g][q * 4]);
-                st.acc[0] = fmaf(w, v.x, st.acc[0]);
-                st.acc[1] = fmaf(w, v.y, st.acc[1]);
-                st.acc[2] = fmaf(w, v.z, st.acc[2]);
-                st.acc[3] = fmaf(w, v.w, st.acc[3]);
-            } else {
-#pragma unroll
-                for (int c2 = 0; c2 < KMAX; ++c2) st.acc[c2] = fmaf(w, S.v[g][q * KMAX + c2], st.acc[c2]);
-            }
-            const float om = 1.0f - al;
-            st.Tf = st.Tf * om;
-            st.errT = fmaf(dal * rcp_approx(om), 1.01e-4f, st.errT + 1.3e-11f);
-            ++st.nc;
-            st.last = base + q + 1;
-            if (st.Tf < 1.0000001e-4f + st.errT) {
-                st.done = true;
-                st.replay = !(st.Tf < 0.9999999e-4f - st.errT);
-                break;
-            }
-        }
+        walk_chunk_fast<KMAX>(S.r0[g], S.r1[g], S.v[g], st.done ? 0u : m, base, px, py, st);
         __syncwarp();  // every lane is done reading stage g
         request(c + kStages, in);
 #pragma unroll
@@ -602,8 +614,95 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
     __syncwarp();
 }
 
+// Wide values (FAST, 4 < K <= 16, e.g. the K=15 training forward): records
+// go through the same ring, but a chunk's values (up to 64 B per pair) are
+// requested only for the pairs that survive the 8x4 cull, one chunk ahead:
+// at step c the warp culls chunk c + 1 (its records are in), requests those
+// survivors' values, walks chunk c (values requested at step c - 1) and then
+// refills chunk c's record slot with chunk c + 3.  Copy groups per step:
+// values(c + 1), then records(c + 3), so `wait_group 1` at the top of step c
+// leaves only records(c + 2) in flight.
+template <int KMAX>
+__device__ __forceinline__ void warp_walk_staged_sv(const BlendArgs &A, StageSlots<KMAX> &S,
+                                                    int s0, int s1, int px, int py, int sx0,
+                                                    int sx1, int sy0, int sy1,
+                                                    PixelState<KMAX, false> &st) {
+    static_assert(kStages == 3, "the copy-group schedule assumes a 3-deep ring");
+    const int lane = threadIdx.x & 31;
+    const int K = A.K;
+    const int nch = (s1 - s0 + 31) >> 5;
+    auto fetch_id = [&](int c) {
+        const int j = s0 + 32 * c + lane;
+        return c < nch && j < s1 ? __ldg(A.pair_splat + j) : -1;
+    };
+    auto request_rec = [&](int c, int id) {
+        if (id >= 0) {
+            const int g = c % kStages;
+            cp_async16(&S.r0[g][lane], A.rec + 2 * id);
+            cp_async16(&S.r1[g][lane], A.rec + 2 * id + 1);
+        }
+        cp_async_commit();
+    };
+    auto request_val = [&](int c, int id, bool keep) {
+        if (keep) {
+            const int g = c % kStages;
+            const float *v = A.values + (int64_t)K * id;
+#pragma unroll
+            for (int c2 = 0; c2 < KMAX; ++c2)
+                if (c2 < K) cp_async4(&S.v[g][lane * KMAX + c2], v + c2);
+        }
+        cp_async_commit();
+    };
+    // cull chunk c against the block (records in), stage thr_lo for the walk
+    auto cull = [&](int c, int id) {
+        bool keep = false;
+        if (id >= 0) {
+            const int g = c % kStages;
+            const float4 r0 = S.r0[g][lane], r1 = S.r1[g][lane];
+            keep = !tile_cull32(r0, r1, sx0, sx1, sy0, sy1);
+            if (keep) S.r1[g][lane].w = r1.w - (2.4e-7f * fabsf(r1.w) + 1e-7f);
+        }
+        return keep;
+    };
+    int ids[kStages];
+#pragma unroll
+    for (int k = 0; k < kStages; ++k) ids[k] = fetch_id(k);
+#pragma unroll
+    for (int k = 0; k < kStages; ++k) request_rec(k, ids[k]);
+    int in = fetch_id(kStages);
+    cp_async_wait<kStages - 1>();  // records of chunk 0
+    __syncwarp();
+    const bool k0 = cull(0, ids[0]);
+    uint32_t m_cur = __ballot_sync(0xffffffffu, k0);  // survivors of the chunk walked next
+    __syncwarp();
+    request_val(0, ids[0], k0);
+    for (int c = 0; c < nch; ++c) {
+        if (__all_sync(0xffffffffu, st.done)) break;
+        if (c == 0) asm volatile("cp.async.wait_all;" ::: "memory");
+        else cp_async_wait<1>();
+        __syncwarp();
+        const int g = c % kStages;
+        // cull the next chunk and request its survivors' values
+        bool kn = false;
+        if (c + 1 < nch) kn = cull(c + 1, ids[1]);
+        const uint32_t m_next = __ballot_sync(0xffffffffu, kn);
+        __syncwarp();
+        request_val(c + 1, ids[1], kn);
+        walk_chunk_fast<KMAX>(S.r0[g], S.r1[g], S.v[g], st.done ? 0u : m_cur, s0 + 32 * c, px, py, st);
+        __syncwarp();  // every lane is done reading chunk c's slots
+        request_rec(c + kStages, in);
+#pragma unroll
+        for (int k = 0; k + 1 < kStages; ++k) ids[k] = ids[k + 1];
+        ids[kStages - 1] = in;
+        in = fetch_id(c + kStages + 1);
+        m_cur = m_next;
+    }
+    asm volatile("cp.async.wait_all;" ::: "memory");  // the ring may be reused (EXACT re-walk)
+    __syncwarp();
+}
+
 template <int KMAX, bool F64, int MODE>
-constexpr bool kStaged = MODE == kModeFast && !F64 && KMAX <= 4;
+constexpr bool kStaged = MODE == kModeFast && !F64 && KMAX <= 16;
 
 template <int KMAX, bool F64, int MODE>
 __global__ void __launch_bounds__(kBlendThreads, (KMAX <= 4 && !F64) ? 4 : 3)
@@ -640,7 +739,10 @@ blend_fwd_kernel(BlendArgs A) {
     if constexpr (kStaged<KMAX, F64, MODE>) {
         // the ring aliases the warp's WarpSlots region (warp_walk runs after it)
         StageSlots<KMAX> &S = *reinterpret_cast<StageSlots<KMAX> *>(smem + (tid >> 5) * kRegion);
-        warp_walk_staged<KMAX>(A, S, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
+        if constexpr (KMAX <= 4)
+            warp_walk_staged<KMAX>(A, S, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
+        else
+            warp_walk_staged_sv<KMAX>(A, S, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
     } else {
         warp_walk<KMAX, F64, MODE, kModeExact>(A, W, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
     }
