@@ -377,13 +377,23 @@ __device__ __forceinline__ void warp_walk(const BlendArgs &A, WarpSlots<KMAX, F6
 constexpr int kStages = 3;
 
 template <int KMAX>
-struct StageSlots {
+struct StageBase {
     float4 r0[kStages][32], r1[kStages][32];
     float v[kStages][32 * KMAX];
 #if IVR_K3_BULK_IDS
     int ids[2][40];                 // bulk-copied pair-id windows (36 ints used)
     unsigned long long bar[2];      // their mbarriers
 #endif
+};
+template <int KMAX, bool F64 = false>
+struct StageSlots : StageBase<KMAX> {};
+// float64-decision mode: the float64 mean rides along (its float32 residual
+// corrects dx, dy) and the splat id serves the band pairs' lazy float64 read
+template <int KMAX>
+struct StageSlots<KMAX, true> : StageBase<KMAX> {
+    double2 m64[kStages][32];
+    float2 lo[kStages][32];
+    int sp[kStages][32];
 };
 
 #if IVR_K3_BULK_IDS
@@ -439,10 +449,13 @@ __device__ __forceinline__ void cp_async_wait() {
 // FAST float32 walk of one staged chunk: the survivors `mbits` (records r0,
 // r1 with thr_lo in r1.w, values v zero-padded to KMAX) in list order for
 // this lane's pixel; sets st.done (+ st.replay when ambiguous) at the stop.
-template <int KMAX>
+template <int KMAX, bool F64 = false>
 __device__ __forceinline__ void walk_chunk_fast(const float4 *r0s, const float4 *r1s,
                                                 const float *vs, uint32_t mbits, int base, int px,
-                                                int py, PixelState<KMAX, false> &st) {
+                                                int py, PixelState<KMAX, F64> &st,
+                                                const float2 *los = nullptr,
+                                                const int *sps = nullptr,
+                                                const double *rec64 = nullptr) {
     const float fpx = (float)px, fpy = (float)py;
     while (mbits) {
         const int q = __ffs(mbits) - 1;
@@ -453,20 +466,37 @@ __device__ __forceinline__ void walk_chunk_fast(const float4 *r0s, const float4 
         const float bdy = a1.y * dy, hcdy = a1.z * dy;
         const float sig = fmaf(fmaf(a1.x, dx, bdy), dx, hcdy * dy);
         if (sig > a0.w) continue;  // reference alpha < 1/255 for certain
-        const float terms = fmaf(a1.x * dx, dx, fmaf(hcdy, dy, fabsf(bdy * dx)));
+        // float64 decisions: dx, dy from the float64 mean (float32 residual)
+        float cdx = dx, cdy = dy, cbdy = bdy, chcdy = hcdy, csig = sig;
+        if (F64) {
+            const float2 lo = los[q];
+            cdx = dx - lo.x;
+            cdy = dy - lo.y;
+            cbdy = a1.y * cdy;
+            chcdy = a1.z * cdy;
+            csig = fmaf(fmaf(a1.x, cdx, cbdy), cdx, chcdy * cdy);
+        }
+        const float terms = fmaf(a1.x * cdx, cdx, fmaf(chcdy, cdy, fabsf(cbdy * cdx)));
         const float E = kSigmaErr * terms + 1e-30f;
         float al, dal;
-        if (sig - E > 0.0f && sig + E < a1.w) {
-            const float au = a0.z * ex2_approx(-1.4426950408889634f * sig);
-            const float rel = E + 1.2e-7f * sig + 3.6e-7f;
+        if (csig - E > 0.0f && csig + E < a1.w) {
+            const float au = a0.z * ex2_approx(-1.4426950408889634f * csig);
+            const float rel = E + 1.2e-7f * csig + 3.6e-7f;
             const bool capped = au > 0.99f * (1.0f + rel);
             al = fminf(au, 0.99f);
             dal = capped ? 1.1e-8f : au * rel;
-        } else if (sig - E > a0.w) {
+        } else if (csig - E > a0.w) {
             continue;
         } else {
-            const double ad = exact_alpha((double)px, (double)py, a0.x, a0.y, 2.0 * (double)a1.x,
-                                          a1.y, 2.0 * (double)a1.z, a0.z);
+            double ad;
+            if (F64) {
+                const double *r = rec64 + 8 * (int64_t)sps[q];
+                ad = exact_alpha((double)px, (double)py, __ldg(r), __ldg(r + 1), __ldg(r + 2),
+                                 __ldg(r + 3), __ldg(r + 4), __ldg(r + 5));
+            } else {
+                ad = exact_alpha((double)px, (double)py, a0.x, a0.y, 2.0 * (double)a1.x, a1.y,
+                                 2.0 * (double)a1.z, a0.z);
+            }
             if (ad < 0.0) continue;
             al = (float)ad;
             dal = 6e-8f * al;
@@ -499,10 +529,10 @@ __device__ __forceinline__ void walk_chunk_fast(const float4 *r0s, const float4 
     }
 }
 
-template <int KMAX>
-__device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<KMAX> &S, int s0,
-                                                 int s1, int px, int py, int sx0, int sx1,
-                                                 int sy0, int sy1, PixelState<KMAX, false> &st) {
+template <int KMAX, bool F64 = false>
+__device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<KMAX, F64> &S,
+                                                 int s0, int s1, int px, int py, int sx0, int sx1,
+                                                 int sy0, int sy1, PixelState<KMAX, F64> &st) {
     const int lane = threadIdx.x & 31;
     const int K = A.K;
     const int nch = (s1 - s0 + 31) >> 5;
@@ -516,6 +546,7 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
             const int g = c % kStages;
             cp_async16(&S.r0[g][lane], A.rec + 2 * id);
             cp_async16(&S.r1[g][lane], A.rec + 2 * id + 1);
+            if constexpr (F64) cp_async16(&S.m64[g][lane], A.rec64 + 8 * (int64_t)id);
             if (KMAX == 4 && K == 4) {
                 cp_async16(&S.v[g][lane * 4], A.values + 4 * (int64_t)id);
             } else {
@@ -565,10 +596,21 @@ __device__ __forceinline__ void warp_walk_staged(const BlendArgs &A, StageSlots<
             keep = !tile_cull32(r0, r1, sx0, sx1, sy0, sy1);
             // the walk reads thr_lo = thr - (thr rounding + margins) in place of thr
             if (keep) S.r1[g][lane].w = r1.w - (2.4e-7f * fabsf(r1.w) + 1e-7f);
+            if constexpr (F64) {
+                if (keep) {  // mean - float32(mean): exact in float64, tiny
+                    const double2 m = S.m64[g][lane];
+                    S.lo[g][lane] = make_float2((float)(m.x - (double)r0.x), (float)(m.y - (double)r0.y));
+                    S.sp[g][lane] = ids[0];
+                }
+            }
         }
         const uint32_t m = __ballot_sync(0xffffffffu, keep);
         __syncwarp();
-        walk_chunk_fast<KMAX>(S.r0[g], S.r1[g], S.v[g], st.done ? 0u : m, base, px, py, st);
+        if constexpr (F64)
+            walk_chunk_fast<KMAX, true>(S.r0[g], S.r1[g], S.v[g], st.done ? 0u : m, base, px, py,
+                                        st, S.lo[g], S.sp[g], A.rec64);
+        else
+            walk_chunk_fast<KMAX>(S.r0[g], S.r1[g], S.v[g], st.done ? 0u : m, base, px, py, st);
         __syncwarp();  // every lane is done reading stage g
         request(c + kStages, in);
 #pragma unroll
@@ -702,7 +744,7 @@ __device__ __forceinline__ void warp_walk_staged_sv(const BlendArgs &A, StageSlo
 }
 
 template <int KMAX, bool F64, int MODE>
-constexpr bool kStaged = MODE == kModeFast && !F64 && KMAX <= 16;
+constexpr bool kStaged = MODE == kModeFast && (F64 ? KMAX <= 4 : KMAX <= 16);
 
 template <int KMAX, bool F64, int MODE>
 __global__ void __launch_bounds__(kBlendThreads, (KMAX <= 4 && !F64) ? 4 : 3)
@@ -710,8 +752,9 @@ blend_fwd_kernel(BlendArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     using Slots = WarpSlots<KMAX, F64, kModeExact>;  // EXACT layout also serves FAST
     // per-warp region: WarpSlots, or (staged FAST walk) the StageSlots ring
-    constexpr size_t kRegion = (kStaged<KMAX, F64, MODE> && sizeof(StageSlots<KMAX>) > sizeof(Slots))
-                                   ? sizeof(StageSlots<KMAX>) : sizeof(Slots);
+    constexpr size_t kRegion =
+        (kStaged<KMAX, F64, MODE> && sizeof(StageSlots<KMAX, F64>) > sizeof(Slots))
+            ? sizeof(StageSlots<KMAX, F64>) : sizeof(Slots);
     Slots &W = *reinterpret_cast<Slots *>(smem + (threadIdx.x >> 5) * kRegion);
 
     // a CTA holds blockDim.x / 32 of the tile's 8 blocks (the warps are
@@ -738,10 +781,11 @@ blend_fwd_kernel(BlendArgs A) {
     st.reset(s0, !inside);
     if constexpr (kStaged<KMAX, F64, MODE>) {
         // the ring aliases the warp's WarpSlots region (warp_walk runs after it)
-        StageSlots<KMAX> &S = *reinterpret_cast<StageSlots<KMAX> *>(smem + (tid >> 5) * kRegion);
+        StageSlots<KMAX, F64> &S =
+            *reinterpret_cast<StageSlots<KMAX, F64> *>(smem + (tid >> 5) * kRegion);
         if constexpr (KMAX <= 4)
-            warp_walk_staged<KMAX>(A, S, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
-        else
+            warp_walk_staged<KMAX, F64>(A, S, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
+        else if constexpr (!F64)
             warp_walk_staged_sv<KMAX>(A, S, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
     } else {
         warp_walk<KMAX, F64, MODE, kModeExact>(A, W, s0, s1, px, py, sx0, sx1, sy0, sy1, st);
@@ -803,7 +847,7 @@ blend_fwd_kernel(BlendArgs A) {
 template <int KMAX, bool F64, int MODE>
 size_t blend_smem_bytes() {
     const size_t slots = sizeof(WarpSlots<KMAX, F64, kModeExact>);
-    const size_t ring = kStaged<KMAX, F64, MODE> ? sizeof(StageSlots<KMAX>) : 0;
+    const size_t ring = kStaged<KMAX, F64, MODE> ? sizeof(StageSlots<KMAX, F64>) : 0;
     return (kBlendThreads / 32) * (ring > slots ? ring : slots);
 }
 
