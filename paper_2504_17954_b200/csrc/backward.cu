@@ -2,7 +2,7 @@
 //
 // K4a blend_bwd_kernel replaces _kernels.composite_backward
 // (_kernels.py:75-135) + the per-Gaussian np.add.at reductions
-// (rasterizer.py:240-243).  One CTA per tile, one thread per pixel, each warp
+// (rasterizer.py:240-243).  Two CTAs per tile, one thread per pixel, each warp
 // an independent 8x4 pixel block that streams the tile list in 32-pair chunks
 // with the K3 strip cull; each pixel walks its contributors BACK to front
 // from last_pos, as the reference does: the transmittance in front of
@@ -124,7 +124,7 @@ struct BwdSlots {
 
 constexpr int kBwdWarpW = 8;  // warp footprint 8x4 pixels (as K3)
 
-// One CTA per tile, each warp an independent 8x4 block of pixels walking
+// Two CTAs per tile (4 warps each), each warp an independent 8x4 block of pixels walking
 // the tile list in 32-pair chunks up to the largest last_pos of its pixels
 // (same strip cull and prefetch as K3; no CTA barrier).
 template <int KMAX, bool F64, bool GEOM>
