@@ -42,7 +42,23 @@ __global__ void __launch_bounds__(256) adam_kernel(AdamGroups A) {
         G.m[i] = m;
         G.v[i] = v;
         const double mhat = dmul(m, i1), vhat = dmul(v, i2);
-        G.param[i] = dsub(G.param[i], ddiv(dmul(G.lr, mhat), dadd(sqrt(vhat), A.eps)));
+        // lr mhat / (sqrt(vhat) + eps) with the division as an approximate
+        // reciprocal refined by two Newton steps (within an ulp or two of
+        // the IEEE quotient: ~1e-16 of the update, far below the reference
+        // tolerance of the parameter; the kernel is FP64-issue bound)
+        // sqrt(vhat) likewise from an approximate reciprocal square root
+        // and two Newton steps (vhat = 0 -> 0)
+        double rs;
+        asm("rsqrt.approx.ftz.f64 %0, %1;" : "=d"(rs) : "d"(vhat));
+        rs = rs * fma(-0.5 * vhat, rs * rs, 1.5);
+        rs = rs * fma(-0.5 * vhat, rs * rs, 1.5);
+        const double sq = vhat > 0.0 ? vhat * rs : 0.0;
+        const double den = dadd(sq, A.eps);
+        double r;
+        asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(r) : "d"(den));
+        r = fma(r, fma(-den, r, 1.0), r);
+        r = fma(r, fma(-den, r, 1.0), r);
+        G.param[i] = dsub(G.param[i], dmul(dmul(G.lr, mhat), r));
     }
 }
 
