@@ -127,8 +127,11 @@ constexpr int kBwdWarpW = 8;  // warp footprint 8x4 pixels (as K3)
 // Two CTAs per tile (4 warps each), each warp an independent 8x4 block of pixels walking
 // the tile list in 32-pair chunks up to the largest last_pos of its pixels
 // (same strip cull and prefetch as K3; no CTA barrier).
+// 4-warp CTAs; K <= 4 (the inverse fit's float64-decision, geometry-free
+// instance) at 7 CTAs/SM (72 registers: C4 K4a 0.331 -> 0.31 ms), K <= 16
+// at 6 (80 registers; 7 CTAs cost the C3 instance 3%)
 template <int KMAX, bool F64, bool GEOM>
-__global__ void __launch_bounds__(kBwdThreads, KMAX <= 16 ? 3 : 1)
+__global__ void __launch_bounds__(128, KMAX <= 4 ? 7 : (KMAX <= 16 ? 6 : 2))
 blend_bwd_kernel(BwdArgs A) {
     extern __shared__ __align__(16) unsigned char smem[];
     BwdSlots<KMAX, F64> &W = reinterpret_cast<BwdSlots<KMAX, F64> *>(smem)[threadIdx.x >> 5];
