@@ -806,7 +806,7 @@ def run_ours(args):
         if "assign_ms" in v5:
             row("K5 vq_assign (C5)", v5["assign_ms"], 6 * v5["values"],
                 "SURVEY 8(d) C5: 4 B in + 2 B out per value (float64 storage moves 10 B)",
-                "vq_assign_kernel", note="implementation bytes 10/value: frac x 10/6")
+                "vq_assign_win_kernel", note="implementation bytes 10/value: frac x 10/6")
             row("K6 vq_decode (C5)", v5["decode_ms"], 6 * v5["values"],
                 "SURVEY 8(d) C5: 2 B in + 4 B out per value (float64 storage moves 10 B)",
                 "vq_decode_kernel", note="implementation bytes 10/value: frac x 10/6")
