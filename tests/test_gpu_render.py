@@ -198,10 +198,12 @@ def test_depth_sort_fallback_long_runs():
     assert np.array_equal(out.per_pixel_contrib_count, ref["contrib"])
 
 
+@pytest.mark.parametrize("exact", [True, False])
 @pytest.mark.parametrize("W,H", [(1920, 1080), (3840, 2160)])
-def test_large_frames_banded_placement(W, H):
+def test_large_frames_banded_placement(W, H, exact):
     """Tile grids too large for the shared-memory placement tables (1080p: 2
-    bands, 4K: 6 bands) give the reference's lists and image."""
+    bands, 4K: 6 bands) give the reference's lists and image, with the EXACT
+    and the FAST (certified float32) blend."""
     import oracle as O
     from paper_2504_17954_b200 import GaussianGeometry, rasterize_forward
     from paper_2504_17954_b200.synthetic import bench_camera, editable_arrays
@@ -210,12 +212,13 @@ def test_large_frames_banded_placement(W, H):
     cam = bench_camera(W, H, azimuth=0.7)
     colors = np.random.default_rng(11).uniform(0, 1, (n, 3))
     geom = GaussianGeometry(a["mu"], a["q_raw"], a["log_s"], a["o_logit"], a["n_raw"])
-    out, st = rasterize_forward(geom, colors, cam)
+    out, st = rasterize_forward(geom, colors, cam, exact=exact)
     ref = O.rasterize(a["mu"], a["q_raw"], a["log_s"], a["o_logit"], a["n_raw"], colors, cam)
     F = st["frame"]
     assert np.array_equal(F.pairs(), ref["pair_splat"])
     assert np.array_equal(F.tile_ranges.cpu().numpy(), ref["tile_ranges"])
     assert np.array_equal(out.per_pixel_contrib_count, ref["contrib"])
+    assert np.array_equal(F.last_pos.cpu().numpy(), ref["last_pos"])
     assert np.abs(out.color - O.maps(ref)["color"]).max() <= IMG_TOL
 
 
