@@ -139,16 +139,16 @@ vq_assign_kernel(const double *__restrict__ values, int64_t n, const double *__r
     }
 }
 
-// Assign, windowed form (K - 1 <= kVqSmemMids, at least one midpoint): the
-// bucket table (kLutWin) is widened in shared memory to one word per bucket
-// holding its search window [lut[b - 1], lut[b + 2]), and the window is
-// searched by four branch-free binary-lifting steps (windows of <= 15
+// Assign, windowed form (K - 1 <= kVqSmemMids, at least one midpoint): a
+// 32768-bucket table (kLutWin) is widened in shared memory to one word per
+// bucket holding its search window [lut[b - 1], lut[b + 2]), and the window
+// is searched by two branch-free binary-lifting steps (windows of <= 3
 // midpoints: all of the C5 attribute values; wider windows,
 // and the corner cases the float32 bucket index can hit, take the verified
 // full search).  A warp moves 256 contiguous values per step: four 16-byte
 // loads and four 4-byte stores (two indices each) per lane.
-constexpr int kWinSteps = 4;
-constexpr int kLutWin = 8192;  // buckets of the windowed search (32 KB of windows)
+constexpr int kWinSteps = 2;
+constexpr int kLutWin = 32768;  // buckets of the windowed search (128 KB of windows)
 
 template <int NB>
 __device__ __forceinline__ int vq_pos_win(const double *mid, const uint32_t *win, int nm, double v,
@@ -176,12 +176,12 @@ __device__ __forceinline__ int vq_pos_win(const double *mid, const uint32_t *win
     return pos;
 }
 
-constexpr int kWinThreads = 512;  // larger CTAs: more warps per SM under the 64 KB of tables
+constexpr int kWinThreads = 1024;  // one 32-warp CTA per SM under the 160 KB of tables
 constexpr int kWinR = 2;          // 16-byte value loads per lane per step
 constexpr int kWinTile = 64 * kWinR;  // values per warp per step
 
 template <int NB>
-__global__ void __launch_bounds__(kWinThreads, 3)
+__global__ void __launch_bounds__(kWinThreads, 1)
 vq_assign_win_kernel(const double *__restrict__ values, int64_t n, const double *__restrict__ cents,
                      int k, const uint16_t *__restrict__ lut, const double *__restrict__ params,
                      uint16_t *__restrict__ out) {
