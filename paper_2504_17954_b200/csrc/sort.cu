@@ -551,32 +551,62 @@ pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
         hist[(int64_t)blockIdx.x * C.ntiles + tb + t] = (uint32_t)D[(t / C.ntx) * w1 + t % C.ntx];
 }
 
-// Per-tile exclusive scan of the per-block pair counts hist[block][tile]:
-// thread (tile t, chunk c) scans blocks [c * bpc, (c + 1) * bpc) in place
-// (coalesced over tiles) and leaves the chunk total in ctot[c][t]; the
-// kernel's last block to finish scans the chunk totals per tile (ctot becomes
-// the chunk offsets; pair_place adds both), then writes tile_ranges =
-// exclusive scan of the tile totals (P = their sum, ranges clamped to the
-// pair capacity so an overflowed frame never makes K3/K4 read past
-// pair_splat), the optional heaviest-first tile schedule for K3/K4 (a
-// 64-bucket counting sort of the tile pair counts; scheduling only), and
-// re-arms the depth min/max words that K1 of the next frame reduces into.
+// Per-tile exclusive scan of the per-block pair counts hist[block][tile], in
+// place.  A CTA owns 32 consecutive tiles (lane = tile) and splits the blocks
+// into 32 groups (warp = group): each thread sums its group's counts
+// (coalesced 128-byte rows), the CTA scans the 32 group sums of each tile in
+// shared memory, and each thread rewrites its group's counts as offsets inside
+// the tile.  The kernel's last block scans the tile totals into tile_ranges
+// (P = their sum, ranges clamped to the pair capacity so an overflowed frame
+// never makes K3/K4 read past pair_splat), writes the optional heaviest-first
+// tile schedule for K3/K4 (a 64-bucket counting sort of the tile pair counts;
+// scheduling only), and re-arms the depth min/max words that K1 of the next
+// frame reduces into.
 constexpr int kOrderBuckets = 64;
 
 constexpr int kScanThreads = 1024;
-constexpr int kScanChunks = 16;  // tile scan: block chunks per tile
-constexpr int kScanWarps = kScanThreads / 32;
+constexpr int kScanGroups = kScanThreads / 32;  // block groups per tile column
 
 __global__ void __launch_bounds__(kScanThreads)
-tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, int bpc, uint32_t *ctot,
-                 uint32_t *totals, uint32_t *done, int32_t *ranges, uint32_t cap, int32_t *n_pairs,
-                 int32_t *order, unsigned long long *mm) {
-    const int t = blockIdx.x * kScanThreads + threadIdx.x;
-    const int c = blockIdx.y;
+tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, uint32_t *totals, uint32_t *done,
+                 int32_t *ranges, uint32_t cap, int32_t *n_pairs, int32_t *order,
+                 unsigned long long *mm) {
+    __shared__ uint32_t s_grp[kScanGroups][33];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int t = blockIdx.x * 32 + lane;
+    const int bpg = (nblocks + kScanGroups - 1) / kScanGroups;
+    const int b0 = min(warp * bpg, nblocks), b1 = min(b0 + bpg, nblocks);
+    uint32_t sum = 0;
     if (t < ntiles) {
-        const int b0 = c * bpc, b1 = min(b0 + bpc, nblocks);
-        uint32_t run = 0;
-        for (int bb = b0; bb < b1; bb += 8) {  // 8 independent loads, then the scan
+        for (int bb = b0; bb < b1; bb += 8) {  // 8 independent loads per round
+            uint32_t v[8];
+#pragma unroll
+            for (int q = 0; q < 8; ++q) v[q] = bb + q < b1 ? hist[(int64_t)(bb + q) * ntiles + t] : 0u;
+#pragma unroll
+            for (int q = 0; q < 8; ++q) sum += v[q];
+        }
+    }
+    s_grp[warp][lane] = sum;
+    __syncthreads();
+    {  // warp w scans tile w's group sums (lane = group; padded rows: no conflicts)
+        const uint32_t v = s_grp[lane][warp];
+        uint32_t x = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const uint32_t y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        s_grp[lane][warp] = x - v;
+        const int tw = blockIdx.x * 32 + warp;
+        if (lane == 31 && tw < ntiles) {
+            totals[tw] = x;
+            __threadfence();  // the totals are read by the last block
+        }
+    }
+    __syncthreads();
+    if (t < ntiles) {
+        uint32_t run = s_grp[warp][lane];
+        for (int bb = b0; bb < b1; bb += 8) {
             uint32_t v[8];
 #pragma unroll
             for (int q = 0; q < 8; ++q) v[q] = bb + q < b1 ? hist[(int64_t)(bb + q) * ntiles + t] : 0u;
@@ -586,36 +616,17 @@ tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, int bpc, uint32_t *cto
                 run += v[q];
             }
         }
-        ctot[(int64_t)c * ntiles + t] = run;
     }
     __shared__ bool s_last;
-    __threadfence();
-    __syncthreads();
-    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x * gridDim.y - 1;
+    if (threadIdx.x == 0) s_last = atomicAdd(done, 1u) == gridDim.x - 1;
     __syncthreads();
     if (!s_last) return;
     __threadfence();
-    const int nch = gridDim.y;
-    for (int tt = threadIdx.x; tt < ntiles; tt += kScanThreads) {
-        uint32_t v[kScanChunks];
-#pragma unroll
-        for (int cc = 0; cc < kScanChunks; ++cc)
-            v[cc] = cc < nch ? __ldcg(ctot + (int64_t)cc * ntiles + tt) : 0u;
-        uint32_t run = 0;
-#pragma unroll
-        for (int cc = 0; cc < kScanChunks; ++cc) {
-            if (cc < nch) ctot[(int64_t)cc * ntiles + tt] = run;
-            run += v[cc];
-        }
-        totals[tt] = run;
-    }
-    __syncthreads();
     __shared__ uint32_t s_warp[32];
     uint64_t carry = 0;
-    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     for (int base = 0; base < ntiles; base += kScanThreads) {
         const int i = base + threadIdx.x;
-        const uint32_t v = i < ntiles ? totals[i] : 0;
+        const uint32_t v = i < ntiles ? __ldcg(totals + i) : 0;
         uint32_t x = v;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -657,28 +668,43 @@ tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, int bpc, uint32_t *cto
         const int b = (int)(2.0f * __log2f((float)cnt + 1.0f));
         return kOrderBuckets - 1 - (b < kOrderBuckets - 1 ? b : kOrderBuckets - 1);
     };
-    for (int t = threadIdx.x; t < ntiles; t += kScanThreads)
-        atomicAdd(&s_hist[bucket(ranges[t + 1] - ranges[t])], 1);
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        int run = 0;
-        for (int b = 0; b < kOrderBuckets; ++b) {
-            const int c = s_hist[b];
-            s_hist[b] = run;
-            run += c;
-        }
+    // warp-aggregated: lanes with equal buckets add once (the counts cluster)
+    const uint32_t lt = lanemask_lt();
+    for (int t = threadIdx.x; t < ntiles; t += kScanThreads) {
+        const int b = bucket(ranges[t + 1] - ranges[t]);
+        const uint32_t peers = __match_any_sync(__activemask(), b);
+        if (lane == __ffs(peers) - 1) atomicAdd(&s_hist[b], __popc(peers));
     }
     __syncthreads();
-    for (int t = threadIdx.x; t < ntiles; t += kScanThreads)
-        order[atomicAdd(&s_hist[bucket(ranges[t + 1] - ranges[t])], 1)] = t;
+    if (warp == 0) {  // exclusive scan of the 64 buckets, two per lane
+        const int c0 = s_hist[2 * lane], c1 = s_hist[2 * lane + 1];
+        int x = c0 + c1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const int ex = x - c0 - c1;
+        s_hist[2 * lane] = ex;
+        s_hist[2 * lane + 1] = ex + c0;
+    }
+    __syncthreads();
+    for (int t = threadIdx.x; t < ntiles; t += kScanThreads) {
+        const int b = bucket(ranges[t + 1] - ranges[t]);
+        const uint32_t peers = __match_any_sync(__activemask(), b);
+        const int leader = __ffs(peers) - 1;
+        int base = 0;
+        if (lane == leader) base = atomicAdd(&s_hist[b], __popc(peers));
+        base = __shfl_sync(peers, base, leader);
+        order[base + __popc(peers & lt)] = t;
+    }
 }
 
 // stable placement: warp w of block b owns ranks [b*2048 + w*256, +256).
 // Per-warp tile counts come from per-warp 2-D difference arrays; the pairs
 // are expanded once, ranked within the warp by match_any and written.
 __global__ void __launch_bounds__(kThreads)
-pair_place_kernel(PairCtx C, const uint32_t *hist, const uint32_t *ctot, int bpc,
-                  const int32_t *ranges, int32_t *pair_splat, int W, int H) {
+pair_place_kernel(PairCtx C, const uint32_t *hist, const int32_t *ranges, int32_t *pair_splat, int W, int H) {
     extern __shared__ int smem_i32[];
     const int w1 = C.ntx + 1, h1 = C.bh + 1, cells = w1 * h1;
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -737,9 +763,7 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, const uint32_t *ctot, int bpc
             smem_i32[w * cells + cell] = run;
             run += c;
         }
-        s_base[cell] = run ? (uint32_t)ranges[t] + hist[(int64_t)blockIdx.x * C.ntiles + t] +
-                                 ctot[(int64_t)(blockIdx.x / bpc) * C.ntiles + t]
-                           : 0u;
+        s_base[cell] = run ? (uint32_t)ranges[t] + hist[(int64_t)blockIdx.x * C.ntiles + t] : 0u;
     }
     __syncthreads();
     // phase 3: expand once, place (and cull-flag) every pair
@@ -807,7 +831,7 @@ Plan plan(int64_t n, int64_t cap, int32_t ntiles) {
         al(4),                                                   // 6 (unused)
         al(4),                                                   // 7 (unused)
         al(L.ctrl_bytes),                                        // 8 control block
-        al(4 * (size_t)kScanChunks * ntiles),                    // 9 tile-scan chunk totals
+        al(4),                                                   // 9 (unused)
         al(4 * (size_t)ntiles * (L.nbp + 1)),                    // 10 pair tile hist
         al(4 * (size_t)(ntiles + 1)),                            // 11 tile totals
         al(16),                                                  // 12 minmax (keys supplied directly)
@@ -940,17 +964,14 @@ extern "C" int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key,
         C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
         pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
     }
-    const int nch = nbp < kScanChunks ? nbp : kScanChunks;
-    const int bpc = (nbp + nch - 1) / nch;
-    uint32_t *ctot = (uint32_t *)(ws + L.off[9]);
-    tile_scan_kernel<<<dim3((ntiles + kScanThreads - 1) / kScanThreads, nch), kScanThreads, 0, st>>>(
-        phist, ntiles, nbp, bpc, ctot, ttot, done_tiles, tile_ranges, (uint32_t)pair_capacity,
-        n_pairs, tile_order, depth_minmax);
+    tile_scan_kernel<<<(ntiles + 31) / 32, kScanThreads, 0, st>>>(
+        phist, ntiles, nbp, ttot, done_tiles, tile_ranges, (uint32_t)pair_capacity, n_pairs,
+        tile_order, depth_minmax);
     for (int y0 = 0; y0 < nty; y0 += band_rows) {
         C.ty_lo = y0;
         C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
-        pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, ctot, bpc, tile_ranges,
-                                                           pair_splat, width, height);
+        pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, tile_ranges, pair_splat,
+                                                           width, height);
     }
     return ivr::check_launch("ivr_bin_sort");
 }
