@@ -1,5 +1,6 @@
 // C-ABI plumbing: version, thread-local error strings, launch checks.
 #include <stdio.h>
+#include <stdlib.h>
 #include <string.h>
 
 #include "ivr_common.cuh"
@@ -9,6 +10,14 @@ thread_local char g_err[512] = "";
 }
 
 namespace ivr {
+int pdl_level() {
+    static const int lvl = [] {
+        const char *e = getenv("IVR_PDL");
+        return e && e[0] >= '0' && e[0] <= '9' ? e[0] - '0' : 1;
+    }();
+    return lvl;
+}
+
 void set_error(const char *msg) {
     strncpy(g_err, msg, sizeof(g_err) - 1);
     g_err[sizeof(g_err) - 1] = 0;

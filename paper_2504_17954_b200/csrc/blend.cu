@@ -749,6 +749,7 @@ constexpr bool kStaged = MODE == kModeFast && (F64 ? KMAX <= 4 : KMAX <= 16);
 template <int KMAX, bool F64, int MODE>
 __global__ void __launch_bounds__(kBlendThreads, (KMAX <= 4 && !F64) ? 4 : 3)
 blend_fwd_kernel(BlendArgs A) {
+    pdl_begin();
     extern __shared__ __align__(16) unsigned char smem[];
     using Slots = WarpSlots<KMAX, F64, kModeExact>;  // EXACT layout also serves FAST
     // per-warp region: WarpSlots, or (staged FAST walk) the StageSlots ring
@@ -861,7 +862,7 @@ int launch_blend(const BlendArgs &A, int ntiles, cudaStream_t st) {
     // C3 forward 0.539 -> 0.533 ms; 1-warp CTAs: K3 +4%)
     constexpr int wpc = kCtaWarps;
     const int cpt = (kBlendThreads / 32) / wpc;
-    fn<<<ntiles * cpt, 32 * wpc, (sm / (kBlendThreads / 32)) * wpc, st>>>(A);
+    launch<3>(fn, ntiles * cpt, 32 * wpc, (sm / (kBlendThreads / 32)) * wpc, st, A);
     return check_launch("blend_fwd_kernel");
 }
 

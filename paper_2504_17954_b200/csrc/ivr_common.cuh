@@ -9,6 +9,8 @@
 #include <cuda_runtime.h>
 #include <stdint.h>
 
+#include <utility>
+
 #include "../../include/ivrgs.h"
 
 namespace ivr {
@@ -61,6 +63,48 @@ __device__ __forceinline__ uint32_t lanemask_lt() {
     uint32_t m;
     asm volatile("mov.u32 %0, %%lanemask_lt;" : "=r"(m));
     return m;
+}
+
+// Programmatic dependent launch (sm_90+).  A kernel started by `launch`
+// below may be scheduled while its stream predecessor drains; pdl_begin()
+// first waits for that predecessor's completion and memory flush (so nothing
+// before it may touch global memory), then lets the NEXT kernel of the stream
+// be scheduled onto SMs this grid's retiring CTAs free.  Without the launch
+// attribute both instructions are no-ops.
+__device__ __forceinline__ void pdl_begin() {
+    asm volatile("griddepcontrol.wait;" ::: "memory");
+    asm volatile("griddepcontrol.launch_dependents;" ::: "memory");
+}
+
+// IVR_PDL: 0 off; 1 (default) K2's chain outside graph capture; 2 K2's chain
+// always; 3 also K1 and K3.  Inside a captured graph the programmatic edges
+// measured neutral for the isolated C2 frame and -3% for the 6-slot frame
+// stream (CTAs waiting at griddepcontrol.wait hold SM slots other frames
+// could use); eager launches gain ~13 us of K2 per frame.
+int pdl_level();
+
+// kernel<<<grid, block, smem, stream>>>(args...) with the programmatic
+// stream-serialisation attribute when IVR_PDL allows it for LEVEL
+template <int LEVEL = 1, typename... P, typename... A>
+inline cudaError_t launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem,
+                          cudaStream_t st, A &&...args) {
+    const int lvl = pdl_level();
+    bool pdl = lvl >= LEVEL && lvl > 0;
+    if (pdl && lvl == 1) {
+        cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
+        pdl = cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+    }
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = st;
+    cudaLaunchAttribute at[1];
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = 1;
+    cfg.attrs = at;
+    cfg.numAttrs = pdl ? 1 : 0;
+    return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
 }
 
 }  // namespace ivr

@@ -162,6 +162,7 @@ __global__ void __launch_bounds__(kK1Threads)
 preprocess_kernel(ivr_gaussians G, ivr_shading S, int has_shading, ivr_edits E, int has_edits,
                   ivr_frame_params Pv, const ivr_frame_params *__restrict__ Pd, ivr_layout L,
                   ivr_proj_out O, int f64_mode) {
+    pdl_begin();
     __shared__ ivr_frame_params sp;
     stage_params(Pd ? Pd : &Pv, sp);
     const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -312,8 +313,9 @@ extern "C" int ivr_preprocess_fwd(const ivr_gaussians *g, const ivr_shading *sha
     const int threads = ivr::kK1Threads;
     const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
     ivr_frame_params P = ivr::params_from(*cam, shading, edits);
-    ivr::preprocess_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
-        *g, S, shading != nullptr, E, edits != nullptr, P, nullptr, *layout, *out, f64_mode);
+    ivr::launch<3>(ivr::preprocess_kernel, blocks, threads, 0, (cudaStream_t)stream, *g, S,
+                (int)(shading != nullptr), E, (int)(edits != nullptr), P,
+                (const ivr_frame_params *)nullptr, *layout, *out, (int)f64_mode);
     return ivr::check_launch("preprocess_kernel");
 }
 
@@ -342,8 +344,9 @@ extern "C" int ivr_preprocess_fwd_params(const ivr_gaussians *g, const ivr_shadi
     ivr_frame_params Pv{};
     Pv.cam.width = width;
     Pv.cam.height = height;
-    ivr::preprocess_kernel<<<blocks, threads, 0, (cudaStream_t)stream>>>(
-        *g, S, shading != nullptr, E, edits != nullptr, Pv, params, *layout, *out, f64_mode);
+    ivr::launch<3>(ivr::preprocess_kernel, blocks, threads, 0, (cudaStream_t)stream, *g, S,
+                (int)(shading != nullptr), E, (int)(edits != nullptr), Pv, params, *layout, *out,
+                (int)f64_mode);
     return ivr::check_launch("preprocess_kernel(params)");
 }
 

@@ -134,6 +134,7 @@ minmax_kernel(const uint64_t *keys, int64_t n, unsigned long long *mm /* [min, m
 __global__ void __launch_bounds__(kThreads)
 bucket_count_kernel(const uint64_t *full, int64_t n, const unsigned long long *mm, int vbits,
                     uint32_t *ck, uint32_t *counts) {
+    pdl_begin();
     const unsigned long long lo = mm[0], hi = mm[1];
     const unsigned long long range = hi >= lo ? hi - lo : 0ull;
     const int bits = range ? 64 - __clzll((long long)range) : 0;
@@ -163,6 +164,7 @@ bucket_count_kernel(const uint64_t *full, int64_t n, const unsigned long long *m
 // c starts at boff[c >> 12] + counts[c]).
 __global__ void __launch_bounds__(kThreads)
 bucket_scan_kernel(uint32_t *counts, int64_t m, uint32_t *boff, uint32_t *done) {
+    pdl_begin();
     __shared__ uint32_t s_warp[kWarps];
     __shared__ bool s_last;
     __shared__ uint32_t s_c[kChunk + kChunk / 32];  // padded: conflict-free row reads
@@ -219,6 +221,7 @@ bucket_scan_kernel(uint32_t *counts, int64_t m, uint32_t *boff, uint32_t *done) 
 __global__ void __launch_bounds__(kThreads)
 bucket_scatter_kernel(const uint32_t *ck, int64_t n, uint32_t *cursor, const uint32_t *boff,
                       uint32_t *idx) {
+    pdl_begin();
     const int64_t base = (int64_t)blockIdx.x * kChunk;
     uint32_t c[kItems];
 #pragma unroll
@@ -342,6 +345,7 @@ __global__ void __launch_bounds__(kFixThreads)
 fixup_buckets_kernel(const uint32_t *end, const uint32_t *boff, uint32_t nb, uint32_t *idx,
                      int64_t n, const uint64_t *full, int32_t *need_full, uint32_t *done,
                      uint64_t *fkA, uint64_t *fkB, uint32_t *vscratch) {
+    pdl_begin();
     bool flagged = false;
     const int64_t c0 = ((int64_t)blockIdx.x * kFixThreads + threadIdx.x) * kFixPer;
     uint32_t ends[kFixPer + 1];
@@ -523,6 +527,7 @@ pair_hist_kernel(PairCtx C, uint32_t *hist, int nblocks) {
     int *D = smem_i32;
     for (int i = threadIdx.x; i < w1 * h1; i += kThreads) D[i] = 0;
     __syncthreads();
+    pdl_begin();
     const int64_t r0 = (int64_t)blockIdx.x * kRanksPerBlock;
     // the thread's 8 ranks: rank loads together, then count and rectangle
     // loads together (K1 writes a rectangle for every splat)
@@ -571,6 +576,7 @@ __global__ void __launch_bounds__(kScanThreads)
 tile_scan_kernel(uint32_t *hist, int ntiles, int nblocks, uint32_t *totals, uint32_t *done,
                  int32_t *ranges, uint32_t cap, int32_t *n_pairs, int32_t *order,
                  unsigned long long *mm) {
+    pdl_begin();
     __shared__ uint32_t s_grp[kScanGroups][33];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int t = blockIdx.x * 32 + lane;
@@ -710,6 +716,7 @@ pair_place_kernel(PairCtx C, const uint32_t *hist, const int32_t *ranges, int32_
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     for (int i = tid; i < kWarps * cells; i += kThreads) smem_i32[i] = 0;
     __syncthreads();
+    pdl_begin();
     int *Dw = smem_i32 + warp * cells;
     const uint32_t lt = lanemask_lt();
     const int64_t rb = (int64_t)blockIdx.x * kRanksPerBlock + (int64_t)warp * kRanksPerWarp;
@@ -931,14 +938,14 @@ extern "C" int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key,
         gb = gb < 1 ? 1 : (gb > 1184 ? 1184 : gb);
         minmax_kernel<<<gb, kThreads, 0, st>>>(depth_key, n, mm);
     }
-    bucket_count_kernel<<<nbk, kThreads, 0, st>>>(depth_key, n, mm, L.vbits, ck, bcount);
-    bucket_scan_kernel<<<(int)L.nscan, kThreads, 0, st>>>(bcount, L.nbuckets, sstatus, vctr);
-    bucket_scatter_kernel<<<nbk, kThreads, 0, st>>>(ck, n, bcount, sstatus, ord);
+    ivr::launch(bucket_count_kernel, nbk, kThreads, 0, st, depth_key, n, mm, L.vbits, ck, bcount);
+    ivr::launch(bucket_scan_kernel, (int)L.nscan, kThreads, 0, st, bcount, L.nbuckets, sstatus, vctr);
+    ivr::launch(bucket_scatter_kernel, nbk, kThreads, 0, st, ck, n, bcount, sstatus, ord);
     const uint32_t nb_vis = (uint32_t)(L.nbuckets - 1);
     const int64_t fix_threads = (nb_vis + kFixPer - 1) / kFixPer;
-    fixup_buckets_kernel<<<(int)((fix_threads + kFixThreads - 1) / kFixThreads), kFixThreads, 0,
-                           st>>>(bcount, sstatus, nb_vis, ord, n, depth_key, need_full, done_fix,
-                                 fkA, fkB, vscratch);
+    ivr::launch(fixup_buckets_kernel, (int)((fix_threads + kFixThreads - 1) / kFixThreads), kFixThreads,
+           0, st, bcount, sstatus, nb_vis, ord, n, depth_key, need_full, done_fix, fkA, fkB,
+           vscratch);
     // ---- 2. counting placement by tile (+ optional tile cull flag); the
     // tile scan's last block writes the ranges, P = n_pairs and the schedule
     PairCtx C{};
@@ -962,16 +969,15 @@ extern "C" int ivr_bin_sort_frame(int64_t n, const uint64_t *depth_key,
     for (int y0 = 0; y0 < nty; y0 += band_rows) {  // one band unless the grid is too large
         C.ty_lo = y0;
         C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
-        pair_hist_kernel<<<nbp, kThreads, sm_hist, st>>>(C, phist, nbp);
+        ivr::launch(pair_hist_kernel, nbp, kThreads, sm_hist, st, C, phist, nbp);
     }
-    tile_scan_kernel<<<(ntiles + 31) / 32, kScanThreads, 0, st>>>(
-        phist, ntiles, nbp, ttot, done_tiles, tile_ranges, (uint32_t)pair_capacity, n_pairs,
-        tile_order, depth_minmax);
+    ivr::launch(tile_scan_kernel, (ntiles + 31) / 32, kScanThreads, 0, st, phist, ntiles, nbp, ttot,
+           done_tiles, tile_ranges, (uint32_t)pair_capacity, n_pairs, tile_order, depth_minmax);
     for (int y0 = 0; y0 < nty; y0 += band_rows) {
         C.ty_lo = y0;
         C.bh = y0 + band_rows <= nty ? band_rows : nty - y0;
-        pair_place_kernel<<<nbp, kThreads, sm_place, st>>>(C, phist, tile_ranges, pair_splat,
-                                                           width, height);
+        ivr::launch(pair_place_kernel, nbp, kThreads, sm_place, st, C, phist, tile_ranges, pair_splat,
+               width, height);
     }
     return ivr::check_launch("ivr_bin_sort");
 }
