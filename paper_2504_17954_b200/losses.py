@@ -108,8 +108,9 @@ def _photometric_frame_dev(frame, cols, y, a, b, with_ssim):
     nc = len(cols)
     if any(not 0 <= int(c) < k for c in cols):
         raise ShapeMismatch(f"columns {list(cols)} outside the frame's {k} channels")
-    if tuple(y.shape) != (h, w, nc):
-        raise ShapeMismatch(f"prediction {(h, w, nc)} vs ground truth {tuple(y.shape)}")
+    if tuple(y.shape) != (h, w, nc) or y.dtype != torch.float64:
+        raise ShapeMismatch(f"prediction {(h, w, nc)} vs ground truth {y.dtype} "
+                            f"{tuple(y.shape)} (float64 expected)")
     nbytes = L.lib().ivr_photometric_workspace_size(h, w, nc)
     key = (y.device, nbytes)
     ws = _WS.get(key)

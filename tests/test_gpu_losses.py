@@ -118,3 +118,7 @@ def test_photometric_frame_source_is_bit_identical(with_ssim):
         _photometric_frame_dev(frame, cols[:3], gt, 0.3, -0.7, with_ssim)
     with pytest.raises(Exception):
         _photometric_frame_dev(frame, (0, 1, 2, 15), gt, 0.3, -0.7, with_ssim)
+    with pytest.raises(ShapeMismatch):  # float32 ground truth, float64 frame
+        _photometric_frame_dev(frame, cols, gt.float(), 0.3, -0.7, with_ssim)
+    with pytest.raises(ShapeMismatch):
+        _photometric_frame_dev(frame.double(), cols, gt, 0.3, -0.7, with_ssim)
