@@ -8,6 +8,8 @@
 // these kernels are HBM-bound (6 B per value in + out).  Midpoints live in
 // shared memory (K=4096 -> 32 KB) next to a uniform bucket table that cuts
 // the search to ~2 compares per value.
+#include <cooperative_groups.h>
+
 #include "ivr_common.cuh"
 
 namespace ivr {
@@ -554,6 +556,395 @@ seed_pick_kernel(const double *x, int64_t n, const double *d2, const double *bsu
     }
 }
 
+// ----------------------------------------------------------------- k-means++, sorted
+// The same seeding in one persistent cooperative kernel that touches only the
+// samples a new centre can change.  Scalar k-means is 1-D: with the samples
+// in value order (xs = x[order]), a centre c at sorted position p can only
+// lower d2 for samples strictly between the chosen centres next to it
+// (positions L < p < R); every other sample is at least as close to L or R,
+// and fl((x - v)^2) is monotone in |x - v|, so np.minimum would keep its d2
+// bit for bit.  Per step: every CTA makes the same pick from the block sums
+// (d2 in INDEX order, 32 values per block, 64 blocks per super-block, fixed
+// tree order), finds L and R in its shared copy of the chosen positions, and
+// the grid updates d2 over (L, R), marking the blocks it lowers; after a grid
+// barrier the marked blocks and their super-blocks are re-summed; a second
+// barrier ends the step.  The samples updated per step fall off like n / i
+// (~n ln k in all instead of n k), so a step costs two barriers and one pick.
+namespace cg = cooperative_groups;
+
+constexpr int kSsThreads = 512;
+constexpr int kSsBlk = 32;  // d2 values per block sum
+constexpr int kSsSup = 64;  // block sums per super-block sum
+constexpr int kSsMaxK = 32768;  // chosen positions kept in shared memory
+constexpr int kSsPer = 16;      // super-block sums per thread held in registers by the pick
+
+struct SeedSorted {
+    const double *x;
+    const int32_t *order;
+    int64_t n;
+    int k;
+    int64_t first;
+    const double *u;
+    double *centers;
+    double *xs;
+    int32_t *rank;
+    double *d2, *bs1, *bs2;
+    unsigned long long *dmask;
+    int32_t *dlist;   // two lists of super-blocks with lowered blocks (nb2 each, step parity)
+    int32_t *dcount;  // their lengths
+    long long *ctl;   // published pick: j, L, R, step
+    unsigned *arrive;
+    unsigned long long *phase_ns;  // CTA 0's time per phase: pick, wait, update, barrier, re-sum, arrive
+    int64_t nb1;
+    int nb2;
+};
+
+__device__ __forceinline__ double warp_tree_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    return v;
+}
+
+// block sum: the 32 d2 values in index order, added sequentially (one thread)
+__device__ __forceinline__ double ss_block_sum(const SeedSorted &S, int64_t blk) {
+    const int64_t i0 = blk * kSsBlk;
+    double t = 0.0;
+    if (i0 + kSsBlk <= S.n) {
+        const double2 *p = reinterpret_cast<const double2 *>(S.d2 + i0);
+        double2 v[kSsBlk / 2];
+#pragma unroll
+        for (int q = 0; q < kSsBlk / 2; ++q) v[q] = __ldcg(p + q);
+#pragma unroll
+        for (int q = 0; q < kSsBlk / 2; ++q) {
+            t += v[q].x;
+            t += v[q].y;
+        }
+    } else {
+        for (int64_t i = i0; i < S.n; ++i) t += __ldcg(S.d2 + i);
+    }
+    return t;
+}
+
+// inclusive scan over a CTA of kSsThreads threads
+__device__ __forceinline__ double ss_block_scan(double v, double *s_w, double &total) {
+    constexpr int kW = kSsThreads / 32;
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const double y = __shfl_up_sync(0xffffffffu, v, o);
+        if (lane >= o) v += y;
+    }
+    if (lane == 31) s_w[warp] = v;
+    __syncthreads();
+    if (warp == 0) {
+        double w = lane < kW ? s_w[lane] : 0.0;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, w, o);
+            if (lane >= o) w += y;
+        }
+        if (lane < kW) s_w[lane] = w;
+    }
+    __syncthreads();
+    if (warp > 0) v += s_w[warp - 1];
+    total = s_w[kW - 1];
+    __syncthreads();
+    return v;
+}
+
+__device__ __forceinline__ unsigned long long gtimer() {
+    unsigned long long t;
+    asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+    return t;
+}
+
+__device__ __forceinline__ long long ld_volatile_s64(const long long *p) {
+    long long v;
+    asm volatile("ld.volatile.global.s64 %0, [%1];" : "=l"(v) : "l"(p));
+    return v;
+}
+
+__global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ int32_t s_chosen[];  // CTA 0: chosen sorted positions (append order)
+    __shared__ double s_w[32], s_before;
+    __shared__ int s_sup, s_supmass, s_lr[2];
+    __shared__ long long s_ctl[3];
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t gtid = (int64_t)blockIdx.x * kSsThreads + tid;
+    const int64_t gsz = (int64_t)gridDim.x * kSsThreads;
+    const int64_t n = S.n;
+    const int nb2 = S.nb2;
+    const double c0 = S.x[S.first];
+    for (int64_t s = gtid; s < n; s += gsz) {
+        const int32_t i = S.order[s];
+        S.xs[s] = S.x[i];
+        S.rank[i] = (int32_t)s;
+    }
+    for (int64_t i = gtid; i < n; i += gsz) {
+        const double d = S.x[i] - c0;
+        S.d2[i] = d * d;
+    }
+    for (int64_t b = gtid; b < nb2; b += gsz) S.dmask[b] = 0ull;
+    if (gtid == 0) {
+        S.centers[0] = c0;
+        S.dcount[0] = S.dcount[1] = S.dcount[2] = S.dcount[3] = 0;
+        S.ctl[3] = 0;     // published step
+        S.arrive[0] = 0;  // CTAs done re-summing, cumulative
+    }
+    grid.sync();
+    for (int64_t blk = gtid; blk < S.nb1; blk += gsz) S.bs1[blk] = ss_block_sum(S, blk);
+    grid.sync();
+    for (int64_t sp = gtid >> 5; sp < nb2; sp += gsz >> 5) {  // one warp each, as re-summed
+        const int64_t b0 = sp * kSsSup + lane, b1 = b0 + 32;
+        const double a = b0 < S.nb1 ? __ldcg(S.bs1 + b0) : 0.0;
+        const double b = b1 < S.nb1 ? __ldcg(S.bs1 + b1) : 0.0;
+        const double t = warp_tree_sum(a + b);
+        if (lane == 0) S.bs2[sp] = t;
+    }
+    if (blockIdx.x == 0 && tid == 0) s_chosen[0] = __ldcg(S.rank + S.first);
+    grid.sync();
+    int nch = 1;
+    const int per = (nb2 + kSsThreads - 1) / kSsThreads;
+    const int q0 = min(tid * per, nb2), q1 = min(q0 + per, nb2);
+    const bool prof = blockIdx.x == 0 && tid == 0;
+    unsigned long long ph[6] = {0, 0, 0, 0, 0, 0}, t0 = prof ? gtimer() : 0, t1;
+    auto mark = [&](int k) {
+        if (prof) {
+            t1 = gtimer();
+            ph[k] += t1 - t0;
+            t0 = t1;
+        }
+    };
+    for (int step = 1; step < S.k; ++step) {
+        const int buf = step & 1;
+        if (blockIdx.x == 0) {
+            // ---- CTA 0 picks the super-block, block and value (every CTA has
+            // arrived after re-summing the previous step's lowered blocks)
+            if (tid == 0) {
+                s_sup = 0x7fffffff;
+                s_supmass = -1;
+            }
+            // the thread's super-block sums in registers (independent loads;
+            // nb2 <= kSsPer * kSsThreads, i.e. n <= 2^24, in one round)
+            double mine = 0.0;
+            double vq[kSsPer];
+            for (int qb = q0; qb < q1; qb += kSsPer) {
+#pragma unroll
+                for (int u = 0; u < kSsPer; ++u) vq[u] = qb + u < q1 ? __ldcg(S.bs2 + qb + u) : 0.0;
+#pragma unroll
+                for (int u = 0; u < kSsPer; ++u) mine += vq[u];
+            }
+            const bool one = q1 - q0 <= kSsPer;  // vq holds the whole chunk
+            double tot;
+            const double incl = ss_block_scan(mine, s_w, tot);
+            long long j = -1, L = -1, R = n;
+            if (tot > 0.0) {
+                const double target = S.u[step - 1] * tot;
+                double run = incl - mine, bhit = 0.0, blast = 0.0;
+                int lastm = -1, hitq = 0x7fffffff;
+                for (int qb = q0; qb < q1; qb += kSsPer) {
+                    if (!one) {
+#pragma unroll
+                        for (int u = 0; u < kSsPer; ++u)
+                            vq[u] = qb + u < q1 ? __ldcg(S.bs2 + qb + u) : 0.0;
+                    }
+#pragma unroll
+                    for (int u = 0; u < kSsPer; ++u) {
+                        const int q = qb + u;
+                        if (q < q1) {
+                            const double v = vq[u];
+                            if (v > 0.0) {
+                                lastm = q;
+                                blast = run;
+                            }
+                            if (hitq == 0x7fffffff && run + v > target) {
+                                hitq = q;
+                                bhit = run;
+                            }
+                            run += v;
+                        }
+                    }
+                }
+                if (hitq != 0x7fffffff) atomicMin(&s_sup, hitq);
+                if (lastm >= 0) atomicMax(&s_supmass, lastm);
+                __syncthreads();
+                // the cumulative sum before the chosen super-block, from its owner
+                const bool fb = s_sup == 0x7fffffff;  // rounding: the last one with mass
+                if (fb ? (lastm >= 0 && lastm == s_supmass) : hitq == s_sup) s_before = fb ? blast : bhit;
+                __syncthreads();
+                const int sup = !fb ? s_sup : (s_supmass >= 0 ? s_supmass : nb2 - 1);
+                const double before = s_before;
+                if (tid < 32) {
+                    // block inside the super-block: lane l holds blocks 2l, 2l + 1
+                    const int64_t bb = (int64_t)sup * kSsSup + 2 * lane;
+                    const double v0 = bb < S.nb1 ? __ldcg(S.bs1 + bb) : 0.0;
+                    const double v1 = bb + 1 < S.nb1 ? __ldcg(S.bs1 + bb + 1) : 0.0;
+                    double x = v0 + v1;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double y = __shfl_up_sync(0xffffffffu, x, o);
+                        if (lane >= o) x += y;
+                    }
+                    const double r0 = before + (x - v0 - v1);
+                    const bool h0 = r0 + v0 > target, h1 = !h0 && r0 + v0 + v1 > target;
+                    const uint32_t hm = __ballot_sync(0xffffffffu, h0 || h1);
+                    int blk;
+                    double before2 = 0.0;
+                    if (hm) {
+                        const int l = __ffs(hm) - 1;
+                        const int sel = __shfl_sync(0xffffffffu, h0 ? 0 : 1, l);
+                        blk = 2 * l + sel;
+                        before2 = __shfl_sync(0xffffffffu, sel ? r0 + v0 : r0, l);
+                    } else {  // rounding: the last block with mass
+                        const uint32_t m1 = __ballot_sync(0xffffffffu, v1 > 0.0);
+                        const uint32_t m0 = __ballot_sync(0xffffffffu, v0 > 0.0);
+                        const int l1 = m1 ? 31 - __clz(m1) : -1, l0 = m0 ? 31 - __clz(m0) : -1;
+                        blk = l1 >= 0 && 2 * l1 + 1 > 2 * l0 ? 2 * l1 + 1 : (l0 >= 0 ? 2 * l0 : 0);
+                    }
+                    // value inside the block
+                    const int64_t b1 = (int64_t)sup * kSsSup + blk;
+                    const int64_t i = b1 * kSsBlk + lane;
+                    const double v = i < n ? __ldcg(S.d2 + i) : 0.0;
+                    double xv = v;
+#pragma unroll
+                    for (int o = 1; o < 32; o <<= 1) {
+                        const double y = __shfl_up_sync(0xffffffffu, xv, o);
+                        if (lane >= o) xv += y;
+                    }
+                    const uint32_t vm = __ballot_sync(0xffffffffu, hm && before2 + xv > target);
+                    if (vm) {
+                        j = b1 * kSsBlk + (__ffs(vm) - 1);
+                    } else {  // rounding: the block's last value with mass
+                        const uint32_t mm = __ballot_sync(0xffffffffu, v > 0.0);
+                        j = b1 * kSsBlk + (mm ? 31 - __clz(mm) : 0);
+                    }
+                    if (lane == 0) s_ctl[0] = j;
+                }
+                __syncthreads();
+                j = s_ctl[0];
+                // chosen neighbours L < p < R (positions are distinct: a chosen
+                // sample has d2 = 0 and is never drawn again)
+                const int p = __ldcg(S.rank + j);
+                int l = -1, r = (int)n;
+                for (int q = tid; q < nch; q += kSsThreads) {
+                    const int v = s_chosen[q];
+                    if (v < p && v > l) l = v;
+                    if (v > p && v < r) r = v;
+                }
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) {
+                    l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
+                    r = min(r, __shfl_xor_sync(0xffffffffu, r, o));
+                }
+                if (tid == 0) {
+                    s_lr[0] = -1;
+                    s_lr[1] = (int)n;
+                }
+                __syncthreads();
+                if (lane == 0) {
+                    atomicMax(&s_lr[0], l);
+                    atomicMin(&s_lr[1], r);
+                }
+                __syncthreads();
+                L = s_lr[0];
+                R = s_lr[1];
+                if (tid == 0) s_chosen[nch] = p;
+            }
+            ++nch;
+            if (tid == 0) {  // publish (j = -1: all mass on chosen centres)
+                if (j >= 0) S.centers[step] = S.x[j];
+                S.ctl[0] = j;
+                S.ctl[1] = L;
+                S.ctl[2] = R;
+                __threadfence();
+                atomicExch((unsigned long long *)(S.ctl + 3), (unsigned long long)step);
+            }
+        }
+        mark(0);
+        // ---- every CTA: the published pick
+        if (tid == 0) {
+            while (ld_volatile_s64(S.ctl + 3) < step) {
+            }
+            __threadfence();
+            s_ctl[0] = ld_volatile_s64(S.ctl);
+            s_ctl[1] = ld_volatile_s64(S.ctl + 1);
+            s_ctl[2] = ld_volatile_s64(S.ctl + 2);
+        }
+        __syncthreads();
+        const long long j = s_ctl[0], L = s_ctl[1], R = s_ctl[2];
+        mark(1);
+        if (j < 0) {  // the reference repeats c0 for the remaining centres
+            if (blockIdx.x == 0)
+                for (int q = step + tid; q < S.k; q += kSsThreads) S.centers[q] = c0;
+            return;
+        }
+        const double c = S.x[j];
+        // ---- d2 = min(d2, (x - c)^2) over (L, R); a lowered block is marked
+        // in its super-block's mask, a super-block joins the list once
+        int32_t *slist = S.dlist + buf * nb2;
+        for (int64_t s = L + 1 + gtid; s < R; s += gsz) {
+            const int32_t i = __ldg(S.order + s);
+            const double d = __ldcg(S.xs + s) - c;
+            const double nv = d * d;
+            if (nv < __ldcg(S.d2 + i)) {
+                S.d2[i] = nv;
+                const int64_t blk = i / kSsBlk;
+                const int sp = (int)(blk / kSsSup);
+                const unsigned long long bit = 1ull << (blk % kSsSup);
+                if (!(__ldcg(S.dmask + sp) & bit)) {
+                    const unsigned long long old = atomicOr(S.dmask + sp, bit);
+                    if (old == 0ull) slist[atomicAdd(S.dcount + buf, 1)] = sp;
+                }
+            }
+        }
+        mark(2);
+        grid.sync();
+        mark(3);
+        // ---- re-sum the listed super-blocks, one warp each: lane l owns blocks
+        // l and l + 32 (re-summed from d2 when marked), then the tree sum
+        const int cnt = __ldcg(S.dcount + buf);
+        const int64_t wg = gtid >> 5, nwg = gsz >> 5;
+        bool wrote = false;
+        for (int64_t q = wg; q < cnt; q += nwg) {
+            const int sp = __ldcg(slist + q);
+            const unsigned long long m = __ldcg(S.dmask + sp);
+            const int64_t b0 = (int64_t)sp * kSsSup + lane, b1 = b0 + 32;
+            double a = b0 < S.nb1 ? __ldcg(S.bs1 + b0) : 0.0;
+            double b = b1 < S.nb1 ? __ldcg(S.bs1 + b1) : 0.0;
+            const bool ma = (m >> lane) & 1ull, mb = (m >> (lane + 32)) & 1ull;
+            if (ma) a = ss_block_sum(S, b0);
+            if (mb) b = ss_block_sum(S, b1);
+            if (ma) S.bs1[b0] = a;
+            if (mb) S.bs1[b1] = b;
+            const double t = warp_tree_sum(a + b);
+            if (lane == 0) {
+                S.bs2[sp] = t;
+                S.dmask[sp] = 0ull;
+            }
+            wrote = true;
+        }
+        if (wrote) __threadfence();
+        if (gtid == 0) S.dcount[buf ^ 1] = 0;
+        __syncthreads();
+        mark(4);
+        // ---- arrive; CTA 0 waits for everyone before the next pick
+        if (tid == 0) {
+            atomicAdd(S.arrive, 1u);
+            if (blockIdx.x == 0) {
+                const unsigned want = (unsigned)gridDim.x * (unsigned)step;
+                while (*(volatile unsigned *)S.arrive < want) {
+                }
+                __threadfence();
+            }
+        }
+        __syncthreads();
+        mark(5);
+    }
+    if (prof)
+        for (int q = 0; q < 6; ++q) S.phase_ns[q] = ph[q];
+}
+
 }  // namespace ivr
 
 extern "C" size_t ivr_kmeans_lloyd_workspace_size(int32_t k) {
@@ -688,4 +1079,75 @@ extern "C" int ivr_kmeans_seed(const double *values, int64_t n, int32_t k, int64
         seed_pick_kernel<<<1, kPickThreads, 0, st>>>(values, n, d2, bsum, nb, u, centers, i);
     }
     return check_launch("ivr_kmeans_seed");
+}
+
+extern "C" size_t ivr_kmeans_seed_sorted_workspace_size(int64_t n) {
+    const int64_t m = n < 1 ? 1 : n;
+    const int64_t nb1 = (m + ivr::kSsBlk - 1) / ivr::kSsBlk;
+    const int64_t nb2 = (nb1 + ivr::kSsSup - 1) / ivr::kSsSup;
+    return ((8 * (size_t)m + 255) & ~(size_t)255) * 2 + ((4 * (size_t)m + 255) & ~(size_t)255) +
+           ((8 * (size_t)nb1 + 255) & ~(size_t)255) * 2 + 3 * ((8 * (size_t)nb2 + 255) & ~(size_t)255) +
+           256;
+}
+
+extern "C" int ivr_kmeans_seed_sorted(const double *values, const int32_t *order, int64_t n,
+                                      int32_t k, int64_t first, const double *u, double *centers,
+                                      void *workspace, size_t workspace_bytes,
+                                      ivr_stream_t stream) {
+    using namespace ivr;
+    if (n < 1 || n > 0x7fffffffll || k < 1 || k > kSsMaxK || first < 0 || first >= n || !values ||
+        !order || !centers || (k > 1 && !u) || !workspace ||
+        workspace_bytes < ivr_kmeans_seed_sorted_workspace_size(n)) {
+        set_error("ivr_kmeans_seed_sorted: bad argument");
+        return IVR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    SeedSorted S{};
+    S.x = values;
+    S.order = order;
+    S.n = n;
+    S.k = k;
+    S.first = first;
+    S.u = u;
+    S.centers = centers;
+    S.nb1 = (n + kSsBlk - 1) / kSsBlk;
+    S.nb2 = (int)((S.nb1 + kSsSup - 1) / kSsSup);
+    char *w = (char *)workspace;
+    S.xs = (double *)w;
+    w += al(8 * (size_t)n);
+    S.d2 = (double *)w;
+    w += al(8 * (size_t)n);
+    S.rank = (int32_t *)w;
+    w += al(4 * (size_t)n);
+    S.bs1 = (double *)w;
+    w += al(8 * (size_t)S.nb1);
+    S.bs2 = (double *)w;
+    w += al(8 * (size_t)S.nb2);
+    S.dmask = (unsigned long long *)w;
+    w += al(8 * (size_t)S.nb2);
+    S.dlist = (int32_t *)w;
+    w += al(8 * (size_t)S.nb1 + 8 * (size_t)S.nb2);
+    S.dcount = (int32_t *)w;
+    S.ctl = (long long *)(w + 64);
+    S.arrive = (unsigned *)(w + 128);
+    S.phase_ns = (unsigned long long *)(w + 192);
+    const size_t smem = 4 * (size_t)k;
+    if (smem > 48 * 1024 &&
+        cudaFuncSetAttribute(seed_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                             (int)smem) != cudaSuccess)
+        return check_launch("ivr_kmeans_seed_sorted smem");
+    int dev = 0, sms = 0, per_sm = 0;
+    cudaGetDevice(&dev);
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seed_sorted_kernel, kSsThreads, smem);
+    if (sms < 1 || per_sm < 1) {
+        set_error("ivr_kmeans_seed_sorted: kernel does not fit on an SM");
+        return IVR_ERR_ARG;
+    }
+    void *args[] = {&S};
+    if (cudaLaunchCooperativeKernel((const void *)seed_sorted_kernel, dim3(sms), dim3(kSsThreads),
+                                    args, smem, st) != cudaSuccess)
+        return check_launch("ivr_kmeans_seed_sorted");
+    return check_launch("ivr_kmeans_seed_sorted");
 }

@@ -125,9 +125,10 @@ def kmeans(samples, k, seed=0, restarts=5):
         return distinct.cpu().numpy()
     rng = np.random.default_rng(seed)
     n = samples.size
+    order = _value_order(x)  # shared by the restarts' seedings
     best, best_sse = None, np.inf
     for _ in range(restarts):
-        c = _seed_plusplus(x, k, rng)
+        c = _seed_plusplus(x, k, rng, order)
         c = _lloyd(x, c)
         idx = _assign_idx(x, c)
         sse = float(((x - c[idx]) ** 2).sum())
@@ -137,16 +138,38 @@ def kmeans(samples, k, seed=0, restarts=5):
     return torch.unique(best).cpu().numpy()
 
 
-def _seed_plusplus(x, k, rng):
+SEED_SORTED_MAX_K = 32768
+
+
+def _value_order(x):
+    """int32 permutation sorting x ascending (the value order the sorted
+    seeding walks), or None where that path does not apply."""
+    if x.numel() >= 2 ** 31:
+        return None
+    return torch.argsort(x).to(torch.int32)
+
+
+def _seed_plusplus(x, k, rng, order=None):
     """k-means++ seeding on the device (vq.py:60-72) with the reference's
     random stream: rng.integers for the first centre, then one rng.random()
     per rng.choice(p = d2 / sum d2) -- the first index (in sample order) whose
-    cumulative d2 exceeds u * sum d2.  ivr_kmeans_seed: two kernels per centre
-    (d2 update + block sums, then the pick)."""
+    cumulative d2 exceeds u * sum d2.  ivr_kmeans_seed_sorted (one
+    cooperative kernel; d2 lowered only between the adjacent chosen centres
+    in value order) when k <= 32768 and n < 2^31, else ivr_kmeans_seed (two
+    kernels per centre over every sample)."""
     n = x.numel()
     first = int(rng.integers(n))
     u = torch.from_numpy(rng.random(k - 1)).to(x.device)  # k == 1: no draw, as the reference
     c = torch.empty(k, dtype=torch.float64, device=x.device)
+    if k <= SEED_SORTED_MAX_K and n < 2 ** 31:
+        if order is None:
+            order = _value_order(x)
+        nb = int(L.lib().ivr_kmeans_seed_sorted_workspace_size(n))
+        ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+        L.check(L.lib().ivr_kmeans_seed_sorted(D.ptr(x), D.ptr(order), n, int(k), first, D.ptr(u),
+                                               D.ptr(c), D.ptr(ws), nb, D.stream_handle()),
+                "ivr_kmeans_seed_sorted")
+        return c
     nb = int(L.lib().ivr_kmeans_seed_workspace_size(n))
     ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
     L.check(L.lib().ivr_kmeans_seed(D.ptr(x), n, int(k), first, D.ptr(u), D.ptr(c), D.ptr(ws), nb,

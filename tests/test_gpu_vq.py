@@ -114,3 +114,50 @@ def test_seed_plusplus_follows_the_reference_stream():
         d2 = np.minimum(d2, (x - ref[i]) ** 2)
     got = _seed_plusplus(to_dev(x), k, np.random.default_rng(3)).cpu().numpy()
     assert np.array_equal(got, ref)
+
+
+def _seed_full_pass(x, k, rng):
+    """ivr_kmeans_seed (every sample every step) with the same draws."""
+    import torch
+    from paper_2504_17954_b200 import _lib as L
+    from paper_2504_17954_b200 import device as D
+    n = x.numel()
+    first = int(rng.integers(n))
+    u = torch.from_numpy(rng.random(k - 1)).to(x.device)
+    c = torch.empty(k, dtype=torch.float64, device=x.device)
+    nb = int(L.lib().ivr_kmeans_seed_workspace_size(n))
+    ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+    L.check(L.lib().ivr_kmeans_seed(D.ptr(x), n, int(k), first, D.ptr(u), D.ptr(c), D.ptr(ws), nb,
+                                    D.stream_handle()), "ivr_kmeans_seed")
+    return c.cpu().numpy()
+
+
+@pytest.mark.parametrize("case", ["cubed", "ties", "clusters", "tiny", "exhausted", "large"])
+def test_sorted_seeding_equals_full_pass(case):
+    """ivr_kmeans_seed_sorted (d2 lowered only between the adjacent chosen
+    centres in value order) picks the same centres as the full-pass seeding
+    from the same draws: heavy ties, clustered values, n < one block, more
+    centres than distinct values (the all-mass-chosen fill), 3M values."""
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.vq import _seed_plusplus
+    g = np.random.default_rng(5)
+    k = 256
+    if case == "cubed":
+        x = g.normal(size=200_000) ** 3
+    elif case == "ties":
+        x = g.integers(0, 3000, size=150_000).astype(np.float64) * 0.25
+    elif case == "clusters":
+        x = np.concatenate([g.normal(m, 1e-3, size=40_000) for m in (-5.0, 0.0, 0.1, 7.0)])
+        g.shuffle(x)
+    elif case == "tiny":
+        x, k = g.normal(size=23), 9
+    elif case == "exhausted":
+        x, k = g.integers(0, 40, size=5_000).astype(np.float64), 64
+    else:
+        x, k = g.standard_t(3, size=3_000_000), 1024
+    xd = to_dev(x)
+    got = _seed_plusplus(xd, k, np.random.default_rng(8)).cpu().numpy()
+    ref = _seed_full_pass(xd, k, np.random.default_rng(8))
+    assert np.array_equal(got, ref)
+    if case == "exhausted":  # the remaining centres repeat the first one, as the reference
+        assert len(np.unique(got)) == 40 and np.all(got[40:] == got[0])
