@@ -391,18 +391,22 @@ int ivr_kmeans_seed(const double *values, int64_t n, int32_t k, int64_t first, c
                     double *centers, void *workspace, size_t workspace_bytes,
                     ivr_stream_t stream);
 
-/* The same seeding (same draws, same picks up to float64 summation order) in
- * one cooperative kernel that only revisits the samples a new centre can
- * change: `order` (int32, n < 2^31) sorts `values` ascending (any order of
- * ties); d2 is lowered only between the chosen centres adjacent to the new
- * one in value order (~n ln k updates in all instead of n k), and the pick
- * walks 32-value block sums and 2048-value super-block sums in index order.
- * 1 <= k <= 32768.  Per centre: 14 us at n = 4M, 24 us at 16M (B200; the
- * full-pass ivr_kmeans_seed: 17 / 77 us). */
-size_t ivr_kmeans_seed_sorted_workspace_size(int64_t n);
+/* The same seeding (same draws, same picks up to float64 summation order) for
+ * `restarts` (1..8) independent seedings of the same values in one
+ * cooperative kernel that only revisits the samples a new centre can change:
+ * `order` (int32, n < 2^31) sorts `values` ascending (any order of ties); d2
+ * is lowered only between the chosen centres adjacent to the new one in
+ * value order (~n ln k updates in all instead of n k), and the picks walk
+ * 32-value block sums and 2048-value super-block sums in index order.
+ * Seeding r: first[r] (device int64), draws u[r * (k - 1) ...], centres
+ * centers[r * k ...].  1 <= k <= 32768.  k-means' restarts draw from one
+ * stream but their draws do not depend on the data, so they are all known
+ * up front (vq.kmeans). */
+size_t ivr_kmeans_seed_sorted_workspace_size(int64_t n, int32_t restarts);
 int ivr_kmeans_seed_sorted(const double *values, const int32_t *order, int64_t n, int32_t k,
-                           int64_t first, const double *u, double *centers, void *workspace,
-                           size_t workspace_bytes, ivr_stream_t stream);
+                           int32_t restarts, const int64_t *first, const double *u,
+                           double *centers, void *workspace, size_t workspace_bytes,
+                           ivr_stream_t stream);
 
 /* Compose on the device (scene.py:147-186, gaussians.py:98-106): concatenate
  * n_src (<= 64) row-major float64 arrays of `width` columns (rows[m] rows

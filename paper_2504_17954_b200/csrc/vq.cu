@@ -558,45 +558,51 @@ seed_pick_kernel(const double *x, int64_t n, const double *d2, const double *bsu
 
 // ----------------------------------------------------------------- k-means++, sorted
 // The same seeding in one persistent cooperative kernel that touches only the
-// samples a new centre can change.  Scalar k-means is 1-D: with the samples
-// in value order (xs = x[order]), a centre c at sorted position p can only
-// lower d2 for samples strictly between the chosen centres next to it
-// (positions L < p < R); every other sample is at least as close to L or R,
-// and fl((x - v)^2) is monotone in |x - v|, so np.minimum would keep its d2
-// bit for bit.  Per step: every CTA makes the same pick from the block sums
-// (d2 in INDEX order, 32 values per block, 64 blocks per super-block, fixed
-// tree order), finds L and R in its shared copy of the chosen positions, and
-// the grid updates d2 over (L, R), marking the blocks it lowers; after a grid
-// barrier the marked blocks and their super-blocks are re-summed; a second
-// barrier ends the step.  The samples updated per step fall off like n / i
-// (~n ln k in all instead of n k), so a step costs two barriers and one pick.
+// samples a new centre can change, for up to kSsMaxR independent seedings of
+// the same values at once (k-means' restarts: their draws do not depend on
+// the data, so all of them are known before the first one runs).  Scalar
+// k-means is 1-D: with the samples in value order (xs = x[order]), a centre c
+// at sorted position p can only lower d2 for samples strictly between the
+// chosen centres next to it (positions L < p < R); every other sample is at
+// least as close to L or R, and fl((x - v)^2) is monotone in |x - v|, so
+// np.minimum would keep its d2 bit for bit.  Per step: CTA r picks seeding
+// r's centre from its block sums (d2 in INDEX order: 32 values per block, 64
+// blocks per super-block) and publishes (index, L, R); the grid lowers d2
+// over every seeding's (L, R), marking the lowered blocks; after a grid
+// barrier one warp per marked super-block re-sums its marked blocks and the
+// super-block (fixed order: bit-identical runs), and the CTAs arrive on a
+// counter the picking CTAs wait for.  The samples updated per step fall off
+// like n / i (~n ln k in all instead of n k).
 namespace cg = cooperative_groups;
 
 constexpr int kSsThreads = 512;
-constexpr int kSsBlk = 32;  // d2 values per block sum
-constexpr int kSsSup = 64;  // block sums per super-block sum
+constexpr int kSsBlk = 32;      // d2 values per block sum
+constexpr int kSsSup = 64;      // block sums per super-block sum
 constexpr int kSsMaxK = 32768;  // chosen positions kept in shared memory
 constexpr int kSsPer = 16;      // super-block sums per thread held in registers by the pick
+constexpr int kSsMaxR = 8;      // seedings per launch
 
 struct SeedSorted {
     const double *x;
     const int32_t *order;
     int64_t n;
-    int k;
-    int64_t first;
-    const double *u;
-    double *centers;
+    int k, R;
+    const int64_t *first;  // [R]
+    const double *u;       // [R][k - 1]
+    double *centers;       // [R][k]
     double *xs;
     int32_t *rank;
+    // per seeding r (stride below): d2 [n], block sums [nb1], super-block sums
+    // [nb2], marked-block masks [nb2], two super-block lists [2][nb2] (step
+    // parity), their lengths [2], published pick {j, L, R, step}
     double *d2, *bs1, *bs2;
     unsigned long long *dmask;
-    int32_t *dlist;   // two lists of super-blocks with lowered blocks (nb2 each, step parity)
-    int32_t *dcount;  // their lengths
-    long long *ctl;   // published pick: j, L, R, step
+    int32_t *dlist, *dcount;
+    long long *ctl;
     unsigned *arrive;
     unsigned long long *phase_ns;  // CTA 0's time per phase: pick, wait, update, barrier, re-sum, arrive
-    int64_t nb1;
-    int nb2;
+    int64_t nb1, sd2, sb1;         // d2 / block-sum strides (elements)
+    int nb2, sb2;                  // super-block stride (elements)
 };
 
 __device__ __forceinline__ double warp_tree_sum(double v) {
@@ -606,11 +612,11 @@ __device__ __forceinline__ double warp_tree_sum(double v) {
 }
 
 // block sum: the 32 d2 values in index order, added sequentially (one thread)
-__device__ __forceinline__ double ss_block_sum(const SeedSorted &S, int64_t blk) {
+__device__ __forceinline__ double ss_block_sum(const double *d2, int64_t n, int64_t blk) {
     const int64_t i0 = blk * kSsBlk;
     double t = 0.0;
-    if (i0 + kSsBlk <= S.n) {
-        const double2 *p = reinterpret_cast<const double2 *>(S.d2 + i0);
+    if (i0 + kSsBlk <= n) {
+        const double2 *p = reinterpret_cast<const double2 *>(d2 + i0);
         double2 v[kSsBlk / 2];
 #pragma unroll
         for (int q = 0; q < kSsBlk / 2; ++q) v[q] = __ldcg(p + q);
@@ -620,7 +626,7 @@ __device__ __forceinline__ double ss_block_sum(const SeedSorted &S, int64_t blk)
             t += v[q].y;
         }
     } else {
-        for (int64_t i = i0; i < S.n; ++i) t += __ldcg(S.d2 + i);
+        for (int64_t i = i0; i < n; ++i) t += __ldcg(d2 + i);
     }
     return t;
 }
@@ -664,49 +670,205 @@ __device__ __forceinline__ long long ld_volatile_s64(const long long *p) {
     return v;
 }
 
-__global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S) {
-    cg::grid_group grid = cg::this_grid();
-    extern __shared__ int32_t s_chosen[];  // CTA 0: chosen sorted positions (append order)
+// CTA r's pick for seeding r at `step`: the first index whose cumulative d2
+// (index order) exceeds u * sum d2, and its chosen neighbours L < p < R in
+// value order (j = -1: all mass on chosen centres)
+__device__ void ss_pick(const SeedSorted &S, int r, int step, int32_t *s_chosen, int nch,
+                        long long &j, long long &L, long long &R) {
     __shared__ double s_w[32], s_before;
     __shared__ int s_sup, s_supmass, s_lr[2];
-    __shared__ long long s_ctl[3];
+    __shared__ long long s_j;
+    const int tid = threadIdx.x, lane = tid & 31;
+    const int64_t n = S.n;
+    const int nb2 = S.nb2;
+    const double *d2 = S.d2 + r * S.sd2, *bs1 = S.bs1 + r * S.sb1, *bs2 = S.bs2 + (int64_t)r * S.sb2;
+    const int per = (nb2 + kSsThreads - 1) / kSsThreads;
+    const int q0 = min(tid * per, nb2), q1 = min(q0 + per, nb2);
+    if (tid == 0) {
+        s_sup = 0x7fffffff;
+        s_supmass = -1;
+    }
+    // the thread's super-block sums in registers (independent loads; nb2 <=
+    // kSsPer * kSsThreads, i.e. n <= 2^24, in one round)
+    double mine = 0.0;
+    double vq[kSsPer];
+    for (int qb = q0; qb < q1; qb += kSsPer) {
+#pragma unroll
+        for (int u = 0; u < kSsPer; ++u) vq[u] = qb + u < q1 ? __ldcg(bs2 + qb + u) : 0.0;
+#pragma unroll
+        for (int u = 0; u < kSsPer; ++u) mine += vq[u];
+    }
+    const bool one = q1 - q0 <= kSsPer;  // vq holds the whole chunk
+    double tot;
+    const double incl = ss_block_scan(mine, s_w, tot);
+    j = -1;
+    L = -1;
+    R = n;
+    if (!(tot > 0.0)) return;  // uniform over the CTA
+    const double target = S.u[(int64_t)r * (S.k - 1) + step - 1] * tot;
+    double run = incl - mine, bhit = 0.0, blast = 0.0;
+    int lastm = -1, hitq = 0x7fffffff;
+    for (int qb = q0; qb < q1; qb += kSsPer) {
+        if (!one) {
+#pragma unroll
+            for (int u = 0; u < kSsPer; ++u) vq[u] = qb + u < q1 ? __ldcg(bs2 + qb + u) : 0.0;
+        }
+#pragma unroll
+        for (int u = 0; u < kSsPer; ++u) {
+            const int q = qb + u;
+            if (q < q1) {
+                const double v = vq[u];
+                if (v > 0.0) {
+                    lastm = q;
+                    blast = run;
+                }
+                if (hitq == 0x7fffffff && run + v > target) {
+                    hitq = q;
+                    bhit = run;
+                }
+                run += v;
+            }
+        }
+    }
+    if (hitq != 0x7fffffff) atomicMin(&s_sup, hitq);
+    if (lastm >= 0) atomicMax(&s_supmass, lastm);
+    __syncthreads();
+    // the cumulative sum before the chosen super-block, from its owner
+    const bool fb = s_sup == 0x7fffffff;  // rounding: the last one with mass
+    if (fb ? (lastm >= 0 && lastm == s_supmass) : hitq == s_sup) s_before = fb ? blast : bhit;
+    __syncthreads();
+    const int sup = !fb ? s_sup : (s_supmass >= 0 ? s_supmass : nb2 - 1);
+    const double before = s_before;
+    if (tid < 32) {
+        // block inside the super-block: lane l holds blocks 2l, 2l + 1
+        const int64_t bb = (int64_t)sup * kSsSup + 2 * lane;
+        const double v0 = bb < S.nb1 ? __ldcg(bs1 + bb) : 0.0;
+        const double v1 = bb + 1 < S.nb1 ? __ldcg(bs1 + bb + 1) : 0.0;
+        double x = v0 + v1;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, x, o);
+            if (lane >= o) x += y;
+        }
+        const double r0 = before + (x - v0 - v1);
+        const bool h0 = r0 + v0 > target, h1 = !h0 && r0 + v0 + v1 > target;
+        const uint32_t hm = __ballot_sync(0xffffffffu, h0 || h1);
+        int blk;
+        double before2 = 0.0;
+        if (hm) {
+            const int l = __ffs(hm) - 1;
+            const int sel = __shfl_sync(0xffffffffu, h0 ? 0 : 1, l);
+            blk = 2 * l + sel;
+            before2 = __shfl_sync(0xffffffffu, sel ? r0 + v0 : r0, l);
+        } else {  // rounding: the last block with mass
+            const uint32_t m1 = __ballot_sync(0xffffffffu, v1 > 0.0);
+            const uint32_t m0 = __ballot_sync(0xffffffffu, v0 > 0.0);
+            const int l1 = m1 ? 31 - __clz(m1) : -1, l0 = m0 ? 31 - __clz(m0) : -1;
+            blk = l1 >= 0 && 2 * l1 + 1 > 2 * l0 ? 2 * l1 + 1 : (l0 >= 0 ? 2 * l0 : 0);
+        }
+        // value inside the block
+        const int64_t b1 = (int64_t)sup * kSsSup + blk;
+        const int64_t i = b1 * kSsBlk + lane;
+        const double v = i < n ? __ldcg(d2 + i) : 0.0;
+        double xv = v;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const double y = __shfl_up_sync(0xffffffffu, xv, o);
+            if (lane >= o) xv += y;
+        }
+        const uint32_t vm = __ballot_sync(0xffffffffu, hm && before2 + xv > target);
+        long long jj;
+        if (vm) {
+            jj = b1 * kSsBlk + (__ffs(vm) - 1);
+        } else {  // rounding: the block's last value with mass
+            const uint32_t mm = __ballot_sync(0xffffffffu, v > 0.0);
+            jj = b1 * kSsBlk + (mm ? 31 - __clz(mm) : 0);
+        }
+        if (lane == 0) s_j = jj;
+    }
+    __syncthreads();
+    j = s_j;
+    // chosen neighbours L < p < R (positions are distinct: a chosen sample
+    // has d2 = 0 and is never drawn again)
+    const int p = __ldcg(S.rank + j);
+    int l = -1, rr = (int)n;
+    for (int q = tid; q < nch; q += kSsThreads) {
+        const int v = s_chosen[q];
+        if (v < p && v > l) l = v;
+        if (v > p && v < rr) rr = v;
+    }
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+        l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
+        rr = min(rr, __shfl_xor_sync(0xffffffffu, rr, o));
+    }
+    if (tid == 0) {
+        s_lr[0] = -1;
+        s_lr[1] = (int)n;
+    }
+    __syncthreads();
+    if (lane == 0) {
+        atomicMax(&s_lr[0], l);
+        atomicMin(&s_lr[1], rr);
+    }
+    __syncthreads();
+    L = s_lr[0];
+    R = s_lr[1];
+    if (tid == 0) s_chosen[nch] = p;
+}
+
+__global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S) {
+    cg::grid_group grid = cg::this_grid();
+    extern __shared__ int32_t s_chosen[];  // CTA r < R: seeding r's chosen sorted positions
+    __shared__ long long s_ctl[kSsMaxR][3];
+    __shared__ int64_t s_start[kSsMaxR + 1], s_cst[kSsMaxR + 1];
+    __shared__ bool s_done[kSsMaxR];
     const int tid = threadIdx.x, lane = tid & 31;
     const int64_t gtid = (int64_t)blockIdx.x * kSsThreads + tid;
     const int64_t gsz = (int64_t)gridDim.x * kSsThreads;
     const int64_t n = S.n;
-    const int nb2 = S.nb2;
-    const double c0 = S.x[S.first];
+    const int nb2 = S.nb2, R = S.R;
     for (int64_t s = gtid; s < n; s += gsz) {
         const int32_t i = S.order[s];
         S.xs[s] = S.x[i];
         S.rank[i] = (int32_t)s;
     }
-    for (int64_t i = gtid; i < n; i += gsz) {
-        const double d = S.x[i] - c0;
-        S.d2[i] = d * d;
+    for (int r = 0; r < R; ++r) {
+        const double c0 = S.x[S.first[r]];
+        double *d2 = S.d2 + r * S.sd2;
+        for (int64_t i = gtid; i < n; i += gsz) {
+            const double d = S.x[i] - c0;
+            d2[i] = d * d;
+        }
+        for (int64_t b = gtid; b < nb2; b += gsz) S.dmask[(int64_t)r * S.sb2 + b] = 0ull;
+        if (gtid == 0) {
+            S.centers[(int64_t)r * S.k] = c0;
+            S.dcount[2 * r] = S.dcount[2 * r + 1] = 0;
+            S.ctl[4 * r + 3] = 0;  // published step
+        }
     }
-    for (int64_t b = gtid; b < nb2; b += gsz) S.dmask[b] = 0ull;
-    if (gtid == 0) {
-        S.centers[0] = c0;
-        S.dcount[0] = S.dcount[1] = S.dcount[2] = S.dcount[3] = 0;
-        S.ctl[3] = 0;     // published step
-        S.arrive[0] = 0;  // CTAs done re-summing, cumulative
+    if (gtid == 0) S.arrive[0] = 0;  // CTAs done re-summing, cumulative
+    if (tid < kSsMaxR) s_done[tid] = false;
+    grid.sync();
+    for (int64_t q = gtid; q < (int64_t)R * S.nb1; q += gsz) {
+        const int r = (int)(q / S.nb1);
+        const int64_t blk = q - (int64_t)r * S.nb1;
+        S.bs1[r * S.sb1 + blk] = ss_block_sum(S.d2 + r * S.sd2, n, blk);
     }
     grid.sync();
-    for (int64_t blk = gtid; blk < S.nb1; blk += gsz) S.bs1[blk] = ss_block_sum(S, blk);
-    grid.sync();
-    for (int64_t sp = gtid >> 5; sp < nb2; sp += gsz >> 5) {  // one warp each, as re-summed
+    for (int64_t q = gtid >> 5; q < (int64_t)R * nb2; q += gsz >> 5) {  // one warp each, as re-summed
+        const int r = (int)(q / nb2);
+        const int64_t sp = q - (int64_t)r * nb2;
+        const double *bs1 = S.bs1 + r * S.sb1;
         const int64_t b0 = sp * kSsSup + lane, b1 = b0 + 32;
-        const double a = b0 < S.nb1 ? __ldcg(S.bs1 + b0) : 0.0;
-        const double b = b1 < S.nb1 ? __ldcg(S.bs1 + b1) : 0.0;
+        const double a = b0 < S.nb1 ? __ldcg(bs1 + b0) : 0.0;
+        const double b = b1 < S.nb1 ? __ldcg(bs1 + b1) : 0.0;
         const double t = warp_tree_sum(a + b);
-        if (lane == 0) S.bs2[sp] = t;
+        if (lane == 0) S.bs2[(int64_t)r * S.sb2 + sp] = t;
     }
-    if (blockIdx.x == 0 && tid == 0) s_chosen[0] = __ldcg(S.rank + S.first);
+    if (blockIdx.x < R && tid == 0) s_chosen[0] = __ldcg(S.rank + S.first[blockIdx.x]);
     grid.sync();
     int nch = 1;
-    const int per = (nb2 + kSsThreads - 1) / kSsThreads;
-    const int q0 = min(tid * per, nb2), q1 = min(q0 + per, nb2);
     const bool prof = blockIdx.x == 0 && tid == 0;
     unsigned long long ph[6] = {0, 0, 0, 0, 0, 0}, t0 = prof ? gtimer() : 0, t1;
     auto mark = [&](int k) {
@@ -718,183 +880,83 @@ __global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S
     };
     for (int step = 1; step < S.k; ++step) {
         const int buf = step & 1;
-        if (blockIdx.x == 0) {
-            // ---- CTA 0 picks the super-block, block and value (every CTA has
-            // arrived after re-summing the previous step's lowered blocks)
-            if (tid == 0) {
-                s_sup = 0x7fffffff;
-                s_supmass = -1;
-            }
-            // the thread's super-block sums in registers (independent loads;
-            // nb2 <= kSsPer * kSsThreads, i.e. n <= 2^24, in one round)
-            double mine = 0.0;
-            double vq[kSsPer];
-            for (int qb = q0; qb < q1; qb += kSsPer) {
-#pragma unroll
-                for (int u = 0; u < kSsPer; ++u) vq[u] = qb + u < q1 ? __ldcg(S.bs2 + qb + u) : 0.0;
-#pragma unroll
-                for (int u = 0; u < kSsPer; ++u) mine += vq[u];
-            }
-            const bool one = q1 - q0 <= kSsPer;  // vq holds the whole chunk
-            double tot;
-            const double incl = ss_block_scan(mine, s_w, tot);
-            long long j = -1, L = -1, R = n;
-            if (tot > 0.0) {
-                const double target = S.u[step - 1] * tot;
-                double run = incl - mine, bhit = 0.0, blast = 0.0;
-                int lastm = -1, hitq = 0x7fffffff;
-                for (int qb = q0; qb < q1; qb += kSsPer) {
-                    if (!one) {
-#pragma unroll
-                        for (int u = 0; u < kSsPer; ++u)
-                            vq[u] = qb + u < q1 ? __ldcg(S.bs2 + qb + u) : 0.0;
-                    }
-#pragma unroll
-                    for (int u = 0; u < kSsPer; ++u) {
-                        const int q = qb + u;
-                        if (q < q1) {
-                            const double v = vq[u];
-                            if (v > 0.0) {
-                                lastm = q;
-                                blast = run;
-                            }
-                            if (hitq == 0x7fffffff && run + v > target) {
-                                hitq = q;
-                                bhit = run;
-                            }
-                            run += v;
-                        }
-                    }
-                }
-                if (hitq != 0x7fffffff) atomicMin(&s_sup, hitq);
-                if (lastm >= 0) atomicMax(&s_supmass, lastm);
-                __syncthreads();
-                // the cumulative sum before the chosen super-block, from its owner
-                const bool fb = s_sup == 0x7fffffff;  // rounding: the last one with mass
-                if (fb ? (lastm >= 0 && lastm == s_supmass) : hitq == s_sup) s_before = fb ? blast : bhit;
-                __syncthreads();
-                const int sup = !fb ? s_sup : (s_supmass >= 0 ? s_supmass : nb2 - 1);
-                const double before = s_before;
-                if (tid < 32) {
-                    // block inside the super-block: lane l holds blocks 2l, 2l + 1
-                    const int64_t bb = (int64_t)sup * kSsSup + 2 * lane;
-                    const double v0 = bb < S.nb1 ? __ldcg(S.bs1 + bb) : 0.0;
-                    const double v1 = bb + 1 < S.nb1 ? __ldcg(S.bs1 + bb + 1) : 0.0;
-                    double x = v0 + v1;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const double y = __shfl_up_sync(0xffffffffu, x, o);
-                        if (lane >= o) x += y;
-                    }
-                    const double r0 = before + (x - v0 - v1);
-                    const bool h0 = r0 + v0 > target, h1 = !h0 && r0 + v0 + v1 > target;
-                    const uint32_t hm = __ballot_sync(0xffffffffu, h0 || h1);
-                    int blk;
-                    double before2 = 0.0;
-                    if (hm) {
-                        const int l = __ffs(hm) - 1;
-                        const int sel = __shfl_sync(0xffffffffu, h0 ? 0 : 1, l);
-                        blk = 2 * l + sel;
-                        before2 = __shfl_sync(0xffffffffu, sel ? r0 + v0 : r0, l);
-                    } else {  // rounding: the last block with mass
-                        const uint32_t m1 = __ballot_sync(0xffffffffu, v1 > 0.0);
-                        const uint32_t m0 = __ballot_sync(0xffffffffu, v0 > 0.0);
-                        const int l1 = m1 ? 31 - __clz(m1) : -1, l0 = m0 ? 31 - __clz(m0) : -1;
-                        blk = l1 >= 0 && 2 * l1 + 1 > 2 * l0 ? 2 * l1 + 1 : (l0 >= 0 ? 2 * l0 : 0);
-                    }
-                    // value inside the block
-                    const int64_t b1 = (int64_t)sup * kSsSup + blk;
-                    const int64_t i = b1 * kSsBlk + lane;
-                    const double v = i < n ? __ldcg(S.d2 + i) : 0.0;
-                    double xv = v;
-#pragma unroll
-                    for (int o = 1; o < 32; o <<= 1) {
-                        const double y = __shfl_up_sync(0xffffffffu, xv, o);
-                        if (lane >= o) xv += y;
-                    }
-                    const uint32_t vm = __ballot_sync(0xffffffffu, hm && before2 + xv > target);
-                    if (vm) {
-                        j = b1 * kSsBlk + (__ffs(vm) - 1);
-                    } else {  // rounding: the block's last value with mass
-                        const uint32_t mm = __ballot_sync(0xffffffffu, v > 0.0);
-                        j = b1 * kSsBlk + (mm ? 31 - __clz(mm) : 0);
-                    }
-                    if (lane == 0) s_ctl[0] = j;
-                }
-                __syncthreads();
-                j = s_ctl[0];
-                // chosen neighbours L < p < R (positions are distinct: a chosen
-                // sample has d2 = 0 and is never drawn again)
-                const int p = __ldcg(S.rank + j);
-                int l = -1, r = (int)n;
-                for (int q = tid; q < nch; q += kSsThreads) {
-                    const int v = s_chosen[q];
-                    if (v < p && v > l) l = v;
-                    if (v > p && v < r) r = v;
-                }
-#pragma unroll
-                for (int o = 16; o > 0; o >>= 1) {
-                    l = max(l, __shfl_xor_sync(0xffffffffu, l, o));
-                    r = min(r, __shfl_xor_sync(0xffffffffu, r, o));
-                }
-                if (tid == 0) {
-                    s_lr[0] = -1;
-                    s_lr[1] = (int)n;
-                }
-                __syncthreads();
-                if (lane == 0) {
-                    atomicMax(&s_lr[0], l);
-                    atomicMin(&s_lr[1], r);
-                }
-                __syncthreads();
-                L = s_lr[0];
-                R = s_lr[1];
-                if (tid == 0) s_chosen[nch] = p;
-            }
+        if (blockIdx.x < R) {
+            // ---- CTA r picks seeding r's centre (every CTA has arrived after
+            // re-summing the previous step's marked blocks)
+            const int r = blockIdx.x;
+            long long j = -1, L = -1, Rr = n;
+            if (!s_done[r]) ss_pick(S, r, step, s_chosen, nch, j, L, Rr);
             ++nch;
             if (tid == 0) {  // publish (j = -1: all mass on chosen centres)
-                if (j >= 0) S.centers[step] = S.x[j];
-                S.ctl[0] = j;
-                S.ctl[1] = L;
-                S.ctl[2] = R;
+                if (j >= 0) S.centers[(int64_t)r * S.k + step] = S.x[j];
+                S.ctl[4 * r] = j;
+                S.ctl[4 * r + 1] = L;
+                S.ctl[4 * r + 2] = Rr;
                 __threadfence();
-                atomicExch((unsigned long long *)(S.ctl + 3), (unsigned long long)step);
+                atomicExch((unsigned long long *)(S.ctl + 4 * r + 3), (unsigned long long)step);
             }
         }
         mark(0);
-        // ---- every CTA: the published pick
-        if (tid == 0) {
-            while (ld_volatile_s64(S.ctl + 3) < step) {
+        // ---- every CTA: the published picks
+        if (tid < R) {
+            while (ld_volatile_s64(S.ctl + 4 * tid + 3) < step) {
             }
             __threadfence();
-            s_ctl[0] = ld_volatile_s64(S.ctl);
-            s_ctl[1] = ld_volatile_s64(S.ctl + 1);
-            s_ctl[2] = ld_volatile_s64(S.ctl + 2);
+            s_ctl[tid][0] = ld_volatile_s64(S.ctl + 4 * tid);
+            s_ctl[tid][1] = ld_volatile_s64(S.ctl + 4 * tid + 1);
+            s_ctl[tid][2] = ld_volatile_s64(S.ctl + 4 * tid + 2);
         }
         __syncthreads();
-        const long long j = s_ctl[0], L = s_ctl[1], R = s_ctl[2];
         mark(1);
-        if (j < 0) {  // the reference repeats c0 for the remaining centres
-            if (blockIdx.x == 0)
-                for (int q = step + tid; q < S.k; q += kSsThreads) S.centers[q] = c0;
-            return;
+        if (tid == 0) {  // range offsets of the seedings still running
+            int64_t t = 0;
+            for (int r = 0; r < R; ++r) {
+                s_start[r] = t;
+                if (s_ctl[r][0] >= 0) t += s_ctl[r][2] - s_ctl[r][1] - 1;
+            }
+            s_start[R] = t;
         }
-        const double c = S.x[j];
-        // ---- d2 = min(d2, (x - c)^2) over (L, R); a lowered block is marked
-        // in its super-block's mask, a super-block joins the list once
-        int32_t *slist = S.dlist + buf * nb2;
-        for (int64_t s = L + 1 + gtid; s < R; s += gsz) {
-            const int32_t i = __ldg(S.order + s);
-            const double d = __ldcg(S.xs + s) - c;
-            const double nv = d * d;
-            if (nv < __ldcg(S.d2 + i)) {
-                S.d2[i] = nv;
-                const int64_t blk = i / kSsBlk;
-                const int sp = (int)(blk / kSsSup);
-                const unsigned long long bit = 1ull << (blk % kSsSup);
-                if (!(__ldcg(S.dmask + sp) & bit)) {
-                    const unsigned long long old = atomicOr(S.dmask + sp, bit);
-                    if (old == 0ull) slist[atomicAdd(S.dcount + buf, 1)] = sp;
+        for (int r = 0; r < R; ++r)
+            if (s_ctl[r][0] < 0 && !s_done[r] && blockIdx.x == r) {  // the reference repeats c0
+                const double c0 = S.x[S.first[r]];
+                for (int q = step + tid; q < S.k; q += kSsThreads) S.centers[(int64_t)r * S.k + q] = c0;
+            }
+        bool any = false;
+        for (int r = 0; r < R; ++r) any |= s_ctl[r][0] >= 0;
+        __syncthreads();
+        if (tid < R && s_ctl[tid][0] < 0) s_done[tid] = true;
+        if (!any) return;  // every seeding done (uniform over the grid)
+        const int64_t tot_len = s_start[R];
+        // ---- d2 = min(d2, (x - c)^2) over each seeding's (L, R); a lowered
+        // block is marked in its super-block's mask, which joins the list once
+        {
+            int r = 0;
+            double c = 0.0;
+            int64_t rbeg = -1, rend = -1;
+            for (int64_t g = gtid; g < tot_len; g += gsz) {
+                if (g >= rend) {  // next seeding with a range (empty ranges skipped)
+                    r = 0;
+                    while (s_start[r + 1] <= g) ++r;
+                    rbeg = s_start[r];
+                    rend = s_start[r + 1];
+                    c = S.x[s_ctl[r][0]];
+                }
+                const int64_t s = s_ctl[r][1] + 1 + (g - rbeg);
+                double *d2 = S.d2 + r * S.sd2;
+                const int32_t i = __ldg(S.order + s);
+                const double d = __ldcg(S.xs + s) - c;
+                const double nv = d * d;
+                if (nv < __ldcg(d2 + i)) {
+                    d2[i] = nv;
+                    const int64_t blk = i / kSsBlk;
+                    const int sp = (int)(blk / kSsSup);
+                    unsigned long long *dm = S.dmask + (int64_t)r * S.sb2 + sp;
+                    const unsigned long long bit = 1ull << (blk % kSsSup);
+                    if (!(__ldcg(dm) & bit)) {
+                        const unsigned long long old = atomicOr(dm, bit);
+                        if (old == 0ull)
+                            S.dlist[(int64_t)(2 * r + buf) * nb2 + atomicAdd(S.dcount + 2 * r + buf, 1)] = sp;
+                    }
                 }
             }
         }
@@ -903,35 +965,46 @@ __global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S
         mark(3);
         // ---- re-sum the listed super-blocks, one warp each: lane l owns blocks
         // l and l + 32 (re-summed from d2 when marked), then the tree sum
-        const int cnt = __ldcg(S.dcount + buf);
-        const int64_t wg = gtid >> 5, nwg = gsz >> 5;
-        bool wrote = false;
-        for (int64_t q = wg; q < cnt; q += nwg) {
-            const int sp = __ldcg(slist + q);
-            const unsigned long long m = __ldcg(S.dmask + sp);
-            const int64_t b0 = (int64_t)sp * kSsSup + lane, b1 = b0 + 32;
-            double a = b0 < S.nb1 ? __ldcg(S.bs1 + b0) : 0.0;
-            double b = b1 < S.nb1 ? __ldcg(S.bs1 + b1) : 0.0;
-            const bool ma = (m >> lane) & 1ull, mb = (m >> (lane + 32)) & 1ull;
-            if (ma) a = ss_block_sum(S, b0);
-            if (mb) b = ss_block_sum(S, b1);
-            if (ma) S.bs1[b0] = a;
-            if (mb) S.bs1[b1] = b;
-            const double t = warp_tree_sum(a + b);
-            if (lane == 0) {
-                S.bs2[sp] = t;
-                S.dmask[sp] = 0ull;
+        {
+            if (tid == 0) {
+                s_cst[0] = 0;
+                for (int r = 0; r < R; ++r) s_cst[r + 1] = s_cst[r] + __ldcg(S.dcount + 2 * r + buf);
             }
-            wrote = true;
+            __syncthreads();
+            const int64_t wg = gtid >> 5, nwg = gsz >> 5;
+            bool wrote = false;
+            int r = 0;
+            for (int64_t q = wg; q < s_cst[R]; q += nwg) {
+                while (s_cst[r + 1] <= q) ++r;
+                const int sp = __ldcg(S.dlist + (int64_t)(2 * r + buf) * nb2 + (q - s_cst[r]));
+                unsigned long long *dm = S.dmask + (int64_t)r * S.sb2 + sp;
+                const unsigned long long m = __ldcg(dm);
+                double *bs1 = S.bs1 + r * S.sb1;
+                const double *d2 = S.d2 + r * S.sd2;
+                const int64_t b0 = (int64_t)sp * kSsSup + lane, b1 = b0 + 32;
+                double a = b0 < S.nb1 ? __ldcg(bs1 + b0) : 0.0;
+                double b = b1 < S.nb1 ? __ldcg(bs1 + b1) : 0.0;
+                const bool ma = (m >> lane) & 1ull, mb = (m >> (lane + 32)) & 1ull;
+                if (ma) a = ss_block_sum(d2, n, b0);
+                if (mb) b = ss_block_sum(d2, n, b1);
+                if (ma) bs1[b0] = a;
+                if (mb) bs1[b1] = b;
+                const double t = warp_tree_sum(a + b);
+                if (lane == 0) {
+                    S.bs2[(int64_t)r * S.sb2 + sp] = t;
+                    *dm = 0ull;
+                }
+                wrote = true;
+            }
+            if (wrote) __threadfence();
+            if (gtid < R) S.dcount[2 * gtid + (buf ^ 1)] = 0;
         }
-        if (wrote) __threadfence();
-        if (gtid == 0) S.dcount[buf ^ 1] = 0;
         __syncthreads();
         mark(4);
-        // ---- arrive; CTA 0 waits for everyone before the next pick
+        // ---- arrive; the picking CTAs wait for everyone
         if (tid == 0) {
             atomicAdd(S.arrive, 1u);
-            if (blockIdx.x == 0) {
+            if (blockIdx.x < R) {
                 const unsigned want = (unsigned)gridDim.x * (unsigned)step;
                 while (*(volatile unsigned *)S.arrive < want) {
                 }
@@ -1081,57 +1154,86 @@ extern "C" int ivr_kmeans_seed(const double *values, int64_t n, int32_t k, int64
     return check_launch("ivr_kmeans_seed");
 }
 
-extern "C" size_t ivr_kmeans_seed_sorted_workspace_size(int64_t n) {
-    const int64_t m = n < 1 ? 1 : n;
-    const int64_t nb1 = (m + ivr::kSsBlk - 1) / ivr::kSsBlk;
-    const int64_t nb2 = (nb1 + ivr::kSsSup - 1) / ivr::kSsSup;
-    return ((8 * (size_t)m + 255) & ~(size_t)255) * 2 + ((4 * (size_t)m + 255) & ~(size_t)255) +
-           ((8 * (size_t)nb1 + 255) & ~(size_t)255) * 2 + 3 * ((8 * (size_t)nb2 + 255) & ~(size_t)255) +
-           256;
+namespace {
+struct SsLayout {
+    size_t xs, rank, d2, bs1, bs2, dmask, dlist, ctrl, total;
+    int64_t nb1, sd2, sb1;
+    int nb2, sb2;
+};
+SsLayout ss_layout(int64_t n, int R) {
+    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    SsLayout Y{};
+    Y.nb1 = (n + ivr::kSsBlk - 1) / ivr::kSsBlk;
+    Y.nb2 = (int)((Y.nb1 + ivr::kSsSup - 1) / ivr::kSsSup);
+    Y.sd2 = (int64_t)(al(8 * (size_t)n) / 8);
+    Y.sb1 = (int64_t)(al(8 * (size_t)Y.nb1) / 8);
+    Y.sb2 = (int)(al(8 * (size_t)Y.nb2) / 8);
+    size_t o = 0;
+    Y.xs = o;
+    o += al(8 * (size_t)n);
+    Y.rank = o;
+    o += al(4 * (size_t)n);
+    Y.d2 = o;
+    o += 8 * (size_t)Y.sd2 * R;
+    Y.bs1 = o;
+    o += 8 * (size_t)Y.sb1 * R;
+    Y.bs2 = o;
+    o += 8 * (size_t)Y.sb2 * R;
+    Y.dmask = o;
+    o += 8 * (size_t)Y.sb2 * R;
+    Y.dlist = o;
+    o += al(4 * 2 * (size_t)Y.nb2 * R);
+    Y.ctrl = o;  // dcount [2R] | ctl [4R] | arrive | phase_ns [6]
+    o += al(8 * (size_t)ivr::kSsMaxR + 32 * (size_t)ivr::kSsMaxR + 8 + 48);
+    Y.total = o;
+    return Y;
+}
+}  // namespace
+
+extern "C" size_t ivr_kmeans_seed_sorted_workspace_size(int64_t n, int32_t restarts) {
+    const int R = restarts < 1 ? 1 : (restarts > ivr::kSsMaxR ? ivr::kSsMaxR : restarts);
+    return ss_layout(n < 1 ? 1 : n, R).total;
 }
 
 extern "C" int ivr_kmeans_seed_sorted(const double *values, const int32_t *order, int64_t n,
-                                      int32_t k, int64_t first, const double *u, double *centers,
-                                      void *workspace, size_t workspace_bytes,
-                                      ivr_stream_t stream) {
+                                      int32_t k, int32_t restarts, const int64_t *first,
+                                      const double *u, double *centers, void *workspace,
+                                      size_t workspace_bytes, ivr_stream_t stream) {
     using namespace ivr;
-    if (n < 1 || n > 0x7fffffffll || k < 1 || k > kSsMaxK || first < 0 || first >= n || !values ||
-        !order || !centers || (k > 1 && !u) || !workspace ||
-        workspace_bytes < ivr_kmeans_seed_sorted_workspace_size(n)) {
+    if (n < 1 || n > 0x7fffffffll || k < 1 || k > kSsMaxK || restarts < 1 ||
+        restarts > kSsMaxR || !values || !order || !first || !centers || (k > 1 && !u) ||
+        !workspace || workspace_bytes < ivr_kmeans_seed_sorted_workspace_size(n, restarts)) {
         set_error("ivr_kmeans_seed_sorted: bad argument");
         return IVR_ERR_ARG;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
+    const SsLayout Y = ss_layout(n, restarts);
+    char *w = (char *)workspace;
     SeedSorted S{};
     S.x = values;
     S.order = order;
     S.n = n;
     S.k = k;
+    S.R = restarts;
     S.first = first;
     S.u = u;
     S.centers = centers;
-    S.nb1 = (n + kSsBlk - 1) / kSsBlk;
-    S.nb2 = (int)((S.nb1 + kSsSup - 1) / kSsSup);
-    char *w = (char *)workspace;
-    S.xs = (double *)w;
-    w += al(8 * (size_t)n);
-    S.d2 = (double *)w;
-    w += al(8 * (size_t)n);
-    S.rank = (int32_t *)w;
-    w += al(4 * (size_t)n);
-    S.bs1 = (double *)w;
-    w += al(8 * (size_t)S.nb1);
-    S.bs2 = (double *)w;
-    w += al(8 * (size_t)S.nb2);
-    S.dmask = (unsigned long long *)w;
-    w += al(8 * (size_t)S.nb2);
-    S.dlist = (int32_t *)w;
-    w += al(8 * (size_t)S.nb1 + 8 * (size_t)S.nb2);
-    S.dcount = (int32_t *)w;
-    S.ctl = (long long *)(w + 64);
-    S.arrive = (unsigned *)(w + 128);
-    S.phase_ns = (unsigned long long *)(w + 192);
+    S.nb1 = Y.nb1;
+    S.nb2 = Y.nb2;
+    S.sd2 = Y.sd2;
+    S.sb1 = Y.sb1;
+    S.sb2 = Y.sb2;
+    S.xs = (double *)(w + Y.xs);
+    S.rank = (int32_t *)(w + Y.rank);
+    S.d2 = (double *)(w + Y.d2);
+    S.bs1 = (double *)(w + Y.bs1);
+    S.bs2 = (double *)(w + Y.bs2);
+    S.dmask = (unsigned long long *)(w + Y.dmask);
+    S.dlist = (int32_t *)(w + Y.dlist);
+    S.dcount = (int32_t *)(w + Y.ctrl);
+    S.ctl = (long long *)(w + Y.ctrl + 8 * kSsMaxR);
+    S.arrive = (unsigned *)(w + Y.ctrl + 40 * kSsMaxR);
+    S.phase_ns = (unsigned long long *)(w + Y.ctrl + 40 * kSsMaxR + 8);
     const size_t smem = 4 * (size_t)k;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(seed_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1141,8 +1243,8 @@ extern "C" int ivr_kmeans_seed_sorted(const double *values, const int32_t *order
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seed_sorted_kernel, kSsThreads, smem);
-    if (sms < 1 || per_sm < 1) {
-        set_error("ivr_kmeans_seed_sorted: kernel does not fit on an SM");
+    if (sms < restarts || per_sm < 1) {
+        set_error("ivr_kmeans_seed_sorted: kernel does not fit on the device");
         return IVR_ERR_ARG;
     }
     void *args[] = {&S};

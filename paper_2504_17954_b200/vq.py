@@ -126,9 +126,10 @@ def kmeans(samples, k, seed=0, restarts=5):
     rng = np.random.default_rng(seed)
     n = samples.size
     order = _value_order(x)  # shared by the restarts' seedings
+    seeds = _seed_restarts(x, k, rng, restarts, order)
     best, best_sse = None, np.inf
-    for _ in range(restarts):
-        c = _seed_plusplus(x, k, rng, order)
+    for r in range(restarts):
+        c = seeds[r] if seeds is not None else _seed_plusplus(x, k, rng, order)
         c = _lloyd(x, c)
         idx = _assign_idx(x, c)
         sse = float(((x - c[idx]) ** 2).sum())
@@ -139,6 +140,7 @@ def kmeans(samples, k, seed=0, restarts=5):
 
 
 SEED_SORTED_MAX_K = 32768
+SEED_SORTED_MAX_R = 8  # seedings per ivr_kmeans_seed_sorted launch
 
 
 def _value_order(x):
@@ -147,6 +149,42 @@ def _value_order(x):
     if x.numel() >= 2 ** 31:
         return None
     return torch.argsort(x).to(torch.int32)
+
+
+def _sorted_seeding(n, k):
+    return k <= SEED_SORTED_MAX_K and n < 2 ** 31
+
+
+def _seed_restarts(x, k, rng, restarts, order=None):
+    """All of k-means' restart seedings in one ivr_kmeans_seed_sorted launch
+    (up to 8 per launch).  The draws are taken in the reference's order --
+    per restart rng.integers for the first centre, then one rng.random() per
+    centre -- before any seeding runs: they do not depend on the data, and
+    the distinct-value shortcut in kmeans means no seeding runs out of mass
+    early (which would leave draws unconsumed in the reference).  Returns
+    (restarts, k) centres, or None where the sorted seeding does not apply."""
+    n = x.numel()
+    if not _sorted_seeding(n, k):
+        return None
+    if order is None:
+        order = _value_order(x)
+    out = []
+    for r0 in range(0, restarts, SEED_SORTED_MAX_R):
+        R = min(SEED_SORTED_MAX_R, restarts - r0)
+        firsts, us = [], []
+        for _ in range(R):
+            firsts.append(int(rng.integers(n)))
+            us.append(rng.random(k - 1))  # k == 1: no draw, as the reference
+        first = torch.tensor(firsts, dtype=torch.int64, device=x.device)
+        u = torch.from_numpy(np.concatenate(us)).to(x.device)
+        c = torch.empty((R, k), dtype=torch.float64, device=x.device)
+        nb = int(L.lib().ivr_kmeans_seed_sorted_workspace_size(n, R))
+        ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+        L.check(L.lib().ivr_kmeans_seed_sorted(D.ptr(x), D.ptr(order), n, int(k), R, D.ptr(first),
+                                               D.ptr(u), D.ptr(c), D.ptr(ws), nb,
+                                               D.stream_handle()), "ivr_kmeans_seed_sorted")
+        out.append(c)
+    return torch.cat(out)
 
 
 def _seed_plusplus(x, k, rng, order=None):
@@ -158,18 +196,11 @@ def _seed_plusplus(x, k, rng, order=None):
     in value order) when k <= 32768 and n < 2^31, else ivr_kmeans_seed (two
     kernels per centre over every sample)."""
     n = x.numel()
+    if _sorted_seeding(n, k):
+        return _seed_restarts(x, k, rng, 1, order)[0]
     first = int(rng.integers(n))
     u = torch.from_numpy(rng.random(k - 1)).to(x.device)  # k == 1: no draw, as the reference
     c = torch.empty(k, dtype=torch.float64, device=x.device)
-    if k <= SEED_SORTED_MAX_K and n < 2 ** 31:
-        if order is None:
-            order = _value_order(x)
-        nb = int(L.lib().ivr_kmeans_seed_sorted_workspace_size(n))
-        ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
-        L.check(L.lib().ivr_kmeans_seed_sorted(D.ptr(x), D.ptr(order), n, int(k), first, D.ptr(u),
-                                               D.ptr(c), D.ptr(ws), nb, D.stream_handle()),
-                "ivr_kmeans_seed_sorted")
-        return c
     nb = int(L.lib().ivr_kmeans_seed_workspace_size(n))
     ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
     L.check(L.lib().ivr_kmeans_seed(D.ptr(x), n, int(k), first, D.ptr(u), D.ptr(c), D.ptr(ws), nb,

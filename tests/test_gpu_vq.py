@@ -161,3 +161,19 @@ def test_sorted_seeding_equals_full_pass(case):
     assert np.array_equal(got, ref)
     if case == "exhausted":  # the remaining centres repeat the first one, as the reference
         assert len(np.unique(got)) == 40 and np.all(got[40:] == got[0])
+
+
+@pytest.mark.parametrize("n,k,restarts", [(120_000, 300, 5), (5_000, 64, 8), (40_000, 500, 3)])
+def test_batched_restart_seedings_equal_sequential(n, k, restarts):
+    """k-means' restarts seeded in one launch (all draws taken up front in the
+    reference's order) == the restarts seeded one after the other."""
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.vq import _seed_restarts
+    g = np.random.default_rng(n)
+    x = np.concatenate([g.normal(size=n - n // 4) ** 3, g.integers(0, 50, size=n // 4) * 0.5])
+    g.shuffle(x)
+    xd = to_dev(x)
+    got = _seed_restarts(xd, k, np.random.default_rng(2), restarts).cpu().numpy()
+    rng = np.random.default_rng(2)
+    for r in range(restarts):
+        assert np.array_equal(got[r], _seed_full_pass(xd, k, rng)), r

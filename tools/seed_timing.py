@@ -22,26 +22,31 @@ K = 4096
 for n in (4_000_000, 12_000_000, 16_000_000):
     x = torch.randn(n, dtype=torch.float64, device="cuda")
     order = torch.argsort(x).to(torch.int32)
-    rng = np.random.default_rng(0)
-    first = int(rng.integers(n))
-    u = torch.from_numpy(rng.random(K - 1)).cuda()
-    c = torch.empty(K, dtype=torch.float64, device="cuda")
-    nb = int(L.lib().ivr_kmeans_seed_sorted_workspace_size(n))
-    ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
-    for rep in range(2):
-        torch.cuda.synchronize()
-        t0 = time.perf_counter()
-        L.check(L.lib().ivr_kmeans_seed_sorted(D.ptr(x), D.ptr(order), n, K, first, D.ptr(u),
-                                               D.ptr(c), D.ptr(ws), nb, D.stream_handle()), "s")
-        torch.cuda.synchronize()
-        ms = (time.perf_counter() - t0) * 1e3
-    nb1 = (n + 31) // 32
-    nb2 = (nb1 + 63) // 64
-    off = 2 * al(8 * n) + al(4 * n) + al(8 * nb1) + 2 * al(8 * nb2) + al(8 * nb1 + 8 * nb2) + 192
-    ph = ws[off:off + 48].cpu().numpy().view(np.uint64) / 1e3 / (K - 1)
-    names = ("pick", "wait", "update", "barrier", "resum", "arrive")
-    print(n, "sorted seeding ms", round(ms, 1), "us/centre", round(ms * 1e3 / (K - 1), 2),
-          {a: round(float(b), 2) for a, b in zip(names, ph)})
+    for R in (1, 5):
+        rng = np.random.default_rng(0)
+        first = torch.tensor([int(rng.integers(n)) for _ in range(R)], dtype=torch.int64,
+                             device="cuda")
+        u = torch.from_numpy(rng.random(R * (K - 1))).cuda()
+        c = torch.empty((R, K), dtype=torch.float64, device="cuda")
+        nb = int(L.lib().ivr_kmeans_seed_sorted_workspace_size(n, R))
+        ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+        for rep in range(2):
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            L.check(L.lib().ivr_kmeans_seed_sorted(D.ptr(x), D.ptr(order), n, K, R, D.ptr(first),
+                                                   D.ptr(u), D.ptr(c), D.ptr(ws), nb,
+                                                   D.stream_handle()), "s")
+            torch.cuda.synchronize()
+            ms = (time.perf_counter() - t0) * 1e3
+        # phase_ns sits after dcount [2 * 8] and ctl [4 * 8] and the arrival word
+        ph = ws[nb - al(8 * 8 + 32 * 8 + 8 + 48) + 40 * 8 + 8:][:48].cpu().numpy().view(np.uint64)
+        ph = ph / 1e3 / (K - 1)
+        names = ("pick", "wait", "update", "barrier", "resum", "arrive")
+        print(n, R, "seedings ms", round(ms, 1), "us/centre", round(ms * 1e3 / (K - 1), 2),
+              {a: round(float(b), 2) for a, b in zip(names, ph)})
+    first = int(first[0].item())
+    u = u[:K - 1]
+    c = c[0]
     wf = torch.empty(int(L.lib().ivr_kmeans_seed_workspace_size(n)), dtype=torch.uint8,
                      device="cuda")
     c2 = torch.empty_like(c)
