@@ -119,12 +119,16 @@ def kmeans(samples, k, seed=0, restarts=5):
         raise EmptyInput("kmeans needs at least one sample")
     if k < 1:
         raise OutOfRange("codebook size must be >= 1")
-    x = D.to_dev(samples)
+    return _kmeans_dev(D.to_dev(samples), k, seed, restarts)
+
+
+def _kmeans_dev(x, k, seed=0, restarts=5):
+    """kmeans on a float64 device vector (numpy centroids out)."""
     distinct = torch.unique(x)  # sorted
     if distinct.numel() <= k:
         return distinct.cpu().numpy()
     rng = np.random.default_rng(seed)
-    n = samples.size
+    n = x.numel()
     order = _value_order(x)  # shared by the restarts' seedings
     seeds = _seed_restarts(x, k, rng, restarts, order)
     best, best_sse = None, np.inf
@@ -245,11 +249,24 @@ def _lloyd(x, c):
 
 
 def quantize_attributes(arrays, k=DEFAULT_CODEBOOK_SIZE, seed=0):
+    """vq.py:137-147: per attribute, kmeans over all its components, then the
+    indices (Codebook.encode's values) -- one upload per attribute, indices
+    come back in the codebook's index dtype."""
+    if k < 1:
+        raise OutOfRange("codebook size must be >= 1")
     out = {}
     for name, arr in arrays.items():
         arr = np.asarray(arr, dtype=np.float64)
-        cb = Codebook(name, kmeans(arr.reshape(-1), k, seed=seed))
-        out[name] = (cb, cb.encode(arr))
+        if arr.size == 0:
+            raise EmptyInput("kmeans needs at least one sample")
+        x = D.to_dev(arr.reshape(-1))
+        cb = Codebook(name, _kmeans_dev(x, k, seed=seed))
+        if cb.k == 1:
+            idx = np.zeros(arr.shape, dtype=cb.index_dtype)
+        else:
+            idx = assign_device(x, D.to_dev(cb.centroids)).cpu().numpy().view(np.uint16)
+            idx = idx.astype(cb.index_dtype, copy=False).reshape(arr.shape)
+        out[name] = (cb, idx)
     return out
 
 

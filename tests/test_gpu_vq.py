@@ -177,3 +177,20 @@ def test_batched_restart_seedings_equal_sequential(n, k, restarts):
     rng = np.random.default_rng(2)
     for r in range(restarts):
         assert np.array_equal(got[r], _seed_full_pass(xd, k, rng)), r
+
+
+def test_quantize_attributes_indices_equal_codebook_encode():
+    """quantize_attributes' device-side encode (one upload per attribute,
+    uint16 straight into the index dtype) == Codebook.encode (the reference's
+    assign_nearest path), shapes and dtypes included."""
+    from paper_2504_17954_b200.vq import quantize_attributes
+    g = np.random.default_rng(4)
+    arrays = {"a": g.normal(size=(3000, 4)), "b": g.standard_t(2, size=5000),
+              "c": np.repeat(g.normal(size=7), 100)}
+    for k in (64, 300):
+        q = quantize_attributes(arrays, k=k, seed=1)
+        for name, arr in arrays.items():
+            cb, idx = q[name]
+            ref = cb.encode(arr)
+            assert idx.dtype == ref.dtype == cb.index_dtype and idx.shape == arr.shape
+            assert np.array_equal(idx, ref), (k, name)
