@@ -380,6 +380,17 @@ int ivr_kmeans_lloyd_step(const double *values, int64_t n, const double *centroi
                           double *new_centroids, double *shift, void *workspace,
                           size_t workspace_bytes, ivr_stream_t stream);
 
+/* The same step for `sets` sorted centroid sets (k-means' restarts, row r at
+ * centroids[r * k]) on the values in ascending order: bucket b is the
+ * contiguous range of sorted values between the midpoints, so its sum is a
+ * segment sum (one CTA per bucket and set, no atomics); new = count > 0 ?
+ * sum / count : old, shift[r] = max |new - old| of set r (device doubles).
+ * k >= 2. */
+size_t ivr_kmeans_lloyd_sorted_workspace_size(int32_t k, int32_t sets);
+int ivr_kmeans_lloyd_step_sorted(const double *sorted_values, int64_t n, const double *centroids,
+                                 int32_t k, int32_t sets, double *new_centroids, double *shift,
+                                 void *workspace, size_t workspace_bytes, ivr_stream_t stream);
+
 /* k-means++ seeding, vq._seed_plusplus (vq.py:60-72): centers[0] =
  * values[first] (the reference's rng.integers draw), then for i = 1..k-1 the
  * first index whose cumulative d2 (index order) exceeds u[i-1] * sum(d2)

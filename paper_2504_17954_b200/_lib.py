@@ -158,6 +158,9 @@ _SIGS = {
     "ivr_kmeans_seed_workspace_size": ([ctypes.c_int64], ctypes.c_size_t),
     "ivr_kmeans_seed": ([P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int64, P, P, P,
                          ctypes.c_size_t, P], ctypes.c_int),
+    "ivr_kmeans_lloyd_sorted_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),
+    "ivr_kmeans_lloyd_step_sorted": ([P, ctypes.c_int64, P, ctypes.c_int32, ctypes.c_int32, P, P, P,
+                                      ctypes.c_size_t, P], ctypes.c_int),
     "ivr_kmeans_seed_sorted_workspace_size": ([ctypes.c_int64, ctypes.c_int32], ctypes.c_size_t),
     "ivr_kmeans_seed_sorted": ([P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P, P, P, P,
                                 ctypes.c_size_t, P], ctypes.c_int),

@@ -408,6 +408,66 @@ lloyd_finish_kernel(const double *cents, int k, const double *sums, const unsign
     }
 }
 
+// Lloyd step on the values in sorted order (vq.py:75-87) for `sets` centroid
+// sets at once (k-means' restarts): bucket b (searchsorted on the float64
+// midpoints, as K5) is the contiguous range xs[bnd[b], bnd[b + 1]) with
+// bnd[b] = #{xs <= mid[b - 1]}, so the per-centroid sums are segment sums --
+// one CTA per bucket, fixed tree order, no atomics -- instead of a scatter
+// of float64 atomics (a CAS loop per value in shared memory).  Sums run in
+// value order rather than np.bincount's index order (same float64 sums up to
+// rounding, as the atomic form).
+constexpr int kLlThreads = 256;
+
+__global__ void __launch_bounds__(kLlThreads)
+lloyd_bounds_kernel(const double *__restrict__ xs, int64_t n, const double *__restrict__ cents,
+                    int k, int64_t *bnd, unsigned long long *shift) {
+    const int r = blockIdx.y;
+    const double *c = cents + (int64_t)r * k;
+    int64_t *b = bnd + (int64_t)r * (k + 1);
+    const int i = blockIdx.x * kLlThreads + threadIdx.x;  // boundary i + 1 (mid i)
+    if (i == 0) {
+        b[0] = 0;
+        b[k] = n;
+        shift[r] = 0ull;
+    }
+    if (i >= k - 1) return;
+    const double m = vq_mid(c, i);
+    int64_t lo = 0, hi = n;  // first position with xs > m (NaN sorts last, never <= m)
+    while (lo < hi) {
+        const int64_t md = (lo + hi) >> 1;
+        if (__ldg(xs + md) <= m) lo = md + 1;
+        else hi = md;
+    }
+    b[i + 1] = lo;
+}
+
+__global__ void __launch_bounds__(kLlThreads)
+lloyd_segsum_kernel(const double *__restrict__ xs, const double *__restrict__ cents, int k,
+                    const int64_t *__restrict__ bnd, double *out, unsigned long long *shift) {
+    __shared__ double s_red[kLlThreads / 32];
+    const int r = blockIdx.y, bk = blockIdx.x;
+    const int64_t *b = bnd + (int64_t)r * (k + 1);
+    const int64_t b0 = b[bk], b1 = b[bk + 1];
+    double t = 0.0;
+    for (int64_t i = b0 + threadIdx.x; i < b1; i += kLlThreads) t += __ldg(xs + i);
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+    if ((threadIdx.x & 31) == 0) s_red[threadIdx.x >> 5] = t;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        double sum = 0.0;
+#pragma unroll
+        for (int w = 0; w < kLlThreads / 32; ++w) sum += s_red[w];
+        const double old = cents[(int64_t)r * k + bk];
+        const int64_t cnt = b1 - b0;
+        const double nw = cnt > 0 ? sum / (double)cnt : old;  // vq.py:81-83
+        out[(int64_t)r * k + bk] = nw;
+        const double d = fabs(nw - old);  // max over the set: non-negative doubles order as bits
+        atomicMax(shift + r, d == d ? (unsigned long long)__double_as_longlong(d)
+                                    : 0x7ff8000000000000ull);
+    }
+}
+
 // ----------------------------------------------------------------- k-means++
 // vq._seed_plusplus (vq.py:60-72) with the reference's random stream: every
 // step draws one uniform u (rng.choice(n, p = d2 / sum d2) == the first index
@@ -1051,6 +1111,31 @@ extern "C" int ivr_kmeans_lloyd_step(const double *values, int64_t n, const doub
                                                               sums, counts);
     lloyd_finish_kernel<<<1, 1024, 0, st>>>(centroids, k, sums, counts, new_centroids, shift);
     return check_launch("ivr_kmeans_lloyd_step");
+}
+
+extern "C" size_t ivr_kmeans_lloyd_sorted_workspace_size(int32_t k, int32_t sets) {
+    return 8 * (size_t)(k < 1 ? 1 : k + 1) * (size_t)(sets < 1 ? 1 : sets);
+}
+
+extern "C" int ivr_kmeans_lloyd_step_sorted(const double *sorted_values, int64_t n,
+                                            const double *centroids, int32_t k, int32_t sets,
+                                            double *new_centroids, double *shift, void *workspace,
+                                            size_t workspace_bytes, ivr_stream_t stream) {
+    using namespace ivr;
+    if (n < 1 || k < 2 || sets < 1 || sets > 65535 || !sorted_values || !centroids ||
+        !new_centroids || !shift || !workspace ||
+        workspace_bytes < ivr_kmeans_lloyd_sorted_workspace_size(k, sets)) {
+        set_error("ivr_kmeans_lloyd_step_sorted: bad argument");
+        return IVR_ERR_ARG;
+    }
+    cudaStream_t st = (cudaStream_t)stream;
+    int64_t *bnd = reinterpret_cast<int64_t *>(workspace);
+    unsigned long long *sh = reinterpret_cast<unsigned long long *>(shift);
+    lloyd_bounds_kernel<<<dim3((k - 1 + kLlThreads - 1) / kLlThreads, sets), kLlThreads, 0, st>>>(
+        sorted_values, n, centroids, k, bnd, sh);
+    lloyd_segsum_kernel<<<dim3(k, sets), kLlThreads, 0, st>>>(sorted_values, centroids, k, bnd,
+                                                              new_centroids, sh);
+    return check_launch("ivr_kmeans_lloyd_step_sorted");
 }
 
 extern "C" size_t ivr_vq_assign_workspace_size(void) {

@@ -131,10 +131,13 @@ def _kmeans_dev(x, k, seed=0, restarts=5):
     n = x.numel()
     order = _value_order(x)  # shared by the restarts' seedings
     seeds = _seed_restarts(x, k, rng, restarts, order)
+    fitted = _lloyd_sets(x, x[order.long()], seeds) if seeds is not None else None
     best, best_sse = None, np.inf
     for r in range(restarts):
-        c = seeds[r] if seeds is not None else _seed_plusplus(x, k, rng, order)
-        c = _lloyd(x, c)
+        if fitted is not None:
+            c = fitted[r]
+        else:
+            c = _lloyd(x, _seed_plusplus(x, k, rng, order))
         idx = _assign_idx(x, c)
         sse = float(((x - c[idx]) ** 2).sum())
         if sse < best_sse:
@@ -246,6 +249,39 @@ def _lloyd(x, c):
         if shift < KMEANS_SHIFT_TOL:
             break
     return torch.sort(c).values
+
+
+def _lloyd_sets(x, xs, seeds):
+    """Lloyd iterations (vq.py:75-87) of every restart at once on the sorted
+    values xs (ivr_kmeans_lloyd_step_sorted: segment sums between the
+    midpoints, all sets in one launch, one host read of the shifts per
+    iteration); each set stops at its own convergence or after
+    KMEANS_MAX_ITERS, exactly as its own loop would.  Returns (R, k) sorted
+    centroids."""
+    R, k = seeds.shape
+    scale = max(float(x.abs().max()), 1e-12)
+    c = torch.sort(seeds, dim=1).values
+    if k < 2:
+        return c
+    nb = int(L.lib().ivr_kmeans_lloyd_sorted_workspace_size(k, R))
+    ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
+    shift = torch.empty(R, dtype=torch.float64, device=x.device)
+    active = list(range(R))
+    for _ in range(KMEANS_MAX_ITERS):
+        cur = c[active].contiguous() if len(active) < R else c
+        cur = torch.sort(cur, dim=1).values
+        new = torch.empty_like(cur)
+        na = len(active)
+        L.check(L.lib().ivr_kmeans_lloyd_step_sorted(D.ptr(xs), xs.numel(), D.ptr(cur), k, na,
+                                                     D.ptr(new), D.ptr(shift), D.ptr(ws), nb,
+                                                     D.stream_handle()),
+                "ivr_kmeans_lloyd_step_sorted")
+        sh = shift[:na].cpu().numpy() / scale
+        c[active] = new
+        active = [r for r, v in zip(active, sh) if not v < KMEANS_SHIFT_TOL]
+        if not active:
+            break
+    return torch.sort(c, dim=1).values
 
 
 def quantize_attributes(arrays, k=DEFAULT_CODEBOOK_SIZE, seed=0):

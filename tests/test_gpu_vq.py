@@ -194,3 +194,22 @@ def test_quantize_attributes_indices_equal_codebook_encode():
             ref = cb.encode(arr)
             assert idx.dtype == ref.dtype == cb.index_dtype and idx.shape == arr.shape
             assert np.array_equal(idx, ref), (k, name)
+
+
+def test_lloyd_sets_match_per_restart_lloyd():
+    """The restarts' Lloyd runs in one loop on the sorted values (segment sums
+    between midpoints, ivr_kmeans_lloyd_step_sorted) == each restart's own
+    loop with the atomic accumulation (ivr_kmeans_lloyd_step), up to the
+    float64 summation order."""
+    import torch
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.vq import _lloyd, _lloyd_sets, _seed_restarts
+    g = np.random.default_rng(6)
+    x = np.concatenate([g.normal(size=60_000) ** 3, g.integers(0, 30, size=20_000) * 0.1])
+    g.shuffle(x)
+    xd = to_dev(x)
+    seeds = _seed_restarts(xd, 128, np.random.default_rng(1), 4)
+    got = _lloyd_sets(xd, torch.sort(xd).values, seeds).cpu().numpy()
+    for r in range(4):
+        ref = _lloyd(xd, seeds[r].clone()).cpu().numpy()
+        np.testing.assert_allclose(got[r], ref, rtol=1e-9, atol=1e-12, err_msg=str(r))

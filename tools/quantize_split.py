@@ -28,6 +28,7 @@ def timed(name, fn):
 vq._seed_plusplus = timed("seed", vq._seed_plusplus)
 vq._seed_restarts = timed("seed", vq._seed_restarts)
 vq._lloyd = timed("lloyd", vq._lloyd)
+vq._lloyd_sets = timed("lloyd", vq._lloyd_sets)
 vq._value_order = timed("sort", vq._value_order)
 m = editable_model(0, 4_000_000, density=4_000_000)
 vq.quantize_model(m, k=64, seed=0)  # warm-up (kernels, allocator)
