@@ -92,7 +92,14 @@ inline cudaError_t launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t sm
     bool pdl = lvl >= LEVEL && lvl > 0;
     if (pdl && lvl == 1) {
         cudaStreamCaptureStatus cs = cudaStreamCaptureStatusNone;
-        pdl = cudaStreamIsCapturing(st, &cs) == cudaSuccess && cs == cudaStreamCaptureStatusNone;
+        if (cudaStreamIsCapturing(st, &cs) != cudaSuccess) {
+            // the legacy stream while another thread captures globally: no
+            // programmatic edge, and the query's error is not this launch's
+            (void)cudaGetLastError();
+            pdl = false;
+        } else {
+            pdl = cs == cudaStreamCaptureStatusNone;
+        }
     }
     cudaLaunchConfig_t cfg{};
     cfg.gridDim = grid;
