@@ -163,10 +163,12 @@ def test_sorted_seeding_equals_full_pass(case):
         assert len(np.unique(got)) == 40 and np.all(got[40:] == got[0])
 
 
-@pytest.mark.parametrize("n,k,restarts", [(120_000, 300, 5), (5_000, 64, 8), (40_000, 500, 3)])
+@pytest.mark.parametrize("n,k,restarts", [(120_000, 300, 5), (5_000, 64, 8), (40_000, 500, 3),
+                                          (3_000, 40, 11), (2_000, 1, 3)])
 def test_batched_restart_seedings_equal_sequential(n, k, restarts):
     """k-means' restarts seeded in one launch (all draws taken up front in the
-    reference's order) == the restarts seeded one after the other."""
+    reference's order) == the restarts seeded one after the other; more than
+    8 restarts take two launches; k = 1 draws only the first centres."""
     from paper_2504_17954_b200.device import to_dev
     from paper_2504_17954_b200.vq import _seed_restarts
     g = np.random.default_rng(n)
