@@ -403,21 +403,28 @@ int ivr_kmeans_seed(const double *values, int64_t n, int32_t k, int64_t first, c
                     ivr_stream_t stream);
 
 /* The same seeding (same draws, same picks up to float64 summation order) for
- * `restarts` (1..8) independent seedings of the same values in one
- * cooperative kernel that only revisits the samples a new centre can change:
- * `order` (int32, n < 2^31) sorts `values` ascending (any order of ties); d2
- * is lowered only between the chosen centres adjacent to the new one in
- * value order (~n ln k updates in all instead of n k), and the picks walk
- * 32-value block sums and 2048-value super-block sums in index order.
- * Seeding r: first[r] (device int64), draws u[r * (k - 1) ...], centres
- * centers[r * k ...].  1 <= k <= 32768.  k-means' restarts draw from one
- * stream but their draws do not depend on the data, so they are all known
- * up front (vq.kmeans). */
-size_t ivr_kmeans_seed_sorted_workspace_size(int64_t n, int32_t restarts);
-int ivr_kmeans_seed_sorted(const double *values, const int32_t *order, int64_t n, int32_t k,
-                           int32_t restarts, const int64_t *first, const double *u,
-                           double *centers, void *workspace, size_t workspace_bytes,
-                           ivr_stream_t stream);
+ * `count` (1..64) independent seedings -- k-means' restarts of every
+ * attribute -- in one cooperative kernel that only revisits the samples a
+ * new centre can change: `order` (int32, n < 2^31) sorts `values` ascending
+ * (any order of ties); d2 is lowered only between the chosen centres
+ * adjacent to the new one in value order (~n ln k updates in all instead of
+ * n k), and the picks walk 32-value block sums and 2048-value super-block
+ * sums in index order.  Per seeding: the rng.integers draw `first`, the k - 1
+ * rng.random draws `u` (device), `centers` (device, k).  1 <= k <= 32768.
+ * k-means' restarts draw from one stream but their draws do not depend on
+ * the data, so they are all known up front (vq.kmeans).  `problems` is a host
+ * array. */
+typedef struct {
+    const double *values;  /* n float64 (device) */
+    const int32_t *order;  /* ascending order of values (device) */
+    int64_t n;
+    int64_t first;
+    const double *u;  /* k - 1 draws (device) */
+    double *centers;  /* k centres out (device) */
+} ivr_seed_problem;
+size_t ivr_kmeans_seed_sorted_workspace_size(const ivr_seed_problem *problems, int32_t count);
+int ivr_kmeans_seed_sorted(const ivr_seed_problem *problems, int32_t count, int32_t k,
+                           void *workspace, size_t workspace_bytes, ivr_stream_t stream);
 
 /* Compose on the device (scene.py:147-186, gaussians.py:98-106): concatenate
  * n_src (<= 64) row-major float64 arrays of `width` columns (rows[m] rows

@@ -58,6 +58,11 @@ class Shading_t(ctypes.Structure):
                 ("lam", ctypes.c_double * 4), ("b", ctypes.c_double * 4)]
 
 
+class SeedProblem_t(ctypes.Structure):
+    _fields_ = [("values", P), ("order", P), ("n", ctypes.c_int64), ("first", ctypes.c_int64),
+                ("u", P), ("centers", P)]
+
+
 class Edits_t(ctypes.Structure):
     _fields_ = [("scene_id", P), ("opacity_scale", P), ("rescale_opacity", ctypes.c_int32)]
 
@@ -161,9 +166,9 @@ _SIGS = {
     "ivr_kmeans_lloyd_sorted_workspace_size": ([ctypes.c_int32, ctypes.c_int32], ctypes.c_size_t),
     "ivr_kmeans_lloyd_step_sorted": ([P, ctypes.c_int64, P, ctypes.c_int32, ctypes.c_int32, P, P, P,
                                       ctypes.c_size_t, P], ctypes.c_int),
-    "ivr_kmeans_seed_sorted_workspace_size": ([ctypes.c_int64, ctypes.c_int32], ctypes.c_size_t),
-    "ivr_kmeans_seed_sorted": ([P, P, ctypes.c_int64, ctypes.c_int32, ctypes.c_int32, P, P, P, P,
-                                ctypes.c_size_t, P], ctypes.c_int),
+    "ivr_kmeans_seed_sorted_workspace_size": ([P, ctypes.c_int32], ctypes.c_size_t),
+    "ivr_kmeans_seed_sorted": ([P, ctypes.c_int32, ctypes.c_int32, P, ctypes.c_size_t, P],
+                               ctypes.c_int),
     "ivr_blend_bwd_det_workspace_size": ([ctypes.c_int64, ctypes.c_int32], ctypes.c_size_t),
     "ivr_blend_bwd_deterministic": ([P, P, ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int32,
                                      ctypes.c_int32, ctypes.c_int32, P, P, P, ctypes.c_int64, P, P,

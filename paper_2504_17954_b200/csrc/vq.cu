@@ -618,8 +618,8 @@ seed_pick_kernel(const double *x, int64_t n, const double *d2, const double *bsu
 
 // ----------------------------------------------------------------- k-means++, sorted
 // The same seeding in one persistent cooperative kernel that touches only the
-// samples a new centre can change, for up to kSsMaxR independent seedings of
-// the same values at once (k-means' restarts: their draws do not depend on
+// samples a new centre can change, for up to kSsMaxP independent seedings at
+// once (k-means' restarts of every attribute: their draws do not depend on
 // the data, so all of them are known before the first one runs).  Scalar
 // k-means is 1-D: with the samples in value order (xs = x[order]), a centre c
 // at sorted position p can only lower d2 for samples strictly between the
@@ -632,7 +632,8 @@ seed_pick_kernel(const double *x, int64_t n, const double *d2, const double *bsu
 // barrier one warp per marked super-block re-sums its marked blocks and the
 // super-block (fixed order: bit-identical runs), and the CTAs arrive on a
 // counter the picking CTAs wait for.  The samples updated per step fall off
-// like n / i (~n ln k in all instead of n k).
+// like n / i (~n ln k in all instead of n k); the step is a chain of
+// dependent L2 round trips, which the seedings of one launch share.
 namespace cg = cooperative_groups;
 
 constexpr int kSsThreads = 512;
@@ -640,29 +641,31 @@ constexpr int kSsBlk = 32;      // d2 values per block sum
 constexpr int kSsSup = 64;      // block sums per super-block sum
 constexpr int kSsMaxK = 32768;  // chosen positions kept in shared memory
 constexpr int kSsPer = 16;      // super-block sums per thread held in registers by the pick
-constexpr int kSsMaxR = 8;      // seedings per launch
+constexpr int kSsMaxP = 64;     // seedings per launch (one picking CTA each)
 
-struct SeedSorted {
+struct SsProb {
     const double *x;
     const int32_t *order;
-    int64_t n;
-    int k, R;
-    const int64_t *first;  // [R]
-    const double *u;       // [R][k - 1]
-    double *centers;       // [R][k]
+    int64_t n, nb1, first;
+    int nb2;
+    const double *u;  // k - 1 draws
+    double *centers;  // k
+    // workspace: values in sorted order, sorted position of each index, d2,
+    // block sums, super-block sums, marked-block masks, two super-block lists
+    // (step parity), their lengths, the published pick {j, L, R, step}
     double *xs;
     int32_t *rank;
-    // per seeding r (stride below): d2 [n], block sums [nb1], super-block sums
-    // [nb2], marked-block masks [nb2], two super-block lists [2][nb2] (step
-    // parity), their lengths [2], published pick {j, L, R, step}
     double *d2, *bs1, *bs2;
     unsigned long long *dmask;
     int32_t *dlist, *dcount;
     long long *ctl;
+};
+
+struct SeedSorted {
+    int k, P;
     unsigned *arrive;
     unsigned long long *phase_ns;  // CTA 0's time per phase: pick, wait, update, barrier, re-sum, arrive
-    int64_t nb1, sd2, sb1;         // d2 / block-sum strides (elements)
-    int nb2, sb2;                  // super-block stride (elements)
+    SsProb pr[kSsMaxP];
 };
 
 __device__ __forceinline__ double warp_tree_sum(double v) {
@@ -733,15 +736,15 @@ __device__ __forceinline__ long long ld_volatile_s64(const long long *p) {
 // CTA r's pick for seeding r at `step`: the first index whose cumulative d2
 // (index order) exceeds u * sum d2, and its chosen neighbours L < p < R in
 // value order (j = -1: all mass on chosen centres)
-__device__ void ss_pick(const SeedSorted &S, int r, int step, int32_t *s_chosen, int nch,
-                        long long &j, long long &L, long long &R) {
+__device__ void ss_pick(const SsProb &Q, int step, int32_t *s_chosen, int nch, long long &j,
+                        long long &L, long long &R) {
     __shared__ double s_w[32], s_before;
     __shared__ int s_sup, s_supmass, s_lr[2];
     __shared__ long long s_j;
     const int tid = threadIdx.x, lane = tid & 31;
-    const int64_t n = S.n;
-    const int nb2 = S.nb2;
-    const double *d2 = S.d2 + r * S.sd2, *bs1 = S.bs1 + r * S.sb1, *bs2 = S.bs2 + (int64_t)r * S.sb2;
+    const int64_t n = Q.n;
+    const int nb2 = Q.nb2;
+    const double *d2 = Q.d2, *bs1 = Q.bs1, *bs2 = Q.bs2;
     const int per = (nb2 + kSsThreads - 1) / kSsThreads;
     const int q0 = min(tid * per, nb2), q1 = min(q0 + per, nb2);
     if (tid == 0) {
@@ -765,7 +768,7 @@ __device__ void ss_pick(const SeedSorted &S, int r, int step, int32_t *s_chosen,
     L = -1;
     R = n;
     if (!(tot > 0.0)) return;  // uniform over the CTA
-    const double target = S.u[(int64_t)r * (S.k - 1) + step - 1] * tot;
+    const double target = Q.u[step - 1] * tot;
     double run = incl - mine, bhit = 0.0, blast = 0.0;
     int lastm = -1, hitq = 0x7fffffff;
     for (int qb = q0; qb < q1; qb += kSsPer) {
@@ -802,8 +805,8 @@ __device__ void ss_pick(const SeedSorted &S, int r, int step, int32_t *s_chosen,
     if (tid < 32) {
         // block inside the super-block: lane l holds blocks 2l, 2l + 1
         const int64_t bb = (int64_t)sup * kSsSup + 2 * lane;
-        const double v0 = bb < S.nb1 ? __ldcg(bs1 + bb) : 0.0;
-        const double v1 = bb + 1 < S.nb1 ? __ldcg(bs1 + bb + 1) : 0.0;
+        const double v0 = bb < Q.nb1 ? __ldcg(bs1 + bb) : 0.0;
+        const double v1 = bb + 1 < Q.nb1 ? __ldcg(bs1 + bb + 1) : 0.0;
         double x = v0 + v1;
 #pragma unroll
         for (int o = 1; o < 32; o <<= 1) {
@@ -850,7 +853,7 @@ __device__ void ss_pick(const SeedSorted &S, int r, int step, int32_t *s_chosen,
     j = s_j;
     // chosen neighbours L < p < R (positions are distinct: a chosen sample
     // has d2 = 0 and is never drawn again)
-    const int p = __ldcg(S.rank + j);
+    const int p = __ldcg(Q.rank + j);
     int l = -1, rr = (int)n;
     for (int q = tid; q < nch; q += kSsThreads) {
         const int v = s_chosen[q];
@@ -877,56 +880,54 @@ __device__ void ss_pick(const SeedSorted &S, int r, int step, int32_t *s_chosen,
     if (tid == 0) s_chosen[nch] = p;
 }
 
-__global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S) {
+__global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(const __grid_constant__ SeedSorted S) {
     cg::grid_group grid = cg::this_grid();
-    extern __shared__ int32_t s_chosen[];  // CTA r < R: seeding r's chosen sorted positions
-    __shared__ long long s_ctl[kSsMaxR][3];
-    __shared__ int64_t s_start[kSsMaxR + 1], s_cst[kSsMaxR + 1];
-    __shared__ bool s_done[kSsMaxR];
+    extern __shared__ int32_t s_chosen[];  // CTA r < P: seeding r's chosen sorted positions
+    __shared__ long long s_ctl[kSsMaxP][3];
+    __shared__ int64_t s_start[kSsMaxP + 1], s_cst[kSsMaxP + 1];
+    __shared__ bool s_done[kSsMaxP];
     const int tid = threadIdx.x, lane = tid & 31;
     const int64_t gtid = (int64_t)blockIdx.x * kSsThreads + tid;
     const int64_t gsz = (int64_t)gridDim.x * kSsThreads;
-    const int64_t n = S.n;
-    const int nb2 = S.nb2, R = S.R;
-    for (int64_t s = gtid; s < n; s += gsz) {
-        const int32_t i = S.order[s];
-        S.xs[s] = S.x[i];
-        S.rank[i] = (int32_t)s;
-    }
-    for (int r = 0; r < R; ++r) {
-        const double c0 = S.x[S.first[r]];
-        double *d2 = S.d2 + r * S.sd2;
-        for (int64_t i = gtid; i < n; i += gsz) {
-            const double d = S.x[i] - c0;
-            d2[i] = d * d;
+    const int P = S.P;
+    for (int r = 0; r < P; ++r) {
+        const SsProb &Q = S.pr[r];
+        const double c0 = Q.x[Q.first];
+        for (int64_t s = gtid; s < Q.n; s += gsz) {
+            const int32_t i = Q.order[s];
+            Q.xs[s] = Q.x[i];
+            Q.rank[i] = (int32_t)s;
         }
-        for (int64_t b = gtid; b < nb2; b += gsz) S.dmask[(int64_t)r * S.sb2 + b] = 0ull;
+        for (int64_t i = gtid; i < Q.n; i += gsz) {
+            const double d = Q.x[i] - c0;
+            Q.d2[i] = d * d;
+        }
+        for (int64_t b = gtid; b < Q.nb2; b += gsz) Q.dmask[b] = 0ull;
         if (gtid == 0) {
-            S.centers[(int64_t)r * S.k] = c0;
-            S.dcount[2 * r] = S.dcount[2 * r + 1] = 0;
-            S.ctl[4 * r + 3] = 0;  // published step
+            Q.centers[0] = c0;
+            Q.dcount[0] = Q.dcount[1] = 0;
+            Q.ctl[3] = 0;  // published step
         }
     }
     if (gtid == 0) S.arrive[0] = 0;  // CTAs done re-summing, cumulative
-    if (tid < kSsMaxR) s_done[tid] = false;
+    if (tid < kSsMaxP) s_done[tid] = false;
     grid.sync();
-    for (int64_t q = gtid; q < (int64_t)R * S.nb1; q += gsz) {
-        const int r = (int)(q / S.nb1);
-        const int64_t blk = q - (int64_t)r * S.nb1;
-        S.bs1[r * S.sb1 + blk] = ss_block_sum(S.d2 + r * S.sd2, n, blk);
+    for (int r = 0; r < P; ++r) {
+        const SsProb &Q = S.pr[r];
+        for (int64_t blk = gtid; blk < Q.nb1; blk += gsz) Q.bs1[blk] = ss_block_sum(Q.d2, Q.n, blk);
     }
     grid.sync();
-    for (int64_t q = gtid >> 5; q < (int64_t)R * nb2; q += gsz >> 5) {  // one warp each, as re-summed
-        const int r = (int)(q / nb2);
-        const int64_t sp = q - (int64_t)r * nb2;
-        const double *bs1 = S.bs1 + r * S.sb1;
-        const int64_t b0 = sp * kSsSup + lane, b1 = b0 + 32;
-        const double a = b0 < S.nb1 ? __ldcg(bs1 + b0) : 0.0;
-        const double b = b1 < S.nb1 ? __ldcg(bs1 + b1) : 0.0;
-        const double t = warp_tree_sum(a + b);
-        if (lane == 0) S.bs2[(int64_t)r * S.sb2 + sp] = t;
+    for (int r = 0; r < P; ++r) {  // one warp per super-block, as re-summed
+        const SsProb &Q = S.pr[r];
+        for (int64_t sp = gtid >> 5; sp < Q.nb2; sp += gsz >> 5) {
+            const int64_t b0 = sp * kSsSup + lane, b1 = b0 + 32;
+            const double a = b0 < Q.nb1 ? __ldcg(Q.bs1 + b0) : 0.0;
+            const double b = b1 < Q.nb1 ? __ldcg(Q.bs1 + b1) : 0.0;
+            const double t = warp_tree_sum(a + b);
+            if (lane == 0) Q.bs2[sp] = t;
+        }
     }
-    if (blockIdx.x < R && tid == 0) s_chosen[0] = __ldcg(S.rank + S.first[blockIdx.x]);
+    if (blockIdx.x < P && tid == 0) s_chosen[0] = __ldcg(S.pr[blockIdx.x].rank + S.pr[blockIdx.x].first);
     grid.sync();
     int nch = 1;
     const bool prof = blockIdx.x == 0 && tid == 0;
@@ -940,53 +941,56 @@ __global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S
     };
     for (int step = 1; step < S.k; ++step) {
         const int buf = step & 1;
-        if (blockIdx.x < R) {
+        if (blockIdx.x < P) {
             // ---- CTA r picks seeding r's centre (every CTA has arrived after
             // re-summing the previous step's marked blocks)
             const int r = blockIdx.x;
-            long long j = -1, L = -1, Rr = n;
-            if (!s_done[r]) ss_pick(S, r, step, s_chosen, nch, j, L, Rr);
+            const SsProb &Q = S.pr[r];
+            long long j = -1, L = -1, Rr = Q.n;
+            if (!s_done[r]) ss_pick(Q, step, s_chosen, nch, j, L, Rr);
             ++nch;
             if (tid == 0) {  // publish (j = -1: all mass on chosen centres)
-                if (j >= 0) S.centers[(int64_t)r * S.k + step] = S.x[j];
-                S.ctl[4 * r] = j;
-                S.ctl[4 * r + 1] = L;
-                S.ctl[4 * r + 2] = Rr;
+                if (j >= 0) Q.centers[step] = Q.x[j];
+                Q.ctl[0] = j;
+                Q.ctl[1] = L;
+                Q.ctl[2] = Rr;
                 __threadfence();
-                atomicExch((unsigned long long *)(S.ctl + 4 * r + 3), (unsigned long long)step);
+                atomicExch((unsigned long long *)(Q.ctl + 3), (unsigned long long)step);
             }
         }
         mark(0);
         // ---- every CTA: the published picks
-        if (tid < R) {
-            while (ld_volatile_s64(S.ctl + 4 * tid + 3) < step) {
+        for (int r = tid; r < P; r += kSsThreads) {
+            const SsProb &Q = S.pr[r];
+            while (ld_volatile_s64(Q.ctl + 3) < step) {
             }
             __threadfence();
-            s_ctl[tid][0] = ld_volatile_s64(S.ctl + 4 * tid);
-            s_ctl[tid][1] = ld_volatile_s64(S.ctl + 4 * tid + 1);
-            s_ctl[tid][2] = ld_volatile_s64(S.ctl + 4 * tid + 2);
+            s_ctl[r][0] = ld_volatile_s64(Q.ctl);
+            s_ctl[r][1] = ld_volatile_s64(Q.ctl + 1);
+            s_ctl[r][2] = ld_volatile_s64(Q.ctl + 2);
         }
         __syncthreads();
         mark(1);
         if (tid == 0) {  // range offsets of the seedings still running
             int64_t t = 0;
-            for (int r = 0; r < R; ++r) {
+            for (int r = 0; r < P; ++r) {
                 s_start[r] = t;
                 if (s_ctl[r][0] >= 0) t += s_ctl[r][2] - s_ctl[r][1] - 1;
             }
-            s_start[R] = t;
+            s_start[P] = t;
         }
-        for (int r = 0; r < R; ++r)
-            if (s_ctl[r][0] < 0 && !s_done[r] && blockIdx.x == r) {  // the reference repeats c0
-                const double c0 = S.x[S.first[r]];
-                for (int q = step + tid; q < S.k; q += kSsThreads) S.centers[(int64_t)r * S.k + q] = c0;
-            }
+        if (blockIdx.x < P && s_ctl[blockIdx.x][0] < 0 && !s_done[blockIdx.x]) {
+            const SsProb &Q = S.pr[blockIdx.x];  // the reference repeats c0
+            const double c0 = Q.x[Q.first];
+            for (int q = step + tid; q < S.k; q += kSsThreads) Q.centers[q] = c0;
+        }
         bool any = false;
-        for (int r = 0; r < R; ++r) any |= s_ctl[r][0] >= 0;
+        for (int r = 0; r < P; ++r) any |= s_ctl[r][0] >= 0;
         __syncthreads();
-        if (tid < R && s_ctl[tid][0] < 0) s_done[tid] = true;
+        for (int r = tid; r < P; r += kSsThreads)
+            if (s_ctl[r][0] < 0) s_done[r] = true;
         if (!any) return;  // every seeding done (uniform over the grid)
-        const int64_t tot_len = s_start[R];
+        const int64_t tot_len = s_start[P];
         // ---- d2 = min(d2, (x - c)^2) over each seeding's (L, R); a lowered
         // block is marked in its super-block's mask, which joins the list once
         {
@@ -999,23 +1003,22 @@ __global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S
                     while (s_start[r + 1] <= g) ++r;
                     rbeg = s_start[r];
                     rend = s_start[r + 1];
-                    c = S.x[s_ctl[r][0]];
+                    c = S.pr[r].x[s_ctl[r][0]];
                 }
+                const SsProb &Q = S.pr[r];
                 const int64_t s = s_ctl[r][1] + 1 + (g - rbeg);
-                double *d2 = S.d2 + r * S.sd2;
-                const int32_t i = __ldg(S.order + s);
-                const double d = __ldcg(S.xs + s) - c;
+                const int32_t i = __ldg(Q.order + s);
+                const double d = __ldcg(Q.xs + s) - c;
                 const double nv = d * d;
-                if (nv < __ldcg(d2 + i)) {
-                    d2[i] = nv;
+                if (nv < __ldcg(Q.d2 + i)) {
+                    Q.d2[i] = nv;
                     const int64_t blk = i / kSsBlk;
                     const int sp = (int)(blk / kSsSup);
-                    unsigned long long *dm = S.dmask + (int64_t)r * S.sb2 + sp;
+                    unsigned long long *dm = Q.dmask + sp;
                     const unsigned long long bit = 1ull << (blk % kSsSup);
                     if (!(__ldcg(dm) & bit)) {
                         const unsigned long long old = atomicOr(dm, bit);
-                        if (old == 0ull)
-                            S.dlist[(int64_t)(2 * r + buf) * nb2 + atomicAdd(S.dcount + 2 * r + buf, 1)] = sp;
+                        if (old == 0ull) Q.dlist[(int64_t)buf * Q.nb2 + atomicAdd(Q.dcount + buf, 1)] = sp;
                     }
                 }
             }
@@ -1028,43 +1031,42 @@ __global__ void __launch_bounds__(kSsThreads, 1) seed_sorted_kernel(SeedSorted S
         {
             if (tid == 0) {
                 s_cst[0] = 0;
-                for (int r = 0; r < R; ++r) s_cst[r + 1] = s_cst[r] + __ldcg(S.dcount + 2 * r + buf);
+                for (int r = 0; r < P; ++r) s_cst[r + 1] = s_cst[r] + __ldcg(S.pr[r].dcount + buf);
             }
             __syncthreads();
             const int64_t wg = gtid >> 5, nwg = gsz >> 5;
             bool wrote = false;
             int r = 0;
-            for (int64_t q = wg; q < s_cst[R]; q += nwg) {
+            for (int64_t q = wg; q < s_cst[P]; q += nwg) {
                 while (s_cst[r + 1] <= q) ++r;
-                const int sp = __ldcg(S.dlist + (int64_t)(2 * r + buf) * nb2 + (q - s_cst[r]));
-                unsigned long long *dm = S.dmask + (int64_t)r * S.sb2 + sp;
+                const SsProb &Q = S.pr[r];
+                const int sp = __ldcg(Q.dlist + (int64_t)buf * Q.nb2 + (q - s_cst[r]));
+                unsigned long long *dm = Q.dmask + sp;
                 const unsigned long long m = __ldcg(dm);
-                double *bs1 = S.bs1 + r * S.sb1;
-                const double *d2 = S.d2 + r * S.sd2;
                 const int64_t b0 = (int64_t)sp * kSsSup + lane, b1 = b0 + 32;
-                double a = b0 < S.nb1 ? __ldcg(bs1 + b0) : 0.0;
-                double b = b1 < S.nb1 ? __ldcg(bs1 + b1) : 0.0;
+                double a = b0 < Q.nb1 ? __ldcg(Q.bs1 + b0) : 0.0;
+                double b = b1 < Q.nb1 ? __ldcg(Q.bs1 + b1) : 0.0;
                 const bool ma = (m >> lane) & 1ull, mb = (m >> (lane + 32)) & 1ull;
-                if (ma) a = ss_block_sum(d2, n, b0);
-                if (mb) b = ss_block_sum(d2, n, b1);
-                if (ma) bs1[b0] = a;
-                if (mb) bs1[b1] = b;
+                if (ma) a = ss_block_sum(Q.d2, Q.n, b0);
+                if (mb) b = ss_block_sum(Q.d2, Q.n, b1);
+                if (ma) Q.bs1[b0] = a;
+                if (mb) Q.bs1[b1] = b;
                 const double t = warp_tree_sum(a + b);
                 if (lane == 0) {
-                    S.bs2[(int64_t)r * S.sb2 + sp] = t;
+                    Q.bs2[sp] = t;
                     *dm = 0ull;
                 }
                 wrote = true;
             }
             if (wrote) __threadfence();
-            if (gtid < R) S.dcount[2 * gtid + (buf ^ 1)] = 0;
+            if (gtid < P) S.pr[gtid].dcount[buf ^ 1] = 0;
         }
         __syncthreads();
         mark(4);
         // ---- arrive; the picking CTAs wait for everyone
         if (tid == 0) {
             atomicAdd(S.arrive, 1u);
-            if (blockIdx.x < R) {
+            if (blockIdx.x < P) {
                 const unsigned want = (unsigned)gridDim.x * (unsigned)step;
                 while (*(volatile unsigned *)S.arrive < want) {
                 }
@@ -1240,85 +1242,77 @@ extern "C" int ivr_kmeans_seed(const double *values, int64_t n, int32_t k, int64
 }
 
 namespace {
-struct SsLayout {
-    size_t xs, rank, d2, bs1, bs2, dmask, dlist, ctrl, total;
-    int64_t nb1, sd2, sb1;
-    int nb2, sb2;
-};
-SsLayout ss_layout(int64_t n, int R) {
-    auto al = [](size_t x) { return (x + 255) & ~(size_t)255; };
-    SsLayout Y{};
-    Y.nb1 = (n + ivr::kSsBlk - 1) / ivr::kSsBlk;
-    Y.nb2 = (int)((Y.nb1 + ivr::kSsSup - 1) / ivr::kSsSup);
-    Y.sd2 = (int64_t)(al(8 * (size_t)n) / 8);
-    Y.sb1 = (int64_t)(al(8 * (size_t)Y.nb1) / 8);
-    Y.sb2 = (int)(al(8 * (size_t)Y.nb2) / 8);
-    size_t o = 0;
-    Y.xs = o;
-    o += al(8 * (size_t)n);
-    Y.rank = o;
-    o += al(4 * (size_t)n);
-    Y.d2 = o;
-    o += 8 * (size_t)Y.sd2 * R;
-    Y.bs1 = o;
-    o += 8 * (size_t)Y.sb1 * R;
-    Y.bs2 = o;
-    o += 8 * (size_t)Y.sb2 * R;
-    Y.dmask = o;
-    o += 8 * (size_t)Y.sb2 * R;
-    Y.dlist = o;
-    o += al(4 * 2 * (size_t)Y.nb2 * R);
-    Y.ctrl = o;  // dcount [2R] | ctl [4R] | arrive | phase_ns [6]
-    o += al(8 * (size_t)ivr::kSsMaxR + 32 * (size_t)ivr::kSsMaxR + 8 + 48);
-    Y.total = o;
-    return Y;
+inline size_t ss_al(size_t x) { return (x + 255) & ~(size_t)255; }
+// per seeding: xs | rank | d2 | block sums | super-block sums | masks | two
+// lists | lengths + published pick
+size_t ss_bytes(int64_t n) {
+    const int64_t nb1 = (n + ivr::kSsBlk - 1) / ivr::kSsBlk;
+    const int64_t nb2 = (nb1 + ivr::kSsSup - 1) / ivr::kSsSup;
+    return 2 * ss_al(8 * (size_t)n) + ss_al(4 * (size_t)n) + ss_al(8 * (size_t)nb1) +
+           2 * ss_al(8 * (size_t)nb2) + ss_al(8 * (size_t)nb2) + 256;
 }
 }  // namespace
 
-extern "C" size_t ivr_kmeans_seed_sorted_workspace_size(int64_t n, int32_t restarts) {
-    const int R = restarts < 1 ? 1 : (restarts > ivr::kSsMaxR ? ivr::kSsMaxR : restarts);
-    return ss_layout(n < 1 ? 1 : n, R).total;
+extern "C" size_t ivr_kmeans_seed_sorted_workspace_size(const ivr_seed_problem *problems,
+                                                       int32_t count) {
+    size_t t = 256;  // arrival counter + phase clock
+    for (int p = 0; problems && p < count; ++p)
+        t += ss_bytes(problems[p].n < 1 ? 1 : problems[p].n);
+    return t;
 }
 
-extern "C" int ivr_kmeans_seed_sorted(const double *values, const int32_t *order, int64_t n,
-                                      int32_t k, int32_t restarts, const int64_t *first,
-                                      const double *u, double *centers, void *workspace,
-                                      size_t workspace_bytes, ivr_stream_t stream) {
+extern "C" int ivr_kmeans_seed_sorted(const ivr_seed_problem *problems, int32_t count, int32_t k,
+                                      void *workspace, size_t workspace_bytes,
+                                      ivr_stream_t stream) {
     using namespace ivr;
-    if (n < 1 || n > 0x7fffffffll || k < 1 || k > kSsMaxK || restarts < 1 ||
-        restarts > kSsMaxR || !values || !order || !first || !centers || (k > 1 && !u) ||
-        !workspace || workspace_bytes < ivr_kmeans_seed_sorted_workspace_size(n, restarts)) {
+    bool ok = problems && count >= 1 && count <= kSsMaxP && k >= 1 && k <= kSsMaxK && workspace &&
+              workspace_bytes >= ivr_kmeans_seed_sorted_workspace_size(problems, count);
+    for (int p = 0; ok && p < count; ++p) {
+        const ivr_seed_problem &q = problems[p];
+        ok = q.values && q.order && q.centers && q.n >= 1 && q.n <= 0x7fffffffll && q.first >= 0 &&
+             q.first < q.n && (k == 1 || q.u);
+    }
+    if (!ok) {
         set_error("ivr_kmeans_seed_sorted: bad argument");
         return IVR_ERR_ARG;
     }
     cudaStream_t st = (cudaStream_t)stream;
-    const SsLayout Y = ss_layout(n, restarts);
     char *w = (char *)workspace;
     SeedSorted S{};
-    S.x = values;
-    S.order = order;
-    S.n = n;
     S.k = k;
-    S.R = restarts;
-    S.first = first;
-    S.u = u;
-    S.centers = centers;
-    S.nb1 = Y.nb1;
-    S.nb2 = Y.nb2;
-    S.sd2 = Y.sd2;
-    S.sb1 = Y.sb1;
-    S.sb2 = Y.sb2;
-    S.xs = (double *)(w + Y.xs);
-    S.rank = (int32_t *)(w + Y.rank);
-    S.d2 = (double *)(w + Y.d2);
-    S.bs1 = (double *)(w + Y.bs1);
-    S.bs2 = (double *)(w + Y.bs2);
-    S.dmask = (unsigned long long *)(w + Y.dmask);
-    S.dlist = (int32_t *)(w + Y.dlist);
-    S.dcount = (int32_t *)(w + Y.ctrl);
-    S.ctl = (long long *)(w + Y.ctrl + 8 * kSsMaxR);
-    S.arrive = (unsigned *)(w + Y.ctrl + 40 * kSsMaxR);
-    S.phase_ns = (unsigned long long *)(w + Y.ctrl + 40 * kSsMaxR + 8);
+    S.P = count;
+    S.arrive = (unsigned *)w;
+    S.phase_ns = (unsigned long long *)(w + 64);
+    w += 256;
+    for (int p = 0; p < count; ++p) {
+        const ivr_seed_problem &q = problems[p];
+        SsProb &Q = S.pr[p];
+        Q.x = q.values;
+        Q.order = q.order;
+        Q.n = q.n;
+        Q.first = q.first;
+        Q.u = q.u;
+        Q.centers = q.centers;
+        Q.nb1 = (q.n + kSsBlk - 1) / kSsBlk;
+        Q.nb2 = (int)((Q.nb1 + kSsSup - 1) / kSsSup);
+        Q.xs = (double *)w;
+        w += ss_al(8 * (size_t)q.n);
+        Q.d2 = (double *)w;
+        w += ss_al(8 * (size_t)q.n);
+        Q.rank = (int32_t *)w;
+        w += ss_al(4 * (size_t)q.n);
+        Q.bs1 = (double *)w;
+        w += ss_al(8 * (size_t)Q.nb1);
+        Q.bs2 = (double *)w;
+        w += ss_al(8 * (size_t)Q.nb2);
+        Q.dmask = (unsigned long long *)w;
+        w += ss_al(8 * (size_t)Q.nb2);
+        Q.dlist = (int32_t *)w;
+        w += ss_al(8 * (size_t)Q.nb2);
+        Q.dcount = (int32_t *)w;
+        Q.ctl = (long long *)(w + 64);
+        w += 256;
+    }
     const size_t smem = 4 * (size_t)k;
     if (smem > 48 * 1024 &&
         cudaFuncSetAttribute(seed_sorted_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
@@ -1328,7 +1322,7 @@ extern "C" int ivr_kmeans_seed_sorted(const double *values, const int32_t *order
     cudaGetDevice(&dev);
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
     cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, seed_sorted_kernel, kSsThreads, smem);
-    if (sms < restarts || per_sm < 1) {
+    if (sms < count || per_sm < 1) {
         set_error("ivr_kmeans_seed_sorted: kernel does not fit on the device");
         return IVR_ERR_ARG;
     }

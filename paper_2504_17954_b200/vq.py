@@ -129,25 +129,38 @@ def _kmeans_dev(x, k, seed=0, restarts=5):
         return distinct.cpu().numpy()
     rng = np.random.default_rng(seed)
     n = x.numel()
+    if not _sorted_seeding(n, k):
+        best, best_sse = None, np.inf
+        for _ in range(restarts):
+            c = _lloyd(x, _seed_plusplus(x, k, rng))
+            sse = _sse(x, c)
+            if sse < best_sse:
+                best, best_sse = c, sse
+        return torch.unique(best).cpu().numpy()
     order = _value_order(x)  # shared by the restarts' seedings
-    seeds = _seed_restarts(x, k, rng, restarts, order)
-    fitted = _lloyd_sets(x, x[order.long()], seeds) if seeds is not None else None
+    seeds = _seed_batch([(x, order, f, u) for f, u in _draw_seeds(n, k, rng, restarts)], k)
+    return _kmeans_finish(x, order, seeds)
+
+
+def _sse(x, c):
+    idx = _assign_idx(x, c)
+    return float(((x - c[idx]) ** 2).sum())
+
+
+def _kmeans_finish(x, order, seeds):
+    """Lloyd for every restart's seeding (one loop, sorted values), then the
+    lowest-SSE restart (the first on ties), as vq.py:47-57."""
+    fitted = _lloyd_sets(x, x[order.long()], torch.stack(list(seeds)))
     best, best_sse = None, np.inf
-    for r in range(restarts):
-        if fitted is not None:
-            c = fitted[r]
-        else:
-            c = _lloyd(x, _seed_plusplus(x, k, rng, order))
-        idx = _assign_idx(x, c)
-        sse = float(((x - c[idx]) ** 2).sum())
+    for r in range(fitted.shape[0]):
+        sse = _sse(x, fitted[r])
         if sse < best_sse:
-            best, best_sse = c, sse
-    del n
+            best, best_sse = fitted[r], sse
     return torch.unique(best).cpu().numpy()
 
 
 SEED_SORTED_MAX_K = 32768
-SEED_SORTED_MAX_R = 8  # seedings per ivr_kmeans_seed_sorted launch
+SEED_SORTED_MAX_P = 64  # seedings per ivr_kmeans_seed_sorted launch
 
 
 def _value_order(x):
@@ -162,36 +175,53 @@ def _sorted_seeding(n, k):
     return k <= SEED_SORTED_MAX_K and n < 2 ** 31
 
 
+def _draw_seeds(n, k, rng, restarts):
+    """The restarts' draws in the reference's order: per restart rng.integers
+    for the first centre, then k - 1 rng.random() (one per rng.choice).  They
+    do not depend on the data, and the distinct-value shortcut in kmeans means
+    no seeding runs out of mass early (which would leave draws unconsumed in
+    the reference)."""
+    out = []
+    for _ in range(restarts):
+        first = int(rng.integers(n))
+        out.append((first, rng.random(k - 1)))  # k == 1: no draw, as the reference
+    return out
+
+
+def _seed_batch(problems, k):
+    """ivr_kmeans_seed_sorted over independent seedings: problems = [(x, order,
+    first, u_host)] (values on the device, int32 value order); up to 64 per
+    launch.  Returns one (k,) centre tensor per problem."""
+    out = []
+    for p0 in range(0, len(problems), SEED_SORTED_MAX_P):
+        chunk = problems[p0:p0 + SEED_SORTED_MAX_P]
+        dev = chunk[0][0].device
+        u = torch.from_numpy(np.concatenate([p[3] for p in chunk] + [np.zeros(1)])).to(dev)
+        cents = torch.empty((len(chunk), k), dtype=torch.float64, device=dev)
+        arr = (L.SeedProblem_t * len(chunk))()
+        for i, (x, order, first, _) in enumerate(chunk):
+            arr[i].values, arr[i].order, arr[i].n = D.ptr(x), D.ptr(order), x.numel()
+            arr[i].first, arr[i].centers = first, D.ptr(cents[i])
+            arr[i].u = u.data_ptr() + 8 * (k - 1) * i
+        nb = int(L.lib().ivr_kmeans_seed_sorted_workspace_size(arr, len(chunk)))
+        ws = torch.empty(nb, dtype=torch.uint8, device=dev)
+        L.check(L.lib().ivr_kmeans_seed_sorted(arr, len(chunk), int(k), D.ptr(ws), nb,
+                                               D.stream_handle()), "ivr_kmeans_seed_sorted")
+        out.extend(cents.unbind(0))
+    return out
+
+
 def _seed_restarts(x, k, rng, restarts, order=None):
-    """All of k-means' restart seedings in one ivr_kmeans_seed_sorted launch
-    (up to 8 per launch).  The draws are taken in the reference's order --
-    per restart rng.integers for the first centre, then one rng.random() per
-    centre -- before any seeding runs: they do not depend on the data, and
-    the distinct-value shortcut in kmeans means no seeding runs out of mass
-    early (which would leave draws unconsumed in the reference).  Returns
-    (restarts, k) centres, or None where the sorted seeding does not apply."""
+    """All of k-means' restart seedings of one attribute in one
+    ivr_kmeans_seed_sorted launch.  Returns (restarts, k) centres, or None
+    where the sorted seeding does not apply."""
     n = x.numel()
     if not _sorted_seeding(n, k):
         return None
     if order is None:
         order = _value_order(x)
-    out = []
-    for r0 in range(0, restarts, SEED_SORTED_MAX_R):
-        R = min(SEED_SORTED_MAX_R, restarts - r0)
-        firsts, us = [], []
-        for _ in range(R):
-            firsts.append(int(rng.integers(n)))
-            us.append(rng.random(k - 1))  # k == 1: no draw, as the reference
-        first = torch.tensor(firsts, dtype=torch.int64, device=x.device)
-        u = torch.from_numpy(np.concatenate(us)).to(x.device)
-        c = torch.empty((R, k), dtype=torch.float64, device=x.device)
-        nb = int(L.lib().ivr_kmeans_seed_sorted_workspace_size(n, R))
-        ws = torch.empty(nb, dtype=torch.uint8, device=x.device)
-        L.check(L.lib().ivr_kmeans_seed_sorted(D.ptr(x), D.ptr(order), n, int(k), R, D.ptr(first),
-                                               D.ptr(u), D.ptr(c), D.ptr(ws), nb,
-                                               D.stream_handle()), "ivr_kmeans_seed_sorted")
-        out.append(c)
-    return torch.cat(out)
+    return torch.stack(_seed_batch([(x, order, f, u) for f, u in _draw_seeds(n, k, rng, restarts)],
+                                   k))
 
 
 def _seed_plusplus(x, k, rng, order=None):
@@ -284,19 +314,36 @@ def _lloyd_sets(x, xs, seeds):
     return torch.sort(c, dim=1).values
 
 
-def quantize_attributes(arrays, k=DEFAULT_CODEBOOK_SIZE, seed=0):
+def quantize_attributes(arrays, k=DEFAULT_CODEBOOK_SIZE, seed=0, restarts=5):
     """vq.py:137-147: per attribute, kmeans over all its components, then the
-    indices (Codebook.encode's values) -- one upload per attribute, indices
-    come back in the codebook's index dtype."""
+    indices (Codebook.encode's values).  One upload per attribute; every
+    attribute's restart seedings share one ivr_kmeans_seed_sorted launch (each
+    attribute draws from its own default_rng(seed), as the reference's
+    per-attribute kmeans call); indices come back in the index dtype."""
     if k < 1:
         raise OutOfRange("codebook size must be >= 1")
-    out = {}
+    prep, problems = [], []
     for name, arr in arrays.items():
         arr = np.asarray(arr, dtype=np.float64)
         if arr.size == 0:
             raise EmptyInput("kmeans needs at least one sample")
         x = D.to_dev(arr.reshape(-1))
-        cb = Codebook(name, _kmeans_dev(x, k, seed=seed))
+        distinct = torch.unique(x)
+        if distinct.numel() <= k:
+            prep.append((name, arr, x, distinct.cpu().numpy(), None, 0))
+        elif not _sorted_seeding(x.numel(), k):
+            prep.append((name, arr, x, _kmeans_dev(x, k, seed, restarts), None, 0))
+        else:
+            order = _value_order(x)
+            draws = _draw_seeds(x.numel(), k, np.random.default_rng(seed), restarts)
+            prep.append((name, arr, x, None, order, len(problems)))
+            problems.extend((x, order, f, u) for f, u in draws)
+    seeds = _seed_batch(problems, k) if problems else []
+    out = {}
+    for name, arr, x, cents, order, p0 in prep:
+        if cents is None:
+            cents = _kmeans_finish(x, order, seeds[p0:p0 + restarts])
+        cb = Codebook(name, cents)
         if cb.k == 1:
             idx = np.zeros(arr.shape, dtype=cb.index_dtype)
         else:

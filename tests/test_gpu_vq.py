@@ -215,3 +215,16 @@ def test_lloyd_sets_match_per_restart_lloyd():
     for r in range(4):
         ref = _lloyd(xd, seeds[r].clone()).cpu().numpy()
         np.testing.assert_allclose(got[r], ref, rtol=1e-9, atol=1e-12, err_msg=str(r))
+
+
+def test_quantize_attributes_batched_seedings_equal_per_attribute_kmeans():
+    """All attributes' restart seedings in one launch (quantize_attributes) ==
+    each attribute's own kmeans call (vq.py:137-147: a fresh default_rng(seed)
+    per attribute), codebook for codebook."""
+    from paper_2504_17954_b200.vq import kmeans, quantize_attributes
+    g = np.random.default_rng(9)
+    arrays = {"q": g.normal(size=(20_000, 4)), "s": g.standard_t(3, size=(15_000, 3)),
+              "o": g.normal(size=9_000) ** 3, "few": np.repeat([0.5, -1.0, 2.0], 50)}
+    q = quantize_attributes(arrays, k=200, seed=3)
+    for name, arr in arrays.items():
+        assert np.array_equal(q[name][0].centroids, kmeans(arr.reshape(-1), 200, seed=3)), name

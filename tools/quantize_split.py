@@ -26,7 +26,7 @@ def timed(name, fn):
 
 
 vq._seed_plusplus = timed("seed", vq._seed_plusplus)
-vq._seed_restarts = timed("seed", vq._seed_restarts)
+vq._seed_batch = timed("seed", vq._seed_batch)
 vq._lloyd = timed("lloyd", vq._lloyd)
 vq._lloyd_sets = timed("lloyd", vq._lloyd_sets)
 vq._value_order = timed("sort", vq._value_order)
