@@ -91,6 +91,10 @@ def test_quantize_dequantize_round_trip():
     assert q.is_quantized and q.shading is None
     for name, (cb, idx) in q.quantized.items():
         assert cb.k <= 64 and idx.dtype == np.uint8
+    for name in ("q_raw", "log_s", "o_logit"):  # the model's dequantized views
+        cb, idx = q.quantized[name]
+        got = getattr(q.geometry, name)
+        assert got.shape == idx.shape and np.array_equal(got, cb.decode(idx)), name
     d = dequantize_model(q)
     for name, (cb, idx) in q.quantized.items():
         owner = d.geometry if name in ("q_raw", "log_s", "o_logit") else d.shading

@@ -1,5 +1,5 @@
 """C5 quantize_model (4M editable model, K=4096) with the host wall time split
-into seeding, Lloyd and the rest (unique, SSE, encode, host copies)."""
+into seeding, Lloyd, value sort, SSE, assign, decode, uploads and the rest."""
 import collections
 import os
 import sys
@@ -30,6 +30,10 @@ vq._seed_batch = timed("seed", vq._seed_batch)
 vq._lloyd = timed("lloyd", vq._lloyd)
 vq._lloyd_sets = timed("lloyd", vq._lloyd_sets)
 vq._value_order = timed("sort", vq._value_order)
+vq._sse = timed("sse", vq._sse)
+vq.assign_device = timed("assign", vq.assign_device)
+vq.Codebook.decode = timed("decode", vq.Codebook.decode)
+vq.D.to_dev = timed("upload", vq.D.to_dev)
 m = editable_model(0, 4_000_000, density=4_000_000)
 vq.quantize_model(m, k=64, seed=0)  # warm-up (kernels, allocator)
 acc.clear()
