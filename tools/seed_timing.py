@@ -52,3 +52,35 @@ for n in (4_000_000, 12_000_000, 16_000_000):
     torch.cuda.synchronize()
     ms2 = (time.perf_counter() - t0) * 1e3
     print("   full-pass seeding ms", round(ms2, 1), "same centres", bool(torch.equal(c[0], c2)))
+
+# every attribute's 5 restart seedings of a 4M editable model in one launch,
+# as quantize_attributes makes them
+from paper_2504_17954_b200.synthetic import editable_model  # noqa: E402
+
+m = editable_model(0, 4_000_000, density=4_000_000)
+probs, keep = [], []
+for name, owner in vq.QUANTIZED_ATTRIBUTES:
+    xa = D.to_dev(np.asarray(getattr(getattr(m, owner), name), dtype=np.float64).reshape(-1))
+    o = vq._value_order(xa)
+    keep.append((xa, o))
+    probs.extend((xa, o, f, u) for f, u in vq._draw_seeds(xa.numel(), K, np.random.default_rng(0), 5))
+u = torch.from_numpy(np.concatenate([p[3] for p in probs])).cuda()
+c = torch.empty((len(probs), K), dtype=torch.float64, device="cuda")
+arr = (L.SeedProblem_t * len(probs))()
+for i, (xa, o, f, _) in enumerate(probs):
+    arr[i].values, arr[i].order, arr[i].n, arr[i].first = D.ptr(xa), D.ptr(o), xa.numel(), f
+    arr[i].u, arr[i].centers = u.data_ptr() + 8 * (K - 1) * i, D.ptr(c[i])
+nb = int(L.lib().ivr_kmeans_seed_sorted_workspace_size(arr, len(probs)))
+ws = torch.empty(nb, dtype=torch.uint8, device="cuda")
+for rep in range(2):
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    L.check(L.lib().ivr_kmeans_seed_sorted(arr, len(probs), K, D.ptr(ws), nb, D.stream_handle()),
+            "s")
+    torch.cuda.synchronize()
+    ms = (time.perf_counter() - t0) * 1e3
+ph = ws[64:64 + 48].cpu().numpy().view(np.uint64) / 1e3 / (K - 1)
+print("4M model,", len(probs), "seedings in one launch: ms", round(ms, 1), "us/centre",
+      round(ms * 1e3 / (K - 1), 2),
+      {a: round(float(b), 2) for a, b in zip(("pick", "wait", "update", "barrier", "resum",
+                                              "arrive"), ph)})
