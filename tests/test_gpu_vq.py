@@ -232,3 +232,35 @@ def test_quantize_attributes_batched_seedings_equal_per_attribute_kmeans():
     q = quantize_attributes(arrays, k=200, seed=3)
     for name, arr in arrays.items():
         assert np.array_equal(q[name][0].centroids, kmeans(arr.reshape(-1), 200, seed=3)), name
+
+
+def test_sorted_lloyd_step_ties_empty_buckets_and_sets():
+    """One ivr_kmeans_lloyd_step_sorted step == vq.py:75-87's step in numpy
+    (searchsorted on the midpoints, bincount means, empty buckets keep their
+    centroid) for values exactly on midpoints, empty buckets and 3 sets."""
+    import torch
+    from paper_2504_17954_b200 import _lib as L
+    from paper_2504_17954_b200 import device as D
+    g = np.random.default_rng(12)
+    x = np.concatenate([g.normal(size=5000), [0.5, 2.0, 2.0, -7.0, 11.0]])
+    sets = np.array([[0.0, 1.0, 3.0, 4.0, 50.0], [-9.0, -8.0, 0.0, 0.25, 0.3],
+                     [-1.0, -1.0, 0.0, 1.0, 1.0]])
+    xs = D.to_dev(np.sort(x))
+    c = D.to_dev(sets.reshape(-1))
+    new = torch.empty_like(c)
+    shift = torch.empty(3, dtype=torch.float64, device=c.device)
+    k = sets.shape[1]
+    nb = int(L.lib().ivr_kmeans_lloyd_sorted_workspace_size(k, 3))
+    ws = torch.empty(nb, dtype=torch.uint8, device=c.device)
+    L.check(L.lib().ivr_kmeans_lloyd_step_sorted(D.ptr(xs), xs.numel(), D.ptr(c), k, 3,
+                                                 D.ptr(new), D.ptr(shift), D.ptr(ws), nb,
+                                                 D.stream_handle()), "lloyd sorted")
+    got = new.cpu().numpy().reshape(3, k)
+    for r in range(3):
+        cen = sets[r]
+        idx = np.searchsorted(0.5 * (cen[1:] + cen[:-1]), x)
+        sums = np.bincount(idx, weights=x, minlength=k)
+        cnt = np.bincount(idx, minlength=k)
+        ref = np.where(cnt > 0, sums / np.maximum(cnt, 1), cen)
+        np.testing.assert_allclose(got[r], ref, rtol=1e-13, atol=1e-15, err_msg=str(r))
+        assert shift[r].item() == pytest.approx(np.abs(ref - cen).max(), rel=1e-12)
