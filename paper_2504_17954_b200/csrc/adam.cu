@@ -23,6 +23,7 @@ struct AdamGroups {
 };
 
 __global__ void __launch_bounds__(256) adam_kernel(AdamGroups A) {
+    ::ivr::pdl_begin();
     if (A.skip && *A.skip) return;
     ivr_adam_group G = A.g[blockIdx.y];
     if (A.sched) {
@@ -93,7 +94,7 @@ int adam_impl(const ivr_adam_group *groups, int32_t n_groups, double beta1, doub
     if (n_groups == 0 || nmax == 0) return IVR_OK;
     int64_t bx = (nmax + 255) / 256;
     if (bx > 148 * 8) bx = 148 * 8;
-    adam_kernel<<<dim3((unsigned)bx, (unsigned)n_groups), 256, 0, (cudaStream_t)stream>>>(A);
+    ivr::launch<3>(adam_kernel, dim3((unsigned)bx, (unsigned)n_groups), 256, 0, (cudaStream_t)stream, A);
     return check_launch("adam_kernel");
 }
 }  // namespace

@@ -133,6 +133,7 @@ constexpr int kBwdWarpW = 8;  // warp footprint 8x4 pixels (as K3)
 template <int KMAX, bool F64, bool GEOM>
 __global__ void __launch_bounds__(128, KMAX <= 4 ? 7 : (KMAX <= 16 ? 6 : 2))
 blend_bwd_kernel(BwdArgs A) {
+    ::ivr::pdl_begin();
     extern __shared__ __align__(16) unsigned char smem[];
     BwdSlots<KMAX, F64> &W = reinterpret_cast<BwdSlots<KMAX, F64> *>(smem)[threadIdx.x >> 5];
 
@@ -410,7 +411,7 @@ int launch_bwd(const BwdArgs &A, int ntiles, bool geom, cudaStream_t st) {
     // half-tile CTAs, as K3 (C4 K4a 0.332 -> 0.326 ms, C3 0.339 -> 0.335 ms)
     constexpr int wpc = 4;
     const int cpt = (kBwdThreads / 32) / wpc;
-    fn<<<ntiles * cpt, 32 * wpc, (sm / (kBwdThreads / 32)) * wpc, st>>>(A);
+    launch<3>(fn, ntiles * cpt, 32 * wpc, (sm / (kBwdThreads / 32)) * wpc, st, A);
     return check_launch("blend_bwd_kernel");
 }
 
@@ -493,6 +494,7 @@ struct BwdConst {
 template <bool GEOM>
 __global__ void __launch_bounds__(128, GEOM ? 4 : 5)
 preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *__restrict__ Pd) {
+    ::ivr::pdl_begin();
     __shared__ ivr_frame_params P;
     __shared__ double s_glob[10];
     extern __shared__ double s_scene[];  // [S][4] per-scene d_c_p (3) + d_scale
@@ -803,6 +805,7 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
 __global__ void __launch_bounds__(256)
 bwd_sums_kernel(const double *part, int nblocks, int nsc, int has_globals, double *d_globals,
                 double *d_c_p, double *d_scale) {
+    ::ivr::pdl_begin();
     __shared__ double s[256];
     const int nsl = 10 + 4 * nsc, slot = blockIdx.x;
     double t = 0.0;
@@ -1016,9 +1019,9 @@ extern "C" int ivr_preprocess_bwd(const ivr_gaussians *g, const ivr_shading *sha
     const unsigned blocks = (unsigned)((g->n + threads - 1) / threads);
     const size_t sm = (size_t)grads->per_scene * 4 * sizeof(double);
     if (geometry)
-        preprocess_bwd_kernel<true><<<blocks, threads, sm, (cudaStream_t)stream>>>(B, Pv, params);
+        ivr::launch<3>(preprocess_bwd_kernel<true>, blocks, threads, sm, (cudaStream_t)stream, B, Pv, params);
     else
-        preprocess_bwd_kernel<false><<<blocks, threads, sm, (cudaStream_t)stream>>>(B, Pv, params);
+        ivr::launch<3>(preprocess_bwd_kernel<false>, blocks, threads, sm, (cudaStream_t)stream, B, Pv, params);
     if (grads->scratch) {
         const int nsl = 10 + 4 * grads->per_scene;
         bwd_sums_kernel<<<nsl, 256, 0, (cudaStream_t)stream>>>(

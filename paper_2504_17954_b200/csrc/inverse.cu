@@ -34,6 +34,7 @@ __global__ void __launch_bounds__(kThreads)
 pack_kernel(ivr_inverse_step A, const double *photo_sums, double numel, double windows,
             const double *d_c_p, const double *d_scale, const double *d_globals,
             const int32_t *n_pairs, int64_t capacity) {
+    ::ivr::pdl_begin();
     const int S = A.n_scenes, N = 4 * S + 10;
     double *g = A.grad;
     for (int j = threadIdx.x; j < N; j += kThreads) {
@@ -60,6 +61,7 @@ __device__ double softplus_d(double x) {  // np.logaddexp(0, x)
 }
 
 __global__ void __launch_bounds__(kThreads) update_kernel(ivr_inverse_step A) {
+    ::ivr::pdl_begin();
     const int S = A.n_scenes, N = 4 * S + 10;
     const int tid = threadIdx.x;
     __shared__ double s_g[4 * kMaxScenes + 10];

@@ -77,10 +77,12 @@ __device__ __forceinline__ void pdl_begin() {
 }
 
 // IVR_PDL: 0 off; 1 (default) K2's chain outside graph capture; 2 K2's chain
-// always; 3 also K1 and K3.  Inside a captured graph the programmatic edges
-// measured neutral for the isolated C2 frame and -3% for the 6-slot frame
-// stream (CTAs waiting at griddepcontrol.wait hold SM slots other frames
-// could use); eager launches gain ~13 us of K2 per frame.
+// always; 3 every kernel launched through here (K1, K3 and the training /
+// inverse step kernels too).  Inside a captured graph the programmatic edges
+// measured neutral for the isolated C2 frame, -3% for the 6-slot frame stream
+// (CTAs waiting at griddepcontrol.wait hold SM slots other frames could use)
+// and -3% / -1% for the C3 / C4 steps; eager launches gain ~13 us of K2 per
+// frame.
 int pdl_level();
 
 // kernel<<<grid, block, smem, stream>>>(args...) with the programmatic

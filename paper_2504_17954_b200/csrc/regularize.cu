@@ -123,6 +123,7 @@ __device__ __forceinline__ double edge_weight(const Args &A, int y, int x) {
 }
 
 __global__ void __launch_bounds__(kThreads) mask_count_kernel(Args A) {
+    ::ivr::pdl_begin();
     __shared__ int s_c;
     if (threadIdx.x == 0) s_c = 0;
     __syncthreads();
@@ -151,6 +152,7 @@ __device__ __forceinline__ double sgn(double v) { return v > 0.0 ? 1.0 : (v < 0.
 // rendered maps and coalesced stores of d_out, instead of K scattered 4-byte
 // accesses per pixel at a 4K-byte stride.
 __global__ void __launch_bounds__(kThreads) reg_grad_kernel(Args A) {
+    ::ivr::pdl_begin();
     __shared__ double s_red[kThreads / 32];
     extern __shared__ float s_reg[];  // [kThreads * K] maps in, [kThreads * K] d_out
     const int tid = threadIdx.x;
@@ -242,6 +244,7 @@ __global__ void __launch_bounds__(kThreads) reg_grad_kernel(Args A) {
 // terms[0] = normal loss, [1] = mean |delta_c|, [2] = bilateral sum (all maps)
 __global__ void __launch_bounds__(kThreads) reg_finish_kernel(const double *part, int nb, int64_t npx,
                                                               double *terms) {
+    ::ivr::pdl_begin();
     __shared__ double s_red[kThreads / 32];
     double a = 0.0, b = 0.0, c = 0.0;
     for (int i = threadIdx.x; i < nb; i += kThreads) {
@@ -314,11 +317,11 @@ extern "C" int ivr_regularize(const float *out, int32_t k, int32_t height, int32
     A.nmap = reinterpret_cast<double4 *>(((uintptr_t)(A.wmap + npx) + 31) & ~(uintptr_t)31);
     if (cudaMemsetAsync(A.mask_count, 0, sizeof(int), st) != cudaSuccess)
         return check_launch("ivr_regularize memset");
-    if (w_normal > 0.0 || (w_bil > 0.0 && n_bil > 0)) mask_count_kernel<<<nb, kThreads, 0, st>>>(A);
+    if (w_normal > 0.0 || (w_bil > 0.0 && n_bil > 0)) ivr::launch<3>(mask_count_kernel, nb, kThreads, 0, st, A);
     const size_t sm_grad = 2 * (size_t)kThreads * k * sizeof(float);
     if (sm_grad > 48 * 1024)
         cudaFuncSetAttribute(reg_grad_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)sm_grad);
-    reg_grad_kernel<<<nb, kThreads, sm_grad, st>>>(A);
-    reg_finish_kernel<<<1, kThreads, 0, st>>>(A.part, nb, npx, terms);
+    ivr::launch<3>(reg_grad_kernel, nb, kThreads, sm_grad, st, A);
+    ivr::launch<3>(reg_finish_kernel, 1, kThreads, 0, st, (const double *)A.part, nb, npx, terms);
     return check_launch("ivr_regularize");
 }

@@ -68,6 +68,7 @@ __device__ __forceinline__ double block_sum(double v, double *s_red) {
 
 // A: window statistics -> SSIM partial sum + the three partial maps
 __global__ void __launch_bounds__(kThreads) ssim_window_kernel(Args A) {
+    ::ivr::pdl_begin();
     extern __shared__ __align__(16) double sm[];
     double *sx = sm, *sy = sx + IH * IW;
     double *hq = sy + IH * IW;  // [5][IH][TW]
@@ -183,6 +184,7 @@ __global__ void __launch_bounds__(kThreads) ssim_window_kernel(Args A) {
 // 0.158 ms, C3 losses 0.282 -> 0.269 ms)
 template <bool SSIM>
 __global__ void __launch_bounds__(kThreads, 3) ssim_grad_kernel(Args A) {
+    ::ivr::pdl_begin();
     extern __shared__ __align__(16) double sm[];
     double *mq = sm;                    // [3][IH][IW]
     double *hq = mq + 3 * IH * IW;      // [3][IH][TW]
@@ -287,6 +289,7 @@ __global__ void __launch_bounds__(kThreads, 3) ssim_grad_kernel(Args A) {
 __global__ void __launch_bounds__(kThreads) ssim_finish_kernel(const double *partA, int na,
                                                                const double *partB, int nb,
                                                                double *sums) {
+    ::ivr::pdl_begin();
     __shared__ double s_red[kThreads / 32];
     double a = 0.0, b = 0.0;
     for (int i = threadIdx.x; i < na; i += kThreads) a += partA[i];
@@ -380,16 +383,16 @@ static int photometric(const double *pred, const float *frame, int32_t frame_k,
     if (with_ssim) {
         cudaFuncSetAttribute(ssim_window_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smA);
         const dim3 gA((A.Wv + TW - 1) / TW, (A.Hv + TH - 1) / TH);
-        ssim_window_kernel<<<gA, kThreads, smA, st>>>(A);
+        ivr::launch<3>(ssim_window_kernel, gA, kThreads, smA, st, A);
         na = p.na;
         cudaFuncSetAttribute(ssim_grad_kernel<true>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smB);
     }
     const dim3 gB((width + TW - 1) / TW, (height + TH - 1) / TH);
     if (with_ssim)
-        ssim_grad_kernel<true><<<gB, kThreads, smB, st>>>(A);
+        ivr::launch<3>(ssim_grad_kernel<true>, gB, kThreads, smB, st, A);
     else
-        ssim_grad_kernel<false><<<gB, kThreads, 0, st>>>(A);
-    ssim_finish_kernel<<<1, kThreads, 0, st>>>(A.partA, na, A.partB, p.nb, sums);
+        ivr::launch<3>(ssim_grad_kernel<false>, gB, kThreads, 0, st, A);
+    ivr::launch<3>(ssim_finish_kernel, 1, kThreads, 0, st, (const double *)A.partA, na, (const double *)A.partB, p.nb, sums);
     return check_launch("ivr_photometric_loss");
 }
 

@@ -28,6 +28,7 @@ constexpr int kMaxBlocks = 148 * 4;  // fixed grid: deterministic partial sums
 __global__ void __launch_bounds__(kThreads)
 attrs_kernel(int64_t n, const double *ka, const double *kd, const double *ks, const double *lb,
              double *oa, double *od, double *os, double *ob) {
+    ::ivr::pdl_begin();
     for (int64_t i = (int64_t)blockIdx.x * kThreads + threadIdx.x; i < n;
          i += (int64_t)gridDim.x * kThreads) {
         oa[i] = sigmoid_ref(ka[i]);
@@ -44,6 +45,7 @@ __device__ __forceinline__ double dsig(double d, double raw) {
 }
 
 __global__ void __launch_bounds__(kThreads) assemble_kernel(ivr_step_grads A) {
+    ::ivr::pdl_begin();
     __shared__ double s_red[kThreads / 32];
     double osum = 0.0;
     const int K = A.k;
@@ -104,6 +106,7 @@ constexpr int kFinThreads = 256;
 
 __global__ void __launch_bounds__(kFinThreads)
 finalize_kernel(ivr_loss_terms T, double *loss, int64_t *state, double *last_bad) {
+    ::ivr::pdl_begin();
     // opacity partials: fixed strided split + fixed-order tree (deterministic);
     // one thread summing them serially put ~25 us of dependent loads on the
     // step's critical path
@@ -161,7 +164,7 @@ extern "C" int ivr_stage2_attrs(int64_t n, const double *k_a_raw, const double *
         return IVR_ERR_ARG;
     }
     if (n == 0) return IVR_OK;
-    attrs_kernel<<<grid_for(n), kThreads, 0, (cudaStream_t)stream>>>(n, k_a_raw, k_d_raw, k_s_raw,
+    ivr::launch<3>(attrs_kernel, grid_for(n), kThreads, 0, (cudaStream_t)stream, n, k_a_raw, k_d_raw, k_s_raw,
                                                                      log_beta, k_a, k_d, k_s, beta);
     return ivr::check_launch("attrs_kernel");
 }
@@ -180,7 +183,7 @@ extern "C" int ivr_step_assemble(const ivr_step_grads *a, ivr_stream_t stream) {
         return IVR_ERR_ARG;
     }
     if (a->n == 0) return IVR_OK;
-    assemble_kernel<<<grid_for(a->n), kThreads, 0, (cudaStream_t)stream>>>(*a);
+    ivr::launch<3>(assemble_kernel, grid_for(a->n), kThreads, 0, (cudaStream_t)stream, *a);
     return ivr::check_launch("assemble_kernel");
 }
 
@@ -190,6 +193,6 @@ extern "C" int ivr_loss_finalize(const ivr_loss_terms *t, double *loss, int64_t 
         ivr::set_error("ivr_loss_finalize: bad argument");
         return IVR_ERR_ARG;
     }
-    finalize_kernel<<<1, kFinThreads, 0, (cudaStream_t)stream>>>(*t, loss, state, last_bad);
+    ivr::launch<3>(finalize_kernel, 1, kFinThreads, 0, (cudaStream_t)stream, *t, loss, state, last_bad);
     return ivr::check_launch("finalize_kernel");
 }
