@@ -1,4 +1,5 @@
-// K5/K6 -- scalar-codebook VQ assign and decode (bandwidth kernels).
+// K5/K6 -- scalar-codebook VQ assign and decode (bandwidth kernels), and the
+// k-means that builds the codebooks (K5s: k-means++ seeding, Lloyd steps).
 //
 // The reference's codebooks are 1-D (one scalar codebook per attribute,
 // shared across components; vq.py:1-6, 137-147) and assignment is
