@@ -264,3 +264,27 @@ def test_sorted_lloyd_step_ties_empty_buckets_and_sets():
         ref = np.where(cnt > 0, sums / np.maximum(cnt, 1), cen)
         np.testing.assert_allclose(got[r], ref, rtol=1e-13, atol=1e-15, err_msg=str(r))
         assert shift[r].item() == pytest.approx(np.abs(ref - cen).max(), rel=1e-12)
+
+
+@pytest.mark.parametrize("n,k,dist", [(200_000, 1000, "t2"), (120_000, 2048, "mixture")])
+def test_seed_plusplus_follows_the_reference_stream_at_scale(n, k, dist):
+    """The sorted seeding against the reference's own _seed_plusplus loop
+    (vq.py:60-72, numpy rng.choice) on heavier inputs: every centre equal."""
+    from paper_2504_17954_b200.device import to_dev
+    from paper_2504_17954_b200.vq import _seed_plusplus
+    g = np.random.default_rng(n)
+    if dist == "t2":
+        x = g.standard_t(2, size=n)
+    else:
+        x = np.concatenate([g.normal(-3, 0.1, n // 3), g.exponential(2.0, n // 3),
+                            g.integers(0, 500, n - 2 * (n // 3)) * 0.01])
+        g.shuffle(x)
+    rng = np.random.default_rng(7)
+    ref = np.empty(k)
+    ref[0] = x[rng.integers(x.size)]
+    d2 = (x - ref[0]) ** 2
+    for i in range(1, k):
+        ref[i] = x[rng.choice(x.size, p=d2 / d2.sum())]
+        d2 = np.minimum(d2, (x - ref[i]) ** 2)
+    got = _seed_plusplus(to_dev(x), k, np.random.default_rng(7)).cpu().numpy()
+    assert np.array_equal(got, ref)
