@@ -102,9 +102,18 @@ class Codebook:
         indices = np.asarray(indices)
         if indices.size == 0:
             return np.zeros(indices.shape)
-        if int(indices.max()) >= self.k:  # also checked on device below
+        if indices.dtype not in (np.uint8, np.uint16) and int(indices.max()) >= self.k:
+            # wider or signed index types: a value >= 2^16 would wrap below
             raise CorruptIndex(f"codebook {self.name!r}: index {int(indices.max())} >= K={self.k}")
-        idx = D.to_dev(indices.reshape(-1).astype(np.uint16).view(np.int16), torch.int16)
+        if indices.dtype not in (np.uint8, np.uint16) and int(indices.min()) < 0:
+            # the reference indexes centroids[indices] with numpy semantics:
+            # -k <= i < 0 counts from the end, below that numpy's IndexError
+            if int(indices.min()) < -self.k:
+                raise IndexError(f"index {int(indices.min())} is out of bounds for axis 0 "
+                                 f"with size {self.k}")
+            indices = np.where(indices < 0, indices + self.k, indices)
+        flat = np.ascontiguousarray(indices.reshape(-1)).astype(np.uint16, copy=False)
+        idx = D.to_dev(flat.view(np.int16), torch.int16)  # out-of-range: the device check
         out, bad = decode_device(idx, D.to_dev(self.centroids))
         if int(bad.item()) >= 0:
             raise CorruptIndex(f"codebook {self.name!r}: index {int(bad.item())} >= K={self.k}")

@@ -66,6 +66,12 @@ def test_decode_and_corrupt_index():
     assert np.array_equal(cb.decode(idx), cb.centroids[idx.astype(np.int64)])
     with pytest.raises(CorruptIndex):
         cb.decode(np.array([0, 3], dtype=np.uint8))
+    with pytest.raises(CorruptIndex):  # wider types: checked before the uint16 upload
+        cb.decode(np.array([0, 65536 + 1], dtype=np.int64))
+    # signed indices follow numpy indexing, as the reference's centroids[indices]
+    assert np.array_equal(cb.decode(np.array([-1, -3, 2])), cb.centroids[[-1, -3, 2]])
+    with pytest.raises(IndexError):
+        cb.decode(np.array([0, -4]))
 
 
 def test_kmeans_matches_reference():
