@@ -47,8 +47,8 @@ def fill_pairs(offsets, tx0, tx1, ty0, ty1, ntx, pair_tile, pair_splat):
     w = (_t(tx1, torch.int64) - _t(tx0, torch.int64) + 1)[splat]
     ty = _t(ty0, torch.int64)[splat] + q // w
     tx = _t(tx0, torch.int64)[splat] + q % w
-    pair_tile[:] = (ty * int(ntx) + tx).cpu().numpy()
-    pair_splat[:] = splat.cpu().numpy()
+    pair_tile[:] = D.to_host(ty * int(ntx) + tx)
+    pair_splat[:] = D.to_host(splat)
 
 
 def _records(mean2d, conic, opacity, values):
@@ -108,10 +108,10 @@ def composite_forward(tile_ranges, pair_splat, mean2d, conic, opacity, values, w
     _check_tile(tile_size)
     tr, ps, R, o32, o64, cnt, last, tf, K, nty = _forward(
         tile_ranges, pair_splat, mean2d, conic, opacity, values, width, height, ntx)
-    out[...] = (o64 if o64 is not None else o32).cpu().numpy().astype(out.dtype, copy=False)
-    contrib[...] = cnt.cpu().numpy()
-    last_pos[...] = last.cpu().numpy()
-    t_final[...] = tf.cpu().numpy()
+    out[...] = D.to_host(o64 if o64 is not None else o32).astype(out.dtype, copy=False)
+    contrib[...] = D.to_host(cnt)
+    last_pos[...] = D.to_host(last)
+    t_final[...] = D.to_host(tf)
 
 
 def composite_backward(tile_ranges, pair_splat, mean2d, conic, opacity, values, width, height,

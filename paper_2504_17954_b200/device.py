@@ -32,6 +32,33 @@ def ptr(t):
     return None if t is None else ctypes.c_void_p(t.data_ptr())
 
 
+def _pinned_copy(t):
+    h = torch.empty(t.shape, dtype=t.dtype, pin_memory=True)  # torch's cached page-locked blocks
+    h.copy_(t)
+    return h
+
+
+def to_host(t):
+    """Device tensor -> (ordinary) numpy array through a page-locked staging
+    block from torch's caching host allocator: a pageable D2H runs at ~2 GB/s
+    on these hosts (128 MB: 57 ms), a pinned one at ~55 GB/s (2.3 ms) plus the
+    host copy out of the staging block; the block goes back to the cache, so
+    no page-locked memory stays attached to the returned array."""
+    if t.device.type != "cuda":
+        return t.numpy()
+    h = _pinned_copy(t)
+    out = np.empty(tuple(t.shape), dtype=h.numpy().dtype)
+    np.copyto(out, h.numpy())
+    return out
+
+
+def to_host_bytes(t):
+    """Device tensor -> bytes through a page-locked staging block (to_host)."""
+    if t.device.type != "cuda":
+        return t.numpy().tobytes()
+    return _pinned_copy(t).numpy().tobytes()
+
+
 def to_dev(a, dtype=torch.float64, device=None):
     """Host array -> contiguous device tensor (no copy if already on device)."""
     if a is None:

@@ -240,7 +240,7 @@ def render_view_device(volume, tf, cam, light, material=None, step_scale=0.5, de
 
 def render_view(volume, tf, cam, light, material=None, step_scale=0.5):
     """Ray-march a full RGBA image for one camera (dvr.py:424-452)."""
-    return render_view_device(volume, tf, cam, light, material, step_scale).cpu().numpy()
+    return D.to_host(render_view_device(volume, tf, cam, light, material, step_scale))
 
 
 def raymarch_pixel(volume, tf, cam, light, pixel, material=None, step_scale=0.5):

@@ -108,8 +108,8 @@ def rasterize_forward(geom, colors, cam, channels=("color", "alpha"), attrs=None
     # the returned state owns its buffers (a later call must not overwrite them)
     F = D.rasterize_device(dg, cam, K, cols, D.Workspace(dg.device), colors=colors_dev,
                            attrs=attrs_dev, f64=f64, want_state=True, exact=exact)
-    out = (F.out64 if f64 else F.out).cpu().numpy().astype(dtype, copy=False)
-    contrib = F.contrib.cpu().numpy()
+    out = D.to_host(F.out64 if f64 else F.out).astype(dtype, copy=False)
+    contrib = D.to_host(F.contrib)
     state.update(frame=F, dg=dg, empty=False)
     return _unpack(out, layout, contrib), state
 

@@ -162,7 +162,7 @@ class DisplayRenderer:
     def float_image(self, cam, mode="shaded"):
         """The float image render_mode_image returns (host float64)."""
         out, cols, K = self._render(cam, mode)
-        o = out.cpu().numpy()
+        o = D.to_host(out)
         cc, ca, cd, cn = cols
         if mode in ("shaded", "ambient", "diffuse", "specular"):
             return np.concatenate([np.clip(o[..., cc:cc + 3], 0, 1), o[..., ca:ca + 1]], axis=-1)
@@ -177,7 +177,7 @@ class DisplayRenderer:
         device and copied to the host once."""
         img = self.frame_u8(cam, mode)
         if fmt == "raw":
-            return img.cpu().numpy().tobytes()
+            return D.to_host_bytes(img)
         if fmt != "png":
             raise OutOfRange(f"unknown format {fmt!r}")
         H, W = img.shape[0], img.shape[1]
@@ -187,4 +187,4 @@ class DisplayRenderer:
         ws = torch.empty(64, dtype=torch.uint8, device=self.dev)
         L.check(L.lib().ivr_png_encode(D.ptr(img), H, W, C, D.ptr(buf), size, D.ptr(ws),
                                        D.stream_handle()), "ivr_png_encode")
-        return buf.cpu().numpy().tobytes()
+        return D.to_host_bytes(buf)

@@ -326,8 +326,8 @@ class DeviceScene:
             H, W = cam.height, cam.width
             K = sum(w for _, w in F.layout)
             return _unpack(np.zeros((H, W, K), dtype=dtype), F.layout, np.zeros((H, W), np.int32))
-        out = (F.out64 if F.f64 else F.out).cpu().numpy().astype(dtype, copy=False)
-        return _unpack(out, F.layout, F.contrib.cpu().numpy())
+        out = D.to_host(F.out64 if F.f64 else F.out).astype(dtype, copy=False)
+        return _unpack(out, F.layout, D.to_host(F.contrib))
 
 
 class FrameGraph:

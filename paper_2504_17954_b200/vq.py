@@ -66,7 +66,7 @@ def assign_nearest(values, centroids):
     if values.size == 0:
         return np.zeros(values.shape, dtype=np.int64)
     idx = assign_device(D.to_dev(values.reshape(-1)), D.to_dev(centroids))
-    return (idx.cpu().numpy().view(np.uint16).astype(np.int64)).reshape(values.shape)
+    return D.to_host(idx).view(np.uint16).astype(np.int64).reshape(values.shape)
 
 
 def _index_dtype(k):
@@ -117,7 +117,7 @@ class Codebook:
         out, bad = decode_device(idx, D.to_dev(self.centroids))
         if int(bad.item()) >= 0:
             raise CorruptIndex(f"codebook {self.name!r}: index {int(bad.item())} >= K={self.k}")
-        return out.cpu().numpy().reshape(indices.shape)
+        return D.to_host(out).reshape(indices.shape)
 
 
 def kmeans(samples, k, seed=0, restarts=5):
@@ -356,7 +356,7 @@ def quantize_attributes(arrays, k=DEFAULT_CODEBOOK_SIZE, seed=0, restarts=5):
         if cb.k == 1:
             idx = np.zeros(arr.shape, dtype=cb.index_dtype)
         else:
-            idx = assign_device(x, D.to_dev(cb.centroids)).cpu().numpy().view(np.uint16)
+            idx = D.to_host(assign_device(x, D.to_dev(cb.centroids))).view(np.uint16)
             idx = idx.astype(cb.index_dtype, copy=False).reshape(arr.shape)
         out[name] = (cb, idx)
     return out
