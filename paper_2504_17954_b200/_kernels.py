@@ -140,7 +140,7 @@ def composite_backward(tile_ranges, pair_splat, mean2d, conic, opacity, values, 
                                         int(width), int(height), D.ptr(tfd), D.ptr(last), D.ptr(d),
                                         P, D.ptr(ws), nb, D.ptr(g),
                                         D.stream_handle()), "ivr_blend_bwd_pairs")
-    h = g.double().cpu().numpy()
+    h = D.to_host(g.double())
     pair_dv += h[:, :K]
     pair_dmean += h[:, K:K + 2]
     pair_dconic += h[:, K + 2:K + 5]

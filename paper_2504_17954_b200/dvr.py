@@ -275,7 +275,7 @@ def generate_dataset(volume, tf, cameras, light, out_dir, material=None, step_sc
     images, entries = [], []
     for idx, cam in enumerate(cameras):
         rgba = render_view_device(volume, tf, cam, light, material, step_scale, vals)
-        u8 = (rgba * 255.0).round_().clamp_(0, 255).to(torch.uint8).cpu().numpy()
+        u8 = D.to_host((rgba * 255.0).round_().clamp_(0, 255).to(torch.uint8))
         name = "view_%04d.png" % idx
         Image.fromarray(u8, mode="RGBA").save(os.path.join(out_dir, name))
         images.append(u8 / 255.0)

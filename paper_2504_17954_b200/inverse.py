@@ -183,7 +183,7 @@ def render_with_transform(scene, params, cam, dtype=np.float32):
     (inverse.py:154-158)."""
     fit = InverseFitter(scene, [], [], exact=True)
     F = fit.render(params, cam, dtype=dtype)
-    return (F.out64 if F.f64 else F.out).cpu().numpy().astype(dtype, copy=False)
+    return D.to_host(F.out64 if F.f64 else F.out).astype(dtype, copy=False)
 
 
 def reduce_views(total, loss_sum, n_views, dist=None, group=None):

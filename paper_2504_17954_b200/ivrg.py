@@ -234,7 +234,7 @@ class DeviceModelFile:
         from .scene import STAGE_BASE, BasicSceneModel, ComposedScene
         from .shading import ShadingAttributes
         from .vq import Codebook
-        host = lambda t, a, b: t[a:b].cpu().numpy()  # noqa: E731
+        host = lambda t, a, b: D.to_host(t[a:b])  # noqa: E731
         out = []
         for m in self.models:
             a, b = m.rows

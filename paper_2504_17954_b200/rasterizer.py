@@ -176,9 +176,9 @@ def rasterize_backward(state, d_maps):
     D.raise_if_bad(bad, n, ("d_mu", "d_q_raw", "d_log_s", "d_o_logit", "d_n_raw", "d_colors"))
     for key, w in (("d_mu", 3), ("d_q_raw", 4), ("d_log_s", 3), ("d_n_raw", 3), ("d_colors", 3),
                    ("d_mean2d", 2)):
-        grads[key] = out[key].cpu().numpy().reshape(n, w)
-    grads["d_o_logit"] = out["d_o_logit"].cpu().numpy()
-    dv = out["d_values"].cpu().numpy().reshape(n, K)
+        grads[key] = D.to_host(out[key]).reshape(n, w)
+    grads["d_o_logit"] = D.to_host(out["d_o_logit"])
+    dv = D.to_host(out["d_values"]).reshape(n, K)
     for name, c, w in attr_cols:
         grads["d_attrs"][name] = dv[:, c:c + w].reshape(np.asarray(state["attrs"][name]).shape).copy()
     return grads
