@@ -490,7 +490,7 @@ class BaseTrainer(_StageTrainer):
         return self._rgba(F.out.double())
 
     def model(self, metadata=None):
-        h = {k: v.cpu().numpy() for k, v in self.p.items()}
+        h = {k: D.to_host(v) for k, v in self.p.items()}
         geom = GaussianGeometry(*(h[k] for k in GEOM))
         return BasicSceneModel(STAGE_BASE, geom, sh=ShColor(h["sh"], self.degree),
                                metadata=metadata or {})
@@ -580,7 +580,7 @@ class EditableTrainer(_StageTrainer):
         return self._rgba(F.out.double())
 
     def model(self, palette, metadata=None):
-        h = {k: v.cpu().numpy() for k, v in self.p.items()}
+        h = {k: D.to_host(v) for k, v in self.p.items()}
         geom = GaussianGeometry(*(h[k] for k in GEOM))
         attrs = ShadingAttributes(*(h[k] for k in SHADE))
         return BasicSceneModel(STAGE_EDITABLE, geom, shading=attrs, palette=Palette(palette),
