@@ -541,9 +541,13 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
         if (R.d_mean2d) { R.d_mean2d[2 * i] = gmean[0]; R.d_mean2d[2 * i + 1] = gmean[1]; }
         for (int k = 0; k < 3; ++k) flag_bad(R.bad, i, 5, gv_color[k]);
 
-        double d_mu[3] = {0, 0, 0}, d_n_raw[3] = {0, 0, 0};
-        const double nraw[3] = {G.n_raw[3 * i], G.n_raw[3 * i + 1], G.n_raw[3 * i + 2]};
-        if (B.L.col_normal >= 0 && R.g_values) normalize_bwd(nraw, gv_norm, d_n_raw);
+        // d_mu / d_n_raw only when asked for (transform fits skip both chains)
+        const bool want_mu = R.d_mu || R.d_n_raw;
+        double d_mu[3] = {0, 0, 0}, d_n_raw[3] = {0, 0, 0}, nraw[3] = {0, 0, 0};
+        if (want_mu) {
+            for (int k = 0; k < 3; ++k) nraw[k] = G.n_raw[3 * i + k];
+            if (B.L.col_normal >= 0 && R.g_values) normalize_bwd(nraw, gv_norm, d_n_raw);
+        }
 
         // ---- opacity: effective logit chain (rasterizer.py:278-279) + inverse scale
         const bool rescale = B.has_edits && P.rescale_opacity && B.E.opacity_scale;
@@ -707,12 +711,14 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
                 red[8] = dp;
                 red[9] = da;
             }
-            double d_w[3];
-            normalize_bwd(st.w_cam, d_v, d_w);
-            for (int k = 0; k < 3; ++k) d_mu[k] -= d_w[k];
-            double d_nr2[3];
-            normalize_bwd(nraw, d_n_unit, d_nr2);
-            for (int k = 0; k < 3; ++k) d_n_raw[k] += d_nr2[k];
+            if (want_mu) {
+                double d_w[3];
+                normalize_bwd(st.w_cam, d_v, d_w);
+                for (int k = 0; k < 3; ++k) d_mu[k] -= d_w[k];
+                double d_nr2[3];
+                normalize_bwd(nraw, d_n_unit, d_nr2);
+                for (int k = 0; k < 3; ++k) d_n_raw[k] += d_nr2[k];
+            }
             const double e_a = d_k_a * P.term_scales[0] * (st.gates[0] ? 1.0 : 0.0);
             const double e_d = d_k_d * P.term_scales[1] * (st.gates[1] ? 1.0 : 0.0);
             const double e_s = d_k_s * P.term_scales[2] * (st.gates[2] ? 1.0 : 0.0);
@@ -751,9 +757,11 @@ preprocess_bwd_kernel(BwdConst B, ivr_frame_params Pv, const ivr_frame_params *_
         }
         if (R.d_mu) for (int k = 0; k < 3; ++k) R.d_mu[3 * i + k] = d_mu[k];
         if (R.d_n_raw) for (int k = 0; k < 3; ++k) R.d_n_raw[3 * i + k] = d_n_raw[k];
-        for (int k = 0; k < 3; ++k) {
-            flag_bad(R.bad, i, 0, d_mu[k]);
-            flag_bad(R.bad, i, 4, d_n_raw[k]);
+        if (want_mu) {
+            for (int k = 0; k < 3; ++k) {
+                flag_bad(R.bad, i, 0, d_mu[k]);
+                flag_bad(R.bad, i, 4, d_n_raw[k]);
+            }
         }
     }
     if (R.d_globals || nsc > 0) {  // transform gradients requested (fits, shade_backward)
